@@ -1,0 +1,650 @@
+// TEST INFRASTRUCTURE ONLY — see o_core.hpp.
+// o_feti.hpp — restatement of feti.hpp (FetiOperator :74-232, feti_pcg
+// :263-308, unpack :443-454) and timeloop.hpp (:51-221), generalised to N
+// subdomains with the FETI-1 natural coarse space and the
+// sign-split preconditioned MINRES used when pressure multipliers make the
+// interface operator indefinite (App. C D3, option A).
+#pragma once
+
+#include <atomic>
+#include <chrono>
+#include <thread>
+
+#include "o_assembly.hpp"
+#include "o_ldlt.hpp"
+
+namespace oracle {
+
+template <class F>
+inline void parallel_for(int n, int threads, F&& f) {
+  if (threads <= 1 || n <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::atomic<int> next{0};
+  for (int t = 0; t < std::min(threads, n); ++t)
+    pool.emplace_back([&] {
+      for (int i = next++; i < n; i = next++) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+/// Integer half-cell coordinates of every saddle dof (for the ND ordering).
+inline std::vector<std::array<int, 2>> dof_grid_coords(const Sub& S) {
+  const Rect& r = S.mesh.rect;
+  const double hx = r.w() / S.mesh.nx * 0.5, hy = r.h() / S.mesh.ny * 0.5;
+  auto ic = [&](const V2& x) {
+    return std::array<int, 2>{(int)std::llround((x.x - r.x0) / hx), (int)std::llround((x.y - r.y0) / hy)};
+  };
+  std::vector<std::array<int, 2>> c(S.dim);
+  for (int nd = 0; nd < S.u.nnode; ++nd)
+    for (int k = 0; k < 2; ++k) c[S.off_u + S.u.dof(nd, k)] = ic(S.u.xy[nd]);
+  for (int v = 0; v < S.n_s; ++v) {
+    c[S.off_xi + v] = ic(S.s.xy[v]);
+    if (S.region == Region::P) c[S.off_eta + v] = c[S.off_p + v] = ic(S.s.xy[v]);
+  }
+  return c;
+}
+
+inline Csr submatrix(const Csr& M, const std::vector<int>& rows_keep /* -1 dropped, else new idx */, int n) {
+  std::vector<Trip> t;
+  for (int i = 0; i < M.nr; ++i) {
+    if (rows_keep[i] < 0) continue;
+    for (int q = M.ptr[i]; q < M.ptr[i + 1]; ++q)
+      if (rows_keep[M.col[q]] >= 0) t.push_back({rows_keep[i], rows_keep[M.col[q]], M.val[q]});
+  }
+  return Csr::from_trips(n, n, t);
+}
+
+struct PcgReport {
+  int step = 0;
+  std::string method;
+  int iterations = 0;
+  bool converged = false;
+  double rel_residual = 0.0;
+  std::vector<double> history;
+  double time_solve = 0.0;
+};
+
+class Feti {
+ public:
+  enum class Prec { identity, generalized, dirichlet };
+  enum class Kry { pcg, minres, sqmr };
+  // mortar scaling: M <- Q M Q with Q = (sum_s G_s G_s^T)^{-1} (Stefanica-Klawonn
+  // scaling for mortar multipliers; SURVEY App. C D6 "scaling behind a flag")
+
+  explicit Feti(const Disc& D) : D_(&D) {
+    const auto& cfg = D.cfg;
+    nthreads_ = cfg.threads > 0 ? cfg.threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    std::string pk = cfg.precond;
+    if (pk.size() > 7 && pk.substr(pk.size() - 7) == "-mortar") {
+      scaled_ = true;
+      pk = pk.substr(0, pk.size() - 7);
+    }
+    prec_ = pk == "identity" ? Prec::identity : pk == "generalized" ? Prec::generalized : Prec::dirichlet;
+    if (pk != "identity" && pk != "generalized" && pk != "dirichlet")
+      throw ConfigError("unknown preconditioner '" + cfg.precond + "'");
+    // auto: REF PCG when the interface operator is SPD (no pressure multipliers),
+    // otherwise SQMR (symmetric indefinite operator and preconditioner)
+    const bool indefinite = D.n_lambda > D.n_lambda_u;
+    kry_ = cfg.krylov == "minres" ? Kry::minres
+           : cfg.krylov == "sqmr" ? Kry::sqmr
+           : cfg.krylov == "pcg"  ? Kry::pcg
+           : (indefinite ? Kry::sqmr : Kry::pcg);
+    if (cfg.krylov != "auto" && cfg.krylov != "pcg" && cfg.krylov != "minres" && cfg.krylov != "sqmr")
+      throw ConfigError("unknown krylov method '" + cfg.krylov + "'");
+    minres_ = kry_ == Kry::minres;
+    split_ = minres_;  // MINRES needs an SPD preconditioner: sign-split pressure block
+    const int ns = (int)D.subs.size();
+    fac_.resize(ns);
+    ifac_.resize(ns);
+    parallel_for(ns, nthreads_, [&](int s) {
+      const Sub& S = D.subs[s];
+      const auto ic = dof_grid_coords(S);
+      if (S.floating) {
+        std::vector<int> keep(S.dim);
+        std::iota(keep.begin(), keep.end(), 0);
+        std::vector<Trip> t;
+        std::vector<char> isfix(S.dim, 0);
+        for (int f : S.fix) isfix[f] = 1;
+        for (int i = 0; i < S.dim; ++i)
+          for (int q = S.K.ptr[i]; q < S.K.ptr[i + 1]; ++q)
+            if (!isfix[i] && !isfix[S.K.col[q]]) t.push_back({i, S.K.col[q], S.K.val[q]});
+        for (int f : S.fix) t.push_back({f, f, 1.0});
+        fac_[s].factor(Csr::from_trips(S.dim, S.dim, t), nd_order(ic));
+      } else {
+        fac_[s].factor(S.K, nd_order(ic));
+      }
+      if (prec_ == Prec::dirichlet) {
+        std::vector<int> newi(S.dim, 0), inv;
+        for (int b : S.Bu) newi[b] = -1;
+        for (int b : S.Bp) newi[b] = -1;
+        int ni = 0;
+        std::vector<std::array<int, 2>> icI;
+        for (int i = 0; i < S.dim; ++i)
+          if (newi[i] == 0) {
+            newi[i] = ni++;
+            icI.push_back(ic[i]);
+          } else {
+            newi[i] = -1;
+          }
+        ifac_[s].factor(submatrix(S.K, newi, ni), nd_order(icI), false);
+      }
+    });
+    if (prec_ == Prec::generalized) {
+      std::vector<Trip> t;
+      for (const Sub& S : D.subs) {
+        // G K G^T with G rows sparse: form (K G^T) column by column via triplets
+        const Csr Gt = S.G.transpose();  // dim x n_lambda
+        for (int i = 0; i < S.dim; ++i)
+          for (int q = S.K.ptr[i]; q < S.K.ptr[i + 1]; ++q) {
+            const int j = S.K.col[q];
+            for (int a = Gt.ptr[i]; a < Gt.ptr[i + 1]; ++a)
+              for (int b = Gt.ptr[j]; b < Gt.ptr[j + 1]; ++b)
+                t.push_back({Gt.col[a], Gt.col[b], Gt.val[a] * S.K.val[q] * Gt.val[b]});
+          }
+      }
+      if (split_)
+        for (auto& e : t)
+          if (e.r >= D.n_lambda_u && e.c >= D.n_lambda_u) e.v = -e.v;  // sign split on p block
+      Mgen_ = Csr::from_trips(D.n_lambda, D.n_lambda, t);
+    }
+    if (scaled_) {
+      std::vector<Trip> t;
+      for (const Sub& S : D.subs) {
+        const Csr Gt = S.G.transpose();
+        for (int i = 0; i < S.dim; ++i)
+          for (int a = Gt.ptr[i]; a < Gt.ptr[i + 1]; ++a)
+            for (int b = Gt.ptr[i]; b < Gt.ptr[i + 1]; ++b)
+              t.push_back({Gt.col[a], Gt.col[b], Gt.val[a] * Gt.val[b]});
+      }
+      // ordering: multiplier vertex coordinates on the global half-cell grid
+      std::vector<std::array<int, 2>> ic(D.n_lambda);
+      for (int i = 0; i < D.n_lambda; ++i) {
+        const Mult& m = D.mults[i];
+        const Iface& I = D.ifs[m.iface];
+        const V2 x = D.subs[I.a].mesh.vtx[I.va[m.k]];
+        ic[i] = {(int)std::llround(x.x * 2 * D.cfg.mesh_n), (int)std::llround(x.y * 2 * D.cfg.mesh_n)};
+      }
+      const Csr BBt = Csr::from_trips(D.n_lambda, D.n_lambda, t);
+      qfac_.factor(BBt, nd_order(ic, &BBt), true);
+    }
+    // natural coarse space G_c = [G_s R_s] over floating subdomains
+    for (int s = 0; s < ns; ++s)
+      if (D.subs[s].floating) floating_.push_back(s);
+    nc_ = 3 * (int)floating_.size();
+    if (nc_ > 0) {
+      std::vector<Trip> t;
+      for (int f = 0; f < (int)floating_.size(); ++f) {
+        const Sub& S = D.subs[floating_[f]];
+        for (int i = 0; i < S.G.nr; ++i)
+          for (int q = S.G.ptr[i]; q < S.G.ptr[i + 1]; ++q)
+            for (int m = 0; m < 3; ++m)
+              if (S.Rk(S.G.col[q], m) != 0.0) t.push_back({i, 3 * f + m, S.G.val[q] * S.Rk(S.G.col[q], m)});
+      }
+      Gc_ = Csr::from_trips(D.n_lambda, nc_, t);
+      const Csr GcT = Gc_.transpose();
+      GtG_ = Dense(nc_, nc_);
+      for (int a = 0; a < nc_; ++a) {
+        // column a of G^T G = G^T (G e_a)
+        Vec col(D.n_lambda, 0.0);
+        for (int q = GcT.ptr[a]; q < GcT.ptr[a + 1]; ++q) col[GcT.col[q]] = GcT.val[q];
+        const Vec r = GcT.mul(col);
+        for (int b = 0; b < nc_; ++b) GtG_(b, a) = r[b];
+      }
+      dense_cholesky(GtG_);
+    }
+  }
+
+  int n_lambda() const { return D_->n_lambda; }
+  bool uses_minres() const { return minres_; }
+  int krylov_kind() const { return (int)kry_; }
+  int n_coarse() const { return nc_; }
+  const Ldlt& factor(int s) const { return fac_[s]; }
+
+  /// K_s^+ b (fixing-node generalised inverse for floating subdomains).
+  void local_solve(int s, double* x) const {
+    for (int f : D_->subs[s].fix) x[f] = 0.0;
+    fac_[s].solve_inplace(x);
+  }
+
+  /// y = sum_s G_s K_s^+ G_s^T x (feti.hpp:101-125), summed in subdomain order.
+  Vec apply(const Vec& x) const {
+    const int ns = (int)D_->subs.size();
+    std::vector<Vec> z(ns);
+    parallel_for(ns, nthreads_, [&](int s) {
+      const Sub& S = D_->subs[s];
+      z[s].assign(S.dim, 0.0);
+      S.G.mtv(x.data(), z[s].data());
+      local_solve(s, z[s].data());
+    });
+    Vec y(D_->n_lambda, 0.0);
+    for (int s = 0; s < ns; ++s) D_->subs[s].G.mv(z[s].data(), y.data(), true);
+    return y;
+  }
+
+  /// REF schur_part (feti.hpp:212-224) on the boundary set B = Bu (+ Bp).
+  void schur_apply(int s, const Vec& w, Vec& out) const {
+    const Sub& S = D_->subs[s];
+    const Vec y = S.K.mul(w);
+    std::vector<char> isB(S.dim, 0);
+    for (int b : S.Bu) isB[b] = 1;
+    for (int b : S.Bp) isB[b] = 1;
+    Vec vI;
+    vI.reserve(S.dim);
+    for (int i = 0; i < S.dim; ++i)
+      if (!isB[i]) vI.push_back(y[i]);
+    ifac_[s].solve_inplace(vI.data());
+    Vec v(S.dim, 0.0);
+    for (int i = 0, k = 0; i < S.dim; ++i)
+      if (!isB[i]) v[i] = vI[k++];
+    const Vec mv = S.K.mul(v);
+    out.assign(S.dim, 0.0);
+    for (int i = 0; i < S.dim; ++i)
+      if (isB[i]) out[i] = y[i] - mv[i];
+  }
+
+  Vec precondition(const Vec& r0) const {
+    if (!scaled_) return precondition_raw(r0);
+    Vec r = r0;
+    qfac_.solve_inplace(r.data());
+    Vec z = precondition_raw(r);
+    qfac_.solve_inplace(z.data());
+    return z;
+  }
+
+  Vec precondition_raw(const Vec& r) const {
+    if (prec_ == Prec::identity) return r;
+    if (prec_ == Prec::generalized) return Mgen_.mul(r);
+    const int ns = (int)D_->subs.size();
+    std::vector<Vec> z(ns);
+    parallel_for(ns, nthreads_, [&](int s) {
+      const Sub& S = D_->subs[s];
+      Vec w(S.dim, 0.0);
+      S.G.mtv(r.data(), w.data());
+      if (S.Bp.empty() || !split_) {
+        schur_apply(s, w, z[s]);
+      } else {
+        // sign split: [S(w_u,0)]_u and -[S(0,w_p)]_p
+        Vec wu = w, wp(S.dim, 0.0), su, sp;
+        for (int b : S.Bp) wp[b] = w[b], wu[b] = 0.0;
+        schur_apply(s, wu, su);
+        schur_apply(s, wp, sp);
+        z[s].assign(S.dim, 0.0);
+        for (int b : S.Bu) z[s][b] = su[b];
+        for (int b : S.Bp) z[s][b] = -sp[b];
+      }
+    });
+    Vec y(D_->n_lambda, 0.0);
+    for (int s = 0; s < ns; ++s) D_->subs[s].G.mv(z[s].data(), y.data(), true);
+    return y;
+  }
+
+  // ---- coarse space (FETI-1 natural projector) ----
+  Vec coarse_solve(const Vec& v_nc) const {
+    Vec x = v_nc;
+    dense_cholesky_solve(GtG_, x.data());
+    return x;
+  }
+  void project(Vec& v) const {
+    if (nc_ == 0) return;
+    const Vec a = coarse_solve(Gc_.tmul(v));
+    Gc_.mv(a.data(), v.data(), true, -1.0);
+  }
+  Vec rigid_rhs(const std::vector<Vec>& b) const {  // e = [R_s^T b_s]
+    Vec e(nc_, 0.0);
+    for (int f = 0; f < (int)floating_.size(); ++f) {
+      const Sub& S = D_->subs[floating_[f]];
+      for (int m = 0; m < 3; ++m) {
+        double s = 0.0;
+        for (int i = 0; i < S.dim; ++i) s += S.Rk(i, m) * b[floating_[f]][i];
+        e[3 * f + m] = s;
+      }
+    }
+    return e;
+  }
+
+  /// F = sum_s G_s K_s^+ b_s - d (feti.hpp:147-155).
+  Vec interface_rhs(const StepRhs& r) const {
+    const int ns = (int)D_->subs.size();
+    std::vector<Vec> z(ns);
+    parallel_for(ns, nthreads_, [&](int s) {
+      z[s] = r.b[s];
+      local_solve(s, z[s].data());
+    });
+    Vec y(D_->n_lambda, 0.0);
+    for (int s = 0; s < ns; ++s) D_->subs[s].G.mv(z[s].data(), y.data(), true);
+    for (int i = 0; i < D_->n_lambda; ++i) y[i] -= r.d[i];
+    return y;
+  }
+
+  /// Solve the interface problem; returns lambda and the rigid amplitudes.
+  Vec solve(const Vec& rhs, const StepRhs& r, const Vec& lambda_prev, bool warm, PcgReport& rep,
+            Vec& alpha) const {
+    const auto& cfg = D_->cfg;
+    if (!(cfg.tol > 0)) throw SolverError("feti_pcg: tolerance must be positive");
+    Vec lambda(D_->n_lambda, 0.0);
+    Vec e;
+    if (nc_ > 0) {
+      e = rigid_rhs(r.b);
+      const Vec a = coarse_solve(e);
+      Gc_.mv(a.data(), lambda.data());  // lambda0 = G (G^T G)^{-1} e
+      if (warm) {
+        Vec lp = lambda_prev;
+        project(lp);
+        axpy(1.0, lp, lambda);
+      }
+    } else if (warm) {
+      lambda = lambda_prev;
+    }
+    rep.method = kry_ == Kry::minres ? "minres" : kry_ == Kry::sqmr ? "sqmr" : "pcg";
+    if (kry_ == Kry::minres)
+      minres(rhs, lambda, rep);
+    else if (kry_ == Kry::sqmr)
+      sqmr(rhs, lambda, rep);
+    else
+      pcg(rhs, lambda, rep);
+    alpha.assign(nc_, 0.0);
+    if (nc_ > 0) {
+      Vec res = apply(lambda);
+      for (int i = 0; i < D_->n_lambda; ++i) res[i] -= rhs[i];
+      alpha = coarse_solve(Gc_.tmul(res));
+    }
+    return lambda;
+  }
+
+  /// REF feti_pcg (feti.hpp:263-308), projected when a coarse space exists.
+  void pcg(const Vec& rhs, Vec& lambda, PcgReport& rep) const {
+    const auto& cfg = D_->cfg;
+    Vec r = apply(lambda);
+    for (std::size_t i = 0; i < r.size(); ++i) r[i] = rhs[i] - r[i];
+    project(r);
+    Vec z = precondition(r);
+    project(z);
+    double rz = dot(r, z);
+    const double d0 = std::sqrt(std::max(rz, 0.0));
+    rep.history.push_back(d0);
+    if (d0 == 0.0 || !(d0 > 0.0)) {
+      rep.converged = true;
+      rep.rel_residual = 0.0;
+      return;
+    }
+    Vec p = z;
+    for (int k = 0; k < cfg.max_iter; ++k) {
+      Vec Kp = apply(p);
+      const double pKp = dot(p, Kp);
+      if (pKp <= 1e-14 * dot(p, p)) throw PcgBreakdownError("feti_pcg: <p, Kp> not positive (operator not SPD?)");
+      const double a = rz / pKp;
+      axpy(a, p, lambda);
+      project(Kp);
+      axpy(-a, Kp, r);
+      z = precondition(r);
+      project(z);
+      const double rzn = dot(r, z);
+      const double dl = std::sqrt(std::max(rzn, 0.0));
+      rep.history.push_back(dl);
+      rep.iterations = k + 1;
+      if (dl <= cfg.tol * d0) {
+        rep.converged = true;
+        break;
+      }
+      if (rzn <= 0.0) throw PcgBreakdownError("feti_pcg: preconditioned residual norm lost positivity");
+      const double b = rzn / rz;
+      rz = rzn;
+      for (std::size_t i = 0; i < p.size(); ++i) p[i] = z[i] + b * p[i];
+    }
+    rep.rel_residual = rep.history.back() / d0;
+  }
+
+  /// Symmetric QMR with a symmetric (indefinite) preconditioner, right
+  /// preconditioned form (Freund & Nachtigal 1994, Alg. 2 with M_L = I).
+  /// Converged when the quasi-residual bound tau_k sqrt(k+1) <= tol * ||r_0||.
+  void sqmr(const Vec& rhs, Vec& lambda, PcgReport& rep) const {
+    const auto& cfg = D_->cfg;
+    const int n = D_->n_lambda;
+    Vec r = apply(lambda);
+    for (int i = 0; i < n; ++i) r[i] = rhs[i] - r[i];
+    project(r);
+    double tau = norm2(r);
+    const double t0 = tau;
+    rep.history.push_back(t0);
+    if (t0 == 0.0 || !(t0 > 0.0)) {
+      rep.converged = true;
+      return;
+    }
+    Vec q = precondition(r);
+    project(q);
+    double rho = dot(r, q), theta = 0.0;
+    Vec d(n, 0.0);
+    for (int k = 0; k < cfg.max_iter; ++k) {
+      Vec t = apply(q);
+      project(t);
+      const double sigma = dot(q, t);
+      if (sigma == 0.0 || !std::isfinite(sigma)) throw PcgBreakdownError("sqmr: <q, Fq> vanished (Lanczos breakdown)");
+      const double a = rho / sigma;
+      axpy(-a, t, r);
+      const double th_old = theta;
+      theta = norm2(r) / tau;
+      const double c = 1.0 / std::sqrt(1.0 + theta * theta);
+      tau = tau * theta * c;
+      for (int i = 0; i < n; ++i) {
+        d[i] = c * c * th_old * th_old * d[i] + c * c * a * q[i];
+        lambda[i] += d[i];
+      }
+      const double est = tau * std::sqrt(double(k + 2));
+      rep.history.push_back(est);
+      rep.iterations = k + 1;
+      if (est <= cfg.tol * t0) {
+        rep.converged = true;
+        break;
+      }
+      if (rho == 0.0) throw PcgBreakdownError("sqmr: rho vanished");
+      Vec u = precondition(r);
+      project(u);
+      const double rho_n = dot(r, u);
+      const double b = rho_n / rho;
+      rho = rho_n;
+      for (int i = 0; i < n; ++i) q[i] = u[i] + b * q[i];
+    }
+    rep.rel_residual = rep.history.back() / t0;
+  }
+
+  /// Preconditioned MINRES (Paige-Saunders recurrences) on P F P with the
+  /// SPD preconditioner P M P; residual measured as sqrt(r^T M r) like REF.
+  void minres(const Vec& rhs, Vec& lambda, PcgReport& rep) const {
+    const auto& cfg = D_->cfg;
+    const int n = D_->n_lambda;
+    Vec r1 = apply(lambda);
+    for (int i = 0; i < n; ++i) r1[i] = rhs[i] - r1[i];
+    project(r1);
+    Vec y = precondition(r1);
+    project(y);
+    double b2 = dot(r1, y);
+    if (b2 < 0) throw PcgBreakdownError("minres: preconditioner not positive definite");
+    const double beta1 = std::sqrt(b2);
+    rep.history.push_back(beta1);
+    if (beta1 == 0.0 || !(beta1 > 0.0)) {
+      rep.converged = true;
+      return;
+    }
+    double oldb = 0, beta = beta1, dbar = 0, epsln = 0, phibar = beta1, cs = -1, sn = 0;
+    Vec r2 = r1, w(n, 0.0), w2(n, 0.0), v(n);
+    for (int k = 0; k < cfg.max_iter; ++k) {
+      const double s = 1.0 / beta;
+      for (int i = 0; i < n; ++i) v[i] = s * y[i];
+      y = apply(v);
+      project(y);
+      if (k >= 1) axpy(-beta / oldb, r1, y);
+      const double alfa = dot(v, y);
+      axpy(-alfa / beta, r2, y);
+      r1 = r2;
+      r2 = y;
+      y = precondition(r2);
+      project(y);
+      oldb = beta;
+      b2 = dot(r2, y);
+      if (b2 < 0) throw PcgBreakdownError("minres: preconditioner not positive definite");
+      beta = std::sqrt(b2);
+      const double oldeps = epsln;
+      const double delta = cs * dbar + sn * alfa;
+      const double gbar = sn * dbar - cs * alfa;
+      epsln = sn * beta;
+      dbar = -cs * beta;
+      double gamma = std::sqrt(gbar * gbar + beta * beta);
+      gamma = std::max(gamma, 1e-300);
+      cs = gbar / gamma;
+      sn = beta / gamma;
+      const double phi = cs * phibar;
+      phibar = sn * phibar;
+      const double den = 1.0 / gamma;
+      for (int i = 0; i < n; ++i) {
+        const double w1 = w2[i];
+        w2[i] = w[i];
+        w[i] = (v[i] - oldeps * w1 - delta * w2[i]) * den;
+        lambda[i] += phi * w[i];
+      }
+      rep.history.push_back(phibar);
+      rep.iterations = k + 1;
+      if (phibar <= cfg.tol * beta1) {
+        rep.converged = true;
+        break;
+      }
+    }
+    rep.rel_residual = rep.history.back() / beta1;
+  }
+
+  /// x_s = K_s^+(b_s - G_s^T lambda) + R_s alpha_s (feti.hpp:158-168).
+  std::vector<Vec> back_substitute(const Vec& lambda, const StepRhs& r, const Vec& alpha) const {
+    const int ns = (int)D_->subs.size();
+    std::vector<Vec> x(ns);
+    std::vector<int> fpos(ns, -1);
+    for (int f = 0; f < (int)floating_.size(); ++f) fpos[floating_[f]] = f;
+    parallel_for(ns, nthreads_, [&](int s) {
+      const Sub& S = D_->subs[s];
+      x[s] = r.b[s];
+      S.G.mtv(lambda.data(), x[s].data(), true, -1.0);
+      local_solve(s, x[s].data());
+      if (fpos[s] >= 0)
+        for (int i = 0; i < S.dim; ++i)
+          for (int m = 0; m < 3; ++m) x[s][i] += S.Rk(i, m) * alpha[3 * fpos[s] + m];
+    });
+    return x;
+  }
+
+ private:
+  const Disc* D_;
+  int nthreads_ = 1;
+  Prec prec_ = Prec::dirichlet;
+  bool scaled_ = false;
+  Ldlt qfac_;
+  bool minres_ = false, split_ = false;
+  Kry kry_ = Kry::pcg;
+  std::vector<Ldlt> fac_, ifac_;
+  Csr Mgen_;
+  std::vector<int> floating_;
+  int nc_ = 0;
+  Csr Gc_;
+  Dense GtG_;
+};
+
+/// Per-subdomain saddle solutions of one time level plus the multiplier.
+struct State {
+  int step = 0;
+  double t = 0.0;
+  std::vector<Vec> x;
+  Vec lambda;
+};
+
+/// project_initial (timeloop.hpp:75-111).
+inline State project_initial(const Disc& D) {
+  State st;
+  st.x.resize(D.subs.size());
+  for (std::size_t s = 0; s < D.subs.size(); ++s) {
+    const Sub& S = D.subs[s];
+    Vec& x = st.x[s];
+    x.assign(S.dim, 0.0);
+    const VFn& u0 = S.region == Region::P ? D.sc.u0_P : D.sc.u0_E;
+    for (int nd = 0; nd < S.u.nnode; ++nd) {
+      const V2 v = u0(S.u.xy[nd], 0.0);
+      x[S.off_u + S.u.dof(nd, 0)] = v.x;
+      x[S.off_u + S.u.dof(nd, 1)] = v.y;
+    }
+    for (int v = 0; v < S.n_s; ++v) {
+      const V2 xy = S.s.xy[v];
+      if (S.region == Region::P) {
+        const double p0 = D.sc.p0(xy, 0.0), du = D.sc.divu0_P(xy, 0.0);
+        x[S.off_p + v] = p0;
+        x[S.off_eta + v] = D.par.c0 * p0 + D.par.alpha * du;
+        x[S.off_xi + v] = D.par.alpha * p0 - D.par.lam_P * du;
+      } else {
+        x[S.off_xi + v] = -D.par.lam_E * D.sc.divu0_E(xy, 0.0);
+      }
+    }
+  }
+  st.lambda.assign(D.n_lambda, 0.0);
+  return st;
+}
+
+inline std::vector<Vec> eta_of(const Disc& D, const State& st) {
+  std::vector<Vec> e(D.subs.size());
+  for (std::size_t s = 0; s < D.subs.size(); ++s) {
+    const Sub& S = D.subs[s];
+    if (S.region == Region::P) e[s].assign(st.x[s].begin() + S.off_eta, st.x[s].begin() + S.off_eta + S.n_s);
+  }
+  return e;
+}
+
+/// StepSolver::advance (timeloop.hpp:150-186).
+inline State advance(const Disc& D, const Feti& op, const State& prev, PcgReport& rep) {
+  const int n = prev.step + 1;
+  const double t = D.time(n);
+  State next;
+  try {
+    const StepRhs r = assemble_rhs(D, t, eta_of(D, prev));
+    const Vec F = op.interface_rhs(r);
+    Vec alpha;
+    next.lambda = op.solve(F, r, prev.lambda, D.cfg.warm, rep, alpha);
+    if (!rep.converged)
+      throw SolverError("PCG stalled at relative residual " + std::to_string(rep.rel_residual) +
+                        " after " + std::to_string(rep.iterations) + " iterations");
+    next.x = op.back_substitute(next.lambda, r, alpha);
+  } catch (const Error& e) {
+    throw SolverError("step " + std::to_string(n) + ": " + e.what());
+  }
+  rep.step = n;
+  next.step = n;
+  next.t = t;
+  return next;
+}
+
+/// Tiny-mesh monolithic oracle (feti.hpp:313-440 restated): dense LU of
+/// [blockdiag(K_s) G^T; G 0] [x; lambda] = [b; d].
+inline void monolithic_solve(const Disc& D, const StepRhs& r, std::vector<Vec>& x, Vec& lambda) {
+  std::vector<int> off(D.subs.size() + 1, 0);
+  for (std::size_t s = 0; s < D.subs.size(); ++s) off[s + 1] = off[s] + D.subs[s].dim;
+  const int nx = off.back(), n = nx + D.n_lambda;
+  if (n > 12000) throw ConfigError("monolithic oracle is for tiny meshes only");
+  Dense M(n, n);
+  Vec b(n, 0.0);
+  for (std::size_t s = 0; s < D.subs.size(); ++s) {
+    const Sub& S = D.subs[s];
+    for (int i = 0; i < S.dim; ++i) {
+      b[off[s] + i] = r.b[s][i];
+      for (int q = S.K.ptr[i]; q < S.K.ptr[i + 1]; ++q) M(off[s] + i, off[s] + S.K.col[q]) = S.K.val[q];
+    }
+    for (int i = 0; i < S.G.nr; ++i)
+      for (int q = S.G.ptr[i]; q < S.G.ptr[i + 1]; ++q) {
+        M(nx + i, off[s] + S.G.col[q]) = S.G.val[q];
+        M(off[s] + S.G.col[q], nx + i) = S.G.val[q];
+      }
+  }
+  for (int i = 0; i < D.n_lambda; ++i) b[nx + i] = r.d[i];
+  const Vec sol = dense_lu_solve(std::move(M), std::move(b));
+  x.resize(D.subs.size());
+  for (std::size_t s = 0; s < D.subs.size(); ++s)
+    x[s].assign(sol.begin() + off[s], sol.begin() + off[s + 1]);
+  lambda.assign(sol.begin() + nx, sol.end());
+}
+
+}  // namespace oracle
