@@ -1,0 +1,148 @@
+/* porofeti_b200.h — C ABI of the B200-native FETI engine
+ * (paper_2509_06673_b200/_lib/libporofeti_b200.so).
+ *
+ * Drop-in boundary for the reference's per-time-step FETI path
+ * (/root/reference/proj/include/porofeti).  The reference is a header-only
+ * C++ library with Eigen types and no FFI; each entry point below replaces the
+ * C++ call named beside it.  Plain pointers and sizes only; all device memory
+ * is owned by the context; one CUDA stream per context; calls on one context
+ * are serialised.  Every entry point returns a status code:
+ *   PF_OK 0, PF_SINGULAR 1 (SingularSubproblemError, core.hpp:52),
+ *   PF_BREAKDOWN 2 (PcgBreakdownError, core.hpp:57),
+ *   PF_NOT_CONVERGED 3 (SolverError, core.hpp:62),
+ *   PF_INVALID 4 (MeshError/AssemblyError/ConfigError, core.hpp:37-70),
+ *   PF_CUDA 5 (no device / CUDA failure — there is no CPU fallback),
+ *   PF_INTERNAL 99.
+ * Vectors in the "saddle" layout follow the reference's per-subdomain saddle
+ * order: P = [u, eta, xi, p], E = [u, xi] (assembly.hpp:338-398); u is
+ * interleaved node-major (mesh.hpp:157-199).
+ */
+#ifndef POROFETI_B200_H
+#define POROFETI_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_SINGULAR 1
+#define PF_BREAKDOWN 2
+#define PF_NOT_CONVERGED 3
+#define PF_INVALID 4
+#define PF_CUDA 5
+#define PF_INTERNAL 99
+
+/* scenario ids */
+#define PF_SCEN_MMS_T 0        /* BASELINE configs 1-4: time-linear MMS */
+#define PF_SCEN_MMS 1          /* reference stationary MMS (model.hpp:146) */
+#define PF_SCEN_INJECTION 2    /* BASELINE config 5 */
+#define PF_SCEN_BARRY_MERCER 3 /* reference Barry-Mercer (model.hpp:274) */
+/* preconditioners: identity, generalized (feti.hpp:86-88,131), dirichlet
+ * (feti-schur, feti.hpp:133-141), and the mortar-scaled variants */
+#define PF_PREC_IDENTITY 0
+#define PF_PREC_GENERALIZED 1
+#define PF_PREC_DIRICHLET 2
+#define PF_PREC_GENERALIZED_MORTAR 3
+#define PF_PREC_DIRICHLET_MORTAR 4
+/* Krylov: auto = reference PCG (feti.hpp:263) when no pressure multipliers,
+ * SQMR otherwise */
+#define PF_KRYLOV_AUTO 0
+#define PF_KRYLOV_PCG 1
+#define PF_KRYLOV_MINRES 2
+#define PF_KRYLOV_SQMR 3
+
+/* Run configuration (reference RunConfig, config.hpp:17-43, plus the
+ * partition).  Same field order as the oracle's or_config. */
+typedef struct pf_config {
+  int mesh_n, SX, SY, order;
+  double E, nu, alpha, c0, kperm, mu_f, dt;
+  int steps;
+  int mu_conv;  /* 0 paper mu=E/(1+nu) (model.hpp:30), 1 standard */
+  int scenario;
+  int precond;
+  int krylov;
+  double tol;
+  int max_iter, warm, threads;
+  unsigned long long seed;
+  double logk_mean, logk_sd;
+} pf_config;
+
+typedef struct pf_info {
+  int n_sub, n_lambda, n_lambda_u, n_coarse, krylov, N, n_floating, n_types;
+  long long total_dim, nnz_L, nnz_L_interior, nnz_K, n_supernodes, n_tasks;
+  double tau, T;
+  double t_setup, t_assemble, t_factor, t_upload;
+  double bytes_fapply;  /* algorithmic bytes of one F-apply (SURVEY §8d B_F) */
+  double bytes_precond; /* algorithmic bytes of one preconditioner apply */
+} pf_info;
+
+typedef struct pf_sub_info {
+  int region, dim, n_u, n_s, off_u, off_eta, off_xi, off_p, floating, n_cons, type;
+  long long nnz_L;
+} pf_sub_info;
+
+/* PcgReport (feti.hpp:59-67) + device timings */
+typedef struct pf_report {
+  int step, iterations, converged, method; /* method: 1 pcg, 2 minres, 3 sqmr */
+  double rel_residual;
+  double seconds;     /* device time of the whole advance (CUDA events) */
+  double t_rhs, t_krylov, t_back;
+  int f_applies, precond_applies;
+} pf_report;
+
+typedef struct pf_ctx pf_ctx;
+
+/* build_discretization (timeloop.hpp:51) + StepSolver ctor (timeloop.hpp:137)
+ * + FetiOperator ctor (feti.hpp:76): partition, device assembly, per-subdomain
+ * factorisation with the seeded residual check (feti.hpp:28-36), projection of
+ * the initial state (timeloop.hpp:75). */
+int pf_create(pf_ctx** out, const pf_config* cfg);
+/* Same, with an explicit per-element permeability array (2*n*n values, global
+ * element order) overriding the seeded generator of the injection scenario. */
+int pf_create_with_permeability(pf_ctx** out, const pf_config* cfg, const double* k_elem);
+void pf_destroy(pf_ctx* ctx);
+const char* pf_last_error(const pf_ctx* ctx); /* ctx may be NULL (creation errors) */
+
+int pf_get_info(const pf_ctx* ctx, pf_info* out);
+int pf_get_sub_info(const pf_ctx* ctx, int s, pf_sub_info* out);
+
+/* FetiOperator::apply (feti.hpp:101): y = sum_s G_s K_s^+ G_s^T x, host buffers. */
+int pf_apply(pf_ctx* ctx, const double* x, double* y);
+/* FetiOperator::apply_preconditioner (feti.hpp:127). */
+int pf_apply_precond(pf_ctx* ctx, const double* r, double* z);
+/* natural coarse projector P = I - G_c (G_c^T G_c)^{-1} G_c^T (in place). */
+int pf_project(pf_ctx* ctx, double* x);
+/* SubdomainFactorization::solve (feti.hpp:38) of subdomain s, saddle layout, in place. */
+int pf_local_solve(pf_ctx* ctx, int s, double* x);
+/* FetiOperator::interface_rhs (feti.hpp:147) of the next step from the current state. */
+int pf_interface_rhs(pf_ctx* ctx, double* F);
+
+/* StepSolver::advance (timeloop.hpp:150) on the device-resident state. */
+int pf_step(pf_ctx* ctx, pf_report* rep);
+/* advance with host buffers (the reference signature): prev state in (all
+ * subdomains' saddle vectors concatenated + lambda), next state out. */
+int pf_advance(pf_ctx* ctx, const double* prev_x, const double* prev_lambda, int prev_step,
+               double* next_x, double* next_lambda, pf_report* rep);
+/* state accessors (saddle layout per subdomain; lambda) */
+int pf_get_state(pf_ctx* ctx, int s, double* x);
+int pf_get_state_all(pf_ctx* ctx, double* x_cat);
+int pf_get_lambda(pf_ctx* ctx, double* lambda);
+int pf_set_state(pf_ctx* ctx, const double* x_cat, const double* lambda, int step);
+int pf_current_step(const pf_ctx* ctx);
+
+/* Device-resident micro-benchmarks (CUDA events on the context stream).
+ * kind: 0 F-apply, 1 preconditioner, 2 F-apply solve phase only. */
+int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
+/* dominant-kernel timing of the last pf_bench_op / pf_step: average ms of the
+ * factor-sweep kernels per F-apply and the number of launches per F-apply */
+int pf_kernel_stats(pf_ctx* ctx, double* sweep_ms, int* launches_per_apply);
+
+/* Element-level entry points (elements.hpp:152-251) evaluated on the device,
+ * used by the parity tests: tri = 3 vertices (x0,y0,x1,y1,x2,y2). */
+int pf_local_matrices(const double* tri, double mu, double kperm, double mu_f, int order,
+                      double* elastic, double* div, double* mass, double* diffusion);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

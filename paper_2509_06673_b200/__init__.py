@@ -1,0 +1,361 @@
+"""B200-native FETI engine for the coupled poroelasticity-elasticity scheme of
+arXiv 2509.06673 (reference: /root/reference/proj, header-only C++ `porofeti`).
+
+The product is the shared library ``_lib/libporofeti_b200.so`` (C ABI in
+``include/porofeti_b200.h``: CUDA kernels for sm_100a plus the host setup in
+C++).  This module is the thin Python host mirror of the reference's
+operator interface used by the tests and the benchmark:
+
+    reference (feti.hpp / timeloop.hpp)      here
+    ----------------------------------      -----------------------------
+    FetiOperator(bs, dofs, variant)          FetiOperator(config)
+    FetiOperator::apply                      FetiOperator.apply
+    FetiOperator::apply_preconditioner       FetiOperator.apply_preconditioner
+    FetiOperator::interface_rhs              FetiOperator.interface_rhs
+    StepSolver::advance                      StepSolver.advance
+    run_simulation                           run_simulation
+    SingularSubproblemError etc.             exceptions below (same names)
+
+There is no CPU fallback: without the compiled library or a CUDA device every
+entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+__all__ = [
+    "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
+    "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
+    "CudaUnavailableError", "lib", "build", "LIB_PATH",
+]
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "_lib", "libporofeti_b200.so")
+
+SCENARIOS = {"mms-t": 0, "mms": 1, "injection": 2, "barry-mercer": 3}
+PRECONDS = {"identity": 0, "generalized": 1, "dirichlet": 2, "generalized-mortar": 3, "dirichlet-mortar": 4}
+KRYLOV = {"auto": 0, "pcg": 1, "minres": 2, "sqmr": 3}
+METHODS = {1: "pcg", 2: "minres", 3: "sqmr"}
+
+
+class Error(RuntimeError):
+    code = 99
+
+
+class SingularSubproblemError(Error):
+    code = 1
+
+
+class PcgBreakdownError(Error):
+    code = 2
+
+
+class SolverError(Error):
+    code = 3
+
+
+class ConfigError(Error):
+    code = 4
+
+
+class CudaUnavailableError(Error):
+    code = 5
+
+
+_ERRORS = {1: SingularSubproblemError, 2: PcgBreakdownError, 3: SolverError, 4: ConfigError,
+           5: CudaUnavailableError}
+
+
+class Config(C.Structure):
+    """pf_config (include/porofeti_b200.h)."""
+
+    _fields_ = [
+        ("mesh_n", C.c_int), ("SX", C.c_int), ("SY", C.c_int), ("order", C.c_int),
+        ("E", C.c_double), ("nu", C.c_double), ("alpha", C.c_double), ("c0", C.c_double),
+        ("kperm", C.c_double), ("mu_f", C.c_double), ("dt", C.c_double),
+        ("steps", C.c_int), ("mu_conv", C.c_int), ("scenario", C.c_int),
+        ("precond", C.c_int), ("krylov", C.c_int),
+        ("tol", C.c_double), ("max_iter", C.c_int), ("warm", C.c_int), ("threads", C.c_int),
+        ("seed", C.c_ulonglong), ("logk_mean", C.c_double), ("logk_sd", C.c_double),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("n_sub", C.c_int), ("n_lambda", C.c_int), ("n_lambda_u", C.c_int), ("n_coarse", C.c_int),
+        ("krylov", C.c_int), ("N", C.c_int), ("n_floating", C.c_int), ("n_types", C.c_int),
+        ("total_dim", C.c_longlong), ("nnz_L", C.c_longlong), ("nnz_L_interior", C.c_longlong),
+        ("nnz_K", C.c_longlong), ("n_supernodes", C.c_longlong), ("n_tasks", C.c_longlong),
+        ("tau", C.c_double), ("T", C.c_double),
+        ("t_setup", C.c_double), ("t_assemble", C.c_double), ("t_factor", C.c_double), ("t_upload", C.c_double),
+        ("bytes_fapply", C.c_double), ("bytes_precond", C.c_double),
+    ]
+
+
+class SubInfo(C.Structure):
+    _fields_ = [(k, C.c_int) for k in ("region", "dim", "n_u", "n_s", "off_u", "off_eta", "off_xi",
+                                        "off_p", "floating", "n_cons", "type")] + [("nnz_L", C.c_longlong)]
+
+
+class Report(C.Structure):
+    """PcgReport (feti.hpp:59-67) + device timings."""
+
+    _fields_ = [
+        ("step", C.c_int), ("iterations", C.c_int), ("converged", C.c_int), ("method", C.c_int),
+        ("rel_residual", C.c_double), ("seconds", C.c_double),
+        ("t_rhs", C.c_double), ("t_krylov", C.c_double), ("t_back", C.c_double),
+        ("f_applies", C.c_int), ("precond_applies", C.c_int),
+    ]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["method"] = METHODS.get(self.method, str(self.method))
+        return d
+
+
+# BASELINE.json configs; c1 uses the reference's own Dirichlet (feti-schur)
+# preconditioner and PCG, c2-c5 the mortar-scaled Dirichlet + SQMR.
+BASELINE_CONFIGS = {
+    "c1": dict(mesh_n=32, SX=1, SY=2, order=1, nu=0.3, c0=1e-3, dt=1e-2, steps=5, scenario="mms-t",
+               precond="dirichlet"),
+    "c2": dict(mesh_n=128, SX=2, SY=2, order=2, nu=0.3, c0=1e-3, dt=1e-2, steps=10, scenario="mms-t",
+               precond="dirichlet-mortar"),
+    "c3": dict(mesh_n=512, SX=8, SY=8, order=2, nu=0.49999, c0=1e-3, dt=1e-3, steps=20, scenario="mms-t",
+               precond="dirichlet-mortar"),
+    "c4": dict(mesh_n=1024, SX=32, SY=32, order=2, nu=0.3, c0=1e-3, dt=1e-2, steps=10, scenario="mms-t",
+               precond="dirichlet-mortar"),
+    "c5": dict(mesh_n=512, SX=16, SY=16, order=2, nu=0.4, c0=1e-4, dt=1e-3, steps=100, scenario="injection",
+               precond="dirichlet-mortar"),
+}
+
+
+def make_config(mesh_n=32, SX=1, SY=2, order=1, E=1.0, nu=0.3, alpha=1.0, c0=1e-3, kperm=1.0, mu_f=1.0,
+                dt=1e-2, steps=5, mu_conv="paper", scenario="mms-t", precond="dirichlet", krylov="auto",
+                tol=1e-10, max_iter=500, warm=True, threads=0, seed=20240901, logk_mean=-2.0, logk_sd=1.0):
+    return Config(mesh_n, SX, SY, order, E, nu, alpha, c0, kperm, mu_f, dt, steps,
+                  0 if mu_conv == "paper" else 1, SCENARIOS[scenario], PRECONDS[precond], KRYLOV[krylov],
+                  tol, max_iter, int(warm), threads, seed, logk_mean, logk_sd)
+
+
+def build(force=False):
+    """Compile the sm_100a library in-tree (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", PKG], check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """Load the product library; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaUnavailableError(f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, dp = C.c_void_p, C.POINTER(C.c_double)
+        L.pf_create.argtypes = [C.POINTER(vp), C.POINTER(Config)]
+        L.pf_create_with_permeability.argtypes = [C.POINTER(vp), C.POINTER(Config), vp]
+        L.pf_destroy.argtypes = [vp]
+        L.pf_last_error.argtypes = [vp]
+        L.pf_last_error.restype = C.c_char_p
+        L.pf_get_info.argtypes = [vp, C.POINTER(Info)]
+        L.pf_get_sub_info.argtypes = [vp, C.c_int, C.POINTER(SubInfo)]
+        for name in ("pf_apply", "pf_apply_precond"):
+            getattr(L, name).argtypes = [vp, vp, vp]
+        L.pf_project.argtypes = [vp, vp]
+        L.pf_local_solve.argtypes = [vp, C.c_int, vp]
+        L.pf_interface_rhs.argtypes = [vp, vp]
+        L.pf_step.argtypes = [vp, C.POINTER(Report)]
+        L.pf_advance.argtypes = [vp, vp, vp, C.c_int, vp, vp, C.POINTER(Report)]
+        L.pf_get_state.argtypes = [vp, C.c_int, vp]
+        L.pf_get_state_all.argtypes = [vp, vp]
+        L.pf_get_lambda.argtypes = [vp, vp]
+        L.pf_set_state.argtypes = [vp, vp, vp, C.c_int]
+        L.pf_current_step.argtypes = [vp]
+        L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
+        L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
+        L.pf_debug_factor_solve.argtypes = [C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_longlong, vp]
+        L.pf_debug_disc.argtypes = [C.POINTER(Config), vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(code, ctx=None):
+    if code != 0:
+        msg = lib().pf_last_error(ctx).decode(errors="replace")
+        raise _ERRORS.get(code, Error)(f"[{code}] {msg}")
+
+
+class FetiOperator:
+    """Device-resident FETI interface operator of one discretisation
+    (reference FetiOperator, feti.hpp:74-232, plus build_discretization)."""
+
+    def __init__(self, config=None, permeability=None, **kw):
+        self.cfg = config if isinstance(config, Config) else make_config(**kw)
+        L = lib()
+        h = C.c_void_p()
+        if permeability is not None:
+            k = np.ascontiguousarray(permeability, np.float64)
+            code = L.pf_create_with_permeability(C.byref(h), C.byref(self.cfg), _ptr(k))
+        else:
+            code = L.pf_create(C.byref(h), C.byref(self.cfg))
+        _check(code, None)
+        self.h = h
+        self.info = Info()
+        L.pf_get_info(h, C.byref(self.info))
+        self.n_lambda = self.info.n_lambda
+        self.subs = []
+        for s in range(self.info.n_sub):
+            si = SubInfo()
+            L.pf_get_sub_info(h, s, C.byref(si))
+            self.subs.append({k: getattr(si, k) for k, _ in SubInfo._fields_})
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().pf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- reference FetiOperator surface ---
+    def apply(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty(self.n_lambda)
+        _check(lib().pf_apply(self.h, _ptr(x), _ptr(y)), self.h)
+        return y
+
+    def apply_preconditioner(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty(self.n_lambda)
+        _check(lib().pf_apply_precond(self.h, _ptr(r), _ptr(z)), self.h)
+        return z
+
+    def project(self, x):
+        y = np.array(x, np.float64)
+        _check(lib().pf_project(self.h, _ptr(y)), self.h)
+        return y
+
+    def local_solve(self, s, b):
+        x = np.array(b, np.float64)
+        _check(lib().pf_local_solve(self.h, s, _ptr(x)), self.h)
+        return x
+
+    def interface_rhs(self):
+        F = np.empty(self.n_lambda)
+        _check(lib().pf_interface_rhs(self.h, _ptr(F)), self.h)
+        return F
+
+    # --- state (StateSnapshot, state.hpp:8-12) ---
+    def state(self):
+        xs = []
+        for s, S in enumerate(self.subs):
+            x = np.empty(S["dim"])
+            _check(lib().pf_get_state(self.h, s, _ptr(x)), self.h)
+            xs.append(x)
+        lam = np.empty(self.n_lambda)
+        _check(lib().pf_get_lambda(self.h, _ptr(lam)), self.h)
+        return xs, lam
+
+    def fields(self, xs):
+        out = []
+        for S, x in zip(self.subs, xs):
+            f = {"u": x[:S["n_u"]], "xi": x[S["off_xi"]:S["off_xi"] + S["n_s"]]}
+            if S["region"] == 0:
+                f["eta"] = x[S["off_eta"]:S["off_eta"] + S["n_s"]]
+                f["p"] = x[S["off_p"]:S["off_p"] + S["n_s"]]
+            out.append(f)
+        return out
+
+    def step(self):
+        rep = Report()
+        _check(lib().pf_step(self.h, C.byref(rep)), self.h)
+        return rep.as_dict()
+
+    def bench(self, kind=0, warmup=5, iters=20):
+        ms = C.c_double()
+        _check(lib().pf_bench_op(self.h, kind, warmup, iters, C.byref(ms)), self.h)
+        sweep, launches = C.c_double(), C.c_int()
+        lib().pf_kernel_stats(self.h, C.byref(sweep), C.byref(launches))
+        return ms.value, sweep.value, launches.value
+
+
+class StepSolver:
+    """StepSolver (timeloop.hpp:135-193): advance() = one backward-Euler step."""
+
+    def __init__(self, op: FetiOperator):
+        self.op = op
+
+    def advance(self, prev_x=None, prev_lambda=None, prev_step=None):
+        """With no arguments: advance the device-resident state.  With host
+        buffers (the reference signature): set the state, step, return the
+        next (x_cat, lambda, report)."""
+        if prev_x is None:
+            return self.op.step()
+        op = self.op
+        x = np.ascontiguousarray(prev_x, np.float64)
+        lam = np.ascontiguousarray(prev_lambda, np.float64)
+        nx = np.empty(op.info.total_dim)
+        nl = np.empty(op.n_lambda)
+        rep = Report()
+        _check(lib().pf_advance(op.h, _ptr(x), _ptr(lam), int(prev_step), _ptr(nx), _ptr(nl), C.byref(rep)), op.h)
+        return nx, nl, rep.as_dict()
+
+
+def run_simulation(op: FetiOperator, steps=None):
+    """run_simulation (timeloop.hpp:206-221): all steps, returns the reports."""
+    n = op.info.N if steps is None else steps
+    return [op.step() for _ in range(n)]
+
+
+def debug_factor_solve(A, ic, b, mode=1, task_cap=4096):
+    """Host-logic check of the symbolic layout (CPU): solve A x = b with the
+    engine's ordering/supernodes/task schedule emulated on the host."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    ptr = np.ascontiguousarray(A.indptr, np.int32)
+    col = np.ascontiguousarray(A.indices, np.int32)
+    val = np.ascontiguousarray(A.data, np.float64)
+    icc = np.ascontiguousarray(ic, np.int32).reshape(-1)
+    x = np.array(b, np.float64)
+    stats = np.zeros(6, np.int64)
+    _check(lib().pf_debug_factor_solve(n, _ptr(ptr), _ptr(col), _ptr(val), _ptr(icc), _ptr(x), mode, task_cap,
+                                       _ptr(stats)))
+    return x, stats
+
+
+def debug_disc(config: Config, s=0):
+    sizes = np.zeros(5, np.int64)
+    nG, nK = C.c_int(), C.c_int()
+    _check(lib().pf_debug_disc(C.byref(config), _ptr(sizes), s, C.byref(nG), None, None, None, C.byref(nK), None,
+                               None, None))
+    gl = np.zeros(max(nG.value, 1), np.int32)
+    gc = np.zeros(max(nG.value, 1), np.int32)
+    gv = np.zeros(max(nG.value, 1))
+    dim = None
+    kp = None
+    # K pattern: rows = dim of subdomain s; allocate generously
+    kc = np.zeros(max(nK.value, 1), np.int32)
+    kp = np.zeros(int(sizes[4]) + 1, np.int32)
+    ic = np.zeros(2 * int(sizes[4]), np.int32)
+    _check(lib().pf_debug_disc(C.byref(config), _ptr(sizes), s, C.byref(nG), _ptr(gl), _ptr(gc), _ptr(gv),
+                               C.byref(nK), _ptr(kp), _ptr(kc), _ptr(ic)))
+    return dict(n_sub=int(sizes[0]), n_lambda=int(sizes[1]), n_lambda_u=int(sizes[2]), n_types=int(sizes[3]),
+                total_dim=int(sizes[4]), G=(gl[:nG.value], gc[:nG.value], gv[:nG.value]), K_ptr=kp,
+                K_col=kc[:nK.value], dof_ic=ic)

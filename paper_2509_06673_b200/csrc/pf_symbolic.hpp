@@ -1,0 +1,492 @@
+// pf_symbolic.hpp — symbolic analysis of one sparse symmetric system (a
+// subdomain saddle K_s, an interior block K_II, or the mortar Gram matrix
+// G G^T): nested-dissection ordering, elimination tree, supernodes, and the
+// two-level task schedule the device sweeps run on:
+//   * "leaf tasks": maximal etree subtrees below a weight cap, one warp each;
+//     their columns are contiguous and their updates to ancestor rows go to a
+//     private contribution buffer (deterministic, no atomics);
+//   * "top": the remaining ancestors, one CTA per problem, which folds the
+//     contribution buffers in fixed task order.
+// Columns are renumbered so that every task is a contiguous range and the top
+// part is the suffix (a topological order of the supernodal tree).
+// Factor storage per supernode: strict lower trapezoid, column-major, column j
+// holding rows j+1..m-1 (the unit diagonal is implicit, D stored separately).
+#pragma once
+
+#include <functional>
+
+#include "pf_common.hpp"
+
+namespace pf {
+
+struct SymFactor {
+  int n = 0;
+  std::vector<int> perm, iperm;  // position -> natural, natural -> position
+  int nsn = 0;
+  std::vector<int> sn_col0, sn_ncol, sn_nrow, sn_task;  // sn_task: owning task or -1 (top)
+  std::vector<long long> sn_rowoff, sn_valoff;
+  std::vector<int> rows;   // row positions per supernode (first ncol = own columns)
+  std::vector<int> slot;   // parallel to rows: slot in the task (or top) workspace
+  long long nval = 0;
+  int ntask = 0;
+  std::vector<int> task_sn0, task_sn1, task_c0, task_c1, task_cboff, task_cblen;
+  std::vector<int> cb_rows;  // positions (all >= top_c0)
+  int top_sn0 = 0, top_c0 = 0;
+  int max_task_ws = 0;       // max (c1-c0)+cblen over tasks
+  long long flops_factor = 0;
+};
+
+/// Nested dissection on half-cell grid coordinates; separators are the
+/// vertices of a cut line plus any left vertex adjacent to the right side.
+inline void nd_rec(std::vector<int>& ids, const std::vector<std::array<int, 2>>& ic, const Csr& A,
+                   std::vector<uint8_t>& side, std::vector<int>& out, int leaf) {
+  if ((int)ids.size() <= leaf) {
+    std::sort(ids.begin(), ids.end());
+    out.insert(out.end(), ids.begin(), ids.end());
+    return;
+  }
+  int lo[2] = {INT32_MAX, INT32_MAX}, hi[2] = {INT32_MIN, INT32_MIN};
+  for (int d : ids)
+    for (int a = 0; a < 2; ++a) lo[a] = std::min(lo[a], ic[d][a]), hi[a] = std::max(hi[a], ic[d][a]);
+  const int first = (hi[0] - lo[0] >= hi[1] - lo[1]) ? 0 : 1;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const int ax = attempt == 0 ? first : 1 - first;
+    if (hi[ax] - lo[ax] < 2) continue;
+    std::vector<int> v;
+    v.reserve(ids.size());
+    for (int d : ids) v.push_back(ic[d][ax]);
+    std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+    int c = v[v.size() / 2];
+    if (c % 2) c += (c + 1 < hi[ax]) ? 1 : -1;  // prefer vertex lines (even)
+    c = std::max(lo[ax] + 1, std::min(hi[ax] - 1, c));
+    std::vector<int> L, R, S;
+    for (int d : ids) (ic[d][ax] < c ? L : ic[d][ax] > c ? R : S).push_back(d);
+    for (int d : R) side[d] = 1;
+    std::vector<int> L2;
+    L2.reserve(L.size());
+    for (int d : L) {
+      bool cross = false;
+      for (int q = A.ptr[d]; q < A.ptr[d + 1] && !cross; ++q) cross = side[A.col[q]] == 1;
+      (cross ? S : L2).push_back(d);
+    }
+    for (int d : R) side[d] = 0;
+    if (L2.empty() && R.empty()) continue;
+    nd_rec(L2, ic, A, side, out, leaf);
+    nd_rec(R, ic, A, side, out, leaf);
+    std::sort(S.begin(), S.end());
+    out.insert(out.end(), S.begin(), S.end());
+    return;
+  }
+  std::sort(ids.begin(), ids.end());
+  out.insert(out.end(), ids.begin(), ids.end());
+}
+
+/// Build the symbolic factor of symmetric pattern A (natural order).
+/// task_cap: maximum packed-value weight of one leaf task (0 = no tasks).
+inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic, long long task_cap,
+                         int ws_cap = 1536, int leaf = 48) {
+  SymFactor F;
+  const int n = A.nr;
+  F.n = n;
+  std::vector<int> order;
+  {
+    std::vector<int> ids(n);
+    std::iota(ids.begin(), ids.end(), 0);
+    std::vector<uint8_t> side(n, 0);
+    order.reserve(n);
+    nd_rec(ids, ic, A, side, order, leaf);
+  }
+  std::vector<int> ip(n);
+  for (int k = 0; k < n; ++k) ip[order[k]] = k;
+  // permuted strictly-lower adjacency: for column k, rows i > k
+  std::vector<std::vector<int>> lower(n);
+  for (int r = 0; r < n; ++r)
+    for (int q = A.ptr[r]; q < A.ptr[r + 1]; ++q) {
+      const int i = ip[r], j = ip[A.col[q]];
+      if (i > j) lower[j].push_back(i);
+    }
+  // elimination tree (Liu) using row view: for row k, entries j < k
+  std::vector<std::vector<int>> upper(n);  // upper[k] = cols j < k with A(k,j) != 0
+  for (int j = 0; j < n; ++j)
+    for (int i : lower[j]) upper[i].push_back(j);
+  std::vector<int> parent(n, -1), anc(n, -1);
+  for (int k = 0; k < n; ++k)
+    for (int j : upper[k]) {
+      int r = j;
+      while (anc[r] != -1 && anc[r] != k) {
+        const int nx = anc[r];
+        anc[r] = k;
+        r = nx;
+      }
+      if (anc[r] == -1) {
+        anc[r] = k;
+        parent[r] = k;
+      }
+    }
+  // column counts via row-subtree traversal
+  std::vector<int> cc(n, 1), flag(n, -1);
+  for (int k = 0; k < n; ++k) {
+    flag[k] = k;
+    for (int j : upper[k])
+      for (int i = j; flag[i] != k; i = parent[i]) {
+        cc[i]++;
+        flag[i] = k;
+      }
+  }
+  // fundamental supernodes
+  std::vector<int> nchild(n, 0);
+  for (int j = 0; j < n; ++j)
+    if (parent[j] >= 0) nchild[parent[j]]++;
+  std::vector<int> sn_of(n), s0;
+  for (int j = 0; j < n; ++j) {
+    const bool join = j > 0 && parent[j - 1] == j && cc[j - 1] == cc[j] + 1 && nchild[j] == 1;
+    if (!join) s0.push_back(j);
+    sn_of[j] = (int)s0.size() - 1;
+  }
+  const int ns = (int)s0.size();
+  s0.push_back(n);
+  // supernodal parent and structures
+  std::vector<int> sparent(ns, -1);
+  for (int s = 0; s < ns; ++s) {
+    const int last = s0[s + 1] - 1;
+    if (parent[last] >= 0) sparent[s] = sn_of[parent[last]];
+  }
+  std::vector<std::vector<int>> schild(ns);
+  for (int s = 0; s < ns; ++s)
+    if (sparent[s] >= 0) schild[sparent[s]].push_back(s);
+  std::vector<std::vector<int>> st(ns);
+  std::vector<int> mark(n, -1);
+  for (int s = 0; s < ns; ++s) {
+    const int c0 = s0[s], c1 = s0[s + 1];
+    std::vector<int>& R = st[s];
+    for (int c = c0; c < c1; ++c) R.push_back(c), mark[c] = s;
+    for (int c = c0; c < c1; ++c)
+      for (int r : lower[c])
+        if (r >= c1 && mark[r] != s) mark[r] = s, R.push_back(r);
+    for (int ch : schild[s])
+      for (int r : st[ch])
+        if (r >= c1 && mark[r] != s) mark[r] = s, R.push_back(r);
+    std::sort(R.begin() + (c1 - c0), R.end());
+  }
+  // ---- task selection on the supernodal tree ----
+  std::vector<long long> w(ns), W(ns);
+  for (int s = 0; s < ns; ++s) {
+    const long long nc = s0[s + 1] - s0[s], m = (long long)st[s].size();
+    w[s] = nc * m - nc * (nc + 1) / 2 + nc;
+  }
+  std::vector<long long> Cc(ns);
+  for (int s = 0; s < ns; ++s) W[s] = w[s], Cc[s] = s0[s + 1] - s0[s];
+  for (int s = 0; s < ns; ++s)
+    if (sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];  // children precede parents
+  std::vector<int> task_root;
+  std::vector<char> is_top(ns, 0);
+  std::function<void(int)> pick = [&](int s) {
+    const long long ws = Cc[s] + (long long)st[s].size() - (s0[s + 1] - s0[s]);
+    if (task_cap > 0 && W[s] <= task_cap && ws <= ws_cap) {
+      task_root.push_back(s);
+      return;
+    }
+    is_top[s] = 1;
+    for (int ch : schild[s]) pick(ch);
+  };
+  for (int s = 0; s < ns; ++s)
+    if (sparent[s] < 0) pick(s);
+  // order of supernodes: tasks (postorder subtrees, in original index order = postorder), then top
+  std::vector<int> owner(ns, -1);
+  std::sort(task_root.begin(), task_root.end());
+  std::vector<int> new_order;
+  new_order.reserve(ns);
+  F.ntask = (int)task_root.size();
+  std::function<void(int, int)> collect = [&](int s, int t) {
+    for (int ch : schild[s]) collect(ch, t);
+    owner[s] = t;
+    new_order.push_back(s);
+  };
+  std::vector<int> tsn0(F.ntask), tsn1(F.ntask);
+  for (int t = 0; t < F.ntask; ++t) {
+    tsn0[t] = (int)new_order.size();
+    collect(task_root[t], t);
+    tsn1[t] = (int)new_order.size();
+  }
+  F.top_sn0 = (int)new_order.size();
+  for (int s = 0; s < ns; ++s)
+    if (is_top[s]) new_order.push_back(s);  // increasing index is topological
+  // relabel columns
+  std::vector<int> newpos(n);
+  {
+    int pos = 0;
+    for (int s : new_order)
+      for (int c = s0[s]; c < s0[s + 1]; ++c) newpos[c] = pos++;
+  }
+  F.perm.resize(n);
+  F.iperm.resize(n);
+  for (int k = 0; k < n; ++k) {
+    F.perm[newpos[k]] = order[k];
+    F.iperm[order[k]] = newpos[k];
+  }
+  F.nsn = ns;
+  F.sn_col0.resize(ns), F.sn_ncol.resize(ns), F.sn_nrow.resize(ns), F.sn_task.resize(ns);
+  F.sn_rowoff.resize(ns + 1), F.sn_valoff.resize(ns + 1);
+  F.sn_rowoff[0] = F.sn_valoff[0] = 0;
+  for (int k = 0; k < ns; ++k) {
+    const int s = new_order[k];
+    const int nc = s0[s + 1] - s0[s], m = (int)st[s].size();
+    F.sn_col0[k] = newpos[s0[s]];
+    F.sn_ncol[k] = nc;
+    F.sn_nrow[k] = m;
+    F.sn_task[k] = owner[s];
+    std::vector<int> r;
+    r.reserve(m);
+    for (int x : st[s]) r.push_back(newpos[x]);
+    std::sort(r.begin() + nc, r.end());
+    F.rows.insert(F.rows.end(), r.begin(), r.end());
+    F.sn_rowoff[k + 1] = F.sn_rowoff[k] + m;
+    F.sn_valoff[k + 1] = F.sn_valoff[k] + (long long)nc * m - (long long)nc * (nc + 1) / 2;
+    F.flops_factor += (long long)nc * m * m;
+  }
+  F.nval = F.sn_valoff[ns];
+  // task column ranges, contribution rows and slots
+  F.slot.assign(F.rows.size(), -1);
+  F.top_c0 = F.top_sn0 < ns ? F.sn_col0[F.top_sn0] : n;
+  for (int t = 0; t < F.ntask; ++t) {
+    F.task_sn0.push_back(tsn0[t]);
+    F.task_sn1.push_back(tsn1[t]);
+    const int c0 = F.sn_col0[tsn0[t]];
+    const int c1 = F.sn_col0[tsn1[t] - 1] + F.sn_ncol[tsn1[t] - 1];
+    F.task_c0.push_back(c0);
+    F.task_c1.push_back(c1);
+    std::vector<int> cb;
+    for (int k = tsn0[t]; k < tsn1[t]; ++k)
+      for (long long q = F.sn_rowoff[k]; q < F.sn_rowoff[k + 1]; ++q)
+        if (F.rows[q] >= c1) cb.push_back(F.rows[q]);
+    std::sort(cb.begin(), cb.end());
+    cb.erase(std::unique(cb.begin(), cb.end()), cb.end());
+    F.task_cboff.push_back((int)F.cb_rows.size());
+    F.task_cblen.push_back((int)cb.size());
+    F.cb_rows.insert(F.cb_rows.end(), cb.begin(), cb.end());
+    F.max_task_ws = std::max(F.max_task_ws, (c1 - c0) + (int)cb.size());
+    for (int k = tsn0[t]; k < tsn1[t]; ++k)
+      for (long long q = F.sn_rowoff[k]; q < F.sn_rowoff[k + 1]; ++q) {
+        const int r = F.rows[q];
+        if (r < c1) {
+          if (r < c0) fail(kInternal, "symbolic: task row below its column range");
+          F.slot[q] = r - c0;
+        } else {
+          F.slot[q] = (c1 - c0) + int(std::lower_bound(cb.begin(), cb.end(), r) - cb.begin());
+        }
+      }
+  }
+  for (int k = F.top_sn0; k < ns; ++k)
+    for (long long q = F.sn_rowoff[k]; q < F.sn_rowoff[k + 1]; ++q) {
+      if (F.rows[q] < F.top_c0) fail(kInternal, "symbolic: top row below top range");
+      F.slot[q] = F.rows[q] - F.top_c0;
+    }
+  for (int v : F.cb_rows)
+    if (v < F.top_c0) fail(kInternal, "symbolic: contribution row outside the top part");
+  return F;
+}
+
+/// Host numeric supernodal LDL^T (setup phase) of a matrix with pattern A and
+/// values `vals` (natural order, symmetric).  Output: packed strict-lower
+/// trapezoids `L` (F.nval) and pivots `D` (F.n), position order.
+/// fixed: natural dofs replaced by identity rows/cols (floating subdomains).
+inline void factor_host(const SymFactor& F, const Csr& A, const double* vals, const std::vector<int>& fixed,
+                        std::vector<double>& L, std::vector<double>& D) {
+  const int n = F.n;
+  std::vector<char> isfix(n, 0);
+  for (int f : fixed) isfix[F.iperm[f]] = 1;
+  // full column-major blocks m x ncol per supernode
+  std::vector<long long> boff(F.nsn + 1, 0);
+  for (int k = 0; k < F.nsn; ++k) boff[k + 1] = boff[k] + (long long)F.sn_nrow[k] * F.sn_ncol[k];
+  std::vector<double> blk(boff[F.nsn], 0.0);
+  std::vector<int> sn_of(n);
+  for (int k = 0; k < F.nsn; ++k)
+    for (int c = 0; c < F.sn_ncol[k]; ++c) sn_of[F.sn_col0[k] + c] = k;
+  std::vector<int> where(n, -1);
+  // scatter lower triangle of P A P^T
+  for (int k = 0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    const int* R = &F.rows[F.sn_rowoff[k]];
+    for (int i = 0; i < m; ++i) where[R[i]] = i;
+    for (int c = 0; c < nc; ++c) {
+      const int pc = F.sn_col0[k] + c, nat = F.perm[pc];
+      if (isfix[pc]) {
+        blk[boff[k] + (long long)c * m + c] = 1.0;
+        continue;
+      }
+      for (int q = A.ptr[nat]; q < A.ptr[nat + 1]; ++q) {
+        const int pr = F.iperm[A.col[q]];
+        if (pr < pc || isfix[pr]) continue;
+        const int i = where[pr];
+        if (i < 0) fail(kInternal, "factor_host: entry outside symbolic structure");
+        blk[boff[k] + (long long)c * m + i] += vals[q];
+      }
+    }
+    for (int i = 0; i < m; ++i) where[R[i]] = -1;
+  }
+  D.assign(n, 0.0);
+  std::vector<double> W;
+  for (int k = 0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    double* B = &blk[boff[k]];
+    const int* R = &F.rows[F.sn_rowoff[k]];
+    // dense LDL^T of the trapezoid (left-looking inside the supernode)
+    for (int j = 0; j < nc; ++j) {
+      double* cj = B + (long long)j * m;
+      for (int p = 0; p < j; ++p) {
+        const double* cp = B + (long long)p * m;
+        const double f = cp[j] * D[F.sn_col0[k] + p];
+        if (f == 0.0) continue;
+        for (int i = j; i < m; ++i) cj[i] -= cp[i] * f;
+      }
+      const double d = cj[j];
+      if (d == 0.0 || !std::isfinite(d)) fail(kSingular, "subdomain saddle factorization failed (zero pivot)");
+      D[F.sn_col0[k] + j] = d;
+      const double inv = 1.0 / d;
+      for (int i = j + 1; i < m; ++i) cj[i] *= inv;
+    }
+    // update ancestors with W = L_R D L_R^T over off-diagonal rows R
+    const int mr = m - nc;
+    if (mr == 0) continue;
+    W.assign((std::size_t)mr * mr, 0.0);
+    for (int p = 0; p < nc; ++p) {
+      const double* cp = B + (long long)p * m + nc;
+      const double dp = D[F.sn_col0[k] + p];
+      for (int b = 0; b < mr; ++b) {
+        const double f = cp[b] * dp;
+        if (f == 0.0) continue;
+        double* wb = &W[(std::size_t)b * mr];
+        for (int a = b; a < mr; ++a) wb[a] += cp[a] * f;
+      }
+    }
+    // scatter-subtract into target supernodes
+    for (int b = 0; b < mr;) {
+      const int t = sn_of[R[nc + b]];
+      const int tm = F.sn_nrow[t];
+      const int* TR = &F.rows[F.sn_rowoff[t]];
+      for (int i = 0; i < tm; ++i) where[TR[i]] = i;
+      double* TB = &blk[boff[t]];
+      int b2 = b;
+      while (b2 < mr && sn_of[R[nc + b2]] == t) {
+        const int tc = R[nc + b2] - F.sn_col0[t];
+        const double* wb = &W[(std::size_t)b2 * mr];
+        double* tcol = TB + (long long)tc * tm;
+        for (int a = b2; a < mr; ++a) tcol[where[R[nc + a]]] -= wb[a];
+        ++b2;
+      }
+      for (int i = 0; i < tm; ++i) where[TR[i]] = -1;
+      b = b2;
+    }
+  }
+  // pack strict lower trapezoids
+  L.assign(F.nval, 0.0);
+  for (int k = 0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    long long o = F.sn_valoff[k];
+    for (int j = 0; j < nc; ++j)
+      for (int i = j + 1; i < m; ++i) L[o++] = blk[boff[k] + (long long)j * m + i];
+  }
+}
+
+/// Host supernodal solve with the packed layout (validation and the seeded
+/// factor check only; the engine's solves run on the device).
+inline void solve_host(const SymFactor& F, const std::vector<double>& L, const std::vector<double>& D,
+                       double* x_natural) {
+  std::vector<double> x(F.n);
+  for (int p = 0; p < F.n; ++p) x[p] = x_natural[F.perm[p]];
+  for (int k = 0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    const int* R = &F.rows[F.sn_rowoff[k]];
+    const double* V = &L[F.sn_valoff[k]];
+    for (int j = 0; j < nc; ++j) {
+      const double xj = x[R[j]];
+      for (int i = j + 1; i < m; ++i) x[R[i]] -= (*V++) * xj;
+    }
+  }
+  for (int p = 0; p < F.n; ++p) x[p] /= D[p];
+  for (int k = F.nsn - 1; k >= 0; --k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    const int* R = &F.rows[F.sn_rowoff[k]];
+    for (int j = nc - 1; j >= 0; --j) {
+      const long long o = F.sn_valoff[k] + (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
+      double s = x[R[j]];
+      for (int i = j + 1; i < m; ++i) s -= L[o + (i - j - 1)] * x[R[i]];
+      x[R[j]] = s;
+    }
+  }
+  for (int p = 0; p < F.n; ++p) x_natural[F.perm[p]] = x[p];
+}
+
+/// Host emulation of the device task schedule (k_leaf_fwd / k_top /
+/// k_leaf_bwd, identical slot and fold semantics) for the CPU validation of
+/// the symbolic layout.  x in position order, solved in place.
+inline void solve_tasks_host(const SymFactor& F, const std::vector<double>& L, const std::vector<double>& D,
+                             std::vector<double>& x) {
+  std::vector<double> CB(F.cb_rows.size(), 0.0);
+  for (int t = 0; t < F.ntask; ++t) {
+    const int c0 = F.task_c0[t], c1 = F.task_c1[t], nct = c1 - c0, cbl = F.task_cblen[t];
+    std::vector<double> ws(nct + cbl, 0.0);
+    for (int i = 0; i < nct; ++i) ws[i] = x[c0 + i];
+    for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
+      const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+      const int* sl = &F.slot[F.sn_rowoff[k]];
+      const double* V = &L[F.sn_valoff[k]];
+      for (int j = 0; j < nc; ++j) {
+        const double xj = ws[sl[j]];
+        for (int i = j + 1; i < m; ++i) ws[sl[i]] -= (*V++) * xj;
+      }
+    }
+    for (int i = 0; i < nct; ++i) x[c0 + i] = ws[i] / D[c0 + i];
+    for (int i = 0; i < cbl; ++i) CB[F.task_cboff[t] + i] = ws[nct + i];
+  }
+  const int ntop = F.n - F.top_c0;
+  std::vector<double> ws(ntop);
+  std::vector<std::vector<int>> lists(ntop);
+  for (int t = 0; t < F.ntask; ++t)
+    for (int i = 0; i < F.task_cblen[t]; ++i) lists[F.cb_rows[F.task_cboff[t] + i] - F.top_c0].push_back(F.task_cboff[t] + i);
+  for (int i = 0; i < ntop; ++i) {
+    double v = x[F.top_c0 + i];
+    for (int q : lists[i]) v += CB[q];
+    ws[i] = v;
+  }
+  for (int k = F.top_sn0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    const int* sl = &F.slot[F.sn_rowoff[k]];
+    const double* V = &L[F.sn_valoff[k]];
+    for (int j = 0; j < nc; ++j) {
+      const double xj = ws[sl[j]];
+      for (int i = j + 1; i < m; ++i) ws[sl[i]] -= (*V++) * xj;
+    }
+  }
+  for (int i = 0; i < ntop; ++i) ws[i] /= D[F.top_c0 + i];
+  for (int k = F.nsn - 1; k >= F.top_sn0; --k) {
+    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+    const int* sl = &F.slot[F.sn_rowoff[k]];
+    for (int j = nc - 1; j >= 0; --j) {
+      const long long o = F.sn_valoff[k] + (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
+      double s = 0;
+      for (int i = j + 1; i < m; ++i) s += L[o + (i - j - 1)] * ws[sl[i]];
+      ws[sl[j]] -= s;
+    }
+  }
+  for (int i = 0; i < ntop; ++i) x[F.top_c0 + i] = ws[i];
+  for (int t = 0; t < F.ntask; ++t) {
+    const int c0 = F.task_c0[t], c1 = F.task_c1[t], nct = c1 - c0, cbl = F.task_cblen[t];
+    std::vector<double> w2(nct + cbl);
+    for (int i = 0; i < nct; ++i) w2[i] = x[c0 + i];
+    for (int i = 0; i < cbl; ++i) w2[nct + i] = x[F.cb_rows[F.task_cboff[t] + i]];
+    for (int k = F.task_sn1[t] - 1; k >= F.task_sn0[t]; --k) {
+      const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+      const int* sl = &F.slot[F.sn_rowoff[k]];
+      for (int j = nc - 1; j >= 0; --j) {
+        const long long o = F.sn_valoff[k] + (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
+        double s = 0;
+        for (int i = j + 1; i < m; ++i) s += L[o + (i - j - 1)] * w2[sl[i]];
+        w2[sl[j]] -= s;
+      }
+    }
+    for (int i = 0; i < nct; ++i) x[c0 + i] = w2[i];
+  }
+}
+
+}  // namespace pf
