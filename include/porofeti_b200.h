@@ -74,6 +74,7 @@ typedef struct pf_info {
   double t_setup, t_assemble, t_factor, t_upload;
   double bytes_fapply;  /* algorithmic bytes of one F-apply (SURVEY §8d B_F) */
   double bytes_precond; /* algorithmic bytes of one preconditioner apply */
+  int n_levels;         /* task levels of the subdomain sweep schedule */
 } pf_info;
 
 typedef struct pf_sub_info {
@@ -133,9 +134,16 @@ int pf_current_step(const pf_ctx* ctx);
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 F-apply solve phase only. */
 int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
+/* nsteps device-resident StepSolver::advance calls bracketed by CUDA events. */
+int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total);
+/* number of kernels this library has launched (process-wide counter). */
+long long pf_launch_count(void);
 /* dominant-kernel timing of the last pf_bench_op / pf_step: average ms of the
  * factor-sweep kernels per F-apply and the number of launches per F-apply */
 int pf_kernel_stats(pf_ctx* ctx, double* sweep_ms, int* launches_per_apply);
+
+/* Per-kernel timing of the sweeps (see pf_engine.cu): 10 doubles. */
+int pf_phase_stats(pf_ctx* ctx, int iters, double* out);
 
 /* Element-level entry points (elements.hpp:152-251) evaluated on the device,
  * used by the parity tests: tri = 3 vertices (x0,y0,x1,y1,x2,y2). */

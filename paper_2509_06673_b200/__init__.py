@@ -93,7 +93,7 @@ class Info(C.Structure):
         ("nnz_K", C.c_longlong), ("n_supernodes", C.c_longlong), ("n_tasks", C.c_longlong),
         ("tau", C.c_double), ("T", C.c_double),
         ("t_setup", C.c_double), ("t_assemble", C.c_double), ("t_factor", C.c_double), ("t_upload", C.c_double),
-        ("bytes_fapply", C.c_double), ("bytes_precond", C.c_double),
+        ("bytes_fapply", C.c_double), ("bytes_precond", C.c_double), ("n_levels", C.c_int),
     ]
 
 
@@ -181,6 +181,9 @@ def lib():
         L.pf_current_step.argtypes = [vp]
         L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
+        L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
+        L.pf_bench_steps.argtypes = [vp, C.c_int, vp, vp, vp]
+        L.pf_launch_count.restype = C.c_longlong
         L.pf_debug_factor_solve.argtypes = [C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_longlong, vp]
         L.pf_debug_disc.argtypes = [C.POINTER(Config), vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib = L
@@ -286,12 +289,29 @@ class FetiOperator:
         _check(lib().pf_step(self.h, C.byref(rep)), self.h)
         return rep.as_dict()
 
+    def bench_steps(self, nsteps):
+        ms = C.c_double()
+        it, fa = C.c_int(), C.c_int()
+        _check(lib().pf_bench_steps(self.h, nsteps, C.byref(ms), C.byref(it), C.byref(fa)), self.h)
+        return ms.value, it.value, fa.value
+
     def bench(self, kind=0, warmup=5, iters=20):
         ms = C.c_double()
         _check(lib().pf_bench_op(self.h, kind, warmup, iters, C.byref(ms)), self.h)
         sweep, launches = C.c_double(), C.c_int()
         lib().pf_kernel_stats(self.h, C.byref(sweep), C.byref(launches))
         return ms.value, sweep.value, launches.value
+
+
+def launch_count():
+    """Kernels launched by the engine library so far (process-wide)."""
+    return int(lib().pf_launch_count())
+
+
+def phase_stats(op, iters=5):
+    out = np.zeros(10)
+    _check(lib().pf_phase_stats(op.h, iters, _ptr(out)), op.h)
+    return dict(K=out[0:3].tolist(), II=out[3:6].tolist(), Q=out[6:9].tolist(), precond=float(out[9]))
 
 
 class StepSolver:

@@ -25,6 +25,8 @@
 
 namespace pf {
 
+std::atomic<long long> g_launches{0};  // kernel launches issued by this library (bench bookkeeping)
+
 #define PF_CUDA_CHECK(x)                                                                    \
   do {                                                                                      \
     cudaError_t e_ = (x);                                                                   \
@@ -39,6 +41,14 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p, n = o.n, o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
   ~DevBuf() {
     if (p) cudaFree(p);
   }
@@ -88,14 +98,17 @@ struct SolveSystem {
   std::vector<int> prob_type;
   std::vector<long long> prob_x, prob_lval, prob_cb;
   long long total_x = 0, total_L = 0, total_cb = 0;
-  int nwork = 0, ws_max = 0, top_max = 0;
+  int nlevel = 0;
+  std::vector<int> level_nwork, level_ws;  // per global level
+  std::vector<DevBuf<int>> d_wp, d_wt;     // per global level work lists
   DevBuf<dev::TypeDesc> d_types;
   DevBuf<int> d_sn_col0, d_sn_ncol, d_sn_nrow, d_slot, d_t0, d_t1, d_c0, d_c1, d_cbo, d_cbl, d_cbrows,
-      d_fold_ptr, d_fold_idx, d_prob_type, d_work_prob, d_work_task, d_perm, d_prob_n;
+      d_fold_ptr, d_fold_idx, d_prob_type, d_perm, d_prob_n;
   DevBuf<long long> d_sn_rowoff, d_sn_valoff, d_prob_x, d_prob_lval, d_prob_cb, d_prob_perm;
   DevBuf<double> L, D, X, CB;
   int nrhs_alloc = 1;
   long long nnzL = 0;
+  int ws_max = 0;  // level-0 warp workspace
 
   void build(const std::vector<const SymFactor*>& types, const std::vector<int>& ptype, int nrhs) {
     syms = types;
@@ -104,54 +117,44 @@ struct SolveSystem {
     std::vector<dev::TypeDesc> td(types.size());
     std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm;
     std::vector<long long> sn_rowoff, sn_valoff, type_perm_off;
+    nlevel = 0;
+    for (auto* F : types) nlevel = std::max(nlevel, F->nlevel);
+    level_ws.assign(nlevel, 0);
+    auto glevel = [&](const SymFactor& F, int l) { return l == F.nlevel - 1 ? nlevel - 1 : l; };
     for (std::size_t k = 0; k < types.size(); ++k) {
       const SymFactor& F = *types[k];
       dev::TypeDesc& T = td[k];
-      T.n = F.n, T.nsn = F.nsn, T.ntask = F.ntask, T.top_sn0 = F.top_sn0, T.top_c0 = F.top_c0;
+      T.n = F.n, T.nsn = F.nsn, T.ntask = F.ntask;
       T.sn_base = (int)sn_col0.size();
       T.task_base = (int)t0.size();
-      T.fold_base = (int)fptr.size();
       T.row_base = (long long)slot.size();
       T.cb_base = (long long)cbrows.size();
-      // cb_base indexes both cb_rows and fold_idx: keep them aligned
+      T.fold_base = (long long)fptr.size();
+      T.foldidx_base = (long long)fidx.size();
       for (int s = 0; s < F.nsn; ++s) {
-        sn_col0.push_back(F.sn_col0[s]);
-        sn_ncol.push_back(F.sn_ncol[s]);
-        sn_nrow.push_back(F.sn_nrow[s]);
-        sn_rowoff.push_back(F.sn_rowoff[s]);
-        sn_valoff.push_back(F.sn_valoff[s]);
+        sn_col0.push_back(F.sn_col0[s]), sn_ncol.push_back(F.sn_ncol[s]), sn_nrow.push_back(F.sn_nrow[s]);
+        sn_rowoff.push_back(F.sn_rowoff[s]), sn_valoff.push_back(F.sn_valoff[s]);
       }
       slot.insert(slot.end(), F.slot.begin(), F.slot.end());
       for (int t = 0; t < F.ntask; ++t) {
         t0.push_back(F.task_sn0[t]), t1.push_back(F.task_sn1[t]);
         c0.push_back(F.task_c0[t]), c1.push_back(F.task_c1[t]);
         cbo.push_back(F.task_cboff[t]), cbl.push_back(F.task_cblen[t]);
+        const int gl = glevel(F, F.task_level[t]);
+        const int ws = (F.task_c1[t] - F.task_c0[t]) + F.task_cblen[t];
+        level_ws[gl] = std::max(level_ws[gl], ws);
       }
-      // cb_rows (positions) and fold lists (per top row: cb slots in task order)
-      const int ntop = F.n - F.top_c0;
-      std::vector<std::vector<int>> lists(ntop);
-      for (int t = 0; t < F.ntask; ++t)
-        for (int i = 0; i < F.task_cblen[t]; ++i)
-          lists[F.cb_rows[F.task_cboff[t] + i] - F.top_c0].push_back(F.task_cboff[t] + i);
-      std::vector<int> fi;
-      fptr.push_back(0);
-      for (int i = 0; i < ntop; ++i) {
-        fi.insert(fi.end(), lists[i].begin(), lists[i].end());
-        fptr.push_back((int)fi.size());
-      }
-      // store: cb_rows at cb_base, fold_idx at cb_base (same length = total cb entries)
       cbrows.insert(cbrows.end(), F.cb_rows.begin(), F.cb_rows.end());
-      if (fi.size() != F.cb_rows.size()) fail(kInternal, "fold list size mismatch");
-      fidx.insert(fidx.end(), fi.begin(), fi.end());
+      fptr.insert(fptr.end(), F.fold_ptr.begin(), F.fold_ptr.end());
+      fidx.insert(fidx.end(), F.fold_idx.begin(), F.fold_idx.end());
       type_perm_off.push_back((long long)perm.size());
       perm.insert(perm.end(), F.perm.begin(), F.perm.end());
-      ws_max = std::max(ws_max, F.max_task_ws);
-      top_max = std::max(top_max, ntop);
     }
-    // problems
+    ws_max = nlevel > 1 ? level_ws[0] : 0;
     const int np = (int)ptype.size();
     prob_x.resize(np), prob_lval.resize(np), prob_cb.resize(np);
-    std::vector<int> wp, wt, pn;
+    std::vector<std::vector<int>> wp(nlevel), wt(nlevel);
+    std::vector<int> pn;
     std::vector<long long> pperm;
     total_x = total_L = total_cb = 0;
     nnzL = 0;
@@ -160,18 +163,26 @@ struct SolveSystem {
       prob_x[p] = total_x, prob_lval[p] = total_L, prob_cb[p] = total_cb;
       total_x += F.n, total_L += F.nval, total_cb += (long long)F.cb_rows.size();
       nnzL += F.nval;
-      for (int t = 0; t < F.ntask; ++t) wp.push_back(p), wt.push_back(t);
+      for (int t = 0; t < F.ntask; ++t) {
+        const int gl = glevel(F, F.task_level[t]);
+        wp[gl].push_back(p), wt[gl].push_back(t);
+      }
       pn.push_back(F.n);
       pperm.push_back(type_perm_off[ptype[p]]);
     }
-    nwork = (int)wp.size();
+    d_wp.clear(), d_wt.clear();
+    d_wp.resize(nlevel), d_wt.resize(nlevel);
+    level_nwork.assign(nlevel, 0);
+    for (int l = 0; l < nlevel; ++l) {
+      d_wp[l].upload(wp[l]), d_wt[l].upload(wt[l]);
+      level_nwork[l] = (int)wp[l].size();
+    }
     d_types.upload(td);
     d_sn_col0.upload(sn_col0), d_sn_ncol.upload(sn_ncol), d_sn_nrow.upload(sn_nrow);
     d_sn_rowoff.upload(sn_rowoff), d_sn_valoff.upload(sn_valoff), d_slot.upload(slot);
     d_t0.upload(t0), d_t1.upload(t1), d_c0.upload(c0), d_c1.upload(c1), d_cbo.upload(cbo), d_cbl.upload(cbl);
     d_cbrows.upload(cbrows), d_fold_ptr.upload(fptr), d_fold_idx.upload(fidx);
     d_prob_type.upload(ptype), d_prob_x.upload(prob_x), d_prob_lval.upload(prob_lval), d_prob_cb.upload(prob_cb);
-    d_work_prob.upload(wp), d_work_task.upload(wt);
     d_perm.upload(perm), d_prob_perm.upload(pperm), d_prob_n.upload(pn);
     L.alloc(total_L);
     D.alloc(total_x);
@@ -179,7 +190,7 @@ struct SolveSystem {
     CB.alloc(std::max<long long>(1, total_cb * nrhs));
   }
 
-  dev::SolveSet set(int nrhs) {
+  dev::SolveSet set(int nrhs, int level) {
     dev::SolveSet S;
     S.types = d_types.p;
     S.sn_col0 = d_sn_col0.p, S.sn_ncol = d_sn_ncol.p, S.sn_nrow = d_sn_nrow.p;
@@ -189,50 +200,72 @@ struct SolveSystem {
     S.fold_ptr = d_fold_ptr.p, S.fold_idx = d_fold_idx.p;
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
-    S.nwork = nwork, S.work_prob = d_work_prob.p, S.work_task = d_work_task.p;
+    S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p;
     S.L = L.p, S.D = D.p, S.X = X.p, S.CB = CB.p;
     S.nrhs = nrhs;
     S.x_stride = total_x, S.cb_stride = total_cb;
     return S;
   }
 
+  static constexpr int kWpb = 4;
+  static constexpr int kCtaSmemDoubles = 24 * 1024;
   int launches = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timed = false;
+  double phase_ms[3] = {0, 0, 0};  // warp levels / CTA levels + root / backward
+
+  void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
+    if (level_nwork[l] == 0) return;
+    dev::SolveSet S = set(nrhs, l);
+    if (l == 0 && nlevel > 1) {
+      const std::size_t sm = sizeof(double) * (std::size_t)(ws_max + 32) * kWpb;
+      if (mode == 0)
+        dev::k_leaf_fwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);
+      else
+        dev::k_leaf_bwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);
+    } else {
+      const bool in_smem = level_ws[l] <= kCtaSmemDoubles;
+      dev::k_cta_level<<<S.nwork, dev::kTopThreads, in_smem ? sizeof(double) * level_ws[l] : 0, st>>>(
+          S, mode, in_smem ? 1 : 0);
+    }
+    ::pf::g_launches++;
+    ++launches;
+  }
+
   /// In-place solve of X (permuted order) for nrhs right-hand sides.
   void solve(cudaStream_t st, int nrhs) {
-    dev::SolveSet S = set(nrhs);
-    const int wpb = 4;
     launches = 0;
-    if (nwork > 0) {
-      const std::size_t sm = sizeof(double) * (std::size_t)ws_max * wpb;
-      dev::k_leaf_fwd<<<cdiv(nwork, wpb), 32 * wpb, sm, st>>>(S, ws_max);
-      ++launches;
+    if (timed) {
+      if (!ev[0])
+        for (auto& e : ev) cudaEventCreate(&e);
+      cudaEventRecord(ev[0], st);
     }
-    if (top_max > 0) {
-      const bool sm = top_in_smem();
-      dev::k_top<<<S.nprob, 256, sm ? sizeof(double) * top_max : 0, st>>>(S, sm ? 1 : 0);
-      ++launches;
-    }
-    if (nwork > 0) {
-      const std::size_t sm = sizeof(double) * (std::size_t)ws_max * wpb;
-      dev::k_leaf_bwd<<<cdiv(nwork, wpb), 32 * wpb, sm, st>>>(S, ws_max);
-      ++launches;
+    for (int l = 0; l + 1 < nlevel; ++l) launch_level(st, nrhs, l, 0);
+    if (timed) cudaEventRecord(ev[1], st);
+    if (nlevel > 0) launch_level(st, nrhs, nlevel - 1, 1);
+    if (timed) cudaEventRecord(ev[2], st);
+    for (int l = nlevel - 2; l >= 0; --l) launch_level(st, nrhs, l, 2);
+    if (timed) {
+      cudaEventRecord(ev[3], st);
+      cudaEventSynchronize(ev[3]);
+      for (int i = 0; i < 3; ++i) {
+        float t;
+        cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+        phase_ms[i] += t;
+      }
     }
     PF_CUDA_CHECK(cudaGetLastError());
   }
 
-  bool top_in_smem() const { return sizeof(double) * (std::size_t)top_max <= 200 * 1024; }
   void prepare_smem() {
-    const int wpb = 4;
-    const std::size_t sm_leaf = sizeof(double) * (std::size_t)ws_max * wpb;
-    const std::size_t sm_top = top_in_smem() ? sizeof(double) * (std::size_t)top_max : 0;
+    const std::size_t sm_leaf = sizeof(double) * (std::size_t)(ws_max + 32) * kWpb;
     if (sm_leaf > 227 * 1024)
       fail(kInternal, "leaf solve workspace exceeds shared memory (" + std::to_string(sm_leaf) + " B)");
-    (void)sm_top;
     // the attribute is per kernel (shared by all systems): raise it to the opt-in maximum once
     const int smax = 227 * 1024;
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_leaf_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_leaf_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_top, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - 1024));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_cta_level, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - 3 * 1024));
   }
 };
 
@@ -657,9 +690,9 @@ struct Engine {
     dev::FemSet S = femset();
     for (int c = 0; c < 8; ++c) {
       const int n = colour_threads(c);
-      if (n) dev::k_assemble<<<cdiv(n, 128), 128, 0, st>>>(S, c, Kv.p, Lv.p);
+      if (n) dev::k_assemble<<<cdiv(n, 128), 128, 0, st>>>(S, c, Kv.p, Lv.p); ::pf::g_launches++;
     }
-    dev::k_constraint_diag<<<dim3(4, S.nsub), 128, 0, st>>>(S, Kv.p);
+    dev::k_constraint_diag<<<dim3(4, S.nsub), 128, 0, st>>>(S, Kv.p); ::pf::g_launches++;
     PF_CUDA_CHECK(cudaGetLastError());
   }
 
@@ -1087,6 +1120,7 @@ struct Engine {
     info.nnz_K = total_kv;
     long long nsn = 0, ntask = 0;
     for (std::size_t s = 0; s < D.subs.size(); ++s) nsn += ksym[D.subs[s].type].nsn, ntask += ksym[D.subs[s].type].ntask;
+    info.n_levels = Ksys.nlevel;
     info.n_supernodes = nsn, info.n_tasks = ntask;
     info.tau = D.mat.tau, info.T = D.mat.T;
     // B_F = sum_s [2*8*nnz(L_s) + 8*dim_s] + 2*(8+4)*nnz(G) + 2*8*n_lambda (supernodal values)
@@ -1099,15 +1133,15 @@ struct Engine {
   // ------------------------------------------------------------------
   // operators (device pointers)
   void dot(int n, const double* a, const double* b, int slot) {
-    dev::k_dot_partial<<<dev::kRedBlocks, dev::kRedThreads, 0, st>>>(n, a, b, red_part.p);
-    dev::k_dot_final<<<1, dev::kRedThreads, 0, st>>>(dev::kRedBlocks, red_part.p, scal.p + slot);
+    dev::k_dot_partial<<<dev::kRedBlocks, dev::kRedThreads, 0, st>>>(n, a, b, red_part.p); ::pf::g_launches++;
+    dev::k_dot_final<<<1, dev::kRedThreads, 0, st>>>(dev::kRedBlocks, red_part.p, scal.p + slot); ::pf::g_launches++;
   }
 
   void spmv2(const DevBuf<int>& ptr, const DevBuf<int>& mid, const DevBuf<long long>& idx, const DevBuf<double>& val,
              const double* X, double* y, double alpha, int acc, const double* sub = nullptr) {
     if (D.n_lambda == 0) return;
     dev::k_spmv2_ll<<<cdiv(D.n_lambda, 256), 256, 0, st>>>(D.n_lambda, ptr.p, mid.p, idx.p, val.p, X, y, alpha, acc,
-                                                           sub);
+                                                           sub); ::pf::g_launches++;
   }
 
   /// y = sum_s G_s K_s^+ G_s^T x
@@ -1115,7 +1149,7 @@ struct Engine {
     Ksys.X.zero(st);
     if (g_lam2X.nrows)
       dev::k_gather_ll<<<cdiv(g_lam2X.nrows, 256), 256, 0, st>>>(g_lam2X.nrows, g_lam2X.rows.p, g_lam2X.ptr.p,
-                                                                g_lam2X.idx.p, g_lam2X.val.p, x, Ksys.X.p, 1.0, 0);
+                                                                g_lam2X.idx.p, g_lam2X.val.p, x, Ksys.X.p, 1.0, 0); ::pf::g_launches++;
     Ksys.solve(st, 1);
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, y, 1.0, 0);
     launches_per_apply = Ksys.launches + 3;
@@ -1125,10 +1159,10 @@ struct Engine {
   void qsolve(const double* x, double* y) {
     const int n = D.n_lambda;
     dev::k_perm_in<<<dim3(cdiv(n, 256), 1), 256, 0, st>>>(1, Qsys.d_prob_x.p, zero_off(), Qsys.d_prob_n.p,
-                                                         Qsys.d_prob_perm.p, Qsys.d_perm.p, x, Qsys.X.p, nullptr, 0);
+                                                         Qsys.d_prob_perm.p, Qsys.d_perm.p, x, Qsys.X.p, nullptr, 0); ::pf::g_launches++;
     Qsys.solve(st, 1);
     dev::k_perm_out<<<dim3(cdiv(n, 256), 1), 256, 0, st>>>(1, Qsys.d_prob_x.p, zero_off(), Qsys.d_prob_n.p,
-                                                          Qsys.d_prob_perm.p, Qsys.d_perm.p, Qsys.X.p, y);
+                                                          Qsys.d_prob_perm.p, Qsys.d_perm.p, Qsys.X.p, y); ::pf::g_launches++;
   }
   DevBuf<long long> d_zero_off;
   const long long* zero_off() {
@@ -1140,7 +1174,7 @@ struct Engine {
   void precond_raw(const double* r, double* z) {
     const int n = D.n_lambda;
     if (use_gen) {
-      dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, m_ptr.p, m_idx.p, m_val.p, r, z, 1.0, 0.0);
+      dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, m_ptr.p, m_idx.p, m_val.p, r, z, 1.0, 0.0); ::pf::g_launches++;
       return;
     }
     if (!use_dir) {
@@ -1151,12 +1185,12 @@ struct Engine {
     WB.zero(st);
     if (g_lam2B.nrows)
       dev::k_gather_ll<<<cdiv(g_lam2B.nrows, 256), 256, 0, st>>>(g_lam2B.nrows, g_lam2B.rows.p, g_lam2B.ptr.p,
-                                                                g_lam2B.idx.p, g_lam2B.val.p, r, WB.p, 1.0, 0);
+                                                                g_lam2B.idx.p, g_lam2B.val.p, r, WB.p, 1.0, 0); ::pf::g_launches++;
     Isys.X.zero(st);
     const int ns = (int)D.subs.size();
-    dev::k_dir_pre<<<dim3(8, ns), 256, 0, st>>>(dirset(false), WB.p, Isys.X.p, YB.p);
+    dev::k_dir_pre<<<dim3(8, ns), 256, 0, st>>>(dirset(false), WB.p, Isys.X.p, YB.p); ::pf::g_launches++;
     Isys.solve(st, 1);
-    dev::k_dir_post<<<dim3(4, ns), 128, 0, st>>>(dirset(true), Isys.X.p, YB.p, SB.p);
+    dev::k_dir_post<<<dim3(4, ns), 128, 0, st>>>(dirset(true), Isys.X.p, YB.p, SB.p); ::pf::g_launches++;
     spmv2(b_ptr, b_mid, b_idx, b_val, SB.p, z, 1.0, 0);
   }
 
@@ -1173,9 +1207,9 @@ struct Engine {
   void project(double* v) {
     if (nc == 0) return;
     const int n = D.n_lambda;
-    dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0);
-    dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, c_tmp2.p);
-    dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, v, -1.0, 1.0);
+    dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0); ::pf::g_launches++;
+    dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, c_tmp2.p); ::pf::g_launches++;
+    dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, v, -1.0, 1.0); ::pf::g_launches++;
   }
 
   // ------------------------------------------------------------------
@@ -1186,14 +1220,14 @@ struct Engine {
     zacc.zero(st);
     for (int c = 0; c < 8; ++c) {
       const int n = colour_threads(c);
-      if (n) dev::k_rhs_elem<<<cdiv(n, 128), 128, 0, st>>>(S, c, t, bvec.p, zacc.p);
+      if (n) dev::k_rhs_elem<<<cdiv(n, 128), 128, 0, st>>>(S, c, t, bvec.p, zacc.p); ::pf::g_launches++;
     }
-    if (total_g) dev::k_constraint_values<<<dim3(4, S.nsub), 128, 0, st>>>(S, t, gval.p);
+    if (total_g) dev::k_constraint_values<<<dim3(4, S.nsub), 128, 0, st>>>(S, t, gval.p); ::pf::g_launches++;
     dev::RhsSet R;
     R.nsub = S.nsub, R.types = d_ftypes.p, R.subs = d_fsubs.p;
     R.kptr = d_kptr.p, R.kcol = d_kcol.p, R.lptr = d_lptr.p, R.lcol = d_lcol.p, R.cpos = d_cpos.p;
     R.Kv = Kv.p, R.Lv = Lv.p, R.state = state.p, R.zacc = zacc.p, R.g = gval.p, R.tau = D.mat.tau;
-    dev::k_rhs_finalize<<<dim3(16, S.nsub), 256, 0, st>>>(R, bvec.p);
+    dev::k_rhs_finalize<<<dim3(16, S.nsub), 256, 0, st>>>(R, bvec.p); ::pf::g_launches++;
     // d = -sum_s Gc_s g_s
     if (D.n_lambda) spmv2(gc_ptr, gc_mid, gc_idx, gc_val, gval.p, dvec.p, -1.0, 0);
     PF_CUDA_CHECK(cudaGetLastError());
@@ -1202,7 +1236,7 @@ struct Engine {
   /// F = sum_s G_s K_s^+ b_s - d  (into out)
   void interface_rhs(double* out) {
     perm_in_K(bvec.p);
-    if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p);
+    if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, out, 1.0, 0, dvec.p);
   }
@@ -1213,14 +1247,14 @@ struct Engine {
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, src, Ksys.X.p, nullptr,
-                                                            0);
+                                                            0); ::pf::g_launches++;
   }
   void perm_out_K(double* dst) {
     const int np = (int)D.subs.size();
     int maxn = 0;
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_out<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
-                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, Ksys.X.p, dst);
+                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, Ksys.X.p, dst); ::pf::g_launches++;
   }
   DevBuf<long long> d_subvec_buf;
   const long long* d_subvec() {
@@ -1233,12 +1267,12 @@ struct Engine {
     perm_in_K(bvec.p);
     if (g_back.nrows)
       dev::k_gather_ll<<<cdiv(g_back.nrows, 256), 256, 0, st>>>(g_back.nrows, g_back.rows.p, g_back.ptr.p,
-                                                               g_back.idx.p, g_back.val.p, lambda, Ksys.X.p, -1.0, 1);
-    if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p);
+                                                               g_back.idx.p, g_back.val.p, lambda, Ksys.X.p, -1.0, 1); ::pf::g_launches++;
+    if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
     perm_out_K(state.p);
     if (nc) dev::k_rigid_add<<<dim3(8, nfloat), 256, 0, st>>>(nfloat, d_fvec.p, d_fnu.p, d_fxy.p, d_fxyoff.p,
-                                                             alpha_vec.p, state.p);
+                                                             alpha_vec.p, state.p); ::pf::g_launches++;
   }
 
   // ------------------------------------------------------------------
@@ -1269,7 +1303,7 @@ struct Engine {
     double* r = kr_r.p;
     // r = rhs - F lambda, projected
     F_(lambda, r);
-    dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, r);
+    dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, r); ::pf::g_launches++;
     project(r);
     rep.iterations = 0;
     rep.converged = 0;
@@ -1297,9 +1331,9 @@ struct Engine {
         PF_CUDA_CHECK(cudaStreamSynchronize(st));
         if (h_scal[1] <= 1e-14 * h_scal[2])
           fail(kBreakdown, "feti_pcg: <p, Kp> not positive (operator not SPD?)");
-        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, 1.0, scal.p + 0, scal.p + 1, p, lambda);
+        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, 1.0, scal.p + 0, scal.p + 1, p, lambda); ::pf::g_launches++;
         project(q);
-        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, -1.0, scal.p + 0, scal.p + 1, q, r);
+        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, -1.0, scal.p + 0, scal.p + 1, q, r); ::pf::g_launches++;
         M_(r, z);
         dot(n, r, z, 3);  // rz_next
         const double rzn = read_scal(3);
@@ -1310,7 +1344,7 @@ struct Engine {
           break;
         }
         if (rzn <= 0.0) fail(kBreakdown, "feti_pcg: preconditioned residual norm lost positivity");
-        dev::k_xpay_dev<<<nb, 256, 0, st>>>(n, z, p, scal.p + 3, scal.p + 0);
+        dev::k_xpay_dev<<<nb, 256, 0, st>>>(n, z, p, scal.p + 3, scal.p + 0); ::pf::g_launches++;
         PF_CUDA_CHECK(cudaMemcpyAsync(scal.p + 0, scal.p + 3, sizeof(double), cudaMemcpyDeviceToDevice, st));
       }
       rep.rel_residual = delta / d0;
@@ -1340,7 +1374,7 @@ struct Engine {
       const double sigma = read_scal(1);
       if (sigma == 0.0 || !std::isfinite(sigma)) fail(kBreakdown, "sqmr: <q, Fq> vanished (Lanczos breakdown)");
       const double a = rho / sigma;
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, -a, t, 1.0, r);
+      dev::k_axpby<<<nb, 256, 0, st>>>(n, -a, t, 1.0, r); ::pf::g_launches++;
       dot(n, r, r, 2);
       const double rn = std::sqrt(read_scal(2));
       const double th_old = theta;
@@ -1349,7 +1383,7 @@ struct Engine {
       tau = tau * theta * c;
       h_scal[0] = rho, h_scal[1] = sigma, h_scal[4] = th_old, h_scal[5] = c;
       PF_CUDA_CHECK(cudaMemcpyAsync(scal.p + 20, h_scal.data(), 6 * sizeof(double), cudaMemcpyHostToDevice, st));
-      dev::k_sqmr_dx<<<nb, 256, 0, st>>>(n, scal.p + 20, q, d, lambda);
+      dev::k_sqmr_dx<<<nb, 256, 0, st>>>(n, scal.p + 20, q, d, lambda); ::pf::g_launches++;
       est = tau * std::sqrt(double(k + 2));
       rep.iterations = k + 1;
       if (est <= tol * t0) {
@@ -1362,7 +1396,7 @@ struct Engine {
       const double rho_n = read_scal(3);
       const double b = rho_n / rho;
       rho = rho_n;
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, u, b, q);  // q = u + b q
+      dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, u, b, q); ::pf::g_launches++;  // q = u + b q
     }
     rep.rel_residual = est / t0;
   }
@@ -1441,16 +1475,16 @@ struct Engine {
       // initial multiplier: warm start (timeloop.hpp:168-169) / coarse lambda0
       if (nc > 0) {
         dev::k_rigid_dot<<<nfloat, 256, 0, st>>>(nfloat, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p, d_fxyoff.p, bvec.p,
-                                                 e_vec.p);
+                                                 e_vec.p); ::pf::g_launches++;
         if (D.cfg.warm) {
           PF_CUDA_CHECK(cudaMemcpyAsync(kr_tmp.p, lam.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
           project(kr_tmp.p);
         } else {
           kr_tmp.zero(st);
         }
-        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, e_vec.p, c_tmp2.p);
-        dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, lam.p, 1.0, 0.0);
-        dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_tmp.p, 1.0, lam.p);
+        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, e_vec.p, c_tmp2.p); ::pf::g_launches++;
+        dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, lam.p, 1.0, 0.0); ::pf::g_launches++;
+        dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_tmp.p, 1.0, lam.p); ::pf::g_launches++;
       } else if (!D.cfg.warm) {
         lam.zero(st);
       }
@@ -1465,9 +1499,9 @@ struct Engine {
       if (nc > 0) {
         // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
         F_(lam.p, kr_tmp.p);
-        dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, kr_rhs.p, 1.0, kr_tmp.p);
-        dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, kr_tmp.p, c_tmp1.p, 1.0, 0.0);
-        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, alpha_vec.p);
+        dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, kr_rhs.p, 1.0, kr_tmp.p); ::pf::g_launches++;
+        dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, kr_tmp.p, c_tmp1.p, 1.0, 0.0); ::pf::g_launches++;
+        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, alpha_vec.p); ::pf::g_launches++;
       }
       back_substitute(lam.p);
       cudaEventRecord(e3, st);
@@ -1613,7 +1647,7 @@ int pf_local_solve(pf_ctx* ctx, int s, double* x) {
     pf::DevBuf<double> tmp;
     tmp.upload(h);
     E.perm_in_K(tmp.p);
-    if (E.nfix) pf::dev::k_zero_idx<<<pf::cdiv(E.nfix, 128), 128, 0, E.st>>>(E.nfix, E.d_fixpos.p, E.Ksys.X.p);
+    if (E.nfix) pf::dev::k_zero_idx<<<pf::cdiv(E.nfix, 128), 128, 0, E.st>>>(E.nfix, E.d_fixpos.p, E.Ksys.X.p); ::pf::g_launches++;
     E.Ksys.solve(E.st, 1);
     E.perm_out_K(tmp.p);
     PF_CUDA_CHECK(cudaMemcpyAsync(x, tmp.p + E.sub_vec[s], sizeof(double) * T.dim, cudaMemcpyDeviceToHost, E.st));
@@ -1733,6 +1767,35 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
   });
 }
 
+/// K time steps on the device-resident state bracketed by CUDA events on the
+/// engine stream; reports summed (iterations, F-applies) and total ms.
+int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total) {
+  if (!ctx || nsteps < 1) return PF_INVALID;
+  return guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a), cudaEventCreate(&b);
+    PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
+    cudaEventRecord(a, E.st);
+    int it = 0, fa = 0;
+    for (int k = 0; k < nsteps; ++k) {
+      pf_report r{};
+      E.step(r);
+      it += r.iterations, fa += r.f_applies;
+    }
+    cudaEventRecord(b, E.st);
+    PF_CUDA_CHECK(cudaEventSynchronize(b));
+    float t;
+    cudaEventElapsedTime(&t, a, b);
+    cudaEventDestroy(a), cudaEventDestroy(b);
+    if (ms_total) *ms_total = t;
+    if (iters_total) *iters_total = it;
+    if (fapplies_total) *fapplies_total = fa;
+  });
+}
+
+long long pf_launch_count(void) { return pf::g_launches.load(); }
+
 int pf_kernel_stats(pf_ctx* ctx, double* sweep_ms, int* launches) {
   if (!ctx) return PF_INVALID;
   if (sweep_ms) *sweep_ms = ctx->eng.last_sweep_ms;
@@ -1798,6 +1861,39 @@ int pf_debug_disc(const pf_config* cfg, long long* sizes, int s, int* nG, int* G
       if (dof_ic)
         for (int i = 0; i < T.dim; ++i) dof_ic[2 * i] = T.dof_ic[i][0], dof_ic[2 * i + 1] = T.dof_ic[i][1];
     }
+  });
+}
+
+/// Per-kernel split of the factor sweeps, averaged over `iters` solves:
+/// out[0..2] = K system (leaf fwd, top, leaf bwd); out[3..5] interior system;
+/// out[6..8] mortar Gram system; out[9] whole preconditioner apply.
+int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
+  if (!ctx || !out || iters < 1) return PF_INVALID;
+  return guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    pf::SolveSystem* sys[3] = {&E.Ksys, E.use_dir ? &E.Isys : nullptr, E.use_q ? &E.Qsys : nullptr};
+    for (int k = 0; k < 3; ++k) {
+      for (int i = 0; i < 3; ++i) out[3 * k + i] = 0.0;
+      if (!sys[k] || !sys[k]->L.p) continue;
+      sys[k]->timed = true;
+      for (double& v : sys[k]->phase_ms) v = 0.0;
+      for (int it = 0; it < iters; ++it) sys[k]->solve(E.st, 1);
+      sys[k]->timed = false;
+      for (int i = 0; i < 3; ++i) out[3 * k + i] = sys[k]->phase_ms[i] / iters;
+    }
+    pf::DevBuf<double> dx, dy;
+    dx.alloc(E.D.n_lambda), dy.alloc(E.D.n_lambda);
+    dx.zero(E.st);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a), cudaEventCreate(&b);
+    cudaEventRecord(a, E.st);
+    for (int it = 0; it < iters; ++it) E.precond(dx.p, dy.p);
+    cudaEventRecord(b, E.st);
+    PF_CUDA_CHECK(cudaEventSynchronize(b));
+    float t;
+    cudaEventElapsedTime(&t, a, b);
+    out[9] = t / iters;
+    cudaEventDestroy(a), cudaEventDestroy(b);
   });
 }
 

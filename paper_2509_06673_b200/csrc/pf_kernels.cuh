@@ -19,9 +19,10 @@ constexpr int kWarp = 32;
 // Batched supernodal solve data (concatenated over symbolic types)
 // ---------------------------------------------------------------------------
 struct TypeDesc {
-  int n, nsn, ntask, top_sn0, top_c0;
-  int sn_base, task_base, fold_base;  // into sn_* / task_* / fold_ptr arrays
-  long long row_base, cb_base;        // into rows(slot) / cb_rows + fold_idx
+  int n, nsn, ntask;
+  int sn_base, task_base;            // into sn_* / task_* arrays
+  long long row_base, cb_base;       // into slot / cb_rows
+  long long fold_base, foldidx_base; // into fold_ptr (n+1 per type) / fold_idx
 };
 
 struct SolveSet {
@@ -31,13 +32,13 @@ struct SolveSet {
   const int* slot;
   const int *task_sn0, *task_sn1, *task_c0, *task_c1, *task_cboff, *task_cblen;
   const int* cb_rows;                      // relative to type cb_base
-  const int* fold_ptr;                     // per type: n_top+1 entries (relative), at fold_base
-  const int* fold_idx;                     // cb slot indices (relative to the problem's cb region)
+  const int* fold_ptr;                     // per type: n+1 entries at fold_base (relative to foldidx_base)
+  const int* fold_idx;                     // cb indices (relative to the problem's cb region)
   // problems
   int nprob;
   const int* prob_type;
   const long long *prob_lval, *prob_x, *prob_cb;
-  // leaf work list
+  // work list of one level: (problem, type-relative task)
   int nwork;
   const int *work_prob, *work_task;
   // data
@@ -59,14 +60,123 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// Panel primitives.  A supernode (nc columns, m rows, packed strict-lower
+// trapezoid, column-major) is processed in panels of up to 32 columns:
+//   forward : 32x32 unit-lower triangle by one warp with shuffles, then the
+//             rows below the panel updated with coalesced column reads;
+//   backward: rows below the panel reduced into 32 partial sums (warp
+//             transpose-reduction, 31 shuffles), then the transposed triangle.
+// All loads of a panel's off-diagonal block are independent of x, so they
+// are issued back to back (memory-level parallelism), and there is no
+// per-column barrier.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double Lval(const double* V, int m, int i, int j) {  // L(i, j), i > j
+  return V[col_off(j, m) + (i - j - 1)];
+}
+
+/// lane l ends with sum over lanes of acc[l] (acc fully unrolled in registers)
+__device__ __forceinline__ double transpose_reduce32(double (&acc)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      const double send = upper ? acc[k] : acc[k + off];
+      const double keep = upper ? acc[k + off] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return acc[0];
+}
+
+/// Warp forward elimination of one supernode on workspace ws (slots sl).
+__device__ __forceinline__ void warp_fwd_sn(const double* __restrict__ V, const int* __restrict__ sl, int nc, int m,
+                                            double* ws, double* xp, int lane) {
+  for (int p0 = 0; p0 < nc; p0 += 32) {
+    const int pw = min(32, nc - p0);
+    // panel triangle: lane i owns x_{p0+i}
+    double xi = lane < pw ? ws[sl[p0 + lane]] : 0.0;
+    double lrow[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) lrow[j] = (j < pw && lane > j && lane < pw) ? Lval(V, m, p0 + lane, p0 + j) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double xj = __shfl_sync(0xffffffffu, xi, j);
+      xi -= lrow[j] * xj;
+    }
+    if (lane < pw) ws[sl[p0 + lane]] = xi;
+    xp[lane] = xi;
+    __syncwarp();
+    // rows below the panel
+    for (int r = p0 + pw + lane; r < m; r += 32) {
+      double acc = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < pw; ++j) acc += Lval(V, m, r, p0 + j) * xp[j];
+      ws[sl[r]] -= acc;
+    }
+    __syncwarp();
+  }
+}
+
+/// lanes l and l^16 end with the sum over all lanes of acc[l & 15]
+__device__ __forceinline__ double transpose_reduce16(double (&acc)[16], int lane) {
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      const double send = upper ? acc[k] : acc[k + off];
+      const double keep = upper ? acc[k + off] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
+}
+
+constexpr int kBw = 16;  // backward panel width (register budget)
+
+/// Warp backward substitution of one supernode (ancestor rows final in ws).
+__device__ __forceinline__ void warp_bwd_sn(const double* __restrict__ V, const int* __restrict__ sl, int nc, int m,
+                                            double* ws, int lane) {
+  const int np = (nc + kBw - 1) / kBw;
+  for (int pi = np - 1; pi >= 0; --pi) {
+    const int p0 = pi * kBw, pw = min(kBw, nc - p0);
+    double acc[kBw];
+#pragma unroll
+    for (int j = 0; j < kBw; ++j) acc[j] = 0.0;
+    for (int r = p0 + pw + lane; r < m; r += 32) {
+      const double xr = ws[sl[r]];
+#pragma unroll
+      for (int j = 0; j < kBw; ++j)
+        if (j < pw) acc[j] += Lval(V, m, r, p0 + j) * xr;
+    }
+    const double t = transpose_reduce16(acc, lane);
+    double xi = lane < pw ? ws[sl[p0 + lane]] - t : 0.0;
+    // transposed triangle: x_i -= sum_{k>i in panel} L(k, i) x_k, k descending
+    double lcol[kBw];
+#pragma unroll
+    for (int k = 0; k < kBw; ++k) lcol[k] = (k < pw && k > lane) ? Lval(V, m, p0 + k, p0 + lane) : 0.0;
+#pragma unroll
+    for (int k = kBw - 1; k >= 0; --k) {
+      const double xk = __shfl_sync(0xffffffffu, xi, k);
+      xi -= lcol[k] * xk;
+    }
+    if (lane < pw) ws[sl[p0 + lane]] = xi;
+    __syncwarp();
+  }
+}
+
 /// Leaf forward sweep + diagonal scaling: one warp per (problem, task).
 /// Workspace per warp in shared memory: task columns then contribution rows.
-__global__ void k_leaf_fwd(SolveSet S, int ws_max) {
+__global__ void __launch_bounds__(128, 4) k_leaf_fwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
   if (w >= S.nwork) return;
-  double* ws = smem + (size_t)wib * ws_max;
+  double* xp = smem + (size_t)wib * (ws_max + 32);
+  double* ws = xp + 32;
   const int p = S.work_prob[w];
   const TypeDesc T = S.types[S.prob_type[p]];
   const int t = T.task_base + S.work_task[w];
@@ -80,15 +190,8 @@ __global__ void k_leaf_fwd(SolveSet S, int ws_max) {
     __syncwarp();
     for (int k = S.task_sn0[t]; k < S.task_sn1[t]; ++k) {
       const int sk = T.sn_base + k;
-      const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
-      const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
-      const double* V = L + S.sn_valoff[sk];
-      for (int j = 0; j < nc; ++j) {
-        const double xj = ws[sl[j]];
-        const double* col = V + col_off(j, m) - (j + 1);
-        for (int i = j + 1 + lane; i < m; i += kWarp) ws[sl[i]] -= col[i] * xj;
-        __syncwarp();
-      }
+      warp_fwd_sn(L + S.sn_valoff[sk], S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, xp,
+                  lane);
     }
     const double* Dp = S.D + S.prob_x[p];
     for (int i = lane; i < nc_task; i += kWarp) X[c0 + i] = ws[i] / Dp[c0 + i];
@@ -109,69 +212,143 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-/// Top part: fold contributions, forward, diagonal, backward. One CTA per problem.
-__global__ void k_top(SolveSet S, int in_smem) {
-  extern __shared__ double smem[];
-  __shared__ double red[32];
-  const int p = blockIdx.x;
-  if (p >= S.nprob) return;
+constexpr int kTopThreads = 256;
+
+/// CTA task workspace: task columns (smem or in place in X) and the task's
+/// contribution rows (smem or in place in its CB region).
+struct CtaWs {
+  double* col;
+  double* cb;
+  int nct;
+  __device__ __forceinline__ double& operator[](int s) const { return s < nct ? col[s] : cb[s - nct]; }
+};
+
+/// mode 0: forward (fold, eliminate, scale, emit contributions)
+/// mode 1: root (fold, forward, scale, backward)
+/// mode 2: backward (ancestors final in X)
+__device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem, double* smem, double (*red)[32],
+                         double* xp) {
   const TypeDesc T = S.types[S.prob_type[p]];
-  const int ntop = T.n - T.top_c0;
-  if (ntop == 0) return;
+  const int t = T.task_base + tt;
+  const int c0 = S.task_c0[t], c1 = S.task_c1[t], nct = c1 - c0;
+  const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const double* L = S.L + S.prob_lval[p];
-  const double* Dp = S.D + S.prob_x[p] + T.top_c0;
   const int* fp = S.fold_ptr + T.fold_base;
+  const int* fi = S.fold_idx + T.foldidx_base;
+  const int* cbr = S.cb_rows + T.cb_base + cbo;
   for (int r = 0; r < S.nrhs; ++r) {
-    double* X = S.X + S.prob_x[p] + r * S.x_stride + T.top_c0;
-    double* ws = in_smem ? smem : X;  // large top parts work in place in global memory (L2)
-    const double* CB = S.CB + S.prob_cb[p] + r * S.cb_stride;
-    for (int i = threadIdx.x; i < ntop; i += blockDim.x) {
-      double v = X[i];
-      for (int q = fp[i]; q < fp[i + 1]; ++q) v += CB[S.fold_idx[T.cb_base + q]];
-      ws[i] = v;
+    double* X = S.X + S.prob_x[p] + r * S.x_stride;
+    double* CBp = S.CB + S.prob_cb[p] + r * S.cb_stride;
+    CtaWs ws{in_smem ? smem : X + c0, in_smem ? smem + nct : CBp + cbo, nct};
+    if (mode != 2) {
+      for (int i = threadIdx.x; i < nct; i += blockDim.x) {
+        double v = X[c0 + i];
+        for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];
+        ws.col[i] = v;
+      }
+      for (int i = threadIdx.x; i < cbl; i += blockDim.x) ws.cb[i] = 0.0;
+    } else {
+      if (in_smem)
+        for (int i = threadIdx.x; i < nct; i += blockDim.x) ws.col[i] = X[c0 + i];
+      for (int i = threadIdx.x; i < cbl; i += blockDim.x) ws.cb[i] = X[cbr[i]];
     }
     __syncthreads();
-    for (int k = T.top_sn0; k < T.nsn; ++k) {
-      const int sk = T.sn_base + k;
-      const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
-      const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
-      const double* V = L + S.sn_valoff[sk];
-      for (int j = 0; j < nc; ++j) {
-        const double xj = ws[sl[j]];
-        const double* col = V + col_off(j, m) - (j + 1);
-        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) ws[sl[i]] -= col[i] * xj;
-        __syncthreads();
+    if (mode != 2) {
+      for (int k = S.task_sn0[t]; k < S.task_sn1[t]; ++k) {
+        const int sk = T.sn_base + k;
+        const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
+        const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
+        const double* V = L + S.sn_valoff[sk];
+        for (int p0 = 0; p0 < nc; p0 += 32) {
+          const int pw = min(32, nc - p0);
+          if (wid == 0) {
+            double xi = lane < pw ? ws[sl[p0 + lane]] : 0.0;
+            double lrow[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              lrow[j] = (j < pw && lane > j && lane < pw) ? Lval(V, m, p0 + lane, p0 + j) : 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xi -= lrow[j] * __shfl_sync(0xffffffffu, xi, j);
+            if (lane < pw) ws[sl[p0 + lane]] = xi;
+            xp[lane] = xi;
+          }
+          __syncthreads();
+          for (int rr = p0 + pw + threadIdx.x; rr < m; rr += blockDim.x) {
+            double acc = 0.0;
+#pragma unroll 8
+            for (int j = 0; j < pw; ++j) acc += Lval(V, m, rr, p0 + j) * xp[j];
+            ws[sl[rr]] -= acc;
+          }
+          __syncthreads();
+        }
+      }
+      const double* Dp = S.D + S.prob_x[p] + c0;
+      for (int i = threadIdx.x; i < nct; i += blockDim.x) ws.col[i] /= Dp[i];
+      __syncthreads();
+    }
+    if (mode != 0) {
+      for (int k = S.task_sn1[t] - 1; k >= S.task_sn0[t]; --k) {
+        const int sk = T.sn_base + k;
+        const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
+        const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
+        const double* V = L + S.sn_valoff[sk];
+        const int np = (nc + kBw - 1) / kBw;
+        for (int pi = np - 1; pi >= 0; --pi) {
+          const int p0 = pi * kBw, pw = min(kBw, nc - p0);
+          double acc[kBw];
+#pragma unroll
+          for (int j = 0; j < kBw; ++j) acc[j] = 0.0;
+          for (int rr = p0 + pw + threadIdx.x; rr < m; rr += blockDim.x) {
+            const double xr = ws[sl[rr]];
+#pragma unroll
+            for (int j = 0; j < kBw; ++j)
+              if (j < pw) acc[j] += Lval(V, m, rr, p0 + j) * xr;
+          }
+          const double tw = transpose_reduce16(acc, lane);
+          if (lane < 16) red[wid][lane] = tw;
+          __syncthreads();
+          if (wid == 0) {
+            double tsum = 0.0;
+            for (int w2 = 0; w2 < nwarp; ++w2) tsum += red[w2][lane & 15];  // fixed order
+            double xi = lane < pw ? ws[sl[p0 + lane]] - tsum : 0.0;
+            double lcol[kBw];
+#pragma unroll
+            for (int kk = 0; kk < kBw; ++kk) lcol[kk] = (kk < pw && kk > lane) ? Lval(V, m, p0 + kk, p0 + lane) : 0.0;
+#pragma unroll
+            for (int kk = kBw - 1; kk >= 0; --kk) xi -= lcol[kk] * __shfl_sync(0xffffffffu, xi, kk);
+            if (lane < pw) ws[sl[p0 + lane]] = xi;
+          }
+          __syncthreads();
+        }
       }
     }
-    for (int i = threadIdx.x; i < ntop; i += blockDim.x) ws[i] /= Dp[i];
-    __syncthreads();
-    for (int k = T.nsn - 1; k >= T.top_sn0; --k) {
-      const int sk = T.sn_base + k;
-      const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
-      const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
-      const double* V = L + S.sn_valoff[sk];
-      for (int j = nc - 1; j >= 0; --j) {
-        const double* col = V + col_off(j, m) - (j + 1);
-        double acc = 0.0;
-        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) acc += col[i] * ws[sl[i]];
-        const double s = block_sum(acc, red);
-        if (threadIdx.x == 0) ws[sl[j]] -= s;
-        __syncthreads();
-      }
+    if (in_smem) {
+      for (int i = threadIdx.x; i < nct; i += blockDim.x) X[c0 + i] = ws.col[i];
+      if (mode == 0)
+        for (int i = threadIdx.x; i < cbl; i += blockDim.x) CBp[cbo + i] = ws.cb[i];
     }
-    if (in_smem)
-      for (int i = threadIdx.x; i < ntop; i += blockDim.x) X[i] = ws[i];
     __syncthreads();
   }
 }
 
+/// One CTA per (problem, task) of a level; mode as in cta_task.
+__global__ void __launch_bounds__(kTopThreads) k_cta_level(SolveSet S, int mode, int in_smem) {
+  extern __shared__ double smem[];
+  __shared__ double xp[32];
+  __shared__ double red[kTopThreads / 32][32];
+  const int w = blockIdx.x;
+  if (w >= S.nwork) return;
+  cta_task(S, S.work_prob[w], S.work_task[w], mode, in_smem, smem, red, xp);
+}
+
 /// Leaf backward sweep: one warp per (problem, task); ancestors read from X.
-__global__ void k_leaf_bwd(SolveSet S, int ws_max) {
+__global__ void __launch_bounds__(128, 4) k_leaf_bwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
   if (w >= S.nwork) return;
-  double* ws = smem + (size_t)wib * ws_max;
+  double* ws = smem + (size_t)wib * (ws_max + 32) + 32;
   const int p = S.work_prob[w];
   const TypeDesc T = S.types[S.prob_type[p]];
   const int t = T.task_base + S.work_task[w];
@@ -186,17 +363,7 @@ __global__ void k_leaf_bwd(SolveSet S, int ws_max) {
     __syncwarp();
     for (int k = S.task_sn1[t] - 1; k >= S.task_sn0[t]; --k) {
       const int sk = T.sn_base + k;
-      const int nc = S.sn_ncol[sk], m = S.sn_nrow[sk];
-      const int* sl = S.slot + T.row_base + S.sn_rowoff[sk];
-      const double* V = L + S.sn_valoff[sk];
-      for (int j = nc - 1; j >= 0; --j) {
-        const double* col = V + col_off(j, m) - (j + 1);
-        double acc = 0.0;
-        for (int i = j + 1 + lane; i < m; i += kWarp) acc += col[i] * ws[sl[i]];
-        acc = warp_sum(acc);
-        if (lane == 0) ws[sl[j]] -= acc;
-        __syncwarp();
-      }
+      warp_bwd_sn(L + S.sn_valoff[sk], S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, lane);
     }
     for (int i = lane; i < nc_task; i += kWarp) X[c0 + i] = ws[i];
     __syncwarp();

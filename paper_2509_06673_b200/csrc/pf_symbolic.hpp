@@ -28,11 +28,15 @@ struct SymFactor {
   std::vector<int> rows;   // row positions per supernode (first ncol = own columns)
   std::vector<int> slot;   // parallel to rows: slot in the task (or top) workspace
   long long nval = 0;
-  int ntask = 0;
-  std::vector<int> task_sn0, task_sn1, task_c0, task_c1, task_cboff, task_cblen;
-  std::vector<int> cb_rows;  // positions (all >= top_c0)
-  int top_sn0 = 0, top_c0 = 0;
-  int max_task_ws = 0;       // max (c1-c0)+cblen over tasks
+  int ntask = 0;             // all tasks, ordered by level
+  std::vector<int> task_sn0, task_sn1, task_c0, task_c1, task_cboff, task_cblen, task_level;
+  std::vector<int> level_ptr;  // tasks of level l: [level_ptr[l], level_ptr[l+1])
+  int nlevel = 0;              // level 0: warp tasks; 1..nlevel-2: CTA tasks; nlevel-1: root tasks
+  std::vector<int> cb_rows;    // positions (ancestor rows of each task)
+  std::vector<int> fold_ptr, fold_idx;  // per column: contributions (CB indices) from lower-level tasks
+  int top_sn0 = 0, top_c0 = 0; // first supernode / column of the root level
+  int max_task_ws = 0;         // max (c1-c0)+cblen over level-0 tasks
+  std::vector<int> level_ws;   // max (c1-c0)+cblen per level
   long long flops_factor = 0;
 };
 
@@ -168,49 +172,85 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
         if (r >= c1 && mark[r] != s) mark[r] = s, R.push_back(r);
     std::sort(R.begin() + (c1 - c0), R.end());
   }
-  // ---- task selection on the supernodal tree ----
-  std::vector<long long> w(ns), W(ns);
+  // ---- multi-level task selection on the supernodal tree ----
+  std::vector<long long> w(ns);
   for (int s = 0; s < ns; ++s) {
     const long long nc = s0[s + 1] - s0[s], m = (long long)st[s].size();
     w[s] = nc * m - nc * (nc + 1) / 2 + nc;
   }
-  std::vector<long long> Cc(ns);
-  for (int s = 0; s < ns; ++s) W[s] = w[s], Cc[s] = s0[s + 1] - s0[s];
-  for (int s = 0; s < ns; ++s)
-    if (sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];  // children precede parents
-  std::vector<int> task_root;
-  std::vector<char> is_top(ns, 0);
-  std::function<void(int)> pick = [&](int s) {
-    const long long ws = Cc[s] + (long long)st[s].size() - (s0[s + 1] - s0[s]);
-    if (task_cap > 0 && W[s] <= task_cap && ws <= ws_cap) {
-      task_root.push_back(s);
-      return;
+  long long wtot = 0;
+  for (long long x : w) wtot += x;
+  std::vector<char> removed(ns, 0);
+  std::vector<std::vector<int>> level_roots;
+  const int kMaxLevels = 8;
+  for (int lvl = 0; lvl < kMaxLevels; ++lvl) {
+    // remaining-forest subtree weights / column counts
+    std::vector<long long> W(ns, 0), Cc(ns, 0);
+    long long wrem = 0;
+    for (int s = 0; s < ns; ++s)
+      if (!removed[s]) W[s] += w[s], Cc[s] += s0[s + 1] - s0[s], wrem += w[s];
+    if (wrem == 0) break;
+    for (int s = 0; s < ns; ++s)
+      if (!removed[s] && sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];
+    std::vector<int> roots;
+    for (int s = 0; s < ns; ++s)
+      if (!removed[s] && sparent[s] < 0) roots.push_back(s);
+    const long long cap = lvl == 0 ? task_cap : task_cap << (3 * lvl);
+    const long long wscap = lvl == 0 ? ws_cap : 24000;
+    const bool last = task_cap <= 0 || lvl == kMaxLevels - 1 || wrem <= 2 * cap;
+    std::vector<int> picked;
+    if (last) {
+      picked = roots;
+    } else {
+      std::function<void(int)> pick = [&](int s) {
+        const long long ws = Cc[s] + (long long)st[s].size() - (s0[s + 1] - s0[s]);
+        if (W[s] <= cap && ws <= wscap) {
+          picked.push_back(s);
+          return;
+        }
+        for (int ch : schild[s])
+          if (!removed[ch]) pick(ch);
+      };
+      for (int r : roots) pick(r);
     }
-    is_top[s] = 1;
-    for (int ch : schild[s]) pick(ch);
-  };
-  for (int s = 0; s < ns; ++s)
-    if (sparent[s] < 0) pick(s);
-  // order of supernodes: tasks (postorder subtrees, in original index order = postorder), then top
-  std::vector<int> owner(ns, -1);
-  std::sort(task_root.begin(), task_root.end());
-  std::vector<int> new_order;
+    std::function<void(int)> mark_rm = [&](int s) {
+      removed[s] = 1;
+      for (int ch : schild[s])
+        if (!removed[ch]) mark_rm(ch);
+    };
+    for (int r : picked) mark_rm(r);
+    std::sort(picked.begin(), picked.end());
+    level_roots.push_back(picked);
+    if (last) break;
+  }
+  F.nlevel = (int)level_roots.size();
+  // supernode order: tasks level by level, each task a postorder of its
+  // (remaining-forest) subtree
+  std::vector<int> owner(ns, -1), new_order;
   new_order.reserve(ns);
-  F.ntask = (int)task_root.size();
+  std::vector<int> tsn0, tsn1, tlvl;
+  std::vector<char> placed(ns, 0);
   std::function<void(int, int)> collect = [&](int s, int t) {
-    for (int ch : schild[s]) collect(ch, t);
+    for (int ch : schild[s])
+      if (!placed[ch] && owner[ch] < 0) collect(ch, t);
     owner[s] = t;
+    placed[s] = 1;
     new_order.push_back(s);
   };
-  std::vector<int> tsn0(F.ntask), tsn1(F.ntask);
-  for (int t = 0; t < F.ntask; ++t) {
-    tsn0[t] = (int)new_order.size();
-    collect(task_root[t], t);
-    tsn1[t] = (int)new_order.size();
+  F.level_ptr.push_back(0);
+  for (int lvl = 0; lvl < F.nlevel; ++lvl) {
+    for (int r : level_roots[lvl]) {
+      const int t = (int)tsn0.size();
+      tsn0.push_back((int)new_order.size());
+      collect(r, t);
+      tsn1.push_back((int)new_order.size());
+      tlvl.push_back(lvl);
+    }
+    F.level_ptr.push_back((int)tsn0.size());
   }
-  F.top_sn0 = (int)new_order.size();
-  for (int s = 0; s < ns; ++s)
-    if (is_top[s]) new_order.push_back(s);  // increasing index is topological
+  if ((int)new_order.size() != ns) fail(kInternal, "symbolic: task selection did not cover the tree");
+  F.ntask = (int)tsn0.size();
+  F.top_sn0 = F.nlevel > 0 ? tsn0[F.level_ptr[F.nlevel - 1]] : 0;
   // relabel columns
   std::vector<int> newpos(n);
   {
@@ -245,12 +285,15 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     F.flops_factor += (long long)nc * m * m;
   }
   F.nval = F.sn_valoff[ns];
-  // task column ranges, contribution rows and slots
+  // task column ranges, contribution rows, slots and fold lists
   F.slot.assign(F.rows.size(), -1);
   F.top_c0 = F.top_sn0 < ns ? F.sn_col0[F.top_sn0] : n;
+  F.level_ws.assign(F.nlevel, 0);
+  std::vector<std::vector<int>> fold(n);
   for (int t = 0; t < F.ntask; ++t) {
     F.task_sn0.push_back(tsn0[t]);
     F.task_sn1.push_back(tsn1[t]);
+    F.task_level.push_back(tlvl[t]);
     const int c0 = F.sn_col0[tsn0[t]];
     const int c1 = F.sn_col0[tsn1[t] - 1] + F.sn_ncol[tsn1[t] - 1];
     F.task_c0.push_back(c0);
@@ -263,8 +306,11 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     cb.erase(std::unique(cb.begin(), cb.end()), cb.end());
     F.task_cboff.push_back((int)F.cb_rows.size());
     F.task_cblen.push_back((int)cb.size());
+    for (std::size_t i = 0; i < cb.size(); ++i) fold[cb[i]].push_back(F.task_cboff[t] + (int)i);
     F.cb_rows.insert(F.cb_rows.end(), cb.begin(), cb.end());
-    F.max_task_ws = std::max(F.max_task_ws, (c1 - c0) + (int)cb.size());
+    const int ws = (c1 - c0) + (int)cb.size();
+    F.level_ws[tlvl[t]] = std::max(F.level_ws[tlvl[t]], ws);
+    if (tlvl[t] == 0) F.max_task_ws = std::max(F.max_task_ws, ws);
     for (int k = tsn0[t]; k < tsn1[t]; ++k)
       for (long long q = F.sn_rowoff[k]; q < F.sn_rowoff[k + 1]; ++q) {
         const int r = F.rows[q];
@@ -276,13 +322,19 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
         }
       }
   }
-  for (int k = F.top_sn0; k < ns; ++k)
-    for (long long q = F.sn_rowoff[k]; q < F.sn_rowoff[k + 1]; ++q) {
-      if (F.rows[q] < F.top_c0) fail(kInternal, "symbolic: top row below top range");
-      F.slot[q] = F.rows[q] - F.top_c0;
-    }
-  for (int v : F.cb_rows)
-    if (v < F.top_c0) fail(kInternal, "symbolic: contribution row outside the top part");
+  // every contribution row must belong to a task of a strictly higher level
+  std::vector<int> col_level(n, -1);
+  for (int t = 0; t < F.ntask; ++t)
+    for (int c = F.task_c0[t]; c < F.task_c1[t]; ++c) col_level[c] = F.task_level[t];
+  for (int t = 0; t < F.ntask; ++t)
+    for (int i = 0; i < F.task_cblen[t]; ++i)
+      if (col_level[F.cb_rows[F.task_cboff[t] + i]] <= F.task_level[t])
+        fail(kInternal, "symbolic: contribution row not owned by a higher level");
+  F.fold_ptr.assign(n + 1, 0);
+  for (int c = 0; c < n; ++c) {
+    F.fold_idx.insert(F.fold_idx.end(), fold[c].begin(), fold[c].end());
+    F.fold_ptr[c + 1] = (int)F.fold_idx.size();
+  }
   return F;
 }
 
@@ -417,16 +469,20 @@ inline void solve_host(const SymFactor& F, const std::vector<double>& L, const s
   for (int p = 0; p < F.n; ++p) x_natural[F.perm[p]] = x[p];
 }
 
-/// Host emulation of the device task schedule (k_leaf_fwd / k_top /
-/// k_leaf_bwd, identical slot and fold semantics) for the CPU validation of
+/// Host emulation of the device task schedule (warp/CTA tasks level by level,
+/// identical slot / contribution / fold semantics) for the CPU validation of
 /// the symbolic layout.  x in position order, solved in place.
 inline void solve_tasks_host(const SymFactor& F, const std::vector<double>& L, const std::vector<double>& D,
                              std::vector<double>& x) {
   std::vector<double> CB(F.cb_rows.size(), 0.0);
-  for (int t = 0; t < F.ntask; ++t) {
+  auto fwd_task = [&](int t, bool also_bwd) {
     const int c0 = F.task_c0[t], c1 = F.task_c1[t], nct = c1 - c0, cbl = F.task_cblen[t];
     std::vector<double> ws(nct + cbl, 0.0);
-    for (int i = 0; i < nct; ++i) ws[i] = x[c0 + i];
+    for (int i = 0; i < nct; ++i) {
+      double v = x[c0 + i];
+      for (int q = F.fold_ptr[c0 + i]; q < F.fold_ptr[c0 + i + 1]; ++q) v += CB[F.fold_idx[q]];
+      ws[i] = v;
+    }
     for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
       const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
       const int* sl = &F.slot[F.sn_rowoff[k]];
@@ -436,41 +492,23 @@ inline void solve_tasks_host(const SymFactor& F, const std::vector<double>& L, c
         for (int i = j + 1; i < m; ++i) ws[sl[i]] -= (*V++) * xj;
       }
     }
-    for (int i = 0; i < nct; ++i) x[c0 + i] = ws[i] / D[c0 + i];
+    for (int i = 0; i < nct; ++i) ws[i] /= D[c0 + i];
     for (int i = 0; i < cbl; ++i) CB[F.task_cboff[t] + i] = ws[nct + i];
-  }
-  const int ntop = F.n - F.top_c0;
-  std::vector<double> ws(ntop);
-  std::vector<std::vector<int>> lists(ntop);
-  for (int t = 0; t < F.ntask; ++t)
-    for (int i = 0; i < F.task_cblen[t]; ++i) lists[F.cb_rows[F.task_cboff[t] + i] - F.top_c0].push_back(F.task_cboff[t] + i);
-  for (int i = 0; i < ntop; ++i) {
-    double v = x[F.top_c0 + i];
-    for (int q : lists[i]) v += CB[q];
-    ws[i] = v;
-  }
-  for (int k = F.top_sn0; k < F.nsn; ++k) {
-    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
-    const int* sl = &F.slot[F.sn_rowoff[k]];
-    const double* V = &L[F.sn_valoff[k]];
-    for (int j = 0; j < nc; ++j) {
-      const double xj = ws[sl[j]];
-      for (int i = j + 1; i < m; ++i) ws[sl[i]] -= (*V++) * xj;
+    if (also_bwd) {
+      for (int k = F.task_sn1[t] - 1; k >= F.task_sn0[t]; --k) {
+        const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
+        const int* sl = &F.slot[F.sn_rowoff[k]];
+        for (int j = nc - 1; j >= 0; --j) {
+          const long long o = F.sn_valoff[k] + (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
+          double s = 0;
+          for (int i = j + 1; i < m; ++i) s += L[o + (i - j - 1)] * ws[sl[i]];
+          ws[sl[j]] -= s;
+        }
+      }
     }
-  }
-  for (int i = 0; i < ntop; ++i) ws[i] /= D[F.top_c0 + i];
-  for (int k = F.nsn - 1; k >= F.top_sn0; --k) {
-    const int m = F.sn_nrow[k], nc = F.sn_ncol[k];
-    const int* sl = &F.slot[F.sn_rowoff[k]];
-    for (int j = nc - 1; j >= 0; --j) {
-      const long long o = F.sn_valoff[k] + (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
-      double s = 0;
-      for (int i = j + 1; i < m; ++i) s += L[o + (i - j - 1)] * ws[sl[i]];
-      ws[sl[j]] -= s;
-    }
-  }
-  for (int i = 0; i < ntop; ++i) x[F.top_c0 + i] = ws[i];
-  for (int t = 0; t < F.ntask; ++t) {
+    for (int i = 0; i < nct; ++i) x[c0 + i] = ws[i];
+  };
+  auto bwd_task = [&](int t) {
     const int c0 = F.task_c0[t], c1 = F.task_c1[t], nct = c1 - c0, cbl = F.task_cblen[t];
     std::vector<double> w2(nct + cbl);
     for (int i = 0; i < nct; ++i) w2[i] = x[c0 + i];
@@ -486,7 +524,11 @@ inline void solve_tasks_host(const SymFactor& F, const std::vector<double>& L, c
       }
     }
     for (int i = 0; i < nct; ++i) x[c0 + i] = w2[i];
-  }
+  };
+  for (int l = 0; l < F.nlevel; ++l)
+    for (int t = F.level_ptr[l]; t < F.level_ptr[l + 1]; ++t) fwd_task(t, l == F.nlevel - 1);
+  for (int l = F.nlevel - 2; l >= 0; --l)
+    for (int t = F.level_ptr[l]; t < F.level_ptr[l + 1]; ++t) bwd_task(t);
 }
 
 }  // namespace pf

@@ -243,3 +243,148 @@ class Oracle:
                 f["p"] = x[S["off_p"]:S["off_p"] + S["n_s"]]
             out.append(f)
         return out
+
+
+# ---------------------------------------------------------------------------
+# element / mesh level entry points (re-expression of the reference's own
+# known-answer tests, tests/test_elements.cpp and tests/test_mesh.cpp)
+# ---------------------------------------------------------------------------
+def _kat_lib():
+    L = lib()
+    if getattr(L, "_kat_ready", False):
+        return L
+    vp = C.c_void_p
+    L.or_triangle_rule.argtypes = [C.c_int, vp, vp, C.POINTER(C.c_int)]
+    L.or_edge_rule.argtypes = [C.c_int, vp, vp, C.POINTER(C.c_int)]
+    L.or_eval_basis.argtypes = [C.c_int, C.c_double, C.c_double, vp, vp]
+    L.or_local_elastic.argtypes = [vp, C.c_double, C.c_int, vp]
+    L.or_local_div.argtypes = [vp, C.c_int, vp]
+    L.or_local_mass.argtypes = [vp, vp]
+    L.or_local_diffusion.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double, vp]
+    L.or_local_interface.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, vp]
+    L.or_mesh_build.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
+    L.or_mesh_free.argtypes = [vp]
+    L.or_mesh_counts.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.or_mesh_vertices.argtypes = [vp, vp]
+    L.or_mesh_triangles.argtypes = [vp, vp, vp]
+    L.or_mesh_tag.argtypes = [vp, C.c_int, C.c_double]
+    L.or_mesh_boundary.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.or_dofmap.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp]
+    L.or_pair.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int), vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L._kat_ready = True
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def triangle_rule(degree):
+    pts, w, n = np.zeros(12), np.zeros(6), C.c_int()
+    check(_kat_lib().or_triangle_rule(degree, _p(pts), _p(w), C.byref(n)))
+    return pts[:2 * n.value].reshape(-1, 2), w[:n.value]
+
+
+def edge_rule(degree):
+    pts, w, n = np.zeros(3), np.zeros(3), C.c_int()
+    check(_kat_lib().or_edge_rule(degree, _p(pts), _p(w), C.byref(n)))
+    return pts[:n.value], w[:n.value]
+
+
+def eval_basis(order, x, y):
+    v, g = np.zeros(6), np.zeros(12)
+    check(_kat_lib().or_eval_basis(order, x, y, _p(v), _p(g)))
+    nb = 3 if order == 1 else 6
+    return v[:nb], g[:2 * nb].reshape(-1, 2)
+
+
+def _tri(tri):
+    return np.ascontiguousarray(np.asarray(tri, np.float64).reshape(6))
+
+
+def local_elastic(tri, mu, order):
+    nb = 3 if order == 1 else 6
+    out = np.zeros((2 * nb, 2 * nb))
+    check(_kat_lib().or_local_elastic(_p(_tri(tri)), mu, order, _p(out)))
+    return out
+
+
+def local_div(tri, order):
+    nb = 3 if order == 1 else 6
+    out = np.zeros((3, 2 * nb))
+    check(_kat_lib().or_local_div(_p(_tri(tri)), order, _p(out)))
+    return out
+
+
+def local_mass(tri):
+    out = np.zeros((3, 3))
+    check(_kat_lib().or_local_mass(_p(_tri(tri)), _p(out)))
+    return out
+
+
+def local_diffusion(tri, K, mu_f):
+    out = np.zeros((3, 3))
+    check(_kat_lib().or_local_diffusion(_p(_tri(tri)), K[0][0], K[0][1], K[1][1], mu_f, _p(out)))
+    return out
+
+
+def local_interface(a, b, trace_order):
+    out = np.zeros((2, trace_order + 1))
+    check(_kat_lib().or_local_interface(a[0], a[1], b[0], b[1], trace_order, _p(out)))
+    return out
+
+
+class Mesh:
+    """oracle Mesh (mesh.hpp restatement): region 0 = P, 1 = E."""
+
+    def __init__(self, region, rect, nx, ny):
+        h = C.c_void_p()
+        r = np.asarray(rect, np.float64)
+        check(_kat_lib().or_mesh_build(region, _p(r), nx, ny, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            _kat_lib().or_mesh_free(self.h)
+        except Exception:
+            pass
+
+    def counts(self):
+        nv, nt, ne = C.c_int(), C.c_int(), C.c_int()
+        _kat_lib().or_mesh_counts(self.h, C.byref(nv), C.byref(nt), C.byref(ne))
+        return nv.value, nt.value, ne.value
+
+    def vertices(self):
+        nv = self.counts()[0]
+        xy = np.zeros(2 * nv)
+        _kat_lib().or_mesh_vertices(self.h, _p(xy))
+        return xy.reshape(-1, 2)
+
+    def triangles(self):
+        nt = self.counts()[1]
+        t, a = np.zeros(3 * nt, np.int32), np.zeros(nt)
+        _kat_lib().or_mesh_triangles(self.h, _p(t), _p(a))
+        return t.reshape(-1, 3), a
+
+    def tag(self, rule, param=0.5):
+        check(_kat_lib().or_mesh_tag(self.h, rule, param))
+
+    def boundary(self):
+        n = 4 * sum(self.counts())
+        e, m, pt, i = (np.zeros(n, np.int32) for _ in range(4))
+        mid = np.zeros(2 * n)
+        k = _kat_lib().or_mesh_boundary(self.h, _p(e), _p(m), _p(pt), _p(i), _p(mid))
+        return e[:k], m[:k], pt[:k], i[:k].astype(bool), mid[:2 * k].reshape(-1, 2)
+
+    def dofmap(self, kind, order):
+        nn, nd = C.c_int(), C.c_int()
+        on = np.zeros(sum(self.counts()) + 8, np.int8)
+        check(_kat_lib().or_dofmap(self.h, kind, order, C.byref(nn), C.byref(nd), _p(on)))
+        return nn.value, nd.value, on[:nn.value].astype(bool)
+
+
+def pair(ma, mb, order):
+    npairs, nmult, ned = C.c_int(), C.c_int(), C.c_int()
+    pairs = np.zeros(2 * (sum(ma.counts()) + 8), np.int32)
+    check(_kat_lib().or_pair(ma.h, mb.h, order, C.byref(npairs), _p(pairs), C.byref(nmult), C.byref(ned)))
+    return pairs[:2 * npairs.value].reshape(-1, 2), nmult.value, ned.value
