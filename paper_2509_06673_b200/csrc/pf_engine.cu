@@ -150,7 +150,7 @@ struct SolveSystem {
       type_perm_off.push_back((long long)perm.size());
       perm.insert(perm.end(), F.perm.begin(), F.perm.end());
     }
-    ws_max = nlevel > 1 ? level_ws[0] : 0;
+    ws_max = nlevel > 1 ? ((level_ws[0] + 1) & ~1) : 0;  // even: 16-byte aligned stage buffers
     const int np = (int)ptype.size();
     prob_x.resize(np), prob_lval.resize(np), prob_cb.resize(np);
     std::vector<std::vector<int>> wp(nlevel), wt(nlevel);
@@ -218,7 +218,7 @@ struct SolveSystem {
     if (level_nwork[l] == 0) return;
     dev::SolveSet S = set(nrhs, l);
     if (l == 0 && nlevel > 1) {
-      const std::size_t sm = sizeof(double) * (std::size_t)(ws_max + 32) * kWpb;
+      const std::size_t sm = sizeof(double) * (std::size_t)(ws_max + 32 + 2 * (dev::kStage + 2)) * kWpb;
       if (mode == 0)
         dev::k_leaf_fwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);
       else
@@ -258,7 +258,7 @@ struct SolveSystem {
   }
 
   void prepare_smem() {
-    const std::size_t sm_leaf = sizeof(double) * (std::size_t)(ws_max + 32) * kWpb;
+    const std::size_t sm_leaf = sizeof(double) * (std::size_t)(ws_max + 32 + 2 * (dev::kStage + 2)) * kWpb;
     if (sm_leaf > 227 * 1024)
       fail(kInternal, "leaf solve workspace exceeds shared memory (" + std::to_string(sm_leaf) + " B)");
     // the attribute is per kernel (shared by all systems): raise it to the opt-in maximum once

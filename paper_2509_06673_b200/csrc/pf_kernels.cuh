@@ -168,31 +168,90 @@ __device__ __forceinline__ void warp_bwd_sn(const double* __restrict__ V, const 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Async staging of a warp task's packed factor values (cp.async, 16-byte
+// pieces, double-buffered chunks of whole supernodes).
+// ---------------------------------------------------------------------------
+constexpr int kStage = 1024;  // doubles per stage buffer (+2 alignment slack)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+/// Forward chunk: supernodes [k, ke) with values <= kStage (or one oversized supernode).
+__device__ __forceinline__ int chunk_fwd_end(const SolveSet& S, const TypeDesc& T, int k, int kend) {
+  const long long v0 = S.sn_valoff[T.sn_base + k];
+  int e = k + 1;
+  while (e < kend && S.sn_valoff[T.sn_base + e + 1] - v0 <= kStage) ++e;
+  return e;
+}
+/// Backward chunk: supernodes [kb, k) ending at k.
+__device__ __forceinline__ int chunk_bwd_begin(const SolveSet& S, const TypeDesc& T, int k, int kbeg) {
+  const long long v1 = S.sn_valoff[T.sn_base + k];
+  int b = k - 1;
+  while (b > kbeg && v1 - S.sn_valoff[T.sn_base + b - 1] <= kStage) --b;
+  return b;
+}
+
+/// Issue the copy of values [v0, v1) (doubles, relative to L) into buf; returns
+/// the offset (0/1 double) of v0 inside buf, or -1 when the range is oversized.
+__device__ __forceinline__ int stage_issue(const double* L, long long v0, long long v1, double* buf, int lane) {
+  if (v1 - v0 > kStage) return -1;
+  const double* g = L + v0;
+  const int shift = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+  const double* ga = g - shift;
+  const int n16 = (int)((v1 - v0 + shift + 1) >> 1);
+  for (int i = lane; i < n16; i += 32) cp_async16(buf + 2 * i, ga + 2 * i);
+  return shift;
+}
+
 /// Leaf forward sweep + diagonal scaling: one warp per (problem, task).
-/// Workspace per warp in shared memory: task columns then contribution rows.
+/// Shared memory per warp: [xp 32][workspace ws_max][2 stage buffers].
 __global__ void __launch_bounds__(128, 4) k_leaf_fwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
   if (w >= S.nwork) return;
-  double* xp = smem + (size_t)wib * (ws_max + 32);
+  double* xp = smem + (size_t)wib * (ws_max + 32 + 2 * (kStage + 2));
   double* ws = xp + 32;
+  double* stg[2] = {ws + ws_max, ws + ws_max + kStage + 2};
   const int p = S.work_prob[w];
   const TypeDesc T = S.types[S.prob_type[p]];
   const int t = T.task_base + S.work_task[w];
   const int c0 = S.task_c0[t], c1 = S.task_c1[t], nc_task = c1 - c0;
   const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
+  const int sn0 = S.task_sn0[t], sn1 = S.task_sn1[t];
   const double* L = S.L + S.prob_lval[p];
   for (int r = 0; r < S.nrhs; ++r) {
     double* X = S.X + S.prob_x[p] + r * S.x_stride;
+    int kc = sn0, kn = chunk_fwd_end(S, T, kc, sn1), buf = 0;
+    int sh = stage_issue(L, S.sn_valoff[T.sn_base + kc], S.sn_valoff[T.sn_base + kn], stg[0], lane);
+    cp_async_commit();
     for (int i = lane; i < nc_task; i += kWarp) ws[i] = X[c0 + i];
     for (int i = lane; i < cbl; i += kWarp) ws[nc_task + i] = 0.0;
-    __syncwarp();
-    for (int k = S.task_sn0[t]; k < S.task_sn1[t]; ++k) {
-      const int sk = T.sn_base + k;
-      warp_fwd_sn(L + S.sn_valoff[sk], S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, xp,
-                  lane);
+    while (kc < sn1) {
+      const int kn2 = kn < sn1 ? chunk_fwd_end(S, T, kn, sn1) : kn;
+      int sh2 = 0;
+      if (kn < sn1) sh2 = stage_issue(L, S.sn_valoff[T.sn_base + kn], S.sn_valoff[T.sn_base + kn2], stg[buf ^ 1], lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const long long vb = S.sn_valoff[T.sn_base + kc];
+      for (int k = kc; k < kn; ++k) {
+        const int sk = T.sn_base + k;
+        const double* V = sh >= 0 ? stg[buf] + sh + (S.sn_valoff[sk] - vb) : L + S.sn_valoff[sk];
+        warp_fwd_sn(V, S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, xp, lane);
+      }
+      __syncwarp();
+      kc = kn, kn = kn2, sh = sh2, buf ^= 1;
     }
+    cp_async_wait<0>();
     const double* Dp = S.D + S.prob_x[p];
     for (int i = lane; i < nc_task; i += kWarp) X[c0 + i] = ws[i] / Dp[c0 + i];
     double* CB = S.CB + S.prob_cb[p] + r * S.cb_stride + cbo;
@@ -342,29 +401,48 @@ __global__ void __launch_bounds__(kTopThreads) k_cta_level(SolveSet S, int mode,
   cta_task(S, S.work_prob[w], S.work_task[w], mode, in_smem, smem, red, xp);
 }
 
-/// Leaf backward sweep: one warp per (problem, task); ancestors read from X.
+/// Leaf backward sweep: one warp per (problem, task); ancestors read from X;
+/// factor values staged backwards in chunks.
 __global__ void __launch_bounds__(128, 4) k_leaf_bwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
   if (w >= S.nwork) return;
-  double* ws = smem + (size_t)wib * (ws_max + 32) + 32;
+  double* ws = smem + (size_t)wib * (ws_max + 32 + 2 * (kStage + 2)) + 32;
+  double* stg[2] = {ws + ws_max, ws + ws_max + kStage + 2};
   const int p = S.work_prob[w];
   const TypeDesc T = S.types[S.prob_type[p]];
   const int t = T.task_base + S.work_task[w];
   const int c0 = S.task_c0[t], c1 = S.task_c1[t], nc_task = c1 - c0;
   const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
+  const int sn0 = S.task_sn0[t], sn1 = S.task_sn1[t];
   const int* cbr = S.cb_rows + T.cb_base + cbo;
   const double* L = S.L + S.prob_lval[p];
   for (int r = 0; r < S.nrhs; ++r) {
     double* X = S.X + S.prob_x[p] + r * S.x_stride;
+    // chunk [kb, ke) processed in descending supernode order
+    int ke = sn1, kb = chunk_bwd_begin(S, T, ke, sn0), buf = 0;
+    int sh = stage_issue(L, S.sn_valoff[T.sn_base + kb], S.sn_valoff[T.sn_base + ke], stg[0], lane);
+    cp_async_commit();
     for (int i = lane; i < nc_task; i += kWarp) ws[i] = X[c0 + i];
     for (int i = lane; i < cbl; i += kWarp) ws[nc_task + i] = X[cbr[i]];
-    __syncwarp();
-    for (int k = S.task_sn1[t] - 1; k >= S.task_sn0[t]; --k) {
-      const int sk = T.sn_base + k;
-      warp_bwd_sn(L + S.sn_valoff[sk], S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, lane);
+    while (ke > sn0) {
+      const int kb2 = kb > sn0 ? chunk_bwd_begin(S, T, kb, sn0) : kb;
+      int sh2 = 0;
+      if (kb > sn0) sh2 = stage_issue(L, S.sn_valoff[T.sn_base + kb2], S.sn_valoff[T.sn_base + kb], stg[buf ^ 1], lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const long long vb = S.sn_valoff[T.sn_base + kb];
+      for (int k = ke - 1; k >= kb; --k) {
+        const int sk = T.sn_base + k;
+        const double* V = sh >= 0 ? stg[buf] + sh + (S.sn_valoff[sk] - vb) : L + S.sn_valoff[sk];
+        warp_bwd_sn(V, S.slot + T.row_base + S.sn_rowoff[sk], S.sn_ncol[sk], S.sn_nrow[sk], ws, lane);
+      }
+      __syncwarp();
+      ke = kb, kb = kb2, sh = sh2, buf ^= 1;
     }
+    cp_async_wait<0>();
     for (int i = lane; i < nc_task; i += kWarp) X[c0 + i] = ws[i];
     __syncwarp();
   }

@@ -88,7 +88,7 @@ inline void nd_rec(std::vector<int>& ids, const std::vector<std::array<int, 2>>&
 /// Build the symbolic factor of symmetric pattern A (natural order).
 /// task_cap: maximum packed-value weight of one leaf task (0 = no tasks).
 inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic, long long task_cap,
-                         int ws_cap = 1536, int leaf = 48) {
+                         int ws_cap = 640, int leaf = 48) {
   SymFactor F;
   const int n = A.nr;
   F.n = n;
