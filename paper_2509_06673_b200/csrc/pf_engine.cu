@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <chrono>
 #include <cstdio>
 #include <memory>
@@ -188,6 +189,20 @@ struct SolveSystem {
     D.alloc(total_x);
     X.alloc(total_x * nrhs);
     CB.alloc(std::max<long long>(1, total_cb * nrhs));
+  }
+
+  long long xidx(int p, int pos) const { return prob_x[p] + pos; }
+
+  /// factorise every problem on the host (threads) and upload its factor;
+  /// fn(p, L, D) produces problem p's factor.
+  template <class Fn>
+  void factor_upload(int threads, Fn&& fn) {
+    parallel_for((int)prob_type.size(), threads, [&](int p) {
+      std::vector<double> l, d;
+      fn(p, l, d);
+      PF_CUDA_CHECK(cudaMemcpy(L.p + prob_lval[p], l.data(), sizeof(double) * l.size(), cudaMemcpyHostToDevice));
+      PF_CUDA_CHECK(cudaMemcpy(D.p + prob_x[p], d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice));
+    });
   }
 
   dev::SolveSet set(int nrhs, int level) {
@@ -550,8 +565,7 @@ struct Engine {
     itype_pos.resize(nt);
     parallel_for(nt, nthreads, [&](int t) {
       const SubType& T = D.types[t];
-      const long long cap = std::max<long long>(4096, (long long)T.K.nnz() / 4);
-      ksym[t] = analyse(T.K, T.dof_ic, cap);
+      ksym[t] = analyse(T.K, T.dof_ic, task_cap(T.K.nnz()), task_ws());
       if (use_dir) {
         std::vector<char> isB(T.dim, 0);
         for (int b : T.Bset) isB[b] = 1;
@@ -568,7 +582,7 @@ struct Engine {
             if (pos[T.K.col[q]] >= 0) rc.emplace_back(pos[i], pos[T.K.col[q]]);
         }
         const Csr KII = pattern_from_pairs((int)idx.size(), (int)idx.size(), rc);
-        isym[t] = analyse(KII, ic, std::max<long long>(4096, (long long)KII.nnz() / 4));
+        isym[t] = analyse(KII, ic, task_cap(KII.nnz()), task_ws());
       }
     });
     const auto t1 = std::chrono::steady_clock::now();
@@ -596,6 +610,17 @@ struct Engine {
 
   ~Engine() {
     if (st) cudaStreamDestroy(st);
+  }
+
+  /// level-0 (warp) task caps of the sweep schedule; PF_TASK_CAP / PF_TASK_WS override
+  static long long task_cap(long long nnzA) {
+    if (const char* v = std::getenv("PF_TASK_CAP")) return std::atoll(v);
+    (void)nnzA;
+    return 16384;
+  }
+  static int task_ws() {
+    if (const char* v = std::getenv("PF_TASK_WS")) return std::atoi(v);
+    return 256;
   }
 
   // ------------------------------------------------------------------
@@ -707,71 +732,59 @@ struct Engine {
     std::vector<int> ptype(ns);
     for (int s = 0; s < ns; ++s) ptype[s] = D.subs[s].type;
     Ksys.build(kt, ptype, 1);
-    if (use_dir) Isys.build(it, ptype, 2);
+    if (use_dir) Isys.build(it, ptype, 1);
     std::vector<double> hK(total_kv);
     PF_CUDA_CHECK(cudaMemcpy(hK.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
     h_K = std::move(hK);
-    parallel_for(ns, nthreads, [&](int s) {
+    Ksys.factor_upload(nthreads, [&](int s, std::vector<double>& L, std::vector<double>& Dg) {
       const Subdomain& S = D.subs[s];
       const SubType& T = D.types[S.type];
       const double* kv = h_K.data() + h_fsubs[s].kval;
       std::vector<int> fixed;
       if (T.floating) fixed.assign(T.fix.begin(), T.fix.end());
-      std::vector<double> L, Dg;
       factor_host(ksym[S.type], T.K, kv, fixed, L, Dg);
-      // seeded residual check on the (regularised) matrix
-      {
-        std::mt19937 rng(20240901u);
-        std::uniform_real_distribution<double> U(-1.0, 1.0);
-        std::vector<double> b(T.dim), x;
-        for (auto& v : b) v = U(rng);
-        x = b;
-        solve_host(ksym[S.type], L, Dg, x.data());
-        std::vector<char> isfix(T.dim, 0);
-        for (int f : fixed) isfix[f] = 1;
-        double rn = 0, bn = 0;
-        for (int i = 0; i < T.dim; ++i) {
-          double r = -b[i];
-          if (isfix[i]) {
-            r += x[i];
-          } else {
-            for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-              if (!isfix[T.K.col[q]]) r += kv[q] * x[T.K.col[q]];
-          }
-          rn += r * r, bn += b[i] * b[i];
+      // seeded residual check on the (regularised) matrix (feti.hpp:28-36)
+      std::mt19937 rng(20240901u);
+      std::uniform_real_distribution<double> U(-1.0, 1.0);
+      std::vector<double> b(T.dim), x;
+      for (auto& v : b) v = U(rng);
+      x = b;
+      solve_host(ksym[S.type], L, Dg, x.data());
+      std::vector<char> isfix(T.dim, 0);
+      for (int f : fixed) isfix[f] = 1;
+      double rn = 0, bn = 0;
+      for (int i = 0; i < T.dim; ++i) {
+        double r = -b[i];
+        if (isfix[i]) {
+          r += x[i];
+        } else {
+          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
+            if (!isfix[T.K.col[q]]) r += kv[q] * x[T.K.col[q]];
         }
-        const double res = std::sqrt(rn / bn);
-        if (!(res < 1e-8))
-          fail(kSingular, "subdomain " + std::to_string(s) + " factorization residual " + std::to_string(res) +
-                              " (check boundary constraints)");
+        rn += r * r, bn += b[i] * b[i];
       }
-      PF_CUDA_CHECK(cudaMemcpy(Ksys.L.p + Ksys.prob_lval[s], L.data(), sizeof(double) * L.size(),
-                               cudaMemcpyHostToDevice));
-      PF_CUDA_CHECK(cudaMemcpy(Ksys.D.p + Ksys.prob_x[s], Dg.data(), sizeof(double) * Dg.size(),
-                               cudaMemcpyHostToDevice));
-      if (use_dir) {
+      const double res = std::sqrt(rn / bn);
+      if (!(res < 1e-8))
+        fail(kSingular, "subdomain " + std::to_string(s) + " factorization residual " + std::to_string(res) +
+                            " (check boundary constraints)");
+    });
+    if (use_dir)
+      Isys.factor_upload(nthreads, [&](int s, std::vector<double>& LI, std::vector<double>& DI) {
+        const Subdomain& S = D.subs[s];
+        const SubType& T = D.types[S.type];
+        const double* kv = h_K.data() + h_fsubs[s].kval;
         const auto& idx = itype_index[S.type];
         const auto& pos = itype_pos[S.type];
-        // K_II values in the interior pattern order
-        Csr KII;
-        {
-          std::vector<std::pair<int, int>> rc;
-          for (int i : idx)
-            for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-              if (pos[T.K.col[q]] >= 0) rc.emplace_back(pos[i], pos[T.K.col[q]]);
-          KII = pattern_from_pairs((int)idx.size(), (int)idx.size(), rc);
-          for (int i : idx)
-            for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-              if (pos[T.K.col[q]] >= 0) KII.val[KII.find(pos[i], pos[T.K.col[q]])] = kv[q];
-        }
-        std::vector<double> LI, DI;
+        std::vector<std::pair<int, int>> rc;
+        for (int i : idx)
+          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
+            if (pos[T.K.col[q]] >= 0) rc.emplace_back(pos[i], pos[T.K.col[q]]);
+        Csr KII = pattern_from_pairs((int)idx.size(), (int)idx.size(), rc);
+        for (int i : idx)
+          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
+            if (pos[T.K.col[q]] >= 0) KII.val[KII.find(pos[i], pos[T.K.col[q]])] = kv[q];
         factor_host(isym[S.type], KII, KII.val.data(), {}, LI, DI);
-        PF_CUDA_CHECK(cudaMemcpy(Isys.L.p + Isys.prob_lval[s], LI.data(), sizeof(double) * LI.size(),
-                                 cudaMemcpyHostToDevice));
-        PF_CUDA_CHECK(cudaMemcpy(Isys.D.p + Isys.prob_x[s], DI.data(), sizeof(double) * DI.size(),
-                                 cudaMemcpyHostToDevice));
-      }
-    });
+      });
     Ksys.prepare_smem();
     if (use_dir) Isys.prepare_smem();
   }
@@ -789,12 +802,12 @@ struct Engine {
       const SymFactor& F = ksym[S.type];
       std::vector<char> isfix(T.dim, 0);
       if (T.floating)
-        for (int f : T.fix) isfix[f] = 1, fixpos.push_back(Ksys.prob_x[s] + F.iperm[f]);
+        for (int f : T.fix) isfix[f] = 1, fixpos.push_back(Ksys.xidx((int)s, F.iperm[f]));
       std::map<int, std::vector<std::pair<int, double>>> bycol;
       for (std::size_t q = 0; q < S.g_lam.size(); ++q) bycol[S.g_col[q]].emplace_back(S.g_lam[q], S.g_val[q]);
       for (auto& kv : bycol) {
         std::sort(kv.second.begin(), kv.second.end());
-        const long long row = Ksys.prob_x[s] + F.iperm[kv.first];
+        const long long row = Ksys.xidx((int)s, F.iperm[kv.first]);
         gb.rows.push_back(row);
         for (auto& e : kv.second) gb.idx.push_back(e.first), gb.val.push_back(e.second);
         gb.ptr.push_back((int)gb.idx.size());
@@ -818,7 +831,7 @@ struct Engine {
         const auto& Cc = constrained ? S.gc_col : S.g_col;
         const auto& V = constrained ? S.gc_val : S.g_val;
         for (std::size_t q = 0; q < L.size(); ++q) {
-          const long long c = constrained ? h_fsubs[s].gval + Cc[q] : Ksys.prob_x[s] + ksym[S.type].iperm[Cc[q]];
+          const long long c = constrained ? h_fsubs[s].gval + Cc[q] : Ksys.xidx((int)s, ksym[S.type].iperm[Cc[q]]);
           rows[L[q]].emplace_back((int)s, c, V[q]);
         }
       }
@@ -897,7 +910,7 @@ struct Engine {
       stype[s] = D.subs[s].type;
       skval[s] = h_fsubs[s].kval;
       swb[s] = total_B;
-      sxii[s] = Isys.prob_x[s];
+      sxii[s] = Isys.prob_x[s];  // (problem, 0); interior positions stride kW
       total_B += (long long)D.types[D.subs[s].type].Bset.size();
     }
     d_subtype.upload(stype), d_sub_kval.upload(skval), d_sub_wb.upload(swb), d_sub_xii.upload(sxii);
@@ -1127,7 +1140,10 @@ struct Engine {
     long long nnzG = 0;
     for (auto& S : D.subs) nnzG += (long long)S.g_lam.size();
     info.bytes_fapply = 2.0 * 8.0 * Ksys.nnzL + 8.0 * total_vec + 2.0 * 12.0 * nnzG + 2.0 * 8.0 * D.n_lambda;
-    info.bytes_precond = use_dir ? 2.0 * 2.0 * 8.0 * Isys.nnzL + 2.0 * 8.0 * Isys.total_x : 0.0;
+    long long idim = 0;
+    if (use_dir)
+      for (auto& S : D.subs) idim += isym[S.type].n;
+    info.bytes_precond = use_dir ? 2.0 * 8.0 * Isys.nnzL + 8.0 * idim : 0.0;
   }
 
   // ------------------------------------------------------------------
@@ -1159,10 +1175,10 @@ struct Engine {
   void qsolve(const double* x, double* y) {
     const int n = D.n_lambda;
     dev::k_perm_in<<<dim3(cdiv(n, 256), 1), 256, 0, st>>>(1, Qsys.d_prob_x.p, zero_off(), Qsys.d_prob_n.p,
-                                                         Qsys.d_prob_perm.p, Qsys.d_perm.p, x, Qsys.X.p, nullptr, 0); ::pf::g_launches++;
+                                                         Qsys.d_prob_perm.p, Qsys.d_perm.p, x, Qsys.X.p, 1); ::pf::g_launches++;
     Qsys.solve(st, 1);
     dev::k_perm_out<<<dim3(cdiv(n, 256), 1), 256, 0, st>>>(1, Qsys.d_prob_x.p, zero_off(), Qsys.d_prob_n.p,
-                                                          Qsys.d_prob_perm.p, Qsys.d_perm.p, Qsys.X.p, y); ::pf::g_launches++;
+                                                          Qsys.d_prob_perm.p, Qsys.d_perm.p, Qsys.X.p, y, 1); ::pf::g_launches++;
   }
   DevBuf<long long> d_zero_off;
   const long long* zero_off() {
@@ -1246,15 +1262,14 @@ struct Engine {
     int maxn = 0;
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
-                                                            Ksys.d_prob_perm.p, Ksys.d_perm.p, src, Ksys.X.p, nullptr,
-                                                            0); ::pf::g_launches++;
+                                                            Ksys.d_prob_perm.p, Ksys.d_perm.p, src, Ksys.X.p, 1); ::pf::g_launches++;
   }
   void perm_out_K(double* dst) {
     const int np = (int)D.subs.size();
     int maxn = 0;
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_out<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
-                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, Ksys.X.p, dst); ::pf::g_launches++;
+                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, Ksys.X.p, dst, 1); ::pf::g_launches++;
   }
   DevBuf<long long> d_subvec_buf;
   const long long* d_subvec() {
@@ -1871,16 +1886,18 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
   if (!ctx || !out || iters < 1) return PF_INVALID;
   return guarded(ctx, [&] {
     auto& E = ctx->eng;
-    pf::SolveSystem* sys[3] = {&E.Ksys, E.use_dir ? &E.Isys : nullptr, E.use_q ? &E.Qsys : nullptr};
-    for (int k = 0; k < 3; ++k) {
-      for (int i = 0; i < 3; ++i) out[3 * k + i] = 0.0;
-      if (!sys[k] || !sys[k]->L.p) continue;
-      sys[k]->timed = true;
-      for (double& v : sys[k]->phase_ms) v = 0.0;
-      for (int it = 0; it < iters; ++it) sys[k]->solve(E.st, 1);
-      sys[k]->timed = false;
-      for (int i = 0; i < 3; ++i) out[3 * k + i] = sys[k]->phase_ms[i] / iters;
-    }
+    auto run = [&](auto* sys, double* o) {
+      for (int i = 0; i < 3; ++i) o[i] = 0.0;
+      if (!sys || !sys->L.p) return;
+      sys->timed = true;
+      for (double& v : sys->phase_ms) v = 0.0;
+      for (int it = 0; it < iters; ++it) sys->solve(E.st, 1);
+      sys->timed = false;
+      for (int i = 0; i < 3; ++i) o[i] = sys->phase_ms[i] / iters;
+    };
+    run(&E.Ksys, out);
+    run(E.use_dir ? &E.Isys : nullptr, out + 3);
+    run(E.use_q ? &E.Qsys : nullptr, out + 6);
     pf::DevBuf<double> dx, dy;
     dx.alloc(E.D.n_lambda), dy.alloc(E.D.n_lambda);
     dx.zero(E.st);

@@ -172,7 +172,7 @@ __device__ __forceinline__ void warp_bwd_sn(const double* __restrict__ V, const 
 // Async staging of a warp task's packed factor values (cp.async, 16-byte
 // pieces, double-buffered chunks of whole supernodes).
 // ---------------------------------------------------------------------------
-constexpr int kStage = 1024;  // doubles per stage buffer (+2 alignment slack)
+constexpr int kStage = 512;  // doubles per stage buffer (+2 alignment slack)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -286,7 +286,7 @@ struct CtaWs {
 /// mode 1: root (fold, forward, scale, backward)
 /// mode 2: backward (ancestors final in X)
 __device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem, double* smem, double (*red)[32],
-                         double* xp) {
+                         double* xp, long long* coff) {
   const TypeDesc T = S.types[S.prob_type[p]];
   const int t = T.task_base + tt;
   const int c0 = S.task_c0[t], c1 = S.task_c1[t], nct = c1 - c0;
@@ -326,17 +326,21 @@ __device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem
             double lrow[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              lrow[j] = (j < pw && lane > j && lane < pw) ? Lval(V, m, p0 + lane, p0 + j) : 0.0;
+              lrow[j] = (j < pw && lane > j && lane < pw) ? __ldg(V + col_off(p0 + j, m) + (p0 + lane - p0 - j - 1)) : 0.0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) xi -= lrow[j] * __shfl_sync(0xffffffffu, xi, j);
             if (lane < pw) ws[sl[p0 + lane]] = xi;
             xp[lane] = xi;
+            coff[lane] = lane < pw ? col_off(p0 + lane, m) - (p0 + lane) - 1 : 0;
           }
           __syncthreads();
           for (int rr = p0 + pw + threadIdx.x; rr < m; rr += blockDim.x) {
+            double v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = j < pw ? __ldg(V + coff[j] + rr) : 0.0;
             double acc = 0.0;
-#pragma unroll 8
-            for (int j = 0; j < pw; ++j) acc += Lval(V, m, rr, p0 + j) * xp[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += v[j] * xp[j];
             ws[sl[rr]] -= acc;
           }
           __syncthreads();
@@ -358,11 +362,14 @@ __device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem
           double acc[kBw];
 #pragma unroll
           for (int j = 0; j < kBw; ++j) acc[j] = 0.0;
+          long long cb[kBw];
+#pragma unroll
+          for (int j = 0; j < kBw; ++j) cb[j] = j < pw ? col_off(p0 + j, m) - (p0 + j) - 1 : 0;
           for (int rr = p0 + pw + threadIdx.x; rr < m; rr += blockDim.x) {
             const double xr = ws[sl[rr]];
 #pragma unroll
             for (int j = 0; j < kBw; ++j)
-              if (j < pw) acc[j] += Lval(V, m, rr, p0 + j) * xr;
+              if (j < pw) acc[j] += __ldg(V + cb[j] + rr) * xr;
           }
           const double tw = transpose_reduce16(acc, lane);
           if (lane < 16) red[wid][lane] = tw;
@@ -395,10 +402,11 @@ __device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem
 __global__ void __launch_bounds__(kTopThreads) k_cta_level(SolveSet S, int mode, int in_smem) {
   extern __shared__ double smem[];
   __shared__ double xp[32];
+  __shared__ long long coff[32];
   __shared__ double red[kTopThreads / 32][32];
   const int w = blockIdx.x;
   if (w >= S.nwork) return;
-  cta_task(S, S.work_prob[w], S.work_task[w], mode, in_smem, smem, red, xp);
+  cta_task(S, S.work_prob[w], S.work_task[w], mode, in_smem, smem, red, xp, coff);
 }
 
 /// Leaf backward sweep: one warp per (problem, task); ancestors read from X;
@@ -503,28 +511,28 @@ __global__ void k_spmv_ind(int nrows, const int* ptr, const long long* vpos, con
 
 /// permute in: X[xo + pos] = src[so + perm[pos]] (per problem, one block-stride loop)
 __global__ void k_perm_in(int nprob, const long long* prob_x, const long long* prob_src, const int* prob_n,
-                          const long long* prob_perm, const int* perm, const double* src, double* X,
-                          const double* bias, double bscale) {
+                          const long long* prob_perm, const int* perm, const double* src, double* X, int stride) {
   const int p = blockIdx.y;
   if (p >= nprob) return;
   const int n = prob_n[p];
   const int* pm = perm + prob_perm[p];
   const double* s = src + prob_src[p];
   double* x = X + prob_x[p];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = s[pm[i]];
-  (void)bias, (void)bscale;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[(long long)i * stride] = s[pm[i]];
 }
 
 /// permute out: dst[so + perm[pos]] = X[xo + pos]
 __global__ void k_perm_out(int nprob, const long long* prob_x, const long long* prob_dst, const int* prob_n,
-                           const long long* prob_perm, const int* perm, const double* X, double* dst) {
+                           const long long* prob_perm, const int* perm, const double* X, double* dst, int stride) {
   const int p = blockIdx.y;
   if (p >= nprob) return;
   const int n = prob_n[p];
   const int* pm = perm + prob_perm[p];
   double* d = dst + prob_dst[p];
   const double* x = X + prob_x[p];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[pm[i]] = x[i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    d[pm[i]] = x[(long long)i * stride];
 }
 
 __global__ void k_zero_idx(int n, const long long* idx, double* X) {

@@ -60,9 +60,26 @@ inline void nd_rec(std::vector<int>& ids, const std::vector<std::array<int, 2>>&
     v.reserve(ids.size());
     for (int d : ids) v.push_back(ic[d][ax]);
     std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
-    int c = v[v.size() / 2];
-    if (c % 2) c += (c + 1 < hi[ax]) ? 1 : -1;  // prefer vertex lines (even)
-    c = std::max(lo[ax] + 1, std::min(hi[ax] - 1, c));
+    const int med = v[v.size() / 2];
+    // among vertex lines (even) near the median, take the one crossing the
+    // fewest dofs (for the multiplier graph this avoids cutting along an
+    // interface line)
+    std::sort(v.begin(), v.end());
+    const int span = std::max(2, (hi[ax] - lo[ax]) / 8);
+    int c = INT32_MIN;
+    long long best = -1;
+    for (int cand = med - span; cand <= med + span; ++cand) {
+      if (cand % 2 || cand <= lo[ax] || cand >= hi[ax]) continue;
+      const long long cnt = std::upper_bound(v.begin(), v.end(), cand) - std::lower_bound(v.begin(), v.end(), cand);
+      const long long left = std::lower_bound(v.begin(), v.end(), cand) - v.begin();
+      const long long imb = std::llabs(2 * left + cnt - (long long)v.size());
+      const long long score = cnt * 4 * (long long)v.size() / std::max<long long>(1, hi[ax] - lo[ax]) + imb;
+      if (best < 0 || score < best) best = score, c = cand;
+    }
+    if (c == INT32_MIN) {
+      c = med + (med % 2 ? 1 : 0);
+      c = std::max(lo[ax] + 1, std::min(hi[ax] - 1, c));
+    }
     std::vector<int> L, R, S;
     for (int d : ids) (ic[d][ax] < c ? L : ic[d][ax] > c ? R : S).push_back(d);
     for (int d : R) side[d] = 1;
@@ -88,7 +105,7 @@ inline void nd_rec(std::vector<int>& ids, const std::vector<std::array<int, 2>>&
 /// Build the symbolic factor of symmetric pattern A (natural order).
 /// task_cap: maximum packed-value weight of one leaf task (0 = no tasks).
 inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic, long long task_cap,
-                         int ws_cap = 640, int leaf = 48) {
+                         int ws_cap = 640, double amalg_zero_frac = 0.15, int amalg_small = 16, int leaf = 48) {
   SymFactor F;
   const int n = A.nr;
   F.n = n;
@@ -147,7 +164,7 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     if (!join) s0.push_back(j);
     sn_of[j] = (int)s0.size() - 1;
   }
-  const int ns = (int)s0.size();
+  int ns = (int)s0.size();
   s0.push_back(n);
   // supernodal parent and structures
   std::vector<int> sparent(ns, -1);
@@ -172,6 +189,63 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
         if (r >= c1 && mark[r] != s) mark[r] = s, R.push_back(r);
     std::sort(R.begin() + (c1 - c0), R.end());
   }
+  // ---- relaxed amalgamation: absorb a child into its parent when the child's
+  // columns immediately precede the parent's and the merged block is small or
+  // adds few explicit zeros (fewer, wider supernodes for the device sweeps) ----
+  if (amalg_zero_frac > 0.0) {
+    std::vector<int> head(ns);  // first supernode index of the merged group ending at s
+    std::vector<long long> nv(ns);
+    auto val_count = [](long long n, long long m) { return n * m - n * (n + 1) / 2; };
+    std::vector<int> c0(ns), nrow(ns);  // current first column and row count of group ending at s
+    std::vector<long long> zeros(ns, 0);
+    for (int s = 0; s < ns; ++s) c0[s] = s0[s], nrow[s] = (int)st[s].size(), nv[s] = val_count(s0[s + 1] - s0[s], nrow[s]);
+    std::vector<char> absorbed(ns, 0);
+    for (int s = 0; s < ns; ++s) {
+      const int p = sparent[s];
+      if (p < 0 || s0[s + 1] != s0[p] || absorbed[s]) continue;
+      // merged group: columns [c0[s], s0[p+1]), rows = own columns + rows of p beyond its columns
+      const long long ncs = s0[s + 1] - c0[s], ncp = s0[p + 1] - s0[p];
+      const long long n = ncs + ncp, m = ncs + nrow[p];
+      const long long merged = val_count(n, m);
+      const long long z = merged - nv[s] - nv[p] + zeros[s] + zeros[p];
+      if (n <= amalg_small || (double)z <= amalg_zero_frac * (double)merged) {
+        if (n > 96) continue;
+        absorbed[s] = 1;
+        c0[p] = c0[s];
+        nrow[p] = (int)m;
+        nv[p] = merged;
+        zeros[p] = z;
+      }
+    }
+    // rebuild fundamental arrays with merged groups
+    std::vector<int> ns0, keep;
+    for (int s = 0; s < ns; ++s)
+      if (!absorbed[s]) keep.push_back(s), ns0.push_back(c0[s]);
+    const int nn = (int)keep.size();
+    ns0.push_back(n);
+    std::vector<int> nsn_of(n);
+    for (int k = 0; k < nn; ++k)
+      for (int c = ns0[k]; c < ns0[k + 1]; ++c) nsn_of[c] = k;
+    std::vector<int> nparent(nn, -1);
+    for (int k = 0; k < nn; ++k) {
+      const int last = ns0[k + 1] - 1;
+      if (parent[last] >= 0) nparent[k] = nsn_of[parent[last]];
+    }
+    std::vector<std::vector<int>> nst(nn), nchild(nn);
+    for (int k = 0; k < nn; ++k) {
+      const int s = keep[k];
+      std::vector<int>& R = nst[k];
+      for (int c = ns0[k]; c < ns0[k + 1]; ++c) R.push_back(c);
+      const int cend = ns0[k + 1];
+      for (int r : st[s])
+        if (r >= cend) R.push_back(r);
+    }
+    for (int k = 0; k < nn; ++k)
+      if (nparent[k] >= 0) nchild[nparent[k]].push_back(k);
+    s0.swap(ns0), sparent.swap(nparent), st.swap(nst), schild.swap(nchild);
+    sn_of.swap(nsn_of);
+    ns = nn;
+  }
   // ---- multi-level task selection on the supernodal tree ----
   std::vector<long long> w(ns);
   for (int s = 0; s < ns; ++s) {
@@ -181,47 +255,72 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
   long long wtot = 0;
   for (long long x : w) wtot += x;
   std::vector<char> removed(ns, 0);
-  std::vector<std::vector<int>> level_roots;
-  const int kMaxLevels = 8;
-  for (int lvl = 0; lvl < kMaxLevels; ++lvl) {
-    // remaining-forest subtree weights / column counts
+  // level 0: subtree roots (one warp per subtree); levels >= 1: chain tasks
+  // given by their bottom and top supernodes
+  std::vector<std::vector<int>> level_roots, level_tops;
+  bool leaf_level = false;
+  {
     std::vector<long long> W(ns, 0), Cc(ns, 0);
-    long long wrem = 0;
+    for (int s = 0; s < ns; ++s) W[s] += w[s], Cc[s] += s0[s + 1] - s0[s];
     for (int s = 0; s < ns; ++s)
-      if (!removed[s]) W[s] += w[s], Cc[s] += s0[s + 1] - s0[s], wrem += w[s];
-    if (wrem == 0) break;
-    for (int s = 0; s < ns; ++s)
-      if (!removed[s] && sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];
-    std::vector<int> roots;
-    for (int s = 0; s < ns; ++s)
-      if (!removed[s] && sparent[s] < 0) roots.push_back(s);
-    const long long cap = lvl == 0 ? task_cap : task_cap << (3 * lvl);
-    const long long wscap = lvl == 0 ? ws_cap : 24000;
-    const bool last = task_cap <= 0 || lvl == kMaxLevels - 1 || wrem <= 2 * cap;
+      if (sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];
     std::vector<int> picked;
-    if (last) {
-      picked = roots;
-    } else {
+    if (task_cap > 0) {
       std::function<void(int)> pick = [&](int s) {
         const long long ws = Cc[s] + (long long)st[s].size() - (s0[s + 1] - s0[s]);
-        if (W[s] <= cap && ws <= wscap) {
+        if (W[s] <= task_cap && ws <= ws_cap) {
           picked.push_back(s);
           return;
         }
-        for (int ch : schild[s])
-          if (!removed[ch]) pick(ch);
+        for (int ch : schild[s]) pick(ch);
       };
-      for (int r : roots) pick(r);
+      for (int s = 0; s < ns; ++s)
+        if (sparent[s] < 0) pick(s);
     }
     std::function<void(int)> mark_rm = [&](int s) {
       removed[s] = 1;
-      for (int ch : schild[s])
-        if (!removed[ch]) mark_rm(ch);
+      for (int ch : schild[s]) mark_rm(ch);
     };
     for (int r : picked) mark_rm(r);
     std::sort(picked.begin(), picked.end());
-    level_roots.push_back(picked);
-    if (last) break;
+    if (!picked.empty()) {
+      leaf_level = true;
+      level_roots.push_back(picked);
+      level_tops.push_back(picked);
+    }
+    // upper part: chains (a supernode with exactly one remaining child joins
+    // its child's task), levelled by height; tasks of one level are independent
+    std::vector<int> task_of(ns, -1), rem_child(ns, 0), tlevel, tbottom, ttop;
+    for (int s = 0; s < ns; ++s)
+      if (!removed[s] && sparent[s] >= 0) rem_child[sparent[s]]++;
+    for (int s = 0; s < ns; ++s) {
+      if (removed[s]) continue;
+      int only = -1;
+      if (rem_child[s] == 1)
+        for (int ch : schild[s])
+          if (!removed[ch]) only = ch;
+      if (only >= 0) {
+        task_of[s] = task_of[only];
+        ttop[task_of[s]] = s;
+      } else {
+        int lv = 0;
+        for (int ch : schild[s])
+          if (!removed[ch]) lv = std::max(lv, tlevel[task_of[ch]] + 1);
+        task_of[s] = (int)tlevel.size();
+        tlevel.push_back(lv);
+        tbottom.push_back(s);
+        ttop.push_back(s);
+      }
+    }
+    int maxlv = -1;
+    for (int lv : tlevel) maxlv = std::max(maxlv, lv);
+    for (int lv = 0; lv <= maxlv; ++lv) {
+      std::vector<int> bots, tops;
+      for (std::size_t t = 0; t < tlevel.size(); ++t)
+        if (tlevel[t] == lv) bots.push_back(tbottom[t]), tops.push_back(ttop[t]);
+      level_roots.push_back(bots);
+      level_tops.push_back(tops);
+    }
   }
   F.nlevel = (int)level_roots.size();
   // supernode order: tasks level by level, each task a postorder of its
@@ -239,10 +338,23 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
   };
   F.level_ptr.push_back(0);
   for (int lvl = 0; lvl < F.nlevel; ++lvl) {
-    for (int r : level_roots[lvl]) {
+    for (std::size_t q = 0; q < level_roots[lvl].size(); ++q) {
       const int t = (int)tsn0.size();
       tsn0.push_back((int)new_order.size());
-      collect(r, t);
+      if (lvl == 0 && leaf_level) {
+        collect(level_roots[lvl][q], t);
+      } else {
+        // chain bottom .. top (every parent on the way has this chain as its only remaining child)
+        int sN = level_roots[lvl][q];
+        const int top = level_tops[lvl][q];
+        while (true) {
+          owner[sN] = t;
+          placed[sN] = 1;
+          new_order.push_back(sN);
+          if (sN == top) break;
+          sN = sparent[sN];
+        }
+      }
       tsn1.push_back((int)new_order.size());
       tlvl.push_back(lvl);
     }
