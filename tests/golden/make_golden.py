@@ -37,7 +37,9 @@ def main():
             xs, lam = o.state(k)
             out[f"x{k}"] = np.concatenate(xs)
             out[f"lambda{k}"] = lam
-            out[f"iters{k}"] = o.report(k)["iterations"]
+            rep = o.report(k)
+            out[f"iters{k}"] = rep["iterations"]
+            out[f"hist{k}"] = rep["history"]
         rng = np.random.default_rng(20240901)
         x = rng.uniform(-1.0, 1.0, o.n_lambda)
         o0 = ol.Oracle(**kw)
