@@ -1,0 +1,154 @@
+// porofeti_b200.hpp — header-only C++ shim that re-creates the reference's
+// FETI entry points (/root/reference/proj/include/porofeti/feti.hpp and
+// timeloop.hpp) on top of the C ABI in porofeti_b200.h.  Eigen is not used:
+// vectors are std::vector<double>.  Errors are rethrown as the reference's
+// exception types (core.hpp:32-75).
+//
+//   reference                                   shim
+//   porofeti::build_discretization + StepSolver  porofeti_b200::Problem(cfg)
+//   FetiOperator::apply (feti.hpp:101)           Problem::apply
+//   FetiOperator::apply_preconditioner (:127)    Problem::apply_preconditioner
+//   FetiOperator::interface_rhs (:147)           Problem::interface_rhs
+//   SubdomainFactorization::solve (:38)          Problem::local_solve
+//   StepSolver::advance (timeloop.hpp:150)       StepSolver::advance
+//   run_simulation (timeloop.hpp:206)            run_simulation
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "porofeti_b200.h"
+
+namespace porofeti_b200 {
+
+using Vector = std::vector<double>;
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct SingularSubproblemError : Error {
+  using Error::Error;
+};
+struct PcgBreakdownError : Error {
+  using Error::Error;
+};
+struct SolverError : Error {
+  using Error::Error;
+};
+struct ConfigError : Error {
+  using Error::Error;
+};
+struct CudaError : Error {
+  using Error::Error;
+};
+
+inline void check(int code, const pf_ctx* ctx) {
+  if (code == PF_OK) return;
+  const std::string msg = pf_last_error(ctx);
+  switch (code) {
+    case PF_SINGULAR: throw SingularSubproblemError(msg);
+    case PF_BREAKDOWN: throw PcgBreakdownError(msg);
+    case PF_NOT_CONVERGED: throw SolverError(msg);
+    case PF_INVALID: throw ConfigError(msg);
+    case PF_CUDA: throw CudaError(msg);
+    default: throw Error(msg);
+  }
+}
+
+/// Reference PcgReport (feti.hpp:59-67).
+struct PcgReport {
+  int step = 0, iterations = 0;
+  bool converged = false;
+  double rel_residual = 0.0, seconds = 0.0;
+};
+
+/// Reference StateSnapshot (state.hpp:8-12): per-subdomain saddle vectors
+/// ([u, eta, xi, p] / [u, xi]) concatenated, plus the multiplier.
+struct StateSnapshot {
+  int step = 0;
+  Vector x;
+  Vector lambda;
+};
+
+inline pf_config default_config() {
+  pf_config c{};
+  c.mesh_n = 32, c.SX = 1, c.SY = 2, c.order = 1;
+  c.E = 1.0, c.nu = 0.3, c.alpha = 1.0, c.c0 = 1e-3, c.kperm = 1.0, c.mu_f = 1.0, c.dt = 1e-2;
+  c.steps = 5, c.mu_conv = 0, c.scenario = PF_SCEN_MMS_T, c.precond = PF_PREC_DIRICHLET;
+  c.krylov = PF_KRYLOV_AUTO, c.tol = 1e-10, c.max_iter = 500, c.warm = 1, c.threads = 0;
+  c.seed = 20240901ull, c.logk_mean = -2.0, c.logk_sd = 1.0;
+  return c;
+}
+
+/// Discretisation + FETI operator living on the device.
+class Problem {
+ public:
+  explicit Problem(const pf_config& cfg) { check(pf_create(&ctx_, &cfg), nullptr); refresh(); }
+  ~Problem() { pf_destroy(ctx_); }
+  Problem(const Problem&) = delete;
+  Problem& operator=(const Problem&) = delete;
+
+  int n_lambda() const { return info_.n_lambda; }
+  const pf_info& info() const { return info_; }
+  pf_ctx* handle() const { return ctx_; }
+
+  Vector apply(const Vector& x) const {
+    Vector y(info_.n_lambda);
+    check(pf_apply(ctx_, x.data(), y.data()), ctx_);
+    return y;
+  }
+  Vector apply_preconditioner(const Vector& r) const {
+    Vector z(info_.n_lambda);
+    check(pf_apply_precond(ctx_, r.data(), z.data()), ctx_);
+    return z;
+  }
+  Vector interface_rhs() const {
+    Vector F(info_.n_lambda);
+    check(pf_interface_rhs(ctx_, F.data()), ctx_);
+    return F;
+  }
+  Vector local_solve(int s, Vector b) const {
+    check(pf_local_solve(ctx_, s, b.data()), ctx_);
+    return b;
+  }
+
+ private:
+  void refresh() { check(pf_get_info(ctx_, &info_), ctx_); }
+  pf_ctx* ctx_ = nullptr;
+  pf_info info_{};
+};
+
+/// Reference StepSolver (timeloop.hpp:135-193).
+class StepSolver {
+ public:
+  explicit StepSolver(Problem& p) : p_(&p) {}
+  StateSnapshot advance(const StateSnapshot& prev, PcgReport* report = nullptr) const {
+    StateSnapshot next;
+    next.x.resize(p_->info().total_dim);
+    next.lambda.resize(p_->n_lambda());
+    pf_report r{};
+    check(pf_advance(p_->handle(), prev.x.data(), prev.lambda.data(), prev.step, next.x.data(), next.lambda.data(), &r),
+          p_->handle());
+    next.step = r.step;
+    if (report) *report = PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds};
+    return next;
+  }
+
+ private:
+  Problem* p_;
+};
+
+/// Reference run_simulation (timeloop.hpp:206-221) on the device-resident state.
+inline std::vector<PcgReport> run_simulation(Problem& p) {
+  std::vector<PcgReport> out;
+  for (int n = 0; n < p.info().N; ++n) {
+    pf_report r{};
+    check(pf_step(p.handle(), &r), p.handle());
+    out.push_back(PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds});
+  }
+  return out;
+}
+
+}  // namespace porofeti_b200
