@@ -151,7 +151,6 @@ struct SolveSystem {
       type_perm_off.push_back((long long)perm.size());
       perm.insert(perm.end(), F.perm.begin(), F.perm.end());
     }
-    ws_max = nlevel > 1 ? ((level_ws[0] + 1) & ~1) : 0;  // even: 16-byte aligned stage buffers
     const int np = (int)ptype.size();
     prob_x.resize(np), prob_lval.resize(np), prob_cb.resize(np);
     std::vector<std::vector<int>> wp(nlevel), wt(nlevel);
@@ -178,6 +177,11 @@ struct SolveSystem {
       d_wp[l].upload(wp[l]), d_wt[l].upload(wt[l]);
       level_nwork[l] = (int)wp[l].size();
     }
+    ws_max = 0;
+    for (int l = 0; l + 1 < nlevel; ++l)
+      if (warp_level(l)) ws_max = std::max(ws_max, level_ws[l]);
+    ws_max = (ws_max + 1) & ~1;  // even: 16-byte aligned stage buffers
+
     d_types.upload(td);
     d_sn_col0.upload(sn_col0), d_sn_ncol.upload(sn_ncol), d_sn_nrow.upload(sn_nrow);
     d_sn_rowoff.upload(sn_rowoff), d_sn_valoff.upload(sn_valoff), d_slot.upload(slot);
@@ -229,10 +233,17 @@ struct SolveSystem {
   bool timed = false;
   double phase_ms[3] = {0, 0, 0};  // warp levels / CTA levels + root / backward
 
+  static constexpr int kWarpWs = 256;  // levels whose tasks all fit run one warp per task
+  // one warp per task only when the level has enough tasks to fill the GPU
+  // with warps (>= one wave at ~16 warps/SM); otherwise a CTA per task splits rows
+  bool warp_level(int l) const {
+    return l < nlevel - 1 && level_ws[l] <= kWarpWs && (l == 0 || level_nwork[l] >= 148 * 16);
+  }
+
   void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
     if (level_nwork[l] == 0) return;
     dev::SolveSet S = set(nrhs, l);
-    if (l == 0 && nlevel > 1) {
+    if (warp_level(l)) {
       const std::size_t sm = sizeof(double) * (std::size_t)(ws_max + 32 + 2 * (dev::kStage + 2)) * kWpb;
       if (mode == 0)
         dev::k_leaf_fwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);

@@ -91,39 +91,11 @@ __device__ __forceinline__ double transpose_reduce32(double (&acc)[32], int lane
   return acc[0];
 }
 
-/// Warp forward elimination of one supernode on workspace ws (slots sl).
-__device__ __forceinline__ void warp_fwd_sn(const double* __restrict__ V, const int* __restrict__ sl, int nc, int m,
-                                            double* ws, double* xp, int lane) {
-  for (int p0 = 0; p0 < nc; p0 += 32) {
-    const int pw = min(32, nc - p0);
-    // panel triangle: lane i owns x_{p0+i}
-    double xi = lane < pw ? ws[sl[p0 + lane]] : 0.0;
-    double lrow[32];
+/// lanes l ends with the sum over all 32 lanes of acc[l % PW]
+template <int PW>
+__device__ __forceinline__ double transpose_reduce(double (&acc)[PW], int lane) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) lrow[j] = (j < pw && lane > j && lane < pw) ? Lval(V, m, p0 + lane, p0 + j) : 0.0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double xj = __shfl_sync(0xffffffffu, xi, j);
-      xi -= lrow[j] * xj;
-    }
-    if (lane < pw) ws[sl[p0 + lane]] = xi;
-    xp[lane] = xi;
-    __syncwarp();
-    // rows below the panel
-    for (int r = p0 + pw + lane; r < m; r += 32) {
-      double acc = 0.0;
-#pragma unroll 8
-      for (int j = 0; j < pw; ++j) acc += Lval(V, m, r, p0 + j) * xp[j];
-      ws[sl[r]] -= acc;
-    }
-    __syncwarp();
-  }
-}
-
-/// lanes l and l^16 end with the sum over all lanes of acc[l & 15]
-__device__ __forceinline__ double transpose_reduce16(double (&acc)[16], int lane) {
-#pragma unroll
-  for (int off = 8; off >= 1; off >>= 1) {
+  for (int off = PW / 2; off >= 1; off >>= 1) {
     const bool upper = (lane & off) != 0;
 #pragma unroll
     for (int k = 0; k < off; ++k) {
@@ -132,10 +104,80 @@ __device__ __forceinline__ double transpose_reduce16(double (&acc)[16], int lane
       acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
-  return acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
+  double v = acc[0];
+#pragma unroll
+  for (int off = PW; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
 }
 
-constexpr int kBw = 16;  // backward panel width (register budget)
+/// Forward elimination of one panel [p0, p0+pw) of a supernode (pw <= PW).
+template <int PW>
+__device__ __forceinline__ void warp_fwd_panel(const double* __restrict__ V, const int* __restrict__ sl, int m, int p0,
+                                               int pw, double* ws, double* xp, int lane) {
+  int cb[PW];  // offsets inside one supernode fit in 32 bits
+#pragma unroll
+  for (int j = 0; j < PW; ++j) cb[j] = j < pw ? (int)(col_off(p0 + j, m) - (p0 + j) - 1) : 0;
+  double xi = lane < pw ? ws[sl[p0 + lane]] : 0.0;
+  double lrow[PW];
+#pragma unroll
+  for (int j = 0; j < PW; ++j) lrow[j] = (j < pw && lane > j && lane < pw) ? V[cb[j] + p0 + lane] : 0.0;
+#pragma unroll
+  for (int j = 0; j < PW; ++j) xi -= lrow[j] * __shfl_sync(0xffffffffu, xi, j);
+  if (lane < pw) ws[sl[p0 + lane]] = xi;
+  if (lane < PW) xp[lane] = xi;
+  __syncwarp();
+  for (int r = p0 + pw + lane; r < m; r += 32) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j < pw) acc += V[cb[j] + r] * xp[j];
+    ws[sl[r]] -= acc;
+  }
+  __syncwarp();
+}
+
+/// Warp forward elimination of one supernode on workspace ws (slots sl).
+__device__ __forceinline__ void warp_fwd_sn(const double* __restrict__ V, const int* __restrict__ sl, int nc, int m,
+                                            double* ws, double* xp, int lane) {
+  for (int p0 = 0; p0 < nc; p0 += 32) {
+    const int pw = min(32, nc - p0);
+    if (pw <= 4) warp_fwd_panel<4>(V, sl, m, p0, pw, ws, xp, lane);
+    else if (pw <= 8) warp_fwd_panel<8>(V, sl, m, p0, pw, ws, xp, lane);
+    else if (pw <= 16) warp_fwd_panel<16>(V, sl, m, p0, pw, ws, xp, lane);
+    else warp_fwd_panel<32>(V, sl, m, p0, pw, ws, xp, lane);
+  }
+}
+
+constexpr int kBw = 16;  // CTA backward panel width (register budget)
+
+/// Backward substitution of one panel [p0, p0+pw) (rows below final in ws).
+template <int PW>
+__device__ __forceinline__ void warp_bwd_panel(const double* __restrict__ V, const int* __restrict__ sl, int m, int p0,
+                                               int pw, double* ws, int lane) {
+  int cb[PW];
+#pragma unroll
+  for (int j = 0; j < PW; ++j) cb[j] = j < pw ? (int)(col_off(p0 + j, m) - (p0 + j) - 1) : 0;
+  double acc[PW];
+#pragma unroll
+  for (int j = 0; j < PW; ++j) acc[j] = 0.0;
+  for (int r = p0 + pw + lane; r < m; r += 32) {
+    const double xr = ws[sl[r]];
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j < pw) acc[j] += V[cb[j] + r] * xr;
+  }
+  const double t = transpose_reduce<PW>(acc, lane);
+  const int li = lane % PW;
+  double xi = (lane < PW && li < pw) ? ws[sl[p0 + li]] - t : 0.0;
+  const long long mycb = lane < pw ? col_off(p0 + lane, m) - (p0 + lane) - 1 : 0;
+  double lcol[PW];
+#pragma unroll
+  for (int k = 0; k < PW; ++k) lcol[k] = (k < pw && k > lane && lane < pw) ? V[mycb + p0 + k] : 0.0;
+#pragma unroll
+  for (int k = PW - 1; k >= 0; --k) xi -= lcol[k] * __shfl_sync(0xffffffffu, xi, k);
+  if (lane < pw) ws[sl[p0 + lane]] = xi;
+  __syncwarp();
+}
 
 /// Warp backward substitution of one supernode (ancestor rows final in ws).
 __device__ __forceinline__ void warp_bwd_sn(const double* __restrict__ V, const int* __restrict__ sl, int nc, int m,
@@ -143,28 +185,9 @@ __device__ __forceinline__ void warp_bwd_sn(const double* __restrict__ V, const 
   const int np = (nc + kBw - 1) / kBw;
   for (int pi = np - 1; pi >= 0; --pi) {
     const int p0 = pi * kBw, pw = min(kBw, nc - p0);
-    double acc[kBw];
-#pragma unroll
-    for (int j = 0; j < kBw; ++j) acc[j] = 0.0;
-    for (int r = p0 + pw + lane; r < m; r += 32) {
-      const double xr = ws[sl[r]];
-#pragma unroll
-      for (int j = 0; j < kBw; ++j)
-        if (j < pw) acc[j] += Lval(V, m, r, p0 + j) * xr;
-    }
-    const double t = transpose_reduce16(acc, lane);
-    double xi = lane < pw ? ws[sl[p0 + lane]] - t : 0.0;
-    // transposed triangle: x_i -= sum_{k>i in panel} L(k, i) x_k, k descending
-    double lcol[kBw];
-#pragma unroll
-    for (int k = 0; k < kBw; ++k) lcol[k] = (k < pw && k > lane) ? Lval(V, m, p0 + k, p0 + lane) : 0.0;
-#pragma unroll
-    for (int k = kBw - 1; k >= 0; --k) {
-      const double xk = __shfl_sync(0xffffffffu, xi, k);
-      xi -= lcol[k] * xk;
-    }
-    if (lane < pw) ws[sl[p0 + lane]] = xi;
-    __syncwarp();
+    if (pw <= 4) warp_bwd_panel<4>(V, sl, m, p0, pw, ws, lane);
+    else if (pw <= 8) warp_bwd_panel<8>(V, sl, m, p0, pw, ws, lane);
+    else warp_bwd_panel<16>(V, sl, m, p0, pw, ws, lane);
   }
 }
 
@@ -213,7 +236,7 @@ __device__ __forceinline__ int stage_issue(const double* L, long long v0, long l
 
 /// Leaf forward sweep + diagonal scaling: one warp per (problem, task).
 /// Shared memory per warp: [xp 32][workspace ws_max][2 stage buffers].
-__global__ void __launch_bounds__(128, 4) k_leaf_fwd(SolveSet S, int ws_max) {
+__global__ void __launch_bounds__(128, 3) k_leaf_fwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -233,7 +256,16 @@ __global__ void __launch_bounds__(128, 4) k_leaf_fwd(SolveSet S, int ws_max) {
     int kc = sn0, kn = chunk_fwd_end(S, T, kc, sn1), buf = 0;
     int sh = stage_issue(L, S.sn_valoff[T.sn_base + kc], S.sn_valoff[T.sn_base + kn], stg[0], lane);
     cp_async_commit();
-    for (int i = lane; i < nc_task; i += kWarp) ws[i] = X[c0 + i];
+    {
+      const int* fp = S.fold_ptr + T.fold_base;
+      const int* fi = S.fold_idx + T.foldidx_base;
+      const double* CBp = S.CB + S.prob_cb[p] + r * S.cb_stride;
+      for (int i = lane; i < nc_task; i += kWarp) {
+        double v = X[c0 + i];
+        for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];  // child contributions, fixed order
+        ws[i] = v;
+      }
+    }
     for (int i = lane; i < cbl; i += kWarp) ws[nc_task + i] = 0.0;
     while (kc < sn1) {
       const int kn2 = kn < sn1 ? chunk_fwd_end(S, T, kn, sn1) : kn;
@@ -371,7 +403,7 @@ __device__ void cta_task(const SolveSet& S, int p, int tt, int mode, int in_smem
             for (int j = 0; j < kBw; ++j)
               if (j < pw) acc[j] += __ldg(V + cb[j] + rr) * xr;
           }
-          const double tw = transpose_reduce16(acc, lane);
+          const double tw = transpose_reduce<kBw>(acc, lane);
           if (lane < 16) red[wid][lane] = tw;
           __syncthreads();
           if (wid == 0) {
@@ -411,7 +443,7 @@ __global__ void __launch_bounds__(kTopThreads) k_cta_level(SolveSet S, int mode,
 
 /// Leaf backward sweep: one warp per (problem, task); ancestors read from X;
 /// factor values staged backwards in chunks.
-__global__ void __launch_bounds__(128, 4) k_leaf_bwd(SolveSet S, int ws_max) {
+__global__ void __launch_bounds__(128, 3) k_leaf_bwd(SolveSet S, int ws_max) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * (blockDim.x >> 5) + wib;
