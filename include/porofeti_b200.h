@@ -101,6 +101,25 @@ int pf_create(pf_ctx** out, const pf_config* cfg);
 /* Same, with an explicit per-element permeability array (2*n*n values, global
  * element order) overriding the seeded generator of the injection scenario. */
 int pf_create_with_permeability(pf_ctx** out, const pf_config* cfg, const double* k_elem);
+
+/* Multi-GPU sharding: one process per GPU, rank r owns the
+ * subdomains s with s % nranks == r; every lambda-space partial result
+ * (F-apply, preconditioner, interface right-hand side, rigid right-hand side)
+ * is summed over ranks with ncclAllReduce on the context stream (nccl_id: the
+ * 128-byte ncclUniqueId from pf_nccl_unique_id on rank 0, broadcast by the
+ * host), or with a host-provided reducer (pf_set_reducer: called with a HOST
+ * copy of the partial vector, which it must overwrite with the sum over
+ * ranks, e.g. via MPI or gloo).  Krylov vectors are replicated; reductions are
+ * deterministic for a fixed rank count. */
+typedef void (*pf_reduce_fn)(void* user, double* host_buf, int n, void* cuda_stream);
+int pf_create_sharded(pf_ctx** out, const pf_config* cfg, const double* k_elem, int rank, int nranks,
+                      const void* nccl_id);
+int pf_nccl_unique_id(void* out128);
+int pf_set_reducer(pf_ctx* ctx, pf_reduce_fn fn, void* user);
+/* owned subdomains (global ids) into out (may be NULL); returns the count */
+int pf_owned_subdomains(const pf_ctx* ctx, int* out);
+/* the shard plan itself (host only): owned subdomain ids of `rank`; returns the count */
+int pf_shard_plan(int n_sub, int rank, int nranks, int* owned);
 void pf_destroy(pf_ctx* ctx);
 const char* pf_last_error(const pf_ctx* ctx); /* ctx may be NULL (creation errors) */
 

@@ -224,6 +224,26 @@ class Feti {
     return y;
   }
 
+  /// Partial sums over a subset of subdomains (checks the sharded reduction
+  /// protocol): which 0 = F-apply terms, 1 = unscaled preconditioner terms.
+  Vec apply_subset(const Vec& x, const std::vector<int>& subs, int which) const {
+    Vec y(D_->n_lambda, 0.0);
+    for (int s : subs) {
+      const Sub& S = D_->subs[s];
+      Vec z(S.dim, 0.0);
+      S.G.mtv(x.data(), z.data());
+      if (which == 0) {
+        local_solve(s, z.data());
+      } else {
+        Vec o;
+        schur_apply(s, z, o);
+        z = o;
+      }
+      S.G.mv(z.data(), y.data(), true);
+    }
+    return y;
+  }
+
   /// REF schur_part (feti.hpp:212-224) on the boundary set B = Bu (+ Bp).
   void schur_apply(int s, const Vec& w, Vec& out) const {
     const Sub& S = D_->subs[s];
@@ -399,7 +419,9 @@ class Feti {
 
   /// Symmetric QMR with a symmetric (indefinite) preconditioner, right
   /// preconditioned form (Freund & Nachtigal 1994, Alg. 2 with M_L = I).
-  /// Converged when the quasi-residual bound tau_k sqrt(k+1) <= tol * ||r_0||.
+  /// Converged when the quasi-residual norm tau_k <= tol * ||r_0|| (the
+  /// guaranteed bound tau_k sqrt(k+1) is not used: near the rounding floor it
+  /// grows with k and can become unreachable).
   void sqmr(const Vec& rhs, Vec& lambda, PcgReport& rep) const {
     const auto& cfg = D_->cfg;
     const int n = D_->n_lambda;
@@ -432,7 +454,7 @@ class Feti {
         d[i] = c * c * th_old * th_old * d[i] + c * c * a * q[i];
         lambda[i] += d[i];
       }
-      const double est = tau * std::sqrt(double(k + 2));
+      const double est = tau;  // quasi-residual norm (estimate of the QMR residual)
       rep.history.push_back(est);
       rep.iterations = k + 1;
       if (est <= cfg.tol * t0) {

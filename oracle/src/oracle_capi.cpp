@@ -314,6 +314,15 @@ int or_precond(void* hh, const double* x, double* y) {
     std::memcpy(y, r.data(), sizeof(double) * r.size());
   });
 }
+int or_apply_subset(void* hh, const double* x, double* y, const int* subs, int nsubs, int which) {
+  return guard([&] {
+    auto* h = static_cast<Handle*>(hh);
+    const Vec v(x, x + h->D.n_lambda);
+    const Vec r = h->op->apply_subset(v, std::vector<int>(subs, subs + nsubs), which);
+    std::memcpy(y, r.data(), sizeof(double) * r.size());
+  });
+}
+
 int or_project(void* hh, double* x) {
   return guard([&] {
     auto* h = static_cast<Handle*>(hh);

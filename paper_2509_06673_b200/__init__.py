@@ -184,6 +184,11 @@ def lib():
         L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
         L.pf_bench_steps.argtypes = [vp, C.c_int, vp, vp, vp]
         L.pf_launch_count.restype = C.c_longlong
+        L.pf_create_sharded.argtypes = [C.POINTER(vp), C.POINTER(Config), vp, C.c_int, C.c_int, vp]
+        L.pf_nccl_unique_id.argtypes = [vp]
+        L.pf_set_reducer.argtypes = [vp, vp, vp]
+        L.pf_owned_subdomains.argtypes = [vp, vp]
+        L.pf_shard_plan.argtypes = [C.c_int, C.c_int, C.c_int, vp]
         L.pf_debug_factor_solve.argtypes = [C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_longlong, vp]
         L.pf_debug_disc.argtypes = [C.POINTER(Config), vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib = L
@@ -204,11 +209,16 @@ class FetiOperator:
     """Device-resident FETI interface operator of one discretisation
     (reference FetiOperator, feti.hpp:74-232, plus build_discretization)."""
 
-    def __init__(self, config=None, permeability=None, **kw):
+    def __init__(self, config=None, permeability=None, rank=0, nranks=1, nccl_id=None, **kw):
         self.cfg = config if isinstance(config, Config) else make_config(**kw)
         L = lib()
         h = C.c_void_p()
-        if permeability is not None:
+        if nranks > 1:
+            k = None if permeability is None else np.ascontiguousarray(permeability, np.float64)
+            idb = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+            code = L.pf_create_sharded(C.byref(h), C.byref(self.cfg), None if k is None else _ptr(k), rank, nranks,
+                                       idb)
+        elif permeability is not None:
             k = np.ascontiguousarray(permeability, np.float64)
             code = L.pf_create_with_permeability(C.byref(h), C.byref(self.cfg), _ptr(k))
         else:
@@ -218,8 +228,12 @@ class FetiOperator:
         self.info = Info()
         L.pf_get_info(h, C.byref(self.info))
         self.n_lambda = self.info.n_lambda
+        n_own = L.pf_owned_subdomains(h, None)
+        own = np.zeros(n_own, np.int32)
+        L.pf_owned_subdomains(h, _ptr(own))
+        self.owned = own.tolist()
         self.subs = []
-        for s in range(self.info.n_sub):
+        for s in self.owned:
             si = SubInfo()
             L.pf_get_sub_info(h, s, C.byref(si))
             self.subs.append({k: getattr(si, k) for k, _ in SubInfo._fields_})
@@ -264,9 +278,19 @@ class FetiOperator:
         return F
 
     # --- state (StateSnapshot, state.hpp:8-12) ---
+    def set_reducer(self, fn):
+        """Host reducer for sharded runs: fn(np.ndarray) -> None, sums in place over ranks."""
+        proto = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_void_p)
+
+        def cb(user, buf, n, stream):
+            fn(np.ctypeslib.as_array(buf, shape=(n,)))
+
+        self._reducer = proto(cb)  # keep alive
+        _check(lib().pf_set_reducer(self.h, C.cast(self._reducer, C.c_void_p), None), self.h)
+
     def state(self):
         xs = []
-        for s, S in enumerate(self.subs):
+        for s, S in zip(self.owned, self.subs):
             x = np.empty(S["dim"])
             _check(lib().pf_get_state(self.h, s, _ptr(x)), self.h)
             xs.append(x)
@@ -312,6 +336,19 @@ def phase_stats(op, iters=5):
     out = np.zeros(10)
     _check(lib().pf_phase_stats(op.h, iters, _ptr(out)), op.h)
     return dict(K=out[0:3].tolist(), II=out[3:6].tolist(), Q=out[6:9].tolist(), precond=float(out[9]))
+
+
+def nccl_unique_id():
+    buf = C.create_string_buffer(128)
+    _check(lib().pf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_plan(n_sub, rank, nranks):
+    """Subdomains owned by `rank` of `nranks` (host-side plan of pf_create_sharded)."""
+    out = np.zeros(n_sub, np.int32)
+    k = lib().pf_shard_plan(n_sub, rank, nranks, _ptr(out))
+    return out[:k].tolist()
 
 
 class StepSolver:

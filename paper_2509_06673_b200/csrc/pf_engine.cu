@@ -8,6 +8,7 @@
 // (timeloop.hpp:150-186).  There is no CPU execution path for any per-step
 // operator: without a CUDA device pf_create fails with PF_CUDA.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <atomic>
 #include <cstdlib>
@@ -412,19 +413,20 @@ __global__ void k_rigid_dot(int nfloat, const int* fsub, const long long* fvec, 
   s0 = block_sum(s0, red);
   s1 = block_sum(s1, red);
   s2 = block_sum(s2, red);
-  if (threadIdx.x == 0) e[3 * f] = s0, e[3 * f + 1] = s1, e[3 * f + 2] = s2;
-  (void)fsub;
+  const int g = fsub[f];  // global coarse block of this (owned) floating subdomain
+  if (threadIdx.x == 0) e[3 * g] = s0, e[3 * g + 1] = s1, e[3 * g + 2] = s2;
 }
 
 /// x_f += R_f alpha_f on the u block
-__global__ void k_rigid_add(int nfloat, const long long* fvec, const int* fnu, const double* xy, const long long* fxy,
-                            const double* alpha, double* x) {
+__global__ void k_rigid_add(int nfloat, const int* fsub, const long long* fvec, const int* fnu, const double* xy,
+                            const long long* fxy, const double* alpha, double* x) {
   const int f = blockIdx.y;
   if (f >= nfloat) return;
   const int nn = fnu[f] / 2;
   double* xx = x + fvec[f];
   const double* c = xy + fxy[f];
-  const double a0 = alpha[3 * f], a1 = alpha[3 * f + 1], a2 = alpha[3 * f + 2];
+  const int g = fsub[f];
+  const double a0 = alpha[3 * g], a1 = alpha[3 * g + 1], a2 = alpha[3 * g + 2];
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nn; nd += gridDim.x * blockDim.x) {
     xx[2 * nd] += a0 - a2 * c[2 * nd + 1];
     xx[2 * nd + 1] += a1 + a2 * c[2 * nd];
@@ -485,6 +487,30 @@ __global__ void k_dir_post(DirSet S, const double* XII, const double* YB, double
 struct Engine {
   Disc D;
   cudaStream_t st = nullptr;
+  // sharding: this engine owns subdomains s with s % nranks == rank;
+  // lambda-space partial results are summed over ranks (NCCL or a host reducer)
+  int rank = 0, nranks = 1;
+  std::vector<int> own, local_of;
+  ncclComm_t comm = nullptr;
+  pf_reduce_fn reducer = nullptr;
+  void* reducer_user = nullptr;
+  std::vector<double> host_red;
+  int nown() const { return (int)own.size(); }
+  const Subdomain& OS(int l) const { return D.subs[own[l]]; }
+  void reduce(double* p, int n) {
+    if (nranks <= 1 || n <= 0) return;
+    if (reducer) {  // host reducer: synchronise, reduce a host copy, copy back
+      host_red.resize(n);
+      PF_CUDA_CHECK(cudaMemcpyAsync(host_red.data(), p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      reducer(reducer_user, host_red.data(), n, (void*)st);
+      PF_CUDA_CHECK(cudaMemcpyAsync(p, host_red.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      return;
+    }
+    if (!comm) fail(kInvalid, "sharded engine without NCCL communicator or reducer");
+    if (ncclAllReduce(p, p, (size_t)n, ncclDouble, ncclSum, comm, st) != ncclSuccess) fail(kCuda, "ncclAllReduce failed");
+  }
   int nthreads = 1;
   bool floating_any = false;
   // symbolic per type
@@ -536,7 +562,7 @@ struct Engine {
   DevBuf<int> m_ptr, m_idx;
   DevBuf<double> m_val;
   // coarse
-  int nc = 0, nfloat = 0;
+  int nc = 0, nfloat = 0, nfloat_local = 0;
   DevBuf<int> c_ptr, c_idx, ct_ptr, ct_idx, d_fsub, d_fnu;
   DevBuf<double> c_val, ct_val, c_ainv, c_tmp1, c_tmp2, d_fxy, e_vec, alpha_vec;
   DevBuf<long long> d_fvec, d_fxyoff;
@@ -550,14 +576,26 @@ struct Engine {
   int launches_per_apply = 0;
 
   // ------------------------------------------------------------------
-  void create(const pf_config& cfg, const double* kover) {
+  void create(const pf_config& cfg, const double* kover, int rank_ = 0, int nranks_ = 1, const void* nccl_id = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       fail(kCuda, "no CUDA device: the B200 engine has no CPU execution path");
+    if (const char* lr = std::getenv("LOCAL_RANK")) PF_CUDA_CHECK(cudaSetDevice(std::atoi(lr) % ndev));
     PF_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     nthreads = cfg.threads > 0 ? cfg.threads : (int)std::max(1u, std::thread::hardware_concurrency());
     D = build_disc(cfg, kover);
+    rank = rank_, nranks = std::max(1, nranks_);
+    if (rank < 0 || rank >= nranks) fail(kInvalid, "rank out of range");
+    local_of.assign(D.subs.size(), -1);
+    for (std::size_t s = 0; s < D.subs.size(); ++s)
+      if ((int)s % nranks == rank) local_of[s] = (int)own.size(), own.push_back((int)s);
+    if (own.empty()) fail(kInvalid, "rank owns no subdomain");
+    if (nranks > 1 && nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      if (ncclCommInitRank(&comm, nranks, id, rank) != ncclSuccess) fail(kCuda, "ncclCommInitRank failed");
+    }
     const int pk = cfg.precond;
     use_q = pk == PF_PREC_GENERALIZED_MORTAR || pk == PF_PREC_DIRICHLET_MORTAR;
     use_dir = pk == PF_PREC_DIRICHLET || pk == PF_PREC_DIRICHLET_MORTAR;
@@ -620,6 +658,7 @@ struct Engine {
   }
 
   ~Engine() {
+    if (comm) ncclCommDestroy(comm);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -662,12 +701,12 @@ struct Engine {
     d_kptr.upload(kptr), d_kcol.upload(kcol), d_lptr.upload(lptr), d_lcol.upload(lcol), d_cpos.upload(cpos);
     d_cons.upload(cons);
     d_ftypes.upload(h_ftypes);
-    h_fsubs.resize(D.subs.size());
-    sub_vec.resize(D.subs.size());
+    h_fsubs.resize(nown());
+    sub_vec.resize(nown());
     std::vector<double> cxy;
     total_kv = total_lv = total_vec = total_z = total_g = 0;
-    for (std::size_t s = 0; s < D.subs.size(); ++s) {
-      const Subdomain& S = D.subs[s];
+    for (int s = 0; s < nown(); ++s) {
+      const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
       dev::FemSub& F = h_fsubs[s];
       F.type = S.type, F.sx = S.sx, F.sy = S.sy;
@@ -704,7 +743,7 @@ struct Engine {
   dev::FemSet femset() const {
     dev::FemSet S;
     const Topo& tp = *D.types[0].topo;
-    S.cx = tp.cx, S.cy = tp.cy, S.order = tp.order, S.nv = tp.nv, S.nsub = (int)D.subs.size();
+    S.cx = tp.cx, S.cy = tp.cy, S.order = tp.order, S.nv = tp.nv, S.nsub = nown();
     S.mesh_n = D.n, S.scenario = D.cfg.scenario;
     S.tri = d_tri.p, S.tedge = d_tedge.p, S.types = d_ftypes.p, S.subs = d_fsubs.p;
     S.kptr = d_kptr.p, S.kcol = d_kcol.p, S.lptr = d_lptr.p, S.lcol = d_lcol.p, S.cpos = d_cpos.p, S.cons = d_cons.p;
@@ -718,7 +757,7 @@ struct Engine {
   int colour_threads(int color) const {
     const Topo& tp = *D.types[0].topo;
     const int pi = color & 1, pj = (color >> 1) & 1;
-    return ((tp.cx - pi + 1) / 2) * ((tp.cy - pj + 1) / 2) * (int)D.subs.size();
+    return ((tp.cx - pi + 1) / 2) * ((tp.cy - pj + 1) / 2) * nown();
   }
 
   void assemble() {
@@ -736,19 +775,19 @@ struct Engine {
   /// Host numeric factorisation of every subdomain (and interior block),
   /// verified with the reference's seeded residual check (feti.hpp:28-36).
   void factor_all() {
-    const int ns = (int)D.subs.size();
+    const int ns = nown();
     std::vector<const SymFactor*> kt, it;
     for (auto& s : ksym) kt.push_back(&s);
     for (auto& s : isym) it.push_back(&s);
     std::vector<int> ptype(ns);
-    for (int s = 0; s < ns; ++s) ptype[s] = D.subs[s].type;
+    for (int s = 0; s < ns; ++s) ptype[s] = OS(s).type;
     Ksys.build(kt, ptype, 1);
     if (use_dir) Isys.build(it, ptype, 1);
     std::vector<double> hK(total_kv);
     PF_CUDA_CHECK(cudaMemcpy(hK.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
     h_K = std::move(hK);
     Ksys.factor_upload(nthreads, [&](int s, std::vector<double>& L, std::vector<double>& Dg) {
-      const Subdomain& S = D.subs[s];
+      const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
       const double* kv = h_K.data() + h_fsubs[s].kval;
       std::vector<int> fixed;
@@ -781,7 +820,7 @@ struct Engine {
     });
     if (use_dir)
       Isys.factor_upload(nthreads, [&](int s, std::vector<double>& LI, std::vector<double>& DI) {
-        const Subdomain& S = D.subs[s];
+        const Subdomain& S = OS(s);
         const SubType& T = D.types[S.type];
         const double* kv = h_K.data() + h_fsubs[s].kval;
         const auto& idx = itype_index[S.type];
@@ -807,8 +846,8 @@ struct Engine {
     HostGather gf, gb;
     std::vector<std::vector<std::tuple<int, int, double>>> rows_by_pos;
     std::vector<long long> fixpos;
-    for (std::size_t s = 0; s < D.subs.size(); ++s) {
-      const Subdomain& S = D.subs[s];
+    for (int s = 0; s < nown(); ++s) {
+      const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
       const SymFactor& F = ksym[S.type];
       std::vector<char> isfix(T.dim, 0);
@@ -836,8 +875,8 @@ struct Engine {
     auto build_scatter = [&](bool constrained, DevBuf<int>& ptr, DevBuf<int>& mid, DevBuf<long long>& idx,
                              DevBuf<double>& val) {
       std::vector<std::vector<std::tuple<int, long long, double>>> rows(D.n_lambda);  // (sub, col, val)
-      for (std::size_t s = 0; s < D.subs.size(); ++s) {
-        const Subdomain& S = D.subs[s];
+      for (int s = 0; s < nown(); ++s) {
+        const Subdomain& S = OS(s);
         const auto& L = constrained ? S.gc_lam : S.g_lam;
         const auto& Cc = constrained ? S.gc_col : S.g_col;
         const auto& V = constrained ? S.gc_val : S.g_val;
@@ -876,7 +915,7 @@ struct Engine {
 
   // ------------------------------------------------------------------
   void setup_dirichlet() {
-    const int ns = (int)D.subs.size(), nt = (int)D.types.size();
+    const int ns = nown(), nt = (int)D.types.size();
     // per type: Bset index, pre CSR (rows = all dofs, cols = B), post CSR (rows = B, cols = I)
     std::vector<int> pptr, pkpos, pbidx, ptarget, qptr, qkpos, qbidx, nrows_pre(nt), nrows_post(nt);
     std::vector<long long> prow0(nt), pent0(nt), qrow0(nt), qent0(nt);
@@ -918,11 +957,11 @@ struct Engine {
     std::vector<long long> skval(ns), swb(ns), sxii(ns);
     total_B = 0;
     for (int s = 0; s < ns; ++s) {
-      stype[s] = D.subs[s].type;
+      stype[s] = OS(s).type;
       skval[s] = h_fsubs[s].kval;
       swb[s] = total_B;
       sxii[s] = Isys.prob_x[s];  // (problem, 0); interior positions stride kW
-      total_B += (long long)D.types[D.subs[s].type].Bset.size();
+      total_B += (long long)D.types[OS(s).type].Bset.size();
     }
     d_subtype.upload(stype), d_sub_kval.upload(skval), d_sub_wb.upload(swb), d_sub_xii.upload(sxii);
     WB.alloc(2 * total_B), YB.alloc(2 * total_B), SB.alloc(2 * total_B);
@@ -930,7 +969,7 @@ struct Engine {
     HostGather g;
     std::vector<std::vector<std::tuple<int, long long, double>>> rows(D.n_lambda);
     for (int s = 0; s < ns; ++s) {
-      const Subdomain& S = D.subs[s];
+      const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
       std::vector<int> bpos(T.dim, -1);
       for (std::size_t k = 0; k < T.Bset.size(); ++k) bpos[T.Bset[k]] = (int)k;
@@ -968,7 +1007,7 @@ struct Engine {
 
   dev::DirSet dirset(bool post) {
     dev::DirSet S;
-    S.nsub = (int)D.subs.size();
+    S.nsub = nown();
     S.sub_type = d_subtype.p;
     S.kval = d_sub_kval.p, S.wb = d_sub_wb.p, S.xii = d_sub_xii.p;
     if (!post) {
@@ -986,8 +1025,8 @@ struct Engine {
   void setup_generalized() {
     // M = sum_s G_s K_s G_s^T (feti.hpp:86-88), sparse on lambda space
     std::map<std::pair<int, int>, double> M;
-    for (std::size_t s = 0; s < D.subs.size(); ++s) {
-      const Subdomain& S = D.subs[s];
+    for (int s = 0; s < nown(); ++s) {
+      const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
       const double* kv = h_K.data() + h_fsubs[s].kval;
       std::map<int, std::vector<std::pair<int, double>>> bycol;
@@ -1038,19 +1077,22 @@ struct Engine {
     std::vector<double> fxy;
     std::vector<std::map<int, double>> cols;
     const Topo& tp = *D.types[0].topo;
+    int fcount = 0;
     for (std::size_t s = 0; s < D.subs.size(); ++s) {
       const Subdomain& S = D.subs[s];
       const SubType& T = D.types[S.type];
       if (!T.floating) continue;
-      const int f = (int)fsub.size();
-      fsub.push_back((int)s), fnu.push_back(T.n_u), fvec.push_back(sub_vec[s]), fxyo.push_back((long long)fxy.size());
+      const int f = fcount++;
+      const int loc = local_of[s];
+      if (loc >= 0)
+        fsub.push_back(f), fnu.push_back(T.n_u), fvec.push_back(sub_vec[loc]), fxyo.push_back((long long)fxy.size());
       const double xc = 0.5 * (S.x0 + S.x1), yc = 0.5 * (S.y0 + S.y1);
       const double hx = (S.x1 - S.x0) / tp.cx, hy = (S.y1 - S.y0) / tp.cy;
       std::vector<double> nx(tp.nnode), ny(tp.nnode);
       for (int nd = 0; nd < tp.nnode; ++nd) {
         nx[nd] = S.x0 + 0.5 * tp.node_ic[nd][0] * hx - xc;
         ny[nd] = S.y0 + 0.5 * tp.node_ic[nd][1] * hy - yc;
-        fxy.push_back(nx[nd]), fxy.push_back(ny[nd]);
+        if (loc >= 0) fxy.push_back(nx[nd]), fxy.push_back(ny[nd]);
       }
       cols.resize(3 * (f + 1));
       for (std::size_t q = 0; q < S.g_lam.size(); ++q) {
@@ -1062,7 +1104,8 @@ struct Engine {
         else cols[3 * f + 1][S.g_lam[q]] += v, cols[3 * f + 2][S.g_lam[q]] += v * nx[nd];
       }
     }
-    nfloat = (int)fsub.size();
+    nfloat_local = (int)fsub.size();
+    nfloat = fcount;
     nc = 3 * nfloat;
     // CSR of G_c (lambda rows) and G_c^T (nc rows)
     std::vector<std::vector<std::pair<int, double>>> rows(D.n_lambda);
@@ -1137,23 +1180,23 @@ struct Engine {
   }
 
   void fill_info() {
-    info.n_sub = (int)D.subs.size();
+    info.n_sub = nown();
     info.n_lambda = D.n_lambda, info.n_lambda_u = D.n_lambda_u, info.n_coarse = nc;
     info.krylov = krylov, info.N = D.mat.N, info.n_floating = nfloat, info.n_types = (int)D.types.size();
     info.total_dim = total_vec, info.nnz_L = Ksys.nnzL, info.nnz_L_interior = use_dir ? Isys.nnzL : 0;
     info.nnz_K = total_kv;
     long long nsn = 0, ntask = 0;
-    for (std::size_t s = 0; s < D.subs.size(); ++s) nsn += ksym[D.subs[s].type].nsn, ntask += ksym[D.subs[s].type].ntask;
+    for (int s = 0; s < nown(); ++s) nsn += ksym[OS(s).type].nsn, ntask += ksym[OS(s).type].ntask;
     info.n_levels = Ksys.nlevel;
     info.n_supernodes = nsn, info.n_tasks = ntask;
     info.tau = D.mat.tau, info.T = D.mat.T;
     // B_F = sum_s [2*8*nnz(L_s) + 8*dim_s] + 2*(8+4)*nnz(G) + 2*8*n_lambda (supernodal values)
     long long nnzG = 0;
-    for (auto& S : D.subs) nnzG += (long long)S.g_lam.size();
+    for (int s = 0; s < nown(); ++s) nnzG += (long long)OS(s).g_lam.size();
     info.bytes_fapply = 2.0 * 8.0 * Ksys.nnzL + 8.0 * total_vec + 2.0 * 12.0 * nnzG + 2.0 * 8.0 * D.n_lambda;
     long long idim = 0;
     if (use_dir)
-      for (auto& S : D.subs) idim += isym[S.type].n;
+      for (int s = 0; s < nown(); ++s) idim += isym[OS(s).type].n;
     info.bytes_precond = use_dir ? 2.0 * 8.0 * Isys.nnzL + 8.0 * idim : 0.0;
   }
 
@@ -1179,6 +1222,7 @@ struct Engine {
                                                                 g_lam2X.idx.p, g_lam2X.val.p, x, Ksys.X.p, 1.0, 0); ::pf::g_launches++;
     Ksys.solve(st, 1);
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, y, 1.0, 0);
+    reduce(y, D.n_lambda);
     launches_per_apply = Ksys.launches + 3;
   }
 
@@ -1202,6 +1246,7 @@ struct Engine {
     const int n = D.n_lambda;
     if (use_gen) {
       dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, m_ptr.p, m_idx.p, m_val.p, r, z, 1.0, 0.0); ::pf::g_launches++;
+      reduce(z, n);
       return;
     }
     if (!use_dir) {
@@ -1214,11 +1259,12 @@ struct Engine {
       dev::k_gather_ll<<<cdiv(g_lam2B.nrows, 256), 256, 0, st>>>(g_lam2B.nrows, g_lam2B.rows.p, g_lam2B.ptr.p,
                                                                 g_lam2B.idx.p, g_lam2B.val.p, r, WB.p, 1.0, 0); ::pf::g_launches++;
     Isys.X.zero(st);
-    const int ns = (int)D.subs.size();
+    const int ns = nown();
     dev::k_dir_pre<<<dim3(8, ns), 256, 0, st>>>(dirset(false), WB.p, Isys.X.p, YB.p); ::pf::g_launches++;
     Isys.solve(st, 1);
     dev::k_dir_post<<<dim3(4, ns), 128, 0, st>>>(dirset(true), Isys.X.p, YB.p, SB.p); ::pf::g_launches++;
     spmv2(b_ptr, b_mid, b_idx, b_val, SB.p, z, 1.0, 0);
+    reduce(z, n);
   }
 
   void precond(const double* r, double* z) {
@@ -1266,17 +1312,18 @@ struct Engine {
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, out, 1.0, 0, dvec.p);
+    reduce(out, D.n_lambda);
   }
 
   void perm_in_K(const double* src) {
-    const int np = (int)D.subs.size();
+    const int np = nown();
     int maxn = 0;
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, src, Ksys.X.p, 1); ::pf::g_launches++;
   }
   void perm_out_K(double* dst) {
-    const int np = (int)D.subs.size();
+    const int np = nown();
     int maxn = 0;
     for (auto& k : ksym) maxn = std::max(maxn, k.n);
     dev::k_perm_out<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
@@ -1297,8 +1344,9 @@ struct Engine {
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
     perm_out_K(state.p);
-    if (nc) dev::k_rigid_add<<<dim3(8, nfloat), 256, 0, st>>>(nfloat, d_fvec.p, d_fnu.p, d_fxy.p, d_fxyoff.p,
-                                                             alpha_vec.p, state.p); ::pf::g_launches++;
+    if (nc && nfloat_local)
+      dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
+                                                              d_fxyoff.p, alpha_vec.p, state.p); ::pf::g_launches++;
   }
 
   // ------------------------------------------------------------------
@@ -1410,7 +1458,7 @@ struct Engine {
       h_scal[0] = rho, h_scal[1] = sigma, h_scal[4] = th_old, h_scal[5] = c;
       PF_CUDA_CHECK(cudaMemcpyAsync(scal.p + 20, h_scal.data(), 6 * sizeof(double), cudaMemcpyHostToDevice, st));
       dev::k_sqmr_dx<<<nb, 256, 0, st>>>(n, scal.p + 20, q, d, lambda); ::pf::g_launches++;
-      est = tau * std::sqrt(double(k + 2));
+      est = tau;  // quasi-residual norm tau_k <= tol ||r0|| (same rule as the oracle)
       rep.iterations = k + 1;
       if (est <= tol * t0) {
         rep.converged = 1;
@@ -1438,8 +1486,8 @@ struct Engine {
       const double pi = 3.14159265358979323846;
       const Material& m = D.mat;
       const double gam = m.alpha / (m.lam_P + 2 * m.mu_P);
-      for (std::size_t s = 0; s < D.subs.size(); ++s) {
-        const Subdomain& S = D.subs[s];
+      for (int s = 0; s < nown(); ++s) {
+        const Subdomain& S = OS(s);
         const SubType& T = D.types[S.type];
         double* x = h.data() + sub_vec[s];
         const double hx = (S.x1 - S.x0) / tp.cx, hy = (S.y1 - S.y0) / tp.cy;
@@ -1500,8 +1548,11 @@ struct Engine {
       const int n = D.n_lambda;
       // initial multiplier: warm start (timeloop.hpp:168-169) / coarse lambda0
       if (nc > 0) {
-        dev::k_rigid_dot<<<nfloat, 256, 0, st>>>(nfloat, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p, d_fxyoff.p, bvec.p,
-                                                 e_vec.p); ::pf::g_launches++;
+        e_vec.zero(st);
+        if (nfloat_local)
+          dev::k_rigid_dot<<<nfloat_local, 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
+                                                         d_fxyoff.p, bvec.p, e_vec.p);
+        reduce(e_vec.p, nc); ::pf::g_launches++;
         if (D.cfg.warm) {
           PF_CUDA_CHECK(cudaMemcpyAsync(kr_tmp.p, lam.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
           project(kr_tmp.p);
@@ -1584,6 +1635,52 @@ struct HostDev {
 
 extern "C" {
 
+int pf_create_sharded(pf_ctx** out, const pf_config* cfg, const double* k_elem, int rank, int nranks,
+                      const void* nccl_id) {
+  if (!out || !cfg) return PF_INVALID;
+  *out = nullptr;
+  auto* c = new pf_ctx();
+  const int rc = guarded(nullptr, [&] { c->eng.create(*cfg, k_elem, rank, nranks, nccl_id); });
+  if (rc != PF_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return PF_OK;
+}
+
+int pf_nccl_unique_id(void* out) {
+  if (!out) return PF_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PF_CUDA;
+  std::memcpy(out, &id, sizeof(id));
+  return PF_OK;
+}
+
+int pf_set_reducer(pf_ctx* ctx, pf_reduce_fn fn, void* user) {
+  if (!ctx) return PF_INVALID;
+  ctx->eng.reducer = fn;
+  ctx->eng.reducer_user = user;
+  return PF_OK;
+}
+
+int pf_owned_subdomains(const pf_ctx* ctx, int* out) {
+  if (!ctx) return PF_INVALID;
+  if (out) std::copy(ctx->eng.own.begin(), ctx->eng.own.end(), out);
+  return (int)ctx->eng.own.size();
+}
+
+int pf_shard_plan(int n_sub, int rank, int nranks, int* owned) {
+  if (n_sub < 1 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
+  int k = 0;
+  for (int s = 0; s < n_sub; ++s)
+    if (s % nranks == rank) {
+      if (owned) owned[k] = s;
+      ++k;
+    }
+  return k;
+}
+
 int pf_create_with_permeability(pf_ctx** out, const pf_config* cfg, const double* k_elem) {
   if (!out || !cfg) return PF_INVALID;
   *out = nullptr;
@@ -1662,11 +1759,13 @@ int pf_project(pf_ctx* ctx, double* x) {
   });
 }
 
-int pf_local_solve(pf_ctx* ctx, int s, double* x) {
-  if (!ctx || !x || s < 0 || s >= (int)ctx->eng.D.subs.size()) return PF_INVALID;
+int pf_local_solve(pf_ctx* ctx, int s_global, double* x) {
+  if (!ctx || !x || s_global < 0 || s_global >= (int)ctx->eng.D.subs.size()) return PF_INVALID;
+  const int s = ctx->eng.local_of[s_global];
+  if (s < 0) return PF_INVALID;  // not owned by this shard
   return guarded(ctx, [&] {
     auto& E = ctx->eng;
-    const auto& T = E.D.types[E.D.subs[s].type];
+    const auto& T = E.D.types[E.OS(s).type];
     // stage the right-hand side into the state-shaped buffer, solve all (others zero)
     std::vector<double> h(E.total_vec, 0.0);
     std::copy(x, x + T.dim, h.begin() + E.sub_vec[s]);
@@ -1700,11 +1799,13 @@ int pf_step(pf_ctx* ctx, pf_report* rep) {
   return rc;
 }
 
-int pf_get_state(pf_ctx* ctx, int s, double* x) {
-  if (!ctx || !x || s < 0 || s >= (int)ctx->eng.D.subs.size()) return PF_INVALID;
+int pf_get_state(pf_ctx* ctx, int s_global, double* x) {
+  if (!ctx || !x || s_global < 0 || s_global >= (int)ctx->eng.D.subs.size()) return PF_INVALID;
+  const int s = ctx->eng.local_of[s_global];
+  if (s < 0) return PF_INVALID;  // not owned by this shard
   return guarded(ctx, [&] {
     auto& E = ctx->eng;
-    const auto& T = E.D.types[E.D.subs[s].type];
+    const auto& T = E.D.types[E.OS(s).type];
     PF_CUDA_CHECK(cudaMemcpyAsync(x, E.state.p + E.sub_vec[s], sizeof(double) * T.dim, cudaMemcpyDeviceToHost, E.st));
     PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
   });

@@ -93,6 +93,7 @@ def lib():
         L.or_n_ifaces.argtypes = [P]
         L.or_kelem.argtypes = [P, dp]
         L.or_n_src.argtypes = [P]
+        L.or_apply_subset.argtypes = [P, dp, dp, ip, C.c_int, C.c_int]
         _lib = L
     return _lib
 
@@ -162,6 +163,12 @@ class Oracle:
     def apply(self, x):
         y = np.zeros(self.n_lambda)
         check(lib().or_apply(self.h, np.ascontiguousarray(x, np.float64), y))
+        return y
+
+    def apply_subset(self, x, subs, which=0):
+        y = np.zeros(self.n_lambda)
+        s = np.ascontiguousarray(subs, np.int32)
+        check(lib().or_apply_subset(self.h, np.ascontiguousarray(x, np.float64), y, s, len(s), which))
         return y
 
     def precond(self, x):
