@@ -648,6 +648,18 @@ struct Engine {
     if (floating_any) setup_coarse();
     setup_krylov();
     project_initial();
+    if (std::getenv("PF_VERBOSE")) {
+      auto dump = [](const char* name, SolveSystem& S) {
+        if (!S.L.p) return;
+        std::fprintf(stderr, "[pf] %s: %d levels, nnzL %lld\n", name, S.nlevel, S.nnzL);
+        for (int l = 0; l < S.nlevel; ++l)
+          std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d, %s\n", l, S.level_nwork[l], S.level_ws[l],
+                       S.warp_level(l) ? "warp" : "cta");
+      };
+      dump("K", Ksys);
+      dump("K_II", Isys);
+      dump("Q", Qsys);
+    }
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
     const auto t4 = std::chrono::steady_clock::now();
     info.t_setup = std::chrono::duration<double>(t1 - t0).count();
@@ -1061,7 +1073,17 @@ struct Engine {
     for (auto& kv : M) rc.push_back(kv.first);
     Csr A = pattern_from_pairs(D.n_lambda, D.n_lambda, rc);
     for (auto& kv : M) A.val[A.find(kv.first.first, kv.first.second)] = kv.second;
-    qsym = analyse(A, D.lambda_ic, std::max<long long>(4096, (long long)A.nnz() / 64));
+    {
+      // the multiplier graph is nearly one-dimensional (chains along the
+      // interfaces joined at cross points): small nested-dissection leaves and
+      // small warp tasks keep the dependency chains short
+      auto envi = [](const char* k, long long d) {
+        const char* v = std::getenv(k);
+        return v ? std::atoll(v) : d;
+      };
+      qsym = analyse(A, D.lambda_ic, envi("PF_Q_CAP", 1024), (int)envi("PF_Q_WS", 256), 0.15, 16,
+                     (int)envi("PF_Q_LEAF", 8));
+    }
     Qsys.build({&qsym}, {0}, 1);
     std::vector<double> L, Dg;
     factor_host(qsym, A, A.val.data(), {}, L, Dg);

@@ -46,10 +46,11 @@ def make_config(mesh_n=32, SX=1, SY=2, order=1, E=1.0, nu=0.3, alpha=1.0, c0=1e-
 BASELINE_CONFIGS = {
     "c1": dict(mesh_n=32, SX=1, SY=2, order=1, nu=0.3, c0=1e-3, dt=1e-2, steps=5, scenario="mms-t"),
     "c2": dict(mesh_n=128, SX=2, SY=2, order=2, nu=0.3, c0=1e-3, dt=1e-2, steps=10, scenario="mms-t"),
-    "c3": dict(mesh_n=512, SX=8, SY=8, order=2, nu=0.49999, c0=1e-3, dt=1e-3, steps=20, scenario="mms-t"),
+    "c3": dict(mesh_n=512, SX=8, SY=8, order=2, nu=0.49999, c0=1e-3, dt=1e-3, steps=20, scenario="mms-t",
+               max_iter=3000),
     "c4": dict(mesh_n=1024, SX=32, SY=32, order=2, nu=0.3, c0=1e-3, dt=1e-2, steps=10, scenario="mms-t"),
     "c5": dict(mesh_n=512, SX=16, SY=16, order=2, nu=0.4, c0=1e-4, dt=1e-3, steps=100,
-               scenario="injection"),
+               scenario="injection", max_iter=3000),
 }
 
 
