@@ -23,6 +23,7 @@
 #include "pf_disc.hpp"
 #include "pf_fem.cuh"
 #include "pf_kernels.cuh"
+#include "pf_factor.cuh"
 #include "pf_symbolic.hpp"
 
 namespace pf {
@@ -61,7 +62,12 @@ struct DevBuf {
   }
   void upload(const std::vector<T>& h) {
     alloc(h.size());
-    if (!h.empty()) PF_CUDA_CHECK(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    if (!h.empty()) {
+      PF_CUDA_CHECK(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+      // pageable H2D may return before the DMA lands; kernels run on a
+      // non-blocking stream, so wait here (setup-time only)
+      PF_CUDA_CHECK(cudaDeviceSynchronize());
+    }
   }
   void zero(cudaStream_t s) {
     if (n) PF_CUDA_CHECK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
@@ -784,8 +790,11 @@ struct Engine {
   }
 
   // ------------------------------------------------------------------
-  /// Host numeric factorisation of every subdomain (and interior block),
-  /// verified with the reference's seeded residual check (feti.hpp:28-36).
+  /// Numeric factorisation of every subdomain saddle K_s and (Dirichlet)
+  /// interior block K_II on the device (batched multifrontal LDL^T,
+  /// pf_factor.cuh), verified with the reference's seeded residual check
+  /// (feti.hpp:28-36) evaluated on the device.  PF_HOST_FACTOR=1 selects the
+  /// host supernodal factorisation (debug / cross-check only).
   void factor_all() {
     const int ns = nown();
     std::vector<const SymFactor*> kt, it;
@@ -795,9 +804,231 @@ struct Engine {
     for (int s = 0; s < ns; ++s) ptype[s] = OS(s).type;
     Ksys.build(kt, ptype, 1);
     if (use_dir) Isys.build(it, ptype, 1);
-    std::vector<double> hK(total_kv);
-    PF_CUDA_CHECK(cudaMemcpy(hK.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
-    h_K = std::move(hK);
+    const bool host = std::getenv("PF_HOST_FACTOR") && std::atoi(std::getenv("PF_HOST_FACTOR")) != 0;
+    if (host || use_gen) {
+      h_K.resize(total_kv);
+      PF_CUDA_CHECK(cudaMemcpy(h_K.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
+    }
+    if (host) {
+      factor_all_host();
+    } else {
+      factor_device(Ksys, ksym, false);
+      if (use_dir) factor_device(Isys, isym, true);
+    }
+    check_factor_residual();
+    Ksys.prepare_smem();
+    if (use_dir) Isys.prepare_smem();
+  }
+
+  /// Batched multifrontal factorisation of a SolveSystem on the device.
+  /// Fronts live in a chunk buffer; subdomains are processed in chunks whose
+  /// fronts fit PF_FRONT_GB (default 8 GB), one launch per etree height.
+  void factor_device(SolveSystem& Sys, const std::vector<SymFactor>& syms, bool interior) {
+    const int nt = (int)syms.size();
+    std::vector<FrontMaps> fm(nt);
+    std::vector<AScatter> as(nt);
+    std::vector<char> used(nt, 0);
+    for (int p = 0; p < nown(); ++p) used[OS(p).type] = 1;
+    parallel_for(nt, nthreads, [&](int t) {
+      if (!used[t]) return;
+      const SubType& T = D.types[t];
+      fm[t] = build_front_maps(syms[t]);
+      if (!interior) {
+        std::vector<int> fixed;
+        if (T.floating) fixed.assign(T.fix.begin(), T.fix.end());
+        as[t] = build_ascatter(syms[t], fm[t], T.K, nullptr, fixed);
+      } else {
+        const auto& idx = itype_index[t];
+        const auto& pos = itype_pos[t];
+        std::vector<std::pair<int, int>> rc;
+        for (int i : idx)
+          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
+            if (pos[T.K.col[q]] >= 0) rc.emplace_back(pos[i], pos[T.K.col[q]]);
+        const Csr KII = pattern_from_pairs((int)idx.size(), (int)idx.size(), rc);
+        std::vector<int> kmap(KII.nnz(), -1);
+        for (int i : idx)
+          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
+            if (pos[T.K.col[q]] >= 0) kmap[KII.find(pos[i], pos[T.K.col[q]])] = q;
+        as[t] = build_ascatter(syms[t], fm[t], KII, kmap.data(), {});
+      }
+    });
+    // concatenate per-type maps
+    std::vector<int> snbase(nt, 0), ncol, nrow, col0, ch_beg, ch_cnt, as_beg, as_cnt, ch_idx, relpos, as_kidx, as_fpos;
+    std::vector<long long> valoff, foff, rp_beg;
+    for (int t = 0; t < nt; ++t) {
+      snbase[t] = (int)ncol.size();
+      if (!used[t]) continue;
+      const SymFactor& F = syms[t];
+      const FrontMaps& M = fm[t];
+      const AScatter& A = as[t];
+      for (int k = 0; k < F.nsn; ++k) {
+        ncol.push_back(F.sn_ncol[k]), nrow.push_back(F.sn_nrow[k]), col0.push_back(F.sn_col0[k]);
+        valoff.push_back(F.sn_valoff[k]), foff.push_back(M.foff[k]);
+        ch_beg.push_back((int)ch_idx.size() + M.ch_ptr[k]), ch_cnt.push_back(M.ch_ptr[k + 1] - M.ch_ptr[k]);
+        rp_beg.push_back((long long)relpos.size() + M.rp_off[k]);
+        if (as_kidx.size() + A.ptr[k] > (std::size_t)INT32_MAX) fail(kInternal, "front scatter map exceeds int32");
+        as_beg.push_back((int)as_kidx.size() + A.ptr[k]), as_cnt.push_back(A.ptr[k + 1] - A.ptr[k]);
+      }
+      ch_idx.insert(ch_idx.end(), M.ch_idx.begin(), M.ch_idx.end());
+      relpos.insert(relpos.end(), M.relpos.begin(), M.relpos.end());
+      as_kidx.insert(as_kidx.end(), A.kidx.begin(), A.kidx.end());
+      as_fpos.insert(as_fpos.end(), A.fpos.begin(), A.fpos.end());
+    }
+    DevBuf<int> d_snbase, d_ncol, d_nrow, d_col0, d_chb, d_chc, d_asb, d_asc, d_chi, d_rp, d_ask, d_asf, d_ptype, d_itp,
+        d_its, d_err;
+    DevBuf<long long> d_valoff, d_foff, d_rpb, d_pkval, d_fbase;
+    d_snbase.upload(snbase), d_ncol.upload(ncol), d_nrow.upload(nrow), d_col0.upload(col0);
+    d_chb.upload(ch_beg), d_chc.upload(ch_cnt), d_asb.upload(as_beg), d_asc.upload(as_cnt);
+    d_chi.upload(ch_idx.empty() ? std::vector<int>{0} : ch_idx), d_rp.upload(relpos.empty() ? std::vector<int>{0} : relpos);
+    d_ask.upload(as_kidx), d_asf.upload(as_fpos);
+    d_valoff.upload(valoff), d_foff.upload(foff), d_rpb.upload(rp_beg);
+    const int np = nown();
+    std::vector<long long> pkval(np);
+    for (int p = 0; p < np; ++p) pkval[p] = h_fsubs[p].kval;
+    d_pkval.upload(pkval);
+    d_err.upload(std::vector<int>{0});
+    // chunks of subdomains whose fronts fit the budget
+    double gb = 8.0;
+    if (const char* v = std::getenv("PF_FRONT_GB")) gb = std::atof(v);
+    std::size_t fr = 0, tot = 0;
+    PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+    const long long budget = (long long)std::min(gb * 1e9, 0.5 * (double)fr) / 8;
+    long long maxf = 0;
+    for (int t = 0; t < nt; ++t)
+      if (used[t]) maxf = std::max(maxf, fm[t].fsize);
+    if (maxf > budget) fail(kInternal, "a single subdomain's fronts exceed the front budget");
+    std::vector<std::pair<int, int>> chunks;
+    for (int p0 = 0; p0 < np;) {
+      long long acc = 0;
+      int p1 = p0;
+      while (p1 < np && acc + fm[OS(p1).type].fsize <= budget) acc += fm[OS(p1).type].fsize, ++p1;
+      chunks.emplace_back(p0, p1);
+      p0 = p1;
+    }
+    long long fmax_chunk = 0;
+    for (auto& c : chunks) {
+      long long acc = 0;
+      for (int p = c.first; p < c.second; ++p) acc += fm[OS(p).type].fsize;
+      fmax_chunk = std::max(fmax_chunk, acc);
+    }
+    DevBuf<double> Fb;
+    Fb.alloc(fmax_chunk);
+    int maxh = 0;
+    for (int t = 0; t < nt; ++t)
+      if (used[t]) maxh = std::max(maxh, fm[t].nheight);
+    d_ptype.upload(ptype_of_own());
+    for (auto& c : chunks) {
+      std::vector<long long> fbase(np, 0);
+      long long acc = 0;
+      for (int p = c.first; p < c.second; ++p) fbase[p] = acc, acc += fm[OS(p).type].fsize;
+      d_fbase.upload(fbase);
+      std::vector<int> ip, is;
+      std::vector<int> hptr(maxh + 1, 0);
+      for (int h = 0; h < maxh; ++h) {
+        for (int p = c.first; p < c.second; ++p) {
+          const FrontMaps& M = fm[OS(p).type];
+          if (h >= M.nheight) continue;
+          for (int q = M.height_ptr[h]; q < M.height_ptr[h + 1]; ++q) ip.push_back(p), is.push_back(M.height_sn[q]);
+        }
+        hptr[h + 1] = (int)ip.size();
+      }
+      d_itp.upload(ip), d_its.upload(is);
+      for (int h = 0; h < maxh; ++h) {
+        const int n = hptr[h + 1] - hptr[h];
+        if (!n) continue;
+        dev::MfSet S;
+        S.type_snbase = d_snbase.p;
+        S.ncol = d_ncol.p, S.nrow = d_nrow.p, S.col0 = d_col0.p;
+        S.valoff = d_valoff.p, S.foff = d_foff.p, S.rp_beg = d_rpb.p;
+        S.ch_beg = d_chb.p, S.ch_cnt = d_chc.p, S.as_beg = d_asb.p, S.as_cnt = d_asc.p;
+        S.ch_idx = d_chi.p, S.relpos = d_rp.p, S.as_kidx = d_ask.p, S.as_fpos = d_asf.p;
+        S.nitem = n, S.it_prob = d_itp.p + hptr[h], S.it_sn = d_its.p + hptr[h];
+        S.prob_type = d_ptype.p, S.prob_kval = d_pkval.p, S.prob_lval = Sys.d_prob_lval.p, S.prob_x = Sys.d_prob_x.p;
+        S.prob_fbase = d_fbase.p;
+        S.Kv = Kv.p, S.F = Fb.p, S.L = Sys.L.p, S.D = Sys.D.p, S.err = d_err.p;
+        dev::k_mf_factor<<<n, 256, 0, st>>>(S);
+        ::pf::g_launches++;
+      }
+      // the chunk's work lists / bases are freed by the next upload: finish first
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    PF_CUDA_CHECK(cudaGetLastError());
+    int err = 0;
+    PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err)
+      fail(kSingular, std::string(interior ? "interior block" : "subdomain saddle") +
+                          " factorization failed (zero pivot)");
+  }
+
+  std::vector<int> ptype_of_own() {
+    std::vector<int> pt(nown());
+    for (int p = 0; p < nown(); ++p) pt[p] = OS(p).type;
+    return pt;
+  }
+
+  /// Seeded residual check (feti.hpp:28-36) on the device for every K_s:
+  /// b ~ U(-1,1) from mt19937(20240901), x = K_s^{-1} b through the sweep
+  /// kernels, ||K_s x - b|| / ||b|| < 1e-8.
+  void check_factor_residual() {
+    const int nt = (int)D.types.size();
+    const int np = nown();
+    std::vector<long long> type_b(nt, 0), type_kptr(nt), type_kcol(nt);
+    std::vector<int> type_dim(nt);
+    std::vector<double> b;
+    std::vector<char> fix;
+    for (int t = 0; t < nt; ++t) {
+      const SubType& T = D.types[t];
+      type_b[t] = (long long)b.size();
+      type_dim[t] = T.dim;
+      type_kptr[t] = h_ftypes[t].kptr, type_kcol[t] = h_ftypes[t].kcol;
+      std::mt19937 rng(20240901u);
+      std::uniform_real_distribution<double> U(-1.0, 1.0);
+      for (int i = 0; i < T.dim; ++i) b.push_back(U(rng));
+      fix.resize(b.size(), 0);
+      if (T.floating)
+        for (int f : T.fix) fix[type_b[t] + f] = 1;
+    }
+    DevBuf<double> d_b, d_y, d_out;
+    DevBuf<char> d_fix;
+    DevBuf<long long> d_tb, d_tkp, d_tkc, d_psrc, d_pkval;
+    DevBuf<int> d_tdim;
+    d_b.upload(b), d_fix.upload(fix), d_tb.upload(type_b), d_tkp.upload(type_kptr), d_tkc.upload(type_kcol);
+    d_tdim.upload(type_dim);
+    std::vector<long long> psrc(np), pkval(np);
+    int maxn = 0;
+    for (int p = 0; p < np; ++p) psrc[p] = type_b[OS(p).type], pkval[p] = h_fsubs[p].kval, maxn = std::max(maxn, D.types[OS(p).type].dim);
+    d_psrc.upload(psrc), d_pkval.upload(pkval);
+    d_y.alloc(Ksys.total_x);
+    d_out.alloc(2 * (std::size_t)np);
+    dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, d_psrc.p, Ksys.d_prob_n.p,
+                                                            Ksys.d_prob_perm.p, Ksys.d_perm.p, d_b.p, Ksys.X.p, 1);
+    ::pf::g_launches++;
+    Ksys.solve(st, 1);
+    dev::k_perm_out<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, Ksys.d_prob_x.p, Ksys.d_prob_x.p, Ksys.d_prob_n.p,
+                                                             Ksys.d_prob_perm.p, Ksys.d_perm.p, Ksys.X.p, d_y.p, 1);
+    ::pf::g_launches++;
+    dev::ResidSet R;
+    R.nprob = np;
+    R.prob_type = Ksys.d_prob_type.p, R.type_dim = d_tdim.p, R.kptr = d_kptr.p, R.kcol = d_kcol.p;
+    R.prob_kval = d_pkval.p, R.prob_y = Ksys.d_prob_x.p, R.type_kptr = d_tkp.p, R.type_kcol = d_tkc.p,
+    R.type_b = d_tb.p;
+    R.Kv = Kv.p, R.b = d_b.p, R.y = d_y.p, R.fix = d_fix.p, R.out = d_out.p;
+    dev::k_residual_norms<<<np, 256, 0, st>>>(R);
+    ::pf::g_launches++;
+    PF_CUDA_CHECK(cudaGetLastError());
+    std::vector<double> out(2 * (std::size_t)np);
+    PF_CUDA_CHECK(cudaMemcpyAsync(out.data(), d_out.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int p = 0; p < np; ++p) {
+      const double res = std::sqrt(out[2 * p] / out[2 * p + 1]);
+      if (!(res < 1e-8))
+        fail(kSingular, "subdomain " + std::to_string(own[p]) + " factorization residual " + std::to_string(res) +
+                            " (check boundary constraints)");
+    }
+  }
+
+  /// Host supernodal factorisation (PF_HOST_FACTOR=1): debug / cross-check.
+  void factor_all_host() {
     Ksys.factor_upload(nthreads, [&](int s, std::vector<double>& L, std::vector<double>& Dg) {
       const Subdomain& S = OS(s);
       const SubType& T = D.types[S.type];
@@ -805,30 +1036,6 @@ struct Engine {
       std::vector<int> fixed;
       if (T.floating) fixed.assign(T.fix.begin(), T.fix.end());
       factor_host(ksym[S.type], T.K, kv, fixed, L, Dg);
-      // seeded residual check on the (regularised) matrix (feti.hpp:28-36)
-      std::mt19937 rng(20240901u);
-      std::uniform_real_distribution<double> U(-1.0, 1.0);
-      std::vector<double> b(T.dim), x;
-      for (auto& v : b) v = U(rng);
-      x = b;
-      solve_host(ksym[S.type], L, Dg, x.data());
-      std::vector<char> isfix(T.dim, 0);
-      for (int f : fixed) isfix[f] = 1;
-      double rn = 0, bn = 0;
-      for (int i = 0; i < T.dim; ++i) {
-        double r = -b[i];
-        if (isfix[i]) {
-          r += x[i];
-        } else {
-          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-            if (!isfix[T.K.col[q]]) r += kv[q] * x[T.K.col[q]];
-        }
-        rn += r * r, bn += b[i] * b[i];
-      }
-      const double res = std::sqrt(rn / bn);
-      if (!(res < 1e-8))
-        fail(kSingular, "subdomain " + std::to_string(s) + " factorization residual " + std::to_string(res) +
-                            " (check boundary constraints)");
     });
     if (use_dir)
       Isys.factor_upload(nthreads, [&](int s, std::vector<double>& LI, std::vector<double>& DI) {
@@ -847,8 +1054,6 @@ struct Engine {
             if (pos[T.K.col[q]] >= 0) KII.val[KII.find(pos[i], pos[T.K.col[q]])] = kv[q];
         factor_host(isym[S.type], KII, KII.val.data(), {}, LI, DI);
       });
-    Ksys.prepare_smem();
-    if (use_dir) Isys.prepare_smem();
   }
   std::vector<double> h_K;
 

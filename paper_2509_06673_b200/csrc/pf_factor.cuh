@@ -1,0 +1,142 @@
+// pf_factor.cuh — device numeric factorisation (north-star item 2): batched
+// multifrontal LDL^T of every subdomain saddle K_s and interior block K_II.
+//
+// One CTA per (subdomain, supernode); all supernodes of one etree height are
+// independent and run in one launch.  Each CTA assembles its frontal matrix
+// (m x m, column-major, lower triangle) in global memory from the subdomain's
+// assembled CSR values (A-scatter map) and the update matrices of its
+// children (extend-add, children in fixed order -> deterministic), performs
+// the partial LDL^T of its nc pivot columns (no pivoting: the constrained
+// saddles are symmetric quasi-definite, SURVEY Fact 6), writes the packed
+// strict-lower trapezoid of L and the pivots D, and leaves its trailing Schur
+// complement in the front for the parent.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace pf {
+namespace dev {
+
+struct MfSet {
+  // per supernode (concatenated over types; index sn_base[type] + k)
+  const int* type_snbase;
+  const int *ncol, *nrow, *col0;
+  const long long *valoff, *foff, *rp_beg;
+  const int *ch_beg, *ch_cnt, *as_beg, *as_cnt;
+  const int *ch_idx, *relpos, *as_kidx, *as_fpos;
+  // this launch: (problem, supernode) items
+  int nitem;
+  const int *it_prob, *it_sn;
+  // per problem
+  const int* prob_type;
+  const long long *prob_kval, *prob_lval, *prob_x, *prob_fbase;
+  const double* Kv;
+  double* F;
+  double* L;
+  double* D;
+  int* err;
+};
+
+__global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
+  const int it = blockIdx.x;
+  if (it >= S.nitem) return;
+  const int p = S.it_prob[it], k = S.it_sn[it];
+  const int t = S.prob_type[p];
+  const int sk = S.type_snbase[t] + k;
+  const int nc = S.ncol[sk], m = S.nrow[sk];
+  double* Fk = S.F + S.prob_fbase[p] + S.foff[sk];
+  const long long mm = (long long)m * m;
+  for (long long q = threadIdx.x; q < mm; q += blockDim.x) Fk[q] = 0.0;
+  __syncthreads();
+  const double* Kv = S.Kv + S.prob_kval[p];
+  for (int q = S.as_beg[sk] + threadIdx.x; q < S.as_beg[sk] + S.as_cnt[sk]; q += blockDim.x) {
+    const int kid = S.as_kidx[q];
+    Fk[S.as_fpos[q]] += kid >= 0 ? Kv[kid] : 1.0;
+  }
+  __syncthreads();
+  for (int ci = 0; ci < S.ch_cnt[sk]; ++ci) {
+    const int sc = S.type_snbase[t] + S.ch_idx[S.ch_beg[sk] + ci];
+    const int ncc = S.ncol[sc], mc = S.nrow[sc], u = mc - ncc;
+    const double* Fc = S.F + S.prob_fbase[p] + S.foff[sc];
+    const int* rp = S.relpos + S.rp_beg[sc];
+    // column-wise (coalesced in the child front), lower triangle only
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int b = warp; b < u; b += nw) {
+      const int rb = rp[b];
+      const double* src = Fc + (long long)(ncc + b) * mc + ncc;
+      double* dst = Fk + (long long)rb * m;
+      for (int a = b + lane; a < u; a += 32) dst[rp[a]] += src[a];
+    }
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = 0; j < nc; ++j) {
+    const double d = Fk[j + (long long)j * m];
+    if (!(d != 0.0) || !isfinite(d)) {
+      if (threadIdx.x == 0) atomicExch(S.err, 1);
+      return;
+    }
+    const double inv = 1.0 / d;
+    const double* cj = Fk + (long long)j * m;
+    for (int c = j + 1 + warp; c < m; c += nw) {
+      const double lc = cj[c] * inv;
+      double* col = Fk + (long long)c * m;
+      for (int i = c + lane; i < m; i += 32) col[i] -= cj[i] * lc;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) Fk[i + (long long)j * m] *= inv;
+    __syncthreads();
+  }
+  double* L = S.L + S.prob_lval[p] + S.valoff[sk];
+  for (int j = 0; j < nc; ++j) {
+    const long long o = (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[o + (i - j - 1)] = Fk[i + (long long)j * m];
+  }
+  double* D = S.D + S.prob_x[p] + S.col0[sk];
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) D[j] = Fk[j + (long long)j * m];
+}
+
+/// Seeded residual check (feti.hpp:28-36) on the device: per problem p,
+/// out = (||K y - b||^2, ||b||^2) with y, b in natural order; fixed dofs are
+/// identity rows with no coupling (the regularised floating saddle).
+struct ResidSet {
+  int nprob;
+  const int *prob_type, *type_dim, *kptr, *kcol;
+  const long long *prob_kval, *prob_y, *type_kptr, *type_kcol, *type_b;
+  const double *Kv, *b, *y;
+  const char* fix;  // per type, natural order (offset type_b)
+  double* out;
+};
+
+__global__ void k_residual_norms(ResidSet R) {
+  __shared__ double red[32];
+  const int p = blockIdx.x;
+  if (p >= R.nprob) return;
+  const int t = R.prob_type[p];
+  const int n = R.type_dim[t];
+  const int* rp = R.kptr + R.type_kptr[t];
+  const int* cc = R.kcol + R.type_kcol[t];
+  const char* fx = R.fix + R.type_b[t];
+  const double* b = R.b + R.type_b[t];
+  const double* yy = R.y + R.prob_y[p];
+  const double* kv = R.Kv + R.prob_kval[p];
+  double rn = 0.0, bn = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double r;
+    if (fx[i]) {
+      r = yy[i] - b[i];
+    } else {
+      r = -b[i];
+      for (int q = rp[i]; q < rp[i + 1]; ++q)
+        if (!fx[cc[q]]) r += kv[q] * yy[cc[q]];
+    }
+    rn += r * r, bn += b[i] * b[i];
+  }
+  rn = block_sum(rn, red);
+  __syncthreads();
+  bn = block_sum(bn, red);
+  if (threadIdx.x == 0) R.out[2 * p] = rn, R.out[2 * p + 1] = bn;
+}
+
+}  // namespace dev
+}  // namespace pf

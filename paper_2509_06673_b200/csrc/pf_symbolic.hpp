@@ -644,3 +644,130 @@ inline void solve_tasks_host(const SymFactor& F, const std::vector<double>& L, c
 }
 
 }  // namespace pf
+
+namespace pf {
+
+/// Structure for the multifrontal numeric factorisation on the device: the
+/// supernodal tree in final numbering, fronts (m x m column-major) per
+/// supernode, children lists with relative row positions for the
+/// extend-add, and supernodes grouped by height (all supernodes of one height
+/// are independent).
+struct FrontMaps {
+  std::vector<int> parent, height;
+  int nheight = 0;
+  std::vector<int> height_ptr, height_sn;  // supernodes by height
+  std::vector<long long> foff;             // front offset per supernode (doubles)
+  long long fsize = 0;
+  std::vector<int> ch_ptr, ch_idx;         // children (ascending)
+  std::vector<long long> rp_off;           // per supernode as a child: relpos offset
+  std::vector<int> relpos;                 // rows beyond own columns -> index in parent rows
+};
+
+inline FrontMaps build_front_maps(const SymFactor& F) {
+  FrontMaps M;
+  const int ns = F.nsn;
+  std::vector<int> sn_of(F.n);
+  for (int k = 0; k < ns; ++k)
+    for (int c = 0; c < F.sn_ncol[k]; ++c) sn_of[F.sn_col0[k] + c] = k;
+  M.parent.assign(ns, -1);
+  for (int k = 0; k < ns; ++k)
+    if (F.sn_nrow[k] > F.sn_ncol[k]) M.parent[k] = sn_of[F.rows[F.sn_rowoff[k] + F.sn_ncol[k]]];
+  M.height.assign(ns, 0);
+  std::vector<int> order(ns);
+  std::iota(order.begin(), order.end(), 0);
+  // children precede parents in the final numbering
+  for (int k = 0; k < ns; ++k)
+    if (M.parent[k] >= 0) {
+      if (M.parent[k] <= k) fail(kInternal, "front maps: parent not after child");
+      M.height[M.parent[k]] = std::max(M.height[M.parent[k]], M.height[k] + 1);
+    }
+  for (int h : M.height) M.nheight = std::max(M.nheight, h + 1);
+  M.height_ptr.assign(M.nheight + 1, 0);
+  for (int h : M.height) M.height_ptr[h + 1]++;
+  for (int h = 0; h < M.nheight; ++h) M.height_ptr[h + 1] += M.height_ptr[h];
+  M.height_sn.resize(ns);
+  {
+    std::vector<int> pos(M.height_ptr.begin(), M.height_ptr.end() - 1);
+    for (int k = 0; k < ns; ++k) M.height_sn[pos[M.height[k]]++] = k;
+  }
+  M.foff.resize(ns + 1);
+  M.foff[0] = 0;
+  for (int k = 0; k < ns; ++k) M.foff[k + 1] = M.foff[k] + (long long)F.sn_nrow[k] * F.sn_nrow[k];
+  M.fsize = M.foff[ns];
+  std::vector<std::vector<int>> ch(ns);
+  for (int k = 0; k < ns; ++k)
+    if (M.parent[k] >= 0) ch[M.parent[k]].push_back(k);
+  M.ch_ptr.assign(ns + 1, 0);
+  for (int k = 0; k < ns; ++k) {
+    M.ch_idx.insert(M.ch_idx.end(), ch[k].begin(), ch[k].end());
+    M.ch_ptr[k + 1] = (int)M.ch_idx.size();
+  }
+  M.rp_off.assign(ns + 1, 0);
+  for (int k = 0; k < ns; ++k) {
+    const int p = M.parent[k];
+    const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+    if (p >= 0) {
+      const int* pr = &F.rows[F.sn_rowoff[p]];
+      const int pm = F.sn_nrow[p];
+      for (int i = nc; i < m; ++i) {
+        const int r = F.rows[F.sn_rowoff[k] + i];
+        const int* it = std::lower_bound(pr, pr + pm, r);
+        if (it == pr + pm || *it != r) fail(kInternal, "front maps: child row not in parent structure");
+        M.relpos.push_back(int(it - pr));
+      }
+    }
+    M.rp_off[k + 1] = (long long)M.relpos.size();
+  }
+  return M;
+}
+
+/// Where the lower-triangle entries of A go in the fronts: for supernode k,
+/// entries [as_ptr[k], as_ptr[k+1]) with value index (into the subdomain's K
+/// values; -1 = unit diagonal of a fixed dof) and front position.
+struct AScatter {
+  std::vector<int> ptr, kidx, fpos;
+};
+
+/// A given by its pattern (natural numbering) and, per entry, the index of its
+/// value in the subdomain's K value array (kmap, nullptr = identity).
+inline AScatter build_ascatter(const SymFactor& F, const FrontMaps& M, const Csr& A, const int* kmap,
+                               const std::vector<int>& fixed_natural) {
+  const int n = F.n;
+  std::vector<char> isfix(n, 0);
+  for (int f : fixed_natural) isfix[F.iperm[f]] = 1;
+  std::vector<int> sn_of(n);
+  for (int k = 0; k < F.nsn; ++k)
+    for (int c = 0; c < F.sn_ncol[k]; ++c) sn_of[F.sn_col0[k] + c] = k;
+  std::vector<std::vector<std::pair<int, int>>> per(F.nsn);
+  std::vector<int> where(n, -1);
+  for (int k = 0; k < F.nsn; ++k) {
+    const int m = F.sn_nrow[k];
+    const int* R = &F.rows[F.sn_rowoff[k]];
+    for (int i = 0; i < m; ++i) where[R[i]] = i;
+    for (int c = 0; c < F.sn_ncol[k]; ++c) {
+      const int pc = F.sn_col0[k] + c, nat = F.perm[pc];
+      if (isfix[pc]) {
+        per[k].emplace_back(-1, c + c * m);
+        continue;
+      }
+      for (int q = A.ptr[nat]; q < A.ptr[nat + 1]; ++q) {
+        const int pr = F.iperm[A.col[q]];
+        if (pr < pc || isfix[pr]) continue;
+        const int i = where[pr];
+        if (i < 0) fail(kInternal, "ascatter: entry outside the symbolic structure");
+        per[k].emplace_back(kmap ? kmap[q] : q, i + c * m);
+      }
+    }
+    for (int i = 0; i < m; ++i) where[R[i]] = -1;
+  }
+  (void)M;
+  AScatter S;
+  S.ptr.assign(F.nsn + 1, 0);
+  for (int k = 0; k < F.nsn; ++k) {
+    for (auto& e : per[k]) S.kidx.push_back(e.first), S.fpos.push_back(e.second);
+    S.ptr[k + 1] = (int)S.kidx.size();
+  }
+  return S;
+}
+
+}  // namespace pf
