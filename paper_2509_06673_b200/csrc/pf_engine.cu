@@ -24,6 +24,7 @@
 #include "pf_fem.cuh"
 #include "pf_kernels.cuh"
 #include "pf_factor.cuh"
+#include "pf_sweep.cuh"
 #include "pf_symbolic.hpp"
 
 namespace pf {
@@ -114,6 +115,11 @@ struct SolveSystem {
       d_fold_ptr, d_fold_idx, d_prob_type, d_perm, d_prob_n;
   DevBuf<long long> d_sn_rowoff, d_sn_valoff, d_prob_x, d_prob_lval, d_prob_cb, d_prob_perm;
   DevBuf<double> L, D, X, CB;
+  DevBuf<int4> d_meta;
+  DevBuf<uint16_t> d_slots16;
+  DevBuf<long long> d_tlbeg;
+  DevBuf<int> d_tlbytes;
+  int smax = 8;  // max supernode row count (padded to 8)
   int nrhs_alloc = 1;
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
@@ -123,8 +129,11 @@ struct SolveSystem {
     prob_type = ptype;
     nrhs_alloc = nrhs;
     std::vector<dev::TypeDesc> td(types.size());
-    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm;
-    std::vector<long long> sn_rowoff, sn_valoff, type_perm_off;
+    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm, tlbytes;
+    std::vector<long long> sn_rowoff, sn_valoff, type_perm_off, tlbeg;
+    std::vector<int4> meta;
+    std::vector<uint16_t> slots16;
+    smax = 8;
     nlevel = 0;
     for (auto* F : types) nlevel = std::max(nlevel, F->nlevel);
     level_ws.assign(nlevel, 0);
@@ -139,15 +148,35 @@ struct SolveSystem {
       T.cb_base = (long long)cbrows.size();
       T.fold_base = (long long)fptr.size();
       T.foldidx_base = (long long)fidx.size();
+      T.slot_base = (long long)slots16.size();
       for (int s = 0; s < F.nsn; ++s) {
         sn_col0.push_back(F.sn_col0[s]), sn_ncol.push_back(F.sn_ncol[s]), sn_nrow.push_back(F.sn_nrow[s]);
         sn_rowoff.push_back(F.sn_rowoff[s]), sn_valoff.push_back(F.sn_valoff[s]);
+        const int m = F.sn_nrow[s];
+        const int ts = F.sn_task[s] >= 0 ? F.task_sn0[F.sn_task[s]] : -1;
+        if (ts < 0) fail(kInternal, "supernode without a sweep task");
+        const long long vrel = 8 * (F.sn_valoff[s] - F.sn_valoff[ts]);
+        if (vrel > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
+        meta.push_back(make_int4(F.sn_ncol[s], m, (int)((long long)slots16.size() - T.slot_base), (int)vrel));
+        for (int i = 0; i < m; ++i) {
+          const int v = F.slot[F.sn_rowoff[s] + i];
+          if (v < 0 || v > 65535) fail(kInternal, "sweep slot out of uint16 range");
+          slots16.push_back((uint16_t)v);
+        }
+        while (slots16.size() % 8) slots16.push_back(0);
+        smax = std::max(smax, (m + 7) & ~7);
       }
+      if ((long long)slots16.size() - T.slot_base > INT32_MAX) fail(kInternal, "slot table exceeds int32");
       slot.insert(slot.end(), F.slot.begin(), F.slot.end());
       for (int t = 0; t < F.ntask; ++t) {
         t0.push_back(F.task_sn0[t]), t1.push_back(F.task_sn1[t]);
         c0.push_back(F.task_c0[t]), c1.push_back(F.task_c1[t]);
         cbo.push_back(F.task_cboff[t]), cbl.push_back(F.task_cblen[t]);
+        long long nb = 0;
+        if (F.task_sn1[t] - F.task_sn0[t] > kMaxTaskSn) fail(kInternal, "sweep task exceeds kMaxTaskSn supernodes");
+        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) nb += 8 * sn_size(F.sn_ncol[k], F.sn_nrow[k]);
+        if (nb > INT32_MAX || (F.sn_valoff[F.task_sn0[t]] & 1)) fail(kInternal, "task value stream layout");
+        tlbeg.push_back(F.sn_valoff[F.task_sn0[t]]), tlbytes.push_back((int)nb);
         const int gl = glevel(F, F.task_level[t]);
         const int ws = (F.task_c1[t] - F.task_c0[t]) + F.task_cblen[t];
         level_ws[gl] = std::max(level_ws[gl], ws);
@@ -167,6 +196,7 @@ struct SolveSystem {
     nnzL = 0;
     for (int p = 0; p < np; ++p) {
       const SymFactor& F = *types[ptype[p]];
+      total_L = (total_L + 1) & ~1LL;  // 16-byte aligned value streams
       prob_x[p] = total_x, prob_lval[p] = total_L, prob_cb[p] = total_cb;
       total_x += F.n, total_L += F.nval, total_cb += (long long)F.cb_rows.size();
       nnzL += F.nval;
@@ -185,9 +215,8 @@ struct SolveSystem {
       level_nwork[l] = (int)wp[l].size();
     }
     ws_max = 0;
-    for (int l = 0; l + 1 < nlevel; ++l)
-      if (warp_level(l)) ws_max = std::max(ws_max, level_ws[l]);
-    ws_max = (ws_max + 1) & ~1;  // even: 16-byte aligned stage buffers
+    for (int l = 0; l < nlevel; ++l) ws_max = std::max(ws_max, level_ws[l]);
+    ws_max = (ws_max + 1) & ~1;  // even: 16-byte aligned slot buffers behind it
 
     d_types.upload(td);
     d_sn_col0.upload(sn_col0), d_sn_ncol.upload(sn_ncol), d_sn_nrow.upload(sn_nrow);
@@ -196,7 +225,8 @@ struct SolveSystem {
     d_cbrows.upload(cbrows), d_fold_ptr.upload(fptr), d_fold_idx.upload(fidx);
     d_prob_type.upload(ptype), d_prob_x.upload(prob_x), d_prob_lval.upload(prob_lval), d_prob_cb.upload(prob_cb);
     d_perm.upload(perm), d_prob_perm.upload(pperm), d_prob_n.upload(pn);
-    L.alloc(total_L);
+    d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_tlbytes.upload(tlbytes);
+    L.alloc(total_L + 4);  // bulk copies round the last stream up to 16 bytes
     D.alloc(total_x);
     X.alloc(total_x * nrhs);
     CB.alloc(std::max<long long>(1, total_cb * nrhs));
@@ -211,6 +241,7 @@ struct SolveSystem {
     parallel_for((int)prob_type.size(), threads, [&](int p) {
       std::vector<double> l, d;
       fn(p, l, d);
+      to_blocked(*syms[prob_type[p]], l);
       PF_CUDA_CHECK(cudaMemcpy(L.p + prob_lval[p], l.data(), sizeof(double) * l.size(), cudaMemcpyHostToDevice));
       PF_CUDA_CHECK(cudaMemcpy(D.p + prob_x[p], d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice));
     });
@@ -224,6 +255,7 @@ struct SolveSystem {
     S.task_sn0 = d_t0.p, S.task_sn1 = d_t1.p, S.task_c0 = d_c0.p, S.task_c1 = d_c1.p;
     S.task_cboff = d_cbo.p, S.task_cblen = d_cbl.p, S.cb_rows = d_cbrows.p;
     S.fold_ptr = d_fold_ptr.p, S.fold_idx = d_fold_idx.p;
+    S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.task_lbytes = d_tlbytes.p;
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
     S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p;
@@ -233,34 +265,17 @@ struct SolveSystem {
     return S;
   }
 
-  static constexpr int kWpb = 4;
-  static constexpr int kCtaSmemDoubles = 24 * 1024;
   int launches = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timed = false;
-  double phase_ms[3] = {0, 0, 0};  // warp levels / CTA levels + root / backward
+  double phase_ms[3] = {0, 0, 0};  // forward levels / root / backward levels
 
-  static constexpr int kWarpWs = 256;  // levels whose tasks all fit run one warp per task
-  // one warp per task only when the level has enough tasks to fill the GPU
-  // with warps (>= one wave at ~16 warps/SM); otherwise a CTA per task splits rows
-  bool warp_level(int l) const {
-    return l < nlevel - 1 && level_ws[l] <= kWarpWs && (l == 0 || level_nwork[l] >= 148 * 16);
-  }
+  int sweep_smem() const { return dev::kSweepWarps * dev::SweepSmem::bytes(ws_max, smax); }
 
   void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
     if (level_nwork[l] == 0) return;
     dev::SolveSet S = set(nrhs, l);
-    if (warp_level(l)) {
-      const std::size_t sm = sizeof(double) * (std::size_t)(ws_max + 32 + 2 * (dev::kStage + 2)) * kWpb;
-      if (mode == 0)
-        dev::k_leaf_fwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);
-      else
-        dev::k_leaf_bwd<<<cdiv(S.nwork, kWpb), 32 * kWpb, sm, st>>>(S, ws_max);
-    } else {
-      const bool in_smem = level_ws[l] <= kCtaSmemDoubles;
-      dev::k_cta_level<<<S.nwork, dev::kTopThreads, in_smem ? sizeof(double) * level_ws[l] : 0, st>>>(
-          S, mode, in_smem ? 1 : 0);
-    }
+    dev::k_sweep<<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(), st>>>(S, mode, ws_max, smax);
     ::pf::g_launches++;
     ++launches;
   }
@@ -291,14 +306,10 @@ struct SolveSystem {
   }
 
   void prepare_smem() {
-    const std::size_t sm_leaf = sizeof(double) * (std::size_t)(ws_max + 32 + 2 * (dev::kStage + 2)) * kWpb;
-    if (sm_leaf > 227 * 1024)
-      fail(kInternal, "leaf solve workspace exceeds shared memory (" + std::to_string(sm_leaf) + " B)");
+    if (sweep_smem() > 227 * 1024)
+      fail(kInternal, "sweep workspace exceeds shared memory (" + std::to_string(sweep_smem()) + " B)");
     // the attribute is per kernel (shared by all systems): raise it to the opt-in maximum once
-    const int smax = 227 * 1024;
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_leaf_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_leaf_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_cta_level, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - 3 * 1024));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
 };
 
@@ -657,10 +668,10 @@ struct Engine {
     if (std::getenv("PF_VERBOSE")) {
       auto dump = [](const char* name, SolveSystem& S) {
         if (!S.L.p) return;
-        std::fprintf(stderr, "[pf] %s: %d levels, nnzL %lld\n", name, S.nlevel, S.nnzL);
+        std::fprintf(stderr, "[pf] %s: %d levels, nnzL %lld, ws_max %d, smax %d, smem/CTA %d\n", name, S.nlevel, S.nnzL,
+                     S.ws_max, S.smax, S.sweep_smem());
         for (int l = 0; l < S.nlevel; ++l)
-          std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d, %s\n", l, S.level_nwork[l], S.level_ws[l],
-                       S.warp_level(l) ? "warp" : "cta");
+          std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d\n", l, S.level_nwork[l], S.level_ws[l]);
       };
       dump("K", Ksys);
       dump("K_II", Isys);
@@ -815,9 +826,9 @@ struct Engine {
       factor_device(Ksys, ksym, false);
       if (use_dir) factor_device(Isys, isym, true);
     }
-    check_factor_residual();
     Ksys.prepare_smem();
     if (use_dir) Isys.prepare_smem();
+    check_factor_residual();
   }
 
   /// Batched multifrontal factorisation of a SolveSystem on the device.
@@ -1292,6 +1303,7 @@ struct Engine {
     Qsys.build({&qsym}, {0}, 1);
     std::vector<double> L, Dg;
     factor_host(qsym, A, A.val.data(), {}, L, Dg);
+    to_blocked(qsym, L);
     PF_CUDA_CHECK(cudaMemcpy(Qsys.L.p, L.data(), sizeof(double) * L.size(), cudaMemcpyHostToDevice));
     PF_CUDA_CHECK(cudaMemcpy(Qsys.D.p, Dg.data(), sizeof(double) * Dg.size(), cudaMemcpyHostToDevice));
     Qsys.prepare_smem();

@@ -14,6 +14,8 @@
 
 #include <cuda_runtime.h>
 
+#include "pf_layout.hpp"
+
 namespace pf {
 namespace dev {
 
@@ -88,10 +90,8 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
     __syncthreads();
   }
   double* L = S.L + S.prob_lval[p] + S.valoff[sk];
-  for (int j = 0; j < nc; ++j) {
-    const long long o = (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[o + (i - j - 1)] = Fk[i + (long long)j * m];
-  }
+  for (int j = 0; j < nc; ++j)
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[blk_off(nc, m, i, j)] = Fk[i + (long long)j * m];
   double* D = S.D + S.prob_x[p] + S.col0[sk];
   for (int j = threadIdx.x; j < nc; j += blockDim.x) D[j] = Fk[j + (long long)j * m];
 }

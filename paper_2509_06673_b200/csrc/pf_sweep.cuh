@@ -1,0 +1,394 @@
+// pf_sweep.cuh — the batched supernodal LDL^T sweep (the F-apply and
+// Dirichlet-preconditioner hot loop), one warp per (subdomain, task).
+//
+// A task's factor values form one 16-byte aligned stream of units
+// (pf_layout.hpp: per panel a triangle, then row blocks).  The warp runs a
+// producer and a consumer over the same unit sequence:
+//   producer: walks the sequence ahead of the consumer and issues one TMA
+//             bulk copy (cp.async.bulk, mbarrier complete_tx) per unit into a
+//             shared-memory ring (contiguous placement, wrapping to the ring
+//             start), plus one per supernode for its slot list (per-type
+//             table, L2 resident);
+//   consumer: waits on the unit's mbarrier and computes straight from shared
+//             memory with base+immediate addressing —
+//             forward : triangle solved with register shuffles, row blocks
+//                       updated with one shared load + one DFMA per value;
+//             backward: row blocks reduced into per-column partial sums,
+//                       warp transpose-reduction, then the transposed triangle.
+// Up to kUnits units (ring bytes permitting) are in flight per warp, so the
+// factor stream stays ahead of the dependency chain of the solve.  The
+// backward sweep walks the same units in reverse order.  All shared memory is
+// addressed as offsets from the kernel's dynamic shared array so every access
+// compiles to LDS/STS with immediate offsets.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pf_layout.hpp"
+
+namespace pf {
+namespace dev {
+
+extern __shared__ __align__(128) unsigned char g_sm[];
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kRingBytes = 16384;  // per warp; >= the largest unit (kRB*kPW*8)
+constexpr int kUnits = 8;          // units in flight per warp (mbarriers)
+constexpr int kSweepWarps = 4;     // warps per CTA
+
+/// Per-warp shared memory: ring | barriers | unit table | task meta | ws | slots.
+struct SweepSmem {
+  static constexpr int kBar = kRingBytes;
+  static constexpr int kUnit = kBar + 8 * kUnits;      // int per unit slot: ring offset
+  static constexpr int kMeta = kUnit + 8 * kUnits;     // int4 per task supernode
+  static constexpr int kWs = kMeta + 16 * kMaxTaskSn;  // ws doubles
+  __host__ __device__ static int bytes(int ws_max, int smax) { return kWs + 8 * ws_max + ((2 * smax + 15) & ~15); }
+};
+
+__device__ __forceinline__ double lds(int byte) { return *reinterpret_cast<const double*>(g_sm + byte); }
+__device__ __forceinline__ int4 meta_at(int wb, int k) {
+  return *reinterpret_cast<const int4*>(g_sm + wb + SweepSmem::kMeta + 16 * k);
+}
+
+/// Producer + consumer state of one warp (warp-uniform registers).
+struct SweepRing {
+  int wb;                   // per-warp region (offset in g_sm)
+  unsigned sbase;           // shared address of g_sm
+  const unsigned char* g;   // task value stream (16-byte aligned)
+  const uint16_t* slots;    // type slot table
+  int nsn;
+  bool fwd;
+  // producer cursor: supernode k, panel p (width pw, rows below nb), block b
+  // (-2 slot list, -1 triangle), stream position pos of the next value unit
+  int k, p, pw, nb, b, m, nc, pos;
+  bool done;
+  int issued, cons, head, tail;
+  int lane;
+
+  __device__ __forceinline__ unsigned bar(int u) const { return sbase + wb + SweepSmem::kBar + 8 * (u & (kUnits - 1)); }
+  __device__ __forceinline__ int& utab(int u) const {
+    return *reinterpret_cast<int*>(g_sm + wb + SweepSmem::kUnit + 8 * (u & (kUnits - 1)));
+  }
+
+  __device__ __forceinline__ void enter_sn() {  // producer enters supernode k
+    const int4 mt = meta_at(wb, k);
+    nc = mt.x, m = mt.y, b = -2;
+  }
+  __device__ __forceinline__ void start(bool forward, int end_bytes) {
+    fwd = forward, done = nsn == 0;
+    k = forward ? 0 : nsn - 1;
+    pos = forward ? 0 : end_bytes;
+    if (!done) enter_sn();
+  }
+  __device__ __forceinline__ void set_panel(int pp) {
+    p = pp;
+    const int p0 = pp * kPW;
+    pw = min(kPW, nc - p0), nb = m - p0 - pw;
+  }
+  /// advance the producer cursor past the current unit
+  __device__ __forceinline__ void advance() {
+    if (fwd) {
+      if (b == -2) {
+        set_panel(0), b = -1;
+      } else if (b + 1 < ((nb + kRB - 1) >> 5)) {
+        ++b;
+      } else if ((p + 1) * kPW < nc) {
+        set_panel(p + 1), b = -1;
+      } else if (k + 1 < nsn) {
+        ++k, enter_sn();
+      } else {
+        done = true;
+      }
+    } else {
+      if (b == -2) {
+        set_panel((nc - 1) / kPW), b = ((nb + kRB - 1) >> 5) - 1;
+      } else if (b >= 0) {
+        --b;
+      } else if (p > 0) {
+        set_panel(p - 1), b = ((nb + kRB - 1) >> 5) - 1;
+      } else if (k > 0) {
+        --k, enter_sn();
+      } else {
+        done = true;
+      }
+    }
+  }
+  /// issue units ahead while barriers and ring space allow
+  __device__ __forceinline__ void pump() {
+    while (!done && issued - cons < kUnits) {
+      int sz;
+      const unsigned char* src;
+      if (b == -2) {
+        sz = ((m + 7) & ~7) * 2;
+        src = reinterpret_cast<const unsigned char*>(slots + meta_at(wb, k).z);
+      } else {
+        sz = b == -1 ? 8 * tri_pad(pw) : 8 * even_up(min(kRB, nb - kRB * b) * pw);
+        if (sz == 0) {  // pw == 1: no triangle unit
+          advance();
+          continue;
+        }
+        if (fwd) {
+          src = g + pos;
+        } else {
+          src = g + pos - sz;
+        }
+      }
+      unsigned h = (unsigned)head;
+      if ((h % kRingBytes) + sz > kRingBytes) h += kRingBytes - h % kRingBytes;
+      if ((int)(h - (unsigned)tail) + sz > kRingBytes) break;
+      const int off = (int)(h % kRingBytes);
+      if (lane == 0) {
+        *reinterpret_cast<int2*>(g_sm + wb + SweepSmem::kUnit + 8 * (issued & (kUnits - 1))) = make_int2(off, (int)h);
+        const unsigned bb = bar(issued);
+        fence_proxy_async();
+        mbar_expect_tx(bb, (unsigned)sz);
+        bulk_g2s(sbase + wb + off, src, (unsigned)sz, bb);
+      }
+      if (b != -2) pos += fwd ? sz : -sz;
+      head = (int)h + sz;
+      ++issued;
+      advance();
+    }
+  }
+  /// offset (in g_sm) of the next unit of the consumer's sequence, resident
+  __device__ __forceinline__ int acquire() {
+    pump();
+    __syncwarp();
+    mbar_wait(bar(cons), (unsigned)(cons / kUnits) & 1u);
+    return wb + utab(cons);
+  }
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    ++cons;
+    tail = cons < issued ? *reinterpret_cast<const int*>(g_sm + wb + SweepSmem::kUnit + 8 * (cons & (kUnits - 1)) + 4)
+                         : head;
+  }
+};
+
+/// copy the supernode's slot list out of the ring
+__device__ __forceinline__ void take_slots(SweepRing& R, int slo, int m) {
+  const int src = R.acquire();
+  for (int i = R.lane; i < (m + 7) >> 3; i += 32)
+    *reinterpret_cast<int4*>(g_sm + slo + 16 * i) = *reinterpret_cast<const int4*>(g_sm + src + 16 * i);
+  R.release();
+}
+
+__device__ __forceinline__ int slot_at(int slo, int r) { return *reinterpret_cast<const uint16_t*>(g_sm + slo + 2 * r); }
+__device__ __forceinline__ double& ws_at(int wso, int s) { return *reinterpret_cast<double*>(g_sm + wso + 8 * s); }
+
+/// forward elimination of one panel; PWC >= pw compile-time bound, EXACT: pw == PWC
+template <int PWC, bool EXACT>
+__device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw, int m, int wso, int lane) {
+  const bool mine = lane < pw;
+  double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) : 0.0;
+  if (pw > 1) {
+    const int T = R.acquire() + 8 * (lane * (lane - 1) / 2);
+    double lrow[PWC];
+#pragma unroll
+    for (int j = 0; j < PWC; ++j) lrow[j] = (lane > j && mine) ? lds(T + 8 * j) : 0.0;
+    R.release();
+#pragma unroll
+    for (int j = 0; j < PWC - 1; ++j) xi -= lrow[j] * __shfl_sync(0xffffffffu, xi, j);
+  }
+  if (mine) ws_at(wso, slot_at(slo, p0 + lane)) = xi;
+  double xr[PWC];
+#pragma unroll
+  for (int j = 0; j < PWC; ++j) xr[j] = __shfl_sync(0xffffffffu, xi, j);
+  const int nb = m - p0 - pw;
+  for (int b0 = 0; b0 < nb; b0 += kRB) {
+    const int nr = min(kRB, nb - b0);
+    const int V = R.acquire() + 8 * lane;
+    if (lane < nr) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (nr == kRB) {
+#pragma unroll
+        for (int j = 0; j < PWC; j += 4) {
+          if (EXACT || j < pw) a0 += lds(V + 8 * kRB * j) * xr[j];
+          if (EXACT || j + 1 < pw) a1 += lds(V + 8 * kRB * (j + 1)) * xr[j + 1];
+          if (EXACT || j + 2 < pw) a2 += lds(V + 8 * kRB * (j + 2)) * xr[j + 2];
+          if (EXACT || j + 3 < pw) a3 += lds(V + 8 * kRB * (j + 3)) * xr[j + 3];
+        }
+      } else {
+        const int st = 8 * nr;
+#pragma unroll
+        for (int j = 0; j < PWC; j += 4) {
+          if (EXACT || j < pw) a0 += lds(V + st * j) * xr[j];
+          if (EXACT || j + 1 < pw) a1 += lds(V + st * (j + 1)) * xr[j + 1];
+          if (EXACT || j + 2 < pw) a2 += lds(V + st * (j + 2)) * xr[j + 2];
+          if (EXACT || j + 3 < pw) a3 += lds(V + st * (j + 3)) * xr[j + 3];
+        }
+      }
+      ws_at(wso, slot_at(slo, p0 + pw + b0 + lane)) -= (a0 + a1) + (a2 + a3);
+    }
+    R.release();
+  }
+}
+
+/// backward substitution of one panel
+template <int PWC, bool EXACT>
+__device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw, int m, int wso, int lane) {
+  double acc[PWC];
+#pragma unroll
+  for (int j = 0; j < PWC; ++j) acc[j] = 0.0;
+  const int nb = m - p0 - pw;
+  if (nb > 0) {
+    for (int b0 = ((nb - 1) / kRB) * kRB; b0 >= 0; b0 -= kRB) {
+      const int nr = min(kRB, nb - b0);
+      const int V = R.acquire() + 8 * lane;
+      if (lane < nr) {
+        const double xr = ws_at(wso, slot_at(slo, p0 + pw + b0 + lane));
+        if (nr == kRB) {
+#pragma unroll
+          for (int j = 0; j < PWC; ++j)
+            if (EXACT || j < pw) acc[j] += lds(V + 8 * kRB * j) * xr;
+        } else {
+          const int st = 8 * nr;
+#pragma unroll
+          for (int j = 0; j < PWC; ++j)
+            if (EXACT || j < pw) acc[j] += lds(V + st * j) * xr;
+        }
+      }
+      R.release();
+    }
+  }
+  const double t = transpose_reduce<PWC>(acc, lane);
+  const bool mine = lane < pw;
+  double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) - t : 0.0;
+  if (pw > 1) {
+    const int T = R.acquire() + 8 * lane;
+    double lcol[PWC];
+#pragma unroll
+    for (int k = 0; k < PWC; ++k) lcol[k] = (k > lane && (EXACT || k < pw)) ? lds(T + 8 * (k * (k - 1) / 2)) : 0.0;
+    R.release();
+#pragma unroll
+    for (int k = PWC - 1; k >= 1; --k) xi -= lcol[k] * __shfl_sync(0xffffffffu, xi, k);
+  }
+  if (mine) ws_at(wso, slot_at(slo, p0 + lane)) = xi;
+}
+
+__device__ __forceinline__ void fwd_sn(SweepRing& R, int slo, int nc, int m, int wso, int lane) {
+  for (int p0 = 0; p0 < nc; p0 += kPW) {
+    const int pw = min(kPW, nc - p0);
+    if (pw == kPW) fwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 16) fwd_panel<32, false>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 8) fwd_panel<16, false>(R, slo, p0, pw, m, wso, lane);
+    else fwd_panel<8, false>(R, slo, p0, pw, m, wso, lane);
+  }
+}
+
+__device__ __forceinline__ void bwd_sn(SweepRing& R, int slo, int nc, int m, int wso, int lane) {
+  for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
+    const int pw = min(kPW, nc - p0);
+    if (pw == kPW) bwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 16) bwd_panel<32, false>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 8) bwd_panel<16, false>(R, slo, p0, pw, m, wso, lane);
+    else bwd_panel<8, false>(R, slo, p0, pw, m, wso, lane);
+  }
+}
+
+/// mode 0: forward (fold children, eliminate, scale by D, emit contributions)
+/// mode 1: root (forward + scale + backward in one pass)
+/// mode 2: backward (ancestor values final in X)
+__global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode, int ws_max, int smax) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kSweepWarps + wib;
+  if (w >= S.nwork) return;
+  const int wb = wib * SweepSmem::bytes(ws_max, smax);
+  const int wso = wb + SweepSmem::kWs;
+  const int slo = wso + 8 * ws_max;
+  const int p = S.work_prob[w];
+  const TypeDesc T = S.types[S.prob_type[p]];
+  const int t = T.task_base + S.work_task[w];
+  const int c0 = S.task_c0[t], c1 = S.task_c1[t], nct = c1 - c0;
+  const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
+  const int sn0 = S.task_sn0[t], nsn = S.task_sn1[t] - sn0;
+  SweepRing R;
+  R.sbase = smem_u32(g_sm), R.wb = wb, R.nsn = nsn, R.lane = lane;
+  if (lane == 0) {
+    for (int i = 0; i < kUnits; ++i) mbar_init(R.bar(i), 1);
+    fence_mbar_init();
+  }
+  for (int i = lane; i < nsn; i += 32)
+    *reinterpret_cast<int4*>(g_sm + wb + SweepSmem::kMeta + 16 * i) = __ldg(S.sn_meta + T.sn_base + sn0 + i);
+  __syncwarp();
+  R.g = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
+  R.slots = S.slots + T.slot_base;
+  R.issued = R.cons = R.head = R.tail = 0;
+  const int end_bytes = S.task_lbytes[t];
+  for (int r = 0; r < S.nrhs; ++r) {
+    double* X = S.X + S.prob_x[p] + r * S.x_stride;
+    double* CBp = S.CB + S.prob_cb[p] + r * S.cb_stride;
+    if (mode != 2) {
+      R.start(true, end_bytes);
+      R.pump();  // first units in flight while the inputs are gathered
+      const int* fp = S.fold_ptr + T.fold_base;
+      const int* fi = S.fold_idx + T.foldidx_base;
+      for (int i = lane; i < nct; i += 32) {
+        double v = X[c0 + i];
+        for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];  // children, fixed order
+        ws_at(wso, i) = v;
+      }
+      for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = 0.0;
+      for (int k = 0; k < nsn; ++k) {
+        const int4 mt = meta_at(wb, k);
+        take_slots(R, slo, mt.y);
+        fwd_sn(R, slo, mt.x, mt.y, wso, lane);
+      }
+      __syncwarp();
+      const double* Dp = S.D + S.prob_x[p] + c0;
+      for (int i = lane; i < nct; i += 32) ws_at(wso, i) /= Dp[i];
+      if (mode == 0)
+        for (int i = lane; i < cbl; i += 32) CBp[cbo + i] = ws_at(wso, nct + i);
+      __syncwarp();
+    }
+    if (mode != 0) {
+      R.start(false, end_bytes);
+      R.pump();
+      if (mode == 2) {
+        const int* cbr = S.cb_rows + T.cb_base + cbo;
+        for (int i = lane; i < nct; i += 32) ws_at(wso, i) = X[c0 + i];
+        for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = X[cbr[i]];
+      }
+      for (int k = nsn - 1; k >= 0; --k) {
+        const int4 mt = meta_at(wb, k);
+        take_slots(R, slo, mt.y);
+        bwd_sn(R, slo, mt.x, mt.y, wso, lane);
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < nct; i += 32) X[c0 + i] = ws_at(wso, i);
+    __syncwarp();
+  }
+}
+
+}  // namespace dev
+}  // namespace pf

@@ -16,6 +16,7 @@
 #include <functional>
 
 #include "pf_common.hpp"
+#include "pf_layout.hpp"
 
 namespace pf {
 
@@ -260,15 +261,15 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
   std::vector<std::vector<int>> level_roots, level_tops;
   bool leaf_level = false;
   {
-    std::vector<long long> W(ns, 0), Cc(ns, 0);
+    std::vector<long long> W(ns, 0), Cc(ns, 0), Nsn(ns, 1);
     for (int s = 0; s < ns; ++s) W[s] += w[s], Cc[s] += s0[s + 1] - s0[s];
     for (int s = 0; s < ns; ++s)
-      if (sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s];
+      if (sparent[s] >= 0) W[sparent[s]] += W[s], Cc[sparent[s]] += Cc[s], Nsn[sparent[s]] += Nsn[s];
     std::vector<int> picked;
     if (task_cap > 0) {
       std::function<void(int)> pick = [&](int s) {
         const long long ws = Cc[s] + (long long)st[s].size() - (s0[s + 1] - s0[s]);
-        if (W[s] <= task_cap && ws <= ws_cap) {
+        if (W[s] <= task_cap && ws <= ws_cap && Nsn[s] <= kMaxTaskSn) {
           picked.push_back(s);
           return;
         }
@@ -290,7 +291,7 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     }
     // upper part: chains (a supernode with exactly one remaining child joins
     // its child's task), levelled by height; tasks of one level are independent
-    std::vector<int> task_of(ns, -1), rem_child(ns, 0), tlevel, tbottom, ttop;
+    std::vector<int> task_of(ns, -1), rem_child(ns, 0), tlevel, tbottom, ttop, tlen;
     for (int s = 0; s < ns; ++s)
       if (!removed[s] && sparent[s] >= 0) rem_child[sparent[s]]++;
     for (int s = 0; s < ns; ++s) {
@@ -299,9 +300,10 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
       if (rem_child[s] == 1)
         for (int ch : schild[s])
           if (!removed[ch]) only = ch;
-      if (only >= 0) {
+      if (only >= 0 && tlen[task_of[only]] < kMaxTaskSn) {
         task_of[s] = task_of[only];
         ttop[task_of[s]] = s;
+        tlen[task_of[s]]++;
       } else {
         int lv = 0;
         for (int ch : schild[s])
@@ -310,6 +312,7 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
         tlevel.push_back(lv);
         tbottom.push_back(s);
         ttop.push_back(s);
+        tlen.push_back(1);
       }
     }
     int maxlv = -1;
@@ -433,6 +436,22 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
           F.slot[q] = (c1 - c0) + int(std::lower_bound(cb.begin(), cb.end(), r) - cb.begin());
         }
       }
+  }
+  // factor values: a task's supernodes are contiguous and every task starts
+  // at an even offset (16-byte aligned streams for the bulk copies)
+  {
+    std::vector<char> tstart(ns, 0);
+    long long cover = 0;
+    for (int t = 0; t < F.ntask; ++t) tstart[F.task_sn0[t]] = 1, cover += F.task_sn1[t] - F.task_sn0[t];
+    if (cover != ns) fail(kInternal, "symbolic: tasks do not partition the supernodes");
+    long long v = 0;
+    for (int k = 0; k < ns; ++k) {
+      if (tstart[k]) v = (v + 1) & ~1LL;
+      F.sn_valoff[k] = v;
+      v += sn_size(F.sn_ncol[k], F.sn_nrow[k]);
+    }
+    F.sn_valoff[ns] = v;
+    F.nval = (v + 1) & ~1LL;
   }
   // every contribution row must belong to a task of a strictly higher level
   std::vector<int> col_level(n, -1);
@@ -768,6 +787,20 @@ inline AScatter build_ascatter(const SymFactor& F, const FrontMaps& M, const Csr
     S.ptr[k + 1] = (int)S.kidx.size();
   }
   return S;
+}
+
+/// Convert factor values from the packed column-major trapezoid (factor_host)
+/// to the panel-blocked sweep layout (pf_layout.hpp), in place.
+inline void to_blocked(const SymFactor& F, std::vector<double>& L) {
+  std::vector<double> out(L.size(), 0.0);
+  for (int k = 0; k < F.nsn; ++k) {
+    const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+    const long long o = F.sn_valoff[k];
+    long long q = o;
+    for (int j = 0; j < nc; ++j)
+      for (int i = j + 1; i < m; ++i) out[o + blk_off(nc, m, i, j)] = L[q++];
+  }
+  L.swap(out);
 }
 
 }  // namespace pf
