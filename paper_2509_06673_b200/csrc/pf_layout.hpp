@@ -23,7 +23,7 @@
 
 namespace pf {
 
-constexpr int kPW = 32;         // panel width (columns); even
+constexpr int kPW = 16;         // panel width (columns); even
 constexpr int kRB = 32;         // rows per row block (one per lane)
 constexpr int kMaxTaskSn = 64;  // supernodes per sweep task (task metadata lives in shared memory)
 

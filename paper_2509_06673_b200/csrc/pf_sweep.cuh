@@ -61,7 +61,7 @@ __device__ __forceinline__ void mbar_wait(unsigned b, unsigned parity) {
       : "memory");
 }
 
-constexpr int kRingBytes = 16384;  // per warp; >= the largest unit (kRB*kPW*8)
+constexpr int kRingBytes = 8192;   // per warp; >= the largest unit (kRB*kPW*8)
 constexpr int kUnits = 8;          // units in flight per warp (mbarriers)
 constexpr int kSweepWarps = 4;     // warps per CTA
 
@@ -299,8 +299,8 @@ __device__ __forceinline__ void fwd_sn(SweepRing& R, int slo, int nc, int m, int
   for (int p0 = 0; p0 < nc; p0 += kPW) {
     const int pw = min(kPW, nc - p0);
     if (pw == kPW) fwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
-    else if (pw > 16) fwd_panel<32, false>(R, slo, p0, pw, m, wso, lane);
-    else if (pw > 8) fwd_panel<16, false>(R, slo, p0, pw, m, wso, lane);
+    else if (kPW > 16 && pw > 16) fwd_panel<kPW, false>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 8) fwd_panel<(kPW < 16 ? kPW : 16), false>(R, slo, p0, pw, m, wso, lane);
     else fwd_panel<8, false>(R, slo, p0, pw, m, wso, lane);
   }
 }
@@ -309,8 +309,8 @@ __device__ __forceinline__ void bwd_sn(SweepRing& R, int slo, int nc, int m, int
   for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
     const int pw = min(kPW, nc - p0);
     if (pw == kPW) bwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
-    else if (pw > 16) bwd_panel<32, false>(R, slo, p0, pw, m, wso, lane);
-    else if (pw > 8) bwd_panel<16, false>(R, slo, p0, pw, m, wso, lane);
+    else if (kPW > 16 && pw > 16) bwd_panel<kPW, false>(R, slo, p0, pw, m, wso, lane);
+    else if (pw > 8) bwd_panel<(kPW < 16 ? kPW : 16), false>(R, slo, p0, pw, m, wso, lane);
     else bwd_panel<8, false>(R, slo, p0, pw, m, wso, lane);
   }
 }
