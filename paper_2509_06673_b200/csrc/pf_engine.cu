@@ -118,7 +118,8 @@ struct SolveSystem {
   DevBuf<int4> d_meta;
   DevBuf<uint16_t> d_slots16;
   DevBuf<long long> d_tlbeg;
-  DevBuf<int> d_tlbytes;
+  DevBuf<unsigned long long> d_udesc;
+  DevBuf<int> d_tuf, d_tnuf, d_tub, d_tnub;
   int smax = 8;  // max supernode row count (padded to 8)
   int nrhs_alloc = 1;
   long long nnzL = 0;
@@ -129,8 +130,10 @@ struct SolveSystem {
     prob_type = ptype;
     nrhs_alloc = nrhs;
     std::vector<dev::TypeDesc> td(types.size());
-    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm, tlbytes;
+    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm, tuf, tnuf, tub,
+        tnub;
     std::vector<long long> sn_rowoff, sn_valoff, type_perm_off, tlbeg;
+    std::vector<unsigned long long> udesc;
     std::vector<int4> meta;
     std::vector<uint16_t> slots16;
     smax = 8;
@@ -149,6 +152,8 @@ struct SolveSystem {
       T.fold_base = (long long)fptr.size();
       T.foldidx_base = (long long)fidx.size();
       T.slot_base = (long long)slots16.size();
+      T.udesc_base = (long long)udesc.size();
+      std::vector<long long> sn_slot(F.nsn);
       for (int s = 0; s < F.nsn; ++s) {
         sn_col0.push_back(F.sn_col0[s]), sn_ncol.push_back(F.sn_ncol[s]), sn_nrow.push_back(F.sn_nrow[s]);
         sn_rowoff.push_back(F.sn_rowoff[s]), sn_valoff.push_back(F.sn_valoff[s]);
@@ -157,7 +162,8 @@ struct SolveSystem {
         if (ts < 0) fail(kInternal, "supernode without a sweep task");
         const long long vrel = 8 * (F.sn_valoff[s] - F.sn_valoff[ts]);
         if (vrel > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
-        meta.push_back(make_int4(F.sn_ncol[s], m, (int)((long long)slots16.size() - T.slot_base), (int)vrel));
+        sn_slot[s] = (long long)slots16.size() - T.slot_base;
+        meta.push_back(make_int4(F.sn_ncol[s], m, (int)sn_slot[s], (int)vrel));
         for (int i = 0; i < m; ++i) {
           const int v = F.slot[F.sn_rowoff[s] + i];
           if (v < 0 || v > 65535) fail(kInternal, "sweep slot out of uint16 range");
@@ -172,11 +178,46 @@ struct SolveSystem {
         t0.push_back(F.task_sn0[t]), t1.push_back(F.task_sn1[t]);
         c0.push_back(F.task_c0[t]), c1.push_back(F.task_c1[t]);
         cbo.push_back(F.task_cboff[t]), cbl.push_back(F.task_cblen[t]);
-        long long nb = 0;
         if (F.task_sn1[t] - F.task_sn0[t] > kMaxTaskSn) fail(kInternal, "sweep task exceeds kMaxTaskSn supernodes");
-        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) nb += 8 * sn_size(F.sn_ncol[k], F.sn_nrow[k]);
-        if (nb > INT32_MAX || (F.sn_valoff[F.task_sn0[t]] & 1)) fail(kInternal, "task value stream layout");
-        tlbeg.push_back(F.sn_valoff[F.task_sn0[t]]), tlbytes.push_back((int)nb);
+        if (F.sn_valoff[F.task_sn0[t]] & 1) fail(kInternal, "task value stream layout");
+        tlbeg.push_back(F.sn_valoff[F.task_sn0[t]]);
+        // unit descriptors in the sweep kernel's consumption order (pf_sweep.cuh)
+        const long long ub = T.udesc_base;
+        tuf.push_back((int)((long long)udesc.size() - ub));
+        long long pos = 0;
+        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
+          const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+          udesc.push_back(dev::unit_desc(2 * sn_slot[k], ((m + 7) & ~7) * 2, dev::kSrcSlots));
+          for (int p0 = 0; p0 < nc; p0 += kPW) {
+            const int pw = std::min(kPW, nc - p0), nb = m - p0 - pw;
+            if (tri_pad(pw)) udesc.push_back(dev::unit_desc(pos, 8 * tri_pad(pw), dev::kSrcValues)), pos += 8 * tri_pad(pw);
+            for (int b0 = 0; b0 < nb; b0 += kRB) {
+              const int sz = 8 * even_up(std::min(kRB, nb - b0) * pw);
+              udesc.push_back(dev::unit_desc(pos, sz, dev::kSrcValues)), pos += sz;
+            }
+          }
+        }
+        const int tc0 = F.task_c0[t], tnc = F.task_c1[t] - tc0;
+        udesc.push_back(dev::unit_desc(8LL * (tc0 & ~1), 8 * even_up((tc0 & 1) + tnc), dev::kSrcDiag));
+        tnuf.push_back((int)((long long)udesc.size() - ub) - tuf.back());
+        if (pos > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
+        tub.push_back((int)((long long)udesc.size() - ub));
+        for (int k = F.task_sn1[t] - 1; k >= F.task_sn0[t]; --k) {
+          const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+          udesc.push_back(dev::unit_desc(2 * sn_slot[k], ((m + 7) & ~7) * 2, dev::kSrcSlots));
+          for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
+            const int pw = std::min(kPW, nc - p0), nb = m - p0 - pw;
+            if (nb > 0)
+              for (int b0 = ((nb - 1) / kRB) * kRB; b0 >= 0; b0 -= kRB) {
+                const int sz = 8 * even_up(std::min(kRB, nb - b0) * pw);
+                pos -= sz;
+                udesc.push_back(dev::unit_desc(pos, sz, dev::kSrcValues));
+              }
+            if (tri_pad(pw)) pos -= 8 * tri_pad(pw), udesc.push_back(dev::unit_desc(pos, 8 * tri_pad(pw), dev::kSrcValues));
+          }
+        }
+        if (pos != 0) fail(kInternal, "sweep unit descriptors do not cover the task stream");
+        tnub.push_back((int)((long long)udesc.size() - ub) - tub.back());
         const int gl = glevel(F, F.task_level[t]);
         const int ws = (F.task_c1[t] - F.task_c0[t]) + F.task_cblen[t];
         level_ws[gl] = std::max(level_ws[gl], ws);
@@ -197,6 +238,7 @@ struct SolveSystem {
     for (int p = 0; p < np; ++p) {
       const SymFactor& F = *types[ptype[p]];
       total_L = (total_L + 1) & ~1LL;  // 16-byte aligned value streams
+      total_x = (total_x + 1) & ~1LL;  // 16-byte aligned pivot rows for the bulk copies
       prob_x[p] = total_x, prob_lval[p] = total_L, prob_cb[p] = total_cb;
       total_x += F.n, total_L += F.nval, total_cb += (long long)F.cb_rows.size();
       nnzL += F.nval;
@@ -225,9 +267,10 @@ struct SolveSystem {
     d_cbrows.upload(cbrows), d_fold_ptr.upload(fptr), d_fold_idx.upload(fidx);
     d_prob_type.upload(ptype), d_prob_x.upload(prob_x), d_prob_lval.upload(prob_lval), d_prob_cb.upload(prob_cb);
     d_perm.upload(perm), d_prob_perm.upload(pperm), d_prob_n.upload(pn);
-    d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_tlbytes.upload(tlbytes);
-    L.alloc(total_L + 4);  // bulk copies round the last stream up to 16 bytes
-    D.alloc(total_x);
+    d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_udesc.upload(udesc);
+    d_tuf.upload(tuf), d_tnuf.upload(tnuf), d_tub.upload(tub), d_tnub.upload(tnub);
+    L.alloc(total_L + 4);
+    D.alloc(total_x + 2);  // the pivot unit of the last task may round up past the end
     X.alloc(total_x * nrhs);
     CB.alloc(std::max<long long>(1, total_cb * nrhs));
   }
@@ -255,7 +298,8 @@ struct SolveSystem {
     S.task_sn0 = d_t0.p, S.task_sn1 = d_t1.p, S.task_c0 = d_c0.p, S.task_c1 = d_c1.p;
     S.task_cboff = d_cbo.p, S.task_cblen = d_cbl.p, S.cb_rows = d_cbrows.p;
     S.fold_ptr = d_fold_ptr.p, S.fold_idx = d_fold_idx.p;
-    S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.task_lbytes = d_tlbytes.p;
+    S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.udesc = d_udesc.p;
+    S.task_uf = d_tuf.p, S.task_nuf = d_tnuf.p, S.task_ub = d_tub.p, S.task_nub = d_tnub.p;
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
     S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p;

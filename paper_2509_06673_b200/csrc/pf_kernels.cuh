@@ -24,6 +24,7 @@ struct TypeDesc {
   long long row_base, cb_base;       // into slot / cb_rows
   long long fold_base, foldidx_base; // into fold_ptr (n+1 per type) / fold_idx
   long long slot_base;               // into slots (uint16, per-supernode lists padded to 8)
+  long long udesc_base;              // into udesc (sweep unit descriptors)
 };
 
 struct SolveSet {
@@ -38,7 +39,8 @@ struct SolveSet {
   const int4* sn_meta;                     // per supernode: ncol, nrow, slot offset (type-relative), 0
   const uint16_t* slots;                   // per supernode row -> workspace slot
   const long long* task_lbeg;              // task value stream start (type-relative, even)
-  const int* task_lbytes;                  // task value stream length (bytes)
+  const unsigned long long* udesc;         // sweep unit descriptors (pf_sweep.cuh)
+  const int *task_uf, *task_nuf, *task_ub, *task_nub;  // per task: forward / backward lists
   // problems
   int nprob;
   const int* prob_type;

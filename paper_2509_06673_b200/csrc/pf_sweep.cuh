@@ -65,138 +65,89 @@ constexpr int kRingBytes = 8192;   // per warp; >= the largest unit (kRB*kPW*8)
 constexpr int kUnits = 8;          // units in flight per warp (mbarriers)
 constexpr int kSweepWarps = 4;     // warps per CTA
 
-/// Per-warp shared memory: ring | barriers | unit table | task meta | ws | slots.
+/// Per-warp shared memory: ring | barriers | task meta | ws | slots.
 struct SweepSmem {
   static constexpr int kBar = kRingBytes;
-  static constexpr int kUnit = kBar + 8 * kUnits;      // int per unit slot: ring offset
-  static constexpr int kMeta = kUnit + 8 * kUnits;     // int4 per task supernode
+  static constexpr int kMeta = kBar + 8 * kUnits;      // int4 per task supernode
   static constexpr int kWs = kMeta + 16 * kMaxTaskSn;  // ws doubles
   __host__ __device__ static int bytes(int ws_max, int smax) { return kWs + 8 * ws_max + ((2 * smax + 15) & ~15); }
 };
+
+/// unit descriptor (host-built, in consumption order): byte offset | size << 32 | source << 48
+enum : int { kSrcValues = 0, kSrcSlots = 1, kSrcDiag = 2 };
+__host__ __device__ inline unsigned long long unit_desc(long long off, int bytes, int src) {
+  return (unsigned long long)(unsigned)off | ((unsigned long long)bytes << 32) | ((unsigned long long)src << 48);
+}
 
 __device__ __forceinline__ double lds(int byte) { return *reinterpret_cast<const double*>(g_sm + byte); }
 __device__ __forceinline__ int4 meta_at(int wb, int k) {
   return *reinterpret_cast<const int4*>(g_sm + wb + SweepSmem::kMeta + 16 * k);
 }
 
-/// Producer + consumer state of one warp (warp-uniform registers).
+/// Producer + consumer state of one warp (warp-uniform registers).  The
+/// producer walks a host-built descriptor list (two 32-entry register
+/// windows, the next one prefetched); the consumer derives the same unit
+/// sizes from its own loop structure and mirrors the ring placement.
 struct SweepRing {
-  int wb;                   // per-warp region (offset in g_sm)
-  unsigned sbase;           // shared address of g_sm
-  const unsigned char* g;   // task value stream (16-byte aligned)
-  const uint16_t* slots;    // type slot table
-  int nsn;
-  bool fwd;
-  // producer cursor: supernode k, panel p (width pw, rows below nb), block b
-  // (-2 slot list, -1 triangle), stream position pos of the next value unit
-  int k, p, pw, nb, b, m, nc, pos;
-  bool done;
-  int issued, cons, head, tail;
+  int wb;                      // per-warp region (offset in g_sm)
+  unsigned sbase;              // shared address of g_sm
+  const unsigned char *sv, *ss, *sd;  // sources: values stream, slot table, pivots
+  const unsigned long long* list;
+  int nu, li, wbase;           // list length, next list entry to issue, window base
+  unsigned long long wcur, wnxt;
+  int issued, cons, head, tail, chead;
   int lane;
 
   __device__ __forceinline__ unsigned bar(int u) const { return sbase + wb + SweepSmem::kBar + 8 * (u & (kUnits - 1)); }
-  __device__ __forceinline__ int& utab(int u) const {
-    return *reinterpret_cast<int*>(g_sm + wb + SweepSmem::kUnit + 8 * (u & (kUnits - 1)));
-  }
 
-  __device__ __forceinline__ void enter_sn() {  // producer enters supernode k
-    const int4 mt = meta_at(wb, k);
-    nc = mt.x, m = mt.y, b = -2;
-  }
-  __device__ __forceinline__ void start(bool forward, int end_bytes) {
-    fwd = forward, done = nsn == 0;
-    k = forward ? 0 : nsn - 1;
-    pos = forward ? 0 : end_bytes;
-    if (!done) enter_sn();
-  }
-  __device__ __forceinline__ void set_panel(int pp) {
-    p = pp;
-    const int p0 = pp * kPW;
-    pw = min(kPW, nc - p0), nb = m - p0 - pw;
-  }
-  /// advance the producer cursor past the current unit
-  __device__ __forceinline__ void advance() {
-    if (fwd) {
-      if (b == -2) {
-        set_panel(0), b = -1;
-      } else if (b + 1 < ((nb + kRB - 1) >> 5)) {
-        ++b;
-      } else if ((p + 1) * kPW < nc) {
-        set_panel(p + 1), b = -1;
-      } else if (k + 1 < nsn) {
-        ++k, enter_sn();
-      } else {
-        done = true;
-      }
-    } else {
-      if (b == -2) {
-        set_panel((nc - 1) / kPW), b = ((nb + kRB - 1) >> 5) - 1;
-      } else if (b >= 0) {
-        --b;
-      } else if (p > 0) {
-        set_panel(p - 1), b = ((nb + kRB - 1) >> 5) - 1;
-      } else if (k > 0) {
-        --k, enter_sn();
-      } else {
-        done = true;
-      }
-    }
+  __device__ __forceinline__ void start(const unsigned long long* l, int n) {
+    list = l, nu = n, li = 0, wbase = 0;
+    wcur = lane < n ? __ldg(l + lane) : 0ull;
+    wnxt = 32 + lane < n ? __ldg(l + 32 + lane) : 0ull;
   }
   /// issue units ahead while barriers and ring space allow
   __device__ __forceinline__ void pump() {
-    while (!done && issued - cons < kUnits) {
-      int sz;
-      const unsigned char* src;
-      if (b == -2) {
-        sz = ((m + 7) & ~7) * 2;
-        src = reinterpret_cast<const unsigned char*>(slots + meta_at(wb, k).z);
-      } else {
-        sz = b == -1 ? 8 * tri_pad(pw) : 8 * even_up(min(kRB, nb - kRB * b) * pw);
-        if (sz == 0) {  // pw == 1: no triangle unit
-          advance();
-          continue;
-        }
-        if (fwd) {
-          src = g + pos;
-        } else {
-          src = g + pos - sz;
-        }
+    while (li < nu && issued - cons < kUnits) {
+      if (li - wbase >= 32) {
+        wcur = wnxt, wbase += 32;
+        wnxt = wbase + 32 + lane < nu ? __ldg(list + wbase + 32 + lane) : 0ull;
       }
-      unsigned h = (unsigned)head;
-      if ((h % kRingBytes) + sz > kRingBytes) h += kRingBytes - h % kRingBytes;
-      if ((int)(h - (unsigned)tail) + sz > kRingBytes) break;
-      const int off = (int)(h % kRingBytes);
+      const unsigned long long d = __shfl_sync(0xffffffffu, wcur, li - wbase);
+      const int sz = (int)((d >> 32) & 0xffffu);
+      int h = head;
+      if ((h & (kRingBytes - 1)) + sz > kRingBytes) h += kRingBytes - (h & (kRingBytes - 1));
+      if (h + sz - tail > kRingBytes) break;
       if (lane == 0) {
-        *reinterpret_cast<int2*>(g_sm + wb + SweepSmem::kUnit + 8 * (issued & (kUnits - 1))) = make_int2(off, (int)h);
         const unsigned bb = bar(issued);
         fence_proxy_async();
         mbar_expect_tx(bb, (unsigned)sz);
-        bulk_g2s(sbase + wb + off, src, (unsigned)sz, bb);
+        const int kind = (int)(d >> 48);
+        const unsigned char* from = kind == kSrcValues ? sv : kind == kSrcSlots ? ss : sd;
+        bulk_g2s(sbase + wb + (h & (kRingBytes - 1)), from + (unsigned)d, (unsigned)sz, bb);
       }
-      if (b != -2) pos += fwd ? sz : -sz;
-      head = (int)h + sz;
-      ++issued;
-      advance();
+      head = h + sz;
+      ++issued, ++li;
     }
   }
-  /// offset (in g_sm) of the next unit of the consumer's sequence, resident
-  __device__ __forceinline__ int acquire() {
+  /// offset (in g_sm) of the consumer's next unit (sz bytes), once resident
+  __device__ __forceinline__ int acquire(int sz) {
     pump();
-    __syncwarp();
+    int h = chead;
+    if ((h & (kRingBytes - 1)) + sz > kRingBytes) h += kRingBytes - (h & (kRingBytes - 1));
+    chead = h + sz;
     mbar_wait(bar(cons), (unsigned)(cons / kUnits) & 1u);
-    return wb + utab(cons);
+    return wb + (h & (kRingBytes - 1));
   }
   __device__ __forceinline__ void release() {
     __syncwarp();
     ++cons;
-    tail = cons < issued ? *reinterpret_cast<const int*>(g_sm + wb + SweepSmem::kUnit + 8 * (cons & (kUnits - 1)) + 4)
-                         : head;
+    tail = chead;
   }
 };
 
 /// copy the supernode's slot list out of the ring
 __device__ __forceinline__ void take_slots(SweepRing& R, int slo, int m) {
-  const int src = R.acquire();
+  const int src = R.acquire(((m + 7) & ~7) * 2);
   for (int i = R.lane; i < (m + 7) >> 3; i += 32)
     *reinterpret_cast<int4*>(g_sm + slo + 16 * i) = *reinterpret_cast<const int4*>(g_sm + src + 16 * i);
   R.release();
@@ -211,7 +162,7 @@ __device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw,
   const bool mine = lane < pw;
   double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) : 0.0;
   if (pw > 1) {
-    const int T = R.acquire() + 8 * (lane * (lane - 1) / 2);
+    const int T = R.acquire(8 * tri_pad(pw)) + 8 * (lane * (lane - 1) / 2);
     double lrow[PWC];
 #pragma unroll
     for (int j = 0; j < PWC; ++j) lrow[j] = (lane > j && mine) ? lds(T + 8 * j) : 0.0;
@@ -226,7 +177,7 @@ __device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw,
   const int nb = m - p0 - pw;
   for (int b0 = 0; b0 < nb; b0 += kRB) {
     const int nr = min(kRB, nb - b0);
-    const int V = R.acquire() + 8 * lane;
+    const int V = R.acquire(8 * even_up(nr * pw)) + 8 * lane;
     if (lane < nr) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       if (nr == kRB) {
@@ -263,7 +214,7 @@ __device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw,
   if (nb > 0) {
     for (int b0 = ((nb - 1) / kRB) * kRB; b0 >= 0; b0 -= kRB) {
       const int nr = min(kRB, nb - b0);
-      const int V = R.acquire() + 8 * lane;
+      const int V = R.acquire(8 * even_up(nr * pw)) + 8 * lane;
       if (lane < nr) {
         const double xr = ws_at(wso, slot_at(slo, p0 + pw + b0 + lane));
         if (nr == kRB) {
@@ -284,7 +235,7 @@ __device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw,
   const bool mine = lane < pw;
   double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) - t : 0.0;
   if (pw > 1) {
-    const int T = R.acquire() + 8 * lane;
+    const int T = R.acquire(8 * tri_pad(pw)) + 8 * lane;
     double lcol[PWC];
 #pragma unroll
     for (int k = 0; k < PWC; ++k) lcol[k] = (k > lane && (EXACT || k < pw)) ? lds(T + 8 * (k * (k - 1) / 2)) : 0.0;
@@ -332,7 +283,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode
   const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
   const int sn0 = S.task_sn0[t], nsn = S.task_sn1[t] - sn0;
   SweepRing R;
-  R.sbase = smem_u32(g_sm), R.wb = wb, R.nsn = nsn, R.lane = lane;
+  R.sbase = smem_u32(g_sm), R.wb = wb, R.lane = lane;
   if (lane == 0) {
     for (int i = 0; i < kUnits; ++i) mbar_init(R.bar(i), 1);
     fence_mbar_init();
@@ -340,15 +291,16 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode
   for (int i = lane; i < nsn; i += 32)
     *reinterpret_cast<int4*>(g_sm + wb + SweepSmem::kMeta + 16 * i) = __ldg(S.sn_meta + T.sn_base + sn0 + i);
   __syncwarp();
-  R.g = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
-  R.slots = S.slots + T.slot_base;
-  R.issued = R.cons = R.head = R.tail = 0;
-  const int end_bytes = S.task_lbytes[t];
+  R.sv = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
+  R.ss = reinterpret_cast<const unsigned char*>(S.slots + T.slot_base);
+  R.sd = reinterpret_cast<const unsigned char*>(S.D + S.prob_x[p]);
+  R.issued = R.cons = R.head = R.tail = R.chead = 0;
+  const unsigned long long* ul = S.udesc + T.udesc_base;
   for (int r = 0; r < S.nrhs; ++r) {
     double* X = S.X + S.prob_x[p] + r * S.x_stride;
     double* CBp = S.CB + S.prob_cb[p] + r * S.cb_stride;
     if (mode != 2) {
-      R.start(true, end_bytes);
+      R.start(ul + S.task_uf[t], S.task_nuf[t]);
       R.pump();  // first units in flight while the inputs are gathered
       const int* fp = S.fold_ptr + T.fold_base;
       const int* fi = S.fold_idx + T.foldidx_base;
@@ -363,21 +315,26 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode
         take_slots(R, slo, mt.y);
         fwd_sn(R, slo, mt.x, mt.y, wso, lane);
       }
-      __syncwarp();
-      const double* Dp = S.D + S.prob_x[p] + c0;
-      for (int i = lane; i < nct; i += 32) ws_at(wso, i) /= Dp[i];
+      {
+        // pivots of the task's columns: the last unit of the forward list
+        const int sh = c0 & 1;
+        const int dof = R.acquire(8 * even_up(sh + nct)) + 8 * sh;
+        for (int i = lane; i < nct; i += 32) ws_at(wso, i) /= lds(dof + 8 * i);
+        R.release();
+      }
       if (mode == 0)
         for (int i = lane; i < cbl; i += 32) CBp[cbo + i] = ws_at(wso, nct + i);
       __syncwarp();
     }
     if (mode != 0) {
-      R.start(false, end_bytes);
+      R.start(ul + S.task_ub[t], S.task_nub[t]);
       R.pump();
       if (mode == 2) {
         const int* cbr = S.cb_rows + T.cb_base + cbo;
         for (int i = lane; i < nct; i += 32) ws_at(wso, i) = X[c0 + i];
         for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = X[cbr[i]];
       }
+      __syncwarp();
       for (int k = nsn - 1; k >= 0; --k) {
         const int4 mt = meta_at(wb, k);
         take_slots(R, slo, mt.y);
