@@ -94,6 +94,29 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
     for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[blk_off(nc, m, i, j)] = Fk[i + (long long)j * m];
   double* D = S.D + S.prob_x[p] + S.col0[sk];
   for (int j = threadIdx.x; j < nc; j += blockDim.x) D[j] = Fk[j + (long long)j * m];
+  __syncthreads();
+  // the sweep's triangle units hold the inverse of each panel's unit-lower
+  // diagonal block: lane j forms column j of Linv by forward substitution
+  const int npan = (nc + kPW - 1) / kPW;
+  for (int q = warp; q < npan; q += nw) {
+    const int p0 = q * kPW, pw = min(kPW, nc - p0);
+    double xc[kPW];
+#pragma unroll
+    for (int i = 0; i < kPW; ++i) {
+      double v = i == lane ? 1.0 : 0.0;
+      if (i > lane && i < pw) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPW; ++k)
+          if (k >= lane && k < i) acc += Fk[(p0 + i) + (long long)(p0 + k) * m] * xc[k];
+        v = -acc;
+      }
+      xc[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < kPW; ++i)
+      if (i > lane && i < pw) L[blk_off(nc, m, p0 + i, p0 + lane)] = xc[i];
+  }
 }
 
 /// Seeded residual check (feti.hpp:28-36) on the device: per problem p,

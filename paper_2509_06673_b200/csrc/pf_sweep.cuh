@@ -156,24 +156,31 @@ __device__ __forceinline__ void take_slots(SweepRing& R, int slo, int m) {
 __device__ __forceinline__ int slot_at(int slo, int r) { return *reinterpret_cast<const uint16_t*>(g_sm + slo + 2 * r); }
 __device__ __forceinline__ double& ws_at(int wso, int s) { return *reinterpret_cast<double*>(g_sm + wso + 8 * s); }
 
-/// forward elimination of one panel; PWC >= pw compile-time bound, EXACT: pw == PWC
+/// Forward elimination of one panel; PWC >= pw compile-time bound, EXACT:
+/// pw == PWC.  The triangle unit holds the INVERSE of the panel's unit-lower
+/// diagonal block (pf_factor.cuh), so x = Linv b is a dot product per lane
+/// with no sequential dependency; the panel's own columns occupy consecutive
+/// workspace slots, so b and x are broadcast through shared memory.
 template <int PWC, bool EXACT>
 __device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw, int m, int wso, int lane) {
   const bool mine = lane < pw;
-  double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) : 0.0;
+  const int wp = wso + 8 * slot_at(slo, p0);
   if (pw > 1) {
     const int T = R.acquire(8 * tri_pad(pw)) + 8 * (lane * (lane - 1) / 2);
-    double lrow[PWC];
+    double lrow[PWC - 1];
 #pragma unroll
-    for (int j = 0; j < PWC; ++j) lrow[j] = (lane > j && mine) ? lds(T + 8 * j) : 0.0;
+    for (int j = 0; j < PWC - 1; ++j) lrow[j] = (lane > j && mine) ? lds(T + 8 * j) : 0.0;
     R.release();
+    double a[4] = {mine ? lds(wp + 8 * lane) : 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < PWC - 1; ++j) xi -= lrow[j] * __shfl_sync(0xffffffffu, xi, j);
+    for (int j = 0; j < PWC - 1; ++j) a[j & 3] += lrow[j] * ((EXACT || j < pw) ? lds(wp + 8 * j) : 0.0);
+    __syncwarp();
+    if (mine) *reinterpret_cast<double*>(g_sm + wp + 8 * lane) = (a[0] + a[1]) + (a[2] + a[3]);
+    __syncwarp();
   }
-  if (mine) ws_at(wso, slot_at(slo, p0 + lane)) = xi;
   double xr[PWC];
 #pragma unroll
-  for (int j = 0; j < PWC; ++j) xr[j] = __shfl_sync(0xffffffffu, xi, j);
+  for (int j = 0; j < PWC; ++j) xr[j] = (EXACT || j < pw) ? lds(wp + 8 * j) : 0.0;
   const int nb = m - p0 - pw;
   for (int b0 = 0; b0 < nb; b0 += kRB) {
     const int nr = min(kRB, nb - b0);
@@ -233,17 +240,23 @@ __device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw,
   }
   const double t = transpose_reduce<PWC>(acc, lane);
   const bool mine = lane < pw;
-  double xi = mine ? ws_at(wso, slot_at(slo, p0 + lane)) - t : 0.0;
+  const int wp = wso + 8 * slot_at(slo, p0);
+  if (mine) *reinterpret_cast<double*>(g_sm + wp + 8 * lane) -= t;
   if (pw > 1) {
+    // x = Linv^T c: lane i needs column i of Linv and every c_k, k > i
     const int T = R.acquire(8 * tri_pad(pw)) + 8 * lane;
     double lcol[PWC];
 #pragma unroll
-    for (int k = 0; k < PWC; ++k) lcol[k] = (k > lane && (EXACT || k < pw)) ? lds(T + 8 * (k * (k - 1) / 2)) : 0.0;
+    for (int k = 1; k < PWC; ++k) lcol[k] = (k > lane && (EXACT || k < pw)) ? lds(T + 8 * (k * (k - 1) / 2)) : 0.0;
     R.release();
+    __syncwarp();
+    double a[4] = {mine ? lds(wp + 8 * lane) : 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = PWC - 1; k >= 1; --k) xi -= lcol[k] * __shfl_sync(0xffffffffu, xi, k);
+    for (int k = 1; k < PWC; ++k) a[k & 3] += lcol[k] * ((EXACT || k < pw) ? lds(wp + 8 * k) : 0.0);
+    __syncwarp();
+    if (mine) *reinterpret_cast<double*>(g_sm + wp + 8 * lane) = (a[0] + a[1]) + (a[2] + a[3]);
   }
-  if (mine) ws_at(wso, slot_at(slo, p0 + lane)) = xi;
+  __syncwarp();
 }
 
 __device__ __forceinline__ void fwd_sn(SweepRing& R, int slo, int nc, int m, int wso, int lane) {

@@ -790,15 +790,31 @@ inline AScatter build_ascatter(const SymFactor& F, const FrontMaps& M, const Csr
 }
 
 /// Convert factor values from the packed column-major trapezoid (factor_host)
-/// to the panel-blocked sweep layout (pf_layout.hpp), in place.
+/// to the panel-blocked sweep layout (pf_layout.hpp), in place; each panel's
+/// triangle unit receives the inverse of its unit-lower diagonal block.
 inline void to_blocked(const SymFactor& F, std::vector<double>& L) {
   std::vector<double> out(L.size(), 0.0);
+  std::vector<double> T, X;
   for (int k = 0; k < F.nsn; ++k) {
     const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
     const long long o = F.sn_valoff[k];
-    long long q = o;
+    auto packed = [&](int i, int j) { return L[o + (long long)j * (m - 1) - (long long)j * (j - 1) / 2 + (i - j - 1)]; };
     for (int j = 0; j < nc; ++j)
-      for (int i = j + 1; i < m; ++i) out[o + blk_off(nc, m, i, j)] = L[q++];
+      for (int i = j + 1; i < m; ++i) out[o + blk_off(nc, m, i, j)] = packed(i, j);
+    for (int p0 = 0; p0 < nc; p0 += kPW) {
+      const int pw = std::min(kPW, nc - p0);
+      X.assign((std::size_t)pw * pw, 0.0);  // X = Linv, column-major
+      for (int j = 0; j < pw; ++j) {
+        X[j + j * pw] = 1.0;
+        for (int i = j + 1; i < pw; ++i) {
+          double acc = 0.0;
+          for (int q = j; q < i; ++q) acc += packed(p0 + i, p0 + q) * X[q + j * pw];
+          X[i + j * pw] = -acc;
+        }
+      }
+      for (int j = 0; j < pw; ++j)
+        for (int i = j + 1; i < pw; ++i) out[o + blk_off(nc, m, p0 + i, p0 + j)] = X[i + j * pw];
+    }
   }
   L.swap(out);
 }
