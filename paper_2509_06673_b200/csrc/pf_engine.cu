@@ -109,8 +109,10 @@ struct SolveSystem {
   long long total_x = 0, total_L = 0, total_cb = 0;
   int nlevel = 0;
   std::vector<int> level_nwork, level_ws;  // per global level
+  std::vector<long long> level_cols, level_vals;  // per global level (all problems)
   std::vector<DevBuf<int>> d_wp, d_wt;     // per global level work lists
   DevBuf<dev::TypeDesc> d_types;
+  std::vector<dev::TypeDesc> d_types_host;
   DevBuf<int> d_sn_col0, d_sn_ncol, d_sn_nrow, d_slot, d_t0, d_t1, d_c0, d_c1, d_cbo, d_cbl, d_cbrows,
       d_fold_ptr, d_fold_idx, d_prob_type, d_perm, d_prob_n;
   DevBuf<long long> d_sn_rowoff, d_sn_valoff, d_prob_x, d_prob_lval, d_prob_cb, d_prob_perm;
@@ -121,6 +123,9 @@ struct SolveSystem {
   DevBuf<unsigned long long> d_udesc;
   DevBuf<int> d_tuf, d_tnuf, d_tub, d_tnub;
   int smax = 8;  // max supernode row count (padded to 8)
+  // dense top (single-problem systems): levels >= top_level replaced by X_top = W y_top
+  int top_level = -1, ntop = 0, top_c0 = 0;
+  DevBuf<double> W, Wres;
   int nrhs_alloc = 1;
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
@@ -231,6 +236,7 @@ struct SolveSystem {
     const int np = (int)ptype.size();
     prob_x.resize(np), prob_lval.resize(np), prob_cb.resize(np);
     std::vector<std::vector<int>> wp(nlevel), wt(nlevel);
+    level_cols.assign(nlevel, 0), level_vals.assign(nlevel, 0);
     std::vector<int> pn;
     std::vector<long long> pperm;
     total_x = total_L = total_cb = 0;
@@ -245,6 +251,8 @@ struct SolveSystem {
       for (int t = 0; t < F.ntask; ++t) {
         const int gl = glevel(F, F.task_level[t]);
         wp[gl].push_back(p), wt[gl].push_back(t);
+        level_cols[gl] += F.task_c1[t] - F.task_c0[t];
+        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) level_vals[gl] += sn_size(F.sn_ncol[k], F.sn_nrow[k]);
       }
       pn.push_back(F.n);
       pperm.push_back(type_perm_off[ptype[p]]);
@@ -261,6 +269,7 @@ struct SolveSystem {
     ws_max = (ws_max + 1) & ~1;  // even: 16-byte aligned slot buffers behind it
 
     d_types.upload(td);
+    d_types_host = td;
     d_sn_col0.upload(sn_col0), d_sn_ncol.upload(sn_ncol), d_sn_nrow.upload(sn_nrow);
     d_sn_rowoff.upload(sn_rowoff), d_sn_valoff.upload(sn_valoff), d_slot.upload(slot);
     d_t0.upload(t0), d_t1.upload(t1), d_c0.upload(c0), d_c1.upload(c1), d_cbo.upload(cbo), d_cbl.upload(cbl);
@@ -332,11 +341,25 @@ struct SolveSystem {
         for (auto& e : ev) cudaEventCreate(&e);
       cudaEventRecord(ev[0], st);
     }
-    for (int l = 0; l + 1 < nlevel; ++l) launch_level(st, nrhs, l, 0);
-    if (timed) cudaEventRecord(ev[1], st);
-    if (nlevel > 0) launch_level(st, nrhs, nlevel - 1, 1);
-    if (timed) cudaEventRecord(ev[2], st);
-    for (int l = nlevel - 2; l >= 0; --l) launch_level(st, nrhs, l, 2);
+    if (top_level >= 0) {
+      if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
+      for (int l = 0; l < top_level; ++l) launch_level(st, nrhs, l, 0);
+      if (timed) cudaEventRecord(ev[1], st);
+      dev::k_dense_top<<<cdiv(ntop, 8), 256, sizeof(double) * ntop, st>>>(
+          ntop, top_c0, W.p, d_fold_ptr.p + d_types_host[0].fold_base, d_fold_idx.p + d_types_host[0].foldidx_base,
+          CB.p, X.p, Wres.p);
+      dev::k_dense_top_store<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, Wres.p, X.p);
+      ::pf::g_launches += 2;
+      launches += 2;
+      if (timed) cudaEventRecord(ev[2], st);
+      for (int l = top_level - 1; l >= 0; --l) launch_level(st, nrhs, l, 2);
+    } else {
+      for (int l = 0; l + 1 < nlevel; ++l) launch_level(st, nrhs, l, 0);
+      if (timed) cudaEventRecord(ev[1], st);
+      if (nlevel > 0) launch_level(st, nrhs, nlevel - 1, 1);
+      if (timed) cudaEventRecord(ev[2], st);
+      for (int l = nlevel - 2; l >= 0; --l) launch_level(st, nrhs, l, 2);
+    }
     if (timed) {
       cudaEventRecord(ev[3], st);
       cudaEventSynchronize(ev[3]);
@@ -347,6 +370,58 @@ struct SolveSystem {
       }
     }
     PF_CUDA_CHECK(cudaGetLastError());
+  }
+
+  /// Replace the top levels of a single-problem system by a dense inverse of
+  /// their Schur complement: the top block of the factor (packed, host) is
+  /// S = Lt Dt Lt^T, W = Lt^-T Dt^-1 Lt^-1.  Levels >= the smallest level whose
+  /// suffix holds at most max_cols columns (at least one level stays sparse).
+  void set_dense_top(const SymFactor& F, const std::vector<double>& Lp, const std::vector<double>& Dg, int max_cols,
+                     int threads) {
+    if (prob_type.size() != 1 || nlevel < 2) return;
+    int L = nlevel;
+    long long cols = 0;
+    while (L - 1 >= 1 && cols + level_cols[L - 1] <= max_cols) cols += level_cols[--L];
+    if (L == nlevel) return;
+    const int c0 = F.task_c0[F.level_ptr[L]];
+    const int n = F.n - c0;
+    if (n != cols) fail(kInternal, "dense top: top levels are not a column suffix");
+    // dense unit-lower Lt (column-major) from the packed supernodes of the top
+    std::vector<double> Lt((std::size_t)n * n, 0.0), Xi((std::size_t)n * n, 0.0), Wh((std::size_t)n * n, 0.0);
+    for (int k = 0; k < F.nsn; ++k) {
+      const int nc = F.sn_ncol[k], m = F.sn_nrow[k], col0 = F.sn_col0[k];
+      if (col0 < c0) continue;
+      const int* R = &F.rows[F.sn_rowoff[k]];
+      long long q = F.sn_valoff[k];
+      for (int j = 0; j < nc; ++j)
+        for (int i = j + 1; i < m; ++i) Lt[(std::size_t)(col0 + j - c0) * n + (R[i] - c0)] = Lp[q++];
+    }
+    // Xi = Lt^-1 (column j: forward substitution from e_j)
+    parallel_for(n, threads, [&](int j) {
+      double* x = &Xi[(std::size_t)j * n];
+      x[j] = 1.0;
+      for (int c = j; c < n; ++c) {
+        const double v = x[c];
+        if (v == 0.0) continue;
+        const double* lc = &Lt[(std::size_t)c * n];
+        for (int i = c + 1; i < n; ++i) x[i] -= lc[i] * v;
+      }
+    });
+    // W = Xi^T D^-1 Xi (symmetric): W[i][j] = sum_k Xi[k][i] Xi[k][j] / D[k]
+    parallel_for(n, threads, [&](int i) {
+      const double* xi = &Xi[(std::size_t)i * n];
+      for (int j = 0; j <= i; ++j) {
+        const double* xj = &Xi[(std::size_t)j * n];
+        double acc = 0.0;
+        for (int k = i; k < n; ++k) acc += xi[k] * xj[k] / Dg[c0 + k];
+        Wh[(std::size_t)i * n + j] = acc;
+      }
+    });
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) Wh[(std::size_t)i * n + j] = Wh[(std::size_t)j * n + i];
+    W.upload(Wh);
+    Wres.alloc(n);
+    top_level = L, ntop = n, top_c0 = c0;
   }
 
   void prepare_smem() {
@@ -715,7 +790,8 @@ struct Engine {
         std::fprintf(stderr, "[pf] %s: %d levels, nnzL %lld, ws_max %d, smax %d, smem/CTA %d\n", name, S.nlevel, S.nnzL,
                      S.ws_max, S.smax, S.sweep_smem());
         for (int l = 0; l < S.nlevel; ++l)
-          std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d\n", l, S.level_nwork[l], S.level_ws[l]);
+          std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d, cols %lld, values %lld\n", l, S.level_nwork[l],
+                       S.level_ws[l], S.level_cols[l], S.level_vals[l]);
       };
       dump("K", Ksys);
       dump("K_II", Isys);
@@ -1347,6 +1423,11 @@ struct Engine {
     Qsys.build({&qsym}, {0}, 1);
     std::vector<double> L, Dg;
     factor_host(qsym, A, A.val.data(), {}, L, Dg);
+    {
+      const char* v = std::getenv("PF_Q_DENSE_TOP");
+      const int cap = v ? std::atoi(v) : 2048;
+      if (cap > 0) Qsys.set_dense_top(qsym, L, Dg, cap, nthreads);
+    }
     to_blocked(qsym, L);
     PF_CUDA_CHECK(cudaMemcpy(Qsys.L.p, L.data(), sizeof(double) * L.size(), cudaMemcpyHostToDevice));
     PF_CUDA_CHECK(cudaMemcpy(Qsys.D.p, Dg.data(), sizeof(double) * Dg.size(), cudaMemcpyHostToDevice));
