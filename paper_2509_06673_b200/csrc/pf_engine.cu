@@ -345,10 +345,11 @@ struct SolveSystem {
       if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
       for (int l = 0; l < top_level; ++l) launch_level(st, nrhs, l, 0);
       if (timed) cudaEventRecord(ev[1], st);
-      dev::k_dense_top<<<cdiv(ntop, 8), 256, sizeof(double) * ntop, st>>>(
-          ntop, top_c0, W.p, d_fold_ptr.p + d_types_host[0].fold_base, d_fold_idx.p + d_types_host[0].foldidx_base,
-          CB.p, X.p, Wres.p);
-      dev::k_dense_top_store<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, Wres.p, X.p);
+      dev::k_dense_top_gather<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, d_fold_ptr.p + d_types_host[0].fold_base,
+                                                              d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, X.p,
+                                                              Wres.p);
+      dev::k_dense_top_gemv<<<std::min(cdiv(ntop, 8), 2 * 148), 256, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p,
+                                                                                                   Wres.p, X.p);
       ::pf::g_launches += 2;
       launches += 2;
       if (timed) cudaEventRecord(ev[2], st);

@@ -248,36 +248,32 @@ __global__ void k_dense_gemv(int n, const double* A, const double* x, double* y)
   if (threadIdx.x == 0) y[i] = s;
 }
 
-/// Dense top of a single-problem sweep: y = X[c0..c0+n) + folded child
-/// contributions, X[c0 + i] = sum_j W[i][j] y[j] (W = inverse of the top
-/// Schur complement).  Every CTA gathers y into shared memory, then one warp
-/// per row (fixed summation order).
-__global__ void __launch_bounds__(256) k_dense_top(int n, int c0, const double* __restrict__ W,
-                                                   const int* __restrict__ fold_ptr, const int* __restrict__ fold_idx,
-                                                   const double* __restrict__ CB, const double* X,
-                                                   double* res) {
-  extern __shared__ double ytop[];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double v = X[c0 + i];
-    for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) v += CB[fold_idx[q]];
-    ytop[i] = v;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row = blockIdx.x * 8 + warp;
-  if (row >= n) return;
-  const double* w = W + (size_t)row * n;
-  double s = 0.0;
-  for (int j = lane; j < n; j += 32) s += w[j] * ytop[j];
-  s = warp_sum(s);
-  if (lane == 0) res[row] = s;  // X is overwritten by a second launch once every CTA has read it
+/// Dense top of a single-problem sweep, pass 1: y = X[c0..c0+n) + folded
+/// child contributions (fixed order).
+__global__ void k_dense_top_gather(int n, int c0, const int* __restrict__ fold_ptr, const int* __restrict__ fold_idx,
+                                   const double* __restrict__ CB, const double* X, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = X[c0 + i];
+  for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) v += CB[fold_idx[q]];
+  y[i] = v;
 }
 
-/// write-back pass of k_dense_top (separate launch: all CTAs must finish
-/// reading X before it is overwritten)
-__global__ void k_dense_top_store(int n, int c0, const double* __restrict__ res, double* X) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) X[c0 + i] = res[i];
+/// pass 2: X[c0 + i] = sum_j W[i][j] y[j] (W = inverse of the top Schur
+/// complement), one warp per row, y staged in shared memory.
+__global__ void __launch_bounds__(256) k_dense_top_gemv(int n, int c0, const double* __restrict__ W,
+                                                        const double* __restrict__ y, double* X) {
+  extern __shared__ double ys[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
+    const double* w = W + (size_t)row * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s += w[j] * ys[j];
+    s = warp_sum(s);
+    if (lane == 0) X[c0 + row] = s;
+  }
 }
 
 }  // namespace dev
