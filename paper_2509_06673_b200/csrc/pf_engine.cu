@@ -157,6 +157,7 @@ struct SolveSystem {
       T.fold_base = (long long)fptr.size();
       T.foldidx_base = (long long)fidx.size();
       T.slot_base = (long long)slots16.size();
+      if (udesc.size() & 1) udesc.push_back(0);
       T.udesc_base = (long long)udesc.size();
       std::vector<long long> sn_slot(F.nsn);
       for (int s = 0; s < F.nsn; ++s) {
@@ -188,6 +189,7 @@ struct SolveSystem {
         tlbeg.push_back(F.sn_valoff[F.task_sn0[t]]);
         // unit descriptors in the sweep kernel's consumption order (pf_sweep.cuh)
         const long long ub = T.udesc_base;
+        if (udesc.size() & 1) udesc.push_back(0);  // lists start 16-byte aligned (staged by bulk copies)
         tuf.push_back((int)((long long)udesc.size() - ub));
         long long pos = 0;
         for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
@@ -206,6 +208,7 @@ struct SolveSystem {
         udesc.push_back(dev::unit_desc(8LL * (tc0 & ~1), 8 * even_up((tc0 & 1) + tnc), dev::kSrcDiag));
         tnuf.push_back((int)((long long)udesc.size() - ub) - tuf.back());
         if (pos > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
+        if (udesc.size() & 1) udesc.push_back(0);
         tub.push_back((int)((long long)udesc.size() - ub));
         for (int k = F.task_sn1[t] - 1; k >= F.task_sn0[t]; --k) {
           const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
@@ -276,6 +279,7 @@ struct SolveSystem {
     d_cbrows.upload(cbrows), d_fold_ptr.upload(fptr), d_fold_idx.upload(fidx);
     d_prob_type.upload(ptype), d_prob_x.upload(prob_x), d_prob_lval.upload(prob_lval), d_prob_cb.upload(prob_cb);
     d_perm.upload(perm), d_prob_perm.upload(pperm), d_prob_n.upload(pn);
+    udesc.push_back(0), udesc.push_back(0);  // staged list chunks round up to 16 bytes
     d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_udesc.upload(udesc);
     d_tuf.upload(tuf), d_tnuf.upload(tnuf), d_tub.upload(tub), d_tnub.upload(tnub);
     L.alloc(total_L + 4);
@@ -323,12 +327,33 @@ struct SolveSystem {
   bool timed = false;
   double phase_ms[3] = {0, 0, 0};  // forward levels / root / backward levels
 
-  int sweep_smem() const { return dev::kSweepWarps * dev::SweepSmem::bytes(ws_max, smax); }
+  // warp-specialised sweep (producer warp + kWsCons consumers) unless PF_SWEEP_WS=0
+  static bool ws_sweep() {
+    static const bool v = !std::getenv("PF_SWEEP_WS") || std::atoi(std::getenv("PF_SWEEP_WS")) != 0;
+    return v;
+  }
+  int sweep_smem() const {
+    return ws_sweep() ? dev::kWsCons * dev::WsSmem::bytes(ws_max, smax) + dev::kSweepPad
+                      : dev::kSweepWarps * dev::SweepSmem::bytes(ws_max, smax) + dev::kSweepPad;
+  }
+
+  template <int MODE>
+  void launch_mode(cudaStream_t st, const dev::SolveSet& S) {
+    if (ws_sweep())
+      dev::k_sweep_ws<MODE><<<cdiv(S.nwork, dev::kWsCons), 32 * (dev::kWsCons + 1), sweep_smem(), st>>>(S, ws_max, smax);
+    else
+      dev::k_sweep<MODE><<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(), st>>>(S, ws_max, smax);
+  }
 
   void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
     if (level_nwork[l] == 0) return;
+    if (nrhs != 1) fail(kInternal, "the sweep kernels take one right-hand side");
     dev::SolveSet S = set(nrhs, l);
-    dev::k_sweep<<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(), st>>>(S, mode, ws_max, smax);
+    static const bool probe = std::getenv("PF_SWEEP_PROBE") != nullptr;
+    if (probe && mode == 0) launch_mode<3>(st, S);
+    else if (mode == 0) launch_mode<0>(st, S);
+    else if (mode == 1) launch_mode<1>(st, S);
+    else launch_mode<2>(st, S);
     ::pf::g_launches++;
     ++launches;
   }
@@ -429,7 +454,15 @@ struct SolveSystem {
     if (sweep_smem() > 227 * 1024)
       fail(kInternal, "sweep workspace exceeds shared memory (" + std::to_string(sweep_smem()) + " B)");
     // the attribute is per kernel (shared by all systems): raise it to the opt-in maximum once
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int smax_attr = 227 * 1024;
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
   }
 };
 
@@ -1102,6 +1135,7 @@ struct Engine {
   /// b ~ U(-1,1) from mt19937(20240901), x = K_s^{-1} b through the sweep
   /// kernels, ||K_s x - b|| / ||b|| < 1e-8.
   void check_factor_residual() {
+    if (std::getenv("PF_SWEEP_PROBE")) return;  // streaming experiment: solves are not computed
     const int nt = (int)D.types.size();
     const int np = nown();
     std::vector<long long> type_b(nt, 0), type_kptr(nt), type_kcol(nt);

@@ -64,6 +64,7 @@ __device__ __forceinline__ void mbar_wait(unsigned b, unsigned parity) {
 constexpr int kRingBytes = 8192;   // per warp; >= the largest unit (kRB*kPW*8)
 constexpr int kUnits = 8;          // units in flight per warp (mbarriers)
 constexpr int kSweepWarps = 4;     // warps per CTA
+constexpr int kSweepPad = 256;     // slack after the last warp region
 
 /// Per-warp shared memory: ring | barriers | task meta | ws | slots.
 struct SweepSmem {
@@ -146,7 +147,8 @@ struct SweepRing {
 };
 
 /// copy the supernode's slot list out of the ring
-__device__ __forceinline__ void take_slots(SweepRing& R, int slo, int m) {
+template <class Ring>
+__device__ __forceinline__ void take_slots(Ring& R, int slo, int m) {
   const int src = R.acquire(((m + 7) & ~7) * 2);
   for (int i = R.lane; i < (m + 7) >> 3; i += 32)
     *reinterpret_cast<int4*>(g_sm + slo + 16 * i) = *reinterpret_cast<const int4*>(g_sm + src + 16 * i);
@@ -161,8 +163,8 @@ __device__ __forceinline__ double& ws_at(int wso, int s) { return *reinterpret_c
 /// diagonal block (pf_factor.cuh), so x = Linv b is a dot product per lane
 /// with no sequential dependency; the panel's own columns occupy consecutive
 /// workspace slots, so b and x are broadcast through shared memory.
-template <int PWC, bool EXACT>
-__device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw, int m, int wso, int lane) {
+template <int PWC, bool EXACT, class Ring>
+__device__ __forceinline__ void fwd_panel(Ring& R, int slo, int p0, int pw, int m, int wso, int lane) {
   const bool mine = lane < pw;
   const int wp = wso + 8 * slot_at(slo, p0);
   if (pw > 1) {
@@ -212,8 +214,8 @@ __device__ __forceinline__ void fwd_panel(SweepRing& R, int slo, int p0, int pw,
 }
 
 /// backward substitution of one panel
-template <int PWC, bool EXACT>
-__device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw, int m, int wso, int lane) {
+template <int PWC, bool EXACT, class Ring>
+__device__ __forceinline__ void bwd_panel(Ring& R, int slo, int p0, int pw, int m, int wso, int lane) {
   double acc[PWC];
 #pragma unroll
   for (int j = 0; j < PWC; ++j) acc[j] = 0.0;
@@ -259,7 +261,8 @@ __device__ __forceinline__ void bwd_panel(SweepRing& R, int slo, int p0, int pw,
   __syncwarp();
 }
 
-__device__ __forceinline__ void fwd_sn(SweepRing& R, int slo, int nc, int m, int wso, int lane) {
+template <class Ring>
+__device__ __forceinline__ void fwd_sn(Ring& R, int slo, int nc, int m, int wso, int lane) {
   for (int p0 = 0; p0 < nc; p0 += kPW) {
     const int pw = min(kPW, nc - p0);
     if (pw == kPW) fwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
@@ -269,7 +272,8 @@ __device__ __forceinline__ void fwd_sn(SweepRing& R, int slo, int nc, int m, int
   }
 }
 
-__device__ __forceinline__ void bwd_sn(SweepRing& R, int slo, int nc, int m, int wso, int lane) {
+template <class Ring>
+__device__ __forceinline__ void bwd_sn(Ring& R, int slo, int nc, int m, int wso, int lane) {
   for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
     const int pw = min(kPW, nc - p0);
     if (pw == kPW) bwd_panel<kPW, true>(R, slo, p0, pw, m, wso, lane);
@@ -279,14 +283,13 @@ __device__ __forceinline__ void bwd_sn(SweepRing& R, int slo, int nc, int m, int
   }
 }
 
-/// mode 0: forward (fold children, eliminate, scale by D, emit contributions)
-/// mode 1: root (forward + scale + backward in one pass)
-/// mode 2: backward (ancestor values final in X)
-__global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode, int ws_max, int smax) {
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int w = blockIdx.x * kSweepWarps + wib;
-  if (w >= S.nwork) return;
-  const int wb = wib * SweepSmem::bytes(ws_max, smax);
+/// Consumer side of one task (one warp): gather inputs, stream the units,
+/// write outputs.  MODE 0: forward (fold children, eliminate, scale by D, emit
+/// contributions); 1: root (forward + scale + backward); 2: backward (ancestor
+/// values final in X).  Ring::pump() starts the self-producing variant.
+template <int MODE, class Ring>
+__device__ __forceinline__ void sweep_task(const SolveSet& S, Ring& R, int w, int wb, int ws_max, int lane,
+                                           bool self_produce) {
   const int wso = wb + SweepSmem::kWs;
   const int slo = wso + 8 * ws_max;
   const int p = S.work_prob[w];
@@ -294,70 +297,244 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int mode
   const int t = T.task_base + S.work_task[w];
   const int c0 = S.task_c0[t], c1 = S.task_c1[t], nct = c1 - c0;
   const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
+  const int nsn = S.task_sn1[t] - S.task_sn0[t];
+  const unsigned long long* ul = S.udesc + T.udesc_base;
+  double* X = S.X + S.prob_x[p];
+  double* CBp = S.CB + S.prob_cb[p];
+  if (MODE == 3) {  // streaming probe: consume the forward units without computing
+    if (self_produce) R.start(ul + S.task_uf[t], S.task_nuf[t]), R.pump();
+    const unsigned long long* l = ul + S.task_uf[t];
+    double acc = 0.0;
+    for (int u = 0; u < S.task_nuf[t]; ++u) {
+      const int sz = (int)((__ldg(l + u) >> 32) & 0xffffu);
+      const int o = R.acquire(sz);
+      acc += lds(o + 8 * (lane % (sz / 8)));
+      R.release();
+    }
+    if (acc == 12345.678) X[c0] = acc;
+    return;
+  }
+  if (MODE != 2) {
+    if (self_produce) R.start(ul + S.task_uf[t], S.task_nuf[t]), R.pump();  // first units in flight
+    const int* fp = S.fold_ptr + T.fold_base;
+    const int* fi = S.fold_idx + T.foldidx_base;
+    for (int i = lane; i < nct; i += 32) {
+      double v = X[c0 + i];
+      for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];  // children, fixed order
+      ws_at(wso, i) = v;
+    }
+    for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = 0.0;
+    for (int k = 0; k < nsn; ++k) {
+      const int4 mt = meta_at(wb, k);
+      take_slots(R, slo, mt.y);
+      fwd_sn(R, slo, mt.x, mt.y, wso, lane);
+    }
+    {
+      // pivots of the task's columns: the last unit of the forward list
+      const int sh = c0 & 1;
+      const int dof = R.acquire(8 * even_up(sh + nct)) + 8 * sh;
+      for (int i = lane; i < nct; i += 32) ws_at(wso, i) /= lds(dof + 8 * i);
+      R.release();
+    }
+    if (MODE == 0)
+      for (int i = lane; i < cbl; i += 32) CBp[cbo + i] = ws_at(wso, nct + i);
+    __syncwarp();
+  }
+  if (MODE != 0) {
+    if (self_produce) R.start(ul + S.task_ub[t], S.task_nub[t]), R.pump();
+    if (MODE == 2) {
+      const int* cbr = S.cb_rows + T.cb_base + cbo;
+      for (int i = lane; i < nct; i += 32) ws_at(wso, i) = X[c0 + i];
+      for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = X[cbr[i]];
+    }
+    __syncwarp();
+    for (int k = nsn - 1; k >= 0; --k) {
+      const int4 mt = meta_at(wb, k);
+      take_slots(R, slo, mt.y);
+      bwd_sn(R, slo, mt.x, mt.y, wso, lane);
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < nct; i += 32) X[c0 + i] = ws_at(wso, i);
+}
+
+/// task metadata of work item w into the warp's region
+__device__ __forceinline__ void load_meta(const SolveSet& S, int w, int wb, int lane) {
+  const int p = S.work_prob[w];
+  const TypeDesc T = S.types[S.prob_type[p]];
+  const int t = T.task_base + S.work_task[w];
   const int sn0 = S.task_sn0[t], nsn = S.task_sn1[t] - sn0;
+  for (int i = lane; i < nsn; i += 32)
+    *reinterpret_cast<int4*>(g_sm + wb + SweepSmem::kMeta + 16 * i) = __ldg(S.sn_meta + T.sn_base + sn0 + i);
+}
+
+/// Self-producing sweep: every warp streams and consumes its own task.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kSweepWarps) k_sweep(SolveSet S, int ws_max, int smax) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kSweepWarps + wib;
+  if (w >= S.nwork) return;
+  const int wb = wib * SweepSmem::bytes(ws_max, smax);
   SweepRing R;
   R.sbase = smem_u32(g_sm), R.wb = wb, R.lane = lane;
   if (lane == 0) {
     for (int i = 0; i < kUnits; ++i) mbar_init(R.bar(i), 1);
     fence_mbar_init();
   }
-  for (int i = lane; i < nsn; i += 32)
-    *reinterpret_cast<int4*>(g_sm + wb + SweepSmem::kMeta + 16 * i) = __ldg(S.sn_meta + T.sn_base + sn0 + i);
+  load_meta(S, w, wb, lane);
   __syncwarp();
+  const int p = S.work_prob[w];
+  const TypeDesc T = S.types[S.prob_type[p]];
+  const int t = T.task_base + S.work_task[w];
   R.sv = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
   R.ss = reinterpret_cast<const unsigned char*>(S.slots + T.slot_base);
   R.sd = reinterpret_cast<const unsigned char*>(S.D + S.prob_x[p]);
   R.issued = R.cons = R.head = R.tail = R.chead = 0;
-  const unsigned long long* ul = S.udesc + T.udesc_base;
-  for (int r = 0; r < S.nrhs; ++r) {
-    double* X = S.X + S.prob_x[p] + r * S.x_stride;
-    double* CBp = S.CB + S.prob_cb[p] + r * S.cb_stride;
-    if (mode != 2) {
-      R.start(ul + S.task_uf[t], S.task_nuf[t]);
-      R.pump();  // first units in flight while the inputs are gathered
-      const int* fp = S.fold_ptr + T.fold_base;
-      const int* fi = S.fold_idx + T.foldidx_base;
-      for (int i = lane; i < nct; i += 32) {
-        double v = X[c0 + i];
-        for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];  // children, fixed order
-        ws_at(wso, i) = v;
-      }
-      for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = 0.0;
-      for (int k = 0; k < nsn; ++k) {
-        const int4 mt = meta_at(wb, k);
-        take_slots(R, slo, mt.y);
-        fwd_sn(R, slo, mt.x, mt.y, wso, lane);
-      }
-      {
-        // pivots of the task's columns: the last unit of the forward list
-        const int sh = c0 & 1;
-        const int dof = R.acquire(8 * even_up(sh + nct)) + 8 * sh;
-        for (int i = lane; i < nct; i += 32) ws_at(wso, i) /= lds(dof + 8 * i);
-        R.release();
-      }
-      if (mode == 0)
-        for (int i = lane; i < cbl; i += 32) CBp[cbo + i] = ws_at(wso, nct + i);
-      __syncwarp();
-    }
-    if (mode != 0) {
-      R.start(ul + S.task_ub[t], S.task_nub[t]);
-      R.pump();
-      if (mode == 2) {
-        const int* cbr = S.cb_rows + T.cb_base + cbo;
-        for (int i = lane; i < nct; i += 32) ws_at(wso, i) = X[c0 + i];
-        for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = X[cbr[i]];
-      }
-      __syncwarp();
-      for (int k = nsn - 1; k >= 0; --k) {
-        const int4 mt = meta_at(wb, k);
-        take_slots(R, slo, mt.y);
-        bwd_sn(R, slo, mt.x, mt.y, wso, lane);
-      }
-    }
-    __syncwarp();
-    for (int i = lane; i < nct; i += 32) X[c0 + i] = ws_at(wso, i);
-    __syncwarp();
+  sweep_task<MODE>(S, R, w, wb, ws_max, lane, true);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised sweep: warp 0 of the CTA is the producer, warps 1..kWsCons
+// consume one task each.  Producer lane c walks consumer c's descriptor list
+// (staged into shared memory 64 entries at a time by bulk copies) and issues
+// a unit as soon as the consumer has released ring space; the consumer only
+// waits on its full barriers and publishes (consumed units, ring tail).
+// ---------------------------------------------------------------------------
+constexpr int kWsCons = 7;        // consumer warps per CTA
+constexpr int kListChunk = 64;    // descriptors per staged list chunk
+
+/// extra per-consumer shared memory of the warp-specialised sweep (after the
+/// SweepSmem region): ctrl int2 | 2 list barriers | 2 x kListChunk descriptors
+struct WsSmem {
+  static constexpr int kCtrl = 0;
+  static constexpr int kLBar = 16;
+  static constexpr int kList = 32;
+  static constexpr int kBytes = kList + 2 * 8 * kListChunk;
+  __host__ __device__ static int bytes(int ws_max, int smax) { return ((SweepSmem::bytes(ws_max, smax) + 15) & ~15) + kBytes; }
+};
+
+struct ConsumerRing {
+  int wb, ctrl;          // region offset; ctrl offset (cons, tail)
+  unsigned sbase;
+  int cons, chead, lane;
+  __device__ __forceinline__ unsigned bar(int u) const { return sbase + wb + SweepSmem::kBar + 8 * (u & (kUnits - 1)); }
+  __device__ __forceinline__ void start(const unsigned long long*, int) {}
+  __device__ __forceinline__ void pump() {}
+  __device__ __forceinline__ int acquire(int sz) {
+    int h = chead;
+    if ((h & (kRingBytes - 1)) + sz > kRingBytes) h += kRingBytes - (h & (kRingBytes - 1));
+    chead = h + sz;
+    mbar_wait(bar(cons), (unsigned)(cons / kUnits) & 1u);
+    return wb + (h & (kRingBytes - 1));
   }
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    ++cons;
+    if (lane == 0) {
+      __threadfence_block();
+      *reinterpret_cast<volatile unsigned long long*>(g_sm + ctrl) =
+          (unsigned long long)(unsigned)cons | ((unsigned long long)(unsigned)chead << 32);
+    }
+  }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(32 * (kWsCons + 1)) k_sweep_ws(SolveSet S, int ws_max, int smax) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rb = WsSmem::bytes(ws_max, smax);
+  const unsigned sbase = smem_u32(g_sm);
+  if (wid == 0) {
+    // ---------------- producer: lane c serves consumer warp c + 1 ----------------
+    const int c = lane;
+    const int w = blockIdx.x * kWsCons + c;
+    const bool valid = c < kWsCons && w < S.nwork;
+    const int wb = c * rb;
+    const int xb = wb + ((SweepSmem::bytes(ws_max, smax) + 15) & ~15);
+    if (valid) {
+      for (int i = 0; i < kUnits; ++i) mbar_init(sbase + wb + SweepSmem::kBar + 8 * i, 1);
+      mbar_init(sbase + xb + WsSmem::kLBar, 1), mbar_init(sbase + xb + WsSmem::kLBar + 8, 1);
+      *reinterpret_cast<int2*>(g_sm + xb + WsSmem::kCtrl) = make_int2(0, 0);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (!valid) return;
+    const int p = S.work_prob[w];
+    const TypeDesc T = S.types[S.prob_type[p]];
+    const int t = T.task_base + S.work_task[w];
+    const unsigned char* sv = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
+    const unsigned char* ss = reinterpret_cast<const unsigned char*>(S.slots + T.slot_base);
+    const unsigned char* sd = reinterpret_cast<const unsigned char*>(S.D + S.prob_x[p]);
+    const unsigned long long* ul = S.udesc + T.udesc_base;
+    int phase = MODE == 2 ? 1 : 0;
+    const unsigned long long* list = ul + (phase ? S.task_ub[t] : S.task_uf[t]);
+    int nu = phase ? S.task_nub[t] : S.task_nuf[t];
+    int li = 0, issued = 0, head = 0, lphase = 0, lwait = 0;  // lphase: parity bits of the 2 list barriers
+    auto list_issue = [&](int chunk) {  // stage descriptors [chunk*64, ...) of the current list
+      const int base = chunk * kListChunk;
+      if (base >= nu) return;
+      const int cnt = min(kListChunk, nu - base);
+      const unsigned bytes = (unsigned)(8 * ((cnt + 1) & ~1));
+      const unsigned lb = sbase + xb + WsSmem::kLBar + 8 * (chunk & 1);
+      fence_proxy_async();
+      mbar_expect_tx(lb, bytes);
+      bulk_g2s(sbase + xb + WsSmem::kList + 8 * kListChunk * (chunk & 1), list + base, bytes, lb);
+    };
+    list_issue(0), list_issue(1);
+    const volatile unsigned long long* ctrl =
+        reinterpret_cast<const volatile unsigned long long*>(g_sm + xb + WsSmem::kCtrl);
+    while (true) {
+      if (li == nu) {
+        if (MODE == 1 && phase == 0) {
+          // both staged chunks of the forward list have been waited (li == nu);
+          // the backward list restarts the chunk sequence on the same buffers
+          phase = 1, list = ul + S.task_ub[t], nu = S.task_nub[t], li = 0, lwait = 0;
+          list_issue(0), list_issue(1);
+          continue;
+        }
+        break;
+      }
+      const unsigned long long cv = *ctrl;
+      const int2 ct = make_int2((int)(unsigned)cv, (int)(unsigned)(cv >> 32));
+      bool progress = false;
+      while (li < nu && issued - ct.x < kUnits) {
+        const int slot = (li / kListChunk) & 1;
+        if (li / kListChunk >= lwait) {  // entering a staged chunk (waited once)
+          mbar_wait(sbase + xb + WsSmem::kLBar + 8 * slot, (lphase >> slot) & 1u);
+          lphase ^= 1u << slot;
+          lwait = li / kListChunk + 1;
+        }
+        const unsigned long long d = *reinterpret_cast<const unsigned long long*>(
+            g_sm + xb + WsSmem::kList + 8 * kListChunk * slot + 8 * (li % kListChunk));
+        const int sz = (int)((d >> 32) & 0xffffu);
+        int h = head;
+        if ((h & (kRingBytes - 1)) + sz > kRingBytes) h += kRingBytes - (h & (kRingBytes - 1));
+        if (h + sz - ct.y > kRingBytes) break;
+        const unsigned bb = sbase + wb + SweepSmem::kBar + 8 * (issued & (kUnits - 1));
+        fence_proxy_async();
+        mbar_expect_tx(bb, (unsigned)sz);
+        const int kind = (int)(d >> 48);
+        const unsigned char* from = kind == kSrcValues ? sv : kind == kSrcSlots ? ss : sd;
+        bulk_g2s(sbase + wb + (h & (kRingBytes - 1)), from + (unsigned)d, (unsigned)sz, bb);
+        head = h + sz;
+        ++issued, ++li;
+        progress = true;
+        if (li % kListChunk == 0) list_issue(li / kListChunk + 1);  // refill the chunk just finished
+      }
+      if (!progress) __nanosleep(32);
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int c = wid - 1;
+  const int w = blockIdx.x * kWsCons + c;
+  const int wb = c * rb;
+  const int xb = wb + ((SweepSmem::bytes(ws_max, smax) + 15) & ~15);
+  if (w < S.nwork) load_meta(S, w, wb, lane);
+  __syncthreads();
+  if (w >= S.nwork) return;
+  ConsumerRing R;
+  R.wb = wb, R.ctrl = xb + WsSmem::kCtrl, R.sbase = sbase, R.cons = 0, R.chead = 0, R.lane = lane;
+  sweep_task<MODE>(S, R, w, wb, ws_max, lane, false);
 }
 
 }  // namespace dev
