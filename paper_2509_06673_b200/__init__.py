@@ -35,7 +35,8 @@ __all__ = [
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "_lib", "libporofeti_b200.so")
+# PF_LIB=prof selects the cycle-accounting build (make prof); default: product build
+LIB_PATH = os.path.join(PKG, "_lib", "libporofeti_b200" + ("_" + os.environ["PF_LIB"] if os.environ.get("PF_LIB") else "") + ".so")
 
 SCENARIOS = {"mms-t": 0, "mms": 1, "injection": 2, "barry-mercer": 3}
 PRECONDS = {"identity": 0, "generalized": 1, "dirichlet": 2, "generalized-mortar": 3, "dirichlet-mortar": 4}

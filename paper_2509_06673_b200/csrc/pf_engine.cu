@@ -108,7 +108,7 @@ struct SolveSystem {
   std::vector<long long> prob_x, prob_lval, prob_cb;
   long long total_x = 0, total_L = 0, total_cb = 0;
   int nlevel = 0;
-  std::vector<int> level_nwork, level_ws;  // per global level
+  std::vector<int> level_nwork, level_ws, level_smax;  // per global level
   std::vector<long long> level_cols, level_vals;  // per global level (all problems)
   std::vector<DevBuf<int>> d_wp, d_wt;     // per global level work lists
   DevBuf<dev::TypeDesc> d_types;
@@ -117,11 +117,10 @@ struct SolveSystem {
       d_fold_ptr, d_fold_idx, d_prob_type, d_perm, d_prob_n;
   DevBuf<long long> d_sn_rowoff, d_sn_valoff, d_prob_x, d_prob_lval, d_prob_cb, d_prob_perm;
   DevBuf<double> L, D, X, CB;
-  DevBuf<int4> d_meta;
+  DevBuf<int2> d_meta;
   DevBuf<uint16_t> d_slots16;
   DevBuf<long long> d_tlbeg;
-  DevBuf<unsigned long long> d_udesc;
-  DevBuf<int> d_tuf, d_tnuf, d_tub, d_tnub;
+  DevBuf<int> d_tlbytes;
   int smax = 8;  // max supernode row count (padded to 8)
   // dense top (single-problem systems): levels >= top_level replaced by X_top = W y_top
   int top_level = -1, ntop = 0, top_c0 = 0;
@@ -135,16 +134,15 @@ struct SolveSystem {
     prob_type = ptype;
     nrhs_alloc = nrhs;
     std::vector<dev::TypeDesc> td(types.size());
-    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm, tuf, tnuf, tub,
-        tnub;
+    std::vector<int> sn_col0, sn_ncol, sn_nrow, slot, t0, t1, c0, c1, cbo, cbl, cbrows, fptr, fidx, perm, tlbytes;
     std::vector<long long> sn_rowoff, sn_valoff, type_perm_off, tlbeg;
-    std::vector<unsigned long long> udesc;
-    std::vector<int4> meta;
+    std::vector<int2> meta;
     std::vector<uint16_t> slots16;
     smax = 8;
     nlevel = 0;
     for (auto* F : types) nlevel = std::max(nlevel, F->nlevel);
     level_ws.assign(nlevel, 0);
+    level_smax.assign(nlevel, 8);
     auto glevel = [&](const SymFactor& F, int l) { return l == F.nlevel - 1 ? nlevel - 1 : l; };
     for (std::size_t k = 0; k < types.size(); ++k) {
       const SymFactor& F = *types[k];
@@ -157,8 +155,6 @@ struct SolveSystem {
       T.fold_base = (long long)fptr.size();
       T.foldidx_base = (long long)fidx.size();
       T.slot_base = (long long)slots16.size();
-      if (udesc.size() & 1) udesc.push_back(0);
-      T.udesc_base = (long long)udesc.size();
       std::vector<long long> sn_slot(F.nsn);
       for (int s = 0; s < F.nsn; ++s) {
         sn_col0.push_back(F.sn_col0[s]), sn_ncol.push_back(F.sn_ncol[s]), sn_nrow.push_back(F.sn_nrow[s]);
@@ -169,7 +165,8 @@ struct SolveSystem {
         const long long vrel = 8 * (F.sn_valoff[s] - F.sn_valoff[ts]);
         if (vrel > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
         sn_slot[s] = (long long)slots16.size() - T.slot_base;
-        meta.push_back(make_int4(F.sn_ncol[s], m, (int)sn_slot[s], (int)vrel));
+        if (F.sn_ncol[s] > 65535 || m > 65535) fail(kInternal, "supernode exceeds 16-bit sweep metadata");
+        meta.push_back(make_int2(F.sn_ncol[s] | (m << 16), (int)sn_slot[s]));
         for (int i = 0; i < m; ++i) {
           const int v = F.slot[F.sn_rowoff[s] + i];
           if (v < 0 || v > 65535) fail(kInternal, "sweep slot out of uint16 range");
@@ -187,48 +184,15 @@ struct SolveSystem {
         if (F.task_sn1[t] - F.task_sn0[t] > kMaxTaskSn) fail(kInternal, "sweep task exceeds kMaxTaskSn supernodes");
         if (F.sn_valoff[F.task_sn0[t]] & 1) fail(kInternal, "task value stream layout");
         tlbeg.push_back(F.sn_valoff[F.task_sn0[t]]);
-        // unit descriptors in the sweep kernel's consumption order (pf_sweep.cuh)
-        const long long ub = T.udesc_base;
-        if (udesc.size() & 1) udesc.push_back(0);  // lists start 16-byte aligned (staged by bulk copies)
-        tuf.push_back((int)((long long)udesc.size() - ub));
-        long long pos = 0;
-        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
-          const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
-          udesc.push_back(dev::unit_desc(2 * sn_slot[k], ((m + 7) & ~7) * 2, dev::kSrcSlots));
-          for (int p0 = 0; p0 < nc; p0 += kPW) {
-            const int pw = std::min(kPW, nc - p0), nb = m - p0 - pw;
-            if (tri_pad(pw)) udesc.push_back(dev::unit_desc(pos, 8 * tri_pad(pw), dev::kSrcValues)), pos += 8 * tri_pad(pw);
-            for (int b0 = 0; b0 < nb; b0 += kRB) {
-              const int sz = 8 * even_up(std::min(kRB, nb - b0) * pw);
-              udesc.push_back(dev::unit_desc(pos, sz, dev::kSrcValues)), pos += sz;
-            }
-          }
-        }
-        const int tc0 = F.task_c0[t], tnc = F.task_c1[t] - tc0;
-        udesc.push_back(dev::unit_desc(8LL * (tc0 & ~1), 8 * even_up((tc0 & 1) + tnc), dev::kSrcDiag));
-        tnuf.push_back((int)((long long)udesc.size() - ub) - tuf.back());
-        if (pos > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
-        if (udesc.size() & 1) udesc.push_back(0);
-        tub.push_back((int)((long long)udesc.size() - ub));
-        for (int k = F.task_sn1[t] - 1; k >= F.task_sn0[t]; --k) {
-          const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
-          udesc.push_back(dev::unit_desc(2 * sn_slot[k], ((m + 7) & ~7) * 2, dev::kSrcSlots));
-          for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
-            const int pw = std::min(kPW, nc - p0), nb = m - p0 - pw;
-            if (nb > 0)
-              for (int b0 = ((nb - 1) / kRB) * kRB; b0 >= 0; b0 -= kRB) {
-                const int sz = 8 * even_up(std::min(kRB, nb - b0) * pw);
-                pos -= sz;
-                udesc.push_back(dev::unit_desc(pos, sz, dev::kSrcValues));
-              }
-            if (tri_pad(pw)) pos -= 8 * tri_pad(pw), udesc.push_back(dev::unit_desc(pos, 8 * tri_pad(pw), dev::kSrcValues));
-          }
-        }
-        if (pos != 0) fail(kInternal, "sweep unit descriptors do not cover the task stream");
-        tnub.push_back((int)((long long)udesc.size() - ub) - tub.back());
+        long long nbytes = 0;
+        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) nbytes += 8 * sn_size(F.sn_ncol[k], F.sn_nrow[k]);
+        if (nbytes > INT32_MAX) fail(kInternal, "task value stream exceeds int32 bytes");
+        tlbytes.push_back((int)nbytes);
         const int gl = glevel(F, F.task_level[t]);
         const int ws = (F.task_c1[t] - F.task_c0[t]) + F.task_cblen[t];
         level_ws[gl] = std::max(level_ws[gl], ws);
+        for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k)
+          level_smax[gl] = std::max(level_smax[gl], (F.sn_nrow[k] + 7) & ~7);
       }
       cbrows.insert(cbrows.end(), F.cb_rows.begin(), F.cb_rows.end());
       fptr.insert(fptr.end(), F.fold_ptr.begin(), F.fold_ptr.end());
@@ -279,9 +243,7 @@ struct SolveSystem {
     d_cbrows.upload(cbrows), d_fold_ptr.upload(fptr), d_fold_idx.upload(fidx);
     d_prob_type.upload(ptype), d_prob_x.upload(prob_x), d_prob_lval.upload(prob_lval), d_prob_cb.upload(prob_cb);
     d_perm.upload(perm), d_prob_perm.upload(pperm), d_prob_n.upload(pn);
-    udesc.push_back(0), udesc.push_back(0);  // staged list chunks round up to 16 bytes
-    d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_udesc.upload(udesc);
-    d_tuf.upload(tuf), d_tnuf.upload(tnuf), d_tub.upload(tub), d_tnub.upload(tnub);
+    d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_tlbytes.upload(tlbytes);
     L.alloc(total_L + 4);
     D.alloc(total_x + 2);  // the pivot unit of the last task may round up past the end
     X.alloc(total_x * nrhs);
@@ -311,8 +273,7 @@ struct SolveSystem {
     S.task_sn0 = d_t0.p, S.task_sn1 = d_t1.p, S.task_c0 = d_c0.p, S.task_c1 = d_c1.p;
     S.task_cboff = d_cbo.p, S.task_cblen = d_cbl.p, S.cb_rows = d_cbrows.p;
     S.fold_ptr = d_fold_ptr.p, S.fold_idx = d_fold_idx.p;
-    S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.udesc = d_udesc.p;
-    S.task_uf = d_tuf.p, S.task_nuf = d_tnuf.p, S.task_ub = d_tub.p, S.task_nub = d_tnub.p;
+    S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.task_lbytes = d_tlbytes.p;
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
     S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p;
@@ -327,22 +288,21 @@ struct SolveSystem {
   bool timed = false;
   double phase_ms[3] = {0, 0, 0};  // forward levels / root / backward levels
 
-  // warp-specialised sweep (producer warp + kWsCons consumers) unless PF_SWEEP_WS=0
-  static bool ws_sweep() {
-    static const bool v = !std::getenv("PF_SWEEP_WS") || std::atoi(std::getenv("PF_SWEEP_WS")) != 0;
-    return v;
+  // shared memory of a level's launch (its own workspace and slot-list bounds)
+  int lvl_ws(int l) const { return (level_ws[l] + 1) & ~1; }
+  int sweep_smem(int l) const {
+    return dev::kSweepWarps * dev::SweepSmem::bytes(lvl_ws(l), level_smax[l]) + dev::kSweepPad;
   }
   int sweep_smem() const {
-    return ws_sweep() ? dev::kWsCons * dev::WsSmem::bytes(ws_max, smax) + dev::kSweepPad
-                      : dev::kSweepWarps * dev::SweepSmem::bytes(ws_max, smax) + dev::kSweepPad;
+    int m = 0;
+    for (int l = 0; l < nlevel; ++l) m = std::max(m, sweep_smem(l));
+    return m;
   }
 
   template <int MODE>
-  void launch_mode(cudaStream_t st, const dev::SolveSet& S) {
-    if (ws_sweep())
-      dev::k_sweep_ws<MODE><<<cdiv(S.nwork, dev::kWsCons), 32 * (dev::kWsCons + 1), sweep_smem(), st>>>(S, ws_max, smax);
-    else
-      dev::k_sweep<MODE><<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(), st>>>(S, ws_max, smax);
+  void launch_mode(cudaStream_t st, const dev::SolveSet& S, int l) {
+    dev::k_sweep<MODE><<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(l), st>>>(
+        S, lvl_ws(l), level_smax[l]);
   }
 
   void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
@@ -350,10 +310,10 @@ struct SolveSystem {
     if (nrhs != 1) fail(kInternal, "the sweep kernels take one right-hand side");
     dev::SolveSet S = set(nrhs, l);
     static const bool probe = std::getenv("PF_SWEEP_PROBE") != nullptr;
-    if (probe && mode == 0) launch_mode<3>(st, S);
-    else if (mode == 0) launch_mode<0>(st, S);
-    else if (mode == 1) launch_mode<1>(st, S);
-    else launch_mode<2>(st, S);
+    if (probe && mode == 0) launch_mode<3>(st, S, l);
+    else if (mode == 0) launch_mode<0>(st, S, l);
+    else if (mode == 1) launch_mode<1>(st, S, l);
+    else launch_mode<2>(st, S, l);
     ::pf::g_launches++;
     ++launches;
   }
@@ -459,10 +419,8 @@ struct SolveSystem {
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_ws<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+
+
   }
 };
 
@@ -1796,6 +1754,7 @@ struct Engine {
       }
       PF_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       double delta = d0;
+      static const bool trace = std::getenv("PF_KRYLOV_TRACE") != nullptr;
       for (int k = 0; k < maxit; ++k) {
         F_(p, q);
         dot(n, p, q, 1);  // pKp
@@ -1812,6 +1771,7 @@ struct Engine {
         const double rzn = read_scal(3);
         delta = std::sqrt(std::max(rzn, 0.0));
         rep.iterations = k + 1;
+        if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, delta / d0);
         if (delta <= tol * d0) {
           rep.converged = 1;
           break;
@@ -2358,6 +2318,17 @@ int pf_debug_factor_solve(int n, const int* ptr, const int* col, const double* v
       stats[0] = F.nsn, stats[1] = F.ntask, stats[2] = F.nval, stats[3] = F.n - F.top_c0, stats[4] = F.max_task_ws;
       stats[5] = F.nsn - F.top_sn0;
     }
+  });
+}
+
+/// Sweep cycle accounting (library built with -DPF_SWEEP_PROF, `make prof`):
+/// copies and resets g_sweep_prof (4 modes x 8 counters); zeros otherwise.
+int pf_debug_sweep_prof(unsigned long long* out) {
+  return guarded(nullptr, [&] {
+    PF_CUDA_CHECK(cudaDeviceSynchronize());
+    PF_CUDA_CHECK(cudaMemcpyFromSymbol(out, pf::dev::g_sweep_prof, sizeof(unsigned long long) * 32));
+    const unsigned long long z[32] = {};
+    PF_CUDA_CHECK(cudaMemcpyToSymbol(pf::dev::g_sweep_prof, z, sizeof(z)));
   });
 }
 

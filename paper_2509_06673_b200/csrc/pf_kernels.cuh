@@ -24,7 +24,6 @@ struct TypeDesc {
   long long row_base, cb_base;       // into slot / cb_rows
   long long fold_base, foldidx_base; // into fold_ptr (n+1 per type) / fold_idx
   long long slot_base;               // into slots (uint16, per-supernode lists padded to 8)
-  long long udesc_base;              // into udesc (sweep unit descriptors)
 };
 
 struct SolveSet {
@@ -36,11 +35,10 @@ struct SolveSet {
   const int* cb_rows;                      // relative to type cb_base
   const int* fold_ptr;                     // per type: n+1 entries at fold_base (relative to foldidx_base)
   const int* fold_idx;                     // cb indices (relative to the problem's cb region)
-  const int4* sn_meta;                     // per supernode: ncol, nrow, slot offset (type-relative), 0
+  const int2* sn_meta;                     // per supernode: ncol | nrow << 16, slot offset (type-relative)
   const uint16_t* slots;                   // per supernode row -> workspace slot
   const long long* task_lbeg;              // task value stream start (type-relative, even)
-  const unsigned long long* udesc;         // sweep unit descriptors (pf_sweep.cuh)
-  const int *task_uf, *task_nuf, *task_ub, *task_nub;  // per task: forward / backward lists
+  const int* task_lbytes;                  // task value stream length (bytes)
   // problems
   int nprob;
   const int* prob_type;
