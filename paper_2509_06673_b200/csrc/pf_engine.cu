@@ -110,7 +110,9 @@ struct SolveSystem {
   int nlevel = 0;
   std::vector<int> level_nwork, level_ws, level_smax;  // per global level
   std::vector<long long> level_cols, level_vals;  // per global level (all problems)
+  std::vector<long long> level_cbl, level_folds;  // per global level, per type (non-zero tests only)
   std::vector<DevBuf<int>> d_wp, d_wt;     // per global level work lists
+  std::vector<DevBuf<dev::WorkRec>> d_work;
   DevBuf<dev::TypeDesc> d_types;
   std::vector<dev::TypeDesc> d_types_host;
   DevBuf<int> d_sn_col0, d_sn_ncol, d_sn_nrow, d_slot, d_t0, d_t1, d_c0, d_c1, d_cbo, d_cbl, d_cbrows,
@@ -143,6 +145,7 @@ struct SolveSystem {
     for (auto* F : types) nlevel = std::max(nlevel, F->nlevel);
     level_ws.assign(nlevel, 0);
     level_smax.assign(nlevel, 8);
+    level_cbl.assign(nlevel, 0), level_folds.assign(nlevel, 0);
     auto glevel = [&](const SymFactor& F, int l) { return l == F.nlevel - 1 ? nlevel - 1 : l; };
     for (std::size_t k = 0; k < types.size(); ++k) {
       const SymFactor& F = *types[k];
@@ -193,6 +196,8 @@ struct SolveSystem {
         level_ws[gl] = std::max(level_ws[gl], ws);
         for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k)
           level_smax[gl] = std::max(level_smax[gl], (F.sn_nrow[k] + 7) & ~7);
+        level_cbl[gl] += F.task_cblen[t];
+        level_folds[gl] += F.fold_ptr[F.task_c1[t]] - F.fold_ptr[F.task_c0[t]];
       }
       cbrows.insert(cbrows.end(), F.cb_rows.begin(), F.cb_rows.end());
       fptr.insert(fptr.end(), F.fold_ptr.begin(), F.fold_ptr.end());
@@ -224,12 +229,28 @@ struct SolveSystem {
       pn.push_back(F.n);
       pperm.push_back(type_perm_off[ptype[p]]);
     }
-    d_wp.clear(), d_wt.clear();
-    d_wp.resize(nlevel), d_wt.resize(nlevel);
+    d_wp.clear(), d_wt.clear(), d_work.clear();
+    d_wp.resize(nlevel), d_wt.resize(nlevel), d_work.resize(nlevel);
     level_nwork.assign(nlevel, 0);
     for (int l = 0; l < nlevel; ++l) {
       d_wp[l].upload(wp[l]), d_wt[l].upload(wt[l]);
       level_nwork[l] = (int)wp[l].size();
+      std::vector<dev::WorkRec> wr(wp[l].size());
+      for (std::size_t i = 0; i < wr.size(); ++i) {
+        const int p = wp[l][i], tt = wt[l][i];
+        const SymFactor& F = *types[ptype[p]];
+        const dev::TypeDesc& T = td[ptype[p]];
+        const int t = T.task_base + tt;
+        dev::WorkRec& r = wr[i];
+        r.lofs = prob_lval[p] + tlbeg[t], r.xofs = prob_x[p], r.cbofs = prob_cb[p];
+        r.c0 = F.task_c0[tt], r.nct = F.task_c1[tt] - F.task_c0[tt], r.cbo = F.task_cboff[tt], r.cbl = F.task_cblen[tt];
+        r.sn = T.sn_base + F.task_sn0[tt], r.nsn = F.task_sn1[tt] - F.task_sn0[tt], r.lbytes = tlbytes[t];
+        if (T.slot_base > INT32_MAX || T.fold_base > INT32_MAX || T.foldidx_base > INT32_MAX || T.cb_base > INT32_MAX)
+          fail(kInternal, "sweep type tables exceed int32");
+        r.slot_base = (int)T.slot_base, r.fold_base = (int)T.fold_base, r.foldidx_base = (int)T.foldidx_base;
+        r.cb_base = (int)T.cb_base, r.pad = 0;
+      }
+      d_work[l].upload(wr);
     }
     ws_max = 0;
     for (int l = 0; l < nlevel; ++l) ws_max = std::max(ws_max, level_ws[l]);
@@ -276,7 +297,7 @@ struct SolveSystem {
     S.sn_meta = d_meta.p, S.slots = d_slots16.p, S.task_lbeg = d_tlbeg.p, S.task_lbytes = d_tlbytes.p;
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
-    S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p;
+    S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p, S.work = d_work[level].p;
     S.L = L.p, S.D = D.p, S.X = X.p, S.CB = CB.p;
     S.nrhs = nrhs;
     S.x_stride = total_x, S.cb_stride = total_cb;
@@ -309,6 +330,18 @@ struct SolveSystem {
     if (level_nwork[l] == 0) return;
     if (nrhs != 1) fail(kInternal, "the sweep kernels take one right-hand side");
     dev::SolveSet S = set(nrhs, l);
+    // fold children into the level's columns (forward) / gather the ancestor
+    // values of its tasks (backward) so every task starts with contiguous loads
+    if (mode != 2 && level_folds[l]) {
+      dev::k_fold_level<<<cdiv(S.nwork, 8), 256, 0, st>>>(S);
+      ::pf::g_launches++;
+      ++launches;
+    }
+    if (mode == 2 && level_cbl[l]) {
+      dev::k_gather_level<<<cdiv(S.nwork, 8), 256, 0, st>>>(S);
+      ::pf::g_launches++;
+      ++launches;
+    }
     static const bool probe = std::getenv("PF_SWEEP_PROBE") != nullptr;
     if (probe && mode == 0) launch_mode<3>(st, S, l);
     else if (mode == 0) launch_mode<0>(st, S, l);

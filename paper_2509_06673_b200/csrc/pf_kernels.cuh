@@ -26,6 +26,21 @@ struct TypeDesc {
   long long slot_base;               // into slots (uint16, per-supernode lists padded to 8)
 };
 
+/// One work item of a sweep level, flattened on the host so a warp starts
+/// its task with a single 80-byte broadcast load instead of a chain of
+/// dependent lookups (problem -> type -> task -> ...).
+struct __align__(16) WorkRec {
+  long long lofs;   // value stream of the task: offset into L (doubles)
+  long long xofs;   // problem offset into X / D (prob_x)
+  long long cbofs;  // problem offset into CB (prob_cb)
+  int c0, nct, cbo, cbl;
+  int sn, nsn;      // first supernode (global index into sn_meta), count
+  int lbytes;       // value stream bytes
+  int slot_base;    // type's slot table base (uint16 elements)
+  int fold_base, foldidx_base, cb_base;  // type bases of fold_ptr / fold_idx / cb_rows
+  int pad;
+};
+
 struct SolveSet {
   const TypeDesc* types;
   const int *sn_col0, *sn_ncol, *sn_nrow;
@@ -46,6 +61,7 @@ struct SolveSet {
   // work list of one level: (problem, type-relative task)
   int nwork;
   const int *work_prob, *work_task;
+  const WorkRec* work;
   // data
   const double* L;
   const double* D;

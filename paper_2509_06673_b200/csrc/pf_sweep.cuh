@@ -340,29 +340,26 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
   const int pvo = wb + SweepSmem::piv(ws_max);
   const int slb = wb + SweepSmem::slots(ws_max);
   const int sls = (2 * smax + 15) & ~15;  // one slot buffer
-  const int p = S.work_prob[w];
-  const TypeDesc T = S.types[S.prob_type[p]];
-  const int t = T.task_base + S.work_task[w];
-  const int c0 = S.task_c0[t], c1 = S.task_c1[t], nct = c1 - c0;
-  const int cbo = S.task_cboff[t], cbl = S.task_cblen[t];
-  const int sn0 = S.task_sn0[t], nsn = S.task_sn1[t] - sn0;
+  const WorkRec wr = S.work[w];
+  const int c0 = wr.c0, nct = wr.nct, cbo = wr.cbo, cbl = wr.cbl, nsn = wr.nsn;
   StreamRing R;
   R.k.sbase = smem_u32(g_sm), R.k.wb = wb, R.k.lane = lane, R.r.phase = 0;
-  R.k.g = reinterpret_cast<const unsigned char*>(S.L + S.prob_lval[p] + S.task_lbeg[t]);
-  const int end = S.task_lbytes[t];
+  R.k.g = reinterpret_cast<const unsigned char*>(S.L + wr.lofs);
+  const int end = wr.lbytes;
   R.k.end16 = (end + 15) & ~15, R.k.lastc = (R.k.end16 - 1) / kCh;
   if (lane == 0) {
     for (int i = 0; i < kNs; ++i) mbar_init(R.k.bar(i), 1);
     fence_mbar_init();
   }
-  for (int i = lane; i < nsn; i += 32)
-    *reinterpret_cast<int2*>(g_sm + wb + SweepSmem::kMeta + 8 * i) = __ldg(S.sn_meta + T.sn_base + sn0 + i);
   __syncwarp();
-  const uint16_t* table = S.slots + T.slot_base;
-  double* X = S.X + S.prob_x[p];
-  double* CBp = S.CB + S.prob_cb[p];
+  if (MODE != 2) R.start_fwd(); else R.start_bwd();  // first chunks in flight during the prologue
+  for (int i = lane; i < nsn; i += 32)
+    *reinterpret_cast<int2*>(g_sm + wb + SweepSmem::kMeta + 8 * i) = __ldg(S.sn_meta + wr.sn + i);
+  __syncwarp();
+  const uint16_t* table = S.slots + wr.slot_base;
+  double* X = S.X + wr.xofs;
+  double* CBp = S.CB + wr.cbofs;
   if (MODE == 3) {
-    R.start_fwd();
     double acc = 0.0;
     for (int pos = 0; pos < end; pos += kMirror) {
       const int sz = min(kMirror, end - pos);
@@ -372,19 +369,15 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
     return;
   }
   if (MODE != 2) {
-    R.start_fwd();
-    // pivots and the first slot list: one cp.async group
-    const double* Dp = S.D + S.prob_x[p] + c0;
-    for (int i = lane; i < nct; i += 32) cp_async8(R.k.sbase + pvo + 8 * i, Dp + i);
+    // task inputs (children already folded into X by k_fold_level), pivots
+    // and the first slot list: one cp.async group
+    const double* Dp = S.D + wr.xofs + c0;
+    for (int i = lane; i < nct; i += 32) {
+      cp_async8(R.k.sbase + wso + 8 * i, X + c0 + i);
+      cp_async8(R.k.sbase + pvo + 8 * i, Dp + i);
+    }
     prefetch_slots(table, meta_at(wb, 0), R.k.sbase + slb, lane);
     cp_async_commit();
-    const int* fp = S.fold_ptr + T.fold_base;
-    const int* fi = S.fold_idx + T.foldidx_base;
-    for (int i = lane; i < nct; i += 32) {
-      double v = X[c0 + i];
-      for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) v += CBp[fi[q]];  // children, fixed order
-      ws_at(wso, i) = v;
-    }
     for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = 0.0;
     int pos = 0;
     PF_PROF(t_start = clock64() - tk0);
@@ -405,14 +398,14 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
     __syncwarp();
   }
   if (MODE == 1 || MODE == 2) {
-    R.start_bwd();
+    if (MODE == 1) R.start_bwd();
+    if (MODE == 2) {
+      // own values and the ancestor values (gathered into CB by k_gather_level)
+      for (int i = lane; i < nct; i += 32) cp_async8(R.k.sbase + wso + 8 * i, X + c0 + i);
+      for (int i = lane; i < cbl; i += 32) cp_async8(R.k.sbase + wso + 8 * (nct + i), CBp + cbo + i);
+    }
     prefetch_slots(table, meta_at(wb, nsn - 1), R.k.sbase + slb, lane);
     cp_async_commit();
-    if (MODE == 2) {
-      const int* cbr = S.cb_rows + T.cb_base + cbo;
-      for (int i = lane; i < nct; i += 32) ws_at(wso, i) = X[c0 + i];
-      for (int i = lane; i < cbl; i += 32) ws_at(wso, nct + i) = X[cbr[i]];
-    }
     int pos = end;
     PF_PROF(if (MODE == 2) t_start = clock64() - tk0);
     for (int k = nsn - 1, b = 0; k >= 0; --k, b ^= 1) {
@@ -439,6 +432,40 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
     atomicAdd(&g_sweep_prof[MODE][5], 1ull);
   }
 #endif
+}
+
+/// Forward fold of a level: X[c] += child contributions (fixed order), one
+/// warp per work item.  Runs between the sweeps of consecutive levels so a
+/// task's prologue is a contiguous asynchronous load.
+__global__ void k_fold_level(SolveSet S) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= S.nwork) return;
+  const WorkRec wr = S.work[w];
+  const int* fp = S.fold_ptr + wr.fold_base;
+  const int* fi = S.fold_idx + wr.foldidx_base;
+  const double* CBp = S.CB + wr.cbofs;
+  double* X = S.X + wr.xofs;
+  for (int i = lane; i < wr.nct; i += 32) {
+    const int q0 = fp[wr.c0 + i], q1 = fp[wr.c0 + i + 1];
+    if (q0 == q1) continue;
+    double v = X[wr.c0 + i];
+    for (int q = q0; q < q1; ++q) v += CBp[fi[q]];
+    X[wr.c0 + i] = v;
+  }
+}
+
+/// Backward gather of a level: CB[cbo + i] = X[cb_rows[i]] (the ancestor
+/// values of every task), one warp per work item.
+__global__ void k_gather_level(SolveSet S) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= S.nwork) return;
+  const WorkRec wr = S.work[w];
+  const int* cbr = S.cb_rows + wr.cb_base + wr.cbo;
+  double* CBp = S.CB + wr.cbofs + wr.cbo;
+  const double* X = S.X + wr.xofs;
+  for (int i = lane; i < wr.cbl; i += 32) CBp[i] = X[cbr[i]];
 }
 
 }  // namespace dev
