@@ -81,12 +81,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-constexpr int kCh = 2048;                 // bytes per bulk copy
-constexpr int kNs = 4;                    // chunks in the ring
+constexpr int kCh = 4096;                 // bytes per bulk copy
+constexpr int kNs = 2;                    // chunks in the ring
 constexpr int kRingB = kCh * kNs;         // ring bytes per warp
 constexpr int kHalfCols = 8;              // row blocks are consumed in halves of 8 columns
 constexpr int kMirror = kRB * kHalfCols * 8;  // largest piece consumed at once: mirrored behind the ring
-constexpr int kSweepWarps = 2;            // warps per CTA
+constexpr int kSweepWarps = 1;            // warps per CTA
 constexpr int kSweepPad = 256;            // slack after the last warp region
 static_assert(kMirror <= kCh, "a piece must fit in one chunk");
 static_assert(kPW == 2 * kHalfCols, "row blocks are split into two column halves");
@@ -116,6 +116,7 @@ __device__ __forceinline__ double& ws_at(int wso, int s) { return *reinterpret_c
 struct RingState {
   int keep, nx, wt;
   unsigned phase;
+  PF_PROF(long long tw;)
 };
 
 struct RingConst {
@@ -136,7 +137,9 @@ struct RingConst {
   }
   __device__ __forceinline__ void wait(RingState& r, int c) const {
     const int s = c % kNs;
+    PF_PROF(const long long t0 = clock64());
     mbar_wait(bar(s), (r.phase >> s) & 1u);
+    PF_PROF(r.tw += clock64() - t0);
     r.phase ^= 1u << s;
   }
 };
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
   const int c0 = wr.c0, nct = wr.nct, cbo = wr.cbo, cbl = wr.cbl, nsn = wr.nsn;
   StreamRing R;
   R.k.sbase = smem_u32(g_sm), R.k.wb = wb, R.k.lane = lane, R.r.phase = 0;
+  PF_PROF(R.r.tw = 0);
   R.k.g = reinterpret_cast<const unsigned char*>(S.L + wr.lofs);
   const int end = wr.lbytes;
   R.k.end16 = (end + 15) & ~15, R.k.lastc = (R.k.end16 - 1) / kCh;
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
 #ifdef PF_SWEEP_PROF
   if (lane == 0) {
     atomicAdd(&g_sweep_prof[MODE][0], (unsigned long long)(clock64() - tk0));
-    atomicAdd(&g_sweep_prof[MODE][1], (unsigned long long)R.t_wait);
+    atomicAdd(&g_sweep_prof[MODE][1], (unsigned long long)R.r.tw);
     atomicAdd(&g_sweep_prof[MODE][2], (unsigned long long)t_slot);
     atomicAdd(&g_sweep_prof[MODE][3], (unsigned long long)t_start);
     atomicAdd(&g_sweep_prof[MODE][5], 1ull);
