@@ -248,7 +248,7 @@ def run_ours(args, rank, world, dist):
         "sweep_phase_ms": ph,
         "e2e": {"value": e2e_s, "unit": "s/step", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "batched supernodal LDL^T sweep (k_leaf_fwd+k_top+k_leaf_bwd)",
+                     "traffic": traffic, "kernel": "batched supernodal LDL^T sweep (k_sweep forward/root/backward levels + k_fold_level/k_gather_level)",
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
         "gpu_launches": None,
         "clocks": clk.summary(),
