@@ -730,6 +730,8 @@ struct Engine {
   // Krylov workspace
   DevBuf<double> kr_r, kr_z, kr_p, kr_q, kr_d, kr_t, kr_tmp, kr_rhs, red_part, scal;
   std::vector<double> h_scal;
+  DevBuf<int> d_status;
+  int* h_status = nullptr;  // pinned (2 ints)
   // stats
   pf_info info{};
   std::string last_error;
@@ -832,6 +834,7 @@ struct Engine {
   }
 
   ~Engine() {
+    if (h_status) cudaFreeHost(h_status);
     if (comm) ncclCommDestroy(comm);
     if (st) cudaStreamDestroy(st);
   }
@@ -1567,6 +1570,8 @@ struct Engine {
     red_part.alloc(dev::kRedBlocks);
     scal.alloc(64);
     h_scal.assign(64, 0.0);
+    d_status.alloc(2);
+    if (!h_status) PF_CUDA_CHECK(cudaMallocHost(&h_status, 2 * sizeof(int)));
   }
 
   void fill_info() {
@@ -1771,49 +1776,65 @@ struct Engine {
     project(r);
     rep.iterations = 0;
     rep.converged = 0;
+    double* sc = scal.p;
+    int* stat = d_status.p;
+    static const bool trace = std::getenv("PF_KRYLOV_TRACE") != nullptr;
+    // the only host traffic of the loop: the status word (state, iterations)
+    auto status = [&]() {
+      PF_CUDA_CHECK(cudaMemcpyAsync(h_status, stat, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      return h_status[0];
+    };
+    auto rel_residual = [&]() {
+      double v;
+      PF_CUDA_CHECK(cudaMemcpyAsync(&v, sc + dev::KS_REL, sizeof(double), cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      return v;
+    };
+    auto breakdown = [&](int code) {
+      switch (code) {
+        case dev::KST_SIGMA: fail(kBreakdown, "sqmr: <q, Fq> vanished (Lanczos breakdown)");
+        case dev::KST_RHO: fail(kBreakdown, "sqmr: rho vanished");
+        case dev::KST_PKP: fail(kBreakdown, "feti_pcg: <p, Kp> not positive (operator not SPD?)");
+        default: fail(kBreakdown, "feti_pcg: preconditioned residual norm lost positivity");
+      }
+    };
     if (krylov == PF_KRYLOV_PCG) {
       // REF feti_pcg (feti.hpp:263-308)
       double* z = kr_z.p;
       double* p = kr_p.p;
       double* q = kr_q.p;
       M_(r, z);
-      dot(n, r, z, 0);  // rz
-      const double rz0 = read_scal(0);
-      const double d0 = std::sqrt(std::max(rz0, 0.0));
-      if (d0 == 0.0 || !(d0 > 0.0)) {
+      dot(n, r, z, dev::KS_RZ);
+      dev::k_ks_pcg_init<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+      if (status() == dev::KST_CONV) {
         rep.converged = 1;
         rep.rel_residual = 0.0;
         return;
       }
       PF_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-      double delta = d0;
-      static const bool trace = std::getenv("PF_KRYLOV_TRACE") != nullptr;
       for (int k = 0; k < maxit; ++k) {
         F_(p, q);
-        dot(n, p, q, 1);  // pKp
-        dot(n, p, p, 2);  // pp
-        PF_CUDA_CHECK(cudaMemcpyAsync(h_scal.data() + 1, scal.p + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        PF_CUDA_CHECK(cudaStreamSynchronize(st));
-        if (h_scal[1] <= 1e-14 * h_scal[2])
-          fail(kBreakdown, "feti_pcg: <p, Kp> not positive (operator not SPD?)");
-        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, 1.0, scal.p + 0, scal.p + 1, p, lambda); ::pf::g_launches++;
+        dot(n, p, q, dev::KS_PKP);
+        dot(n, p, p, dev::KS_PP);
+        dev::k_ks_pcg_alpha<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+        dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, 1.0, p, lambda); ::pf::g_launches++;
         project(q);
-        dev::k_axpy_dev<<<nb, 256, 0, st>>>(n, -1.0, scal.p + 0, scal.p + 1, q, r); ::pf::g_launches++;
+        dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, q, r); ::pf::g_launches++;
         M_(r, z);
-        dot(n, r, z, 3);  // rz_next
-        const double rzn = read_scal(3);
-        delta = std::sqrt(std::max(rzn, 0.0));
+        dot(n, r, z, dev::KS_RZN);
+        dev::k_ks_pcg_beta<<<1, 1, 0, st>>>(sc, stat, k, tol); ::pf::g_launches++;
+        const int s_ = status();
         rep.iterations = k + 1;
-        if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, delta / d0);
-        if (delta <= tol * d0) {
+        if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, rel_residual());
+        if (s_ == dev::KST_CONV) {
           rep.converged = 1;
           break;
         }
-        if (rzn <= 0.0) fail(kBreakdown, "feti_pcg: preconditioned residual norm lost positivity");
-        dev::k_xpay_dev<<<nb, 256, 0, st>>>(n, z, p, scal.p + 3, scal.p + 0); ::pf::g_launches++;
-        PF_CUDA_CHECK(cudaMemcpyAsync(scal.p + 0, scal.p + 3, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        if (s_ != dev::KST_RUN) breakdown(s_);
+        dev::k_xpay_s<<<nb, 256, 0, st>>>(n, z, p, sc + dev::KS_B); ::pf::g_launches++;
       }
-      rep.rel_residual = delta / d0;
+      rep.rel_residual = rel_residual();
       return;
     }
     // SQMR (Freund & Nachtigal) with the symmetric indefinite preconditioner
@@ -1821,50 +1842,38 @@ struct Engine {
     double* t = kr_t.p;
     double* d = kr_d.p;
     double* u = kr_z.p;
-    dot(n, r, r, 10);
-    double tau = std::sqrt(read_scal(10));
-    const double t0 = tau;
-    if (t0 == 0.0 || !(t0 > 0.0)) {
+    dot(n, r, r, dev::KS_RR);
+    dev::k_ks_sqmr_init<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+    if (status() == dev::KST_CONV) {
       rep.converged = 1;
       rep.rel_residual = 0.0;
       return;
     }
     M_(r, q);
-    dot(n, r, q, 0);  // rho
-    double rho = read_scal(0), theta = 0.0, est = t0;
+    dot(n, r, q, dev::KS_RHO);
     kr_d.zero(st);
     for (int k = 0; k < maxit; ++k) {
       F_(q, t);
       project(t);
-      dot(n, q, t, 1);  // sigma
-      const double sigma = read_scal(1);
-      if (sigma == 0.0 || !std::isfinite(sigma)) fail(kBreakdown, "sqmr: <q, Fq> vanished (Lanczos breakdown)");
-      const double a = rho / sigma;
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, -a, t, 1.0, r); ::pf::g_launches++;
-      dot(n, r, r, 2);
-      const double rn = std::sqrt(read_scal(2));
-      const double th_old = theta;
-      theta = rn / tau;
-      const double c = 1.0 / std::sqrt(1.0 + theta * theta);
-      tau = tau * theta * c;
-      h_scal[0] = rho, h_scal[1] = sigma, h_scal[4] = th_old, h_scal[5] = c;
-      PF_CUDA_CHECK(cudaMemcpyAsync(scal.p + 20, h_scal.data(), 6 * sizeof(double), cudaMemcpyHostToDevice, st));
-      dev::k_sqmr_dx<<<nb, 256, 0, st>>>(n, scal.p + 20, q, d, lambda); ::pf::g_launches++;
-      est = tau;  // quasi-residual norm tau_k <= tol ||r0|| (same rule as the oracle)
+      dot(n, q, t, dev::KS_SIGMA);
+      dev::k_ks_sqmr_a<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+      dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, t, r); ::pf::g_launches++;
+      dot(n, r, r, dev::KS_RR);
+      dev::k_ks_sqmr_tau<<<1, 1, 0, st>>>(sc, stat, k, tol); ::pf::g_launches++;
+      dev::k_sqmr_dx_s<<<nb, 256, 0, st>>>(n, sc, q, d, lambda); ::pf::g_launches++;
+      const int s_ = status();
       rep.iterations = k + 1;
-      if (est <= tol * t0) {
+      if (s_ == dev::KST_CONV) {
         rep.converged = 1;
         break;
       }
-      if (rho == 0.0) fail(kBreakdown, "sqmr: rho vanished");
+      if (s_ != dev::KST_RUN) breakdown(s_);
       M_(r, u);
-      dot(n, r, u, 3);
-      const double rho_n = read_scal(3);
-      const double b = rho_n / rho;
-      rho = rho_n;
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, u, b, q); ::pf::g_launches++;  // q = u + b q
+      dot(n, r, u, dev::KS_RHON);
+      dev::k_ks_sqmr_b<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+      dev::k_xpay_s<<<nb, 256, 0, st>>>(n, u, q, sc + dev::KS_B); ::pf::g_launches++;  // q = u + b q
     }
-    rep.rel_residual = est / t0;
+    rep.rel_residual = rel_residual();
   }
 
   // ------------------------------------------------------------------

@@ -250,6 +250,91 @@ __global__ void k_sqmr_dx(int n, const double* sc, const double* q, double* d, d
 }
 
 // ---------------------------------------------------------------------------
+// Krylov scalars on the device (only the status word crosses to the host):
+// single-thread kernels between the dot products update them; the vector
+// kernels read their coefficients from device memory.
+// status[0]: 0 running, 1 converged, >= 2 breakdown code; status[1]: iterations
+// ---------------------------------------------------------------------------
+enum : int {
+  KS_RHO = 32, KS_SIGMA, KS_A, KS_RR, KS_THETA, KS_THOLD, KS_C, KS_TAU, KS_T0, KS_RHON, KS_B, KS_REL,
+  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0
+};
+enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5 };
+
+/// y += sgn * (*coef) * x
+__global__ void k_axpy_s(int n, const double* coef, double sgn, const double* x, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double c = sgn * *coef;
+  if (i < n) y[i] += c * x[i];
+}
+/// y = x + (*coef) * y
+__global__ void k_xpay_s(int n, const double* x, double* y, const double* coef) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double c = *coef;
+  if (i < n) y[i] = x[i] + c * y[i];
+}
+/// SQMR: d = c^2 theta_old^2 d + c^2 a q; x += d
+__global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double c2 = sc[KS_C] * sc[KS_C];
+  const double dn = c2 * sc[KS_THOLD] * sc[KS_THOLD] * d[i] + c2 * sc[KS_A] * q[i];
+  d[i] = dn;
+  x[i] += dn;
+}
+__global__ void k_ks_sqmr_init(double* sc, int* status) {
+  const double t0 = sqrt(sc[KS_RR]);
+  sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0;
+  status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
+  if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
+}
+__global__ void k_ks_sqmr_a(double* sc, int* status) {
+  const double sigma = sc[KS_SIGMA];
+  if (sigma == 0.0 || !isfinite(sigma)) status[0] = KST_SIGMA;
+  sc[KS_A] = sc[KS_RHO] / sigma;
+}
+__global__ void k_ks_sqmr_tau(double* sc, int* status, int k, double tol) {
+  const double rn = sqrt(sc[KS_RR]);
+  const double th_old = sc[KS_THETA];
+  const double theta = rn / sc[KS_TAU];
+  const double c = 1.0 / sqrt(1.0 + theta * theta);
+  const double tau = sc[KS_TAU] * theta * c;
+  sc[KS_THOLD] = th_old, sc[KS_THETA] = theta, sc[KS_C] = c, sc[KS_TAU] = tau;
+  sc[KS_REL] = tau / sc[KS_T0];  // quasi-residual tau_k <= tol ||r0|| (oracle rule)
+  status[1] = k + 1;
+  if (status[0] == KST_RUN && tau <= tol * sc[KS_T0]) status[0] = KST_CONV;
+}
+__global__ void k_ks_sqmr_b(double* sc, int* status) {
+  if (sc[KS_RHO] == 0.0 && status[0] == KST_RUN) status[0] = KST_RHO;
+  sc[KS_B] = sc[KS_RHON] / sc[KS_RHO];
+  sc[KS_RHO] = sc[KS_RHON];
+}
+__global__ void k_ks_pcg_init(double* sc, int* status) {
+  const double d0 = sqrt(fmax(sc[KS_RZ], 0.0));
+  sc[KS_D0] = d0, sc[KS_REL] = 1.0;
+  status[0] = (d0 == 0.0 || !(d0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
+  if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
+}
+__global__ void k_ks_pcg_alpha(double* sc, int* status) {
+  if (sc[KS_PKP] <= 1e-14 * sc[KS_PP]) status[0] = KST_PKP;
+  sc[KS_A] = sc[KS_RZ] / sc[KS_PKP];
+}
+__global__ void k_ks_pcg_beta(double* sc, int* status, int k, double tol) {
+  const double rzn = sc[KS_RZN];
+  const double delta = sqrt(fmax(rzn, 0.0));
+  sc[KS_REL] = delta / sc[KS_D0];
+  status[1] = k + 1;
+  if (status[0] != KST_RUN) return;
+  if (delta <= tol * sc[KS_D0]) {
+    status[0] = KST_CONV;
+    return;
+  }
+  if (rzn <= 0.0) status[0] = KST_RZ;
+  sc[KS_B] = rzn / sc[KS_RZ];
+  sc[KS_RZ] = rzn;
+}
+
+// ---------------------------------------------------------------------------
 // Coarse space: dense symmetric GEMV  y = A x  (nc x nc, row-major)
 // ---------------------------------------------------------------------------
 __global__ void k_dense_gemv(int n, const double* A, const double* x, double* y) {
