@@ -56,6 +56,9 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
                "l"(src), "r"(bytes), "r"(b)
                : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned b, unsigned parity) {
   asm volatile(
       "{\n"
@@ -87,6 +90,7 @@ constexpr int kRingB = kCh * kNs;         // ring bytes per warp
 constexpr int kHalfCols = 8;              // row blocks are consumed in halves of 8 columns
 constexpr int kMirror = kRB * kHalfCols * 8;  // largest piece consumed at once: mirrored behind the ring
 constexpr int kSweepWarps = 1;            // warps per CTA
+constexpr int kL2Ahead = 2;               // chunks prefetched into L2 beyond the ring (forward order)
 constexpr int kSweepPad = 256;            // slack after the last warp region
 static_assert(kMirror <= kCh, "a piece must fit in one chunk");
 static_assert(kPW == 2 * kHalfCols, "row blocks are split into two column halves");
@@ -124,6 +128,7 @@ struct RingConst {
   unsigned sbase;          // shared address of g_sm
   int wb, end16, lastc, lane;
   __device__ __forceinline__ unsigned bar(int s) const { return sbase + wb + SweepSmem::kBar + 8 * s; }
+  template <int DIR>  // +1 forward stream, -1 backward stream
   __device__ __forceinline__ void issue(int c) const {
     if (lane == 0) {
       const int s = c % kNs, a = c * kCh, bytes = min(kCh, end16 - a);
@@ -133,6 +138,10 @@ struct RingConst {
       mbar_expect_tx(b, (unsigned)(bytes + mb));
       bulk_g2s(sbase + wb + s * kCh, g + a, (unsigned)bytes, b);
       if (mb) bulk_g2s(sbase + wb + kRingB, g + a, (unsigned)mb, b);
+      // deepen the pipeline beyond the ring: the chunk kL2Ahead further on in
+      // stream order is pulled into L2 now
+      const int pa = a + DIR * kL2Ahead * kCh;
+      if (kL2Ahead > 0 && pa >= 0 && pa < end16) prefetch_l2(g + pa, (unsigned)min(kCh, end16 - pa));
     }
   }
   __device__ __forceinline__ void wait(RingState& r, int c) const {
@@ -148,7 +157,7 @@ __device__ __noinline__ RingState ring_refill_fwd(RingState r, RingConst k, int 
   if (first > r.keep) {  // chunks below `first` are consumed: refill their slots
     r.keep = first;
     __syncwarp();
-    while (r.nx <= min(k.lastc, r.keep + kNs - 1)) k.issue(r.nx++);
+    while (r.nx <= min(k.lastc, r.keep + kNs - 1)) k.template issue<1>(r.nx++);
   }
   while (r.wt <= last) k.wait(r, r.wt++);
   return r;
@@ -157,7 +166,7 @@ __device__ __noinline__ RingState ring_refill_bwd(RingState r, RingConst k, int 
   if (last < r.keep) {
     r.keep = last;
     __syncwarp();
-    while (r.nx >= max(0, r.keep - kNs + 1)) k.issue(r.nx--);
+    while (r.nx >= max(0, r.keep - kNs + 1)) k.template issue<-1>(r.nx--);
   }
   while (r.wt >= first) k.wait(r, r.wt--);
   return r;
@@ -171,11 +180,11 @@ struct StreamRing {
 
   __device__ __forceinline__ void start_fwd() {
     r.nx = r.wt = r.keep = 0;
-    while (r.nx <= min(k.lastc, kNs - 1)) k.issue(r.nx++);
+    while (r.nx <= min(k.lastc, kNs - 1)) k.template issue<1>(r.nx++);
   }
   __device__ __forceinline__ void start_bwd() {
     r.nx = r.wt = r.keep = k.lastc;
-    while (r.nx >= max(0, k.lastc - kNs + 1)) k.issue(r.nx--);
+    while (r.nx >= max(0, k.lastc - kNs + 1)) k.template issue<-1>(r.nx--);
   }
   /// unit [pos, pos + sz) resident and contiguous; returns its g_sm offset
   __device__ __forceinline__ int need_fwd(int pos, int sz) {
