@@ -834,6 +834,7 @@ struct Engine {
   }
 
   ~Engine() {
+    if (kr_exec) cudaGraphExecDestroy(kr_exec);
     if (h_status) cudaFreeHost(h_status);
     if (comm) ncclCommDestroy(comm);
     if (st) cudaStreamDestroy(st);
@@ -1813,7 +1814,9 @@ struct Engine {
         return;
       }
       PF_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-      for (int k = 0; k < maxit; ++k) {
+      // iteration = [p = z + beta p (not in the first)] F p, alpha, lambda, r, M r, beta
+      auto iter = [&](bool first) {
+        if (!first) dev::k_xpay_s<<<nb, 256, 0, st>>>(n, z, p, sc + dev::KS_B), ::pf::g_launches++;
         F_(p, q);
         dot(n, p, q, dev::KS_PKP);
         dot(n, p, p, dev::KS_PP);
@@ -1823,16 +1826,19 @@ struct Engine {
         dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, q, r); ::pf::g_launches++;
         M_(r, z);
         dot(n, r, z, dev::KS_RZN);
-        dev::k_ks_pcg_beta<<<1, 1, 0, st>>>(sc, stat, k, tol); ::pf::g_launches++;
+        dev::k_ks_pcg_beta<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
+      };
+      for (int k = 0; k < maxit; ++k) {
+        if (k == 0) iter(true);
+        else graphed(lambda, 1, [&] { iter(false); });
         const int s_ = status();
-        rep.iterations = k + 1;
+        rep.iterations = h_status[1];
         if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, rel_residual());
         if (s_ == dev::KST_CONV) {
           rep.converged = 1;
           break;
         }
         if (s_ != dev::KST_RUN) breakdown(s_);
-        dev::k_xpay_s<<<nb, 256, 0, st>>>(n, z, p, sc + dev::KS_B); ::pf::g_launches++;
       }
       rep.rel_residual = rel_residual();
       return;
@@ -1852,28 +1858,69 @@ struct Engine {
     M_(r, q);
     dot(n, r, q, dev::KS_RHO);
     kr_d.zero(st);
-    for (int k = 0; k < maxit; ++k) {
+    // iteration = [u = M r, rho, q = u + b q (not in the first)] F q, sigma, r, tau, lambda
+    auto iter = [&](bool first) {
+      if (!first) {
+        M_(r, u);
+        dot(n, r, u, dev::KS_RHON);
+        dev::k_ks_sqmr_b<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+        dev::k_xpay_s<<<nb, 256, 0, st>>>(n, u, q, sc + dev::KS_B); ::pf::g_launches++;  // q = u + b q
+      }
       F_(q, t);
       project(t);
       dot(n, q, t, dev::KS_SIGMA);
       dev::k_ks_sqmr_a<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
       dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, t, r); ::pf::g_launches++;
       dot(n, r, r, dev::KS_RR);
-      dev::k_ks_sqmr_tau<<<1, 1, 0, st>>>(sc, stat, k, tol); ::pf::g_launches++;
+      dev::k_ks_sqmr_tau<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
       dev::k_sqmr_dx_s<<<nb, 256, 0, st>>>(n, sc, q, d, lambda); ::pf::g_launches++;
+    };
+    for (int k = 0; k < maxit; ++k) {
+      if (k == 0) iter(true);
+      else graphed(lambda, 2, [&] { iter(false); });
       const int s_ = status();
-      rep.iterations = k + 1;
+      rep.iterations = h_status[1];
       if (s_ == dev::KST_CONV) {
         rep.converged = 1;
         break;
       }
       if (s_ != dev::KST_RUN) breakdown(s_);
-      M_(r, u);
-      dot(n, r, u, dev::KS_RHON);
-      dev::k_ks_sqmr_b<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
-      dev::k_xpay_s<<<nb, 256, 0, st>>>(n, u, q, sc + dev::KS_B); ::pf::g_launches++;  // q = u + b q
     }
     rep.rel_residual = rel_residual();
+  }
+
+  /// Run `body` (a fixed sequence of launches on st) as a CUDA graph: captured
+  /// once per (lambda buffer, Krylov kind) and replayed; host launch gaps vanish.
+  /// Not used with a host reducer (it synchronises) or while phase timing.
+  cudaGraphExec_t kr_exec = nullptr;
+  const void* kr_key_ptr = nullptr;
+  int kr_key_kind = 0;
+  long long kr_nlaunch = 0;
+  int kr_dF = 0, kr_dM = 0;
+  template <class Fn>
+  void graphed(const void* key, int kind, Fn&& body) {
+    static const bool off = std::getenv("PF_NO_GRAPH") != nullptr;
+    if (off || reducer || Ksys.timed || Isys.timed || Qsys.timed) {
+      body();
+      return;
+    }
+    if (!kr_exec || kr_key_ptr != key || kr_key_kind != kind) {
+      if (kr_exec) cudaGraphExecDestroy(kr_exec), kr_exec = nullptr;
+      const long long l0 = ::pf::g_launches;
+      const int f0 = fapplies, m0 = papplies;
+      cudaGraph_t g;
+      PF_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      body();
+      PF_CUDA_CHECK(cudaStreamEndCapture(st, &g));
+      PF_CUDA_CHECK(cudaGraphInstantiate(&kr_exec, g, 0));
+      PF_CUDA_CHECK(cudaGraphDestroy(g));
+      kr_nlaunch = ::pf::g_launches - l0, ::pf::g_launches = l0;
+      kr_dF = fapplies - f0, kr_dM = papplies - m0, fapplies = f0, papplies = m0;
+      kr_key_ptr = key, kr_key_kind = kind;
+    }
+    PF_CUDA_CHECK(cudaGraphLaunch(kr_exec, st));
+    ::pf::g_launches += kr_nlaunch;
+    fapplies += kr_dF, papplies += kr_dM;
   }
 
   // ------------------------------------------------------------------

@@ -293,7 +293,7 @@ __global__ void k_ks_sqmr_a(double* sc, int* status) {
   if (sigma == 0.0 || !isfinite(sigma)) status[0] = KST_SIGMA;
   sc[KS_A] = sc[KS_RHO] / sigma;
 }
-__global__ void k_ks_sqmr_tau(double* sc, int* status, int k, double tol) {
+__global__ void k_ks_sqmr_tau(double* sc, int* status, double tol) {
   const double rn = sqrt(sc[KS_RR]);
   const double th_old = sc[KS_THETA];
   const double theta = rn / sc[KS_TAU];
@@ -301,7 +301,7 @@ __global__ void k_ks_sqmr_tau(double* sc, int* status, int k, double tol) {
   const double tau = sc[KS_TAU] * theta * c;
   sc[KS_THOLD] = th_old, sc[KS_THETA] = theta, sc[KS_C] = c, sc[KS_TAU] = tau;
   sc[KS_REL] = tau / sc[KS_T0];  // quasi-residual tau_k <= tol ||r0|| (oracle rule)
-  status[1] = k + 1;
+  status[1] += 1;
   if (status[0] == KST_RUN && tau <= tol * sc[KS_T0]) status[0] = KST_CONV;
 }
 __global__ void k_ks_sqmr_b(double* sc, int* status) {
@@ -319,11 +319,11 @@ __global__ void k_ks_pcg_alpha(double* sc, int* status) {
   if (sc[KS_PKP] <= 1e-14 * sc[KS_PP]) status[0] = KST_PKP;
   sc[KS_A] = sc[KS_RZ] / sc[KS_PKP];
 }
-__global__ void k_ks_pcg_beta(double* sc, int* status, int k, double tol) {
+__global__ void k_ks_pcg_beta(double* sc, int* status, double tol) {
   const double rzn = sc[KS_RZN];
   const double delta = sqrt(fmax(rzn, 0.0));
   sc[KS_REL] = delta / sc[KS_D0];
-  status[1] = k + 1;
+  status[1] += 1;
   if (status[0] != KST_RUN) return;
   if (delta <= tol * sc[KS_D0]) {
     status[0] = KST_CONV;
