@@ -173,31 +173,41 @@ __device__ __noinline__ RingState ring_refill_bwd(RingState r, RingConst k, int 
 }
 
 /// The task's value stream in a shared-memory chunk ring (warp-uniform state).
+/// The fast path of need_*() is two compares against byte thresholds that
+/// the out-of-line refill keeps current.
 struct StreamRing {
   RingConst k;
   RingState r;
+  int lim, rel;  // fwd: resident below lim, release when pos >= rel; bwd: resident from lim, release when end <= rel
   long long t_wait = 0;  // PF_SWEEP_PROF (not tracked in the out-of-line path)
 
   __device__ __forceinline__ void start_fwd() {
     r.nx = r.wt = r.keep = 0;
     while (r.nx <= min(k.lastc, kNs - 1)) k.template issue<1>(r.nx++);
+    lim = 0, rel = kCh;
   }
   __device__ __forceinline__ void start_bwd() {
     r.nx = r.wt = r.keep = k.lastc;
     while (r.nx >= max(0, k.lastc - kNs + 1)) k.template issue<-1>(r.nx--);
+    lim = (k.lastc + 1) * kCh, rel = k.lastc * kCh;
   }
   /// unit [pos, pos + sz) resident and contiguous; returns its g_sm offset
   __device__ __forceinline__ int need_fwd(int pos, int sz) {
-    const int first = pos / kCh, last = (pos + sz - 1) / kCh;
-    if (first > r.keep || last >= r.wt) r = ring_refill_fwd(r, k, first, last);
-    return k.wb + pos % kRingB;
+    if (pos + sz > lim || pos >= rel) {
+      r = ring_refill_fwd(r, k, pos / kCh, (pos + sz - 1) / kCh);
+      lim = r.wt * kCh, rel = (r.keep + 1) * kCh;
+    }
+    return k.wb + (pos & (kRingB - 1));
   }
   __device__ __forceinline__ int need_bwd(int pos, int sz) {
-    const int first = pos / kCh, last = (pos + sz - 1) / kCh;
-    if (last < r.keep || first <= r.wt) r = ring_refill_bwd(r, k, first, last);
-    return k.wb + pos % kRingB;
+    if (pos < lim || pos + sz <= rel) {
+      r = ring_refill_bwd(r, k, pos / kCh, (pos + sz - 1) / kCh);
+      lim = (r.wt + 1) * kCh, rel = r.keep * kCh;
+    }
+    return k.wb + (pos & (kRingB - 1));
   }
 };
+static_assert((kRingB & (kRingB - 1)) == 0, "ring size must be a power of two");
 
 // Forward elimination of one panel; PWC >= pw compile-time bound, EXACT:
 // pw == PWC.  The panel's own columns occupy consecutive workspace slots, so
