@@ -125,7 +125,7 @@ struct SolveSystem {
   DevBuf<int> d_tlbytes;
   int smax = 8;  // max supernode row count (padded to 8)
   // dense top (single-problem systems): levels >= top_level replaced by X_top = W y_top
-  int top_level = -1, ntop = 0, top_c0 = 0;
+  int top_level = -1, ntop = 0, top_c0 = 0, top_cb0 = 0;
   DevBuf<double> W, Wres;
   int nrhs_alloc = 1;
   long long nnzL = 0;
@@ -337,11 +337,6 @@ struct SolveSystem {
       ::pf::g_launches++;
       ++launches;
     }
-    if (mode == 2 && level_cbl[l]) {
-      dev::k_gather_level<<<cdiv(S.nwork, 8), 256, 0, st>>>(S);
-      ::pf::g_launches++;
-      ++launches;
-    }
     static const bool probe = std::getenv("PF_SWEEP_PROBE") != nullptr;
     if (probe && mode == 0) launch_mode<3>(st, S, l);
     else if (mode == 0) launch_mode<0>(st, S, l);
@@ -363,11 +358,16 @@ struct SolveSystem {
       if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
       for (int l = 0; l < top_level; ++l) launch_level(st, nrhs, l, 0);
       if (timed) cudaEventRecord(ev[1], st);
-      dev::k_dense_top_gather<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, d_fold_ptr.p + d_types_host[0].fold_base,
+      dev::k_dense_top_gather<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, top_cb0,
+                                                              d_fold_ptr.p + d_types_host[0].fold_base,
                                                               d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, X.p,
                                                               Wres.p);
       dev::k_dense_top_gemv<<<std::min(cdiv(ntop, 8), 2 * 148), 256, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p,
                                                                                                    Wres.p, X.p);
+      dev::k_scatter_cols<<<cdiv(ntop, 256), 256, 0, st>>>(top_c0, ntop, top_cb0, d_fold_ptr.p + d_types_host[0].fold_base,
+                                                           d_fold_idx.p + d_types_host[0].foldidx_base, X.p, CB.p);
+      ::pf::g_launches++;
+      launches++;
       ::pf::g_launches += 2;
       launches += 2;
       if (timed) cudaEventRecord(ev[2], st);
@@ -440,7 +440,7 @@ struct SolveSystem {
       for (int j = i + 1; j < n; ++j) Wh[(std::size_t)i * n + j] = Wh[(std::size_t)j * n + i];
     W.upload(Wh);
     Wres.alloc(n);
-    top_level = L, ntop = n, top_c0 = c0;
+    top_level = L, ntop = n, top_c0 = c0, top_cb0 = F.task_cboff[F.level_ptr[L]];
   }
 
   void prepare_smem() {

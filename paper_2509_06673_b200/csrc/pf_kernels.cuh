@@ -349,12 +349,18 @@ __global__ void k_dense_gemv(int n, const double* A, const double* x, double* y)
 
 /// Dense top of a single-problem sweep, pass 1: y = X[c0..c0+n) + folded
 /// child contributions (fixed order).
-__global__ void k_dense_top_gather(int n, int c0, const int* __restrict__ fold_ptr, const int* __restrict__ fold_idx,
-                                   const double* __restrict__ CB, const double* X, double* y) {
+/// Only contributions of the sparse levels (CB index < cb_top) count: the
+/// top tasks' own couplings are inside W.
+__global__ void k_dense_top_gather(int n, int c0, int cb_top, const int* __restrict__ fold_ptr,
+                                   const int* __restrict__ fold_idx, const double* __restrict__ CB, const double* X,
+                                   double* y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = X[c0 + i];
-  for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) v += CB[fold_idx[q]];
+  for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) {
+    const int f = fold_idx[q];
+    if (f < cb_top) v += CB[f];
+  }
   y[i] = v;
 }
 

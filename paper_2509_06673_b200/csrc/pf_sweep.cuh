@@ -446,6 +446,17 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 2) k_sweep(SolveSet S, int w
   cp_async_wait<0>();
   __syncwarp();
   for (int i = lane; i < nct; i += 32) X[c0 + i] = ws_at(wso, i);
+  if (MODE == 1 || MODE == 2) {
+    // backward: hand the final values to every descendant task that reads
+    // them (the transpose of the forward fold: each CB entry has one writer),
+    // so their prologues are contiguous loads
+    const int* fp = S.fold_ptr + wr.fold_base;
+    const int* fi = S.fold_idx + wr.foldidx_base;
+    for (int i = lane; i < nct; i += 32) {
+      const double v = ws_at(wso, i);
+      for (int q = fp[c0 + i]; q < fp[c0 + i + 1]; ++q) CBp[fi[q]] = v;
+    }
+  }
 #ifdef PF_SWEEP_PROF
   if (lane == 0) {
     atomicAdd(&g_sweep_prof[MODE][0], (unsigned long long)(clock64() - tk0));
@@ -478,17 +489,17 @@ __global__ void k_fold_level(SolveSet S) {
   }
 }
 
-/// Backward gather of a level: CB[cbo + i] = X[cb_rows[i]] (the ancestor
-/// values of every task), one warp per work item.
-__global__ void k_gather_level(SolveSet S) {
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= S.nwork) return;
-  const WorkRec wr = S.work[w];
-  const int* cbr = S.cb_rows + wr.cb_base + wr.cbo;
-  double* CBp = S.CB + wr.cbofs + wr.cbo;
-  const double* X = S.X + wr.xofs;
-  for (int i = lane; i < wr.cbl; i += 32) CBp[i] = X[cbr[i]];
+/// Backward hand-off of columns [c0, c0 + n) of a single-problem system (the
+/// dense top block): CB[fold_idx[q]] = X[c] for every fold entry q of c.
+__global__ void k_scatter_cols(int c0, int n, int cb_top, const int* __restrict__ fold_ptr,
+                               const int* __restrict__ fold_idx, const double* __restrict__ X, double* CB) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = X[c0 + i];
+  for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) {
+    const int f = fold_idx[q];
+    if (f < cb_top) CB[f] = v;  // entries of the sparse levels only (top tasks never run)
+  }
 }
 
 }  // namespace dev
