@@ -75,6 +75,7 @@ typedef struct pf_info {
   double bytes_fapply;  /* algorithmic bytes of one F-apply (SURVEY §8d B_F) */
   double bytes_precond; /* algorithmic bytes of one preconditioner apply */
   int n_levels;         /* task levels of the subdomain sweep schedule */
+  int dual;             /* 1: explicit local dual operators (F-apply / Dirichlet as dense GEMVs) */
 } pf_info;
 
 typedef struct pf_sub_info {

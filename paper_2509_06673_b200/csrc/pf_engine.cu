@@ -25,7 +25,9 @@
 #include "pf_kernels.cuh"
 #include "pf_factor.cuh"
 #include "pf_sweep.cuh"
+#include "pf_dual.cuh"
 #include "pf_symbolic.hpp"
+#include "pf_dual.hpp"
 
 namespace pf {
 
@@ -680,6 +682,11 @@ struct Engine {
   std::vector<std::vector<int>> itype_pos;     // type: natural -> interior index or -1
   SymFactor qsym;
   bool use_q = false, use_dir = false, use_gen = false;
+  // explicit local dual operators (pf_dual.hpp): F-apply and Dirichlet
+  // preconditioner as batched dense GEMVs; implicit_dir = Dirichlet through
+  // the interior-factor sweeps (PF_FAPPLY=implicit, or a type not supported)
+  bool dual = false, implicit_dir = false;
+  std::vector<DualType> dtypes;
   int krylov = PF_KRYLOV_PCG;
   // systems
   SolveSystem Ksys, Isys, Qsys;
@@ -775,10 +782,27 @@ struct Engine {
     isym.resize(nt);
     itype_index.resize(nt);
     itype_pos.resize(nt);
+    const char* fa = std::getenv("PF_FAPPLY");
+    const bool want_dual = !(fa && std::string(fa) == "implicit");
+    std::vector<int> rep(nt, -1);
+    for (int p = 0; p < nown(); ++p)
+      if (rep[OS(p).type] < 0) rep[OS(p).type] = own[p];
+    dtypes.assign(nt, DualType());
+    if (want_dual)
+      parallel_for(nt, nthreads, [&](int t) {
+        if (rep[t] >= 0) dtypes[t] = build_dual_type(D.types[t], D.subs[rep[t]]);
+      });
+    dual = want_dual;
+    for (int t = 0; t < nt; ++t)
+      if (rep[t] >= 0 && want_dual && !dtypes[t].ok) {
+        dual = false;
+        if (std::getenv("PF_VERBOSE")) std::fprintf(stderr, "[pf] dual operators off: %s\n", dtypes[t].why.c_str());
+      }
+    implicit_dir = use_dir && !dual;
     parallel_for(nt, nthreads, [&](int t) {
       const SubType& T = D.types[t];
       ksym[t] = analyse(T.K, T.dof_ic, task_cap(T.K.nnz()), task_ws());
-      if (use_dir) {
+      if (implicit_dir) {
         std::vector<char> isB(T.dim, 0);
         for (int b : T.Bset) isB[b] = 1;
         auto& idx = itype_index[t];
@@ -803,9 +827,10 @@ struct Engine {
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
     const auto t2 = std::chrono::steady_clock::now();
     factor_all();
+    if (dual) setup_dual();
     const auto t3 = std::chrono::steady_clock::now();
     setup_lambda_maps();
-    if (use_dir) setup_dirichlet();
+    if (implicit_dir) setup_dirichlet();
     if (use_gen) setup_generalized();
     if (use_q) setup_q();
     if (floating_any) setup_coarse();
@@ -820,6 +845,11 @@ struct Engine {
           std::fprintf(stderr, "[pf]   level %d: %d tasks, max ws %d, cols %lld, values %lld\n", l, S.level_nwork[l],
                        S.level_ws[l], S.level_cols[l], S.level_vals[l]);
       };
+      if (dual)
+        for (std::size_t t = 0; t < dtypes.size(); ++t)
+          if (dtypes[t].ok)
+            std::fprintf(stderr, "[pf] dual type %zu: B %d, multipliers %d, fronts %lld doubles, root %d\n", t,
+                         dtypes[t].nB, dtypes[t].nM, dtypes[t].M.fsize, dtypes[t].root);
       dump("K", Ksys);
       dump("K_II", Isys);
       dump("Q", Qsys);
@@ -963,7 +993,7 @@ struct Engine {
     std::vector<int> ptype(ns);
     for (int s = 0; s < ns; ++s) ptype[s] = OS(s).type;
     Ksys.build(kt, ptype, 1);
-    if (use_dir) Isys.build(it, ptype, 1);
+    if (implicit_dir) Isys.build(it, ptype, 1);
     const bool host = std::getenv("PF_HOST_FACTOR") && std::atoi(std::getenv("PF_HOST_FACTOR")) != 0;
     if (host || use_gen) {
       h_K.resize(total_kv);
@@ -973,10 +1003,10 @@ struct Engine {
       factor_all_host();
     } else {
       factor_device(Ksys, ksym, false);
-      if (use_dir) factor_device(Isys, isym, true);
+      if (implicit_dir) factor_device(Isys, isym, true);
     }
     Ksys.prepare_smem();
-    if (use_dir) Isys.prepare_smem();
+    if (implicit_dir) Isys.prepare_smem();
     check_factor_residual();
   }
 
@@ -1012,15 +1042,49 @@ struct Engine {
         as[t] = build_ascatter(syms[t], fm[t], KII, kmap.data(), {});
       }
     });
-    // concatenate per-type maps
+    std::vector<const SymFactor*> sp(nt);
+    std::vector<const FrontMaps*> mp(nt);
+    std::vector<const AScatter*> ap(nt);
+    for (int t = 0; t < nt; ++t) sp[t] = &syms[t], mp[t] = &fm[t], ap[t] = &as[t];
+    FrontRun R;
+    R.syms = sp, R.fm = mp, R.as = ap, R.used = used;
+    R.L = Sys.L.p, R.D = Sys.D.p, R.prob_lval = Sys.d_prob_lval.p, R.prob_x = Sys.d_prob_x.p;
+    const int err = run_fronts(R, nullptr);
+    if (err)
+      fail(kSingular, std::string(interior ? "interior block" : "subdomain saddle") +
+                          " factorization failed (zero pivot)");
+  }
+
+  /// Inputs of one batched multifrontal run over the owned subdomains.
+  struct FrontRun {
+    std::vector<const SymFactor*> syms;
+    std::vector<const FrontMaps*> fm;
+    std::vector<const AScatter*> as;
+    std::vector<char> used;
+    double *L = nullptr, *D = nullptr;  // factor outputs (write_factor)
+    const long long *prob_lval = nullptr, *prob_x = nullptr;
+    int write_factor = 1;
+    std::vector<int> type_stop;          // root supernode per type (dual run), empty = none
+    const double* Gv = nullptr;          // bordered G values (dual run)
+    const long long* prob_gval = nullptr;
+  };
+
+  /// Batched multifrontal factorisation (k_mf_factor) over all owned
+  /// subdomains: fronts live in a chunk buffer; subdomains are processed in
+  /// chunks whose fronts fit PF_FRONT_GB (default 8 GB), one launch per etree
+  /// height.  `chunk_done(p0, p1, F, fbase)` runs after each chunk (before the
+  /// buffer is reused).  Returns the zero-pivot flag.
+  template <class ChunkFn>
+  int run_fronts(const FrontRun& R, ChunkFn* chunk_done) {
+    const int nt = (int)R.syms.size();
     std::vector<int> snbase(nt, 0), ncol, nrow, col0, ch_beg, ch_cnt, as_beg, as_cnt, ch_idx, relpos, as_kidx, as_fpos;
     std::vector<long long> valoff, foff, rp_beg;
     for (int t = 0; t < nt; ++t) {
       snbase[t] = (int)ncol.size();
-      if (!used[t]) continue;
-      const SymFactor& F = syms[t];
-      const FrontMaps& M = fm[t];
-      const AScatter& A = as[t];
+      if (!R.used[t]) continue;
+      const SymFactor& F = *R.syms[t];
+      const FrontMaps& M = *R.fm[t];
+      const AScatter& A = *R.as[t];
       for (int k = 0; k < F.nsn; ++k) {
         ncol.push_back(F.sn_ncol[k]), nrow.push_back(F.sn_nrow[k]), col0.push_back(F.sn_col0[k]);
         valoff.push_back(F.sn_valoff[k]), foff.push_back(M.foff[k]);
@@ -1035,13 +1099,14 @@ struct Engine {
       as_fpos.insert(as_fpos.end(), A.fpos.begin(), A.fpos.end());
     }
     DevBuf<int> d_snbase, d_ncol, d_nrow, d_col0, d_chb, d_chc, d_asb, d_asc, d_chi, d_rp, d_ask, d_asf, d_ptype, d_itp,
-        d_its, d_err;
+        d_its, d_err, d_stop;
     DevBuf<long long> d_valoff, d_foff, d_rpb, d_pkval, d_fbase;
     d_snbase.upload(snbase), d_ncol.upload(ncol), d_nrow.upload(nrow), d_col0.upload(col0);
     d_chb.upload(ch_beg), d_chc.upload(ch_cnt), d_asb.upload(as_beg), d_asc.upload(as_cnt);
     d_chi.upload(ch_idx.empty() ? std::vector<int>{0} : ch_idx), d_rp.upload(relpos.empty() ? std::vector<int>{0} : relpos);
     d_ask.upload(as_kidx), d_asf.upload(as_fpos);
     d_valoff.upload(valoff), d_foff.upload(foff), d_rpb.upload(rp_beg);
+    if (!R.type_stop.empty()) d_stop.upload(R.type_stop);
     const int np = nown();
     std::vector<long long> pkval(np);
     for (int p = 0; p < np; ++p) pkval[p] = h_fsubs[p].kval;
@@ -1053,40 +1118,41 @@ struct Engine {
     std::size_t fr = 0, tot = 0;
     PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
     const long long budget = (long long)std::min(gb * 1e9, 0.5 * (double)fr) / 8;
+    auto fsz = [&](int p) { return R.fm[OS(p).type]->fsize; };
     long long maxf = 0;
     for (int t = 0; t < nt; ++t)
-      if (used[t]) maxf = std::max(maxf, fm[t].fsize);
+      if (R.used[t]) maxf = std::max(maxf, R.fm[t]->fsize);
     if (maxf > budget) fail(kInternal, "a single subdomain's fronts exceed the front budget");
     std::vector<std::pair<int, int>> chunks;
     for (int p0 = 0; p0 < np;) {
       long long acc = 0;
       int p1 = p0;
-      while (p1 < np && acc + fm[OS(p1).type].fsize <= budget) acc += fm[OS(p1).type].fsize, ++p1;
+      while (p1 < np && acc + fsz(p1) <= budget) acc += fsz(p1), ++p1;
       chunks.emplace_back(p0, p1);
       p0 = p1;
     }
     long long fmax_chunk = 0;
     for (auto& c : chunks) {
       long long acc = 0;
-      for (int p = c.first; p < c.second; ++p) acc += fm[OS(p).type].fsize;
+      for (int p = c.first; p < c.second; ++p) acc += fsz(p);
       fmax_chunk = std::max(fmax_chunk, acc);
     }
     DevBuf<double> Fb;
     Fb.alloc(fmax_chunk);
     int maxh = 0;
     for (int t = 0; t < nt; ++t)
-      if (used[t]) maxh = std::max(maxh, fm[t].nheight);
+      if (R.used[t]) maxh = std::max(maxh, R.fm[t]->nheight);
     d_ptype.upload(ptype_of_own());
     for (auto& c : chunks) {
       std::vector<long long> fbase(np, 0);
       long long acc = 0;
-      for (int p = c.first; p < c.second; ++p) fbase[p] = acc, acc += fm[OS(p).type].fsize;
+      for (int p = c.first; p < c.second; ++p) fbase[p] = acc, acc += fsz(p);
       d_fbase.upload(fbase);
       std::vector<int> ip, is;
       std::vector<int> hptr(maxh + 1, 0);
       for (int h = 0; h < maxh; ++h) {
         for (int p = c.first; p < c.second; ++p) {
-          const FrontMaps& M = fm[OS(p).type];
+          const FrontMaps& M = *R.fm[OS(p).type];
           if (h >= M.nheight) continue;
           for (int q = M.height_ptr[h]; q < M.height_ptr[h + 1]; ++q) ip.push_back(p), is.push_back(M.height_sn[q]);
         }
@@ -1103,21 +1169,140 @@ struct Engine {
         S.ch_beg = d_chb.p, S.ch_cnt = d_chc.p, S.as_beg = d_asb.p, S.as_cnt = d_asc.p;
         S.ch_idx = d_chi.p, S.relpos = d_rp.p, S.as_kidx = d_ask.p, S.as_fpos = d_asf.p;
         S.nitem = n, S.it_prob = d_itp.p + hptr[h], S.it_sn = d_its.p + hptr[h];
-        S.prob_type = d_ptype.p, S.prob_kval = d_pkval.p, S.prob_lval = Sys.d_prob_lval.p, S.prob_x = Sys.d_prob_x.p;
+        S.prob_type = d_ptype.p, S.prob_kval = d_pkval.p, S.prob_lval = R.prob_lval, S.prob_x = R.prob_x;
         S.prob_fbase = d_fbase.p;
-        S.Kv = Kv.p, S.F = Fb.p, S.L = Sys.L.p, S.D = Sys.D.p, S.err = d_err.p;
+        S.Kv = Kv.p, S.F = Fb.p, S.L = R.L, S.D = R.D, S.err = d_err.p;
+        S.Gv = R.Gv, S.prob_gval = R.prob_gval, S.type_stop = R.type_stop.empty() ? nullptr : d_stop.p;
+        S.write_factor = R.write_factor;
         dev::k_mf_factor<<<n, 256, 0, st>>>(S);
         ::pf::g_launches++;
       }
+      if (chunk_done) (*chunk_done)(c.first, c.second, Fb.p, d_fbase.p, fbase);
       // the chunk's work lists / bases are freed by the next upload: finish first
       PF_CUDA_CHECK(cudaStreamSynchronize(st));
     }
     PF_CUDA_CHECK(cudaGetLastError());
     int err = 0;
     PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
-    if (err)
-      fail(kSingular, std::string(interior ? "interior block" : "subdomain saddle") +
-                          " factorization failed (zero pivot)");
+    return err;
+  }
+  int run_fronts(const FrontRun& R, std::nullptr_t) {
+    struct Nop {
+      void operator()(int, int, double*, const long long*, const std::vector<long long>&) {}
+    } nop;
+    return run_fronts(R, (Nop*)nullptr);
+  }
+
+  // ------------------------------------------------------------------
+  // explicit local dual operators (pf_dual.hpp / pf_dual.cuh)
+  DevBuf<int> dl_nloc, dl_lam, dl_rptr;
+  DevBuf<long long> dl_loff, dl_opoff, dl_rslot;
+  DevBuf<double> dl_F, dl_S, dl_xloc, dl_Y;
+  long long dl_nslots = 0, dl_opsize = 0;
+  int dl_nmax = 0;
+
+  /// F_s and Sd_s for every owned subdomain: one bordered partial
+  /// factorisation (multifrontal, root front kept) + k_dual_root per chunk.
+  void setup_dual() {
+    const int nt = (int)D.types.size(), np = nown();
+    std::vector<char> used(nt, 0);
+    for (int p = 0; p < np; ++p) used[OS(p).type] = 1;
+    // per subdomain: local multipliers and G values in the type's pattern order
+    std::vector<std::vector<int>> lam(np);
+    std::vector<std::vector<double>> gv(np);
+    std::vector<char> okp(np, 1);
+    parallel_for(np, nthreads, [&](int p) {
+      const Subdomain& S = OS(p);
+      okp[p] = dual_sub_values(dtypes[S.type], D.types[S.type], S, lam[p], gv[p]);
+    });
+    for (int p = 0; p < np; ++p)
+      if (!okp[p]) fail(kInternal, "dual operators: subdomain G pattern differs from its type's");
+    std::vector<long long> pgval(np), pop(np), ploff(np);
+    std::vector<double> gall;
+    std::vector<int> nloc(np), lamall;
+    dl_opsize = dl_nslots = 0, dl_nmax = 0;
+    for (int p = 0; p < np; ++p) {
+      const DualType& X = dtypes[OS(p).type];
+      pgval[p] = (long long)gall.size();
+      gall.insert(gall.end(), gv[p].begin(), gv[p].end());
+      pop[p] = dl_opsize, dl_opsize += (long long)X.nM * X.nM;
+      ploff[p] = dl_nslots, dl_nslots += X.nM;
+      nloc[p] = X.nM, dl_nmax = std::max(dl_nmax, X.nM);
+      lamall.insert(lamall.end(), lam[p].begin(), lam[p].end());
+    }
+    // per type tables
+    std::vector<int> tnB(nt, 0), tnM(nt, 0), tgptr(nt, 0), tgidx(nt, 0), tfix(nt, 0), tnfix(nt, 0), gptr, gb, fixp;
+    std::vector<long long> troot(nt, 0);
+    int mmax = 0;
+    for (int t = 0; t < nt; ++t) {
+      if (!used[t]) continue;
+      const DualType& X = dtypes[t];
+      tnB[t] = X.nB, tnM[t] = X.nM;
+      tgptr[t] = (int)gptr.size(), gptr.insert(gptr.end(), X.g_ptr.begin(), X.g_ptr.end());
+      tgidx[t] = (int)gb.size(), gb.insert(gb.end(), X.g_b.begin(), X.g_b.end());
+      tfix[t] = (int)fixp.size(), tnfix[t] = (int)X.fixpos.size(), fixp.insert(fixp.end(), X.fixpos.begin(), X.fixpos.end());
+      troot[t] = X.M.foff[X.root];
+      mmax = std::max(mmax, X.nB + X.nM);
+    }
+    if (fixp.empty()) fixp.push_back(0);
+    DevBuf<int> d_tnB, d_tnM, d_tgptr, d_tgidx, d_tfix, d_tnfix, d_gptr, d_gb, d_fixp, d_prob, d_ptype, d_err;
+    DevBuf<long long> d_troot, d_pgval, d_pop;
+    DevBuf<double> d_gall;
+    d_tnB.upload(tnB), d_tnM.upload(tnM), d_tgptr.upload(tgptr), d_tgidx.upload(tgidx), d_tfix.upload(tfix);
+    d_tnfix.upload(tnfix), d_gptr.upload(gptr), d_gb.upload(gb), d_fixp.upload(fixp), d_troot.upload(troot);
+    d_pgval.upload(pgval), d_pop.upload(pop), d_gall.upload(gall.empty() ? std::vector<double>{0.0} : gall);
+    d_ptype.upload(ptype_of_own());
+    d_err.upload(std::vector<int>{0});
+    dl_F.alloc(dl_opsize), dl_S.alloc(dl_opsize);
+    const int smem = (int)std::max<long long>(8LL * mmax, 8LL * mmax * dev::kDualLd);
+    if (smem > 227 * 1024) fail(kInternal, "dual root front too large for the shared-memory panel");
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_dual_root, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    std::vector<int> all(np);
+    std::iota(all.begin(), all.end(), 0);
+    d_prob.upload(all);
+    FrontRun R;
+    R.syms.resize(nt), R.fm.resize(nt), R.as.resize(nt), R.used = used;
+    R.type_stop.assign(nt, -1);
+    for (int t = 0; t < nt; ++t)
+      if (used[t]) R.syms[t] = &dtypes[t].F, R.fm[t] = &dtypes[t].M, R.as[t] = &dtypes[t].S, R.type_stop[t] = dtypes[t].root;
+    R.write_factor = 0, R.Gv = d_gall.p, R.prob_gval = d_pgval.p;
+    auto chunk = [&](int p0, int p1, double* Fb, const long long* fbase, const std::vector<long long>&) {
+      dev::DualSet S;
+      S.prob = d_prob.p + p0, S.prob_type = d_ptype.p, S.prob_fbase = fbase, S.type_rootoff = d_troot.p;
+      S.type_nB = d_tnB.p, S.type_nM = d_tnM.p, S.type_gptr = d_tgptr.p, S.type_gidx = d_tgidx.p;
+      S.g_ptr = d_gptr.p, S.g_b = d_gb.p, S.type_fix = d_tfix.p, S.type_nfix = d_tnfix.p, S.fixpos = d_fixp.p;
+      S.Gv = d_gall.p, S.prob_gval = d_pgval.p, S.prob_op = d_pop.p;
+      S.F = Fb, S.Fop = dl_F.p, S.Sop = dl_S.p, S.err = d_err.p;
+      dev::k_dual_root<<<p1 - p0, 512, smem, st>>>(S);
+      ::pf::g_launches++;
+    };
+    if (run_fronts(R, &chunk)) fail(kSingular, "dual operators: zero pivot in a subdomain interior");
+    int err = 0;
+    PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) fail(kSingular, "dual operators: zero pivot on the subdomain boundary");
+    // apply maps: local slots -> multipliers, multipliers -> slots (fixed subdomain order)
+    dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(pop), dl_lam.upload(lamall);
+    std::vector<int> rptr(D.n_lambda + 1, 0);
+    for (int l : lamall) rptr[l + 1]++;
+    for (int i = 0; i < D.n_lambda; ++i) rptr[i + 1] += rptr[i];
+    std::vector<long long> rslot(lamall.size());
+    {
+      std::vector<int> fillp(rptr.begin(), rptr.end() - 1);
+      for (long long k = 0; k < (long long)lamall.size(); ++k) rslot[fillp[lamall[k]]++] = k;
+    }
+    dl_rptr.upload(rptr), dl_rslot.upload(rslot.empty() ? std::vector<long long>{0} : rslot);
+    dl_xloc.alloc(std::max<long long>(1, dl_nslots)), dl_Y.alloc(std::max<long long>(1, dl_nslots));
+  }
+
+  /// y = sum_s Op_s x restricted to the owned subdomains (then all-reduced)
+  void dual_apply(const DevBuf<double>& Op, const double* x, double* y) {
+    const int n = D.n_lambda;
+    dev::k_local_gather<<<cdiv(dl_nslots, 256), 256, 0, st>>>(dl_nslots, dl_lam.p, x, dl_xloc.p); ::pf::g_launches++;
+    dev::k_local_gemv<<<nown(), 256, sizeof(double) * std::max(1, dl_nmax), st>>>(nown(), dl_nloc.p, dl_loff.p,
+                                                                                 dl_opoff.p, Op.p, dl_xloc.p, dl_Y.p);
+    ::pf::g_launches++;
+    dev::k_local_reduce<<<cdiv(n, 256), 256, 0, st>>>(n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0); ::pf::g_launches++;
+    reduce(y, n);
   }
 
   std::vector<int> ptype_of_own() {
@@ -1198,7 +1383,7 @@ struct Engine {
       if (T.floating) fixed.assign(T.fix.begin(), T.fix.end());
       factor_host(ksym[S.type], T.K, kv, fixed, L, Dg);
     });
-    if (use_dir)
+    if (implicit_dir)
       Isys.factor_upload(nthreads, [&](int s, std::vector<double>& LI, std::vector<double>& DI) {
         const Subdomain& S = OS(s);
         const SubType& T = D.types[S.type];
@@ -1579,7 +1764,7 @@ struct Engine {
     info.n_sub = nown();
     info.n_lambda = D.n_lambda, info.n_lambda_u = D.n_lambda_u, info.n_coarse = nc;
     info.krylov = krylov, info.N = D.mat.N, info.n_floating = nfloat, info.n_types = (int)D.types.size();
-    info.total_dim = total_vec, info.nnz_L = Ksys.nnzL, info.nnz_L_interior = use_dir ? Isys.nnzL : 0;
+    info.total_dim = total_vec, info.nnz_L = Ksys.nnzL, info.nnz_L_interior = implicit_dir ? Isys.nnzL : 0;
     info.nnz_K = total_kv;
     long long nsn = 0, ntask = 0;
     for (int s = 0; s < nown(); ++s) nsn += ksym[OS(s).type].nsn, ntask += ksym[OS(s).type].ntask;
@@ -1591,9 +1776,15 @@ struct Engine {
     for (int s = 0; s < nown(); ++s) nnzG += (long long)OS(s).g_lam.size();
     info.bytes_fapply = 2.0 * 8.0 * Ksys.nnzL + 8.0 * total_vec + 2.0 * 12.0 * nnzG + 2.0 * 8.0 * D.n_lambda;
     long long idim = 0;
-    if (use_dir)
+    if (implicit_dir)
       for (int s = 0; s < nown(); ++s) idim += isym[OS(s).type].n;
-    info.bytes_precond = use_dir ? 2.0 * 8.0 * Isys.nnzL + 8.0 * idim : 0.0;
+    info.bytes_precond = implicit_dir ? 2.0 * 8.0 * Isys.nnzL + 8.0 * idim : 0.0;
+    if (dual) {
+      // dense local operators: every apply reads sum_s n_s^2 doubles (+ gather/reduce)
+      info.bytes_fapply = 8.0 * (double)dl_opsize + 2.0 * 12.0 * (double)dl_nslots + 2.0 * 8.0 * D.n_lambda;
+      if (use_dir) info.bytes_precond = info.bytes_fapply;
+    }
+    info.dual = dual ? 1 : 0;
   }
 
   // ------------------------------------------------------------------
@@ -1612,6 +1803,10 @@ struct Engine {
 
   /// y = sum_s G_s K_s^+ G_s^T x
   void fapply(const double* x, double* y) {
+    if (dual) {
+      dual_apply(dl_F, x, y);
+      return;
+    }
     Ksys.X.zero(st);
     if (g_lam2X.nrows)
       dev::k_gather_ll<<<cdiv(g_lam2X.nrows, 256), 256, 0, st>>>(g_lam2X.nrows, g_lam2X.rows.p, g_lam2X.ptr.p,
@@ -1647,6 +1842,10 @@ struct Engine {
     }
     if (!use_dir) {
       PF_CUDA_CHECK(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    if (dual) {  // z = sum_s G_s S_s G_s^T r with the explicit Sd_s
+      dual_apply(dl_S, r, z);
       return;
     }
     // Dirichlet: w_B = G^T r; y = K_{:,B} w_B; v_I = K_II^{-1} y_I; s_B = y_B - K_BI v_I; z = G s_B
@@ -2467,7 +2666,7 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
       for (int i = 0; i < 3; ++i) o[i] = sys->phase_ms[i] / iters;
     };
     run(&E.Ksys, out);
-    run(E.use_dir ? &E.Isys : nullptr, out + 3);
+    run(E.implicit_dir ? &E.Isys : nullptr, out + 3);
     run(E.use_q ? &E.Qsys : nullptr, out + 6);
     pf::DevBuf<double> dx, dy;
     dx.alloc(E.D.n_lambda), dy.alloc(E.D.n_lambda);

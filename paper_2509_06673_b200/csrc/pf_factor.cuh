@@ -37,6 +37,13 @@ struct MfSet {
   double* L;
   double* D;
   int* err;
+  // bordered dual-operator factorisation (pf_dual.hpp): G values per problem
+  // (scatter index -2-g), the root supernode per type (assembled, not
+  // factored) and whether the factor is written at all
+  const double* Gv = nullptr;
+  const long long* prob_gval = nullptr;
+  const int* type_stop = nullptr;
+  int write_factor = 1;
 };
 
 __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
@@ -51,9 +58,10 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
   for (long long q = threadIdx.x; q < mm; q += blockDim.x) Fk[q] = 0.0;
   __syncthreads();
   const double* Kv = S.Kv + S.prob_kval[p];
+  const double* Gv = S.Gv ? S.Gv + S.prob_gval[p] : nullptr;
   for (int q = S.as_beg[sk] + threadIdx.x; q < S.as_beg[sk] + S.as_cnt[sk]; q += blockDim.x) {
     const int kid = S.as_kidx[q];
-    Fk[S.as_fpos[q]] += kid >= 0 ? Kv[kid] : 1.0;
+    Fk[S.as_fpos[q]] += kid >= 0 ? Kv[kid] : kid == -1 ? 1.0 : Gv[-2 - kid];
   }
   __syncthreads();
   for (int ci = 0; ci < S.ch_cnt[sk]; ++ci) {
@@ -71,6 +79,7 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
     }
     __syncthreads();
   }
+  if (S.type_stop && k == S.type_stop[t]) return;  // root front: left assembled for the dense phase
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = 0; j < nc; ++j) {
     const double d = Fk[j + (long long)j * m];
@@ -89,6 +98,7 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
     for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) Fk[i + (long long)j * m] *= inv;
     __syncthreads();
   }
+  if (!S.write_factor) return;
   double* L = S.L + S.prob_lval[p] + S.valoff[sk];
   for (int j = 0; j < nc; ++j)
     for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[blk_off(nc, m, i, j)] = Fk[i + (long long)j * m];

@@ -105,18 +105,29 @@ inline void nd_rec(std::vector<int>& ids, const std::vector<std::array<int, 2>>&
 
 /// Build the symbolic factor of symmetric pattern A (natural order).
 /// task_cap: maximum packed-value weight of one leaf task (0 = no tasks).
+/// Symbolic analysis.  Default: nested dissection of all of A.  With
+/// `root_last` (natural indices, in order), those columns are eliminated last
+/// as ONE dense root supernode and nested dissection orders the rest (the
+/// bordered dual-operator factorisation, pf_dual.hpp).
 inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic, long long task_cap,
-                         int ws_cap = 640, double amalg_zero_frac = 0.15, int amalg_small = 16, int leaf = 48) {
+                         int ws_cap = 640, double amalg_zero_frac = 0.15, int amalg_small = 16, int leaf = 48,
+                         const std::vector<int>* root_last = nullptr) {
   SymFactor F;
   const int n = A.nr;
   F.n = n;
   std::vector<int> order;
+  const int root_cols = root_last ? (int)root_last->size() : 0;
   {
-    std::vector<int> ids(n);
-    std::iota(ids.begin(), ids.end(), 0);
+    std::vector<int> ids;
+    std::vector<char> in_root(n, 0);
+    if (root_last)
+      for (int r : *root_last) in_root[r] = 1;
+    for (int i = 0; i < n; ++i)
+      if (!in_root[i]) ids.push_back(i);
     std::vector<uint8_t> side(n, 0);
     order.reserve(n);
     nd_rec(ids, ic, A, side, order, leaf);
+    if (root_last) order.insert(order.end(), root_last->begin(), root_last->end());
   }
   std::vector<int> ip(n);
   for (int k = 0; k < n; ++k) ip[order[k]] = k;
@@ -161,7 +172,11 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     if (parent[j] >= 0) nchild[parent[j]]++;
   std::vector<int> sn_of(n), s0;
   for (int j = 0; j < n; ++j) {
-    const bool join = j > 0 && parent[j - 1] == j && cc[j - 1] == cc[j] + 1 && nchild[j] == 1;
+    bool join = j > 0 && parent[j - 1] == j && cc[j - 1] == cc[j] + 1 && nchild[j] == 1;
+    if (root_cols) {
+      if (j == n - root_cols) join = false;  // the root block starts a supernode ...
+      else if (j > n - root_cols) join = true;  // ... and is one supernode
+    }
     if (!join) s0.push_back(j);
     sn_of[j] = (int)s0.size() - 1;
   }
@@ -204,6 +219,7 @@ inline SymFactor analyse(const Csr& A, const std::vector<std::array<int, 2>>& ic
     for (int s = 0; s < ns; ++s) {
       const int p = sparent[s];
       if (p < 0 || s0[s + 1] != s0[p] || absorbed[s]) continue;
+      if (root_cols && s0[p] >= n - root_cols) continue;  // the root block stays exactly the root columns
       // merged group: columns [c0[s], s0[p+1]), rows = own columns + rows of p beyond its columns
       const long long ncs = s0[s + 1] - c0[s], ncp = s0[p + 1] - s0[p];
       const long long n = ncs + ncp, m = ncs + nrow[p];
