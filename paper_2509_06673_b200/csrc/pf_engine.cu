@@ -129,6 +129,13 @@ struct SolveSystem {
   // dense top (single-problem systems): levels >= top_level replaced by X_top = W y_top
   int top_level = -1, ntop = 0, top_c0 = 0, top_cb0 = 0;
   DevBuf<double> W, Wres;
+  // dense bottom (single-problem systems): level-0 tasks applied as explicit
+  // dense maps (forward: b -> [y; contributions], backward: [y; ancestors] -> x)
+  bool dense_bottom = false;
+  int db_ntask = 0;
+  DevBuf<int> db_c0, db_nct, db_cbo, db_cbl;
+  DevBuf<long long> db_fo, db_bo;
+  DevBuf<double> db_Tf, db_Tb;
   int nrhs_alloc = 1;
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
@@ -358,7 +365,15 @@ struct SolveSystem {
     }
     if (top_level >= 0) {
       if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
-      for (int l = 0; l < top_level; ++l) launch_level(st, nrhs, l, 0);
+      for (int l = 0; l < top_level; ++l) {
+        if (l == 0 && dense_bottom) {
+          dev::k_dense_task<<<db_ntask, 128, 0, st>>>(db_ntask, 0, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p,
+                                                              db_fo.p, db_Tf.p, X.p, CB.p);
+          ::pf::g_launches++, ++launches;
+        } else {
+          launch_level(st, nrhs, l, 0);
+        }
+      }
       if (timed) cudaEventRecord(ev[1], st);
       dev::k_dense_top_gather<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, top_cb0,
                                                               d_fold_ptr.p + d_types_host[0].fold_base,
@@ -373,7 +388,15 @@ struct SolveSystem {
       ::pf::g_launches += 2;
       launches += 2;
       if (timed) cudaEventRecord(ev[2], st);
-      for (int l = top_level - 1; l >= 0; --l) launch_level(st, nrhs, l, 2);
+      for (int l = top_level - 1; l >= 0; --l) {
+        if (l == 0 && dense_bottom) {
+          dev::k_dense_task<<<db_ntask, 128, 0, st>>>(db_ntask, 1, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p,
+                                                              db_bo.p, db_Tb.p, X.p, CB.p);
+          ::pf::g_launches++, ++launches;
+        } else {
+          launch_level(st, nrhs, l, 2);
+        }
+      }
     } else {
       for (int l = 0; l + 1 < nlevel; ++l) launch_level(st, nrhs, l, 0);
       if (timed) cudaEventRecord(ev[1], st);
@@ -443,6 +466,72 @@ struct SolveSystem {
     W.upload(Wh);
     Wres.alloc(n);
     top_level = L, ntop = n, top_c0 = c0, top_cb0 = F.task_cboff[F.level_ptr[L]];
+  }
+
+  /// Level-0 tasks of a single-problem system as dense operators: forward
+  /// Tf ((nct+cbl) x nct, column-major) maps the task's right-hand side to
+  /// [scaled forward result; contributions], backward Tb (nct x (nct+cbl),
+  /// column-major) maps [forward result; ancestor values] to the solution.
+  /// Built from the packed host factor by applying the task's sweep to unit
+  /// vectors (same arithmetic, another summation order).
+  void set_dense_bottom(const SymFactor& F, const std::vector<double>& Lp, const std::vector<double>& Dg,
+                        int threads) {
+    if (prob_type.size() != 1 || nlevel < 2) return;
+    const int nt0 = F.level_ptr[1] - F.level_ptr[0];
+    std::vector<int> c0(nt0), nct(nt0), cbo(nt0), cbl(nt0);
+    std::vector<long long> fo(nt0 + 1, 0), bo(nt0 + 1, 0);
+    for (int q = 0; q < nt0; ++q) {
+      const int t = F.level_ptr[0] + q;
+      c0[q] = F.task_c0[t], nct[q] = F.task_c1[t] - F.task_c0[t], cbo[q] = F.task_cboff[t], cbl[q] = F.task_cblen[t];
+      const long long nw = nct[q] + cbl[q];
+      if (nw > 128) return;  // k_dense_task stages at most 128 inputs per warp
+      fo[q + 1] = fo[q] + nw * nct[q], bo[q + 1] = bo[q] + nw * nct[q];
+    }
+    std::vector<double> Tf(fo[nt0]), Tb(bo[nt0]);
+    parallel_for(nt0, threads, [&](int q) {
+      const int t = F.level_ptr[0] + q;
+      const int n = nct[q], nw = n + cbl[q];
+      std::vector<double> Ll((std::size_t)nw * n, 0.0), ws(nw);
+      for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
+        const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+        const int* sl = &F.slot[F.sn_rowoff[k]];
+        long long o = F.sn_valoff[k];
+        for (int j = 0; j < nc; ++j) {
+          const int jj = sl[j];
+          for (int i = j + 1; i < m; ++i) Ll[(std::size_t)jj * nw + sl[i]] = Lp[o++];
+        }
+      }
+      for (int e = 0; e < n; ++e) {
+        std::fill(ws.begin(), ws.end(), 0.0);
+        ws[e] = 1.0;
+        for (int jj = 0; jj < n; ++jj) {
+          const double xj = ws[jj];
+          if (xj == 0.0) continue;
+          const double* lc = &Ll[(std::size_t)jj * nw];
+          for (int r = jj + 1; r < nw; ++r) ws[r] -= lc[r] * xj;
+        }
+        double* out = &Tf[fo[q] + (long long)e * nw];
+        for (int r = 0; r < n; ++r) out[r] = ws[r] / Dg[c0[q] + r];
+        for (int r = n; r < nw; ++r) out[r] = ws[r];
+      }
+      for (int e = 0; e < nw; ++e) {
+        std::fill(ws.begin(), ws.end(), 0.0);
+        ws[e] = 1.0;
+        for (int jj = n - 1; jj >= 0; --jj) {
+          const double* lc = &Ll[(std::size_t)jj * nw];
+          double acc = 0.0;
+          for (int r = jj + 1; r < nw; ++r) acc += lc[r] * ws[r];
+          ws[jj] -= acc;
+        }
+        double* out = &Tb[bo[q] + (long long)e * n];
+        for (int r = 0; r < n; ++r) out[r] = ws[r];
+      }
+    });
+    db_c0.upload(c0), db_nct.upload(nct), db_cbo.upload(cbo), db_cbl.upload(cbl);
+    fo.pop_back(), bo.pop_back();
+    db_fo.upload(fo), db_bo.upload(bo), db_Tf.upload(Tf), db_Tb.upload(Tb);
+    db_ntask = nt0;
+    dense_bottom = true;
   }
 
   void prepare_smem() {
@@ -1642,6 +1731,7 @@ struct Engine {
       const char* v = std::getenv("PF_Q_DENSE_TOP");
       const int cap = v ? std::atoi(v) : 2048;
       if (cap > 0) Qsys.set_dense_top(qsym, L, Dg, cap, nthreads);
+      if (Qsys.top_level > 1 && !std::getenv("PF_Q_NO_DENSE_BOTTOM")) Qsys.set_dense_bottom(qsym, L, Dg, nthreads);
     }
     to_blocked(qsym, L);
     PF_CUDA_CHECK(cudaMemcpy(Qsys.L.p, L.data(), sizeof(double) * L.size(), cudaMemcpyHostToDevice));

@@ -381,5 +381,32 @@ __global__ void __launch_bounds__(256) k_dense_top_gemv(int n, int c0, const dou
   }
 }
 
+/// Level-0 tasks of a single-problem system as dense operators (one CTA of
+/// four warps per task, a warp per 32 output rows; operator column-major so a
+/// fixed input index is a coalesced column):
+/// mode 0 (forward): in = X[c0..c0+nct), out = [X[c0..); CB[cbo..cbo+cbl)]
+/// mode 1 (backward): in = [X[c0..); CB[cbo..)], out = X[c0..c0+nct).
+__global__ void __launch_bounds__(128) k_dense_task(int ntask, int mode, const int* __restrict__ c0,
+                                                    const int* __restrict__ nct, const int* __restrict__ cbo,
+                                                    const int* __restrict__ cbl, const long long* __restrict__ toff,
+                                                    const double* __restrict__ T, double* X, double* CB) {
+  __shared__ double in[128];
+  const int q = blockIdx.x;
+  if (q >= ntask) return;
+  const int n = nct[q], nb = cbl[q], nw = n + nb;
+  const int ni = mode == 0 ? n : nw, no = mode == 0 ? nw : n;
+  for (int i = threadIdx.x; i < ni; i += blockDim.x) in[i] = i < n ? X[c0[q] + i] : CB[cbo[q] + i - n];
+  __syncthreads();  // every input staged before any output overwrites X
+  const double* A = T + toff[q];
+  for (int r = threadIdx.x; r < no; r += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0;
+    int j = 0;
+    for (; j + 2 <= ni; j += 2) a0 += A[(long long)j * no + r] * in[j], a1 += A[(long long)(j + 1) * no + r] * in[j + 1];
+    if (j < ni) a0 += A[(long long)j * no + r] * in[j];
+    if (r < n) X[c0[q] + r] = a0 + a1;
+    else CB[cbo[q] + r - n] = a0 + a1;
+  }
+}
+
 }  // namespace dev
 }  // namespace pf
