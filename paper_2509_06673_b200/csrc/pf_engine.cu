@@ -133,6 +133,7 @@ struct SolveSystem {
   // dense maps (forward: b -> [y; contributions], backward: [y; ancestors] -> x)
   bool dense_bottom = false;
   int db_ntask = 0;
+  std::vector<int> db_lptr;  // tasks of dense level l: [db_lptr[l], db_lptr[l+1])
   DevBuf<int> db_c0, db_nct, db_cbo, db_cbl;
   DevBuf<long long> db_fo, db_bo;
   DevBuf<double> db_Tf, db_Tb;
@@ -365,10 +366,14 @@ struct SolveSystem {
     }
     if (top_level >= 0) {
       if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
+      const int* fpp = d_fold_ptr.p + d_types_host[0].fold_base;
+      const int* fip = d_fold_idx.p + d_types_host[0].foldidx_base;
+      const int* cbr = d_cbrows.p + d_types_host[0].cb_base;
       for (int l = 0; l < top_level; ++l) {
-        if (l == 0 && dense_bottom) {
-          dev::k_dense_task<<<db_ntask, 128, 0, st>>>(db_ntask, 0, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p,
-                                                              db_fo.p, db_Tf.p, X.p, CB.p);
+        if (dense_bottom) {
+          const int n0 = db_lptr[l], nn = db_lptr[l + 1] - n0;
+          dev::k_dense_task<<<nn, 128, 0, st>>>(n0, 0, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p, db_fo.p, db_Tf.p,
+                                               fpp, fip, cbr, X.p, CB.p);
           ::pf::g_launches++, ++launches;
         } else {
           launch_level(st, nrhs, l, 0);
@@ -381,17 +386,21 @@ struct SolveSystem {
                                                               Wres.p);
       dev::k_dense_top_gemv<<<std::min(cdiv(ntop, 8), 2 * 148), 256, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p,
                                                                                                    Wres.p, X.p);
-      dev::k_scatter_cols<<<cdiv(ntop, 256), 256, 0, st>>>(top_c0, ntop, top_cb0, d_fold_ptr.p + d_types_host[0].fold_base,
-                                                           d_fold_idx.p + d_types_host[0].foldidx_base, X.p, CB.p);
-      ::pf::g_launches++;
-      launches++;
+      if (!dense_bottom) {  // the sweep kernels read their ancestors from CB
+        dev::k_scatter_cols<<<cdiv(ntop, 256), 256, 0, st>>>(top_c0, ntop, top_cb0,
+                                                             d_fold_ptr.p + d_types_host[0].fold_base,
+                                                             d_fold_idx.p + d_types_host[0].foldidx_base, X.p, CB.p);
+        ::pf::g_launches++;
+        launches++;
+      }
       ::pf::g_launches += 2;
       launches += 2;
       if (timed) cudaEventRecord(ev[2], st);
       for (int l = top_level - 1; l >= 0; --l) {
-        if (l == 0 && dense_bottom) {
-          dev::k_dense_task<<<db_ntask, 128, 0, st>>>(db_ntask, 1, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p,
-                                                              db_bo.p, db_Tb.p, X.p, CB.p);
+        if (dense_bottom) {
+          const int n0 = db_lptr[l], nn = db_lptr[l + 1] - n0;
+          dev::k_dense_task<<<nn, 128, 0, st>>>(n0, 1, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p, db_bo.p, db_Tb.p,
+                                               fpp, fip, cbr, X.p, CB.p);
           ::pf::g_launches++, ++launches;
         } else {
           launch_level(st, nrhs, l, 2);
@@ -476,20 +485,24 @@ struct SolveSystem {
   /// vectors (same arithmetic, another summation order).
   void set_dense_bottom(const SymFactor& F, const std::vector<double>& Lp, const std::vector<double>& Dg,
                         int threads) {
-    if (prob_type.size() != 1 || nlevel < 2) return;
-    const int nt0 = F.level_ptr[1] - F.level_ptr[0];
+    if (prob_type.size() != 1 || top_level < 1) return;
+    // every sparse level below the dense top becomes one dense-operator launch
+    const int nl = top_level;
+    const int tb0 = F.level_ptr[0], nt0 = F.level_ptr[nl] - tb0;
     std::vector<int> c0(nt0), nct(nt0), cbo(nt0), cbl(nt0);
     std::vector<long long> fo(nt0 + 1, 0), bo(nt0 + 1, 0);
     for (int q = 0; q < nt0; ++q) {
-      const int t = F.level_ptr[0] + q;
+      const int t = tb0 + q;
       c0[q] = F.task_c0[t], nct[q] = F.task_c1[t] - F.task_c0[t], cbo[q] = F.task_cboff[t], cbl[q] = F.task_cblen[t];
       const long long nw = nct[q] + cbl[q];
-      if (nw > 128) return;  // k_dense_task stages at most 128 inputs per warp
+      if (nw > 128) return;  // k_dense_task stages at most 128 inputs per CTA
       fo[q + 1] = fo[q] + nw * nct[q], bo[q + 1] = bo[q] + nw * nct[q];
     }
+    db_lptr.assign(nl + 1, 0);
+    for (int l = 0; l <= nl; ++l) db_lptr[l] = F.level_ptr[l] - tb0;
     std::vector<double> Tf(fo[nt0]), Tb(bo[nt0]);
     parallel_for(nt0, threads, [&](int q) {
-      const int t = F.level_ptr[0] + q;
+      const int t = tb0 + q;
       const int n = nct[q], nw = n + cbl[q];
       std::vector<double> Ll((std::size_t)nw * n, 0.0), ws(nw);
       for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
@@ -1731,7 +1744,7 @@ struct Engine {
       const char* v = std::getenv("PF_Q_DENSE_TOP");
       const int cap = v ? std::atoi(v) : 2048;
       if (cap > 0) Qsys.set_dense_top(qsym, L, Dg, cap, nthreads);
-      if (Qsys.top_level > 1 && !std::getenv("PF_Q_NO_DENSE_BOTTOM")) Qsys.set_dense_bottom(qsym, L, Dg, nthreads);
+      if (Qsys.top_level >= 1 && !std::getenv("PF_Q_NO_DENSE_BOTTOM")) Qsys.set_dense_bottom(qsym, L, Dg, nthreads);
     }
     to_blocked(qsym, L);
     PF_CUDA_CHECK(cudaMemcpy(Qsys.L.p, L.data(), sizeof(double) * L.size(), cudaMemcpyHostToDevice));

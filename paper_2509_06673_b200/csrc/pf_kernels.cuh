@@ -381,30 +381,60 @@ __global__ void __launch_bounds__(256) k_dense_top_gemv(int n, int c0, const dou
   }
 }
 
-/// Level-0 tasks of a single-problem system as dense operators (one CTA of
-/// four warps per task, a warp per 32 output rows; operator column-major so a
-/// fixed input index is a coalesced column):
-/// mode 0 (forward): in = X[c0..c0+nct), out = [X[c0..); CB[cbo..cbo+cbl)]
-/// mode 1 (backward): in = [X[c0..); CB[cbo..)], out = X[c0..c0+nct).
-__global__ void __launch_bounds__(128) k_dense_task(int ntask, int mode, const int* __restrict__ c0,
+/// Sparse levels of a single-problem system as dense per-task operators (one
+/// CTA of four warps per task; operator column-major so a fixed input index
+/// is a coalesced column):
+/// mode 0 (forward): in = X[c0..c0+nct) + child contributions (fold lists,
+///                   staged in parallel, summed per column in fixed order),
+///                   out = [X[c0..); CB[cbo..cbo+cbl)]
+/// mode 1 (backward): in = [X[c0..); X[cb_rows]] (ancestor values, final),
+///                   out = X[c0..c0+nct).
+__global__ void __launch_bounds__(128) k_dense_task(int t0, int mode, const int* __restrict__ c0,
                                                     const int* __restrict__ nct, const int* __restrict__ cbo,
                                                     const int* __restrict__ cbl, const long long* __restrict__ toff,
-                                                    const double* __restrict__ T, double* X, double* CB) {
-  __shared__ double in[128];
-  const int q = blockIdx.x;
-  if (q >= ntask) return;
-  const int n = nct[q], nb = cbl[q], nw = n + nb;
+                                                    const double* __restrict__ T, const int* __restrict__ fold_ptr,
+                                                    const int* __restrict__ fold_idx, const int* __restrict__ cb_rows,
+                                                    double* X, double* CB) {
+  constexpr int kFold = 1024;  // fold entries staged per task (longer lists use the serial path)
+  __shared__ double in[128], fv[kFold];
+  __shared__ int fp[129];
+  const int q = t0 + blockIdx.x;
+  const int n = nct[q], nb = cbl[q], nw = n + nb, c = c0[q];
   const int ni = mode == 0 ? n : nw, no = mode == 0 ? nw : n;
-  for (int i = threadIdx.x; i < ni; i += blockDim.x) in[i] = i < n ? X[c0[q] + i] : CB[cbo[q] + i - n];
+  if (mode == 0) {
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) fp[i] = fold_ptr[c + i];
+    __syncthreads();
+    const int f0 = fp[0], nf = fp[n] - f0;
+    const bool staged = nf <= kFold;
+    if (staged) {
+      for (int f = threadIdx.x; f < nf; f += blockDim.x) fv[f] = CB[fold_idx[f0 + f]];
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double v = X[c + i];
+      if (staged)
+        for (int f = fp[i]; f < fp[i + 1]; ++f) v += fv[f - f0];  // fixed order
+      else
+        for (int f = fp[i]; f < fp[i + 1]; ++f) v += CB[fold_idx[f]];
+      in[i] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) in[i] = i < n ? X[c + i] : X[cb_rows[cbo[q] + i - n]];
+  }
   __syncthreads();  // every input staged before any output overwrites X
   const double* A = T + toff[q];
   for (int r = threadIdx.x; r < no; r += blockDim.x) {
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int j = 0;
-    for (; j + 2 <= ni; j += 2) a0 += A[(long long)j * no + r] * in[j], a1 += A[(long long)(j + 1) * no + r] * in[j + 1];
-    if (j < ni) a0 += A[(long long)j * no + r] * in[j];
-    if (r < n) X[c0[q] + r] = a0 + a1;
-    else CB[cbo[q] + r - n] = a0 + a1;
+    for (; j + 4 <= ni; j += 4) {
+      const double v0 = A[(long long)j * no + r], v1 = A[(long long)(j + 1) * no + r];
+      const double v2 = A[(long long)(j + 2) * no + r], v3 = A[(long long)(j + 3) * no + r];
+      a0 += v0 * in[j], a1 += v1 * in[j + 1], a2 += v2 * in[j + 2], a3 += v3 * in[j + 3];
+    }
+    for (; j < ni; ++j) a0 += A[(long long)j * no + r] * in[j];
+    const double v = (a0 + a1) + (a2 + a3);
+    if (r < n) X[c + r] = v;
+    else CB[cbo[q] + r - n] = v;
   }
 }
 
