@@ -14,10 +14,10 @@
 // stride) whose trailing multiplier block is -F.  One CTA per subdomain;
 // setup only.
 //
-// k_local_gemv / k_local_reduce: the per-iteration apply y = sum_s Op_s x_s
-// (one CTA per subdomain, a warp per row of the dense symmetric operator,
-// x_s staged in shared memory), then each multiplier sums its (one or two)
-// subdomain contributions in a fixed order.
+// k_local_symv / k_local_reduce: the per-iteration apply y = sum_s Op_s x_s
+// (one CTA per subdomain over the packed lower tile triangle of the symmetric
+// operator, x_s gathered into shared memory), then each multiplier sums its
+// (one or two) subdomain contributions in a fixed order.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -140,36 +140,96 @@ __global__ void __launch_bounds__(512) k_dual_root(DualSet S) {
   }
 }
 
-/// Y[yoff_s + i] = sum_j Op_s[i][j] x[xoff_s + j]  (x already gathered per subdomain)
-__global__ void __launch_bounds__(256) k_local_gemv(int nsub, const int* __restrict__ nloc,
-                                                    const long long* __restrict__ loff,
-                                                    const long long* __restrict__ opoff,
-                                                    const double* __restrict__ Op,
-                                                    const double* __restrict__ xloc, double* __restrict__ Y) {
-  extern __shared__ double xs[];
-  const int s = blockIdx.x;
+// ---------------------------------------------------------------------------
+// Symmetric packed operators: F_s and Sd_s are symmetric, so only the lower
+// tile triangle is stored.  32x32 tiles (I >= J) in order k = I(I+1)/2 + J;
+// inside a tile, element (row r, column c) sits at double index
+// ((c/2)*32 + r)*2 + (c&1): lane r of a warp loads the double2 of columns
+// (2cp, 2cp+1) of its row, 512 contiguous bytes per warp-load.  Padding rows
+// and columns (>= n) are zero.  Diagonal tiles hold the full symmetric block.
+// ---------------------------------------------------------------------------
+constexpr int kSymT = 32;
+
+__host__ __device__ inline long long sym_tiles(int n) {
+  const long long nt = (n + kSymT - 1) / kSymT;
+  return nt * (nt + 1) / 2;
+}
+
+/// pack: P_s tiles from the full row-major operator A_s (lower triangle read)
+__global__ void k_pack_sym(int nsub, const int* __restrict__ nloc, const long long* __restrict__ full_off,
+                           const double* __restrict__ A, const long long* __restrict__ pack_off, double* P) {
+  const int s = blockIdx.y;
   if (s >= nsub) return;
   const int n = nloc[s];
-  const double* x = xloc + loff[s];
-  for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = x[j];
-  __syncthreads();
-  const double* A = Op + opoff[s];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < n; i += nw) {
-    const double* a = A + (long long)i * n;
-    double v = 0.0;
-    for (int j = lane; j < n; j += 32) v += a[j] * xs[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) Y[loff[s] + i] = v;
+  const long long total = sym_tiles(n) * kSymT * kSymT;
+  const double* a = A + full_off[s];
+  double* p = P + pack_off[s];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e >> 10), w = (int)(e & 1023);
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= k) ++I;
+    const int J = k - I * (I + 1) / 2;
+    const int c = ((w >> 6) << 1) | (w & 1), r = (w >> 1) & 31;
+    const int i = I * kSymT + r, j = J * kSymT + c;
+    p[e] = (i < n && j < n) ? a[(long long)i * n + j] : 0.0;
   }
 }
 
-/// xloc[k] = x[lam[k]] for every (subdomain, local multiplier) slot
-__global__ void k_local_gather(long long n, const int* __restrict__ lam, const double* __restrict__ x,
-                               double* __restrict__ xloc) {
-  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) xloc[k] = x[lam[k]];
+/// Y[loff_s + i] = sum_j Op_s[i][j] x[lam[loff_s + j]] with Op_s symmetric,
+/// packed (above).  One CTA per subdomain; x_s gathered straight from the
+/// multiplier vector into shared memory; warp w takes tiles w, w+8, ... and
+/// accumulates row sums (T x_J into y_I) and, off the diagonal, column sums
+/// (T^T x_I into y_J) into its own shared y buffer in tile order; the buffers
+/// are summed in warp order.  Every summation order is fixed (deterministic).
+__global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restrict__ nloc,
+                                                    const long long* __restrict__ loff,
+                                                    const long long* __restrict__ opoff,
+                                                    const double* __restrict__ Op, const int* __restrict__ lam,
+                                                    const double* __restrict__ x, double* __restrict__ Y) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.x;
+  if (s >= nsub) return;
+  const int n = nloc[s], nt = (n + kSymT - 1) / kSymT, np = nt * kSymT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* xs = sm;            // np
+  double* yb = sm + np;       // nw x np
+  const long long lo = loff[s];
+  for (int j = threadIdx.x; j < np; j += blockDim.x) xs[j] = j < n ? x[lam[lo + j]] : 0.0;
+  for (int j = threadIdx.x; j < nw * np; j += blockDim.x) yb[j] = 0.0;
+  __syncthreads();
+  const double2* A = reinterpret_cast<const double2*>(Op + opoff[s]);
+  double* my = yb + warp * np;
+  const int ntile = nt * (nt + 1) / 2;
+  int I = 0, J = 0, k = 0;
+  for (int t = warp; t < ntile; t += nw) {
+    while (k < t) {  // advance (I, J) to tile t
+      if (++J > I) ++I, J = 0;
+      ++k;
+    }
+    const double2* tp = A + (long long)t * (kSymT * kSymT / 2);
+    double2 v[16];
+#pragma unroll
+    for (int cp = 0; cp < 16; ++cp) v[cp] = __ldg(tp + cp * 32 + lane);
+    const double* xj = xs + J * kSymT;
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int cp = 0; cp < 16; ++cp) r0 += v[cp].x * xj[2 * cp], r1 += v[cp].y * xj[2 * cp + 1];
+    my[I * kSymT + lane] += r0 + r1;
+    if (I != J) {
+      const double xr = xs[I * kSymT + lane];
+      double acc[32];
+#pragma unroll
+      for (int cp = 0; cp < 16; ++cp) acc[2 * cp] = v[cp].x * xr, acc[2 * cp + 1] = v[cp].y * xr;
+      my[J * kSymT + lane] += transpose_reduce<32>(acc, lane);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += yb[w * np + i];
+    Y[lo + i] = v;
+  }
 }
 
 /// y[i] = alpha * sum over the multiplier's slots (fixed order) of Y

@@ -1299,9 +1299,9 @@ struct Engine {
   // explicit local dual operators (pf_dual.hpp / pf_dual.cuh)
   DevBuf<int> dl_nloc, dl_lam, dl_rptr;
   DevBuf<long long> dl_loff, dl_opoff, dl_rslot;
-  DevBuf<double> dl_F, dl_S, dl_xloc, dl_Y;
-  long long dl_nslots = 0, dl_opsize = 0;
-  int dl_nmax = 0;
+  DevBuf<double> dl_F, dl_S, dl_Y;
+  long long dl_nslots = 0, dl_opsize = 0, dl_symvals = 0;  // packed doubles / n(n+1)/2 values per operator
+  int dl_nmax = 0, dl_smem = 0;
 
   /// F_s and Sd_s for every owned subdomain: one bordered partial
   /// factorisation (multifrontal, root front kept) + k_dual_root per chunk.
@@ -1382,8 +1382,32 @@ struct Engine {
     int err = 0;
     PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) fail(kSingular, "dual operators: zero pivot on the subdomain boundary");
+    // symmetric packed storage (lower tile triangle) replaces the full blocks
+    std::vector<long long> ppk(np);
+    long long pk = 0;
+    for (int p = 0; p < np; ++p) ppk[p] = pk, pk += dev::sym_tiles(nloc[p]) * dev::kSymT * dev::kSymT;
+    {
+      DevBuf<int> d_nloc;
+      d_nloc.upload(nloc);
+      DevBuf<long long> d_ppk;
+      d_ppk.upload(ppk);
+      for (DevBuf<double>* op : {&dl_F, &dl_S}) {
+        DevBuf<double> packed;
+        packed.alloc(std::max<long long>(1, pk));
+        dev::k_pack_sym<<<dim3(64, np), 256, 0, st>>>(np, d_nloc.p, d_pop.p, op->p, d_ppk.p, packed.p);
+        ::pf::g_launches++;
+        PF_CUDA_CHECK(cudaStreamSynchronize(st));
+        *op = std::move(packed);
+      }
+    }
+    dl_opsize = pk;
+    dl_symvals = 0;
+    for (int p = 0; p < np; ++p) dl_symvals += (long long)nloc[p] * (nloc[p] + 1) / 2;
+    dl_smem = (int)(sizeof(double) * (1 + 8) * ((dl_nmax + dev::kSymT - 1) / dev::kSymT) * dev::kSymT);
+    if (dl_smem > 227 * 1024) fail(kInternal, "dual operator too large for the staged symmetric GEMV");
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_local_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, dl_smem));
     // apply maps: local slots -> multipliers, multipliers -> slots (fixed subdomain order)
-    dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(pop), dl_lam.upload(lamall);
+    dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(ppk), dl_lam.upload(lamall);
     std::vector<int> rptr(D.n_lambda + 1, 0);
     for (int l : lamall) rptr[l + 1]++;
     for (int i = 0; i < D.n_lambda; ++i) rptr[i + 1] += rptr[i];
@@ -1393,15 +1417,14 @@ struct Engine {
       for (long long k = 0; k < (long long)lamall.size(); ++k) rslot[fillp[lamall[k]]++] = k;
     }
     dl_rptr.upload(rptr), dl_rslot.upload(rslot.empty() ? std::vector<long long>{0} : rslot);
-    dl_xloc.alloc(std::max<long long>(1, dl_nslots)), dl_Y.alloc(std::max<long long>(1, dl_nslots));
+    dl_Y.alloc(std::max<long long>(1, dl_nslots));
   }
 
   /// y = sum_s Op_s x restricted to the owned subdomains (then all-reduced)
   void dual_apply(const DevBuf<double>& Op, const double* x, double* y) {
     const int n = D.n_lambda;
-    dev::k_local_gather<<<cdiv(dl_nslots, 256), 256, 0, st>>>(dl_nslots, dl_lam.p, x, dl_xloc.p); ::pf::g_launches++;
-    dev::k_local_gemv<<<nown(), 256, sizeof(double) * std::max(1, dl_nmax), st>>>(nown(), dl_nloc.p, dl_loff.p,
-                                                                                 dl_opoff.p, Op.p, dl_xloc.p, dl_Y.p);
+    dev::k_local_symv<<<nown(), 256, dl_smem, st>>>(nown(), dl_nloc.p, dl_loff.p, dl_opoff.p, Op.p, dl_lam.p, x,
+                                                    dl_Y.p);
     ::pf::g_launches++;
     dev::k_local_reduce<<<cdiv(n, 256), 256, 0, st>>>(n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0); ::pf::g_launches++;
     reduce(y, n);
@@ -1849,6 +1872,10 @@ struct Engine {
       for (int i = 0; i < nc; ++i) inv[(std::size_t)i * nc + c] = x[i];
     });
     c_ainv.upload(inv);
+    if (sizeof(double) * nc > 227 * 1024) fail(kInternal, "coarse space too large for the staged GEMV");
+    if (sizeof(double) * nc > 48 * 1024)
+      PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_dense_gemv_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(double) * nc)));
     c_tmp1.alloc(nc), c_tmp2.alloc(nc), e_vec.alloc(nc), alpha_vec.alloc(nc);
     d_fsub.upload(fsub), d_fnu.upload(fnu), d_fvec.upload(fvec), d_fxyoff.upload(fxyo), d_fxy.upload(fxy);
   }
@@ -1884,7 +1911,8 @@ struct Engine {
     info.bytes_precond = implicit_dir ? 2.0 * 8.0 * Isys.nnzL + 8.0 * idim : 0.0;
     if (dual) {
       // dense local operators: every apply reads sum_s n_s^2 doubles (+ gather/reduce)
-      info.bytes_fapply = 8.0 * (double)dl_opsize + 2.0 * 12.0 * (double)dl_nslots + 2.0 * 8.0 * D.n_lambda;
+      // symmetric operators: the n(n+1)/2 values of each (tile padding not counted)
+      info.bytes_fapply = 8.0 * (double)dl_symvals + 2.0 * 12.0 * (double)dl_nslots + 2.0 * 8.0 * D.n_lambda;
       if (use_dir) info.bytes_precond = info.bytes_fapply;
     }
     info.dual = dual ? 1 : 0;
@@ -1975,11 +2003,22 @@ struct Engine {
     qsolve(z, z);
   }
 
+  /// y = (G_c^T G_c)^{-1} x (dense inverse, warp per row)
+  void coarse_gemv(const double* x, double* y) {
+    dev::k_dense_gemv_w<<<std::min(cdiv(nc, 8), 4 * 148), 256, sizeof(double) * nc, st>>>(nc, c_ainv.p, x, y);
+    ::pf::g_launches++;
+  }
+  /// y = (G_c^T G_c)^{-1} G_c^T v
+  void coarse_solve(const double* v, double* y) {
+    dev::k_spmv_warp<<<cdiv(nc, 8), 256, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0);
+    ::pf::g_launches++;
+    coarse_gemv(c_tmp1.p, y);
+  }
+
   void project(double* v) {
     if (nc == 0) return;
     const int n = D.n_lambda;
-    dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0); ::pf::g_launches++;
-    dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, c_tmp2.p); ::pf::g_launches++;
+    coarse_solve(v, c_tmp2.p);
     dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, v, -1.0, 1.0); ::pf::g_launches++;
   }
 
@@ -2309,7 +2348,7 @@ struct Engine {
         } else {
           kr_tmp.zero(st);
         }
-        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, e_vec.p, c_tmp2.p); ::pf::g_launches++;
+        coarse_gemv(e_vec.p, c_tmp2.p);
         dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, c_ptr.p, c_idx.p, c_val.p, c_tmp2.p, lam.p, 1.0, 0.0); ::pf::g_launches++;
         dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_tmp.p, 1.0, lam.p); ::pf::g_launches++;
       } else if (!D.cfg.warm) {
@@ -2327,8 +2366,7 @@ struct Engine {
         // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
         F_(lam.p, kr_tmp.p);
         dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, kr_rhs.p, 1.0, kr_tmp.p); ::pf::g_launches++;
-        dev::k_spmv<<<cdiv(nc, 128), 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, kr_tmp.p, c_tmp1.p, 1.0, 0.0); ::pf::g_launches++;
-        dev::k_dense_gemv<<<nc, 128, 0, st>>>(nc, c_ainv.p, c_tmp1.p, alpha_vec.p); ::pf::g_launches++;
+        coarse_solve(kr_tmp.p, alpha_vec.p);
       }
       back_substitute(lam.p);
       cudaEventRecord(e3, st);

@@ -347,6 +347,54 @@ __global__ void k_dense_gemv(int n, const double* A, const double* x, double* y)
   if (threadIdx.x == 0) y[i] = s;
 }
 
+/// y = A x for a dense row-major n x n A: a warp per row (16-byte loads when
+/// the rows are 16-byte aligned, four loads in flight per lane), x staged in
+/// shared memory; grid-stride over rows.  Coarse projector (G_c^T G_c)^{-1}.
+__global__ void __launch_bounds__(256) k_dense_gemv_w(int n, const double* __restrict__ A,
+                                                      const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ double xs[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = (n & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
+    const double* a = A + (size_t)row * n;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (vec) {
+      const double2* a2 = reinterpret_cast<const double2*>(a);
+      const int n2 = n >> 1;
+      int j = lane;
+      for (; j + 32 < n2; j += 64) {
+        const double2 u = __ldg(a2 + j), v = __ldg(a2 + j + 32);
+        s0 += u.x * xs[2 * j], s1 += u.y * xs[2 * j + 1];
+        s2 += v.x * xs[2 * j + 64], s3 += v.y * xs[2 * j + 65];
+      }
+      if (j < n2) {
+        const double2 u = __ldg(a2 + j);
+        s0 += u.x * xs[2 * j], s1 += u.y * xs[2 * j + 1];
+      }
+    } else {
+      for (int j = lane; j < n; j += 32) s0 += __ldg(a + j) * xs[j];
+    }
+    const double s = warp_sum((s0 + s2) + (s1 + s3));
+    if (lane == 0) y[row] = s;
+  }
+}
+
+/// CSR SpMV with a warp per row (long rows: G_c^T, ~400 entries per coarse
+/// mode); y = alpha*A x + beta*y, fixed summation order.
+__global__ void __launch_bounds__(256) k_spmv_warp(int nrows, const int* __restrict__ ptr,
+                                                   const int* __restrict__ idx, const double* __restrict__ val,
+                                                   const double* __restrict__ x, double* y, double alpha,
+                                                   double beta) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  double s = 0.0;
+  for (int q = ptr[row] + lane; q < ptr[row + 1]; q += 32) s += val[q] * x[idx[q]];
+  s = warp_sum(s);
+  if (lane == 0) y[row] = (beta == 0.0 ? 0.0 : beta * y[row]) + alpha * s;
+}
+
 /// Dense top of a single-problem sweep, pass 1: y = X[c0..c0+n) + folded
 /// child contributions (fixed order).
 /// Only contributions of the sparse levels (CB index < cb_top) count: the
