@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <map>
+#include <unordered_map>
 #include <cstdlib>
 #include <chrono>
 #include <cstdio>
@@ -132,11 +134,13 @@ struct SolveSystem {
   // dense bottom (single-problem systems): level-0 tasks applied as explicit
   // dense maps (forward: b -> [y; contributions], backward: [y; ancestors] -> x)
   bool dense_bottom = false;
-  int db_ntask = 0;
-  std::vector<int> db_lptr;  // tasks of dense level l: [db_lptr[l], db_lptr[l+1])
-  DevBuf<int> db_c0, db_nct, db_cbo, db_cbl;
-  DevBuf<long long> db_fo, db_bo;
-  DevBuf<double> db_Tf, db_Tb;
+  int db_cb1 = 0;                        // first CB slot of the levels above 0
+  int db_nwork[2][2] = {{0, 0}, {0, 0}};  // [forward/backward][stage]
+  int db_split[2][2] = {{1, 1}, {1, 1}};  // input slices per CTA
+  DevBuf<dev::UnitWork> db_work[2][2];
+  DevBuf<int> db_in, db_out, db_in_nat, db_out_nat;
+  DevBuf<double> db_T;
+  double db_bytes = 0.0;
   int nrhs_alloc = 1;
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
@@ -366,46 +370,23 @@ struct SolveSystem {
     }
     if (top_level >= 0) {
       if (nrhs != 1) fail(kInternal, "dense-top solve supports one right-hand side");
-      const int* fpp = d_fold_ptr.p + d_types_host[0].fold_base;
-      const int* fip = d_fold_idx.p + d_types_host[0].foldidx_base;
-      const int* cbr = d_cbrows.p + d_types_host[0].cb_base;
-      for (int l = 0; l < top_level; ++l) {
-        if (dense_bottom) {
-          const int n0 = db_lptr[l], nn = db_lptr[l + 1] - n0;
-          dev::k_dense_task<<<nn, 128, 0, st>>>(n0, 0, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p, db_fo.p, db_Tf.p,
-                                               fpp, fip, cbr, X.p, CB.p);
-          ::pf::g_launches++, ++launches;
-        } else {
-          launch_level(st, nrhs, l, 0);
-        }
-      }
+      if (dense_bottom) fail(kInternal, "dense-bottom systems are solved by solve_dense");
+      for (int l = 0; l < top_level; ++l) launch_level(st, nrhs, l, 0);
       if (timed) cudaEventRecord(ev[1], st);
-      dev::k_dense_top_gather<<<cdiv(ntop, 256), 256, 0, st>>>(ntop, top_c0, top_cb0,
+      dev::k_dense_top_gather<<<cdiv(ntop, 8), 256, 0, st>>>(ntop, top_c0, top_cb0,
                                                               d_fold_ptr.p + d_types_host[0].fold_base,
                                                               d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, X.p,
-                                                              Wres.p);
-      dev::k_dense_top_gemv<<<std::min(cdiv(ntop, 8), 2 * 148), 256, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p,
-                                                                                                   Wres.p, X.p);
-      if (!dense_bottom) {  // the sweep kernels read their ancestors from CB
-        dev::k_scatter_cols<<<cdiv(ntop, 256), 256, 0, st>>>(top_c0, ntop, top_cb0,
-                                                             d_fold_ptr.p + d_types_host[0].fold_base,
-                                                             d_fold_idx.p + d_types_host[0].foldidx_base, X.p, CB.p);
-        ::pf::g_launches++;
-        launches++;
-      }
-      ::pf::g_launches += 2;
-      launches += 2;
+                                                              nullptr, Wres.p);
+      dev::k_dense_top_gemv<<<std::min(cdiv(ntop, 8), 4 * 148), 256, sizeof(double) * ntop, st>>>(
+          ntop, top_c0, W.p, Wres.p, X.p, nullptr, nullptr);
+      // the sweep kernels read their ancestors from CB
+      dev::k_scatter_cols<<<cdiv(ntop, 256), 256, 0, st>>>(top_c0, ntop, top_cb0,
+                                                           d_fold_ptr.p + d_types_host[0].fold_base,
+                                                           d_fold_idx.p + d_types_host[0].foldidx_base, X.p, CB.p);
+      ::pf::g_launches += 3;
+      launches += 3;
       if (timed) cudaEventRecord(ev[2], st);
-      for (int l = top_level - 1; l >= 0; --l) {
-        if (dense_bottom) {
-          const int n0 = db_lptr[l], nn = db_lptr[l + 1] - n0;
-          dev::k_dense_task<<<nn, 128, 0, st>>>(n0, 1, db_c0.p, db_nct.p, db_cbo.p, db_cbl.p, db_bo.p, db_Tb.p,
-                                               fpp, fip, cbr, X.p, CB.p);
-          ::pf::g_launches++, ++launches;
-        } else {
-          launch_level(st, nrhs, l, 2);
-        }
-      }
+      for (int l = top_level - 1; l >= 0; --l) launch_level(st, nrhs, l, 2);
     } else {
       for (int l = 0; l + 1 < nlevel; ++l) launch_level(st, nrhs, l, 0);
       if (timed) cudaEventRecord(ev[1], st);
@@ -477,74 +458,256 @@ struct SolveSystem {
     top_level = L, ntop = n, top_c0 = c0, top_cb0 = F.task_cboff[F.level_ptr[L]];
   }
 
-  /// Level-0 tasks of a single-problem system as dense operators: forward
-  /// Tf ((nct+cbl) x nct, column-major) maps the task's right-hand side to
-  /// [scaled forward result; contributions], backward Tb (nct x (nct+cbl),
-  /// column-major) maps [forward result; ancestor values] to the solution.
-  /// Built from the packed host factor by applying the task's sweep to unit
-  /// vectors (same arithmetic, another summation order).
+  /// Sparse levels below the dense top of a single-problem system as dense
+  /// operators, in two stages: every level-0 task is one unit, and every
+  /// maximal subtree of tasks of levels 1..top_level-1 (a "group": a task whose
+  /// parent is in the dense top, with all its descendants above level 0) is
+  /// one unit, so the five latency-bound middle levels become one launch.
+  /// A unit with columns C (task order = elimination order):
+  ///   forward  Tf: [X[C] + folded contributions from lower stages] ->
+  ///                [D^-1 L^-1 result on C; its contributions to every CB
+  ///                 slot that names a row outside the unit]
+  ///   backward Tb: [X[C]; final X on the outside rows it references] -> X[C]
+  /// both row-major (n_out x n_in), built from the packed host factor by
+  /// running the unit's elimination on unit vectors (same arithmetic, another
+  /// summation order).  Contributions between columns of one unit stay inside
+  /// its operator; the slots it writes are exactly those the next stage's
+  /// (or the dense top's) fold lists read.
   void set_dense_bottom(const SymFactor& F, const std::vector<double>& Lp, const std::vector<double>& Dg,
                         int threads) {
     if (prob_type.size() != 1 || top_level < 1) return;
-    // every sparse level below the dense top becomes one dense-operator launch
-    const int nl = top_level;
-    const int tb0 = F.level_ptr[0], nt0 = F.level_ptr[nl] - tb0;
-    std::vector<int> c0(nt0), nct(nt0), cbo(nt0), cbl(nt0);
-    std::vector<long long> fo(nt0 + 1, 0), bo(nt0 + 1, 0);
-    for (int q = 0; q < nt0; ++q) {
-      const int t = tb0 + q;
-      c0[q] = F.task_c0[t], nct[q] = F.task_c1[t] - F.task_c0[t], cbo[q] = F.task_cboff[t], cbl[q] = F.task_cblen[t];
-      const long long nw = nct[q] + cbl[q];
-      if (nw > 128) return;  // k_dense_task stages at most 128 inputs per CTA
-      fo[q + 1] = fo[q] + nw * nct[q], bo[q + 1] = bo[q] + nw * nct[q];
+    const int L = top_level, nt = F.ntask;
+    std::vector<int> own(F.n, -1), parent(nt, -1);
+    for (int q = 0; q < nt; ++q)
+      for (int c = F.task_c0[q]; c < F.task_c1[q]; ++c) own[c] = q;
+    for (int q = 0; q < nt; ++q) {
+      int mn = INT32_MAX;
+      for (int k = 0; k < F.task_cblen[q]; ++k) mn = std::min(mn, F.cb_rows[F.task_cboff[q] + k]);
+      if (mn != INT32_MAX) parent[q] = own[mn];
     }
-    db_lptr.assign(nl + 1, 0);
-    for (int l = 0; l <= nl; ++l) db_lptr[l] = F.level_ptr[l] - tb0;
-    std::vector<double> Tf(fo[nt0]), Tb(bo[nt0]);
-    parallel_for(nt0, threads, [&](int q) {
-      const int t = tb0 + q;
-      const int n = nct[q], nw = n + cbl[q];
-      std::vector<double> Ll((std::size_t)nw * n, 0.0), ws(nw);
-      for (int k = F.task_sn0[t]; k < F.task_sn1[t]; ++k) {
-        const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
-        const int* sl = &F.slot[F.sn_rowoff[k]];
-        long long o = F.sn_valoff[k];
-        for (int j = 0; j < nc; ++j) {
-          const int jj = sl[j];
-          for (int i = j + 1; i < m; ++i) Ll[(std::size_t)jj * nw + sl[i]] = Lp[o++];
+    // CB slots of level-0 tasks precede those of higher levels (fold filter)
+    int cb1 = INT32_MAX, cb0end = 0;
+    for (int q = F.level_ptr[0]; q < F.level_ptr[1]; ++q) cb0end = std::max(cb0end, F.task_cboff[q] + F.task_cblen[q]);
+    for (int q = F.level_ptr[1]; q < nt; ++q) cb1 = std::min(cb1, F.task_cboff[q]);
+    if (cb0end > cb1) return;
+    db_cb1 = cb1;
+    // units: stage 0 = level-0 tasks, stage 1 = groups
+    std::vector<std::vector<int>> units;
+    std::vector<int> ustage;
+    for (int q = F.level_ptr[0]; q < F.level_ptr[1]; ++q) units.push_back({q}), ustage.push_back(0);
+    {
+      std::map<int, int> gi;
+      for (int q = F.level_ptr[1]; q < F.level_ptr[L]; ++q) {
+        int r = q;
+        while (parent[r] >= 0 && F.task_level[parent[r]] < L) r = parent[r];
+        auto it = gi.find(r);
+        if (it == gi.end()) it = gi.emplace(r, (int)units.size()).first, units.push_back({}), ustage.push_back(1);
+        units[it->second].push_back(q);
+      }
+    }
+    // column lists of the factor: (row position, value) below the diagonal
+    std::vector<long long> cptr(F.n + 1, 0);
+    for (int k = 0; k < F.nsn; ++k)
+      for (int j = 0; j < F.sn_ncol[k]; ++j) cptr[F.sn_col0[k] + j + 1] = F.sn_nrow[k] - j - 1;
+    for (int c = 0; c < F.n; ++c) cptr[c + 1] += cptr[c];
+    std::vector<int> crow(cptr[F.n]);
+    std::vector<double> cval(cptr[F.n]);
+    for (int k = 0; k < F.nsn; ++k) {
+      const int nc = F.sn_ncol[k], m = F.sn_nrow[k];
+      const int* R = &F.rows[F.sn_rowoff[k]];
+      long long o = F.sn_valoff[k];
+      for (int j = 0; j < nc; ++j) {
+        long long w = cptr[F.sn_col0[k] + j];
+        for (int i = j + 1; i < m; ++i) crow[w] = R[i], cval[w++] = Lp[o++];
+      }
+    }
+    const int nu = (int)units.size();
+    struct UnitOps {
+      std::vector<int> cols, slots, anc;
+      std::vector<double> Tf, Tb;
+    };
+    std::vector<UnitOps> U(nu);
+    std::atomic<int> bad{0};
+    parallel_for(nu, threads, [&](int u) {
+      UnitOps& O = U[u];
+      std::unordered_map<int, int> lidx, sidx, aidx;
+      for (int q : units[u])
+        for (int c = F.task_c0[q]; c < F.task_c1[q]; ++c) lidx[c] = (int)O.cols.size(), O.cols.push_back(c);
+      const int n = (int)O.cols.size();
+      // outside rows: CB slot of the owning task (forward), ancestor list (backward)
+      std::vector<std::unordered_map<int, int>> tslot(units[u].size());
+      for (std::size_t a = 0; a < units[u].size(); ++a) {
+        const int q = units[u][a];
+        for (int k = 0; k < F.task_cblen[q]; ++k) {
+          const int rr = F.cb_rows[F.task_cboff[q] + k];
+          if (lidx.count(rr)) continue;
+          tslot[a][rr] = (int)O.slots.size();
+          O.slots.push_back(F.task_cboff[q] + k);
+          if (!aidx.count(rr)) aidx[rr] = (int)O.anc.size(), O.anc.push_back(rr);
         }
       }
-      for (int e = 0; e < n; ++e) {
-        std::fill(ws.begin(), ws.end(), 0.0);
-        ws[e] = 1.0;
-        for (int jj = 0; jj < n; ++jj) {
-          const double xj = ws[jj];
-          if (xj == 0.0) continue;
-          const double* lc = &Ll[(std::size_t)jj * nw];
-          for (int r = jj + 1; r < nw; ++r) ws[r] -= lc[r] * xj;
-        }
-        double* out = &Tf[fo[q] + (long long)e * nw];
-        for (int r = 0; r < n; ++r) out[r] = ws[r] / Dg[c0[q] + r];
-        for (int r = n; r < nw; ++r) out[r] = ws[r];
+      std::vector<int> ctask(n);  // position of the column's task in the unit
+      {
+        int i = 0;
+        for (std::size_t a = 0; a < units[u].size(); ++a)
+          for (int c = F.task_c0[units[u][a]]; c < F.task_c1[units[u][a]]; ++c) ctask[i++] = (int)a;
       }
-      for (int e = 0; e < nw; ++e) {
-        std::fill(ws.begin(), ws.end(), 0.0);
-        ws[e] = 1.0;
-        for (int jj = n - 1; jj >= 0; --jj) {
-          const double* lc = &Ll[(std::size_t)jj * nw];
+      const int ns = (int)O.slots.size(), na = (int)O.anc.size();
+      // forward: column j of Tf (column-major (n + ns) x n)
+      O.Tf.assign((std::size_t)(n + ns) * n, 0.0);
+      std::vector<double> x(n), sv(ns);
+      for (int j = 0; j < n; ++j) {
+        std::fill(x.begin(), x.end(), 0.0), std::fill(sv.begin(), sv.end(), 0.0);
+        x[j] = 1.0;
+        for (int i = j; i < n; ++i) {
+          const double xi = x[i];
+          if (xi == 0.0) continue;
+          const int c = O.cols[i];
+          for (long long w = cptr[c]; w < cptr[c + 1]; ++w) {
+            auto it = lidx.find(crow[w]);
+            if (it != lidx.end()) {
+              if (it->second <= i) bad = 1;  // unit order must be an elimination order
+              x[it->second] -= cval[w] * xi;
+            } else {
+              auto st2 = tslot[ctask[i]].find(crow[w]);
+              if (st2 == tslot[ctask[i]].end()) {
+                bad = 1;
+                continue;
+              }
+              sv[st2->second] -= cval[w] * xi;
+            }
+          }
+        }
+        for (int i = 0; i < n; ++i) O.Tf[(std::size_t)j * (n + ns) + i] = x[i] / Dg[O.cols[i]];
+        for (int s2 = 0; s2 < ns; ++s2) O.Tf[(std::size_t)j * (n + ns) + n + s2] = sv[s2];
+      }
+      // backward: column e of Tb (column-major n x (n + na))
+      const int ni = n + na;
+      O.Tb.assign((std::size_t)n * ni, 0.0);
+      std::vector<double> z(n), av(na);
+      for (int e = 0; e < ni; ++e) {
+        std::fill(z.begin(), z.end(), 0.0), std::fill(av.begin(), av.end(), 0.0);
+        if (e < n) z[e] = 1.0;
+        else av[e - n] = 1.0;
+        for (int i = n - 1; i >= 0; --i) {
+          const int c = O.cols[i];
           double acc = 0.0;
-          for (int r = jj + 1; r < nw; ++r) acc += lc[r] * ws[r];
-          ws[jj] -= acc;
+          for (long long w = cptr[c]; w < cptr[c + 1]; ++w) {
+            auto it = lidx.find(crow[w]);
+            acc += cval[w] * (it != lidx.end() ? z[it->second] : av[aidx.at(crow[w])]);
+          }
+          z[i] -= acc;
         }
-        double* out = &Tb[bo[q] + (long long)e * n];
-        for (int r = 0; r < n; ++r) out[r] = ws[r];
+        for (int i = 0; i < n; ++i) O.Tb[(std::size_t)e * n + i] = z[i];
       }
     });
-    db_c0.upload(c0), db_nct.upload(nct), db_cbo.upload(cbo), db_cbl.upload(cbl);
-    fo.pop_back(), bo.pop_back();
-    db_fo.upload(fo), db_bo.upload(bo), db_Tf.upload(Tf), db_Tb.upload(Tb);
-    db_ntask = nt0;
+    if (bad) fail(kInternal, "dense bottom: a factor row outside its unit has no contribution slot");
+    // flatten: fwd units then bwd units; outputs >= 0 are X columns, < 0 CB slots (-1 - slot)
+    std::vector<int> nin, nout, inoff, outoff, idx_in, idx_out;
+    std::vector<long long> toff;
+    std::vector<double> T;
+    for (int dir = 0; dir < 2; ++dir)
+      for (int u = 0; u < nu; ++u) {
+        const UnitOps& O = U[u];
+        const int n = (int)O.cols.size();
+        inoff.push_back((int)idx_in.size()), outoff.push_back((int)idx_out.size()), toff.push_back((long long)T.size());
+        if (dir == 0) {
+          idx_in.insert(idx_in.end(), O.cols.begin(), O.cols.end());
+          idx_out.insert(idx_out.end(), O.cols.begin(), O.cols.end());
+          for (int sl : O.slots) idx_out.push_back(-1 - sl);
+          nin.push_back(n), nout.push_back(n + (int)O.slots.size());
+          T.insert(T.end(), O.Tf.begin(), O.Tf.end());
+        } else {
+          idx_in.insert(idx_in.end(), O.cols.begin(), O.cols.end());
+          idx_in.insert(idx_in.end(), O.anc.begin(), O.anc.end());
+          idx_out.insert(idx_out.end(), O.cols.begin(), O.cols.end());
+          nin.push_back(n + (int)O.anc.size()), nout.push_back(n);
+          T.insert(T.end(), O.Tb.begin(), O.Tb.end());
+        }
+        if (nin.back() > dev::kUnitMaxIn) return;  // inputs are staged per warp in shared memory
+      }
+    // vector indices of the positions (the permutation fused into the units)
+    const std::vector<int>& pm = F.perm;
+    std::vector<int> in_nat(idx_in.size()), out_nat(idx_out.size());
+    for (std::size_t i = 0; i < idx_in.size(); ++i) in_nat[i] = pm[idx_in[i]];
+    for (std::size_t i = 0; i < idx_out.size(); ++i) out_nat[i] = idx_out[i] >= 0 ? pm[idx_out[i]] : 0;
+    // CTA work lists: blocks of <= 128 output rows; a stage runs with S input
+    // slices per CTA (S = 4 when its units have long input ranges)
+    for (int dir = 0; dir < 2; ++dir)
+      for (int stg = 0; stg < 2; ++stg) {
+        std::vector<dev::UnitWork> w;
+        int maxin = 0;
+        for (int u = 0; u < nu; ++u) {
+          if (ustage[u] != stg) continue;
+          const int g = dir * nu + u;
+          maxin = std::max(maxin, nin[g]);
+          for (int r = 0; r < nout[g]; r += dev::kUnitRows) {
+            dev::UnitWork x{};
+            x.toff = toff[g], x.inoff = inoff[g], x.outoff = outoff[g], x.nin = nin[g], x.nout = nout[g], x.r0 = r;
+            x.nrows = std::min(dev::kUnitRows, nout[g] - r);
+            w.push_back(x);
+          }
+        }
+        db_nwork[dir][stg] = (int)w.size();
+        db_split[dir][stg] = maxin > 128 ? 4 : 1;
+        if (w.empty()) w.push_back(dev::UnitWork{});
+        db_work[dir][stg].upload(w);
+      }
+    db_in.upload(idx_in), db_out.upload(idx_out), db_in_nat.upload(in_nat), db_out_nat.upload(out_nat);
+    db_T.upload(T);
+    db_bytes = 8.0 * (double)T.size();
     dense_bottom = true;
+  }
+
+  /// x = A^-1 b for a dense-bottom single-problem system, the permutations
+  /// fused: forward units read b[perm[c]], backward units and the dense top
+  /// write x[perm[c]] (b and x may alias: every read precedes every write).
+  void solve_dense(cudaStream_t st, const double* b, double* x) {
+    launches = 0;
+    if (timed) {
+      if (!ev[0])
+        for (auto& e : ev) cudaEventCreate(&e);
+      cudaEventRecord(ev[0], st);
+    }
+    const int* perm = d_perm.p;  // position -> vector index (single problem)
+    auto units = [&](int dir, int stg) {
+      if (!db_nwork[dir][stg]) return;
+      dev::DenseUnits U;
+      U.in = db_in.p, U.in_nat = db_in_nat.p, U.out = db_out.p, U.out_nat = db_out_nat.p, U.T = db_T.p;
+      U.fold_ptr = d_fold_ptr.p + d_types_host[0].fold_base, U.fold_idx = d_fold_idx.p + d_types_host[0].foldidx_base;
+      U.cbmax = dir == 0 && stg == 1 ? db_cb1 : 0;  // groups fold the level-0 contributions
+      U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
+      U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
+      if (db_split[dir][stg] == 4)
+        dev::k_dense_unit<4><<<db_nwork[dir][stg], 4 * dev::kUnitRows, 0, st>>>(db_work[dir][stg].p, U);
+      else
+        dev::k_dense_unit<1><<<db_nwork[dir][stg], dev::kUnitRows, 0, st>>>(db_work[dir][stg].p, U);
+      ::pf::g_launches++, ++launches;
+    };
+    units(0, 0);
+    units(0, 1);
+    if (timed) cudaEventRecord(ev[1], st);
+    dev::k_dense_top_gather<<<cdiv(ntop, 8), 256, 0, st>>>(ntop, top_c0, top_cb0,
+                                                          d_fold_ptr.p + d_types_host[0].fold_base,
+                                                          d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, b, perm,
+                                                          Wres.p);
+    // twelve warps per CTA, about one CTA per SM: every row's warp co-resident
+    dev::k_dense_top_gemv<<<cdiv(ntop, 12), 384, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p, Wres.p, X.p, perm,
+                                                                               x);
+    ::pf::g_launches += 2, launches += 2;
+    if (timed) cudaEventRecord(ev[2], st);
+    units(1, 1);
+    units(1, 0);
+    if (timed) {
+      cudaEventRecord(ev[3], st);
+      cudaEventSynchronize(ev[3]);
+      for (int i = 0; i < 3; ++i) {
+        float t;
+        cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+        phase_ms[i] += t;
+      }
+    }
+    PF_CUDA_CHECK(cudaGetLastError());
   }
 
   void prepare_smem() {
@@ -1950,6 +2113,10 @@ struct Engine {
 
   /// y = Q x with Q = (G G^T)^{-1} (mortar scaling)
   void qsolve(const double* x, double* y) {
+    if (Qsys.dense_bottom) {
+      Qsys.solve_dense(st, x, y);
+      return;
+    }
     const int n = D.n_lambda;
     dev::k_perm_in<<<dim3(cdiv(n, 256), 1), 256, 0, st>>>(1, Qsys.d_prob_x.p, zero_off(), Qsys.d_prob_n.p,
                                                          Qsys.d_prob_perm.p, Qsys.d_perm.p, x, Qsys.X.p, 1); ::pf::g_launches++;
@@ -2797,21 +2964,24 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
   if (!ctx || !out || iters < 1) return PF_INVALID;
   return guarded(ctx, [&] {
     auto& E = ctx->eng;
+    pf::DevBuf<double> dx, dy;
+    dx.alloc(E.D.n_lambda), dy.alloc(E.D.n_lambda);
+    dx.zero(E.st);
     auto run = [&](auto* sys, double* o) {
       for (int i = 0; i < 3; ++i) o[i] = 0.0;
       if (!sys || !sys->L.p) return;
       sys->timed = true;
       for (double& v : sys->phase_ms) v = 0.0;
-      for (int it = 0; it < iters; ++it) sys->solve(E.st, 1);
+      for (int it = 0; it < iters; ++it) {
+        if (sys->dense_bottom) sys->solve_dense(E.st, dx.p, dy.p);
+        else sys->solve(E.st, 1);
+      }
       sys->timed = false;
       for (int i = 0; i < 3; ++i) o[i] = sys->phase_ms[i] / iters;
     };
     run(&E.Ksys, out);
     run(E.implicit_dir ? &E.Isys : nullptr, out + 3);
     run(E.use_q ? &E.Qsys : nullptr, out + 6);
-    pf::DevBuf<double> dx, dy;
-    dx.alloc(E.D.n_lambda), dy.alloc(E.D.n_lambda);
-    dx.zero(E.st);
     cudaEvent_t a, b;
     cudaEventCreate(&a), cudaEventCreate(&b);
     cudaEventRecord(a, E.st);

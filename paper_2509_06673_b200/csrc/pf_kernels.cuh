@@ -347,6 +347,38 @@ __global__ void k_dense_gemv(int n, const double* A, const double* x, double* y)
   if (threadIdx.x == 0) y[i] = s;
 }
 
+/// sum_j a[j] * xs[j] over one row (a 16-byte aligned when n is even), a
+/// warp per row: eight 16-byte loads per lane in flight, fixed order.
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ a, const double* xs, int n, int lane) {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int j0 = 0;
+  if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(a) & 15) == 0)) {
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const int n2 = n >> 1;
+    for (; j0 + 32 * 8 <= n2; j0 += 32 * 8) {  // full chunks: unpredicated loads, all in flight
+      double2 v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) v[m] = __ldg(a2 + j0 + lane + 32 * m);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int j = j0 + lane + 32 * m;
+        s[m & 1] += v[m].x * xs[2 * j], s[2 + (m & 1)] += v[m].y * xs[2 * j + 1];
+      }
+    }
+    for (int j = j0 + lane; j < n2; j += 32) s[0] += a2[j].x * xs[2 * j], s[1] += a2[j].y * xs[2 * j + 1];
+  } else {
+    for (; j0 + 32 * 8 <= n; j0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) v[m] = __ldg(a + j0 + lane + 32 * m);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) s[m & 3] += v[m] * xs[j0 + lane + 32 * m];
+    }
+    for (int j = j0 + lane; j < n; j += 32) s[0] += __ldg(a + j) * xs[j];
+  }
+  return warp_sum((s[0] + s[2]) + (s[1] + s[3]));
+}
+
 /// y = A x for a dense row-major n x n A: a warp per row (16-byte loads when
 /// the rows are 16-byte aligned, four loads in flight per lane), x staged in
 /// shared memory; grid-stride over rows.  Coarse projector (G_c^T G_c)^{-1}.
@@ -356,28 +388,9 @@ __global__ void __launch_bounds__(256) k_dense_gemv_w(int n, const double* __res
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool vec = (n & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
-    const double* a = A + (size_t)row * n;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    if (vec) {
-      const double2* a2 = reinterpret_cast<const double2*>(a);
-      const int n2 = n >> 1;
-      int j = lane;
-      for (; j + 32 < n2; j += 64) {
-        const double2 u = __ldg(a2 + j), v = __ldg(a2 + j + 32);
-        s0 += u.x * xs[2 * j], s1 += u.y * xs[2 * j + 1];
-        s2 += v.x * xs[2 * j + 64], s3 += v.y * xs[2 * j + 65];
-      }
-      if (j < n2) {
-        const double2 u = __ldg(a2 + j);
-        s0 += u.x * xs[2 * j], s1 += u.y * xs[2 * j + 1];
-      }
-    } else {
-      for (int j = lane; j < n; j += 32) s0 += __ldg(a + j) * xs[j];
-    }
-    const double s = warp_sum((s0 + s2) + (s1 + s3));
-    if (lane == 0) y[row] = s;
+    const double v = warp_row_dot(A + (size_t)row * n, xs, n, lane);
+    if (lane == 0) y[row] = v;
   }
 }
 
@@ -395,94 +408,160 @@ __global__ void __launch_bounds__(256) k_spmv_warp(int nrows, const int* __restr
   if (lane == 0) y[row] = (beta == 0.0 ? 0.0 : beta * y[row]) + alpha * s;
 }
 
-/// Dense top of a single-problem sweep, pass 1: y = X[c0..c0+n) + folded
-/// child contributions (fixed order).
+/// Folded value of one input: v + sum of the column's fold entries < cbmax
+/// (fixed order; four index loads, then four value loads in flight).
+__device__ __forceinline__ double fold_add(double v, int c, const int* __restrict__ fold_ptr,
+                                           const int* __restrict__ fold_idx, const double* __restrict__ CB,
+                                           int cbmax) {
+  for (int q = fold_ptr[c], q1 = fold_ptr[c + 1]; q < q1; q += 4) {
+    int f[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) f[m] = q + m < q1 ? fold_idx[q + m] : cbmax;
+    double w[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) w[m] = f[m] < cbmax ? CB[f[m]] : 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) v += w[m];
+  }
+  return v;
+}
+
+/// Dense top of a single-problem sweep, pass 1: y = b + folded child
+/// contributions (fixed order), b = X[c0 + i] or, with perm, src[perm[c0 + i]].
 /// Only contributions of the sparse levels (CB index < cb_top) count: the
 /// top tasks' own couplings are inside W.
 __global__ void k_dense_top_gather(int n, int c0, int cb_top, const int* __restrict__ fold_ptr,
-                                   const int* __restrict__ fold_idx, const double* __restrict__ CB, const double* X,
-                                   double* y) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                                   const int* __restrict__ fold_idx, const double* __restrict__ CB, const double* src,
+                                   const int* __restrict__ perm, double* y) {
+  // a warp per column: lanes take the fold entries, warp_sum tree (fixed order)
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
-  double v = X[c0 + i];
-  for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) {
+  double v = 0.0;
+  for (int q = fold_ptr[c0 + i] + lane, q1 = fold_ptr[c0 + i + 1]; q < q1; q += 32) {
     const int f = fold_idx[q];
     if (f < cb_top) v += CB[f];
   }
-  y[i] = v;
+  v = warp_sum(v);
+  if (lane == 0) y[i] = (perm ? src[perm[c0 + i]] : src[c0 + i]) + v;
 }
 
 /// pass 2: X[c0 + i] = sum_j W[i][j] y[j] (W = inverse of the top Schur
-/// complement), one warp per row, y staged in shared memory.
-__global__ void __launch_bounds__(256) k_dense_top_gemv(int n, int c0, const double* __restrict__ W,
-                                                        const double* __restrict__ y, double* X) {
+/// complement; also x[perm[c0 + i]] when perm is given), a warp per row, y
+/// staged in shared memory.  With fold_ptr given, each CTA gathers y itself
+/// (pass 1 fused: y = src[perm[c0 + j]] + folded contributions < cb_top).
+__global__ void __launch_bounds__(512) k_dense_top_gemv(int n, int c0, const double* __restrict__ W,
+                                                        const double* __restrict__ y, double* X,
+                                                        const int* __restrict__ perm, double* x,
+                                                        const int* __restrict__ fold_ptr = nullptr,
+                                                        const int* __restrict__ fold_idx = nullptr,
+                                                        const double* __restrict__ CB = nullptr, int cb_top = 0,
+                                                        const double* __restrict__ src = nullptr) {
   extern __shared__ double ys[];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y[i];
+  if (fold_ptr) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double v = src[perm[c0 + i]];
+      for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) {
+        const int f = fold_idx[q];
+        if (f < cb_top) v += CB[f];
+      }
+      ys[i] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y[i];
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
-    const double* w = W + (size_t)row * n;
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s += w[j] * ys[j];
-    s = warp_sum(s);
-    if (lane == 0) X[c0 + row] = s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = blockIdx.x * nw + warp; row < n; row += gridDim.x * nw) {
+    const double v = warp_row_dot(W + (size_t)row * n, ys, n, lane);
+    if (lane == 0) {
+      X[c0 + row] = v;
+      if (perm) x[perm[c0 + row]] = v;
+    }
   }
 }
 
-/// Sparse levels of a single-problem system as dense per-task operators (one
-/// CTA of four warps per task; operator column-major so a fixed input index
-/// is a coalesced column):
-/// mode 0 (forward): in = X[c0..c0+nct) + child contributions (fold lists,
-///                   staged in parallel, summed per column in fixed order),
-///                   out = [X[c0..); CB[cbo..cbo+cbl)]
-/// mode 1 (backward): in = [X[c0..); X[cb_rows]] (ancestor values, final),
-///                   out = X[c0..c0+nct).
-__global__ void __launch_bounds__(128) k_dense_task(int t0, int mode, const int* __restrict__ c0,
-                                                    const int* __restrict__ nct, const int* __restrict__ cbo,
-                                                    const int* __restrict__ cbl, const long long* __restrict__ toff,
-                                                    const double* __restrict__ T, const int* __restrict__ fold_ptr,
-                                                    const int* __restrict__ fold_idx, const int* __restrict__ cb_rows,
-                                                    double* X, double* CB) {
-  constexpr int kFold = 1024;  // fold entries staged per task (longer lists use the serial path)
-  __shared__ double in[128], fv[kFold];
-  __shared__ int fp[129];
-  const int q = t0 + blockIdx.x;
-  const int n = nct[q], nb = cbl[q], nw = n + nb, c = c0[q];
-  const int ni = mode == 0 ? n : nw, no = mode == 0 ? nw : n;
-  if (mode == 0) {
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) fp[i] = fold_ptr[c + i];
-    __syncthreads();
-    const int f0 = fp[0], nf = fp[n] - f0;
-    const bool staged = nf <= kFold;
-    if (staged) {
-      for (int f = threadIdx.x; f < nf; f += blockDim.x) fv[f] = CB[fold_idx[f0 + f]];
-      __syncthreads();
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      double v = X[c + i];
-      if (staged)
-        for (int f = fp[i]; f < fp[i + 1]; ++f) v += fv[f - f0];  // fixed order
-      else
-        for (int f = fp[i]; f < fp[i + 1]; ++f) v += CB[fold_idx[f]];
-      in[i] = v;
-    }
-  } else {
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) in[i] = i < n ? X[c + i] : X[cb_rows[cbo[q] + i - n]];
+/// Dense units of the levels below a dense top (SolveSystem::set_dense_bottom).
+struct DenseUnits {
+  const int *in, *in_nat;      // input positions / their vector indices (perm applied on the host)
+  const int *out, *out_nat;    // outputs: >= 0 position (and its vector index), < 0 CB slot (-1 - slot)
+  const double* T;             // row-major n_out x n_in per unit
+  const int *fold_ptr, *fold_idx;
+  int cbmax;                   // fold contributions with CB index < cbmax (0: none)
+  const double* b;             // forward: inputs b[in_nat] (else X[in])
+  double *X, *CB;
+  double* x;                   // backward: also x[out_nat]
+  int xout;                    // write X[c] for column outputs
+};
+/// one CTA's work: output rows [r0, r0 + nrows) (nrows <= 128) of one unit
+struct __align__(16) UnitWork {
+  long long toff;              // operator offset of the unit (column-major, ld = nout)
+  int inoff, outoff, nin, nout, r0, nrows;
+};
+constexpr int kUnitRows = 128, kUnitMaxIn = 1024;
+
+/// One CTA per (unit, block of <= 128 output rows); thread r of slice q
+/// computes the partial dot product of output row r over the q-th of S
+/// contiguous input ranges (column-major operator: a fixed input column is
+/// one coalesced read across the rows).  The first eight operator values per
+/// thread are loaded before the inputs (b or X, plus folded lower-stage
+/// contributions) are staged in shared memory, then eight loads stay in
+/// flight per thread; slices are summed in slice order (deterministic).
+template <int S>
+__global__ void __launch_bounds__(128 * S) k_dense_unit(const UnitWork* __restrict__ work, DenseUnits U) {
+  constexpr int B = 8;
+  __shared__ double in[kUnitMaxIn];
+  __shared__ double part[S > 1 ? S : 1][kUnitRows];
+  const UnitWork w = work[blockIdx.x];
+  const int r = threadIdx.x & (kUnitRows - 1), q = threadIdx.x >> 7;
+  const int ni = w.nin, ld = w.nout;
+  const int jl = (int)((long long)ni * q / S), jh = (int)((long long)ni * (q + 1) / S);
+  const bool live = r < w.nrows;
+  const double* Tc = U.T + w.toff + w.r0 + r;
+  double v[B];
+#pragma unroll
+  for (int m = 0; m < B; ++m) v[m] = (live && jl + m < jh) ? __ldg(Tc + (long long)(jl + m) * ld) : 0.0;
+  const int* il = U.in + w.inoff;
+  const int* iln = U.in_nat + w.inoff;
+  for (int i = threadIdx.x; i < ni; i += blockDim.x) {
+    const int c = il[i];
+    double x = U.b ? U.b[iln[i]] : U.X[c];
+    if (U.cbmax) x = fold_add(x, c, U.fold_ptr, U.fold_idx, U.CB, U.cbmax);
+    in[i] = x;
   }
-  __syncthreads();  // every input staged before any output overwrites X
-  const double* A = T + toff[q];
-  for (int r = threadIdx.x; r < no; r += blockDim.x) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int j = 0;
-    for (; j + 4 <= ni; j += 4) {
-      const double v0 = A[(long long)j * no + r], v1 = A[(long long)(j + 1) * no + r];
-      const double v2 = A[(long long)(j + 2) * no + r], v3 = A[(long long)(j + 3) * no + r];
-      a0 += v0 * in[j], a1 += v1 * in[j + 1], a2 += v2 * in[j + 2], a3 += v3 * in[j + 3];
-    }
-    for (; j < ni; ++j) a0 += A[(long long)j * no + r] * in[j];
-    const double v = (a0 + a1) + (a2 + a3);
-    if (r < n) X[c + r] = v;
-    else CB[cbo[q] + r - n] = v;
+  __syncthreads();
+  // register double buffer: chunk j+B streams in while chunk j is consumed
+  double a0 = 0.0, a1 = 0.0, u[B];
+  auto ld8 = [&](double (&d)[B], int j) {
+#pragma unroll
+    for (int m = 0; m < B; ++m) d[m] = (live && j + m < jh) ? __ldg(Tc + (long long)(j + m) * ld) : 0.0;
+  };
+  auto fma8 = [&](const double (&d)[B], int j) {
+#pragma unroll
+    for (int m = 0; m < B; ++m)
+      if (j + m < jh) (m & 1 ? a1 : a0) += d[m] * in[j + m];
+  };
+  for (int j = jl; j < jh; j += 2 * B) {
+    if (j + B < jh) ld8(u, j + B);
+    fma8(v, j);
+    if (j + 2 * B < jh) ld8(v, j + 2 * B);
+    if (j + B < jh) fma8(u, j + B);
+  }
+  double acc = a0 + a1;
+  if (S > 1) {
+    part[q][r] = acc;
+    __syncthreads();
+    if (q) return;
+    acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) acc += part[k][r];
+  }
+  if (!live) return;
+  const int o = U.out[w.outoff + w.r0 + r];
+  if (o < 0) {
+    U.CB[-1 - o] = acc;
+  } else {
+    if (U.xout) U.X[o] = acc;
+    if (U.x) U.x[U.out_nat[w.outoff + w.r0 + r]] = acc;
   }
 }
 
