@@ -76,6 +76,9 @@ typedef struct pf_info {
   double bytes_precond; /* algorithmic bytes of one preconditioner apply */
   int n_levels;         /* task levels of the subdomain sweep schedule */
   int dual;             /* 1: explicit local dual operators (F-apply / Dirichlet as dense GEMVs) */
+  double bytes_symv;    /* algorithmic bytes of one k_local_symv launch (n(n+1)/2 values per operator) */
+  double bytes_symv_stored; /* bytes it streams (packed 32x32 tiles incl. padding) */
+  double bytes_qsolve;  /* operator bytes of one mortar Gram solve (dense units + dense top) */
 } pf_info;
 
 typedef struct pf_sub_info {

@@ -1593,6 +1593,14 @@ struct Engine {
     reduce(y, n);
   }
 
+  /// the dominant kernel alone (roofline timing): k_local_symv of one operator
+  void symv_only(const DevBuf<double>& Op, const double* x) {
+    if (!dual) fail(kInvalid, "explicit local operators are not active");
+    dev::k_local_symv<<<nown(), 256, dl_smem, st>>>(nown(), dl_nloc.p, dl_loff.p, dl_opoff.p, Op.p, dl_lam.p, x,
+                                                    dl_Y.p);
+    ::pf::g_launches++;
+  }
+
   std::vector<int> ptype_of_own() {
     std::vector<int> pt(nown());
     for (int p = 0; p < nown(); ++p) pt[p] = OS(p).type;
@@ -2079,6 +2087,11 @@ struct Engine {
       if (use_dir) info.bytes_precond = info.bytes_fapply;
     }
     info.dual = dual ? 1 : 0;
+    if (dual) {
+      info.bytes_symv = 8.0 * (double)dl_symvals + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
+      info.bytes_symv_stored = 8.0 * (double)dl_opsize + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
+    }
+    if (use_q && Qsys.dense_bottom) info.bytes_qsolve = Qsys.db_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
   }
 
   // ------------------------------------------------------------------
@@ -2823,6 +2836,8 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
     auto op = [&] {
       if (kind == 0) E.fapply(dx.p, dy.p);
       else if (kind == 1) E.precond(dx.p, dy.p);
+      else if (kind == 3) E.symv_only(E.dl_F, dx.p);
+      else if (kind == 4) E.qsolve(dx.p, dy.p);
       else E.Ksys.solve(E.st, 1);
     };
     for (int i = 0; i < warmup; ++i) op();

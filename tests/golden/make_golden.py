@@ -27,6 +27,9 @@ FIXTURES = {
 }
 
 
+SENS_FIELDS = ("u", "xi", "eta", "p", "lambda")
+
+
 def main():
     for name, kw in FIXTURES.items():
         o = ol.Oracle(**kw)
@@ -40,6 +43,22 @@ def main():
             rep = o.report(k)
             out[f"iters{k}"] = rep["iterations"]
             out[f"hist{k}"] = rep["history"]
+        # the oracle's own sensitivity to the Krylov tolerance: the same run at
+        # tol/100; per field, max over subdomains of the relative L2 change
+        # (tests hold fields outside the north-star bar -- p -- to 10x this)
+        ot = ol.Oracle(**dict(kw, tol=kw.get("tol", 1e-10) / 100))
+        ot.run(nsteps)
+        for k in range(1, nsteps + 1):
+            xa, la = o.state(k)
+            xb, lb = ot.state(k)
+            sens = dict.fromkeys(SENS_FIELDS, 0.0)
+            for fa, fb in zip(o.fields(xa), ot.fields(xb)):
+                for f in fa:
+                    nb = np.linalg.norm(fb[f])
+                    if nb > 0:
+                        sens[f] = max(sens[f], np.linalg.norm(fa[f] - fb[f]) / nb)
+            sens["lambda"] = np.linalg.norm(la - lb) / max(np.linalg.norm(lb), 1e-300)
+            out[f"sens{k}"] = np.array([sens[f] for f in SENS_FIELDS])
         rng = np.random.default_rng(20240901)
         x = rng.uniform(-1.0, 1.0, o.n_lambda)
         o0 = ol.Oracle(**kw)
