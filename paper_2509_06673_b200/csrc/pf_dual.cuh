@@ -185,10 +185,11 @@ __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restr
                                                     const long long* __restrict__ loff,
                                                     const long long* __restrict__ opoff,
                                                     const double* __restrict__ Op, const int* __restrict__ lam,
-                                                    const double* __restrict__ x, double* __restrict__ Y) {
+                                                    const double* __restrict__ x, double* __restrict__ Y,
+                                                    const int* __restrict__ list) {
   extern __shared__ double sm[];
-  const int s = blockIdx.x;
-  if (s >= nsub) return;
+  if ((int)blockIdx.x >= nsub) return;
+  const int s = list ? list[blockIdx.x] : blockIdx.x;
   const int n = nloc[s], nt = (n + kSymT - 1) / kSymT, np = nt * kSymT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* xs = sm;            // np
@@ -232,13 +233,172 @@ __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Type-shared operators.  Subdomains of one type (same region, same sides on
+// the outer boundary, same interface signs) are translates of each other: on
+// a homogeneous material their F_s / Sd_s agree to rounding.  Setup compares
+// every owned subdomain's operators with its type's first one
+// (k_op_maxdiff); members within 1e-12 (relative, max norm) share it, and the
+// apply over all members of a type is one dense product Y_t = Op_t X_t
+// (k_type_gemm: n_t x n_t times n_t x m_t) instead of m_t GEMVs.
+// ---------------------------------------------------------------------------
+
+/// out[2p] = max_ij |A_p - A_rep(p)|, out[2p+1] = max_ij |A_rep(p)| (full row-major operators)
+__global__ void k_op_maxdiff(int np, const int* __restrict__ nloc, const long long* __restrict__ off,
+                             const int* __restrict__ rep, const double* __restrict__ A, double* out) {
+  __shared__ double rd[32], rm[32];
+  const int p = blockIdx.x;
+  if (p >= np) return;
+  const int n = nloc[p];
+  const double* a = A + off[p];
+  const double* b = A + off[rep[p]];
+  double d = 0.0, m = 0.0;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    d = fmax(d, fabs(a[e] - b[e]));
+    m = fmax(m, fabs(b[e]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) rd[w] = d, rm[w] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) d = fmax(d, rd[i]), m = fmax(m, rm[i]);
+    d = fmax(d, rd[0]), m = fmax(m, rm[0]);
+    out[2 * p] = d, out[2 * p + 1] = m;
+  }
+}
+
+/// xloc[k] = x[lam[k]] for every (subdomain, local multiplier) slot
+__global__ void k_local_gather(long long n, const int* __restrict__ lam, const double* __restrict__ x,
+                               double* __restrict__ xloc) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) xloc[k] = x[lam[k]];
+}
+
+/// one CTA: rows [r0, r0+32) x member columns [c0, c0+32) of a shared type
+struct __align__(16) GemmWork {
+  long long aoff;   // operator offset (full n x n, row-major, leading dimension lda)
+  int n, r0, c0, ncol;  // ncol: member count of the type (columns)
+  int coloff;       // first member in the column list
+  short ch0, ch1;   // K-slice: 16-chunks [ch0, ch1); partial written to plane `plane`
+  int plane, lda;
+};
+constexpr int kGM = 32, kGN = 32, kGK = 16, kGThreads = 64, kGStages = 4, kGLd = 20;
+
+__device__ __forceinline__ void cp_async16_zfill(unsigned dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+
+/// Y[col_loff[j] + i] = sum_k A_t[i][k] xloc[col_loff[j] + k] on the FP64
+/// tensor cores (mma.sync m8n8k4): a 32x32 output tile per 64-thread CTA
+/// (each warp 16 rows x 32 columns = 2 x 4 MMA tiles), K in 16-chunks through
+/// a 4-stage cp.async ring (16-byte copies: operator rows padded to an even
+/// leading dimension, slot ranges even; shared-memory rows of 20 doubles so
+/// the fragment loads are conflict-free; out-of-range elements zero-filled).
+/// K may be split into slices (planes of Y, summed by k_local_reduce in plane
+/// order).  Fixed summation order (deterministic).
+__global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restrict__ work,
+                                                         const double* __restrict__ A,
+                                                         const long long* __restrict__ col_loff,
+                                                         const double* __restrict__ xloc, double* __restrict__ Y,
+                                                         long long plane_stride) {
+  __shared__ __align__(16) double As[kGStages][kGM][kGLd];
+  __shared__ __align__(16) double Bs[kGStages][kGN][kGLd];
+  const GemmWork w = work[blockIdx.x];
+  const int tid = threadIdx.x, n = w.n;
+  const double* a = A + w.aoff;
+  // loader: k pair kp = tid % 8 (16 bytes), rows / columns tid / 8 + 8 m (m < 4)
+  const int kp = tid & 7, lr0 = tid >> 3;
+  const double* ap[4];
+  const double* bp[4];
+  bool av[4], bv[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int r = w.r0 + lr0 + 8 * m, cc = w.c0 + lr0 + 8 * m;
+    av[m] = r < n, bv[m] = cc < w.ncol;
+    ap[m] = a + (long long)(av[m] ? r : 0) * w.lda;
+    bp[m] = xloc + (bv[m] ? col_loff[w.coloff + cc] : 0);
+  }
+  const int c_beg = w.ch0, nch = w.ch1;
+  auto issue = [&](int c) {
+    if (c < nch) {
+      const int st = c % kGStages;
+      const int k = c * kGK + 2 * kp;
+      const int nb = k + 1 < n ? 16 : (k < n ? 8 : 0);  // bytes in range
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int r = lr0 + 8 * m;
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&As[st][r][2 * kp]), ap[m] + (nb ? k : 0), av[m] ? nb : 0);
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&Bs[st][r][2 * kp]), bp[m] + (nb ? k : 0), bv[m] ? nb : 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // warp wp: rows [16 wp, 16 wp + 16) x 32 columns as 2 x 4 m8n8k4 tiles
+  // (A fragment: row lane/4, k lane%4; B fragment: k lane%4, column lane/4;
+  //  C: row lane/4, columns 2 (lane%4) + {0,1})
+  const int lane = tid & 31, wp = tid >> 5;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < kGStages - 1; ++c) issue(c_beg + c);
+  for (int c = c_beg; c < nch; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kGStages - 2) : "memory");
+    __syncthreads();  // chunk c landed for every thread; chunk c-1's slot is free
+    issue(c + kGStages - 1);
+    const int st = c % kGStages;
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      const int kk = k4 + (lane & 3);
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = As[st][wp * 16 + i * 8 + (lane >> 2)][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[st][j * 8 + (lane >> 2)][kk];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cc = w.c0 + j * 8 + (lane & 3) * 2 + h;
+      if (cc >= w.ncol) continue;
+      const long long yo = col_loff[w.coloff + cc] + w.plane * plane_stride;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = w.r0 + wp * 16 + i * 8 + (lane >> 2);
+        if (r < n) Y[yo + r] = acc[i][j][h];
+      }
+    }
+}
+
 /// y[i] = alpha * sum over the multiplier's slots (fixed order) of Y
+/// (nks K-slices of the type GEMM: Y holds nks planes of `stride` slots; the
+/// planes of a slot are summed in plane order, then the slots in slot order)
 __global__ void k_local_reduce(int n, const int* __restrict__ ptr, const long long* __restrict__ slot,
-                               const double* __restrict__ Y, double* __restrict__ y, double alpha) {
+                               const double* __restrict__ Y, double* __restrict__ y, double alpha, int nks,
+                               long long stride) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = 0.0;
-  for (int q = ptr[i]; q < ptr[i + 1]; ++q) v += Y[slot[q]];
+  for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
+    double u = Y[slot[q]];
+    for (int k = 1; k < nks; ++k) u += Y[slot[q] + k * stride];
+    v += u;
+  }
   y[i] = alpha * v;
 }
 

@@ -78,6 +78,10 @@ inline DualType build_dual_type(const SubType& T, const Subdomain& rep) {
   std::vector<std::tuple<int, int, double>> ent;
   dual_local_mults(rep, lam, ent);
   X.nM = (int)lam.size();
+  if (8LL * (X.nB + X.nM) * dev::kDualLd > 227 * 1024) {  // k_dual_root stages a panel of the root front
+    X.why = "root front exceeds the shared-memory panel of k_dual_root";
+    return X;
+  }
   std::vector<std::pair<int, int>> gp;
   for (auto& e : ent) {
     const int col = std::get<1>(e);

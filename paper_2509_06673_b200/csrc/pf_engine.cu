@@ -1463,8 +1463,127 @@ struct Engine {
   DevBuf<int> dl_nloc, dl_lam, dl_rptr;
   DevBuf<long long> dl_loff, dl_opoff, dl_rslot;
   DevBuf<double> dl_F, dl_S, dl_Y;
+  DevBuf<unsigned int> red_count;  // arrival counter of k_dot_fused
   long long dl_nslots = 0, dl_opsize = 0, dl_symvals = 0;  // packed doubles / n(n+1)/2 values per operator
   int dl_nmax = 0, dl_smem = 0;
+
+  // type-shared operators (pf_dual.cuh, k_type_gemm)
+  DevBuf<double> sh_F, sh_S, dl_xloc;
+  DevBuf<dev::GemmWork> sh_work;
+  DevBuf<long long> sh_cols;
+  DevBuf<int> rest_list;
+  int sh_nwork = 0, n_rest = 0, sh_ntypes = 0, sh_members = 0, dl_nks = 1;
+  double sh_flops = 0.0, sh_bytes = 0.0;
+
+  void setup_shared(int np, int nt, const std::vector<int>& nloc, const std::vector<long long>& ploff,
+                    const std::vector<long long>& pop, const DevBuf<long long>& d_pop) {
+    std::vector<int> rep(np), first(nt, -1);
+    for (int p = 0; p < np; ++p) {
+      const int t = OS(p).type;
+      if (first[t] < 0) first[t] = p;
+      rep[p] = first[t];
+    }
+    std::vector<char> sh(np, 0);
+    std::vector<double> dd(4 * (std::size_t)np, 0.0);
+    if (!std::getenv("PF_NO_SHARE") && np > 1) {
+      DevBuf<int> d_rep, d_nl;
+      d_rep.upload(rep), d_nl.upload(nloc);
+      DevBuf<double> d_dd;
+      d_dd.alloc(4 * (std::size_t)np);
+      dev::k_op_maxdiff<<<np, 256, 0, st>>>(np, d_nl.p, d_pop.p, d_rep.p, dl_F.p, d_dd.p);
+      dev::k_op_maxdiff<<<np, 256, 0, st>>>(np, d_nl.p, d_pop.p, d_rep.p, dl_S.p, d_dd.p + 2 * np);
+      ::pf::g_launches += 2;
+      PF_CUDA_CHECK(cudaMemcpyAsync(dd.data(), d_dd.p, sizeof(double) * dd.size(), cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int p = 0; p < np; ++p)
+        sh[p] = dd[2 * p] <= 1e-12 * dd[2 * p + 1] && dd[2 * np + 2 * p] <= 1e-12 * dd[2 * np + 2 * p + 1];
+    }
+    // types with at least two sharing members
+    std::vector<std::vector<int>> mem(nt);
+    for (int p = 0; p < np; ++p)
+      if (sh[p]) mem[OS(p).type].push_back(p);
+    std::vector<std::vector<int>> groups;  // members of one operator copy
+    std::vector<char> grouped(np, 0);
+    for (int t = 0; t < nt; ++t)
+      if (mem[t].size() >= 2) {
+        groups.push_back(mem[t]);
+        for (int p : mem[t]) grouped[p] = 1;
+      }
+    std::vector<int> rest;
+    for (int p = 0; p < np; ++p)
+      if (!grouped[p]) rest.push_back(p);
+    // a handful of own subdomains (corner types) would leave a few lone CTAs
+    // of k_local_symv after the GEMM: run them as one-member groups instead
+    const int nshared = (int)groups.size();
+    if (nshared > 0 && rest.size() <= 32) {
+      for (int p : rest) groups.push_back({p});
+      rest.clear();
+    }
+    std::vector<dev::GemmWork> work;
+    std::vector<long long> cols;
+    sh_ntypes = nshared, sh_members = 0, sh_flops = sh_bytes = 0.0;
+    double maxrel = 0.0;
+    long long asz = 0;
+    auto even = [](int v) { return v + (v & 1); };
+    for (auto& g : groups) asz += (long long)nloc[g[0]] * even(nloc[g[0]]);
+    if (asz > 0) {
+      sh_F.alloc(asz), sh_S.alloc(asz);
+      sh_F.zero(st), sh_S.zero(st);
+      long long ao = 0;
+      for (std::size_t gi = 0; gi < groups.size(); ++gi) {
+        const auto& g = groups[gi];
+        const int r = g[0], n = nloc[r], m = (int)g.size();
+        const int lda = even(n);  // 16-byte aligned rows for the GEMM's cp.async copies
+        PF_CUDA_CHECK(cudaMemcpy2DAsync(sh_F.p + ao, sizeof(double) * lda, dl_F.p + pop[r], sizeof(double) * n,
+                                        sizeof(double) * n, n, cudaMemcpyDeviceToDevice, st));
+        PF_CUDA_CHECK(cudaMemcpy2DAsync(sh_S.p + ao, sizeof(double) * lda, dl_S.p + pop[r], sizeof(double) * n,
+                                        sizeof(double) * n, n, cudaMemcpyDeviceToDevice, st));
+        const int c0 = (int)cols.size();
+        for (int p : g) {
+          cols.push_back(ploff[p]);
+          if ((int)gi < nshared)
+            maxrel = std::max({maxrel, dd[2 * p] / std::max(dd[2 * p + 1], 1e-300),
+                               dd[2 * np + 2 * p] / std::max(dd[2 * np + 2 * p + 1], 1e-300)});
+        }
+        for (int r0 = 0; r0 < n; r0 += dev::kGM)
+          for (int cc = 0; cc < m; cc += dev::kGN) {
+            dev::GemmWork w{};
+            w.aoff = ao, w.n = n, w.r0 = r0, w.c0 = cc, w.ncol = m, w.coloff = c0, w.lda = lda;
+            work.push_back(w);
+          }
+        if ((int)gi < nshared) sh_members += m;
+        sh_flops += 2.0 * n * (double)n * m;
+        sh_bytes += 8.0 * n * (double)n + (8.0 + 4.0 + 8.0) * n * (double)m;
+        ao += (long long)n * lda;
+      }
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      // K-slices: enough CTAs for ~4 per SM (each slice >= 4 chunks)
+      const int tiles = (int)work.size();
+      int nmaxch = 0;
+      for (auto& w : work) nmaxch = std::max(nmaxch, (w.n + dev::kGK - 1) / dev::kGK);
+      dl_nks = std::max(1, std::min({4, (4 * 148 + tiles - 1) / std::max(1, tiles), std::max(1, nmaxch / 4)}));
+      if (const char* v = std::getenv("PF_GEMM_KSLICES")) dl_nks = std::max(1, std::atoi(v));
+      std::vector<dev::GemmWork> sl;
+      for (auto w : work) {
+        const int nch = (w.n + dev::kGK - 1) / dev::kGK;
+        for (int k = 0; k < dl_nks; ++k) {
+          w.ch0 = (short)(nch * k / dl_nks), w.ch1 = (short)(nch * (k + 1) / dl_nks), w.plane = k;
+          sl.push_back(w);
+        }
+      }
+      work.swap(sl);
+      sh_work.upload(work), sh_cols.upload(cols);
+      dl_xloc.alloc(std::max<long long>(1, dl_nslots));
+    }
+    sh_nwork = (int)work.size();
+    n_rest = (int)rest.size();
+    rest_list.upload(rest.empty() ? std::vector<int>{0} : rest);
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr,
+                   "[pf] shared operators: %d types, %d of %d subdomains (max rel. deviation %.2e), %d solo, %d by "
+                   "k_local_symv\n",
+                   sh_ntypes, sh_members, np, maxrel, (int)groups.size() - nshared, n_rest);
+  }
 
   /// F_s and Sd_s for every owned subdomain: one bordered partial
   /// factorisation (multifrontal, root front kept) + k_dual_root per chunk.
@@ -1491,9 +1610,10 @@ struct Engine {
       pgval[p] = (long long)gall.size();
       gall.insert(gall.end(), gv[p].begin(), gv[p].end());
       pop[p] = dl_opsize, dl_opsize += (long long)X.nM * X.nM;
-      ploff[p] = dl_nslots, dl_nslots += X.nM;
+      ploff[p] = dl_nslots, dl_nslots += X.nM + (X.nM & 1);  // even: 16-byte aligned slot ranges
       nloc[p] = X.nM, dl_nmax = std::max(dl_nmax, X.nM);
       lamall.insert(lamall.end(), lam[p].begin(), lam[p].end());
+      if (X.nM & 1) lamall.push_back(-1);  // padding slot (never gathered into a product, never reduced)
     }
     // per type tables
     std::vector<int> tnB(nt, 0), tnM(nt, 0), tgptr(nt, 0), tgidx(nt, 0), tfix(nt, 0), tnfix(nt, 0), gptr, gb, fixp;
@@ -1545,6 +1665,10 @@ struct Engine {
     int err = 0;
     PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) fail(kSingular, "dual operators: zero pivot on the subdomain boundary");
+    // type-shared operators: members of a type whose F_s and Sd_s agree with
+    // the type's first owned subdomain to 1e-12 (max norm, relative) use one
+    // full copy of it through k_type_gemm; the others keep their own
+    setup_shared(np, nt, nloc, ploff, pop, d_pop);
     // symmetric packed storage (lower tile triangle) replaces the full blocks
     std::vector<long long> ppk(np);
     long long pk = 0;
@@ -1570,35 +1694,55 @@ struct Engine {
     if (dl_smem > 227 * 1024) fail(kInternal, "dual operator too large for the staged symmetric GEMV");
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_local_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, dl_smem));
     // apply maps: local slots -> multipliers, multipliers -> slots (fixed subdomain order)
-    dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(ppk), dl_lam.upload(lamall);
+    dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(ppk);
+    {
+      std::vector<int> lg(lamall);
+      for (int& l : lg) l = std::max(l, 0);  // padding slots gather x[0] (never used)
+      dl_lam.upload(lg);
+    }
     std::vector<int> rptr(D.n_lambda + 1, 0);
-    for (int l : lamall) rptr[l + 1]++;
+    for (int l : lamall)
+      if (l >= 0) rptr[l + 1]++;
     for (int i = 0; i < D.n_lambda; ++i) rptr[i + 1] += rptr[i];
-    std::vector<long long> rslot(lamall.size());
+    std::vector<long long> rslot(rptr[D.n_lambda]);
     {
       std::vector<int> fillp(rptr.begin(), rptr.end() - 1);
-      for (long long k = 0; k < (long long)lamall.size(); ++k) rslot[fillp[lamall[k]]++] = k;
+      for (long long k = 0; k < (long long)lamall.size(); ++k)
+        if (lamall[k] >= 0) rslot[fillp[lamall[k]]++] = k;
     }
     dl_rptr.upload(rptr), dl_rslot.upload(rslot.empty() ? std::vector<long long>{0} : rslot);
-    dl_Y.alloc(std::max<long long>(1, dl_nslots));
+    dl_Y.alloc(std::max<long long>(1, dl_nslots * dl_nks));
+    dl_Y.zero(st);  // planes > 0 of slots outside the GEMM stay zero
+  }
+
+  /// local products Y_s = Op_s x_s of every owned subdomain (sd: Dirichlet Sd_s, else F_s)
+  void dual_local(bool sd, const double* x) {
+    if (sh_nwork) {
+      dev::k_local_gather<<<cdiv(dl_nslots, 256), 256, 0, st>>>(dl_nslots, dl_lam.p, x, dl_xloc.p);
+      dev::k_type_gemm<<<sh_nwork, dev::kGThreads, 0, st>>>(sh_work.p, sd ? sh_S.p : sh_F.p, sh_cols.p, dl_xloc.p,
+                                                            dl_Y.p, dl_nslots);
+      ::pf::g_launches += 2;
+    }
+    if (n_rest) {
+      dev::k_local_symv<<<n_rest, 256, dl_smem, st>>>(n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p, sd ? dl_S.p : dl_F.p,
+                                                      dl_lam.p, x, dl_Y.p, rest_list.p);
+      ::pf::g_launches++;
+    }
   }
 
   /// y = sum_s Op_s x restricted to the owned subdomains (then all-reduced)
-  void dual_apply(const DevBuf<double>& Op, const double* x, double* y) {
+  void dual_apply(bool sd, const double* x, double* y) {
     const int n = D.n_lambda;
-    dev::k_local_symv<<<nown(), 256, dl_smem, st>>>(nown(), dl_nloc.p, dl_loff.p, dl_opoff.p, Op.p, dl_lam.p, x,
-                                                    dl_Y.p);
+    dual_local(sd, x);
+    dev::k_local_reduce<<<cdiv(n, 256), 256, 0, st>>>(n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0, dl_nks, dl_nslots);
     ::pf::g_launches++;
-    dev::k_local_reduce<<<cdiv(n, 256), 256, 0, st>>>(n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0); ::pf::g_launches++;
     reduce(y, n);
   }
 
   /// the dominant kernel alone (roofline timing): k_local_symv of one operator
-  void symv_only(const DevBuf<double>& Op, const double* x) {
+  void symv_only(bool sd, const double* x) {
     if (!dual) fail(kInvalid, "explicit local operators are not active");
-    dev::k_local_symv<<<nown(), 256, dl_smem, st>>>(nown(), dl_nloc.p, dl_loff.p, dl_opoff.p, Op.p, dl_lam.p, x,
-                                                    dl_Y.p);
-    ::pf::g_launches++;
+    dual_local(sd, x);
   }
 
   std::vector<int> ptype_of_own() {
@@ -2055,6 +2199,7 @@ struct Engine {
     const int n = std::max(1, D.n_lambda);
     for (auto* b : {&kr_r, &kr_z, &kr_p, &kr_q, &kr_d, &kr_t, &kr_tmp, &kr_rhs}) b->alloc(n);
     red_part.alloc(dev::kRedBlocks);
+    red_count.upload(std::vector<unsigned int>{0u});
     scal.alloc(64);
     h_scal.assign(64, 0.0);
     d_status.alloc(2);
@@ -2111,7 +2256,7 @@ struct Engine {
   /// y = sum_s G_s K_s^+ G_s^T x
   void fapply(const double* x, double* y) {
     if (dual) {
-      dual_apply(dl_F, x, y);
+      dual_apply(false, x, y);
       return;
     }
     Ksys.X.zero(st);
@@ -2156,7 +2301,7 @@ struct Engine {
       return;
     }
     if (dual) {  // z = sum_s G_s S_s G_s^T r with the explicit Sd_s
-      dual_apply(dl_S, r, z);
+      dual_apply(true, r, z);
       return;
     }
     // Dirichlet: w_B = G^T r; y = K_{:,B} w_B; v_I = K_II^{-1} y_I; s_B = y_B - K_BI v_I; z = G s_B
@@ -2181,6 +2326,26 @@ struct Engine {
     qsolve(r, kr_tmp.p);
     precond_raw(kr_tmp.p, z);
     qsolve(z, z);
+  }
+
+  /// sc[slot] = <a, b> (+ the element update of `mode`) and the scalar update
+  /// `sop`, one launch (k_dot_fused); DOT_PROJ finishes the coarse projection
+  /// of b (c_tmp2 holds (G_c^T G_c)^{-1} G_c^T b from coarse_solve).
+  void fdot(int mode, const double* a, double* b, int slot, int sop) {
+    dev::FusedDot F{};
+    F.n = D.n_lambda, F.mode = mode, F.slot = slot, F.sop = sop, F.tol = D.cfg.tol;
+    F.a = a, F.b = b;
+    if (mode == dev::DOT_PROJ) F.ptr = c_ptr.p, F.idx = c_idx.p, F.val = c_val.p, F.c = c_tmp2.p;
+    F.partial = red_part.p, F.counter = red_count.p, F.sc = scal.p, F.status = d_status.p;
+    dev::k_dot_fused<<<dev::kRedBlocks, dev::kRedThreads, 0, st>>>(F);
+    ::pf::g_launches++;
+  }
+  /// M_ followed by <a, z>: preconditioner, coarse projection of z fused into the dot
+  void M_dot(const double* r, double* z, const double* a, int slot, int sop) {
+    precond(r, z);
+    ++papplies;
+    if (nc) coarse_solve(z, c_tmp2.p);
+    fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, a, z, slot, sop);
   }
 
   /// y = (G_c^T G_c)^{-1} x (dense inverse, warp per row)
@@ -2339,15 +2504,12 @@ struct Engine {
       auto iter = [&](bool first) {
         if (!first) dev::k_xpay_s<<<nb, 256, 0, st>>>(n, z, p, sc + dev::KS_B), ::pf::g_launches++;
         F_(p, q);
-        dot(n, p, q, dev::KS_PKP);
-        dot(n, p, p, dev::KS_PP);
-        dev::k_ks_pcg_alpha<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+        fdot(dev::DOT_PLAIN, p, p, dev::KS_PP, dev::SOP_NONE);
+        fdot(dev::DOT_PLAIN, p, q, dev::KS_PKP, dev::SOP_PCG_ALPHA);
         dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, 1.0, p, lambda); ::pf::g_launches++;
         project(q);
         dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, q, r); ::pf::g_launches++;
-        M_(r, z);
-        dot(n, r, z, dev::KS_RZN);
-        dev::k_ks_pcg_beta<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
+        M_dot(r, z, r, dev::KS_RZN, dev::SOP_PCG_BETA);
       };
       for (int k = 0; k < maxit; ++k) {
         if (k == 0) iter(true);
@@ -2382,18 +2544,13 @@ struct Engine {
     // iteration = [u = M r, rho, q = u + b q (not in the first)] F q, sigma, r, tau, lambda
     auto iter = [&](bool first) {
       if (!first) {
-        M_(r, u);
-        dot(n, r, u, dev::KS_RHON);
-        dev::k_ks_sqmr_b<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+        M_dot(r, u, r, dev::KS_RHON, dev::SOP_SQMR_B);                                  // u = P M r, rho
         dev::k_xpay_s<<<nb, 256, 0, st>>>(n, u, q, sc + dev::KS_B); ::pf::g_launches++;  // q = u + b q
       }
       F_(q, t);
-      project(t);
-      dot(n, q, t, dev::KS_SIGMA);
-      dev::k_ks_sqmr_a<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
-      dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, t, r); ::pf::g_launches++;
-      dot(n, r, r, dev::KS_RR);
-      dev::k_ks_sqmr_tau<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
+      if (nc) coarse_solve(t, c_tmp2.p);
+      fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);  // t = P F q, sigma, a
+      fdot(dev::DOT_AXPY, t, r, dev::KS_RR, dev::SOP_SQMR_TAU);                         // r -= a t, tau
       dev::k_sqmr_dx_s<<<nb, 256, 0, st>>>(n, sc, q, d, lambda); ::pf::g_launches++;
     };
     for (int k = 0; k < maxit; ++k) {
@@ -2836,7 +2993,7 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
     auto op = [&] {
       if (kind == 0) E.fapply(dx.p, dy.p);
       else if (kind == 1) E.precond(dx.p, dy.p);
-      else if (kind == 3) E.symv_only(E.dl_F, dx.p);
+      else if (kind == 3) E.symv_only(false, dx.p);
       else if (kind == 4) E.qsolve(dx.p, dy.p);
       else E.Ksys.solve(E.st, 1);
     };

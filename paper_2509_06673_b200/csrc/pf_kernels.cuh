@@ -282,18 +282,18 @@ __global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d,
   d[i] = dn;
   x[i] += dn;
 }
-__global__ void k_ks_sqmr_init(double* sc, int* status) {
+__device__ __forceinline__ void ks_sqmr_init(double* sc, int* status) {
   const double t0 = sqrt(sc[KS_RR]);
   sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0;
   status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
 }
-__global__ void k_ks_sqmr_a(double* sc, int* status) {
+__device__ __forceinline__ void ks_sqmr_a(double* sc, int* status) {
   const double sigma = sc[KS_SIGMA];
   if (sigma == 0.0 || !isfinite(sigma)) status[0] = KST_SIGMA;
   sc[KS_A] = sc[KS_RHO] / sigma;
 }
-__global__ void k_ks_sqmr_tau(double* sc, int* status, double tol) {
+__device__ __forceinline__ void ks_sqmr_tau(double* sc, int* status, double tol) {
   const double rn = sqrt(sc[KS_RR]);
   const double th_old = sc[KS_THETA];
   const double theta = rn / sc[KS_TAU];
@@ -304,22 +304,22 @@ __global__ void k_ks_sqmr_tau(double* sc, int* status, double tol) {
   status[1] += 1;
   if (status[0] == KST_RUN && tau <= tol * sc[KS_T0]) status[0] = KST_CONV;
 }
-__global__ void k_ks_sqmr_b(double* sc, int* status) {
+__device__ __forceinline__ void ks_sqmr_b(double* sc, int* status) {
   if (sc[KS_RHO] == 0.0 && status[0] == KST_RUN) status[0] = KST_RHO;
   sc[KS_B] = sc[KS_RHON] / sc[KS_RHO];
   sc[KS_RHO] = sc[KS_RHON];
 }
-__global__ void k_ks_pcg_init(double* sc, int* status) {
+__device__ __forceinline__ void ks_pcg_init(double* sc, int* status) {
   const double d0 = sqrt(fmax(sc[KS_RZ], 0.0));
   sc[KS_D0] = d0, sc[KS_REL] = 1.0;
   status[0] = (d0 == 0.0 || !(d0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
 }
-__global__ void k_ks_pcg_alpha(double* sc, int* status) {
+__device__ __forceinline__ void ks_pcg_alpha(double* sc, int* status) {
   if (sc[KS_PKP] <= 1e-14 * sc[KS_PP]) status[0] = KST_PKP;
   sc[KS_A] = sc[KS_RZ] / sc[KS_PKP];
 }
-__global__ void k_ks_pcg_beta(double* sc, int* status, double tol) {
+__device__ __forceinline__ void ks_pcg_beta(double* sc, int* status, double tol) {
   const double rzn = sc[KS_RZN];
   const double delta = sqrt(fmax(rzn, 0.0));
   sc[KS_REL] = delta / sc[KS_D0];
@@ -332,6 +332,90 @@ __global__ void k_ks_pcg_beta(double* sc, int* status, double tol) {
   if (rzn <= 0.0) status[0] = KST_RZ;
   sc[KS_B] = rzn / sc[KS_RZ];
   sc[KS_RZ] = rzn;
+}
+
+__global__ void k_ks_sqmr_init(double* sc, int* status) { ks_sqmr_init(sc, status); }
+__global__ void k_ks_sqmr_a(double* sc, int* status) { ks_sqmr_a(sc, status); }
+__global__ void k_ks_sqmr_tau(double* sc, int* status, double tol) { ks_sqmr_tau(sc, status, tol); }
+__global__ void k_ks_sqmr_b(double* sc, int* status) { ks_sqmr_b(sc, status); }
+__global__ void k_ks_pcg_init(double* sc, int* status) { ks_pcg_init(sc, status); }
+__global__ void k_ks_pcg_alpha(double* sc, int* status) { ks_pcg_alpha(sc, status); }
+__global__ void k_ks_pcg_beta(double* sc, int* status, double tol) { ks_pcg_beta(sc, status, tol); }
+
+/// scalar update run by the last block of a fused dot (k_dot_fused)
+enum : int { SOP_NONE = 0, SOP_SQMR_INIT, SOP_SQMR_A, SOP_SQMR_TAU, SOP_SQMR_B, SOP_PCG_INIT, SOP_PCG_ALPHA,
+             SOP_PCG_BETA };
+__device__ __forceinline__ void ks_run(int sop, double* sc, int* status, double tol) {
+  switch (sop) {
+    case SOP_SQMR_INIT: ks_sqmr_init(sc, status); break;
+    case SOP_SQMR_A: ks_sqmr_a(sc, status); break;
+    case SOP_SQMR_TAU: ks_sqmr_tau(sc, status, tol); break;
+    case SOP_SQMR_B: ks_sqmr_b(sc, status); break;
+    case SOP_PCG_INIT: ks_pcg_init(sc, status); break;
+    case SOP_PCG_ALPHA: ks_pcg_alpha(sc, status); break;
+    case SOP_PCG_BETA: ks_pcg_beta(sc, status, tol); break;
+    default: break;
+  }
+}
+
+/// One-launch dot product + Krylov scalar update: every block reduces its
+/// grid-stride share (the k_dot_partial assignment) in a fixed tree, the last
+/// block to arrive (threadfence + counter) sums the block partials in block
+/// order into sc[slot] and runs the scalar update `sop`.  Element modes:
+///   DOT_PLAIN : acc += a_i b_i
+///   DOT_PROJ  : b_i -= sum_q val[q] c[idx[q]] over row i (the last step of the
+///               coarse projection b <- b - G_c c), then acc += a_i b_i
+///   DOT_AXPY  : b_i -= sc[KS_A] a_i, then acc += b_i b_i
+enum : int { DOT_PLAIN = 0, DOT_PROJ = 1, DOT_AXPY = 2 };
+struct FusedDot {
+  int n, mode, slot, sop;
+  double tol;
+  const double* a;
+  double* b;
+  const int *ptr, *idx;
+  const double *val, *c;
+  double* partial;
+  unsigned int* counter;
+  double* sc;
+  int* status;
+};
+__global__ void __launch_bounds__(kRedThreads) k_dot_fused(FusedDot F) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  double s = 0.0;
+  const double ca = F.mode == DOT_AXPY ? F.sc[KS_A] : 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F.n; i += gridDim.x * blockDim.x) {
+    if (F.mode == DOT_PROJ) {
+      double v = 0.0;
+      for (int q = F.ptr[i]; q < F.ptr[i + 1]; ++q) v += F.val[q] * F.c[F.idx[q]];
+      const double bi = F.b[i] - v;
+      F.b[i] = bi;
+      s += F.a[i] * bi;
+    } else if (F.mode == DOT_AXPY) {
+      const double bi = F.b[i] - ca * F.a[i];
+      F.b[i] = bi;
+      s += bi * bi;
+    } else {
+      s += F.a[i] * F.b[i];
+    }
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    F.partial[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(F.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) t += ((volatile double*)F.partial)[i];
+  t = block_sum(t, red);
+  if (threadIdx.x == 0) {
+    F.sc[F.slot] = t;
+    *F.counter = 0u;
+    ks_run(F.sop, F.sc, F.status, F.tol);
+  }
 }
 
 // ---------------------------------------------------------------------------
