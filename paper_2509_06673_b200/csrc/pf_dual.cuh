@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restr
                                                     const double* __restrict__ Op, const int* __restrict__ lam,
                                                     const double* __restrict__ x, double* __restrict__ Y,
                                                     const int* __restrict__ list) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   extern __shared__ double sm[];
   if ((int)blockIdx.x >= nsub) return;
   const int s = list ? list[blockIdx.x] : blockIdx.x;
@@ -274,6 +276,8 @@ __global__ void k_op_maxdiff(int np, const int* __restrict__ nloc, const long lo
 /// xloc[k] = x[lam[k]] for every (subdomain, local multiplier) slot
 __global__ void k_local_gather(long long n, const int* __restrict__ lam, const double* __restrict__ x,
                                double* __restrict__ xloc) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) xloc[k] = x[lam[k]];
 }
@@ -307,6 +311,7 @@ __global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restr
                                                          long long plane_stride) {
   __shared__ __align__(16) double As[kGStages][kGM][kGLd];
   __shared__ __align__(16) double Bs[kGStages][kGN][kGLd];
+  if (kPdlEarly) pdl_trigger();
   const GemmWork w = work[blockIdx.x];
   const int tid = threadIdx.x, n = w.n;
   const double* a = A + w.aoff;
@@ -323,19 +328,34 @@ __global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restr
     bp[m] = xloc + (bv[m] ? col_loff[w.coloff + cc] : 0);
   }
   const int c_beg = w.ch0, nch = w.ch1;
-  auto issue = [&](int c) {
+  // operator (A) and member-input (B) copies of chunk c; B depends on the
+  // predecessor kernel (PDL), A does not
+  auto issueA = [&](int c) {
     if (c < nch) {
       const int st = c % kGStages;
       const int k = c * kGK + 2 * kp;
       const int nb = k + 1 < n ? 16 : (k < n ? 8 : 0);  // bytes in range
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int r = lr0 + 8 * m;
-        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&As[st][r][2 * kp]), ap[m] + (nb ? k : 0), av[m] ? nb : 0);
-        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&Bs[st][r][2 * kp]), bp[m] + (nb ? k : 0), bv[m] ? nb : 0);
-      }
+      for (int m = 0; m < 4; ++m)
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&As[st][lr0 + 8 * m][2 * kp]), ap[m] + (nb ? k : 0),
+                         av[m] ? nb : 0);
+    }
+  };
+  auto issueB = [&](int c) {
+    if (c < nch) {
+      const int st = c % kGStages;
+      const int k = c * kGK + 2 * kp;
+      const int nb = k + 1 < n ? 16 : (k < n ? 8 : 0);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&Bs[st][lr0 + 8 * m][2 * kp]), bp[m] + (nb ? k : 0),
+                         bv[m] ? nb : 0);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto issue = [&](int c) {
+    issueA(c);
+    issueB(c);
   };
   // warp wp: rows [16 wp, 16 wp + 16) x 32 columns as 2 x 4 m8n8k4 tiles
   // (A fragment: row lane/4, k lane%4; B fragment: k lane%4, column lane/4;
@@ -346,8 +366,13 @@ __global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restr
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // prologue: operator chunks before the PDL wait (they land in the first
+  // commit group), member inputs after it
 #pragma unroll
-  for (int c = 0; c < kGStages - 1; ++c) issue(c_beg + c);
+  for (int c = 0; c < kGStages - 1; ++c) issueA(c_beg + c);
+  pdl_wait();
+#pragma unroll
+  for (int c = 0; c < kGStages - 1; ++c) issueB(c_beg + c);
   for (int c = c_beg; c < nch; ++c) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kGStages - 2) : "memory");
     __syncthreads();  // chunk c landed for every thread; chunk c-1's slot is free
@@ -391,6 +416,8 @@ __global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restr
 __global__ void k_local_reduce(int n, const int* __restrict__ ptr, const long long* __restrict__ slot,
                                const double* __restrict__ Y, double* __restrict__ y, double alpha, int nks,
                                long long stride) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = 0.0;

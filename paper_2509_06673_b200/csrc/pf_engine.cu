@@ -103,6 +103,25 @@ static void parallel_for(int n, int threads, F&& f) {
 
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+/// Kernel launch with programmatic dependent launch (PDL): the kernel may be
+/// scheduled while its predecessor on the stream drains and waits for it in
+/// pdl_wait() (pf_kernels.cuh); PF_NO_PDL=1 turns the attribute off.
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("PF_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at, cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+  ::pf::g_launches++;
+}
+
 // ---------------------------------------------------------------------------
 // A batch of sparse LDL^T systems sharing symbolic types, solved on device.
 // ---------------------------------------------------------------------------
@@ -243,11 +262,14 @@ struct SolveSystem {
       pn.push_back(F.n);
       pperm.push_back(type_perm_off[ptype[p]]);
     }
-    d_wp.clear(), d_wt.clear(), d_work.clear();
+    d_wp.clear(), d_wt.clear(), d_work.clear(), h_work.clear(), h_wp.clear();
+    h_tlbeg = tlbeg, h_nval.assign(np, 0);
+    for (int p = 0; p < np; ++p) h_nval[p] = types[ptype[p]]->nval;
     d_wp.resize(nlevel), d_wt.resize(nlevel), d_work.resize(nlevel);
     level_nwork.assign(nlevel, 0);
     for (int l = 0; l < nlevel; ++l) {
       d_wp[l].upload(wp[l]), d_wt[l].upload(wt[l]);
+      h_wp.push_back(wp[l]);
       level_nwork[l] = (int)wp[l].size();
       std::vector<dev::WorkRec> wr(wp[l].size());
       for (std::size_t i = 0; i < wr.size(); ++i) {
@@ -265,6 +287,7 @@ struct SolveSystem {
         r.cb_base = (int)T.cb_base, r.pad = 0;
       }
       d_work[l].upload(wr);
+      h_work.push_back(std::move(wr));
     }
     ws_max = 0;
     for (int l = 0; l < nlevel; ++l) ws_max = std::max(ws_max, level_ws[l]);
@@ -316,6 +339,68 @@ struct SolveSystem {
     S.nrhs = nrhs;
     S.x_stride = total_x, S.cb_stride = total_cb;
     return S;
+  }
+
+  std::vector<std::vector<dev::WorkRec>> h_work;  // host copies (factor sharing rewrites lofs)
+  std::vector<long long> h_tlbeg, h_nval;
+  std::vector<std::vector<int>> h_wp;
+  int shared_factors = 0;  // problems reading another problem's factor values
+
+  /// Same-type factor sharing: problems of one symbolic
+  /// type whose numeric factor values are bitwise identical to the type's
+  /// first problem's (translates of one subdomain on a homogeneous material)
+  /// read that copy; the value storage is compacted to the distinct factors.
+  /// Every solve still runs the full sweep for every problem.
+  void share_factors(cudaStream_t st) {
+    const int np = (int)prob_type.size();
+    std::vector<int> rep(np), first(syms.size(), -1);
+    for (int p = 0; p < np; ++p) {
+      if (first[prob_type[p]] < 0) first[prob_type[p]] = p;
+      rep[p] = first[prob_type[p]];
+    }
+    DevBuf<long long> d_a, d_b, d_n;
+    DevBuf<int> d_eq;
+    std::vector<long long> a(np), b(np), nn(np);
+    for (int p = 0; p < np; ++p) a[p] = prob_lval[p], b[p] = prob_lval[rep[p]], nn[p] = h_nval[p];
+    d_a.upload(a), d_b.upload(b), d_n.upload(nn);
+    d_eq.upload(std::vector<int>(np, 1));
+    dev::k_values_equal<<<dim3(64, np), 256, 0, st>>>(np, d_a.p, d_b.p, d_n.p, L.p, d_eq.p);
+    ::pf::g_launches++;
+    std::vector<int> eq(np);
+    PF_CUDA_CHECK(cudaMemcpyAsync(eq.data(), d_eq.p, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    // compacted storage: one copy per distinct factor
+    std::vector<long long> nl(np, -1);
+    long long tot = 0;
+    for (int p = 0; p < np; ++p) {
+      if (eq[p] && rep[p] != p) continue;
+      tot = (tot + 1) & ~1LL;
+      nl[p] = tot, tot += h_nval[p];
+    }
+    for (int p = 0; p < np; ++p)
+      if (nl[p] < 0) nl[p] = nl[rep[p]];
+    shared_factors = 0;
+    for (int p = 0; p < np; ++p) shared_factors += eq[p] && rep[p] != p;
+    if (!shared_factors) return;
+    DevBuf<double> L2;
+    L2.alloc(tot + 4);
+    for (int p = 0; p < np; ++p)
+      if (!(eq[p] && rep[p] != p))
+        PF_CUDA_CHECK(cudaMemcpyAsync(L2.p + nl[p], L.p + prob_lval[p], sizeof(double) * h_nval[p],
+                                      cudaMemcpyDeviceToDevice, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    L = std::move(L2);
+    total_L = tot;
+    for (int l = 0; l < nlevel; ++l) {
+      auto& wr = h_work[l];
+      for (std::size_t i = 0; i < wr.size(); ++i) {
+        const int p = h_wp[l][i];
+        wr[i].lofs = wr[i].lofs - prob_lval[p] + nl[p];
+      }
+      d_work[l].upload(wr);
+    }
+    prob_lval = nl;
+    d_prob_lval.upload(prob_lval);
   }
 
   int launches = 0;
@@ -631,25 +716,29 @@ struct SolveSystem {
     std::vector<int> in_nat(idx_in.size()), out_nat(idx_out.size());
     for (std::size_t i = 0; i < idx_in.size(); ++i) in_nat[i] = pm[idx_in[i]];
     for (std::size_t i = 0; i < idx_out.size(); ++i) out_nat[i] = idx_out[i] >= 0 ? pm[idx_out[i]] : 0;
-    // CTA work lists: blocks of <= 128 output rows; a stage runs with S input
-    // slices per CTA (S = 4 when its units have long input ranges)
+    // CTA work lists: blocks of <= 64 / 128 output rows; a stage runs with S
+    // input slices per CTA (S = 4, 128-row blocks when its units have long
+    // input ranges)
     for (int dir = 0; dir < 2; ++dir)
       for (int stg = 0; stg < 2; ++stg) {
         std::vector<dev::UnitWork> w;
         int maxin = 0;
+        for (int u = 0; u < nu; ++u)
+          if (ustage[u] == stg) maxin = std::max(maxin, nin[dir * nu + u]);
+        db_split[dir][stg] = maxin > 128 ? 4 : 1;
+        // one slice: 64-row blocks (small level-0 units leave fewer idle threads)
+        const int rb = db_split[dir][stg] == 1 ? 64 : dev::kUnitRows;
         for (int u = 0; u < nu; ++u) {
           if (ustage[u] != stg) continue;
           const int g = dir * nu + u;
-          maxin = std::max(maxin, nin[g]);
-          for (int r = 0; r < nout[g]; r += dev::kUnitRows) {
+          for (int r = 0; r < nout[g]; r += rb) {
             dev::UnitWork x{};
             x.toff = toff[g], x.inoff = inoff[g], x.outoff = outoff[g], x.nin = nin[g], x.nout = nout[g], x.r0 = r;
-            x.nrows = std::min(dev::kUnitRows, nout[g] - r);
+            x.nrows = std::min(rb, nout[g] - r);
             w.push_back(x);
           }
         }
         db_nwork[dir][stg] = (int)w.size();
-        db_split[dir][stg] = maxin > 128 ? 4 : 1;
         if (w.empty()) w.push_back(dev::UnitWork{});
         db_work[dir][stg].upload(w);
       }
@@ -679,22 +768,21 @@ struct SolveSystem {
       U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
       U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
       if (db_split[dir][stg] == 4)
-        dev::k_dense_unit<4><<<db_nwork[dir][stg], 4 * dev::kUnitRows, 0, st>>>(db_work[dir][stg].p, U);
+        launch_pdl(dev::k_dense_unit<4>, db_nwork[dir][stg], 4 * dev::kUnitRows, 0, st, db_work[dir][stg].p, U);
       else
-        dev::k_dense_unit<1><<<db_nwork[dir][stg], dev::kUnitRows, 0, st>>>(db_work[dir][stg].p, U);
-      ::pf::g_launches++, ++launches;
+        launch_pdl(dev::k_dense_unit<1, 64>, db_nwork[dir][stg], 64, 0, st, db_work[dir][stg].p, U);
+      ++launches;
     };
     units(0, 0);
     units(0, 1);
     if (timed) cudaEventRecord(ev[1], st);
-    dev::k_dense_top_gather<<<cdiv(ntop, 8), 256, 0, st>>>(ntop, top_c0, top_cb0,
-                                                          d_fold_ptr.p + d_types_host[0].fold_base,
-                                                          d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, b, perm,
-                                                          Wres.p);
+    launch_pdl(dev::k_dense_top_gather, cdiv(ntop, 8), 256, 0, st, ntop, top_c0, top_cb0,
+               d_fold_ptr.p + d_types_host[0].fold_base, d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, b, perm,
+               Wres.p);
     // twelve warps per CTA, about one CTA per SM: every row's warp co-resident
-    dev::k_dense_top_gemv<<<cdiv(ntop, 12), 384, sizeof(double) * ntop, st>>>(ntop, top_c0, W.p, Wres.p, X.p, perm,
-                                                                               x);
-    ::pf::g_launches += 2, launches += 2;
+    launch_pdl(dev::k_dense_top_gemv, cdiv(ntop, 12), 384, sizeof(double) * ntop, st, ntop, top_c0, W.p, Wres.p, X.p,
+               perm, x, nullptr, nullptr, nullptr, 0, nullptr);
+    launches += 2;
     if (timed) cudaEventRecord(ev[2], st);
     units(1, 1);
     units(1, 0);
@@ -1130,6 +1218,7 @@ struct Engine {
 
   ~Engine() {
     if (kr_exec) cudaGraphExecDestroy(kr_exec);
+    if (lp_exec) cudaGraphExecDestroy(lp_exec);
     if (h_status) cudaFreeHost(h_status);
     if (comm) ncclCommDestroy(comm);
     if (st) cudaStreamDestroy(st);
@@ -1269,6 +1358,13 @@ struct Engine {
     } else {
       factor_device(Ksys, ksym, false);
       if (implicit_dir) factor_device(Isys, isym, true);
+    }
+    if (!std::getenv("PF_NO_SHARE")) {
+      Ksys.share_factors(st);
+      if (implicit_dir) Isys.share_factors(st);
+      if (std::getenv("PF_VERBOSE"))
+        std::fprintf(stderr, "[pf] shared factors: K %d of %d problems read a type copy (%.2f GB of values)\n",
+                     Ksys.shared_factors, (int)Ksys.prob_type.size(), 8e-9 * (double)Ksys.total_L);
     }
     Ksys.prepare_smem();
     if (implicit_dir) Isys.prepare_smem();
@@ -1718,15 +1814,13 @@ struct Engine {
   /// local products Y_s = Op_s x_s of every owned subdomain (sd: Dirichlet Sd_s, else F_s)
   void dual_local(bool sd, const double* x) {
     if (sh_nwork) {
-      dev::k_local_gather<<<cdiv(dl_nslots, 256), 256, 0, st>>>(dl_nslots, dl_lam.p, x, dl_xloc.p);
-      dev::k_type_gemm<<<sh_nwork, dev::kGThreads, 0, st>>>(sh_work.p, sd ? sh_S.p : sh_F.p, sh_cols.p, dl_xloc.p,
-                                                            dl_Y.p, dl_nslots);
-      ::pf::g_launches += 2;
+      launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, x, dl_xloc.p);
+      launch_pdl(dev::k_type_gemm, sh_nwork, dev::kGThreads, 0, st, sh_work.p, sd ? sh_S.p : sh_F.p, sh_cols.p,
+                 dl_xloc.p, dl_Y.p, dl_nslots);
     }
     if (n_rest) {
-      dev::k_local_symv<<<n_rest, 256, dl_smem, st>>>(n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p, sd ? dl_S.p : dl_F.p,
-                                                      dl_lam.p, x, dl_Y.p, rest_list.p);
-      ::pf::g_launches++;
+      launch_pdl(dev::k_local_symv, n_rest, 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p,
+                 sd ? dl_S.p : dl_F.p, dl_lam.p, x, dl_Y.p, rest_list.p);
     }
   }
 
@@ -1734,8 +1828,8 @@ struct Engine {
   void dual_apply(bool sd, const double* x, double* y) {
     const int n = D.n_lambda;
     dual_local(sd, x);
-    dev::k_local_reduce<<<cdiv(n, 256), 256, 0, st>>>(n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0, dl_nks, dl_nslots);
-    ::pf::g_launches++;
+    launch_pdl(dev::k_local_reduce, cdiv(n, 256), 256, 0, st, n, dl_rptr.p, dl_rslot.p, dl_Y.p, y, 1.0, dl_nks,
+               dl_nslots);
     reduce(y, n);
   }
 
@@ -2337,8 +2431,7 @@ struct Engine {
     F.a = a, F.b = b;
     if (mode == dev::DOT_PROJ) F.ptr = c_ptr.p, F.idx = c_idx.p, F.val = c_val.p, F.c = c_tmp2.p;
     F.partial = red_part.p, F.counter = red_count.p, F.sc = scal.p, F.status = d_status.p;
-    dev::k_dot_fused<<<dev::kRedBlocks, dev::kRedThreads, 0, st>>>(F);
-    ::pf::g_launches++;
+    launch_pdl(dev::k_dot_fused, dev::kRedBlocks, dev::kRedThreads, 0, st, F);
   }
   /// M_ followed by <a, z>: preconditioner, coarse projection of z fused into the dot
   void M_dot(const double* r, double* z, const double* a, int slot, int sop) {
@@ -2350,13 +2443,11 @@ struct Engine {
 
   /// y = (G_c^T G_c)^{-1} x (dense inverse, warp per row)
   void coarse_gemv(const double* x, double* y) {
-    dev::k_dense_gemv_w<<<std::min(cdiv(nc, 8), 4 * 148), 256, sizeof(double) * nc, st>>>(nc, c_ainv.p, x, y);
-    ::pf::g_launches++;
+    launch_pdl(dev::k_dense_gemv_w, std::min(cdiv(nc, 8), 4 * 148), 256, sizeof(double) * nc, st, nc, c_ainv.p, x, y);
   }
   /// y = (G_c^T G_c)^{-1} G_c^T v
   void coarse_solve(const double* v, double* y) {
-    dev::k_spmv_warp<<<cdiv(nc, 8), 256, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0);
-    ::pf::g_launches++;
+    launch_pdl(dev::k_spmv_warp, cdiv(nc, 8), 256, 0, st, nc, ct_ptr.p, ct_idx.p, ct_val.p, v, c_tmp1.p, 1.0, 0.0);
     coarse_gemv(c_tmp1.p, y);
   }
 
@@ -2502,27 +2593,30 @@ struct Engine {
       PF_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       // iteration = [p = z + beta p (not in the first)] F p, alpha, lambda, r, M r, beta
       auto iter = [&](bool first) {
-        if (!first) dev::k_xpay_s<<<nb, 256, 0, st>>>(n, z, p, sc + dev::KS_B), ::pf::g_launches++;
+        if (!first) launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, z, p, sc + dev::KS_B);
         F_(p, q);
         fdot(dev::DOT_PLAIN, p, p, dev::KS_PP, dev::SOP_NONE);
         fdot(dev::DOT_PLAIN, p, q, dev::KS_PKP, dev::SOP_PCG_ALPHA);
-        dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, 1.0, p, lambda); ::pf::g_launches++;
+        launch_pdl(dev::k_axpy_s, nb, 256, 0, st, n, sc + dev::KS_A, 1.0, p, lambda);
         project(q);
-        dev::k_axpy_s<<<nb, 256, 0, st>>>(n, sc + dev::KS_A, -1.0, q, r); ::pf::g_launches++;
+        launch_pdl(dev::k_axpy_s, nb, 256, 0, st, n, sc + dev::KS_A, -1.0, q, r);
         M_dot(r, z, r, dev::KS_RZN, dev::SOP_PCG_BETA);
       };
-      for (int k = 0; k < maxit; ++k) {
-        if (k == 0) iter(true);
-        else graphed(lambda, 1, [&] { iter(false); });
-        const int s_ = status();
-        rep.iterations = h_status[1];
-        if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, rel_residual());
-        if (s_ == dev::KST_CONV) {
-          rep.converged = 1;
-          break;
+      iter(true);
+      if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", 1, rel_residual());
+      if (status() == dev::KST_RUN && maxit > 1 && loop_ok() && !trace) {
+        graphed_loop(lambda, 1, maxit, [&] { iter(false); });
+        status();
+      } else {
+        for (int k = 1; k < maxit && h_status[0] == dev::KST_RUN; ++k) {
+          graphed(lambda, 1, [&] { iter(false); });
+          status();
+          if (trace) std::fprintf(stderr, "[pf] pcg %d %.17g\n", k + 1, rel_residual());
         }
-        if (s_ != dev::KST_RUN) breakdown(s_);
       }
+      rep.iterations = h_status[1];
+      if (h_status[0] == dev::KST_CONV) rep.converged = 1;
+      else if (h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
       rep.rel_residual = rel_residual();
       return;
     }
@@ -2545,26 +2639,81 @@ struct Engine {
     auto iter = [&](bool first) {
       if (!first) {
         M_dot(r, u, r, dev::KS_RHON, dev::SOP_SQMR_B);                                  // u = P M r, rho
-        dev::k_xpay_s<<<nb, 256, 0, st>>>(n, u, q, sc + dev::KS_B); ::pf::g_launches++;  // q = u + b q
+        launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, u, q, sc + dev::KS_B);  // q = u + b q
       }
       F_(q, t);
       if (nc) coarse_solve(t, c_tmp2.p);
       fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);  // t = P F q, sigma, a
       fdot(dev::DOT_AXPY, t, r, dev::KS_RR, dev::SOP_SQMR_TAU);                         // r -= a t, tau
-      dev::k_sqmr_dx_s<<<nb, 256, 0, st>>>(n, sc, q, d, lambda); ::pf::g_launches++;
+      launch_pdl(dev::k_sqmr_dx_s, nb, 256, 0, st, n, sc, q, d, lambda);
     };
-    for (int k = 0; k < maxit; ++k) {
-      if (k == 0) iter(true);
-      else graphed(lambda, 2, [&] { iter(false); });
-      const int s_ = status();
-      rep.iterations = h_status[1];
-      if (s_ == dev::KST_CONV) {
-        rep.converged = 1;
-        break;
+    iter(true);
+    if (status() == dev::KST_RUN && maxit > 1 && loop_ok()) {
+      // every further iteration on the device: one launch of a WHILE graph
+      graphed_loop(lambda, 2, maxit, [&] { iter(false); });
+      status();
+    } else {
+      for (int k = 1; k < maxit && h_status[0] == dev::KST_RUN; ++k) {
+        graphed(lambda, 2, [&] { iter(false); });
+        status();
       }
-      if (s_ != dev::KST_RUN) breakdown(s_);
     }
+    rep.iterations = h_status[1];
+    if (h_status[0] == dev::KST_CONV) rep.converged = 1;
+    else if (h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
     rep.rel_residual = rel_residual();
+  }
+
+  /// The device-side loop needs graph capture (no host reducer, no phase
+  /// timing); PF_HOST_LOOP=1 keeps one graph launch + status read per iteration.
+  bool loop_ok() const {
+    static const bool off = std::getenv("PF_HOST_LOOP") != nullptr || std::getenv("PF_NO_GRAPH") != nullptr;
+    return !off && !reducer && !Ksys.timed && !Isys.timed && !Qsys.timed;
+  }
+
+  /// Run iterations `body` on the device until the status word leaves RUN or
+  /// maxit iterations are reached: a graph whose single conditional WHILE node
+  /// holds the captured iteration plus k_loop_cond (cudaGraphSetConditional).
+  /// One launch and one status read per Krylov solve.
+  cudaGraphExec_t lp_exec = nullptr;
+  const void* lp_key_ptr = nullptr;
+  int lp_key_kind = 0, lp_maxit = 0;
+  long long lp_nlaunch = 0;
+  int lp_dF = 0, lp_dM = 0;
+  template <class Fn>
+  void graphed_loop(const void* key, int kind, int maxit, Fn&& body) {
+    if (!lp_exec || lp_key_ptr != key || lp_key_kind != kind || lp_maxit != maxit) {
+      if (lp_exec) cudaGraphExecDestroy(lp_exec), lp_exec = nullptr;
+      cudaGraph_t g;
+      PF_CUDA_CHECK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h;
+      PF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h, cp.conditional.type = cudaGraphCondTypeWhile, cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      PF_CUDA_CHECK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+      cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+      const long long l0 = ::pf::g_launches;
+      const int f0 = fapplies, m0 = papplies;
+      PF_CUDA_CHECK(cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      body();
+      launch_pdl(dev::k_loop_cond, 1, 1, 0, st, h, (const int*)d_status.p, maxit);
+      cudaGraph_t cap;
+      PF_CUDA_CHECK(cudaStreamEndCapture(st, &cap));
+      PF_CUDA_CHECK(cudaGraphInstantiate(&lp_exec, g, 0));
+      PF_CUDA_CHECK(cudaGraphDestroy(g));
+      lp_nlaunch = ::pf::g_launches - l0, ::pf::g_launches = l0;
+      lp_dF = fapplies - f0, lp_dM = papplies - m0, fapplies = f0, papplies = m0;
+      lp_key_ptr = key, lp_key_kind = kind, lp_maxit = maxit;
+    }
+    const int it0 = h_status[1];
+    PF_CUDA_CHECK(cudaGraphLaunch(lp_exec, st));
+    PF_CUDA_CHECK(cudaMemcpyAsync(h_status, d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int ran = h_status[1] - it0;  // body executions (each advances the iteration count once)
+    ::pf::g_launches += lp_nlaunch * ran;
+    fapplies += lp_dF * ran, papplies += lp_dM * ran;
   }
 
   /// Run `body` (a fixed sequence of launches on st) as a CUDA graph: captured

@@ -75,6 +75,20 @@ __device__ __forceinline__ long long col_off(int j, int m) {
   return (long long)j * (m - 1) - (long long)j * (j - 1) / 2;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor
+// drains; pdl_trigger() lets the successor's CTAs be scheduled, pdl_wait()
+// blocks until the predecessor grid has completed and its writes are visible.
+// Both are no-ops for an ordinary launch.
+#ifndef PF_PDL_EARLY
+#define PF_PDL_EARLY 0
+#endif
+// early trigger (successor CTAs scheduled as soon as every CTA started) or the
+// implicit one at CTA exit (only the successor's launch latency is hidden)
+constexpr bool kPdlEarly = PF_PDL_EARLY != 0;
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -162,6 +176,19 @@ __global__ void k_spmv_ind(int nrows, const int* ptr, const long long* vpos, con
   for (int q = ptr[i]; q < ptr[i + 1]; ++q) s += val[vpos[q]] * x[idx[q]];
   const long long o = rows_out[i];
   y[o] = (ysub ? ysub[i] : 0.0) + alpha * s;
+}
+
+/// eq[p] = 0 when the n[p] values at a[p] and b[p] differ anywhere (bitwise)
+__global__ void k_values_equal(int np, const long long* a, const long long* b, const long long* n, const double* L,
+                               int* eq) {
+  const int p = blockIdx.y;
+  if (p >= np || a[p] == b[p]) return;
+  const unsigned long long* x = reinterpret_cast<const unsigned long long*>(L + a[p]);
+  const unsigned long long* y = reinterpret_cast<const unsigned long long*>(L + b[p]);
+  bool same = true;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n[p]; i += (long long)gridDim.x * blockDim.x)
+    same &= x[i] == y[i];
+  if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) eq[p] = 0;
 }
 
 /// permute in: X[xo + pos] = src[so + perm[pos]] (per problem, one block-stride loop)
@@ -263,18 +290,24 @@ enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4,
 
 /// y += sgn * (*coef) * x
 __global__ void k_axpy_s(int n, const double* coef, double sgn, const double* x, double* y) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const double c = sgn * *coef;
   if (i < n) y[i] += c * x[i];
 }
 /// y = x + (*coef) * y
 __global__ void k_xpay_s(int n, const double* x, double* y, const double* coef) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const double c = *coef;
   if (i < n) y[i] = x[i] + c * y[i];
 }
 /// SQMR: d = c^2 theta_old^2 d + c^2 a q; x += d
 __global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d, double* x) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double c2 = sc[KS_C] * sc[KS_C];
@@ -342,6 +375,13 @@ __global__ void k_ks_pcg_init(double* sc, int* status) { ks_pcg_init(sc, status)
 __global__ void k_ks_pcg_alpha(double* sc, int* status) { ks_pcg_alpha(sc, status); }
 __global__ void k_ks_pcg_beta(double* sc, int* status, double tol) { ks_pcg_beta(sc, status, tol); }
 
+/// condition of the device-side Krylov loop (conditional WHILE graph node):
+/// keep iterating while the solver runs and the iteration cap is not reached
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* status, int maxit) {
+  pdl_wait();
+  cudaGraphSetConditional(h, status[0] == KST_RUN && status[1] < maxit ? 1u : 0u);
+}
+
 /// scalar update run by the last block of a fused dot (k_dot_fused)
 enum : int { SOP_NONE = 0, SOP_SQMR_INIT, SOP_SQMR_A, SOP_SQMR_TAU, SOP_SQMR_B, SOP_PCG_INIT, SOP_PCG_ALPHA,
              SOP_PCG_BETA };
@@ -380,6 +420,8 @@ struct FusedDot {
   int* status;
 };
 __global__ void __launch_bounds__(kRedThreads) k_dot_fused(FusedDot F) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   __shared__ double red[32];
   __shared__ bool last;
   double s = 0.0;
@@ -468,6 +510,8 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ a, con
 /// shared memory; grid-stride over rows.  Coarse projector (G_c^T G_c)^{-1}.
 __global__ void __launch_bounds__(256) k_dense_gemv_w(int n, const double* __restrict__ A,
                                                       const double* __restrict__ x, double* __restrict__ y) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   extern __shared__ double xs[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
   __syncthreads();
@@ -484,6 +528,8 @@ __global__ void __launch_bounds__(256) k_spmv_warp(int nrows, const int* __restr
                                                    const int* __restrict__ idx, const double* __restrict__ val,
                                                    const double* __restrict__ x, double* y, double alpha,
                                                    double beta) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= nrows) return;
   double s = 0.0;
@@ -517,6 +563,8 @@ __device__ __forceinline__ double fold_add(double v, int c, const int* __restric
 __global__ void k_dense_top_gather(int n, int c0, int cb_top, const int* __restrict__ fold_ptr,
                                    const int* __restrict__ fold_idx, const double* __restrict__ CB, const double* src,
                                    const int* __restrict__ perm, double* y) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   // a warp per column: lanes take the fold entries, warp_sum tree (fixed order)
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -540,6 +588,8 @@ __global__ void __launch_bounds__(512) k_dense_top_gemv(int n, int c0, const dou
                                                         const int* __restrict__ fold_idx = nullptr,
                                                         const double* __restrict__ CB = nullptr, int cb_top = 0,
                                                         const double* __restrict__ src = nullptr) {
+  if (kPdlEarly) pdl_trigger();
+  pdl_wait();
   extern __shared__ double ys[];
   if (fold_ptr) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -583,20 +633,21 @@ struct __align__(16) UnitWork {
 };
 constexpr int kUnitRows = 128, kUnitMaxIn = 1024;
 
-/// One CTA per (unit, block of <= 128 output rows); thread r of slice q
+/// One CTA per (unit, block of <= RB output rows); thread r of slice q
 /// computes the partial dot product of output row r over the q-th of S
 /// contiguous input ranges (column-major operator: a fixed input column is
 /// one coalesced read across the rows).  The first eight operator values per
 /// thread are loaded before the inputs (b or X, plus folded lower-stage
 /// contributions) are staged in shared memory, then eight loads stay in
 /// flight per thread; slices are summed in slice order (deterministic).
-template <int S>
-__global__ void __launch_bounds__(128 * S) k_dense_unit(const UnitWork* __restrict__ work, DenseUnits U) {
+template <int S, int RB = kUnitRows>
+__global__ void __launch_bounds__(RB * S) k_dense_unit(const UnitWork* __restrict__ work, DenseUnits U) {
   constexpr int B = 8;
   __shared__ double in[kUnitMaxIn];
-  __shared__ double part[S > 1 ? S : 1][kUnitRows];
+  __shared__ double part[S > 1 ? S : 1][RB];
+  if (kPdlEarly) pdl_trigger();
   const UnitWork w = work[blockIdx.x];
-  const int r = threadIdx.x & (kUnitRows - 1), q = threadIdx.x >> 7;
+  const int r = threadIdx.x % RB, q = threadIdx.x / RB;
   const int ni = w.nin, ld = w.nout;
   const int jl = (int)((long long)ni * q / S), jh = (int)((long long)ni * (q + 1) / S);
   const bool live = r < w.nrows;
@@ -604,6 +655,7 @@ __global__ void __launch_bounds__(128 * S) k_dense_unit(const UnitWork* __restri
   double v[B];
 #pragma unroll
   for (int m = 0; m < B; ++m) v[m] = (live && jl + m < jh) ? __ldg(Tc + (long long)(jl + m) * ld) : 0.0;
+  pdl_wait();  // the operator prefetch above does not depend on the predecessor
   const int* il = U.in + w.inoff;
   const int* iln = U.in_nat + w.inoff;
   for (int i = threadIdx.x; i < ni; i += blockDim.x) {
