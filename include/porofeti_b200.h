@@ -78,7 +78,14 @@ typedef struct pf_info {
   int dual;             /* 1: explicit local dual operators (F-apply / Dirichlet as dense GEMVs) */
   double bytes_symv;    /* algorithmic bytes of one k_local_symv launch (n(n+1)/2 values per operator) */
   double bytes_symv_stored; /* bytes it streams (packed 32x32 tiles incl. padding) */
-  double bytes_qsolve;  /* operator bytes of one mortar Gram solve (dense units + dense top) */
+  double bytes_qsolve;  /* operator bytes of one mortar Gram solve (dense units + dense top), as stored
+                           (bitwise-equal unit operators kept once) */
+  double bytes_qsolve_applied; /* operator bytes one solve applies (every unit counted) */
+  double bytes_flocal;  /* bytes of one local dual-operator product (type-shared copies once + per-subdomain
+                           operators + gathered inputs, their indices and the local results) */
+  double flops_flocal;  /* its flops (2 n^2 per subdomain) */
+  double bytes_coarse;  /* bytes of one dense coarse GEMV ((G_c^T G_c)^-1, n_c^2 values) */
+  double bytes_factor_stored; /* factor values stored for the per-step sweeps (after same-type sharing) */
 } pf_info;
 
 typedef struct pf_sub_info {
@@ -155,7 +162,9 @@ int pf_set_state(pf_ctx* ctx, const double* x_cat, const double* lambda, int ste
 int pf_current_step(const pf_ctx* ctx);
 
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
- * kind: 0 F-apply, 1 preconditioner, 2 F-apply solve phase only. */
+ * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
+ * backward over every subdomain), 3 the local dual-operator products alone,
+ * 4 one mortar Gram solve Q, 5 one dense coarse GEMV. */
 int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
 /* nsteps device-resident StepSolver::advance calls bracketed by CUDA events. */
 int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total);

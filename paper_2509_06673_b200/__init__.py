@@ -96,6 +96,8 @@ class Info(C.Structure):
         ("t_setup", C.c_double), ("t_assemble", C.c_double), ("t_factor", C.c_double), ("t_upload", C.c_double),
         ("bytes_fapply", C.c_double), ("bytes_precond", C.c_double), ("n_levels", C.c_int), ("dual", C.c_int),
         ("bytes_symv", C.c_double), ("bytes_symv_stored", C.c_double), ("bytes_qsolve", C.c_double),
+        ("bytes_qsolve_applied", C.c_double), ("bytes_flocal", C.c_double), ("flops_flocal", C.c_double),
+        ("bytes_coarse", C.c_double), ("bytes_factor_stored", C.c_double),
     ]
 
 

@@ -122,6 +122,24 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cu
   ::pf::g_launches++;
 }
 
+namespace dev {
+/// k_dense_unit instantiations: (input slices S, output rows per CTA RB)
+#define PF_DENSE_UNIT_CONFIGS(X) X(1, 32) X(1, 64) X(2, 32) X(2, 64) X(4, 32) X(4, 64) X(4, 128) X(8, 32) X(8, 64)
+inline bool dense_unit_ok(int S, int RB) {
+#define PF_DU_OK(s, r) if (S == s && RB == r) return true;
+  PF_DENSE_UNIT_CONFIGS(PF_DU_OK)
+#undef PF_DU_OK
+  return false;
+}
+inline void launch_dense_unit(int S, int RB, int nwork, cudaStream_t st, const UnitWork* w, const DenseUnits& U) {
+#define PF_DU_LAUNCH(s, r) \
+  if (S == s && RB == r) return launch_pdl(k_dense_unit<s, r>, nwork, s * r, 0, st, w, U);
+  PF_DENSE_UNIT_CONFIGS(PF_DU_LAUNCH)
+#undef PF_DU_LAUNCH
+  fail(kInternal, "k_dense_unit: no such configuration");
+}
+}  // namespace dev
+
 // ---------------------------------------------------------------------------
 // A batch of sparse LDL^T systems sharing symbolic types, solved on device.
 // ---------------------------------------------------------------------------
@@ -156,10 +174,12 @@ struct SolveSystem {
   int db_cb1 = 0;                        // first CB slot of the levels above 0
   int db_nwork[2][2] = {{0, 0}, {0, 0}};  // [forward/backward][stage]
   int db_split[2][2] = {{1, 1}, {1, 1}};  // input slices per CTA
+  int db_rb[2][2] = {{64, 64}, {64, 64}};  // output rows per CTA
   DevBuf<dev::UnitWork> db_work[2][2];
   DevBuf<int> db_in, db_out, db_in_nat, db_out_nat;
   DevBuf<double> db_T;
-  double db_bytes = 0.0;
+  double db_bytes = 0.0;       // stored operator bytes (after sharing)
+  double db_unit_bytes = 0.0;  // operator bytes one solve applies (before sharing)
   int nrhs_alloc = 1;
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
@@ -691,26 +711,53 @@ struct SolveSystem {
     std::vector<int> nin, nout, inoff, outoff, idx_in, idx_out;
     std::vector<long long> toff;
     std::vector<double> T;
+    // units whose operators are bitwise equal (same shape, same values: the
+    // repeated interface stretches of a structured partition) share one copy;
+    // only their index lists differ, so results are unchanged bit for bit
+    std::unordered_map<std::uint64_t, std::vector<std::pair<long long, long long>>> seen;
+    auto place = [&](const std::vector<double>& M, int rows) -> long long {
+      std::uint64_t h = 1469598103934665603ull ^ (std::uint64_t)M.size() ^ ((std::uint64_t)rows << 40);
+      for (double d : M) {
+        std::uint64_t b;
+        std::memcpy(&b, &d, 8);
+        h = (h ^ b) * 1099511628211ull;
+      }
+      auto& cand = seen[h];
+      for (auto& c : cand)
+        if (c.second == (long long)M.size() * 1000003 + rows &&
+            std::memcmp(&T[c.first], M.data(), sizeof(double) * M.size()) == 0)
+          return c.first;
+      const long long o = (long long)T.size();
+      T.insert(T.end(), M.begin(), M.end());
+      cand.push_back({o, (long long)M.size() * 1000003 + rows});
+      return o;
+    };
+    db_unit_bytes = 0.0;
     for (int dir = 0; dir < 2; ++dir)
       for (int u = 0; u < nu; ++u) {
         const UnitOps& O = U[u];
         const int n = (int)O.cols.size();
-        inoff.push_back((int)idx_in.size()), outoff.push_back((int)idx_out.size()), toff.push_back((long long)T.size());
+        inoff.push_back((int)idx_in.size()), outoff.push_back((int)idx_out.size());
         if (dir == 0) {
           idx_in.insert(idx_in.end(), O.cols.begin(), O.cols.end());
           idx_out.insert(idx_out.end(), O.cols.begin(), O.cols.end());
           for (int sl : O.slots) idx_out.push_back(-1 - sl);
           nin.push_back(n), nout.push_back(n + (int)O.slots.size());
-          T.insert(T.end(), O.Tf.begin(), O.Tf.end());
+          toff.push_back(place(O.Tf, nout.back()));
+          db_unit_bytes += 8.0 * (double)O.Tf.size();
         } else {
           idx_in.insert(idx_in.end(), O.cols.begin(), O.cols.end());
           idx_in.insert(idx_in.end(), O.anc.begin(), O.anc.end());
           idx_out.insert(idx_out.end(), O.cols.begin(), O.cols.end());
           nin.push_back(n + (int)O.anc.size()), nout.push_back(n);
-          T.insert(T.end(), O.Tb.begin(), O.Tb.end());
+          toff.push_back(place(O.Tb, nout.back()));
+          db_unit_bytes += 8.0 * (double)O.Tb.size();
         }
         if (nin.back() > dev::kUnitMaxIn) return;  // inputs are staged per warp in shared memory
       }
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr, "[pf] Q dense units: %d units, operators %.1f MB, stored %.1f MB (bitwise shared)\n",
+                   2 * nu, db_unit_bytes / 1e6, 8e-6 * (double)T.size());
     // vector indices of the positions (the permutation fused into the units)
     const std::vector<int>& pm = F.perm;
     std::vector<int> in_nat(idx_in.size()), out_nat(idx_out.size());
@@ -727,7 +774,24 @@ struct SolveSystem {
           if (ustage[u] == stg) maxin = std::max(maxin, nin[dir * nu + u]);
         db_split[dir][stg] = maxin > 128 ? 4 : 1;
         // one slice: 64-row blocks (small level-0 units leave fewer idle threads)
-        const int rb = db_split[dir][stg] == 1 ? 64 : dev::kUnitRows;
+        db_rb[dir][stg] = db_split[dir][stg] == 1 ? 64 : dev::kUnitRows;
+        {  // tuning overrides PF_QU_S<stage>, PF_QU_R<stage>
+          char nm[16];
+          std::snprintf(nm, sizeof nm, "PF_QU_S%d", stg);
+          if (const char* e = std::getenv(nm)) db_split[dir][stg] = std::atoi(e);
+          std::snprintf(nm, sizeof nm, "PF_QU_R%d", stg);
+          if (const char* e = std::getenv(nm)) db_rb[dir][stg] = std::atoi(e);
+          if (!dev::dense_unit_ok(db_split[dir][stg], db_rb[dir][stg])) fail(kInvalid, "PF_QU_*: no such unit kernel");
+        }
+        const int rb = db_rb[dir][stg];
+        if (std::getenv("PF_VERBOSE")) {
+          long long sin = 0, sout = 0, cnt = 0;
+          for (int u = 0; u < nu; ++u)
+            if (ustage[u] == stg) sin += nin[dir * nu + u], sout += nout[dir * nu + u], ++cnt;
+          std::fprintf(stderr, "[pf] Q units dir %d stage %d: %lld units, max in %d, mean in %.1f, mean out %.1f, S %d RB %d\n",
+                       dir, stg, cnt, maxin, cnt ? (double)sin / cnt : 0.0, cnt ? (double)sout / cnt : 0.0,
+                       db_split[dir][stg], rb);
+        }
         for (int u = 0; u < nu; ++u) {
           if (ustage[u] != stg) continue;
           const int g = dir * nu + u;
@@ -767,10 +831,7 @@ struct SolveSystem {
       U.cbmax = dir == 0 && stg == 1 ? db_cb1 : 0;  // groups fold the level-0 contributions
       U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
       U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
-      if (db_split[dir][stg] == 4)
-        launch_pdl(dev::k_dense_unit<4>, db_nwork[dir][stg], 4 * dev::kUnitRows, 0, st, db_work[dir][stg].p, U);
-      else
-        launch_pdl(dev::k_dense_unit<1, 64>, db_nwork[dir][stg], 64, 0, st, db_work[dir][stg].p, U);
+      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_nwork[dir][stg], st, db_work[dir][stg].p, U);
       ++launches;
     };
     units(0, 0);
@@ -1557,6 +1618,7 @@ struct Engine {
   // ------------------------------------------------------------------
   // explicit local dual operators (pf_dual.hpp / pf_dual.cuh)
   DevBuf<int> dl_nloc, dl_lam, dl_rptr;
+  std::vector<int> dl_nloc_h;
   DevBuf<long long> dl_loff, dl_opoff, dl_rslot;
   DevBuf<double> dl_F, dl_S, dl_Y;
   DevBuf<unsigned int> red_count;  // arrival counter of k_dot_fused
@@ -1791,6 +1853,7 @@ struct Engine {
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_local_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, dl_smem));
     // apply maps: local slots -> multipliers, multipliers -> slots (fixed subdomain order)
     dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(ppk);
+    dl_nloc_h = nloc;
     {
       std::vector<int> lg(lamall);
       for (int& l : lg) l = std::max(l, 0);  // padding slots gather x[0] (never used)
@@ -2330,7 +2393,23 @@ struct Engine {
       info.bytes_symv = 8.0 * (double)dl_symvals + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
       info.bytes_symv_stored = 8.0 * (double)dl_opsize + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
     }
-    if (use_q && Qsys.dense_bottom) info.bytes_qsolve = Qsys.db_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
+    if (use_q && Qsys.dense_bottom) {
+      info.bytes_qsolve = Qsys.db_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
+      info.bytes_qsolve_applied = Qsys.db_unit_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
+    }
+    if (dual) {
+      double rb = 0.0, rf = 0.0;
+      std::vector<int> rl(n_rest);
+      if (n_rest) PF_CUDA_CHECK(cudaMemcpy(rl.data(), rest_list.p, sizeof(int) * n_rest, cudaMemcpyDeviceToHost));
+      for (int p : rl) {
+        const double n = dl_nloc_h[p];
+        rb += 8.0 * n * (n + 1) / 2 + 20.0 * n, rf += 2.0 * n * n;
+      }
+      info.bytes_flocal = sh_bytes + rb;
+      info.flops_flocal = sh_flops + rf;
+    }
+    info.bytes_coarse = 8.0 * (double)nc * (double)nc;
+    info.bytes_factor_stored = 8.0 * (double)Ksys.total_L;
   }
 
   // ------------------------------------------------------------------
@@ -3144,6 +3223,9 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
       else if (kind == 1) E.precond(dx.p, dy.p);
       else if (kind == 3) E.symv_only(false, dx.p);
       else if (kind == 4) E.qsolve(dx.p, dy.p);
+      else if (kind == 5) {
+        if (E.nc) E.coarse_gemv(dx.p, dy.p);
+      }
       else E.Ksys.solve(E.st, 1);
     };
     for (int i = 0; i < warmup; ++i) op();
