@@ -161,6 +161,14 @@ int pf_get_lambda(pf_ctx* ctx, double* lambda);
 int pf_set_state(pf_ctx* ctx, const double* x_cat, const double* lambda, int step);
 int pf_current_step(const pf_ctx* ctx);
 
+/* Spatial L2 errors of the current state against the scenario's exact
+ * solution — verify.hpp:62-74 (snapshot_u_error: u over every subdomain;
+ * snapshot_p_error: the Darcy pressure over the poroelastic ones), computed on
+ * the device (degree-4 Dunavant rule, verify.hpp:15, deterministic reduction).
+ * The L-inf(L2) error of verify.hpp:77-83 is the maximum over the steps.
+ * PF_INVALID for scenarios without an exact solution (injection, Barry-Mercer). */
+int pf_errors(pf_ctx* ctx, double* err_u, double* err_p);
+
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
  * backward over every subdomain), 3 the local dual-operator products alone,

@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "o_feti.hpp"
+#include "o_verify.hpp"
 
 using namespace oracle;
 
@@ -375,6 +376,12 @@ int or_state(void* hh, int step, int s, double* x) {
   const Vec& v = h->states[step].x[s];
   std::memcpy(x, v.data(), sizeof(double) * v.size());
   return 0;
+}
+/// verify.hpp:62-74 on time level `step`: displacement / pressure L2 errors
+int or_errors(void* hh, int step, double* eu, double* ep) {
+  auto* h = static_cast<Handle*>(hh);
+  if (step < 0 || step >= (int)h->states.size()) return 4;
+  return guard([&] { snapshot_errors(h->D, h->states[step], *eu, *ep); });
 }
 int or_lambda(void* hh, int step, double* l) {
   auto* h = static_cast<Handle*>(hh);

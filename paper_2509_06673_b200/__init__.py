@@ -185,6 +185,7 @@ def lib():
         L.pf_get_lambda.argtypes = [vp, vp]
         L.pf_set_state.argtypes = [vp, vp, vp, C.c_int]
         L.pf_current_step.argtypes = [vp]
+        L.pf_errors.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
@@ -304,6 +305,14 @@ class FetiOperator:
         _check(lib().pf_get_lambda(self.h, _ptr(lam)), self.h)
         return xs, lam
 
+    def errors(self):
+        """(err_u, err_p): L2 errors of the current state against the exact
+        solution, snapshot_u_error / snapshot_p_error (verify.hpp:62-74),
+        computed on the device."""
+        eu, ep = C.c_double(), C.c_double()
+        _check(lib().pf_errors(self.h, C.byref(eu), C.byref(ep)), self.h)
+        return eu.value, ep.value
+
     def fields(self, xs):
         out = []
         for S, x in zip(self.subs, xs):
@@ -363,17 +372,22 @@ class StepSolver:
     def __init__(self, op: FetiOperator):
         self.op = op
 
-    def advance(self, prev_x=None, prev_lambda=None, prev_step=None):
+    def advance(self, prev_x=None, prev_lambda=None, prev_step=None, out_x=None, out_lambda=None):
         """With no arguments: advance the device-resident state.  With host
         buffers (the reference signature): set the state, step, return the
-        next (x_cat, lambda, report)."""
+        next (x_cat, lambda, report).  out_x / out_lambda: caller-owned
+        (e.g. page-locked) result buffers."""
         if prev_x is None:
             return self.op.step()
         op = self.op
         x = np.ascontiguousarray(prev_x, np.float64)
         lam = np.ascontiguousarray(prev_lambda, np.float64)
-        nx = np.empty(op.info.total_dim)
-        nl = np.empty(op.n_lambda)
+        nx = np.empty(op.info.total_dim) if out_x is None else out_x
+        nl = np.empty(op.n_lambda) if out_lambda is None else out_lambda
+        if nx.dtype != np.float64 or not nx.flags.c_contiguous or nx.size != op.info.total_dim:
+            raise ConfigError("advance: out_x must be a contiguous float64 array of total_dim")
+        if nl.dtype != np.float64 or not nl.flags.c_contiguous or nl.size != op.n_lambda:
+            raise ConfigError("advance: out_lambda must be a contiguous float64 array of n_lambda")
         rep = Report()
         _check(lib().pf_advance(op.h, _ptr(x), _ptr(lam), int(prev_step), _ptr(nx), _ptr(nl), C.byref(rep)), op.h)
         return nx, nl, rep.as_dict()

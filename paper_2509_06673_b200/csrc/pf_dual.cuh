@@ -277,9 +277,10 @@ __global__ void k_op_maxdiff(int np, const int* __restrict__ nloc, const long lo
 __global__ void k_local_gather(long long n, const int* __restrict__ lam, const double* __restrict__ x,
                                double* __restrict__ xloc) {
   if (kPdlEarly) pdl_trigger();
-  pdl_wait();
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) xloc[k] = x[lam[k]];
+  const int l = k < n ? lam[k] : 0;  // before the PDL wait (the map is constant)
+  pdl_wait();
+  if (k < n) xloc[k] = x[l];
 }
 
 /// one CTA: rows [r0, r0+32) x member columns [c0, c0+32) of a shared type
@@ -417,13 +418,17 @@ __global__ void k_local_reduce(int n, const int* __restrict__ ptr, const long lo
                                const double* __restrict__ Y, double* __restrict__ y, double alpha, int nks,
                                long long stride) {
   if (kPdlEarly) pdl_trigger();
-  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // slot lists are constant: loaded before the PDL wait
+  const int q0 = i < n ? ptr[i] : 0, q1 = i < n ? ptr[i + 1] : 0;
+  const long long s0 = q0 < q1 ? slot[q0] : 0, s1 = q0 + 1 < q1 ? slot[q0 + 1] : 0;
+  pdl_wait();
   if (i >= n) return;
   double v = 0.0;
-  for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
-    double u = Y[slot[q]];
-    for (int k = 1; k < nks; ++k) u += Y[slot[q] + k * stride];
+  for (int q = q0; q < q1; ++q) {
+    const long long sq = q == q0 ? s0 : (q == q0 + 1 ? s1 : slot[q]);
+    double u = Y[sq];
+    for (int k = 1; k < nks; ++k) u += Y[sq + k * stride];
     v += u;
   }
   y[i] = alpha * v;

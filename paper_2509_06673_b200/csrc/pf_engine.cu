@@ -123,17 +123,21 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cu
 }
 
 namespace dev {
-/// k_dense_unit instantiations: (input slices S, output rows per CTA RB)
-#define PF_DENSE_UNIT_CONFIGS(X) X(1, 32) X(1, 64) X(2, 32) X(2, 64) X(4, 32) X(4, 64) X(4, 128) X(8, 32) X(8, 64)
-inline bool dense_unit_ok(int S, int RB) {
-#define PF_DU_OK(s, r) if (S == s && RB == r) return true;
+/// k_dense_unit instantiations: (input slices S, output rows per CTA RB,
+/// staged inputs MI); the small-input variants use 1 KB of shared memory
+#define PF_DENSE_UNIT_CONFIGS(X)                                                                             \
+  X(1, 32, 128) X(1, 64, 128) X(2, 32, 128) X(2, 64, 128) X(4, 32, 128) X(4, 64, 128) X(1, 64, 1024)         \
+  X(2, 64, 1024) X(4, 32, 1024) X(4, 64, 1024) X(4, 128, 1024) X(8, 32, 1024) X(8, 64, 1024)
+inline bool dense_unit_ok(int S, int RB, int maxin) {
+#define PF_DU_OK(s, r, mi) if (S == s && RB == r && maxin <= mi) return true;
   PF_DENSE_UNIT_CONFIGS(PF_DU_OK)
 #undef PF_DU_OK
   return false;
 }
-inline void launch_dense_unit(int S, int RB, int nwork, cudaStream_t st, const UnitWork* w, const DenseUnits& U) {
-#define PF_DU_LAUNCH(s, r) \
-  if (S == s && RB == r) return launch_pdl(k_dense_unit<s, r>, nwork, s * r, 0, st, w, U);
+inline void launch_dense_unit(int S, int RB, int maxin, int nwork, cudaStream_t st, const UnitWork* w,
+                              const DenseUnits& U) {
+#define PF_DU_LAUNCH(s, r, mi) \
+  if (S == s && RB == r && maxin <= mi) return launch_pdl(k_dense_unit<s, r, mi>, nwork, s * r, 0, st, w, U);
   PF_DENSE_UNIT_CONFIGS(PF_DU_LAUNCH)
 #undef PF_DU_LAUNCH
   fail(kInternal, "k_dense_unit: no such configuration");
@@ -175,6 +179,7 @@ struct SolveSystem {
   int db_nwork[2][2] = {{0, 0}, {0, 0}};  // [forward/backward][stage]
   int db_split[2][2] = {{1, 1}, {1, 1}};  // input slices per CTA
   int db_rb[2][2] = {{64, 64}, {64, 64}};  // output rows per CTA
+  int db_maxin[2][2] = {{0, 0}, {0, 0}};   // largest unit input count per stage
   DevBuf<dev::UnitWork> db_work[2][2];
   DevBuf<int> db_in, db_out, db_in_nat, db_out_nat;
   DevBuf<double> db_T;
@@ -781,7 +786,8 @@ struct SolveSystem {
           if (const char* e = std::getenv(nm)) db_split[dir][stg] = std::atoi(e);
           std::snprintf(nm, sizeof nm, "PF_QU_R%d", stg);
           if (const char* e = std::getenv(nm)) db_rb[dir][stg] = std::atoi(e);
-          if (!dev::dense_unit_ok(db_split[dir][stg], db_rb[dir][stg])) fail(kInvalid, "PF_QU_*: no such unit kernel");
+          if (!dev::dense_unit_ok(db_split[dir][stg], db_rb[dir][stg], maxin)) fail(kInvalid, "PF_QU_*: no such unit kernel");
+          db_maxin[dir][stg] = maxin;
         }
         const int rb = db_rb[dir][stg];
         if (std::getenv("PF_VERBOSE")) {
@@ -831,7 +837,8 @@ struct SolveSystem {
       U.cbmax = dir == 0 && stg == 1 ? db_cb1 : 0;  // groups fold the level-0 contributions
       U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
       U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
-      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_nwork[dir][stg], st, db_work[dir][stg].p, U);
+      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_maxin[dir][stg], db_nwork[dir][stg], st,
+                             db_work[dir][stg].p, U);
       ++launches;
     };
     units(0, 0);
@@ -2558,6 +2565,33 @@ struct Engine {
     PF_CUDA_CHECK(cudaGetLastError());
   }
 
+  /// verify.hpp:62-74 (snapshot_u_error, snapshot_p_error) on the current
+  /// state at time t: L2 errors of u over all subdomains and of p over the
+  /// poroelastic ones against the manufactured solution (mms-t, mms only)
+  DevBuf<double> err_part, err_out;
+  void errors(double t, double& eu, double& ep) {
+    if (D.cfg.scenario != PF_SCEN_MMS_T && D.cfg.scenario != PF_SCEN_MMS)
+      fail(kInvalid, "errors: the scenario has no exact solution (manufactured scenarios only)");
+    dev::FemSet S = femset();
+    std::vector<int> nb(8);
+    int tot = 0;
+    for (int c = 0; c < 8; ++c) nb[c] = cdiv(colour_threads(c), 256), tot += nb[c];
+    if ((long long)err_part.n < 2LL * std::max(tot, 1)) err_part.alloc(2LL * std::max(tot, 1));
+    if (!err_out.p) err_out.alloc(2);
+    int off = 0;
+    for (int c = 0; c < 8; ++c) {
+      if (nb[c]) dev::k_error_elem<<<nb[c], 256, 0, st>>>(S, c, t, state.p, err_part.p + 2 * off), ::pf::g_launches++;
+      off += nb[c];
+    }
+    dev::k_error_final<<<1, 256, 0, st>>>(tot, err_part.p, err_out.p);
+    ::pf::g_launches++;
+    reduce(err_out.p, 2);
+    double h[2];
+    PF_CUDA_CHECK(cudaMemcpyAsync(h, err_out.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    eu = std::sqrt(h[0]), ep = std::sqrt(h[1]);
+  }
+
   /// F = sum_s G_s K_s^+ b_s - d  (into out)
   void interface_rhs(double* out) {
     perm_in_K(bvec.p);
@@ -3194,6 +3228,14 @@ int pf_set_state(pf_ctx* ctx, const double* x, const double* l, int step) {
 }
 
 int pf_current_step(const pf_ctx* ctx) { return ctx ? ctx->eng.step_index : -1; }
+
+int pf_errors(pf_ctx* ctx, double* err_u, double* err_p) {
+  if (!ctx || !err_u || !err_p) return PF_INVALID;
+  return guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    E.errors(E.D.time(E.step_index), *err_u, *err_p);
+  });
+}
 
 int pf_advance(pf_ctx* ctx, const double* prev_x, const double* prev_lambda, int prev_step, double* next_x,
                double* next_lambda, pf_report* rep) {

@@ -86,6 +86,7 @@ def lib():
         L.or_n_states.argtypes = [P]
         L.or_state.argtypes = [P, C.c_int, C.c_int, dp]
         L.or_lambda.argtypes = [P, C.c_int, dp]
+        L.or_errors.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.or_report.argtypes = [P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p,
                                 C.POINTER(C.c_int)]
@@ -214,6 +215,12 @@ class Oracle:
         lam = np.zeros(self.n_lambda)
         check(lib().or_lambda(self.h, step, lam))
         return xs, lam
+
+    def errors(self, step):
+        """verify.hpp:62-74 on time level `step`: (err_u, err_p)."""
+        eu, ep = C.c_double(), C.c_double()
+        check(lib().or_errors(self.h, step, C.byref(eu), C.byref(ep)))
+        return eu.value, ep.value
 
     def report(self, step):
         it, conv, nh = C.c_int(), C.c_int(), C.c_int()

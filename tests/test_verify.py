@@ -1,0 +1,126 @@
+"""Error norms against the manufactured solution:
+verify.hpp:19-83 restated in the oracle (oracle/src/o_verify.hpp) and on the
+device (k_error_elem, pf_errors).
+
+CPU tests pin the oracle restatement: zero error of the zero initial state of
+the time-linear MMS at t = 0 (u = t S, p = t S), the order estimator
+(verify.hpp:85-87 restated below) on synthetic data, and the convergence
+orders under refinement (halving h roughly quarters the errors,
+order ~ 2 for P1; the P1 mortar multipliers cap P2 displacements at ~ 2 as
+well on these meshes).  GPU tests compare the device norms with the oracle's
+on the same states, and check the full-size norms against the oracle's
+coarse-mesh norms and the measured order.
+"""
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from oracle_lib import Oracle  # noqa: E402
+
+
+def estimate_order(e_coarse, e_fine, h_coarse, h_fine):
+    """verify.hpp:85-87."""
+    return math.log(e_coarse / e_fine) / math.log(h_coarse / h_fine)
+
+
+def mms_t(mesh_n, order, steps=2, **kw):
+    return dict(dict(mesh_n=mesh_n, SX=1, SY=2, order=order, nu=0.3, c0=1e-3, dt=1e-2, steps=steps,
+                     scenario="mms-t", precond="dirichlet"), **kw)
+
+
+def test_order_estimator_recovers_power_law():
+    for q in (1.0, 2.0, 3.7):
+        e = [2.5 * h ** q for h in (1 / 8, 1 / 16)]
+        assert abs(estimate_order(e[0], e[1], 1 / 8, 1 / 16) - q) < 1e-10
+
+
+def test_oracle_zero_state_has_zero_error_at_t0():
+    o = Oracle(**mms_t(8, 2, steps=1))
+    o.run(1)
+    assert o.errors(0) == (0.0, 0.0)
+    eu, ep = o.errors(1)
+    assert 0 < eu < 1e-3 and 0 < ep < 1e-3
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_oracle_error_orders(order):
+    e = {}
+    for n in (8, 16):
+        o = Oracle(**mms_t(n, order))
+        o.run(2)
+        e[n] = o.errors(2)
+    for k in (0, 1):
+        q = estimate_order(e[8][k], e[16][k], 1 / 8, 1 / 16)
+        assert 1.8 <= q <= 3.5, (order, k, q, e)
+
+
+def test_oracle_errors_reject_scenarios_without_exact_solution():
+    o = Oracle(mesh_n=8, SX=2, SY=2, order=1, scenario="injection", precond="dirichlet-mortar", steps=1, dt=1e-3)
+    o.run(1)
+    with pytest.raises(Exception):
+        o.errors(1)
+
+
+# --------------------------------------------------------------------------- GPU
+GPU_CASES = {
+    "c1": dict(mesh_n=32, SX=1, SY=2, order=1, nu=0.3, c0=1e-3, dt=1e-2, steps=3, scenario="mms-t",
+               precond="dirichlet"),
+    "p2_4x4": dict(mesh_n=64, SX=4, SY=4, order=2, nu=0.3, c0=1e-3, dt=1e-2, steps=2, scenario="mms-t",
+                   precond="dirichlet-mortar"),
+    "mms_ref": dict(mesh_n=16, SX=1, SY=2, order=2, E=1e4, nu=0.2, c0=0.1, dt=1e-3, steps=3, scenario="mms",
+                    precond="dirichlet"),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(GPU_CASES))
+def test_device_errors_match_oracle(name):
+    import paper_2509_06673_b200 as pf
+
+    kw = GPU_CASES[name]
+    op = pf.FetiOperator(**kw)
+    o = Oracle(**kw)
+    o.run(kw["steps"])
+    for k in range(1, kw["steps"] + 1):
+        op.step()
+        du, dp = op.errors()
+        ou, opp = o.errors(k)
+        # the fields agree to ~1e-12; their difference from the exact
+        # solution is ~1e-4 of their size, so 1e-6 relative leaves margin
+        assert abs(du - ou) <= 1e-6 * ou and abs(dp - opp) <= 1e-6 * opp, (name, k, du, ou, dp, opp)
+
+
+@pytest.mark.gpu
+def test_device_errors_full_size_c2():
+    """BASELINE c2 (mesh 128, P2, 2x2 subdomains) after one step: the device
+    errors sit on the oracle's convergence line from meshes 16 and 32."""
+    import paper_2509_06673_b200 as pf
+
+    kw = dict(pf.BASELINE_CONFIGS["c2"], steps=1)
+    op = pf.FetiOperator(**kw)
+    op.step()
+    du, dp = op.errors()
+    e = {}
+    for n in (16, 32):
+        o = Oracle(**dict(kw, mesh_n=n))
+        o.run(1)
+        e[n] = o.errors(1)
+    for k, d in ((0, du), (1, dp)):
+        q = estimate_order(e[16][k], e[32][k], 1 / 16, 1 / 32)
+        pred = e[32][k] * (32 / 128) ** q
+        assert 0.5 * pred <= d <= 2.0 * pred, (k, d, pred, q)
+
+
+@pytest.mark.gpu
+def test_device_errors_reject_injection():
+    import paper_2509_06673_b200 as pf
+
+    op = pf.FetiOperator(mesh_n=16, SX=2, SY=2, order=1, scenario="injection", precond="dirichlet-mortar",
+                         steps=1, dt=1e-3)
+    op.step()
+    with pytest.raises(pf.ConfigError):
+        op.errors()
