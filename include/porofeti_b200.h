@@ -169,6 +169,11 @@ int pf_current_step(const pf_ctx* ctx);
  * PF_INVALID for scenarios without an exact solution (injection, Barry-Mercer). */
 int pf_errors(pf_ctx* ctx, double* err_u, double* err_p);
 
+/* min / max of the nodal Darcy pressure of the current state over the
+ * poroelastic subdomains (the per-snapshot inputs of oscillation_check,
+ * verify.hpp:169-195; 0, 0 without a poroelastic subdomain). */
+int pf_pressure_range(pf_ctx* ctx, double* pmin, double* pmax);
+
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
  * backward over every subdomain), 3 the local dual-operator products alone,

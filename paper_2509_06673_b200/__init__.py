@@ -30,7 +30,8 @@ import numpy as np
 __all__ = [
     "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
-    "CudaUnavailableError", "lib", "build", "LIB_PATH",
+    "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
+    "convergence_study", "write_error_csv",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -186,6 +187,7 @@ def lib():
         L.pf_set_state.argtypes = [vp, vp, vp, C.c_int]
         L.pf_current_step.argtypes = [vp]
         L.pf_errors.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.pf_pressure_range.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
@@ -313,6 +315,12 @@ class FetiOperator:
         _check(lib().pf_errors(self.h, C.byref(eu), C.byref(ep)), self.h)
         return eu.value, ep.value
 
+    def pressure_range(self):
+        """(min, max) nodal Darcy pressure of the current state (device)."""
+        lo, hi = C.c_double(), C.c_double()
+        _check(lib().pf_pressure_range(self.h, C.byref(lo), C.byref(hi)), self.h)
+        return lo.value, hi.value
+
     def fields(self, xs):
         out = []
         for S, x in zip(self.subs, xs):
@@ -397,6 +405,89 @@ def run_simulation(op: FetiOperator, steps=None):
     """run_simulation (timeloop.hpp:206-221): all steps, returns the reports."""
     n = op.info.N if steps is None else steps
     return [op.step() for _ in range(n)]
+
+
+def oscillation_check(ranges, max_boundary, delta):
+    """oscillation_check (verify.hpp:167-195) on per-snapshot nodal pressure
+    ranges [(min, max), ...] (FetiOperator.pressure_range after each step):
+    the pressure must stay within [-delta, max_boundary + delta]; the worst
+    offender is reported."""
+    rep = {"pass": True, "lower_bound": -delta, "upper_bound": max_boundary + delta, "worst_violation": 0.0}
+    lo = min((r[0] for r in ranges), default=float("inf"))
+    hi = max((r[1] for r in ranges), default=float("-inf"))
+    if not np.isfinite(lo):
+        lo = hi = 0.0
+    rep["min_p"], rep["max_p"] = lo, hi
+    worst = 0.0
+    if lo < rep["lower_bound"] and rep["lower_bound"] - lo > worst:
+        worst = rep["lower_bound"] - lo
+        rep["worst_violation"], rep["pass"] = lo, False
+    if hi > rep["upper_bound"] and hi - rep["upper_bound"] > worst:
+        rep["worst_violation"], rep["pass"] = hi, False
+    return rep
+
+
+def estimate_order(err_coarse, err_fine, h_coarse, h_fine):
+    """verify.hpp:85-87."""
+    return float(np.log(err_coarse / err_fine) / np.log(h_coarse / h_fine))
+
+
+def mms_errors(nu, mesh_n, fe_order=2, E=1e4, T=1e-2, dt=1e-3, mu_conv="paper", **kw):
+    """mms_errors (verify.hpp:108-123) on the device: one manufactured-solution
+    run of the reference layout (reference `mms` scenario unless `scenario` is
+    given), L-inf over the snapshots (steps 1..N, timeloop.hpp:206-221) of the
+    spatial L2 errors of u and p."""
+    steps = max(1, int(round(T / dt)))
+    cfg = dict(dict(mesh_n=mesh_n, SX=1, SY=2, order=fe_order, E=E, nu=nu, dt=dt, steps=steps, scenario="mms",
+                    precond="dirichlet", mu_conv=mu_conv, c0=0.1), **kw)
+    op = FetiOperator(**cfg)
+    try:
+        eu = ep = 0.0
+        for _ in range(steps):
+            op.step()
+            u, p = op.errors()
+            eu, ep = max(eu, u), max(ep, p)
+        return eu, ep
+    finally:
+        op.close()
+
+
+def convergence_study(mesh_sizes=(8, 16, 24, 32), nus=(0.2, 0.49, 0.499, 0.4999), fe_order=2, E=1e4, T=1e-2,
+                      dt=1e-3, mu_conv="paper", verbose=False, **kw):
+    """convergence_study (verify.hpp:125-158): rows (nu, h, err_u, order_u,
+    err_p, order_p) per (nu, mesh); a failed run drops its row and the study
+    continues (the order chain restarts)."""
+    rows = []
+    for nu in nus:
+        prev = None
+        for n in mesh_sizes:
+            h = 1.0 / n
+            try:
+                eu, ep = mms_errors(nu, n, fe_order, E, T, dt, mu_conv, **kw)
+            except Error as e:
+                import sys
+                print(f"convergence_study: run nu={nu:g} n={n} failed: {e}", file=sys.stderr)
+                prev = None
+                continue
+            row = {"nu": nu, "h": h, "err_u": eu, "order_u": float("nan"), "err_p": ep, "order_p": float("nan")}
+            if prev is not None:
+                row["order_u"] = estimate_order(prev["err_u"], eu, prev["h"], h)
+                row["order_p"] = estimate_order(prev["err_p"], ep, prev["h"], h)
+            if verbose:
+                print(f"nu={nu:<7g} h=1/{n:<3d}  err_u={eu:.6e} ord_u={row['order_u']:6.3f}  "
+                      f"err_p={ep:.6e} ord_p={row['order_p']:6.3f}")
+            rows.append(row)
+            prev = row
+    return rows
+
+
+def write_error_csv(rows, path):
+    """CSV with the fixed header nu,h,err_u,order_u,err_p,order_p."""
+    with open(path, "w") as f:
+        f.write("nu,h,err_u,order_u,err_p,order_p\n")
+        for r in rows:
+            f.write(f"{r['nu']:.17g},{r['h']:.17g},{r['err_u']:.17g},{r['order_u']:.17g},"
+                    f"{r['err_p']:.17g},{r['order_p']:.17g}\n")
 
 
 def debug_factor_solve(A, ic, b, mode=1, task_cap=4096):

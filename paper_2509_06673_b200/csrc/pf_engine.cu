@@ -2592,6 +2592,38 @@ struct Engine {
     eu = std::sqrt(h[0]), ep = std::sqrt(h[1]);
   }
 
+  /// min / max nodal Darcy pressure over the poroelastic subdomains (every
+  /// rank's owned ones; ranks exchange their pair through a sum-reduced slot
+  /// vector so the result is exact)
+  void pressure_range(double& pmin, double& pmax) {
+    dev::FemSet S = femset();
+    const int ns = nown();
+    if (!ns) fail(kInvalid, "pressure_range: no subdomains");
+    DevBuf<double> part;
+    part.alloc(2LL * ns);
+    dev::k_pressure_range<<<ns, 256, 0, st>>>(S, state.p, part.p);
+    ::pf::g_launches++;
+    std::vector<double> h(2 * (std::size_t)ns);
+    PF_CUDA_CHECK(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    double lo = INFINITY, hi = -INFINITY;
+    for (int s = 0; s < ns; ++s) lo = std::min(lo, h[2 * s]), hi = std::max(hi, h[2 * s + 1]);
+    if (nranks > 1) {
+      // (min, max, has-poroelastic) per rank; zero elsewhere, so the sum is exact
+      std::vector<double> slots(3 * (std::size_t)nranks, 0.0);
+      if (std::isfinite(lo)) slots[3 * rank] = lo, slots[3 * rank + 1] = hi, slots[3 * rank + 2] = 1.0;
+      DevBuf<double> d;
+      d.upload(slots);
+      reduce(d.p, 3 * nranks);
+      PF_CUDA_CHECK(cudaMemcpyAsync(slots.data(), d.p, sizeof(double) * slots.size(), cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int r = 0; r < nranks; ++r)
+        if (slots[3 * r + 2] != 0.0) lo = std::min(lo, slots[3 * r]), hi = std::max(hi, slots[3 * r + 1]);
+    }
+    if (!std::isfinite(lo)) lo = hi = 0.0;  // no poroelastic subdomain (verify.hpp:183-185)
+    pmin = lo, pmax = hi;
+  }
+
   /// F = sum_s G_s K_s^+ b_s - d  (into out)
   void interface_rhs(double* out) {
     perm_in_K(bvec.p);
@@ -3235,6 +3267,11 @@ int pf_errors(pf_ctx* ctx, double* err_u, double* err_p) {
     auto& E = ctx->eng;
     E.errors(E.D.time(E.step_index), *err_u, *err_p);
   });
+}
+
+int pf_pressure_range(pf_ctx* ctx, double* pmin, double* pmax) {
+  if (!ctx || !pmin || !pmax) return PF_INVALID;
+  return guarded(ctx, [&] { ctx->eng.pressure_range(*pmin, *pmax); });
 }
 
 int pf_advance(pf_ctx* ctx, const double* prev_x, const double* prev_lambda, int prev_step, double* next_x,

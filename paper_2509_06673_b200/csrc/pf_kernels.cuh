@@ -853,5 +853,30 @@ __global__ void __launch_bounds__(256) k_error_final(int nparts, const double* _
   if (threadIdx.x == 0) out[0] = su, out[1] = sp;
 }
 
+/// verify.hpp:169-195 inputs: min / max of the nodal Darcy pressure of every
+/// poroelastic subdomain (CTA per subdomain; min/max are order-independent)
+__global__ void __launch_bounds__(256) k_pressure_range(FemSet S, const double* __restrict__ state,
+                                                        double* __restrict__ part) {
+  __shared__ double rmin[8], rmax[8];
+  const int sub = blockIdx.x;
+  const FemSub& F = S.subs[sub];
+  const FemType& T = S.types[F.type];
+  double lo = INFINITY, hi = -INFINITY;
+  if (T.region == 0)
+    for (int v = threadIdx.x; v < T.n_s; v += blockDim.x) {
+      const double p = state[F.vec + T.off_p + v];
+      lo = fmin(lo, p), hi = fmax(hi, p);
+    }
+  for (int o = 16; o > 0; o >>= 1)
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o)), hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  if ((threadIdx.x & 31) == 0) rmin[threadIdx.x >> 5] = lo, rmax[threadIdx.x >> 5] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) lo = fmin(lo, rmin[w]), hi = fmax(hi, rmax[w]);
+    lo = fmin(lo, rmin[0]), hi = fmax(hi, rmax[0]);
+    part[2 * sub] = lo, part[2 * sub + 1] = hi;
+  }
+}
+
 }  // namespace dev
 }  // namespace pf

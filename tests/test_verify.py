@@ -124,3 +124,79 @@ def test_device_errors_reject_injection():
     op.step()
     with pytest.raises(pf.ConfigError):
         op.errors()
+
+
+# ------------------------------------------------- oscillation check (verify.hpp:160-195)
+def oracle_pressure_range(o, step):
+    xs, _ = o.state(step)
+    ps = [x[S["off_p"]:S["off_p"] + S["n_s"]] for S, x in zip(o.subs, xs) if S["region"] == 0]
+    if not ps:
+        return 0.0, 0.0
+    return float(min(p.min() for p in ps)), float(max(p.max() for p in ps))
+
+
+def test_oscillation_check_definition():
+    """all-zero history passes; a node at -0.2 with bound
+    0.05 fails reporting -0.2; the larger of two violations is reported."""
+    import paper_2509_06673_b200 as pf
+
+    assert pf.oscillation_check([(0.0, 0.0)] * 3, 0.0, 0.05)["pass"]
+    r = pf.oscillation_check([(0.0, 0.5), (-0.2, 0.4)], 1.0, 0.05)
+    assert not r["pass"] and r["worst_violation"] == -0.2
+    r = pf.oscillation_check([(-0.06, 1.5)], 1.0, 0.05)
+    assert not r["pass"] and r["worst_violation"] == 1.5
+    r = pf.oscillation_check([], 1.0, 0.05)
+    assert r["pass"] and r["min_p"] == 0.0 and r["max_p"] == 0.0
+
+
+def test_error_csv_header(tmp_path):
+    import paper_2509_06673_b200 as pf
+
+    rows = [{"nu": 0.2, "h": 0.125, "err_u": 1e-3, "order_u": float("nan"), "err_p": 2e-3, "order_p": float("nan")}]
+    p = tmp_path / "t.csv"
+    pf.write_error_csv(rows, str(p))
+    lines = p.read_text().splitlines()
+    assert lines[0] == "nu,h,err_u,order_u,err_p,order_p" and len(lines) == 2
+
+
+@pytest.mark.gpu
+def test_barry_mercer_pressure_range_and_oscillation_check():
+    """Barry-Mercer (model.hpp:274-324), h = 1/16, tau = 1e-2: the device's
+    nodal pressure range equals the oracle's at every step, and the
+    oscillation check with bound 0.05 max|p2| passes."""
+    import paper_2509_06673_b200 as pf
+
+    kw = dict(mesh_n=16, SX=1, SY=2, order=2, scenario="barry-mercer", E=1e4, nu=0.2, c0=0.1, dt=1e-2,
+              steps=10, precond="dirichlet")
+    op = pf.FetiOperator(**kw)
+    o = Oracle(**kw)
+    o.run(kw["steps"])
+    ranges = []
+    for k in range(1, kw["steps"] + 1):
+        op.step()
+        r = op.pressure_range()
+        ro = oracle_pressure_range(o, k)
+        assert abs(r[0] - ro[0]) <= 1e-9 * max(1.0, abs(ro[0])) and abs(r[1] - ro[1]) <= 1e-9 * max(1.0, abs(ro[1]))
+        ranges.append(r)
+    max_bnd = max(abs(math.sin(k * kw["dt"])) for k in range(1, kw["steps"] + 1))
+    rep = pf.oscillation_check(ranges, max_bnd, 0.05 * max_bnd)
+    assert rep["pass"], rep
+
+
+@pytest.mark.gpu
+def test_convergence_study_driver():
+    """convergence_study (verify.hpp:125-158) on the device for the time-linear
+    MMS: orders between consecutive meshes >= 1.8 for u and p, matching the
+    oracle's errors on the same runs."""
+    import paper_2509_06673_b200 as pf
+
+    rows = pf.convergence_study(mesh_sizes=(8, 16), nus=(0.3,), fe_order=2, E=1.0, T=2e-2, dt=1e-2,
+                                scenario="mms-t", c0=1e-3)
+    assert len(rows) == 2 and math.isnan(rows[0]["order_u"])
+    assert rows[1]["order_u"] >= 1.8 and rows[1]["order_p"] >= 1.8, rows
+    for r, n in zip(rows, (8, 16)):
+        o = Oracle(**mms_t(n, 2))
+        o.run(2)
+        eu = max(o.errors(k)[0] for k in (1, 2))
+        ep = max(o.errors(k)[1] for k in (1, 2))
+        assert abs(r["err_u"] - eu) <= 1e-6 * eu and abs(r["err_p"] - ep) <= 1e-6 * ep
