@@ -174,6 +174,11 @@ int pf_errors(pf_ctx* ctx, double* err_u, double* err_p);
  * verify.hpp:169-195; 0, 0 without a poroelastic subdomain). */
 int pf_pressure_range(pf_ctx* ctx, double* pmin, double* pmax);
 
+/* Page-locked host buffers for the host-buffer entry points (pf_advance,
+ * pf_set_state, pf_get_state_all): copies from them run at full PCIe/C2C rate. */
+int pf_host_alloc(size_t bytes, void** out);
+void pf_host_free(void* p);
+
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
  * backward over every subdomain), 3 the local dual-operator products alone,

@@ -18,6 +18,10 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <limits>
+#include <cmath>
+#include <algorithm>
+#include <utility>
 
 #include "porofeti_b200.h"
 
@@ -113,6 +117,18 @@ class Problem {
     check(pf_local_solve(ctx_, s, b.data()), ctx_);
     return b;
   }
+  /// snapshot_u_error / snapshot_p_error (verify.hpp:62-74) of the current state
+  std::pair<double, double> errors() const {
+    double eu = 0.0, ep = 0.0;
+    check(pf_errors(ctx_, &eu, &ep), ctx_);
+    return {eu, ep};
+  }
+  /// min / max nodal Darcy pressure of the current state (oscillation_check input)
+  std::pair<double, double> pressure_range() const {
+    double lo = 0.0, hi = 0.0;
+    check(pf_pressure_range(ctx_, &lo, &hi), ctx_);
+    return {lo, hi};
+  }
 
  private:
   void refresh() { check(pf_get_info(ctx_, &info_), ctx_); }
@@ -149,6 +165,27 @@ inline std::vector<PcgReport> run_simulation(Problem& p) {
     out.push_back(PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds});
   }
   return out;
+}
+
+/// Reference OscillationReport / oscillation_check (verify.hpp:160-195) on the
+/// per-snapshot pressure ranges (Problem::pressure_range after each step).
+struct OscillationReport {
+  bool pass = true;
+  double min_p = 0.0, max_p = 0.0, lower_bound = 0.0, upper_bound = 0.0, worst_violation = 0.0;
+};
+inline OscillationReport oscillation_check(const std::vector<std::pair<double, double>>& ranges,
+                                           double max_boundary, double delta) {
+  OscillationReport rep;
+  rep.lower_bound = -delta, rep.upper_bound = max_boundary + delta;
+  rep.min_p = std::numeric_limits<double>::infinity(), rep.max_p = -std::numeric_limits<double>::infinity();
+  for (const auto& r : ranges) rep.min_p = std::min(rep.min_p, r.first), rep.max_p = std::max(rep.max_p, r.second);
+  if (!std::isfinite(rep.min_p)) rep.min_p = rep.max_p = 0.0;
+  double worst = 0.0;
+  if (rep.min_p < rep.lower_bound && rep.lower_bound - rep.min_p > worst)
+    worst = rep.lower_bound - rep.min_p, rep.worst_violation = rep.min_p, rep.pass = false;
+  if (rep.max_p > rep.upper_bound && rep.max_p - rep.upper_bound > worst)
+    rep.worst_violation = rep.max_p, rep.pass = false;
+  return rep;
 }
 
 }  // namespace porofeti_b200

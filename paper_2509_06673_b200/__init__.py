@@ -31,7 +31,7 @@ __all__ = [
     "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
     "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
-    "convergence_study", "write_error_csv",
+    "convergence_study", "write_error_csv", "pinned_empty",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -188,6 +188,8 @@ def lib():
         L.pf_current_step.argtypes = [vp]
         L.pf_errors.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pf_pressure_range.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.pf_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+        L.pf_host_free.argtypes = [vp]
         L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
@@ -405,6 +407,36 @@ def run_simulation(op: FetiOperator, steps=None):
     """run_simulation (timeloop.hpp:206-221): all steps, returns the reports."""
     n = op.info.N if steps is None else steps
     return [op.step() for _ in range(n)]
+
+
+class PinnedArray(np.ndarray):
+    """float64 array in page-locked host memory (pf_host_alloc), freed with
+    the last view."""
+
+    def __array_finalize__(self, obj):
+        if obj is not None and not hasattr(self, "_pin"):
+            self._pin = getattr(obj, "_pin", None)
+
+
+class _Pin:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            lib().pf_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(n):
+    """np.empty(n) in page-locked memory (for StepSolver.advance host buffers)."""
+    p = C.c_void_p()
+    _check(lib().pf_host_alloc(8 * max(int(n), 1), C.byref(p)))
+    buf = (C.c_double * max(int(n), 1)).from_address(p.value)
+    a = np.frombuffer(buf, dtype=np.float64, count=int(n)).view(PinnedArray)
+    a._pin = _Pin(p.value)
+    return a
 
 
 def oscillation_check(ranges, max_boundary, delta):

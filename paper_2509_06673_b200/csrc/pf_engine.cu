@@ -123,21 +123,17 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cu
 }
 
 namespace dev {
-/// k_dense_unit instantiations: (input slices S, output rows per CTA RB,
-/// staged inputs MI); the small-input variants use 1 KB of shared memory
-#define PF_DENSE_UNIT_CONFIGS(X)                                                                             \
-  X(1, 32, 128) X(1, 64, 128) X(2, 32, 128) X(2, 64, 128) X(4, 32, 128) X(4, 64, 128) X(1, 64, 1024)         \
-  X(2, 64, 1024) X(4, 32, 1024) X(4, 64, 1024) X(4, 128, 1024) X(8, 32, 1024) X(8, 64, 1024)
-inline bool dense_unit_ok(int S, int RB, int maxin) {
-#define PF_DU_OK(s, r, mi) if (S == s && RB == r && maxin <= mi) return true;
+/// k_dense_unit instantiations: (input slices S, output rows per CTA RB)
+#define PF_DENSE_UNIT_CONFIGS(X) X(1, 32) X(1, 64) X(2, 32) X(2, 64) X(4, 32) X(4, 64) X(4, 128) X(8, 32) X(8, 64)
+inline bool dense_unit_ok(int S, int RB) {
+#define PF_DU_OK(s, r) if (S == s && RB == r) return true;
   PF_DENSE_UNIT_CONFIGS(PF_DU_OK)
 #undef PF_DU_OK
   return false;
 }
-inline void launch_dense_unit(int S, int RB, int maxin, int nwork, cudaStream_t st, const UnitWork* w,
-                              const DenseUnits& U) {
-#define PF_DU_LAUNCH(s, r, mi) \
-  if (S == s && RB == r && maxin <= mi) return launch_pdl(k_dense_unit<s, r, mi>, nwork, s * r, 0, st, w, U);
+inline void launch_dense_unit(int S, int RB, int nwork, cudaStream_t st, const UnitWork* w, const DenseUnits& U) {
+#define PF_DU_LAUNCH(s, r) \
+  if (S == s && RB == r) return launch_pdl(k_dense_unit<s, r>, nwork, s * r, 0, st, w, U);
   PF_DENSE_UNIT_CONFIGS(PF_DU_LAUNCH)
 #undef PF_DU_LAUNCH
   fail(kInternal, "k_dense_unit: no such configuration");
@@ -179,7 +175,6 @@ struct SolveSystem {
   int db_nwork[2][2] = {{0, 0}, {0, 0}};  // [forward/backward][stage]
   int db_split[2][2] = {{1, 1}, {1, 1}};  // input slices per CTA
   int db_rb[2][2] = {{64, 64}, {64, 64}};  // output rows per CTA
-  int db_maxin[2][2] = {{0, 0}, {0, 0}};   // largest unit input count per stage
   DevBuf<dev::UnitWork> db_work[2][2];
   DevBuf<int> db_in, db_out, db_in_nat, db_out_nat;
   DevBuf<double> db_T;
@@ -786,8 +781,7 @@ struct SolveSystem {
           if (const char* e = std::getenv(nm)) db_split[dir][stg] = std::atoi(e);
           std::snprintf(nm, sizeof nm, "PF_QU_R%d", stg);
           if (const char* e = std::getenv(nm)) db_rb[dir][stg] = std::atoi(e);
-          if (!dev::dense_unit_ok(db_split[dir][stg], db_rb[dir][stg], maxin)) fail(kInvalid, "PF_QU_*: no such unit kernel");
-          db_maxin[dir][stg] = maxin;
+          if (!dev::dense_unit_ok(db_split[dir][stg], db_rb[dir][stg])) fail(kInvalid, "PF_QU_*: no such unit kernel");
         }
         const int rb = db_rb[dir][stg];
         if (std::getenv("PF_VERBOSE")) {
@@ -837,8 +831,7 @@ struct SolveSystem {
       U.cbmax = dir == 0 && stg == 1 ? db_cb1 : 0;  // groups fold the level-0 contributions
       U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
       U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
-      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_maxin[dir][stg], db_nwork[dir][stg], st,
-                             db_work[dir][stg].p, U);
+      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_nwork[dir][stg], st, db_work[dir][stg].p, U);
       ++launches;
     };
     units(0, 0);
@@ -3267,6 +3260,15 @@ int pf_errors(pf_ctx* ctx, double* err_u, double* err_p) {
     auto& E = ctx->eng;
     E.errors(E.D.time(E.step_index), *err_u, *err_p);
   });
+}
+
+int pf_host_alloc(size_t bytes, void** out) {
+  if (!out) return PF_INVALID;
+  *out = nullptr;
+  return cudaMallocHost(out, bytes ? bytes : 1) == cudaSuccess ? PF_OK : PF_CUDA;
+}
+void pf_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int pf_pressure_range(pf_ctx* ctx, double* pmin, double* pmax) {

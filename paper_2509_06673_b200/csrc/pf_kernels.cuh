@@ -505,67 +505,18 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ a, con
   return warp_sum((s[0] + s[2]) + (s[1] + s[3]));
 }
 
-/// The first 16-byte chunk group of a row (what warp_row_dot loads first),
-/// issued before a PDL wait: operator rows never depend on the predecessor.
-struct RowHead {
-  double2 v[8];
-  bool ok;
-};
-__device__ __forceinline__ RowHead row_head(const double* __restrict__ a, int n, int lane) {
-  RowHead h;
-  h.ok = (n & 1) == 0 && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n >> 1) >= 32 * 8;
-  if (h.ok) {
-    const double2* a2 = reinterpret_cast<const double2*>(a);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) h.v[m] = __ldg(a2 + lane + 32 * m);
-  }
-  return h;
-}
-/// warp_row_dot with the head chunk already in registers (same order of sums)
-__device__ __forceinline__ double warp_row_dot_h(const double* __restrict__ a, const double* xs, int n, int lane,
-                                                 const RowHead& h) {
-  if (!h.ok) return warp_row_dot(a, xs, n, lane);
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
-  const double2* a2 = reinterpret_cast<const double2*>(a);
-  const int n2 = n >> 1;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int j = lane + 32 * m;
-    s[m & 1] += h.v[m].x * xs[2 * j], s[2 + (m & 1)] += h.v[m].y * xs[2 * j + 1];
-  }
-  int j0 = 32 * 8;
-  for (; j0 + 32 * 8 <= n2; j0 += 32 * 8) {
-    double2 v[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) v[m] = __ldg(a2 + j0 + lane + 32 * m);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      const int j = j0 + lane + 32 * m;
-      s[m & 1] += v[m].x * xs[2 * j], s[2 + (m & 1)] += v[m].y * xs[2 * j + 1];
-    }
-  }
-  for (int j = j0 + lane; j < n2; j += 32) s[0] += a2[j].x * xs[2 * j], s[1] += a2[j].y * xs[2 * j + 1];
-  return warp_sum((s[0] + s[2]) + (s[1] + s[3]));
-}
-
 /// y = A x for a dense row-major n x n A: a warp per row (16-byte loads when
 /// the rows are 16-byte aligned, four loads in flight per lane), x staged in
 /// shared memory; grid-stride over rows.  Coarse projector (G_c^T G_c)^{-1}.
 __global__ void __launch_bounds__(256) k_dense_gemv_w(int n, const double* __restrict__ A,
                                                       const double* __restrict__ x, double* __restrict__ y) {
   if (kPdlEarly) pdl_trigger();
-  extern __shared__ double xs[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int row = blockIdx.x * 8 + warp;
-  const RowHead h = row_head(A + (size_t)(row < n ? row : 0) * n, n, lane);  // before the wait
   pdl_wait();
+  extern __shared__ double xs[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
   __syncthreads();
-  if (row < n) {
-    const double v = warp_row_dot_h(A + (size_t)row * n, xs, n, lane, h);
-    if (lane == 0) y[row] = v;
-  }
-  for (row += gridDim.x * 8; row < n; row += gridDim.x * 8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
     const double v = warp_row_dot(A + (size_t)row * n, xs, n, lane);
     if (lane == 0) y[row] = v;
   }
@@ -578,16 +529,11 @@ __global__ void __launch_bounds__(256) k_spmv_warp(int nrows, const int* __restr
                                                    const double* __restrict__ x, double* y, double alpha,
                                                    double beta) {
   if (kPdlEarly) pdl_trigger();
-  // the matrix does not depend on the predecessor: row range and the lane's
-  // first entry are loaded before the PDL wait
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int q0 = row < nrows ? ptr[row] : 0, q1 = row < nrows ? ptr[row + 1] : 0;
-  const int i0 = q0 + lane < q1 ? idx[q0 + lane] : 0;
-  const double v0 = q0 + lane < q1 ? val[q0 + lane] : 0.0;
   pdl_wait();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= nrows) return;
-  double s = q0 + lane < q1 ? v0 * x[i0] : 0.0;
-  for (int q = q0 + lane + 32; q < q1; q += 32) s += val[q] * x[idx[q]];
+  double s = 0.0;
+  for (int q = ptr[row] + lane; q < ptr[row + 1]; q += 32) s += val[q] * x[idx[q]];
   s = warp_sum(s);
   if (lane == 0) y[row] = (beta == 0.0 ? 0.0 : beta * y[row]) + alpha * s;
 }
@@ -618,21 +564,17 @@ __global__ void k_dense_top_gather(int n, int c0, int cb_top, const int* __restr
                                    const int* __restrict__ fold_idx, const double* __restrict__ CB, const double* src,
                                    const int* __restrict__ perm, double* y) {
   if (kPdlEarly) pdl_trigger();
-  // a warp per column: lanes take the fold entries, warp_sum tree (fixed order);
-  // the fold lists and the permutation are loaded before the PDL wait
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int q0 = i < n ? fold_ptr[c0 + i] : 0, q1 = i < n ? fold_ptr[c0 + i + 1] : 0;
-  const int f0 = q0 + lane < q1 ? fold_idx[q0 + lane] : cb_top;
-  const int pi = i < n && lane == 0 ? (perm ? perm[c0 + i] : c0 + i) : 0;
   pdl_wait();
+  // a warp per column: lanes take the fold entries, warp_sum tree (fixed order)
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
-  double v = f0 < cb_top ? CB[f0] : 0.0;
-  for (int q = q0 + lane + 32; q < q1; q += 32) {
+  double v = 0.0;
+  for (int q = fold_ptr[c0 + i] + lane, q1 = fold_ptr[c0 + i + 1]; q < q1; q += 32) {
     const int f = fold_idx[q];
     if (f < cb_top) v += CB[f];
   }
   v = warp_sum(v);
-  if (lane == 0) y[i] = src[pi] + v;
+  if (lane == 0) y[i] = (perm ? src[perm[c0 + i]] : src[c0 + i]) + v;
 }
 
 /// pass 2: X[c0 + i] = sum_j W[i][j] y[j] (W = inverse of the top Schur
@@ -647,11 +589,8 @@ __global__ void __launch_bounds__(512) k_dense_top_gemv(int n, int c0, const dou
                                                         const double* __restrict__ CB = nullptr, int cb_top = 0,
                                                         const double* __restrict__ src = nullptr) {
   if (kPdlEarly) pdl_trigger();
-  extern __shared__ double ys[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int row0 = blockIdx.x * nw + warp;
-  const RowHead h = row_head(W + (size_t)(row0 < n ? row0 : 0) * n, n, lane);  // before the wait
   pdl_wait();
+  extern __shared__ double ys[];
   if (fold_ptr) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       double v = src[perm[c0 + i]];
@@ -665,9 +604,9 @@ __global__ void __launch_bounds__(512) k_dense_top_gemv(int n, int c0, const dou
     for (int i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y[i];
   }
   __syncthreads();
-  for (int row = row0; row < n; row += gridDim.x * nw) {
-    const double v = row == row0 ? warp_row_dot_h(W + (size_t)row * n, ys, n, lane, h)
-                                 : warp_row_dot(W + (size_t)row * n, ys, n, lane);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = blockIdx.x * nw + warp; row < n; row += gridDim.x * nw) {
+    const double v = warp_row_dot(W + (size_t)row * n, ys, n, lane);
     if (lane == 0) {
       X[c0 + row] = v;
       if (perm) x[perm[c0 + row]] = v;
@@ -701,79 +640,48 @@ constexpr int kUnitRows = 128, kUnitMaxIn = 1024;
 /// thread are loaded before the inputs (b or X, plus folded lower-stage
 /// contributions) are staged in shared memory, then eight loads stay in
 /// flight per thread; slices are summed in slice order (deterministic).
-template <int S, int RB = kUnitRows, int MI = kUnitMaxIn>
+template <int S, int RB = kUnitRows>
 __global__ void __launch_bounds__(RB * S) k_dense_unit(const UnitWork* __restrict__ work, DenseUnits U) {
-  __shared__ __align__(16) double in[MI];
+  constexpr int B = 8;
+  __shared__ double in[kUnitMaxIn];
   __shared__ double part[S > 1 ? S : 1][RB];
   if (kPdlEarly) pdl_trigger();
   const UnitWork w = work[blockIdx.x];
   const int r = threadIdx.x % RB, q = threadIdx.x / RB;
   const int ni = w.nin, ld = w.nout;
-  // slices of whole 8-input chunks (16-byte aligned shared-memory reads)
-  const int nch = (ni + 7) >> 3;
-  const int jl = 8 * (nch * q / S), jh = min(ni, 8 * (nch * (q + 1) / S));
-  const int nfull = jh > jl ? (jh - jl) >> 3 : 0;
+  const int jl = (int)((long long)ni * q / S), jh = (int)((long long)ni * (q + 1) / S);
   const bool live = r < w.nrows;
-  // dead rows read row r0 (valid memory) and discard: no predicates in the loop
-  const double* Tc = U.T + w.toff + w.r0 + (live ? r : 0);
-  const long long st8 = 8LL * ld;
-  const double* p = Tc + (long long)jl * ld;
-  double v[8], u[8];
-  auto ld8 = [&](double (&d)[8], const double* src) {
+  const double* Tc = U.T + w.toff + w.r0 + r;
+  double v[B];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) d[m] = __ldg(src + (long long)m * ld);
-  };
-  double a0 = 0.0, a1 = 0.0;
-  auto fma8 = [&](const double (&d)[8], int j) {
-    const double2* x2 = reinterpret_cast<const double2*>(in + j);
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const double2 x = x2[m];
-      a0 += d[2 * m] * x.x, a1 += d[2 * m + 1] * x.y;
-    }
-  };
-  if (nfull > 0) ld8(v, p);  // the operator does not depend on the predecessor
-  // input positions / vector indices of the first P inputs and this row's
-  // output index: none depends on the predecessor either
-  constexpr int P = RB * S >= 128 ? 2 : 4;
+  for (int m = 0; m < B; ++m) v[m] = (live && jl + m < jh) ? __ldg(Tc + (long long)(jl + m) * ld) : 0.0;
+  pdl_wait();  // the operator prefetch above does not depend on the predecessor
   const int* il = U.in + w.inoff;
   const int* iln = U.in_nat + w.inoff;
-  int cpre[P], npre[P];
-#pragma unroll
-  for (int m = 0; m < P; ++m) {
-    const int i = threadIdx.x + m * blockDim.x;
-    cpre[m] = i < ni ? il[i] : 0;
-    npre[m] = i < ni && U.b ? iln[i] : 0;
-  }
-  const int o_pre = live && q == 0 ? U.out[w.outoff + w.r0 + r] : 0;
-  const int onat_pre = live && q == 0 && U.x && o_pre >= 0 ? U.out_nat[w.outoff + w.r0 + r] : 0;
-  pdl_wait();  // the operator and index prefetches above do not depend on the predecessor
-  auto stage = [&](int i, int c, int nat) {
-    double x = U.b ? U.b[nat] : U.X[c];
+  for (int i = threadIdx.x; i < ni; i += blockDim.x) {
+    const int c = il[i];
+    double x = U.b ? U.b[iln[i]] : U.X[c];
     if (U.cbmax) x = fold_add(x, c, U.fold_ptr, U.fold_idx, U.CB, U.cbmax);
     in[i] = x;
-  };
-#pragma unroll
-  for (int m = 0; m < P; ++m) {
-    const int i = threadIdx.x + m * blockDim.x;
-    if (i < ni) stage(i, cpre[m], npre[m]);
   }
-  for (int i = threadIdx.x + P * blockDim.x; i < ni; i += blockDim.x) stage(i, il[i], U.b ? iln[i] : 0);
   __syncthreads();
-  // register double buffer over whole chunks: chunk c+1 streams in while chunk
-  // c is consumed (uniform trip counts per warp, no per-element predicates)
-  int j = jl, c = 0;
-  for (; c + 2 <= nfull; c += 2, j += 16, p += 2 * st8) {
-    ld8(u, p + st8);
+  // register double buffer: chunk j+B streams in while chunk j is consumed
+  double a0 = 0.0, a1 = 0.0, u[B];
+  auto ld8 = [&](double (&d)[B], int j) {
+#pragma unroll
+    for (int m = 0; m < B; ++m) d[m] = (live && j + m < jh) ? __ldg(Tc + (long long)(j + m) * ld) : 0.0;
+  };
+  auto fma8 = [&](const double (&d)[B], int j) {
+#pragma unroll
+    for (int m = 0; m < B; ++m)
+      if (j + m < jh) (m & 1 ? a1 : a0) += d[m] * in[j + m];
+  };
+  for (int j = jl; j < jh; j += 2 * B) {
+    if (j + B < jh) ld8(u, j + B);
     fma8(v, j);
-    if (c + 2 < nfull) ld8(v, p + 2 * st8);
-    fma8(u, j + 8);
+    if (j + 2 * B < jh) ld8(v, j + 2 * B);
+    if (j + B < jh) fma8(u, j + B);
   }
-  if (c < nfull) {
-    fma8(v, j);
-    j += 8;
-  }
-  for (; j < jh; ++j) a0 += __ldg(Tc + (long long)j * ld) * in[j];
   double acc = a0 + a1;
   if (S > 1) {
     part[q][r] = acc;
@@ -784,12 +692,12 @@ __global__ void __launch_bounds__(RB * S) k_dense_unit(const UnitWork* __restric
     for (int k = 0; k < S; ++k) acc += part[k][r];
   }
   if (!live) return;
-  const int o = o_pre;
+  const int o = U.out[w.outoff + w.r0 + r];
   if (o < 0) {
     U.CB[-1 - o] = acc;
   } else {
     if (U.xout) U.X[o] = acc;
-    if (U.x) U.x[onat_pre] = acc;
+    if (U.x) U.x[U.out_nat[w.outoff + w.r0 + r]] = acc;
   }
 }
 
