@@ -45,8 +45,18 @@ struct DualSet {
 
 constexpr int kDualPW = 16;   // panel width of the root factorisation
 constexpr int kDualLd = 17;   // padded row stride of the staged panel
+// large root fronts (c3: 64x64-cell P2 subdomains, m ~ 1800) use 8-column
+// panels so the staged panel rows fit in shared memory
+constexpr int kDualPWs = 8, kDualLds = 9;
+constexpr long long kDualSmemMax = 227 * 1024;
+/// panel width k_dual_root uses for a root front of order m (0: too large)
+__host__ __device__ inline int dual_panel_width(long long m) {
+  return 8LL * m * kDualLd <= kDualSmemMax ? kDualPW : (8LL * m * kDualLds <= kDualSmemMax ? kDualPWs : 0);
+}
 
+template <int PW>
 __global__ void __launch_bounds__(512) k_dual_root(DualSet S) {
+  constexpr int LD = PW + 1;
   extern __shared__ double sm_d[];
   const int p = S.prob[blockIdx.x];
   const int t = S.prob_type[p];
@@ -92,9 +102,9 @@ __global__ void __launch_bounds__(512) k_dual_root(DualSet S) {
   }
   // 4. LDL^T of the nB B-pivots; the trailing multiplier block becomes -F
   double* Lp = sm_d;  // staged panel rows (padded stride)
-  __shared__ double Dk[kDualPW];
-  for (int p0 = 0; p0 < nB; p0 += kDualPW) {
-    const int pw = min(kDualPW, nB - p0);
+  __shared__ double Dk[PW];
+  for (int p0 = 0; p0 < nB; p0 += PW) {
+    const int pw = min(PW, nB - p0);
     for (int j = p0; j < p0 + pw; ++j) {
       const double d = at(j, j);
       if (!(d != 0.0) || !isfinite(d)) {
@@ -112,21 +122,21 @@ __global__ void __launch_bounds__(512) k_dual_root(DualSet S) {
     }
     const int r0 = p0 + pw;
     const int nr = m - r0;
-    for (int e = tid; e < nr * kDualPW; e += nth) {
-      const int r = e / kDualPW, k = e - r * kDualPW;
-      Lp[r * kDualLd + k] = k < pw ? at(r0 + r, p0 + k) : 0.0;
+    for (int e = tid; e < nr * PW; e += nth) {
+      const int r = e / PW, k = e - r * PW;
+      Lp[r * LD + k] = k < pw ? at(r0 + r, p0 + k) : 0.0;
     }
-    if (tid < kDualPW) Dk[tid] = tid < pw ? at(p0 + tid, p0 + tid) : 0.0;
+    if (tid < PW) Dk[tid] = tid < pw ? at(p0 + tid, p0 + tid) : 0.0;
     __syncthreads();
     for (int c = r0 + warp; c < m; c += nw) {
-      double w[kDualPW];
+      double w[PW];
 #pragma unroll
-      for (int k = 0; k < kDualPW; ++k) w[k] = Dk[k] * Lp[(c - r0) * kDualLd + k];
+      for (int k = 0; k < PW; ++k) w[k] = Dk[k] * Lp[(c - r0) * LD + k];
       for (int i = c + lane; i < m; i += 32) {
-        const double* li = Lp + (i - r0) * kDualLd;
+        const double* li = Lp + (i - r0) * LD;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < kDualPW; k += 2) a0 += li[k] * w[k], a1 += li[k + 1] * w[k + 1];
+        for (int k = 0; k < PW; k += 2) a0 += li[k] * w[k], a1 += li[k + 1] * w[k + 1];
         at(i, c) -= a0 + a1;
       }
     }

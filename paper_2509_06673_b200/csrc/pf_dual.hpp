@@ -78,7 +78,7 @@ inline DualType build_dual_type(const SubType& T, const Subdomain& rep) {
   std::vector<std::tuple<int, int, double>> ent;
   dual_local_mults(rep, lam, ent);
   X.nM = (int)lam.size();
-  if (8LL * (X.nB + X.nM) * dev::kDualLd > 227 * 1024) {  // k_dual_root stages a panel of the root front
+  if (!dev::dual_panel_width(X.nB + X.nM)) {  // k_dual_root stages a panel of the root front
     X.why = "root front exceeds the shared-memory panel of k_dual_root";
     return X;
   }

@@ -1797,9 +1797,11 @@ struct Engine {
     d_ptype.upload(ptype_of_own());
     d_err.upload(std::vector<int>{0});
     dl_F.alloc(dl_opsize), dl_S.alloc(dl_opsize);
-    const int smem = (int)std::max<long long>(8LL * mmax, 8LL * mmax * dev::kDualLd);
-    if (smem > 227 * 1024) fail(kInternal, "dual root front too large for the shared-memory panel");
-    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_dual_root, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int pw = dev::dual_panel_width(mmax);
+    if (!pw) fail(kInternal, "dual root front too large for the shared-memory panel");
+    const int smem = (int)std::max<long long>(8LL * mmax, 8LL * mmax * (pw + 1));
+    auto root_kernel = pw == dev::kDualPW ? dev::k_dual_root<dev::kDualPW> : dev::k_dual_root<dev::kDualPWs>;
+    PF_CUDA_CHECK(cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     std::vector<int> all(np);
     std::iota(all.begin(), all.end(), 0);
     d_prob.upload(all);
@@ -1816,7 +1818,7 @@ struct Engine {
       S.g_ptr = d_gptr.p, S.g_b = d_gb.p, S.type_fix = d_tfix.p, S.type_nfix = d_tnfix.p, S.fixpos = d_fixp.p;
       S.Gv = d_gall.p, S.prob_gval = d_pgval.p, S.prob_op = d_pop.p;
       S.F = Fb, S.Fop = dl_F.p, S.Sop = dl_S.p, S.err = d_err.p;
-      dev::k_dual_root<<<p1 - p0, 512, smem, st>>>(S);
+      root_kernel<<<p1 - p0, 512, smem, st>>>(S);
       ::pf::g_launches++;
     };
     if (run_fronts(R, &chunk)) fail(kSingular, "dual operators: zero pivot in a subdomain interior");
