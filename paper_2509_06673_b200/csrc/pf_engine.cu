@@ -2785,7 +2785,9 @@ struct Engine {
       if (nc) coarse_solve(t, c_tmp2.p);
       fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);  // t = P F q, sigma, a
       fdot(dev::DOT_AXPY, t, r, dev::KS_RR, dev::SOP_SQMR_TAU);                         // r -= a t, tau
-      launch_pdl(dev::k_sqmr_dx_s, nb, 256, 0, st, n, sc, q, d, lambda);
+      launch_pdl(dev::k_sqmr_dx_s, nb, 256, 0, st, n, sc, q, d, lambda, lp_cap_h, (const int*)d_status.p,
+                 lp_cap_maxit, lp_capturing ? 1 : 0);
+      lp_cond_set = lp_capturing;
     };
     iter(true);
     if (status() == dev::KST_RUN && maxit > 1 && loop_ok()) {
@@ -2820,6 +2822,11 @@ struct Engine {
   int lp_key_kind = 0, lp_maxit = 0;
   long long lp_nlaunch = 0;
   int lp_dF = 0, lp_dM = 0;
+  // while capturing the loop body: the conditional handle, so the body's last
+  // kernel can set the condition itself (lp_cond_set) instead of k_loop_cond
+  bool lp_capturing = false, lp_cond_set = false;
+  cudaGraphConditionalHandle lp_cap_h = 0;
+  int lp_cap_maxit = 0;
   template <class Fn>
   void graphed_loop(const void* key, int kind, int maxit, Fn&& body) {
     if (!lp_exec || lp_key_ptr != key || lp_key_kind != kind || lp_maxit != maxit) {
@@ -2837,8 +2844,10 @@ struct Engine {
       const long long l0 = ::pf::g_launches;
       const int f0 = fapplies, m0 = papplies;
       PF_CUDA_CHECK(cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      lp_capturing = true, lp_cond_set = false, lp_cap_h = h, lp_cap_maxit = maxit;
       body();
-      launch_pdl(dev::k_loop_cond, 1, 1, 0, st, h, (const int*)d_status.p, maxit);
+      lp_capturing = false;
+      if (!lp_cond_set) launch_pdl(dev::k_loop_cond, 1, 1, 0, st, h, (const int*)d_status.p, maxit);
       cudaGraph_t cap;
       PF_CUDA_CHECK(cudaStreamEndCapture(st, &cap));
       PF_CUDA_CHECK(cudaGraphInstantiate(&lp_exec, g, 0));

@@ -305,9 +305,15 @@ __global__ void k_xpay_s(int n, const double* x, double* y, const double* coef) 
   if (i < n) y[i] = x[i] + c * y[i];
 }
 /// SQMR: d = c^2 theta_old^2 d + c^2 a q; x += d
-__global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d, double* x) {
+/// With set_cond, block 0 also sets the device-side loop's WHILE condition
+/// (the status word is final: the tau dot ran before), replacing a separate
+/// k_loop_cond launch at the end of every iteration.
+__global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d, double* x,
+                            cudaGraphConditionalHandle h, const int* status, int maxit, int set_cond) {
   if (kPdlEarly) pdl_trigger();
   pdl_wait();
+  if (set_cond && blockIdx.x == 0 && threadIdx.x == 0)
+    cudaGraphSetConditional(h, status[0] == KST_RUN && status[1] < maxit ? 1u : 0u);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double c2 = sc[KS_C] * sc[KS_C];
