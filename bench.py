@@ -278,6 +278,11 @@ def run_ours(args, rank, world, dist):
         if info.n_coarse:
             extra["coarse_gemv"] = comp(5, info.bytes_coarse + 16.0 * info.n_coarse,
                                         "k_dense_gemv_w: (G_c^T G_c)^-1 y, dense n_c x n_c")
+        if info.flops_backsub > 0:
+            extra["explicit_back_substitution"] = {
+                "what": "k_h_gemm: x_s = K_s^+ b_s - H_t lambda_s, H_t = K_t^+ G_t^T per type (FP64 mma.sync), "
+                        "once per step instead of a factor sweep",
+                "flops": info.flops_backsub, "bytes": info.bytes_backsub}
         # dominant per-iteration piece: the mortar Gram solve when present
         dom = extra.get("mortar_gram_solve") or extra["local_dual_products"]
         kernel = dom["what"]

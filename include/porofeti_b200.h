@@ -86,6 +86,8 @@ typedef struct pf_info {
   double flops_flocal;  /* its flops (2 n^2 per subdomain) */
   double bytes_coarse;  /* bytes of one dense coarse GEMV ((G_c^T G_c)^-1, n_c^2 values) */
   double bytes_factor_stored; /* factor values stored for the per-step sweeps (after same-type sharing) */
+  double flops_backsub;  /* explicit back-substitution GEMM per step (0: the sweep back-substitutes) */
+  double bytes_backsub;  /* its operator + vector bytes */
 } pf_info;
 
 typedef struct pf_sub_info {

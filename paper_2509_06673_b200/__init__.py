@@ -99,6 +99,7 @@ class Info(C.Structure):
         ("bytes_symv", C.c_double), ("bytes_symv_stored", C.c_double), ("bytes_qsolve", C.c_double),
         ("bytes_qsolve_applied", C.c_double), ("bytes_flocal", C.c_double), ("flops_flocal", C.c_double),
         ("bytes_coarse", C.c_double), ("bytes_factor_stored", C.c_double),
+        ("flops_backsub", C.c_double), ("bytes_backsub", C.c_double),
     ]
 
 

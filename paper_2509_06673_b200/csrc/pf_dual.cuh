@@ -421,6 +421,150 @@ __global__ void __launch_bounds__(kGThreads) k_type_gemm(const GemmWork* __restr
     }
 }
 
+/// Explicit back-substitution (per-step, same-type subdomains): for every
+/// member j of a type, X[col_out[j] + i] = Yb[col_out[j] + i] -
+/// sum_k H_t[i][k] xloc[col_in[j] + k], H_t = K_t^+ G_t^T (dim_t x n_t, row
+/// major, built once by the factor sweeps), Yb = K^+ b from the interface
+/// right-hand side: x_s = K_s^+ (b_s - G_s^T lambda) without a sweep.  The
+/// tile machinery of k_type_gemm below (same fragment layout and cp.async
+/// ring); rows bound nr, K bound nk, no K slices.
+struct __align__(16) HWork {
+  long long aoff;
+  int nr, nk, r0, c0, ncol, coloff, lda, pad;
+};
+/// (k_type_gemm) Y[col_loff[j] + i] = sum_k A_t[i][k] xloc[col_loff[j] + k] on the FP64
+/// tensor cores (mma.sync m8n8k4): a 32x32 output tile per 64-thread CTA
+/// (each warp 16 rows x 32 columns = 2 x 4 MMA tiles), K in 16-chunks through
+/// a 4-stage cp.async ring (16-byte copies: operator rows padded to an even
+/// leading dimension, slot ranges even; shared-memory rows of 20 doubles so
+/// the fragment loads are conflict-free; out-of-range elements zero-filled).
+/// K may be split into slices (planes of Y, summed by k_local_reduce in plane
+/// order).  Fixed summation order (deterministic).
+__global__ void __launch_bounds__(kGThreads) k_h_gemm(const HWork* __restrict__ work,
+                                                         const double* __restrict__ A,
+                                                      const long long* __restrict__ col_in,
+                                                      const long long* __restrict__ col_out,
+                                                      const double* __restrict__ xloc, const double* __restrict__ Yb,
+                                                      double* __restrict__ X) {
+  __shared__ __align__(16) double As[kGStages][kGM][kGLd];
+  __shared__ __align__(16) double Bs[kGStages][kGN][kGLd];
+  if (kPdlEarly) pdl_trigger();
+  const HWork w = work[blockIdx.x];
+  const int tid = threadIdx.x, n = w.nk;
+  const double* a = A + w.aoff;
+  // loader: k pair kp = tid % 8 (16 bytes), rows / columns tid / 8 + 8 m (m < 4)
+  const int kp = tid & 7, lr0 = tid >> 3;
+  const double* ap[4];
+  const double* bp[4];
+  bool av[4], bv[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int r = w.r0 + lr0 + 8 * m, cc = w.c0 + lr0 + 8 * m;
+    av[m] = r < w.nr, bv[m] = cc < w.ncol;
+    ap[m] = a + (long long)(av[m] ? r : 0) * w.lda;
+    bp[m] = xloc + (bv[m] ? col_in[w.coloff + cc] : 0);
+  }
+  const int c_beg = 0, nch = (n + kGK - 1) / kGK;
+  // operator (A) and member-input (B) copies of chunk c; B depends on the
+  // predecessor kernel (PDL), A does not
+  auto issueA = [&](int c) {
+    if (c < nch) {
+      const int st = c % kGStages;
+      const int k = c * kGK + 2 * kp;
+      const int nb = k + 1 < n ? 16 : (k < n ? 8 : 0);  // bytes in range
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&As[st][lr0 + 8 * m][2 * kp]), ap[m] + (nb ? k : 0),
+                         av[m] ? nb : 0);
+    }
+  };
+  auto issueB = [&](int c) {
+    if (c < nch) {
+      const int st = c % kGStages;
+      const int k = c * kGK + 2 * kp;
+      const int nb = k + 1 < n ? 16 : (k < n ? 8 : 0);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        cp_async16_zfill((unsigned)__cvta_generic_to_shared(&Bs[st][lr0 + 8 * m][2 * kp]), bp[m] + (nb ? k : 0),
+                         bv[m] ? nb : 0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto issue = [&](int c) {
+    issueA(c);
+    issueB(c);
+  };
+  // warp wp: rows [16 wp, 16 wp + 16) x 32 columns as 2 x 4 m8n8k4 tiles
+  // (A fragment: row lane/4, k lane%4; B fragment: k lane%4, column lane/4;
+  //  C: row lane/4, columns 2 (lane%4) + {0,1})
+  const int lane = tid & 31, wp = tid >> 5;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // prologue: operator chunks before the PDL wait (they land in the first
+  // commit group), member inputs after it
+#pragma unroll
+  for (int c = 0; c < kGStages - 1; ++c) issueA(c_beg + c);
+  pdl_wait();
+#pragma unroll
+  for (int c = 0; c < kGStages - 1; ++c) issueB(c_beg + c);
+  for (int c = c_beg; c < nch; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kGStages - 2) : "memory");
+    __syncthreads();  // chunk c landed for every thread; chunk c-1's slot is free
+    issue(c + kGStages - 1);
+    const int st = c % kGStages;
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      const int kk = k4 + (lane & 3);
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = As[st][wp * 16 + i * 8 + (lane >> 2)][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[st][j * 8 + (lane >> 2)][kk];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cc = w.c0 + j * 8 + (lane & 3) * 2 + h;
+      if (cc >= w.ncol) continue;
+      const long long yo = col_out[w.coloff + cc];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = w.r0 + wp * 16 + i * 8 + (lane >> 2);
+        if (r < w.nr) X[yo + r] = Yb[yo + r] - acc[i][j][h];
+      }
+    }
+}
+
+
+/// H construction: X[idx[e]] = val[e] (scatter of G_s^T e_j into the natural-order
+/// right-hand side, one entry list per round)
+__global__ void k_h_scatter(int n, const long long* __restrict__ idx, const double* __restrict__ val, double* T) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) T[idx[e]] = val[e];
+}
+/// H construction: column j of H_t from a solved subdomain segment of X
+struct HCol {
+  long long xoff, hoff;  // X segment; H_t offset + column j
+  int dim, lda;
+};
+__global__ void k_h_extract(const HCol* __restrict__ cols, const double* __restrict__ X, double* __restrict__ H) {
+  const HCol c = cols[blockIdx.y];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c.dim; r += gridDim.x * blockDim.x)
+    H[c.hoff + (long long)r * c.lda] = X[c.xoff + r];
+}
+
 /// y[i] = alpha * sum over the multiplier's slots (fixed order) of Y
 /// (nks K-slices of the type GEMM: Y holds nks planes of `stride` slots; the
 /// planes of a slot are summed in plane order, then the slots in slot order)

@@ -371,6 +371,7 @@ struct SolveSystem {
   /// first problem's (translates of one subdomain on a homogeneous material)
   /// read that copy; the value storage is compacted to the distinct factors.
   /// Every solve still runs the full sweep for every problem.
+  std::vector<int> prob_eq;  // per problem: factor values equal to its type's first problem (bitwise)
   void share_factors(cudaStream_t st) {
     const int np = (int)prob_type.size();
     std::vector<int> rep(np), first(syms.size(), -1);
@@ -401,6 +402,7 @@ struct SolveSystem {
       if (nl[p] < 0) nl[p] = nl[rep[p]];
     shared_factors = 0;
     for (int p = 0; p < np; ++p) shared_factors += eq[p] && rep[p] != p;
+    prob_eq = eq;
     if (!shared_factors) return;
     DevBuf<double> L2;
     L2.alloc(tot + 4);
@@ -1249,6 +1251,7 @@ struct Engine {
     if (use_q) setup_q();
     if (floating_any) setup_coarse();
     setup_krylov();
+    if (dual) setup_backsub();
     project_initial();
     if (std::getenv("PF_VERBOSE")) {
       auto dump = [](const char* name, SolveSystem& S) {
@@ -1619,6 +1622,7 @@ struct Engine {
   // explicit local dual operators (pf_dual.hpp / pf_dual.cuh)
   DevBuf<int> dl_nloc, dl_lam, dl_rptr;
   std::vector<int> dl_nloc_h;
+  std::vector<long long> dl_loff_h;
   DevBuf<long long> dl_loff, dl_opoff, dl_rslot;
   DevBuf<double> dl_F, dl_S, dl_Y;
   DevBuf<unsigned int> red_count;  // arrival counter of k_dot_fused
@@ -1856,6 +1860,7 @@ struct Engine {
     // apply maps: local slots -> multipliers, multipliers -> slots (fixed subdomain order)
     dl_nloc.upload(nloc), dl_loff.upload(ploff), dl_opoff.upload(ppk);
     dl_nloc_h = nloc;
+    dl_loff_h = ploff;
     {
       std::vector<int> lg(lamall);
       for (int& l : lg) l = std::max(l, 0);  // padding slots gather x[0] (never used)
@@ -2412,6 +2417,8 @@ struct Engine {
     }
     info.bytes_coarse = 8.0 * (double)nc * (double)nc;
     info.bytes_factor_stored = 8.0 * (double)Ksys.total_L;
+    info.flops_backsub = hb_on ? hb_flops : 0.0;
+    info.bytes_backsub = hb_on ? hb_bytes : 0.0;
   }
 
   // ------------------------------------------------------------------
@@ -2619,11 +2626,114 @@ struct Engine {
     pmin = lo, pmax = hi;
   }
 
+  // ------------------------------------------------------------------
+  // Explicit back-substitution: x_s = K_s^+ b_s - H_t lambda_s with
+  // H_t = K_t^+ G_t^T per subdomain type (the factor sweeps build its columns
+  // once: every member of a type solves a different unit right-hand side per
+  // round), K^+ b kept from the interface right-hand side.  Requires every
+  // owned subdomain to read its type's factor (bitwise) and to have its
+  // type's G entries; PF_BACKSUB=sweep keeps the sweep.
+  bool hb_on = false;
+  DevBuf<double> hb_H, hb_Yb;
+  DevBuf<dev::HWork> hb_work;
+  DevBuf<long long> hb_cin, hb_cout;
+  int hb_nwork = 0;
+  double hb_bytes = 0.0, hb_flops = 0.0;
+  void setup_backsub() {
+    const char* bs = std::getenv("PF_BACKSUB");
+    if (bs && std::string(bs) == "sweep") return;
+    const int np = nown(), nt = (int)D.types.size();
+    if (np < 1 || (int)Ksys.prob_eq.size() != np) return;
+    for (int p = 0; p < np; ++p)
+      if (!Ksys.prob_eq[p]) return;
+    std::vector<std::vector<int>> lam(np);
+    std::vector<std::vector<std::tuple<int, int, double>>> ent(np);
+    parallel_for(np, nthreads, [&](int p) { dual_local_mults(OS(p), lam[p], ent[p]); });
+    std::vector<std::vector<int>> mem(nt);
+    for (int p = 0; p < np; ++p) mem[OS(p).type].push_back(p);
+    for (int t = 0; t < nt; ++t)
+      for (int p : mem[t])
+        if (ent[p] != ent[mem[t][0]]) return;  // G of the type's members must coincide
+    // H_t layout (row-major dim_t x lda_t)
+    std::vector<long long> hoff(nt, 0);
+    std::vector<int> hlda(nt, 0), hdim(nt, 0), hn(nt, 0);
+    long long tot = 0;
+    for (int t = 0; t < nt; ++t) {
+      if (mem[t].empty()) continue;
+      hn[t] = (int)lam[mem[t][0]].size(), hdim[t] = ksym[t].n, hlda[t] = hn[t] + (hn[t] & 1);
+      hoff[t] = tot, tot += (long long)hdim[t] * hlda[t];
+    }
+    hb_H.alloc(std::max<long long>(1, tot));
+    hb_H.zero(st);
+    int rounds = 0;
+    for (int t = 0; t < nt; ++t)
+      if (!mem[t].empty()) rounds = std::max(rounds, (hn[t] + (int)mem[t].size() - 1) / (int)mem[t].size());
+    DevBuf<double> T;
+    T.alloc(std::max<long long>(1, total_vec));
+    std::vector<long long> hpx(np);
+    {
+      std::vector<long long> px(Ksys.prob_x.begin(), Ksys.prob_x.end());
+      for (int p = 0; p < np; ++p) hpx[p] = px[p];
+    }
+    for (int k = 0; k < rounds; ++k) {
+      std::vector<long long> idx;
+      std::vector<double> val;
+      std::vector<dev::HCol> cols;
+      for (int t = 0; t < nt; ++t)
+        for (std::size_t i = 0; i < mem[t].size(); ++i) {
+          const int j = k * (int)mem[t].size() + (int)i;
+          if (j >= hn[t]) continue;
+          const int p = mem[t][i];
+          for (auto& e : ent[p])
+            if (std::get<0>(e) == j) idx.push_back(sub_vec[p] + std::get<1>(e)), val.push_back(std::get<2>(e));
+          cols.push_back(dev::HCol{hpx[p], hoff[t] + j, hdim[t], hlda[t]});
+        }
+      if (cols.empty()) continue;
+      T.zero(st);
+      DevBuf<long long> d_idx;
+      DevBuf<double> d_val;
+      DevBuf<dev::HCol> d_cols;
+      d_idx.upload(idx.empty() ? std::vector<long long>{0} : idx), d_val.upload(val.empty() ? std::vector<double>{0.0} : val);
+      d_cols.upload(cols);
+      if (!idx.empty()) dev::k_h_scatter<<<cdiv((long long)idx.size(), 256), 256, 0, st>>>((int)idx.size(), d_idx.p, d_val.p, T.p);
+      perm_in_K(T.p);
+      if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p);
+      Ksys.solve(st, 1);
+      dev::k_h_extract<<<dim3(8, (unsigned)cols.size()), 256, 0, st>>>(d_cols.p, Ksys.X.p, hb_H.p);
+      ::pf::g_launches += 3 + (nfix ? 1 : 0);
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    // per-step GEMM work: 32x32 tiles over (rows of H_t) x (members)
+    std::vector<dev::HWork> work;
+    std::vector<long long> cin, cout;
+    hb_flops = hb_bytes = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      if (mem[t].empty()) continue;
+      const int c0 = (int)cin.size(), m = (int)mem[t].size();
+      for (int p : mem[t]) cin.push_back(dl_loff_h[p]), cout.push_back(hpx[p]);
+      for (int r0 = 0; r0 < hdim[t]; r0 += dev::kGM)
+        for (int cc = 0; cc < m; cc += dev::kGN)
+          work.push_back(dev::HWork{hoff[t], hdim[t], hn[t], r0, cc, m, c0, hlda[t], 0});
+      hb_flops += 2.0 * hdim[t] * (double)hn[t] * m;
+      hb_bytes += 8.0 * hdim[t] * (double)hn[t] + 8.0 * m * (hn[t] + 2.0 * hdim[t]);
+    }
+    hb_work.upload(work), hb_cin.upload(cin), hb_cout.upload(cout);
+    hb_nwork = (int)work.size();
+    hb_Yb.alloc(std::max<long long>(1, Ksys.total_x));
+    if ((long long)dl_xloc.n < std::max<long long>(1, dl_nslots)) dl_xloc.alloc(std::max<long long>(1, dl_nslots));
+    hb_on = true;
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr, "[pf] explicit back-substitution: %d rounds of sweeps, H %.1f MB, %.2f GFLOP per step\n",
+                   rounds, 8e-6 * (double)tot, 1e-9 * hb_flops);
+  }
+
   /// F = sum_s G_s K_s^+ b_s - d  (into out)
   void interface_rhs(double* out) {
     perm_in_K(bvec.p);
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
+    if (hb_on)  // K^+ b for the explicit back-substitution
+      PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, out, 1.0, 0, dvec.p);
     reduce(out, D.n_lambda);
   }
@@ -2650,6 +2760,16 @@ struct Engine {
 
   /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> state
   void back_substitute(const double* lambda) {
+    if (hb_on) {
+      launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, lambda, dl_xloc.p);
+      launch_pdl(dev::k_h_gemm, hb_nwork, dev::kGThreads, 0, st, hb_work.p, hb_H.p, hb_cin.p, hb_cout.p, dl_xloc.p,
+                 hb_Yb.p, Ksys.X.p);
+      perm_out_K(state.p);
+      if (nc && nfloat_local)
+        dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
+                                                                d_fxyoff.p, alpha_vec.p, state.p); ::pf::g_launches++;
+      return;
+    }
     perm_in_K(bvec.p);
     if (g_back.nrows)
       dev::k_gather_ll<<<cdiv(g_back.nrows, 256), 256, 0, st>>>(g_back.nrows, g_back.rows.p, g_back.ptr.p,
