@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(kGThreads) k_h_gemm(const HWork* __restrict__ 
                                                          const double* __restrict__ A,
                                                       const long long* __restrict__ col_in,
                                                       const long long* __restrict__ col_out,
-                                                      const double* __restrict__ xloc, const double* __restrict__ Yb,
-                                                      double* __restrict__ X) {
+                                                      const double* __restrict__ xloc, const double* Yb,
+                                                      double* X) {  // Yb may alias X (in place)
   __shared__ __align__(16) double As[kGStages][kGM][kGLd];
   __shared__ __align__(16) double Bs[kGStages][kGN][kGLd];
   if (kPdlEarly) pdl_trigger();
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kGThreads) k_h_gemm(const HWork* __restrict__ 
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int r = w.r0 + wp * 16 + i * 8 + (lane >> 2);
-        if (r < w.nr) X[yo + r] = Yb[yo + r] - acc[i][j][h];
+        if (r < w.nr) X[yo + r] = Yb ? Yb[yo + r] - acc[i][j][h] : acc[i][j][h];
       }
     }
 }
@@ -556,13 +556,17 @@ __global__ void k_h_scatter(int n, const long long* __restrict__ idx, const doub
 }
 /// H construction: column j of H_t from a solved subdomain segment of X
 struct HCol {
-  long long xoff, hoff;  // X segment; H_t offset + column j
-  int dim, lda;
+  long long xoff, hoff, htoff;  // X segment; H_t offset + column j; H_t^T offset + row j
+  int dim, lda, ldt, pad;
 };
-__global__ void k_h_extract(const HCol* __restrict__ cols, const double* __restrict__ X, double* __restrict__ H) {
+__global__ void k_h_extract(const HCol* __restrict__ cols, const double* __restrict__ X, double* __restrict__ H,
+                            double* __restrict__ HT) {
   const HCol c = cols[blockIdx.y];
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c.dim; r += gridDim.x * blockDim.x)
-    H[c.hoff + (long long)r * c.lda] = X[c.xoff + r];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c.dim; r += gridDim.x * blockDim.x) {
+    const double v = X[c.xoff + r];
+    H[c.hoff + (long long)r * c.lda] = v;
+    HT[c.htoff + r] = v;
+  }
 }
 
 /// y[i] = alpha * sum over the multiplier's slots (fixed order) of Y

@@ -1168,7 +1168,16 @@ struct Engine {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       fail(kCuda, "no CUDA device: the B200 engine has no CPU execution path");
     if (const char* lr = std::getenv("LOCAL_RANK")) PF_CUDA_CHECK(cudaSetDevice(std::atoi(lr) % ndev));
-    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {  // the engine stream at the highest priority: the overlapped factor sweep of
+       // the back-substitution (hb_st, lowest priority) fills idle SMs only
+      int lo = 0, hi = 0;
+      PF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      if (std::getenv("PF_NO_PRIO")) hi = lo;  // A/B: both streams at the default priority
+      PF_CUDA_CHECK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+      PF_CUDA_CHECK(cudaStreamCreateWithPriority(&hb_st, cudaStreamNonBlocking, lo));
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev0, cudaEventDisableTiming));
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev1, cudaEventDisableTiming));
+    }
     nthreads = cfg.threads > 0 ? cfg.threads : (int)std::max(1u, std::thread::hardware_concurrency());
     D = build_disc(cfg, kover);
     rank = rank_, nranks = std::max(1, nranks_);
@@ -1286,6 +1295,9 @@ struct Engine {
     if (h_status) cudaFreeHost(h_status);
     if (comm) ncclCommDestroy(comm);
     if (st) cudaStreamDestroy(st);
+    if (hb_st) cudaStreamDestroy(hb_st);
+    if (hb_ev0) cudaEventDestroy(hb_ev0);
+    if (hb_ev1) cudaEventDestroy(hb_ev1);
   }
 
   /// level-0 (warp) task caps of the sweep schedule; PF_TASK_CAP / PF_TASK_WS override
@@ -2633,11 +2645,13 @@ struct Engine {
   // round), K^+ b kept from the interface right-hand side.  Requires every
   // owned subdomain to read its type's factor (bitwise) and to have its
   // type's G entries; PF_BACKSUB=sweep keeps the sweep.
-  bool hb_on = false;
-  DevBuf<double> hb_H, hb_Yb;
-  DevBuf<dev::HWork> hb_work;
-  DevBuf<long long> hb_cin, hb_cout;
-  int hb_nwork = 0;
+  bool hb_on = false, hb_pending = false;
+  DevBuf<double> hb_H, hb_HT, hb_Yb, hb_Bp;
+  DevBuf<dev::HWork> hb_work, hb_twork;
+  DevBuf<long long> hb_cin, hb_cout, hb_bpo, hb_tin, hb_tout;
+  int hb_nwork = 0, hb_ntwork = 0;
+  cudaStream_t hb_st = nullptr;            // K^+ b sweep, overlapped with the Krylov loop
+  cudaEvent_t hb_ev0 = nullptr, hb_ev1 = nullptr;
   double hb_bytes = 0.0, hb_flops = 0.0;
   void setup_backsub() {
     const char* bs = std::getenv("PF_BACKSUB");
@@ -2665,6 +2679,17 @@ struct Engine {
     }
     hb_H.alloc(std::max<long long>(1, tot));
     hb_H.zero(st);
+    // H_t^T (n_t x ldt, row-major, ldt even): the interface right-hand side's GEMM
+    std::vector<long long> htoff(nt, 0);
+    std::vector<int> hldt(nt, 0);
+    long long ttot = 0;
+    for (int t = 0; t < nt; ++t) {
+      if (mem[t].empty()) continue;
+      hldt[t] = hdim[t] + (hdim[t] & 1);
+      htoff[t] = ttot, ttot += (long long)hn[t] * hldt[t];
+    }
+    hb_HT.alloc(std::max<long long>(1, ttot));
+    hb_HT.zero(st);
     int rounds = 0;
     for (int t = 0; t < nt; ++t)
       if (!mem[t].empty()) rounds = std::max(rounds, (hn[t] + (int)mem[t].size() - 1) / (int)mem[t].size());
@@ -2686,7 +2711,7 @@ struct Engine {
           const int p = mem[t][i];
           for (auto& e : ent[p])
             if (std::get<0>(e) == j) idx.push_back(sub_vec[p] + std::get<1>(e)), val.push_back(std::get<2>(e));
-          cols.push_back(dev::HCol{hpx[p], hoff[t] + j, hdim[t], hlda[t]});
+          cols.push_back(dev::HCol{hpx[p], hoff[t] + j, htoff[t] + (long long)j * hldt[t], hdim[t], hlda[t], hldt[t], 0});
         }
       if (cols.empty()) continue;
       T.zero(st);
@@ -2699,7 +2724,7 @@ struct Engine {
       perm_in_K(T.p);
       if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p);
       Ksys.solve(st, 1);
-      dev::k_h_extract<<<dim3(8, (unsigned)cols.size()), 256, 0, st>>>(d_cols.p, Ksys.X.p, hb_H.p);
+      dev::k_h_extract<<<dim3(8, (unsigned)cols.size()), 256, 0, st>>>(d_cols.p, Ksys.X.p, hb_H.p, hb_HT.p);
       ::pf::g_launches += 3 + (nfix ? 1 : 0);
       PF_CUDA_CHECK(cudaStreamSynchronize(st));
     }
@@ -2719,6 +2744,25 @@ struct Engine {
     }
     hb_work.upload(work), hb_cin.upload(cin), hb_cout.upload(cout);
     hb_nwork = (int)work.size();
+    // interface right-hand side: F_s = H_t^T b_s (b permuted into even-aligned segments)
+    std::vector<long long> bpo(np);
+    long long btot = 0;
+    for (int p = 0; p < np; ++p) bpo[p] = btot, btot += hldt[OS(p).type];
+    hb_Bp.alloc(std::max<long long>(1, btot));
+    hb_Bp.zero(st);
+    hb_bpo.upload(bpo);
+    std::vector<dev::HWork> twork;
+    std::vector<long long> tin, tout;
+    for (int t = 0; t < nt; ++t) {
+      if (mem[t].empty()) continue;
+      const int c0 = (int)tin.size(), m = (int)mem[t].size();
+      for (int p : mem[t]) tin.push_back(bpo[p]), tout.push_back(dl_loff_h[p]);
+      for (int r0 = 0; r0 < hn[t]; r0 += dev::kGM)
+        for (int cc = 0; cc < m; cc += dev::kGN)
+          twork.push_back(dev::HWork{htoff[t], hn[t], hdim[t], r0, cc, m, c0, hldt[t], 0});
+    }
+    hb_twork.upload(twork), hb_tin.upload(tin), hb_tout.upload(tout);
+    hb_ntwork = (int)twork.size();
     hb_Yb.alloc(std::max<long long>(1, Ksys.total_x));
     if ((long long)dl_xloc.n < std::max<long long>(1, dl_nslots)) dl_xloc.alloc(std::max<long long>(1, dl_nslots));
     hb_on = true;
@@ -2729,6 +2773,35 @@ struct Engine {
 
   /// F = sum_s G_s K_s^+ b_s - d  (into out)
   void interface_rhs(double* out) {
+    if (hb_on && !std::getenv("PF_NO_OVERLAP")) {
+      const int np = nown();
+      int maxn = 0;
+      for (auto& k : ksym) maxn = std::max(maxn, k.n);
+      // K^+ b for the back-substitution on the low-priority stream, overlapped
+      // with the Krylov loop (back_substitute waits for it)
+      PF_CUDA_CHECK(cudaEventRecord(hb_ev0, st));
+      PF_CUDA_CHECK(cudaStreamWaitEvent(hb_st, hb_ev0, 0));
+      dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, hb_st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
+                                                                   Ksys.d_prob_perm.p, Ksys.d_perm.p, bvec.p, Ksys.X.p, 1);
+      if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, hb_st>>>(nfix, d_fixpos.p, Ksys.X.p);
+      Ksys.solve(hb_st, 1);
+      PF_CUDA_CHECK(cudaEventRecord(hb_ev1, hb_st));
+      hb_pending = true;
+      ::pf::g_launches += 1 + (nfix ? 1 : 0);
+      // F = sum_s H_t^T b_s - d on the engine stream (H_t's rows at fixing dofs are zero)
+      const int n = D.n_lambda;
+      dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, hb_bpo.p, d_subvec(), Ksys.d_prob_n.p,
+                                                                Ksys.d_prob_perm.p, Ksys.d_perm.p, bvec.p, hb_Bp.p, 1);
+      ::pf::g_launches++;
+      launch_pdl(dev::k_h_gemm, hb_ntwork, dev::kGThreads, 0, st, hb_twork.p, hb_HT.p, hb_tin.p, hb_tout.p, hb_Bp.p,
+                 (const double*)nullptr, dl_Y.p);
+      launch_pdl(dev::k_local_reduce, cdiv(n, 256), 256, 0, st, n, dl_rptr.p, dl_rslot.p, dl_Y.p, out, 1.0, 1,
+                 dl_nslots);
+      dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, dvec.p, 1.0, out);
+      ::pf::g_launches++;
+      reduce(out, n);
+      return;
+    }
     perm_in_K(bvec.p);
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
@@ -2761,9 +2834,15 @@ struct Engine {
   /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> state
   void back_substitute(const double* lambda) {
     if (hb_on) {
+      const double* yb = hb_Yb.p;
+      if (hb_pending) {  // K^+ b from the overlapped sweep, in place in Ksys.X
+        PF_CUDA_CHECK(cudaStreamWaitEvent(st, hb_ev1, 0));
+        hb_pending = false;
+        yb = Ksys.X.p;
+      }
       launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, lambda, dl_xloc.p);
       launch_pdl(dev::k_h_gemm, hb_nwork, dev::kGThreads, 0, st, hb_work.p, hb_H.p, hb_cin.p, hb_cout.p, dl_xloc.p,
-                 hb_Yb.p, Ksys.X.p);
+                 yb, Ksys.X.p);
       perm_out_K(state.p);
       if (nc && nfloat_local)
         dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
