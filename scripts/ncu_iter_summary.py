@@ -18,7 +18,7 @@ for r in rows:
 L = [dict(id=i, kernel=v['kernel'], grid=v['grid'], us=v.get('gpu__time_duration.sum', 0) / 1e3,
           dram_mb=(v.get('dram__bytes_read.sum', 0) + v.get('dram__bytes_write.sum', 0)) / 1e6)
      for i, v in cur.items()]
-ends = [j for j, l in enumerate(L) if l['kernel'] == 'k_sqmr_dx_s']
+ends = [j for j, l in enumerate(L) if l['kernel'] == (sys.argv[4] if len(sys.argv) > 4 else 'k_sqmr_dx_s')]
 a, b = ends[-3] + 1, ends[-2] + 1  # one full steady-state iteration
 it = L[a:b]
 tot = sum(l['us'] for l in it)
