@@ -31,7 +31,7 @@ __all__ = [
     "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
     "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
-    "convergence_study", "write_error_csv", "pinned_empty",
+    "convergence_study", "write_error_csv", "write_solver_log_csv", "pinned_empty",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -514,13 +514,38 @@ def convergence_study(mesh_sizes=(8, 16, 24, 32), nus=(0.2, 0.49, 0.499, 0.4999)
     return rows
 
 
+def _num(v):
+    """detail::num (io.hpp:23-27): %.12g."""
+    return "%.12g" % v
+
+
 def write_error_csv(rows, path):
-    """CSV with the fixed header nu,h,err_u,order_u,err_p,order_p."""
+    """write_error_table_csv (io.hpp:96-106): header nu,h,err_u,order_u,err_p,order_p
+    (SPEC.md:527); non-finite orders (the first row of each nu) left empty."""
+    import math
     with open(path, "w") as f:
         f.write("nu,h,err_u,order_u,err_p,order_p\n")
         for r in rows:
-            f.write(f"{r['nu']:.17g},{r['h']:.17g},{r['err_u']:.17g},{r['order_u']:.17g},"
-                    f"{r['err_p']:.17g},{r['order_p']:.17g}\n")
+            ou = _num(r["order_u"]) if math.isfinite(r["order_u"]) else ""
+            op = _num(r["order_p"]) if math.isfinite(r["order_p"]) else ""
+            f.write(f"{_num(r['nu'])},{_num(r['h'])},{_num(r['err_u'])},{ou},{_num(r['err_p'])},{op}\n")
+
+
+VARIANT_NAMES = {"generalized": "feti-generalized", "dirichlet": "feti-schur",
+                 "generalized-mortar": "feti-generalized-mortar", "dirichlet-mortar": "feti-schur-mortar",
+                 "identity": "feti-identity"}
+
+
+def write_solver_log_csv(reports, path, precond="dirichlet"):
+    """write_solver_log_csv (io.hpp:108-114): step,variant,iterations,residual,
+    time_p,time_e per step report.  The reference's time_P / time_E are the
+    seconds of its two subdomain solves; here every subdomain runs in one
+    launch, so time_p carries the step's device seconds and time_e 0."""
+    with open(path, "w") as f:
+        f.write("step,variant,iterations,residual,time_p,time_e\n")
+        for r in reports:
+            f.write(f"{r['step']},{VARIANT_NAMES.get(precond, precond)},{r['iterations']},"
+                    f"{_num(r['rel_residual'])},{_num(r['seconds'])},{_num(0.0)}\n")
 
 
 def debug_factor_solve(A, ic, b, mode=1, task_cap=4096):

@@ -161,6 +161,19 @@ def test_error_csv_header(tmp_path):
     pf.write_error_csv(rows, str(p))
     lines = p.read_text().splitlines()
     assert lines[0] == "nu,h,err_u,order_u,err_p,order_p" and len(lines) == 2
+    assert lines[1] == "0.2,0.125,0.001,,0.002,"  # io.hpp:100-104: %.12g, empty non-finite orders
+
+
+def test_solver_log_csv(tmp_path):
+    import paper_2509_06673_b200 as pf
+
+    reps = [{"step": 1, "iterations": 51, "rel_residual": 9.5e-11, "seconds": 0.0021},
+            {"step": 2, "iterations": 49, "rel_residual": 8.0e-11, "seconds": 0.002}]
+    p = tmp_path / "log.csv"
+    pf.write_solver_log_csv(reps, str(p), "dirichlet")
+    lines = p.read_text().splitlines()
+    assert lines[0] == "step,variant,iterations,residual,time_p,time_e"
+    assert lines[1] == "1,feti-schur,51,9.5e-11,0.0021,0" and len(lines) == 3
 
 
 @pytest.mark.gpu
