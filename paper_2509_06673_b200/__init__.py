@@ -31,7 +31,7 @@ __all__ = [
     "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
     "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
-    "convergence_study", "write_error_csv", "write_solver_log_csv", "pinned_empty",
+    "convergence_study", "write_error_csv", "write_solver_log_csv", "write_solution_vtk", "pinned_empty",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -324,6 +324,12 @@ class FetiOperator:
         _check(lib().pf_pressure_range(self.h, C.byref(lo), C.byref(hi)), self.h)
         return lo.value, hi.value
 
+    def write_vtk(self, path):
+        """write_solution_vtk (io.hpp:48-86) of the current state."""
+        xs, _ = self.state()
+        kw = {k: getattr(self.cfg, k) for k in ("mesh_n", "SX", "SY")}
+        write_solution_vtk(kw, self.subs, xs, lib().pf_current_step(self.h), path, ids=self.owned)
+
     def fields(self, xs):
         out = []
         for S, x in zip(self.subs, xs):
@@ -546,6 +552,52 @@ def write_solver_log_csv(reports, path, precond="dirichlet"):
         for r in reports:
             f.write(f"{r['step']},{VARIANT_NAMES.get(precond, precond)},{r['iterations']},"
                     f"{_num(r['rel_residual'])},{_num(r['seconds'])},{_num(0.0)}\n")
+
+
+def write_solution_vtk(cfg, subs, xs, step, path, ids=None):
+    """write_solution_vtk (io.hpp:48-86) for a partition: every subdomain's
+    triangulation appended (vertices row-major bottom to top, cells split
+    (a,b,c),(a,c,d), mesh.hpp:104-131), point data subsampled to the vertices
+    (P2 midside values dropped); displacement on every point, pressure and
+    fluid content zero on elastic points, elastic pressure xi on both.
+    cfg: make_config keywords; subs: per-subdomain info (region, n_u, n_s,
+    off_eta, off_xi, off_p) in subdomain order s = sy*SX + sx; xs: the
+    subdomains' saddle vectors (FetiOperator.state or the oracle's); ids: their
+    subdomain indices (default 0..len-1; a shard passes its owned list)."""
+    n, SX, SY = int(cfg["mesh_n"]), int(cfg["SX"]), int(cfg["SY"])
+    cx, cy = n // SX, n // SY
+    nvs = (cx + 1) * (cy + 1)
+    pts, cells, disp, pres, xi, eta = [], [], [], [], [], []
+    for k, (S, x) in enumerate(zip(subs, xs)):
+        s = ids[k] if ids is not None else k
+        sx, sy = s % SX, s // SX
+        base = len(pts)
+        for j in range(cy + 1):
+            for i in range(cx + 1):
+                pts.append(((sx * cx + i) / n, (sy * cy + j) / n))
+        for j in range(cy):
+            for i in range(cx):
+                a = base + j * (cx + 1) + i
+                b, c, d = a + 1, a + cx + 2, a + cx + 1
+                cells += [(a, b, c), (a, c, d)]
+        u = x[:S["n_u"]]
+        disp += [(u[2 * v], u[2 * v + 1]) for v in range(nvs)]
+        xi += list(x[S["off_xi"]:S["off_xi"] + nvs])
+        P = S["region"] == 0
+        pres += list(x[S["off_p"]:S["off_p"] + nvs]) if P else [0.0] * nvs
+        eta += list(x[S["off_eta"]:S["off_eta"] + nvs]) if P else [0.0] * nvs
+    with open(path, "w") as f:
+        f.write(f"# vtk DataFile Version 3.0\nporofeti solution step {step}\nASCII\nDATASET UNSTRUCTURED_GRID\n")
+        f.write(f"POINTS {len(pts)} double\n")
+        f.writelines(f"{_num(px)} {_num(py)} 0\n" for px, py in pts)
+        f.write(f"CELLS {len(cells)} {4 * len(cells)}\n")
+        f.writelines(f"3 {a} {b} {c}\n" for a, b, c in cells)
+        f.write(f"CELL_TYPES {len(cells)}\n" + "5\n" * len(cells))
+        f.write(f"POINT_DATA {len(pts)}\nVECTORS displacement double\n")
+        f.writelines(f"{_num(ux)} {_num(uy)} 0\n" for ux, uy in disp)
+        for name, vals in (("pressure", pres), ("elastic_pressure", xi), ("fluid_content", eta)):
+            f.write(f"SCALARS {name} double 1\nLOOKUP_TABLE default\n")
+            f.writelines(f"{_num(v)}\n" for v in vals)
 
 
 def debug_factor_solve(A, ic, b, mode=1, task_cap=4096):

@@ -217,3 +217,52 @@ def test_convergence_study_driver():
         eu = max(o.errors(k)[0] for k in (1, 2))
         ep = max(o.errors(k)[1] for k in (1, 2))
         assert abs(r["err_u"] - eu) <= 1e-6 * eu and abs(r["err_p"] - ep) <= 1e-6 * ep
+
+
+@pytest.mark.parametrize("kw", [mms_t(8, 1, steps=1), dict(mms_t(8, 2, steps=1), SX=2, SY=2, precond="dirichlet-mortar")])
+def test_solution_vtk_writer(kw, tmp_path):
+    """write_solution_vtk (io.hpp:48-86) on an oracle state: counts, the
+    vertex-subsampled displacement and the P-only pressure."""
+    import paper_2509_06673_b200 as pf
+
+    o = Oracle(**kw)
+    o.run(1)
+    xs, _ = o.state(1)
+    p = tmp_path / "s.vtk"
+    pf.write_solution_vtk(kw, o.subs, xs, 1, str(p))
+    lines = p.read_text().splitlines()
+    nsub = kw["SX"] * kw["SY"]
+    cx, cy = 8 // kw["SX"], 8 // kw["SY"]
+    nv, nt = nsub * (cx + 1) * (cy + 1), nsub * 2 * cx * cy
+    assert lines[1] == "porofeti solution step 1" and lines[4] == f"POINTS {nv} double"
+    assert lines[5 + nv] == f"CELLS {nt} {4 * nt}"
+    i = lines.index("VECTORS displacement double")
+    S0, S1 = o.subs[0], o.subs[-1]
+    ux, uy, _ = (float(v) for v in lines[i + 1 + 3].split())  # subdomain 0, vertex 3
+    assert abs(ux - xs[0][6]) <= 1e-11 * max(1.0, abs(xs[0][6])) and abs(uy - xs[0][7]) <= 1e-11 * max(1.0, abs(xs[0][7]))
+    j = lines.index("SCALARS pressure double 1")
+    assert abs(float(lines[j + 2 + 5]) - xs[0][S0["off_p"] + 5]) <= 1e-11 * max(1.0, abs(xs[0][S0["off_p"] + 5]))
+    assert S1["region"] == 1 and float(lines[j + 2 + nv - 1]) == 0.0  # elastic points carry no pressure
+
+
+@pytest.mark.gpu
+def test_device_vtk_matches_oracle(tmp_path):
+    """FetiOperator.write_vtk of the device state against the same writer on
+    the oracle's state (config-1 layout, one step)."""
+    import paper_2509_06673_b200 as pf
+
+    kw = mms_t(16, 2, steps=1)
+    op = pf.FetiOperator(**kw)
+    op.step()
+    op.write_vtk(str(tmp_path / "d.vtk"))
+    o = Oracle(**kw)
+    o.run(1)
+    xs, _ = o.state(1)
+    pf.write_solution_vtk(kw, o.subs, xs, 1, str(tmp_path / "o.vtk"))
+    a = (tmp_path / "d.vtk").read_text().split()
+    b = (tmp_path / "o.vtk").read_text().split()
+    assert len(a) == len(b)
+    scale = max(abs(float(t)) for t in b if t.replace(".", "").replace("-", "").replace("e", "").isdigit())
+    for x, y in zip(a, b):
+        if x != y:
+            assert abs(float(x) - float(y)) <= 1e-8 * scale, (x, y)
