@@ -31,7 +31,7 @@ __all__ = [
     "Config", "make_config", "BASELINE_CONFIGS", "FetiOperator", "StepSolver", "run_simulation",
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
     "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
-    "convergence_study", "write_error_csv", "write_solver_log_csv", "write_solution_vtk", "pinned_empty",
+    "convergence_study", "write_error_csv", "write_solver_log_csv", "write_solution_vtk", "barry_mercer_check", "pinned_empty",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -464,6 +464,27 @@ def oscillation_check(ranges, max_boundary, delta):
     if hi > rep["upper_bound"] and hi - rep["upper_bound"] > worst:
         rep["worst_violation"], rep["pass"] = hi, False
     return rep
+
+
+def barry_mercer_check(mesh_n=16, order=2, dt=1e-2, T=None, bound_frac=0.05, E=1e4, nu=0.2, c0=0.1, **kw):
+    """The paper's Barry-Mercer oscillation study (model.hpp:274-324 +
+    verify.hpp:160-195; h = 1/16, tau = 1e-2, bound 0.05 max|p2|)
+    on the device: runs the reference layout, reads the nodal pressure range
+    after every step (pf_pressure_range, no state download) and applies
+    oscillation_check with max_boundary = max_t |sin t| over the steps."""
+    import math
+    steps = max(1, int(round((T if T is not None else 10 * dt) / dt)))
+    op = FetiOperator(**dict(dict(mesh_n=mesh_n, SX=1, SY=2, order=order, scenario="barry-mercer", E=E, nu=nu,
+                                  c0=c0, dt=dt, steps=steps, precond="dirichlet"), **kw))
+    try:
+        ranges = []
+        for _ in range(steps):
+            op.step()
+            ranges.append(op.pressure_range())
+    finally:
+        op.close()
+    max_bnd = max(abs(math.sin(k * dt)) for k in range(1, steps + 1))
+    return oscillation_check(ranges, max_bnd, bound_frac * max_bnd)
 
 
 def estimate_order(err_coarse, err_fine, h_coarse, h_fine):

@@ -198,6 +198,8 @@ def test_barry_mercer_pressure_range_and_oscillation_check():
     max_bnd = max(abs(math.sin(k * kw["dt"])) for k in range(1, kw["steps"] + 1))
     rep = pf.oscillation_check(ranges, max_bnd, 0.05 * max_bnd)
     assert rep["pass"], rep
+    rep2 = pf.barry_mercer_check(mesh_n=16, dt=1e-2, T=0.1)  # the study driver: same run, same verdict
+    assert rep2["pass"] and rep2["min_p"] == rep["min_p"] and rep2["max_p"] == rep["max_p"], (rep, rep2)
 
 
 @pytest.mark.gpu
