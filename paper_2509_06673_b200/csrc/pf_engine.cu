@@ -2520,7 +2520,19 @@ struct Engine {
     qsolve(r, kr_tmp.p);
     precond_raw(kr_tmp.p, z);
     qsolve(z, z);
+    // ablation (diagnostics only): repeat a component on scratch output so its
+    // marginal in-graph cost shows in the step time; results are unchanged
+    static const int dup = std::getenv("PF_DUP") ? std::atoi(std::getenv("PF_DUP")) : 0;
+    if (dup) {
+      if (!kr_dup.p) kr_dup.alloc(D.n_lambda);
+      if (dup == 1) qsolve(r, kr_dup.p);                               // one more mortar Gram solve
+      if (dup == 2) dual_local(true, kr_tmp.p);                       // one more local product (gather+GEMM)
+      if (dup == 3) coarse_gemv(r, kr_dup.p);                          // one more dense coarse GEMV
+      if (dup == 4) launch_pdl(dev::k_xpay_s, cdiv(D.n_lambda, 256), 256, 0, st, D.n_lambda, (const double*)r,
+                               kr_dup.p, (const double*)(scal.p + dev::KS_B));  // one more tiny vector kernel
+    }
   }
+  DevBuf<double> kr_dup;
 
   /// sc[slot] = <a, b> (+ the element update of `mode`) and the scalar update
   /// `sop`, one launch (k_dot_fused); DOT_PROJ finishes the coarse projection
