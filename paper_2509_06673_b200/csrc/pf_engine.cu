@@ -2530,6 +2530,7 @@ struct Engine {
       if (dup == 3) coarse_gemv(r, kr_dup.p);                          // one more dense coarse GEMV
       if (dup == 4) launch_pdl(dev::k_xpay_s, cdiv(D.n_lambda, 256), 256, 0, st, D.n_lambda, (const double*)r,
                                kr_dup.p, (const double*)(scal.p + dev::KS_B));  // one more tiny vector kernel
+      if (dup == 5) fdot(dev::DOT_PLAIN, r, kr_tmp.p, 60, dev::SOP_NONE);  // one more fused dot (scratch slot)
     }
   }
   DevBuf<double> kr_dup;

@@ -11,6 +11,6 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
     r = op.step()
     print(f"DUP {os.environ.get('PF_DUP', '0')} step {ms/3:.2f} ms it {it/3:.0f} per-iter {r['t_krylov']*1e6/r['iterations']:.1f} us", flush=True)
     sys.exit(0)
-for d in ["0", "1", "2", "3", "4", "0"]:
+for d in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["0", "1", "2", "3", "4", "5", "0"]):
     out = subprocess.run([sys.executable, __file__, "run"], env=dict(os.environ, PF_DUP=d), capture_output=True, text=True)
     print([l for l in out.stdout.splitlines() if l.startswith("DUP")] or out.stderr[-300:], flush=True)
