@@ -776,7 +776,10 @@ struct SolveSystem {
           if (ustage[u] == stg) maxin = std::max(maxin, nin[dir * nu + u]);
         db_split[dir][stg] = maxin > 128 ? 4 : 1;
         // one slice: 64-row blocks (small level-0 units leave fewer idle threads)
-        db_rb[dir][stg] = db_split[dir][stg] == 1 ? 64 : dev::kUnitRows;
+        // (4 slices, 64 rows) for the subtree stage: -4 us per c4 iteration in
+        // the graph against (4, 128) (scripts/qu_ingraph.sh; the standalone
+        // solve does not show it)
+        db_rb[dir][stg] = 64;
         {  // tuning overrides PF_QU_S<stage>, PF_QU_R<stage>
           char nm[16];
           std::snprintf(nm, sizeof nm, "PF_QU_S%d", stg);
