@@ -2251,7 +2251,7 @@ struct Engine {
         const char* v = std::getenv(k);
         return v ? std::atoll(v) : d;
       };
-      qsym = analyse(A, D.lambda_ic, envi("PF_Q_CAP", 1024), (int)envi("PF_Q_WS", 256), 0.15, 16,
+      qsym = analyse(A, D.lambda_ic, envi("PF_Q_CAP", 256), (int)envi("PF_Q_WS", 256), 0.15, 16,
                      (int)envi("PF_Q_LEAF", 8));
     }
     Qsys.build({&qsym}, {0}, 1);
