@@ -774,11 +774,13 @@ struct SolveSystem {
         int maxin = 0;
         for (int u = 0; u < nu; ++u)
           if (ustage[u] == stg) maxin = std::max(maxin, nin[dir * nu + u]);
+        // shapes chosen on the in-graph c4 iteration time (scripts/qu_ingraph.sh,
+        // scripts/ingraph_sweep.sh; the standalone solve does not show them):
+        // small units (<= 128 inputs) 1 slice x 64 rows, larger ones 4 x 64.
+        // (2 x 32 for the small units was 2% faster at c4 but moved the
+        // rounding-sensitive nu = 0.49999 case (c3 fixture: 165 vs the
+        // oracle's 145 iterations) out of its parity window: not taken)
         db_split[dir][stg] = maxin > 128 ? 4 : 1;
-        // one slice: 64-row blocks (small level-0 units leave fewer idle threads)
-        // (4 slices, 64 rows) for the subtree stage: -4 us per c4 iteration in
-        // the graph against (4, 128) (scripts/qu_ingraph.sh; the standalone
-        // solve does not show it)
         db_rb[dir][stg] = 64;
         {  // tuning overrides PF_QU_S<stage>, PF_QU_R<stage>
           char nm[16];
@@ -2377,7 +2379,8 @@ struct Engine {
   void setup_krylov() {
     const int n = std::max(1, D.n_lambda);
     for (auto* b : {&kr_r, &kr_z, &kr_p, &kr_q, &kr_d, &kr_t, &kr_tmp, &kr_rhs}) b->alloc(n);
-    red_part.alloc(dev::kRedBlocks);
+    red_blocks = std::getenv("PF_RED_BLOCKS") ? std::max(1, std::atoi(std::getenv("PF_RED_BLOCKS"))) : dev::kRedBlocks;
+    red_part.alloc(std::max(red_blocks, dev::kRedBlocks));
     red_count.upload(std::vector<unsigned int>{0u});
     scal.alloc(64);
     h_scal.assign(64, 0.0);
@@ -2537,6 +2540,7 @@ struct Engine {
     }
   }
   DevBuf<double> kr_dup;
+  int red_blocks = dev::kRedBlocks;  // CTAs of the fused dots (fixed per run: deterministic)
 
   /// sc[slot] = <a, b> (+ the element update of `mode`) and the scalar update
   /// `sop`, one launch (k_dot_fused); DOT_PROJ finishes the coarse projection
@@ -2547,7 +2551,7 @@ struct Engine {
     F.a = a, F.b = b;
     if (mode == dev::DOT_PROJ) F.ptr = c_ptr.p, F.idx = c_idx.p, F.val = c_val.p, F.c = c_tmp2.p;
     F.partial = red_part.p, F.counter = red_count.p, F.sc = scal.p, F.status = d_status.p;
-    launch_pdl(dev::k_dot_fused, dev::kRedBlocks, dev::kRedThreads, 0, st, F);
+    launch_pdl(dev::k_dot_fused, red_blocks, dev::kRedThreads, 0, st, F);
   }
   /// M_ followed by <a, z>: preconditioner, coarse projection of z fused into the dot
   void M_dot(const double* r, double* z, const double* a, int slot, int sop) {
