@@ -848,8 +848,9 @@ struct SolveSystem {
                d_fold_ptr.p + d_types_host[0].fold_base, d_fold_idx.p + d_types_host[0].foldidx_base, CB.p, b, perm,
                Wres.p);
     // twelve warps per CTA, about one CTA per SM: every row's warp co-resident
-    launch_pdl(dev::k_dense_top_gemv, cdiv(ntop, 12), 384, sizeof(double) * ntop, st, ntop, top_c0, W.p, Wres.p, X.p,
-               perm, x, nullptr, nullptr, nullptr, 0, nullptr);
+    static const int tw = std::getenv("PF_TOP_WARPS") ? std::clamp(std::atoi(std::getenv("PF_TOP_WARPS")), 1, 16) : 12;
+    launch_pdl(dev::k_dense_top_gemv, cdiv(ntop, tw), 32 * tw, sizeof(double) * ntop, st, ntop, top_c0, W.p, Wres.p,
+               X.p, perm, x, nullptr, nullptr, nullptr, 0, nullptr);
     launches += 2;
     if (timed) cudaEventRecord(ev[2], st);
     units(1, 1);
@@ -2563,7 +2564,10 @@ struct Engine {
 
   /// y = (G_c^T G_c)^{-1} x (dense inverse, warp per row)
   void coarse_gemv(const double* x, double* y) {
-    launch_pdl(dev::k_dense_gemv_w, std::min(cdiv(nc, 8), 4 * 148), 256, sizeof(double) * nc, st, nc, c_ainv.p, x, y);
+    // warp per row (fixed summation order whatever the CTA shape)
+    static const int cw = std::getenv("PF_COARSE_WARPS") ? std::clamp(std::atoi(std::getenv("PF_COARSE_WARPS")), 1, 8) : 8;
+    launch_pdl(dev::k_dense_gemv_w, std::min(cdiv(nc, cw), 4 * 148), 32 * cw, sizeof(double) * nc, st, nc, c_ainv.p, x,
+               y);
   }
   /// y = (G_c^T G_c)^{-1} G_c^T v
   void coarse_solve(const double* v, double* y) {

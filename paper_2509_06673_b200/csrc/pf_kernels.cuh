@@ -521,8 +521,8 @@ __global__ void __launch_bounds__(256) k_dense_gemv_w(int n, const double* __res
   extern __shared__ double xs[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int row = blockIdx.x * 8 + warp; row < n; row += gridDim.x * 8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = blockIdx.x * nw + warp; row < n; row += gridDim.x * nw) {
     const double v = warp_row_dot(A + (size_t)row * n, xs, n, lane);
     if (lane == 0) y[row] = v;
   }
