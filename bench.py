@@ -235,8 +235,10 @@ def run_ours(args, rank, world, dist):
         cur_k = rep["step"]
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_s = reduce_max(dist, e2e_s)
-    h2d = x_cat.nbytes + lam.nbytes
-    d2h = h2d
+    # pf_advance uploads the inputs a step reads (eta^{n-1}, lambda^{n-1}) and
+    # downloads the whole next state
+    h2d = int(pf.lib().pf_last_h2d_bytes(op.h))
+    d2h = x_cat.nbytes + lam.nbytes
     # dominant kernel (factor sweeps of the F-apply), CUDA events, live
     # F-applies/s from 200 back-to-back applies after 20 warm-up calls
     ms_apply, sweep_ms, launches = op.bench(0, 20, 200)
@@ -315,7 +317,7 @@ def run_ours(args, rank, world, dist):
         "f_applies_per_s_microbench": 1e3 / ms_apply,
         "sweep_phase_ms": ph,
         "e2e": {"value": e2e_s, "unit": "s/step", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "host_buffers": "page-locked (pf_host_alloc), caller-owned, through pf_advance"},
+                "host_buffers": "page-locked (pf_host_alloc), caller-owned, through pf_advance (uploads eta^{n-1} and lambda^{n-1}, downloads the full state)"},
         "roofline": dict({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
                           "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src}, **roof_extra),

@@ -162,6 +162,8 @@ int pf_get_state_all(pf_ctx* ctx, double* x_cat);
 int pf_get_lambda(pf_ctx* ctx, double* lambda);
 int pf_set_state(pf_ctx* ctx, const double* x_cat, const double* lambda, int step);
 int pf_current_step(const pf_ctx* ctx);
+/* bytes pf_advance copied host -> device in its last call (the eta blocks and lambda) */
+long long pf_last_h2d_bytes(const pf_ctx* ctx);
 
 /* Spatial L2 errors of the current state against the scenario's exact
  * solution — verify.hpp:62-74 (snapshot_u_error: u over every subdomain;

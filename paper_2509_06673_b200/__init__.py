@@ -187,6 +187,8 @@ def lib():
         L.pf_get_lambda.argtypes = [vp, vp]
         L.pf_set_state.argtypes = [vp, vp, vp, C.c_int]
         L.pf_current_step.argtypes = [vp]
+        L.pf_last_h2d_bytes.argtypes = [vp]
+        L.pf_last_h2d_bytes.restype = C.c_longlong
         L.pf_errors.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pf_pressure_range.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pf_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
