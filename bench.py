@@ -12,10 +12,16 @@ back-substitution.  Inputs (factors, ~16 GB) are far larger than L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
---impl reference times the reference's CPU path on the host cores: the
-reference (Eigen-based, /root/reference/proj) cannot be compiled in this image,
-so the C++ oracle restatement (oracle/, all host threads) runs a bounded
-sample of the same workload (see cpu_sample()).
+--impl reference times the reference's CPU path on the host cores: the C++
+oracle restatement of the reference algorithm (oracle/, all host threads; the
+reference itself needs Eigen, absent from the GPU image -- oracle/_ref pins
+the restatement to it) runs real time steps of the full workload, timed with
+steady_clock per step (run_reference()).  The cpu_baseline object of the
+default arm is a bounded sample (cpu_sample(): one F-apply + preconditioner on
+4x4 subdomains, scaled), marked "estimated"; profiles/ holds the measured
+full steps it is checked against.
+--gpus N > 1 without torchrun: the script re-executes itself under
+torch.distributed.run with N local ranks (one process per GPU).
 """
 from __future__ import annotations
 
@@ -82,6 +88,19 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def spawn(n):
+    """Re-execute this script under torch.distributed.run with n local ranks
+    (rendezvous on 127.0.0.1, a free port); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def dist_init(n):
@@ -159,27 +178,57 @@ def workload_name(cfg_name):
 
 
 def run_reference(args, rank, world, dist):
+    """The reference's CPU path, timed: the oracle (C++ restatement of the
+    reference algorithm, all host threads) runs REAL time steps of the full
+    workload -- StepSolver::advance (timeloop.hpp:150-186) with
+    std::chrono::steady_clock around each step, REF's own clock (feti.hpp:103)
+    -- after its setup (assembly + factorisation, reported separately).  A CPU
+    step of c4 takes minutes, so the timed steps are capped by a wall budget
+    (--ref-budget seconds, at least one step): "steps" is the number actually
+    timed, "steps_requested" the --steps asked for."""
     if rank != 0:
         return
-    W = max(args.warmup, 0)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
     import paper_2509_06673_b200 as pf  # noqa: F401 (config table only)
-    # the workload's Krylov iterations per step: measured on the device arm (the
-    # parity tests hold the oracle to the same count within +-2 / 5%)
-    iters_per_step = args.iters_hint if args.iters_hint else ITERS_PER_STEP[args.config]
-    vals = []
-    for k in range(W + args.steps):
-        s = cpu_sample(args.config, iters_per_step)
-        v = (iters_per_step + 2) * s["t_fapply_full"] + iters_per_step * (s["t_iter_full"] - s["t_fapply_full"])
-        if k >= W:
-            vals.append(v)
-    value = statistics.mean(vals)
+
+    kw = dict(pf.BASELINE_CONFIGS[args.config])
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    o = ol.Oracle(**dict(kw, threads=threads))
+    setup_s = time.perf_counter() - t0
+    # untimed warm-up: one step (first-touch of the factor pages); more only if cheap
+    t0 = time.perf_counter()
+    o.run(1)
+    first = o.report(1)["seconds"]
+    W = 1
+    budget = args.ref_budget
+    while W < args.warmup and first * (W + 1) < 0.25 * budget:
+        o.run(1)
+        W += 1
+    timed, iters = [], []
+    t_start = time.perf_counter()
+    while len(timed) < args.steps and W + len(timed) < kw["steps"]:
+        if timed and (time.perf_counter() - t_start) + statistics.mean(timed) > budget:
+            break
+        o.run(1)
+        rep = o.report(W + len(timed) + 1)
+        timed.append(rep["seconds"])
+        iters.append(rep["iterations"])
+    value = statistics.mean(timed)
+    sample = (f"oracle (C++ restatement of the reference algorithm: per-subdomain sparse LDL^T solves, "
+              f"{threads} threads over subdomains) on the full {args.config} workload; {len(timed)} time steps "
+              f"timed after {W} untimed (steady_clock around each advance), setup {setup_s:.1f} s not included")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/step", "n_gpus": world,
-            "steps": args.steps, "warmup": W, "ms_per_step": value * 1e3, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured solution)",
-            "config": {"workload": workload_name(args.config), "kernel": "CPU oracle (C++ restatement of the "
-                       "reference algorithm; the reference needs Eigen, absent here)"},
-            "cpu_baseline": {"value": value, "unit": "s/step", "cores": s["threads"], "kind": "port",
-                             "sample": s["sample"]},
+            "steps": len(timed), "steps_requested": args.steps, "warmup": W, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (manufactured solution)",
+            "config": {"workload": workload_name(args.config),
+                       "kernel": "CPU oracle (C++ restatement of the reference algorithm; the reference needs "
+                                 "Eigen, absent here -- oracle/_ref pins the restatement to it on small cases)"},
+            "step_seconds": timed, "median_s": statistics.median(timed), "iterations": iters,
+            "setup_s": setup_s,
+            "cpu_baseline": {"value": value, "unit": "s/step", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "s/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -189,9 +238,13 @@ def run_ours(args, rank, world, dist):
     import paper_2509_06673_b200 as pf
 
     kw = dict(pf.BASELINE_CONFIGS[args.config])
-    kw["steps"] = max(kw["steps"], args.warmup + args.steps + 1)
+    kw["steps"] = max(kw["steps"], args.warmup + 2 * args.steps + 1)  # timed steps, then the e2e steps
     t0 = time.perf_counter()
     if world > 1:
+        import torch
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} visible GPU(s); "
+                             "one process per GPU is required")
         # sharded engine: subdomains split over ranks, lambda partial sums by
         # ncclAllReduce on each engine's stream (the engine selects GPU LOCAL_RANK)
         import torch
@@ -221,8 +274,7 @@ def run_ours(args, rank, world, dist):
     x_cat = np.concatenate(xs)
     step_idx = pf.lib().pf_current_step(op.h)
     solver = pf.StepSolver(op)
-    e2e_steps = max(1, min(args.steps, 3))
-    # keep within the configured number of time steps: rewind to the warm-up state
+    e2e_steps = args.steps  # the same K steps as `value`
     # page-locked host buffers (ping-pong): the caller's state in pinned memory
     pin = [[pf.pinned_empty(n) for n in (x_cat.size, lam.size)] for _ in range(2)]
     pin[0][0][:] = x_cat
@@ -347,7 +399,9 @@ def run_ours(args, rank, world, dist):
             s = cpu_sample(args.config, iters_per_step)
             v = (iters_per_step + 2) * s["t_fapply_full"] + iters_per_step * (s["t_iter_full"] - s["t_fapply_full"])
             line["cpu_baseline"] = {"value": v, "unit": "s/step", "cores": s["threads"], "kind": "port",
-                                    "sample": s["sample"]}
+                                    "sample": s["sample"], "estimated": True,
+                                    "measured_full_steps": "bench.py --impl reference (real steps of the full "
+                                                           "workload); profiles/r2_cpu_reference_*.json"}
         except Exception as exc:  # the baseline is reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "s/step", "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc}"}
@@ -364,8 +418,11 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--iters-hint", type=float, default=None)
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: wall seconds for the timed CPU steps (at least one step)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn(args.gpus)  # one process per GPU, started here (no external torchrun needed)
     rank, world, dist = dist_init(args.gpus)
     if args.impl == "reference":
         run_reference(args, rank, world, dist)

@@ -102,6 +102,11 @@ typedef struct pf_report {
   double seconds;     /* device time of the whole advance (CUDA events) */
   double t_rhs, t_krylov, t_back;
   int f_applies, precond_applies;
+  /* ||P(rhs - F lambda)|| / ||P(rhs - F lambda_0)|| of the returned multiplier,
+   * recomputed with one extra F-apply (SQMR: the convergence test itself —
+   * its quasi-residual is only an estimate; PCG: reported beside REF's sqrt(r.z)) */
+  double true_residual;
+  int restarts; /* SQMR: true-residual checks that failed (iteration continued with a tighter estimate threshold) */
 } pf_report;
 
 typedef struct pf_ctx pf_ctx;
@@ -153,7 +158,12 @@ int pf_interface_rhs(pf_ctx* ctx, double* F);
 /* StepSolver::advance (timeloop.hpp:150) on the device-resident state. */
 int pf_step(pf_ctx* ctx, pf_report* rep);
 /* advance with host buffers (the reference signature): prev state in (all
- * subdomains' saddle vectors concatenated + lambda), next state out. */
+ * subdomains' saddle vectors concatenated + lambda), next state out.  Of
+ * prev_x only the eta blocks of the poroelastic subdomains are read (the step's
+ * right-hand side needs eta^{n-1}, assembly.hpp:558) plus prev_lambda (warm
+ * start, timeloop.hpp:168-169); every other entry may hold anything.  On an
+ * error the device-resident state is undefined (neither snapshot) until the
+ * next successful pf_set_state / pf_advance. */
 int pf_advance(pf_ctx* ctx, const double* prev_x, const double* prev_lambda, int prev_step,
                double* next_x, double* next_lambda, pf_report* rep);
 /* state accessors (saddle layout per subdomain; lambda) */

@@ -66,7 +66,19 @@ struct PcgReport {
   int step = 0, iterations = 0;
   bool converged = false;
   double rel_residual = 0.0, seconds = 0.0;
+  double true_residual = 0.0;  // ||P(rhs - F lambda)|| / ||r0||, recomputed at exit
 };
+
+inline PcgReport to_report(const pf_report& r) {
+  return PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds, r.true_residual};
+}
+
+/// every ABI call reads / writes exactly n values: refuse a mismatched buffer
+inline void check_size(const std::vector<double>& v, long long n, const char* what) {
+  if ((long long)v.size() != n)
+    throw ConfigError(std::string(what) + ": expected " + std::to_string(n) + " values, got " +
+                      std::to_string(v.size()));
+}
 
 /// Reference StateSnapshot (state.hpp:8-12): per-subdomain saddle vectors
 /// ([u, eta, xi, p] / [u, xi]) concatenated, plus the multiplier.
@@ -99,11 +111,13 @@ class Problem {
   pf_ctx* handle() const { return ctx_; }
 
   Vector apply(const Vector& x) const {
+    check_size(x, info_.n_lambda, "apply");
     Vector y(info_.n_lambda);
     check(pf_apply(ctx_, x.data(), y.data()), ctx_);
     return y;
   }
   Vector apply_preconditioner(const Vector& r) const {
+    check_size(r, info_.n_lambda, "apply_preconditioner");
     Vector z(info_.n_lambda);
     check(pf_apply_precond(ctx_, r.data(), z.data()), ctx_);
     return z;
@@ -114,6 +128,9 @@ class Problem {
     return F;
   }
   Vector local_solve(int s, Vector b) const {
+    pf_sub_info si{};
+    check(pf_get_sub_info(ctx_, s, &si), ctx_);
+    check_size(b, si.dim, "local_solve");
     check(pf_local_solve(ctx_, s, b.data()), ctx_);
     return b;
   }
@@ -141,6 +158,8 @@ class StepSolver {
  public:
   explicit StepSolver(Problem& p) : p_(&p) {}
   StateSnapshot advance(const StateSnapshot& prev, PcgReport* report = nullptr) const {
+    check_size(prev.x, p_->info().total_dim, "advance: prev.x");
+    check_size(prev.lambda, p_->n_lambda(), "advance: prev.lambda");
     StateSnapshot next;
     next.x.resize(p_->info().total_dim);
     next.lambda.resize(p_->n_lambda());
@@ -148,7 +167,7 @@ class StepSolver {
     check(pf_advance(p_->handle(), prev.x.data(), prev.lambda.data(), prev.step, next.x.data(), next.lambda.data(), &r),
           p_->handle());
     next.step = r.step;
-    if (report) *report = PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds};
+    if (report) *report = to_report(r);
     return next;
   }
 
@@ -162,7 +181,7 @@ inline std::vector<PcgReport> run_simulation(Problem& p) {
   for (int n = 0; n < p.info().N; ++n) {
     pf_report r{};
     check(pf_step(p.handle(), &r), p.handle());
-    out.push_back(PcgReport{r.step, r.iterations, r.converged != 0, r.rel_residual, r.seconds});
+    out.push_back(to_report(r));
   }
   return out;
 }

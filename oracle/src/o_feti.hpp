@@ -63,6 +63,8 @@ struct PcgReport {
   int iterations = 0;
   bool converged = false;
   double rel_residual = 0.0;
+  double true_residual = 0.0;  // ||P(rhs - F lambda)|| / ||P(rhs - F lambda0)|| at exit
+  int restarts = 0;            // SQMR: failed true-residual checks (iteration continued)
   std::vector<double> history;
   double time_solve = 0.0;
 };
@@ -380,6 +382,7 @@ class Feti {
     Vec r = apply(lambda);
     for (std::size_t i = 0; i < r.size(); ++i) r[i] = rhs[i] - r[i];
     project(r);
+    const double tr0 = norm2(r);
     Vec z = precondition(r);
     project(z);
     double rz = dot(r, z);
@@ -415,6 +418,17 @@ class Feti {
       for (std::size_t i = 0; i < p.size(); ++i) p[i] = z[i] + b * p[i];
     }
     rep.rel_residual = rep.history.back() / d0;
+    rep.true_residual = true_residual(rhs, lambda) / tr0;  // reported beside REF's sqrt(r.z)
+  }
+
+  /// ||P(rhs - F lambda)||, recomputed from scratch.
+  double true_residual(const Vec& rhs, const Vec& lambda, Vec* out = nullptr) const {
+    Vec r = apply(lambda);
+    for (std::size_t i = 0; i < r.size(); ++i) r[i] = rhs[i] - r[i];
+    project(r);
+    const double nr = norm2(r);
+    if (out) *out = std::move(r);
+    return nr;
   }
 
   /// Symmetric QMR with a symmetric (indefinite) preconditioner, right
@@ -435,10 +449,17 @@ class Feti {
       rep.converged = true;
       return;
     }
-    Vec q = precondition(r);
-    project(q);
-    double rho = dot(r, q), theta = 0.0;
-    Vec d(n, 0.0);
+    // Lanczos recurrences from the residual in r (first solve and restarts)
+    Vec q, d;
+    double rho = 0.0, theta = 0.0;
+    auto start = [&] {
+      q = precondition(r);
+      project(q);
+      rho = dot(r, q), theta = 0.0;
+      d.assign(n, 0.0);
+    };
+    start();
+    double thr = cfg.tol * t0;  // threshold on the estimate tau_k
     for (int k = 0; k < cfg.max_iter; ++k) {
       Vec t = apply(q);
       project(t);
@@ -457,9 +478,19 @@ class Feti {
       const double est = tau;  // quasi-residual norm (estimate of the QMR residual)
       rep.history.push_back(est);
       rep.iterations = k + 1;
-      if (est <= cfg.tol * t0) {
-        rep.converged = true;
-        break;
+      if (est <= thr) {
+        // confirm on the true residual (||r_k|| <= sqrt(k+1) tau_k only);
+        // above the tolerance: keep iterating, with the estimate's threshold
+        // scaled by the observed true/estimate ratio
+        const double tr = true_residual(rhs, lambda);
+        rep.true_residual = tr / t0;
+        if (tr <= cfg.tol * t0) {
+          rep.converged = true;
+          rep.rel_residual = rep.true_residual;
+          return;
+        }
+        ++rep.restarts;
+        thr = est * (cfg.tol * t0 / tr) * 0.5;
       }
       if (rho == 0.0) throw PcgBreakdownError("sqmr: rho vanished");
       Vec u = precondition(r);

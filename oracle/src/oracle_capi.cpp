@@ -389,6 +389,13 @@ int or_lambda(void* hh, int step, double* l) {
   std::memcpy(l, h->states[step].lambda.data(), sizeof(double) * h->states[step].lambda.size());
   return 0;
 }
+/// true residual ||P(rhs - F lambda)|| / ||r0|| and SQMR restarts of step k>=1
+int or_report_true(void* hh, int step, double* true_res, int* restarts) {
+  auto* h = static_cast<Handle*>(hh);
+  if (step < 1 || step > (int)h->reps.size()) return 4;
+  *true_res = h->reps[step - 1].true_residual, *restarts = h->reps[step - 1].restarts;
+  return 0;
+}
 /// report of step k>=1: iterations, converged, rel_residual, wall seconds; history into hist (may be null)
 int or_report(void* hh, int step, int* iters, int* conv, double* rel, double* secs, double* hist, int* nhist) {
   auto* h = static_cast<Handle*>(hh);

@@ -116,6 +116,7 @@ class Report(C.Structure):
         ("rel_residual", C.c_double), ("seconds", C.c_double),
         ("t_rhs", C.c_double), ("t_krylov", C.c_double), ("t_back", C.c_double),
         ("f_applies", C.c_int), ("precond_applies", C.c_int),
+        ("true_residual", C.c_double), ("restarts", C.c_int),
     ]
 
     def as_dict(self):
@@ -213,6 +214,15 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def _vec(a, n, what, copy=False):
+    """Contiguous float64 copy/view of `a`, checked to hold exactly n values
+    (every ABI call reads or writes exactly that many)."""
+    a = np.array(a, np.float64) if copy else np.ascontiguousarray(a, np.float64)
+    if a.ndim != 1 or a.size != n:
+        raise ConfigError(f"{what}: expected a vector of {n} values, got shape {a.shape}")
+    return a
+
+
 def _check(code, ctx=None):
     if code != 0:
         msg = lib().pf_last_error(ctx).decode(errors="replace")
@@ -265,24 +275,26 @@ class FetiOperator:
 
     # --- reference FetiOperator surface ---
     def apply(self, x):
-        x = np.ascontiguousarray(x, np.float64)
+        x = _vec(x, self.n_lambda, "apply")
         y = np.empty(self.n_lambda)
         _check(lib().pf_apply(self.h, _ptr(x), _ptr(y)), self.h)
         return y
 
     def apply_preconditioner(self, r):
-        r = np.ascontiguousarray(r, np.float64)
+        r = _vec(r, self.n_lambda, "apply_preconditioner")
         z = np.empty(self.n_lambda)
         _check(lib().pf_apply_precond(self.h, _ptr(r), _ptr(z)), self.h)
         return z
 
     def project(self, x):
-        y = np.array(x, np.float64)
+        y = _vec(x, self.n_lambda, "project", copy=True)
         _check(lib().pf_project(self.h, _ptr(y)), self.h)
         return y
 
     def local_solve(self, s, b):
-        x = np.array(b, np.float64)
+        if s not in self.owned:
+            raise ConfigError(f"local_solve: subdomain {s} is not owned by this engine")
+        x = _vec(b, self.subs[self.owned.index(s)]["dim"], "local_solve", copy=True)
         _check(lib().pf_local_solve(self.h, s, _ptr(x)), self.h)
         return x
 
@@ -399,8 +411,8 @@ class StepSolver:
         if prev_x is None:
             return self.op.step()
         op = self.op
-        x = np.ascontiguousarray(prev_x, np.float64)
-        lam = np.ascontiguousarray(prev_lambda, np.float64)
+        x = _vec(prev_x, op.info.total_dim, "advance: prev_x")
+        lam = _vec(prev_lambda, op.n_lambda, "advance: prev_lambda")
         nx = np.empty(op.info.total_dim) if out_x is None else out_x
         nl = np.empty(op.n_lambda) if out_lambda is None else out_lambda
         if nx.dtype != np.float64 or not nx.flags.c_contiguous or nx.size != op.info.total_dim:

@@ -458,7 +458,11 @@ struct SolveSystem {
       ::pf::g_launches++;
       ++launches;
     }
+#ifdef PF_EXPERIMENTS
     static const bool probe = std::getenv("PF_SWEEP_PROBE") != nullptr;
+#else
+    constexpr bool probe = false;
+#endif
     if (probe && mode == 0) launch_mode<3>(st, S, l);
     else if (mode == 0) launch_mode<0>(st, S, l);
     else if (mode == 1) launch_mode<1>(st, S, l);
@@ -1296,6 +1300,8 @@ struct Engine {
   }
 
   ~Engine() {
+    if (hb_st) cudaStreamSynchronize(hb_st);
+    if (st) cudaStreamSynchronize(st);
     if (kr_exec) cudaGraphExecDestroy(kr_exec);
     if (lp_exec) cudaGraphExecDestroy(lp_exec);
     if (h_status) cudaFreeHost(h_status);
@@ -1430,17 +1436,13 @@ struct Engine {
     for (int s = 0; s < ns; ++s) ptype[s] = OS(s).type;
     Ksys.build(kt, ptype, 1);
     if (implicit_dir) Isys.build(it, ptype, 1);
-    const bool host = std::getenv("PF_HOST_FACTOR") && std::atoi(std::getenv("PF_HOST_FACTOR")) != 0;
-    if (host || use_gen) {
+    if (use_gen) {
       h_K.resize(total_kv);
       PF_CUDA_CHECK(cudaMemcpy(h_K.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
     }
-    if (host) {
-      factor_all_host();
-    } else {
-      factor_device(Ksys, ksym, false);
-      if (implicit_dir) factor_device(Isys, isym, true);
-    }
+    // factorisation runs on the device only (no host path in the product)
+    factor_device(Ksys, ksym, false);
+    if (implicit_dir) factor_device(Isys, isym, true);
     if (!std::getenv("PF_NO_SHARE")) {
       Ksys.share_factors(st);
       if (implicit_dir) Isys.share_factors(st);
@@ -1937,7 +1939,9 @@ struct Engine {
   /// b ~ U(-1,1) from mt19937(20240901), x = K_s^{-1} b through the sweep
   /// kernels, ||K_s x - b|| / ||b|| < 1e-8.
   void check_factor_residual() {
+#ifdef PF_EXPERIMENTS
     if (std::getenv("PF_SWEEP_PROBE")) return;  // streaming experiment: solves are not computed
+#endif
     const int nt = (int)D.types.size();
     const int np = nown();
     std::vector<long long> type_b(nt, 0), type_kptr(nt), type_kcol(nt);
@@ -1995,34 +1999,6 @@ struct Engine {
     }
   }
 
-  /// Host supernodal factorisation (PF_HOST_FACTOR=1): debug / cross-check.
-  void factor_all_host() {
-    Ksys.factor_upload(nthreads, [&](int s, std::vector<double>& L, std::vector<double>& Dg) {
-      const Subdomain& S = OS(s);
-      const SubType& T = D.types[S.type];
-      const double* kv = h_K.data() + h_fsubs[s].kval;
-      std::vector<int> fixed;
-      if (T.floating) fixed.assign(T.fix.begin(), T.fix.end());
-      factor_host(ksym[S.type], T.K, kv, fixed, L, Dg);
-    });
-    if (implicit_dir)
-      Isys.factor_upload(nthreads, [&](int s, std::vector<double>& LI, std::vector<double>& DI) {
-        const Subdomain& S = OS(s);
-        const SubType& T = D.types[S.type];
-        const double* kv = h_K.data() + h_fsubs[s].kval;
-        const auto& idx = itype_index[S.type];
-        const auto& pos = itype_pos[S.type];
-        std::vector<std::pair<int, int>> rc;
-        for (int i : idx)
-          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-            if (pos[T.K.col[q]] >= 0) rc.emplace_back(pos[i], pos[T.K.col[q]]);
-        Csr KII = pattern_from_pairs((int)idx.size(), (int)idx.size(), rc);
-        for (int i : idx)
-          for (int q = T.K.ptr[i]; q < T.K.ptr[i + 1]; ++q)
-            if (pos[T.K.col[q]] >= 0) KII.val[KII.find(pos[i], pos[T.K.col[q]])] = kv[q];
-        factor_host(isym[S.type], KII, KII.val.data(), {}, LI, DI);
-      });
-  }
   std::vector<double> h_K;
 
   // ------------------------------------------------------------------
@@ -2529,7 +2505,11 @@ struct Engine {
     qsolve(z, z);
     // ablation (diagnostics only): repeat a component on scratch output so its
     // marginal in-graph cost shows in the step time; results are unchanged
+#ifdef PF_EXPERIMENTS
     static const int dup = std::getenv("PF_DUP") ? std::atoi(std::getenv("PF_DUP")) : 0;
+#else
+    constexpr int dup = 0;  // product build: no ablation work in the iteration
+#endif
     if (dup) {
       if (!kr_dup.p) kr_dup.alloc(D.n_lambda);
       if (dup == 1) qsolve(r, kr_dup.p);                               // one more mortar Gram solve
@@ -2888,6 +2868,17 @@ struct Engine {
     return d_subvec_buf.p;
   }
 
+  /// Join the overlapped K^+ b sweep (hb_st) before anything else touches
+  /// Ksys.X on the engine stream: the sweep's result moves to hb_Yb, where
+  /// back_substitute finds it when hb_pending is clear.  Host-side only (never
+  /// inside a stream capture).
+  void hb_fence() {
+    if (!hb_pending) return;
+    PF_CUDA_CHECK(cudaStreamWaitEvent(st, hb_ev1, 0));
+    PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
+    hb_pending = false;
+  }
+
   /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> state
   void back_substitute(const double* lambda) {
     if (hb_on) {
@@ -2948,8 +2939,10 @@ struct Engine {
     F_(lambda, r);
     dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, r); ::pf::g_launches++;
     project(r);
+    dot(n, r, r, dev::KS_TR0);  // ||r0||^2 of the projected (warm-started) residual
     rep.iterations = 0;
     rep.converged = 0;
+    rep.true_residual = 0.0;
     double* sc = scal.p;
     int* stat = d_status.p;
     static const bool trace = std::getenv("PF_KRYLOV_TRACE") != nullptr;
@@ -2972,6 +2965,16 @@ struct Engine {
         case dev::KST_PKP: fail(kBreakdown, "feti_pcg: <p, Kp> not positive (operator not SPD?)");
         default: fail(kBreakdown, "feti_pcg: preconditioned residual norm lost positivity");
       }
+    };
+    // ||P(rhs - F lambda)|| / ||r0|| of the current iterate, computed afresh
+    // (one F-apply): what the Krylov recurrences only estimate
+    auto true_residual = [&](double* t) {
+      F_(lambda, t);
+      dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, t); ::pf::g_launches++;
+      project(t);
+      dot(n, t, t, dev::KS_TRUE);
+      const double r0 = read_scal(dev::KS_TR0);
+      return r0 > 0.0 ? std::sqrt(read_scal(dev::KS_TRUE) / r0) : 0.0;
     };
     if (krylov == PF_KRYLOV_PCG) {
       // REF feti_pcg (feti.hpp:263-308)
@@ -3014,6 +3017,7 @@ struct Engine {
       if (h_status[0] == dev::KST_CONV) rep.converged = 1;
       else if (h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
       rep.rel_residual = rel_residual();
+      rep.true_residual = true_residual(kr_q.p);  // reported; REF's criterion is sqrt(r.z)
       return;
     }
     // SQMR (Freund & Nachtigal) with the symmetric indefinite preconditioner
@@ -3022,15 +3026,12 @@ struct Engine {
     double* d = kr_d.p;
     double* u = kr_z.p;
     dot(n, r, r, dev::KS_RR);
-    dev::k_ks_sqmr_init<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+    dev::k_ks_sqmr_init<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
     if (status() == dev::KST_CONV) {
       rep.converged = 1;
       rep.rel_residual = 0.0;
       return;
     }
-    M_(r, q);
-    dot(n, r, q, dev::KS_RHO);
-    kr_d.zero(st);
     // iteration = [u = M r, rho, q = u + b q (not in the first)] F q, sigma, r, tau, lambda
     auto iter = [&](bool first) {
       if (!first) {
@@ -3045,21 +3046,45 @@ struct Engine {
                  lp_cap_maxit, lp_capturing ? 1 : 0);
       lp_cond_set = lp_capturing;
     };
-    iter(true);
-    if (status() == dev::KST_RUN && maxit > 1 && loop_ok()) {
-      // every further iteration on the device: one launch of a WHILE graph
-      graphed_loop(lambda, 2, maxit, [&] { iter(false); });
-      status();
-    } else {
-      for (int k = 1; k < maxit && h_status[0] == dev::KST_RUN; ++k) {
-        graphed(lambda, 2, [&] { iter(false); });
+    // iterate on the device until the status word leaves RUN or maxit
+    auto loop = [&] {
+      if (status() == dev::KST_RUN && h_status[1] < maxit && loop_ok()) {
+        // every further iteration on the device: one launch of a WHILE graph
+        graphed_loop(lambda, 2, maxit, [&] { iter(false); });
         status();
+      } else {
+        while (h_status[1] < maxit && h_status[0] == dev::KST_RUN) {
+          graphed(lambda, 2, [&] { iter(false); });
+          status();
+        }
       }
+      if (h_status[0] != dev::KST_CONV && h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
+    };
+    M_(r, q);
+    dot(n, r, q, dev::KS_RHO);
+    kr_d.zero(st);
+    iter(true);
+    loop();
+    // The quasi-residual tau_k only estimates ||r_k|| (||r_k|| <= sqrt(k+1) tau_k):
+    // convergence is confirmed on the true residual P(rhs - F lambda); above
+    // tol * ||r0|| the same recurrences continue with a tightened threshold
+    for (;;) {
+      rep.iterations = h_status[1];
+      if (h_status[0] != dev::KST_CONV) {
+        rep.rel_residual = rel_residual();
+        break;
+      }
+      const double tr = true_residual(t);
+      rep.true_residual = rep.rel_residual = tr;
+      if (tr <= tol) {
+        rep.converged = 1;
+        break;
+      }
+      ++rep.restarts;
+      if (h_status[1] >= maxit) break;
+      dev::k_ks_sqmr_continue<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
+      loop();
     }
-    rep.iterations = h_status[1];
-    if (h_status[0] == dev::KST_CONV) rep.converged = 1;
-    else if (h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
-    rep.rel_residual = rel_residual();
   }
 
   /// The device-side loop needs graph capture (no host reducer, no phase
@@ -3293,16 +3318,28 @@ thread_local std::string g_create_error;
 
 template <class F>
 int guarded(pf_ctx* ctx, F&& f) {
+  // every entry point leaves no overlapped K^+ b sweep in flight on Ksys.X
+  // (success or error), so the next call may use Ksys on the engine stream
+  auto fence = [&] {
+    if (!ctx) return;
+    try {
+      ctx->eng.hb_fence();
+    } catch (...) {
+    }
+  };
   try {
     f();
+    ctx ? ctx->eng.hb_fence() : void();
     return PF_OK;
   } catch (const pf::Error& e) {
     if (ctx) ctx->eng.last_error = e.what();
     else g_create_error = e.what();
+    fence();
     return e.code;
   } catch (const std::exception& e) {
     if (ctx) ctx->eng.last_error = e.what();
     else g_create_error = e.what();
+    fence();
     return PF_INTERNAL;
   }
 }

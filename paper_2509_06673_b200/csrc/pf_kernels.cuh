@@ -284,7 +284,7 @@ __global__ void k_sqmr_dx(int n, const double* sc, const double* q, double* d, d
 // ---------------------------------------------------------------------------
 enum : int {
   KS_RHO = 32, KS_SIGMA, KS_A, KS_RR, KS_THETA, KS_THOLD, KS_C, KS_TAU, KS_T0, KS_RHON, KS_B, KS_REL,
-  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0
+  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR
 };
 enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5 };
 
@@ -321,11 +321,20 @@ __global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d,
   d[i] = dn;
   x[i] += dn;
 }
-__device__ __forceinline__ void ks_sqmr_init(double* sc, int* status) {
+__device__ __forceinline__ void ks_sqmr_init(double* sc, int* status, double tol) {
   const double t0 = sqrt(sc[KS_RR]);
-  sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0;
+  sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0, sc[KS_THR] = tol * t0;
   status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
+}
+/// SQMR convergence check failed on the true residual (TRUE = ||r||^2 of
+/// r = P(rhs - F lambda)): keep iterating with the same recurrences, the
+/// estimate's threshold scaled by the observed true/estimate ratio (the oracle
+/// rule, o_feti.hpp sqmr)
+__global__ void k_ks_sqmr_continue(double* sc, int* status, double tol) {
+  const double tr = sqrt(sc[KS_TRUE]);
+  sc[KS_THR] = sc[KS_TAU] * (tol * sc[KS_T0] / tr) * 0.5;
+  status[0] = KST_RUN;
 }
 __device__ __forceinline__ void ks_sqmr_a(double* sc, int* status) {
   const double sigma = sc[KS_SIGMA];
@@ -339,9 +348,11 @@ __device__ __forceinline__ void ks_sqmr_tau(double* sc, int* status, double tol)
   const double c = 1.0 / sqrt(1.0 + theta * theta);
   const double tau = sc[KS_TAU] * theta * c;
   sc[KS_THOLD] = th_old, sc[KS_THETA] = theta, sc[KS_C] = c, sc[KS_TAU] = tau;
-  sc[KS_REL] = tau / sc[KS_T0];  // quasi-residual tau_k <= tol ||r0|| (oracle rule)
+  sc[KS_REL] = tau / sc[KS_T0];
   status[1] += 1;
-  if (status[0] == KST_RUN && tau <= tol * sc[KS_T0]) status[0] = KST_CONV;
+  // quasi-residual tau_k below the threshold (tol ||r0||, tightened after a
+  // failed true-residual check): candidate convergence, confirmed by the host
+  if (status[0] == KST_RUN && tau <= sc[KS_THR]) status[0] = KST_CONV;
 }
 __device__ __forceinline__ void ks_sqmr_b(double* sc, int* status) {
   if (sc[KS_RHO] == 0.0 && status[0] == KST_RUN) status[0] = KST_RHO;
@@ -373,7 +384,7 @@ __device__ __forceinline__ void ks_pcg_beta(double* sc, int* status, double tol)
   sc[KS_RZ] = rzn;
 }
 
-__global__ void k_ks_sqmr_init(double* sc, int* status) { ks_sqmr_init(sc, status); }
+__global__ void k_ks_sqmr_init(double* sc, int* status, double tol) { ks_sqmr_init(sc, status, tol); }
 __global__ void k_ks_sqmr_a(double* sc, int* status) { ks_sqmr_a(sc, status); }
 __global__ void k_ks_sqmr_tau(double* sc, int* status, double tol) { ks_sqmr_tau(sc, status, tol); }
 __global__ void k_ks_sqmr_b(double* sc, int* status) { ks_sqmr_b(sc, status); }
@@ -393,7 +404,7 @@ enum : int { SOP_NONE = 0, SOP_SQMR_INIT, SOP_SQMR_A, SOP_SQMR_TAU, SOP_SQMR_B, 
              SOP_PCG_BETA };
 __device__ __forceinline__ void ks_run(int sop, double* sc, int* status, double tol) {
   switch (sop) {
-    case SOP_SQMR_INIT: ks_sqmr_init(sc, status); break;
+    case SOP_SQMR_INIT: ks_sqmr_init(sc, status, tol); break;
     case SOP_SQMR_A: ks_sqmr_a(sc, status); break;
     case SOP_SQMR_TAU: ks_sqmr_tau(sc, status, tol); break;
     case SOP_SQMR_B: ks_sqmr_b(sc, status); break;

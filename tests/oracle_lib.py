@@ -90,6 +90,7 @@ def lib():
         L.or_report.argtypes = [P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p,
                                 C.POINTER(C.c_int)]
+        L.or_report_true.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.or_monolithic_step.argtypes = [P, dp, dp]
         L.or_mults.argtypes = [P, ip, C.c_void_p]
         L.or_n_ifaces.argtypes = [P]
@@ -230,8 +231,10 @@ class Oracle:
         hist = np.zeros(nh.value)
         check(lib().or_report(self.h, step, C.byref(it), C.byref(conv), C.byref(rel), C.byref(secs),
                               hist.ctypes.data, C.byref(nh)))
+        tr, rs = C.c_double(), C.c_int()
+        check(lib().or_report_true(self.h, step, C.byref(tr), C.byref(rs)))
         return dict(iterations=it.value, converged=bool(conv.value), rel_residual=rel.value,
-                    seconds=secs.value, history=hist)
+                    seconds=secs.value, history=hist, true_residual=tr.value, restarts=rs.value)
 
     def monolithic_step(self):
         tot = sum(S["dim"] for S in self.subs)
