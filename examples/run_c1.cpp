@@ -1,17 +1,40 @@
-// Minimal C++ user of the drop-in shim: BASELINE config 1, all steps.
-//   g++ -std=c++17 -Iinclude examples/run_c1.cpp -Lpaper_2509_06673_b200/_lib -lporofeti_b200 \
+// Minimal C++ user of the drop-in shim: BASELINE config 1 (the reference's
+// own layout, feti-schur), first through the reference's step decomposition
+// (interface_rhs -> feti_pcg -> back_substitute, timeloop.hpp:163-176), then
+// every step of the run (StepSolver::advance on the device-resident state).  Build (tests/test_gpu_boundary.py does):
+//   g++ -std=c++17 -Iinclude examples/run_c1.cpp -Lpaper_2509_06673_b200/_lib -lporofeti_b200
 //       -Wl,-rpath,$PWD/paper_2509_06673_b200/_lib -o run_c1
+#include <cmath>
 #include <cstdio>
 
 #include "porofeti_b200.hpp"
 
+namespace pb = porofeti_b200;
+
 int main() {
-  pf_config cfg = porofeti_b200::default_config();
+  pf_config cfg = pb::default_config();
   try {
-    porofeti_b200::Problem problem(cfg);
-    for (const auto& r : porofeti_b200::run_simulation(problem))
-      std::printf("step %d  iters %d  rel %.2e  %.3f ms\n", r.step, r.iterations, r.rel_residual, r.seconds * 1e3);
-  } catch (const porofeti_b200::Error& e) {
+    {
+      pb::Problem problem(cfg);
+      const pb::Vector F = problem.interface_rhs();
+      const pb::Vector lambda0(problem.n_lambda(), 0.0);
+      const pb::PcgResult res = pb::feti_pcg(problem, F, lambda0, cfg.tol, cfg.max_iter);
+      const pb::Vector x = problem.back_substitute(res.lambda);
+      double nl = 0.0, nx = 0.0;
+      for (double v : res.lambda) nl += v * v;
+      for (double v : x) nx += v * v;
+      std::printf("pieces step 1 iters %d history %zu delta0 %.17g lambda_norm %.17g x_norm %.17g\n",
+                  res.report.iterations, res.residual_history.size(),
+                  res.residual_history.empty() ? 0.0 : res.residual_history[0], std::sqrt(nl), std::sqrt(nx));
+    }
+    pb::Problem problem(cfg);
+    for (int n = 0; n < problem.info().N; ++n) {
+      const pb::PcgReport r = problem.step();
+      const auto [eu, ep] = problem.errors();
+      std::printf("step %d iters %d rel %.3e true %.3e err_u %.17g err_p %.17g ms %.3f\n", r.step, r.iterations,
+                  r.rel_residual, r.true_residual, eu, ep, r.seconds * 1e3);
+    }
+  } catch (const pb::Error& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;
   }

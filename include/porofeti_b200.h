@@ -209,10 +209,75 @@ int pf_kernel_stats(pf_ctx* ctx, double* sweep_ms, int* launches_per_apply);
 /* Per-kernel timing of the sweeps (see pf_engine.cu): 10 doubles. */
 int pf_phase_stats(pf_ctx* ctx, int iters, double* out);
 
-/* Element-level entry points (elements.hpp:152-251) evaluated on the device,
- * used by the parity tests: tri = 3 vertices (x0,y0,x1,y1,x2,y2). */
+/* Element-level entry point (elements.hpp:152-230) evaluated on the device by
+ * the same device functions the assembly kernel uses: tri = 3 vertices
+ * (x0,y0,x1,y1,x2,y2); outputs row-major: local_elastic_matrix 2nb x 2nb,
+ * local_div_matrix 3 x 2nb, local_mass_matrix 3 x 3, local_diffusion_matrix
+ * 3 x 3 (K = kperm I); nb = 3 (P1) or 6 (P2).  PF_INVALID for a degenerate
+ * triangle (AssemblyError, elements.hpp:139), PF_CUDA without a device. */
 int pf_local_matrices(const double* tri, double mu, double kperm, double mu_f, int order,
                       double* elastic, double* div, double* mass, double* diffusion);
+
+/* ---- the reference's per-step pieces, callable one by one -------------------
+ * REF StepSolver::advance (timeloop.hpp:150-186) is
+ *   rhs = assemble_rhs_step(...)            -> pf_set_loads (optional) + pf_interface_rhs
+ *   F = interface_rhs(rhs)                  -> pf_interface_rhs
+ *   [lambda, rep] = feti_pcg(op, F, l0, ..) -> pf_krylov
+ *   back_substitute(lambda, rhs)            -> pf_back_substitute
+ * pf_step / pf_advance run the same sequence on the device in one call. */
+
+/* feti_pcg (feti.hpp:263-308) on a caller right-hand side: the engine's Krylov
+ * method (REF PCG without pressure multipliers, SQMR with them; projected onto
+ * the natural coarse space when floating subdomains exist, so lambda0 should
+ * satisfy G_c^T lambda0 = e) from lambda0 to relative tolerance tol, at most
+ * max_iter iterations; lambda_out may alias lambda0.  PF_NOT_CONVERGED when
+ * max_iter is reached (lambda_out holds the last iterate, rep is filled),
+ * PF_BREAKDOWN on a breakdown (PcgBreakdownError), PF_NOT_CONVERGED also for
+ * tol <= 0 (SolverError, feti.hpp:265). */
+int pf_krylov(pf_ctx* ctx, const double* rhs, const double* lambda0, double tol, int max_iter,
+              double* lambda_out, pf_report* rep);
+/* PcgReport::residual_history (feti.hpp:65) of the last solve (pf_krylov or a
+ * step): absolute sqrt(r.z) per iteration for PCG, the quasi-residual for
+ * SQMR, entry 0 the initial one.  Copies min(count, cap) values into out (may
+ * be NULL) and returns the count (negative status on error). */
+int pf_last_history(const pf_ctx* ctx, double* out, int cap);
+
+/* FetiOperator::back_substitute (feti.hpp:158-168) for the right-hand side of
+ * the last pf_interface_rhs / step: x_s = K_s^+ (b_s - G_s^T lambda) (+ the
+ * rigid modes of floating subdomains) for every owned subdomain, saddle layout,
+ * concatenated in x_out (total_dim values).  The device state is unchanged. */
+int pf_back_substitute(pf_ctx* ctx, const double* lambda, double* x_out);
+
+/* FetiOperator::set_precond (feti.hpp:97): any PF_PREC_* kind; identity always,
+ * generalized and the mortar scaling are built on first use, the Dirichlet
+ * kinds need the context created with a Dirichlet preconditioner. */
+int pf_set_precond(pf_ctx* ctx, int kind);
+
+/* Field-named snapshot (StateSnapshot, state.hpp:8-12; unpack_state,
+ * feti.hpp:443-454): field of subdomain s (global id), or of every owned
+ * subdomain concatenated in subdomain order with s = -1 (eta and p exist on
+ * poroelastic subdomains only).  pf_field_size returns the value count. */
+#define PF_FIELD_U 0
+#define PF_FIELD_ETA 1
+#define PF_FIELD_XI 2
+#define PF_FIELD_P 3
+int pf_field_size(const pf_ctx* ctx, int field, int s);
+int pf_get_field(pf_ctx* ctx, int field, int s, double* out);
+
+/* Caller-supplied loads (StepLoads, assembly.hpp:475-479, + the essential
+ * values of assemble_rhs_step, :562-571) in place of the scenario's closed
+ * forms.  Layout, owned subdomains in order: F_u n_u values each (body +
+ * traction loads on the displacement dofs), Z n_s values per poroelastic
+ * subdomain (the mass-balance source row), g the constraint values in
+ * pf_get_constraints order (sizes: pf_load_sizes).  NULL = zero.  Applied to
+ * the next right-hand side (every later one with persistent != 0, until
+ * pf_clear_loads).  pf_scenario_loads returns the scenario's own loads at t in
+ * the same layout. */
+int pf_get_constraints(const pf_ctx* ctx, int s, int* saddle_index, int* component, double* xy);
+int pf_load_sizes(const pf_ctx* ctx, long long* n_F, long long* n_Z, long long* n_g);
+int pf_scenario_loads(pf_ctx* ctx, double t, double* F_u, double* Z, double* g);
+int pf_set_loads(pf_ctx* ctx, const double* F_u, const double* Z, const double* g, int persistent);
+int pf_clear_loads(pf_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,11 @@
 //   FetiOperator::apply_preconditioner (:127)    Problem::apply_preconditioner
 //   FetiOperator::interface_rhs (:147)           Problem::interface_rhs
 //   SubdomainFactorization::solve (:38)          Problem::local_solve
+//   FetiOperator::back_substitute (:158)         Problem::back_substitute
+//   FetiOperator::set_precond (:97)              Problem::set_precond
+//   feti_pcg (:263)                              feti_pcg(Problem&, ...)
+//   unpack_state (:443) / StateSnapshot fields   Problem::field
+//   assemble_rhs_step loads (assembly.hpp:550)   Problem::set_loads
 //   StepSolver::advance (timeloop.hpp:150)       StepSolver::advance
 //   run_simulation (timeloop.hpp:206)            run_simulation
 #pragma once
@@ -134,6 +139,37 @@ class Problem {
     check(pf_local_solve(ctx_, s, b.data()), ctx_);
     return b;
   }
+  /// StepSolver::advance on the device-resident state (one time step)
+  PcgReport step() {
+    pf_report r{};
+    check(pf_step(ctx_, &r), ctx_);
+    return to_report(r);
+  }
+  /// FetiOperator::set_precond (feti.hpp:97), PF_PREC_* kinds
+  void set_precond(int kind) { check(pf_set_precond(ctx_, kind), ctx_); }
+  /// FetiOperator::back_substitute (feti.hpp:158) for the current right-hand
+  /// side: every subdomain's saddle vector, concatenated
+  Vector back_substitute(const Vector& lambda) const {
+    check_size(lambda, info_.n_lambda, "back_substitute");
+    Vector x(info_.total_dim);
+    check(pf_back_substitute(ctx_, lambda.data(), x.data()), ctx_);
+    return x;
+  }
+  /// one named field (state.hpp:8-12) of subdomain s, or of all subdomains (s = -1)
+  Vector field(int field, int s = -1) const {
+    const int n = pf_field_size(ctx_, field, s);
+    if (n < 0) throw ConfigError("field: not available for this subdomain");
+    Vector out(n);
+    check(pf_get_field(ctx_, field, s, out.data()), ctx_);
+    return out;
+  }
+  /// caller-supplied loads for the next step (assembly.hpp:475-479 StepLoads + essential values)
+  void set_loads(const Vector& F_u, const Vector& Z, const Vector& g, bool persistent = false) {
+    long long nF = 0, nZ = 0, nG = 0;
+    check(pf_load_sizes(ctx_, &nF, &nZ, &nG), ctx_);
+    check_size(F_u, nF, "set_loads: F_u"), check_size(Z, nZ, "set_loads: Z"), check_size(g, nG, "set_loads: g");
+    check(pf_set_loads(ctx_, F_u.data(), Z.data(), g.data(), persistent ? 1 : 0), ctx_);
+  }
   /// snapshot_u_error / snapshot_p_error (verify.hpp:62-74) of the current state
   std::pair<double, double> errors() const {
     double eu = 0.0, ep = 0.0;
@@ -152,6 +188,28 @@ class Problem {
   pf_ctx* ctx_ = nullptr;
   pf_info info_{};
 };
+
+/// Reference feti_pcg (feti.hpp:263-308): Krylov solve of the interface
+/// problem for a caller right-hand side; throws SolverError when max_iter is
+/// reached, PcgBreakdownError on breakdown.  residual_history as in REF.
+struct PcgResult {
+  Vector lambda;
+  PcgReport report;
+  std::vector<double> residual_history;
+};
+inline PcgResult feti_pcg(Problem& p, const Vector& rhs, const Vector& lambda_init, double tol, int max_iter) {
+  check_size(rhs, p.n_lambda(), "feti_pcg: rhs");
+  check_size(lambda_init, p.n_lambda(), "feti_pcg: lambda_init");
+  PcgResult out;
+  out.lambda.resize(p.n_lambda());
+  pf_report r{};
+  check(pf_krylov(p.handle(), rhs.data(), lambda_init.data(), tol, max_iter, out.lambda.data(), &r), p.handle());
+  out.report = to_report(r);
+  const int n = pf_last_history(p.handle(), nullptr, 0);
+  out.residual_history.resize(n > 0 ? n : 0);
+  if (n > 0) pf_last_history(p.handle(), out.residual_history.data(), n);
+  return out;
+}
 
 /// Reference StepSolver (timeloop.hpp:135-193).
 class StepSolver {

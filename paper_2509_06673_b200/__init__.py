@@ -32,6 +32,7 @@ __all__ = [
     "Error", "SingularSubproblemError", "PcgBreakdownError", "SolverError", "ConfigError",
     "CudaUnavailableError", "lib", "build", "LIB_PATH", "oscillation_check", "estimate_order", "mms_errors",
     "convergence_study", "write_error_csv", "write_solver_log_csv", "write_solution_vtk", "barry_mercer_check", "pinned_empty",
+    "feti_pcg", "unpack_state", "local_matrices",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -206,6 +207,18 @@ def lib():
         L.pf_shard_plan.argtypes = [C.c_int, C.c_int, C.c_int, vp]
         L.pf_debug_factor_solve.argtypes = [C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_longlong, vp]
         L.pf_debug_disc.argtypes = [C.POINTER(Config), vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_local_matrices.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_int, vp, vp, vp, vp]
+        L.pf_krylov.argtypes = [vp, vp, vp, C.c_double, C.c_int, vp, C.POINTER(Report)]
+        L.pf_last_history.argtypes = [vp, vp, C.c_int]
+        L.pf_back_substitute.argtypes = [vp, vp, vp]
+        L.pf_set_precond.argtypes = [vp, C.c_int]
+        L.pf_field_size.argtypes = [vp, C.c_int, C.c_int]
+        L.pf_get_field.argtypes = [vp, C.c_int, C.c_int, vp]
+        L.pf_get_constraints.argtypes = [vp, C.c_int, vp, vp, vp]
+        L.pf_load_sizes.argtypes = [vp, vp, vp, vp]
+        L.pf_scenario_loads.argtypes = [vp, C.c_double, vp, vp, vp]
+        L.pf_set_loads.argtypes = [vp, vp, vp, vp, C.c_int]
+        L.pf_clear_loads.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -302,6 +315,86 @@ class FetiOperator:
         F = np.empty(self.n_lambda)
         _check(lib().pf_interface_rhs(self.h, _ptr(F)), self.h)
         return F
+
+    def set_precond(self, kind):
+        """FetiOperator::set_precond (feti.hpp:97): a PRECONDS name."""
+        _check(lib().pf_set_precond(self.h, PRECONDS[kind]), self.h)
+
+    def krylov(self, rhs, lambda0, tol, max_iter):
+        """feti_pcg (feti.hpp:263-308) on a caller right-hand side -> (lambda,
+        report); report["residual_history"] as in REF's PcgReport.  Raises
+        SolverError when max_iter is reached (like StepSolver::advance)."""
+        rhs = _vec(rhs, self.n_lambda, "krylov: rhs")
+        lam = _vec(lambda0, self.n_lambda, "krylov: lambda0", copy=True)
+        rep = Report()
+        code = lib().pf_krylov(self.h, _ptr(rhs), _ptr(lam), float(tol), int(max_iter), _ptr(lam), C.byref(rep))
+        _check(code, self.h)
+        d = rep.as_dict()
+        d["residual_history"] = self.history()
+        return lam, d
+
+    def history(self):
+        """residual history of the last Krylov solve (pf_last_history)"""
+        n = lib().pf_last_history(self.h, None, 0)
+        if n < 0:
+            _check(-n, self.h)
+        h = np.empty(n)
+        lib().pf_last_history(self.h, _ptr(h), n)
+        return h
+
+    def back_substitute(self, lam):
+        """FetiOperator::back_substitute (feti.hpp:158) for the current
+        right-hand side: all owned subdomains' saddle vectors, concatenated."""
+        lam = _vec(lam, self.n_lambda, "back_substitute: lambda")
+        x = np.empty(self.info.total_dim)
+        _check(lib().pf_back_substitute(self.h, _ptr(lam), _ptr(x)), self.h)
+        return x
+
+    FIELDS = {"u": 0, "eta": 1, "xi": 2, "p": 3}
+
+    def field(self, name, s=-1):
+        """one named field (state.hpp:8-12) of subdomain s, or of every owned
+        subdomain concatenated (s = -1)"""
+        f = self.FIELDS[name]
+        n = lib().pf_field_size(self.h, f, s)
+        if n < 0:
+            raise ConfigError(f"field {name!r} of subdomain {s}: not available")
+        out = np.empty(n)
+        _check(lib().pf_get_field(self.h, f, s, _ptr(out)), self.h)
+        return out
+
+    def constraints(self, s):
+        """(saddle index, component (-1: pressure), xy) of subdomain s's essential dofs"""
+        n = lib().pf_get_constraints(self.h, s, None, None, None)
+        if n < 0:
+            raise ConfigError(f"constraints of subdomain {s}: not owned")
+        idx, comp, xy = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(2 * n)
+        lib().pf_get_constraints(self.h, s, _ptr(idx), _ptr(comp), _ptr(xy))
+        return idx, comp, xy.reshape(n, 2)
+
+    def load_sizes(self):
+        a, b, c = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        _check(lib().pf_load_sizes(self.h, C.byref(a), C.byref(b), C.byref(c)), self.h)
+        return a.value, b.value, c.value
+
+    def scenario_loads(self, t):
+        """(F_u, Z, g) of the scenario at time t (assemble_loads + constraint values)"""
+        nF, nZ, nG = self.load_sizes()
+        F, Z, g = np.empty(max(nF, 1)), np.empty(max(nZ, 1)), np.empty(max(nG, 1))
+        _check(lib().pf_scenario_loads(self.h, float(t), _ptr(F), _ptr(Z), _ptr(g)), self.h)
+        return F[:nF], Z[:nZ], g[:nG]
+
+    def set_loads(self, F_u=None, Z=None, g=None, persistent=False):
+        """caller-supplied loads for the next step (every step with persistent)"""
+        nF, nZ, nG = self.load_sizes()
+        a = None if F_u is None else _vec(F_u, nF, "set_loads: F_u")
+        b = None if Z is None else _vec(Z, nZ, "set_loads: Z")
+        c = None if g is None else _vec(g, nG, "set_loads: g")
+        _check(lib().pf_set_loads(self.h, None if a is None else _ptr(a), None if b is None else _ptr(b),
+                                  None if c is None else _ptr(c), int(persistent)), self.h)
+
+    def clear_loads(self):
+        _check(lib().pf_clear_loads(self.h), self.h)
 
     # --- state (StateSnapshot, state.hpp:8-12) ---
     def set_reducer(self, fn):
@@ -422,6 +515,37 @@ class StepSolver:
         rep = Report()
         _check(lib().pf_advance(op.h, _ptr(x), _ptr(lam), int(prev_step), _ptr(nx), _ptr(nl), C.byref(rep)), op.h)
         return nx, nl, rep.as_dict()
+
+
+def feti_pcg(op: FetiOperator, rhs, lambda_init, tol, max_iter):
+    """feti_pcg (feti.hpp:263): (lambda, report) -- FetiOperator.krylov"""
+    return op.krylov(rhs, lambda_init, tol, max_iter)
+
+
+def unpack_state(op: FetiOperator):
+    """unpack_state (feti.hpp:443-454) of the device-resident state into the
+    reference's StateSnapshot names.  One poroelastic and one elastic
+    subdomain (the reference layout): u_P, eta, xi_P, p, u_E, xi_E, lambda;
+    otherwise per-region fields concatenated over the subdomains of that region
+    in subdomain order."""
+    P = [s for s, S in zip(op.owned, op.subs) if S["region"] == 0]
+    E = [s for s, S in zip(op.owned, op.subs) if S["region"] != 0]
+    cat = lambda name, ids: np.concatenate([op.field(name, s) for s in ids]) if ids else np.empty(0)
+    _, lam = op.state()
+    return {"step": lib().pf_current_step(op.h), "u_P": cat("u", P), "eta": cat("eta", P), "xi_P": cat("xi", P),
+            "p": cat("p", P), "u_E": cat("u", E), "xi_E": cat("xi", E), "lambda": lam}
+
+
+def local_matrices(tri, mu, order, kperm=1.0, mu_f=1.0):
+    """local_elastic_matrix / local_div_matrix / local_mass_matrix /
+    local_diffusion_matrix (elements.hpp:152-230) of one triangle, on the device"""
+    tri = np.ascontiguousarray(tri, np.float64).reshape(6)
+    nb = 3 if order == 1 else 6
+    el, dv = np.empty((2 * nb, 2 * nb)), np.empty((3, 2 * nb))
+    ma, di = np.empty((3, 3)), np.empty((3, 3))
+    _check(lib().pf_local_matrices(_ptr(tri), float(mu), float(kperm), float(mu_f), int(order), _ptr(el), _ptr(dv),
+                                   _ptr(ma), _ptr(di)))
+    return {"elastic": el, "div": dv, "mass": ma, "diffusion": di}
 
 
 def run_simulation(op: FetiOperator, steps=None):

@@ -1381,6 +1381,7 @@ struct Engine {
     }
     d_fsubs.upload(h_fsubs);
     d_cxy.upload(cxy);
+    h_cxy = cxy;
     if (!D.kelem.empty()) d_kelem.upload(D.kelem);
     if (!D.srcel.empty()) d_srcel.upload(D.srcel);
     Kv.alloc(total_kv), Lv.alloc(std::max<long long>(1, total_lv));
@@ -2359,7 +2360,7 @@ struct Engine {
     red_blocks = std::getenv("PF_RED_BLOCKS") ? std::max(1, std::atoi(std::getenv("PF_RED_BLOCKS"))) : dev::kRedBlocks;
     red_part.alloc(std::max(red_blocks, dev::kRedBlocks));
     red_count.upload(std::vector<unsigned int>{0u});
-    scal.alloc(64);
+    scal.alloc(dev::KS_HIST0 + dev::kHistCap + 1);  // Krylov scalars + residual history
     h_scal.assign(64, 0.0);
     d_status.alloc(2);
     if (!h_status) PF_CUDA_CHECK(cudaMallocHost(&h_status, 2 * sizeof(int)));
@@ -2565,14 +2566,23 @@ struct Engine {
   // ------------------------------------------------------------------
   /// b_s and d for step time t from the current state (assemble_rhs_step)
   void build_rhs(double t) {
+    hb_fence();
+    hb_valid = false;  // a new right-hand side
     dev::FemSet S = femset();
-    bvec.zero(st);
-    zacc.zero(st);
-    for (int c = 0; c < 8; ++c) {
-      const int n = colour_threads(c);
-      if (n) dev::k_rhs_elem<<<cdiv(n, 128), 128, 0, st>>>(S, c, t, bvec.p, zacc.p); ::pf::g_launches++;
+    if (loads_set) {  // caller-supplied loads (pf_set_loads)
+      PF_CUDA_CHECK(cudaMemcpyAsync(bvec.p, cl_b.p, sizeof(double) * total_vec, cudaMemcpyDeviceToDevice, st));
+      PF_CUDA_CHECK(cudaMemcpyAsync(zacc.p, cl_z.p, sizeof(double) * zacc.n, cudaMemcpyDeviceToDevice, st));
+      PF_CUDA_CHECK(cudaMemcpyAsync(gval.p, cl_g.p, sizeof(double) * gval.n, cudaMemcpyDeviceToDevice, st));
+      if (!loads_persist) loads_set = false;
+    } else {
+      bvec.zero(st);
+      zacc.zero(st);
+      for (int c = 0; c < 8; ++c) {
+        const int n = colour_threads(c);
+        if (n) dev::k_rhs_elem<<<cdiv(n, 128), 128, 0, st>>>(S, c, t, bvec.p, zacc.p), ::pf::g_launches++;
+      }
+      if (total_g) dev::k_constraint_values<<<dim3(4, S.nsub), 128, 0, st>>>(S, t, gval.p), ::pf::g_launches++;
     }
-    if (total_g) dev::k_constraint_values<<<dim3(4, S.nsub), 128, 0, st>>>(S, t, gval.p); ::pf::g_launches++;
     dev::RhsSet R;
     R.nsub = S.nsub, R.types = d_ftypes.p, R.subs = d_fsubs.p;
     R.kptr = d_kptr.p, R.kcol = d_kcol.p, R.lptr = d_lptr.p, R.lcol = d_lcol.p, R.cpos = d_cpos.p;
@@ -2824,6 +2834,7 @@ struct Engine {
       Ksys.solve(hb_st, 1);
       PF_CUDA_CHECK(cudaEventRecord(hb_ev1, hb_st));
       hb_pending = true;
+      hb_valid = false;
       ::pf::g_launches += 1 + (nfix ? 1 : 0);
       // F = sum_s H_t^T b_s - d on the engine stream (H_t's rows at fixing dofs are zero)
       const int n = D.n_lambda;
@@ -2842,8 +2853,10 @@ struct Engine {
     perm_in_K(bvec.p);
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
-    if (hb_on)  // K^+ b for the explicit back-substitution
+    if (hb_on) {  // K^+ b for the explicit back-substitution
       PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
+      hb_valid = true;
+    }
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, out, 1.0, 0, dvec.p);
     reduce(out, D.n_lambda);
   }
@@ -2868,6 +2881,117 @@ struct Engine {
     return d_subvec_buf.p;
   }
 
+  DevBuf<double> kr_user, bs_out;  // pf_krylov / pf_back_substitute buffers
+  int last_hist_n = 0;              // residual-history entries of the last solve
+  std::vector<double> h_cxy;        // constraint node coordinates (host copy)
+
+  /// rigid amplitudes alpha = (G_c^T G_c)^{-1} G_c^T (F lambda - rhs) (floating
+  /// subdomains), rhs = the interface right-hand side in kr_rhs
+  void recover_rigid(const double* lambda) {
+    if (nc == 0) return;
+    const int n = D.n_lambda;
+    F_(lambda, kr_tmp.p);
+    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, kr_rhs.p, 1.0, kr_tmp.p); ::pf::g_launches++;
+    coarse_solve(kr_tmp.p, alpha_vec.p);
+  }
+
+  // ---- caller-supplied loads (StepLoads, assembly.hpp:475-479) ----
+  bool loads_set = false, loads_persist = false;
+  DevBuf<double> cl_b, cl_z, cl_g;
+  /// F_u: n_u per owned subdomain; Z: n_s per owned poroelastic subdomain;
+  /// g: the constraint values per owned subdomain in pf_get_constraints order
+  /// (NULL: zero).  Used by the next right-hand side assembly (every one with
+  /// `persistent`) in place of the scenario's closed forms.
+  void set_loads(const double* F_u, const double* Z, const double* g, bool persistent) {
+    std::vector<double> hb(total_vec, 0.0), hz(std::max<long long>(1, total_z), 0.0);
+    long long f = 0;
+    for (int p = 0; p < nown(); ++p) {
+      const SubType& T = D.types[OS(p).type];
+      if (F_u) std::copy(F_u + f, F_u + f + T.n_u, hb.begin() + sub_vec[p]);
+      f += T.n_u;
+    }
+    if (Z) std::copy(Z, Z + total_z, hz.begin());
+    cl_b.upload(hb), cl_z.upload(hz);
+    std::vector<double> hg(std::max<long long>(1, total_g), 0.0);
+    if (g) std::copy(g, g + total_g, hg.begin());
+    cl_g.upload(hg);
+    loads_set = true, loads_persist = persistent;
+  }
+  /// the scenario's own loads at t (assemble_loads, assembly.hpp:481-540, and
+  /// the constraint values, :562-571), in set_loads' layout
+  void scenario_loads(double t, double* F_u, double* Z, double* g) {
+    dev::FemSet S = femset();
+    DevBuf<double> b, z, gv;
+    b.alloc(std::max<long long>(1, total_vec)), z.alloc(std::max<long long>(1, total_z));
+    gv.alloc(std::max<long long>(1, total_g));
+    b.zero(st), z.zero(st), gv.zero(st);
+    for (int c = 0; c < 8; ++c) {
+      const int n = colour_threads(c);
+      if (n) dev::k_rhs_elem<<<cdiv(n, 128), 128, 0, st>>>(S, c, t, b.p, z.p), ::pf::g_launches++;
+    }
+    if (total_g) dev::k_constraint_values<<<dim3(4, S.nsub), 128, 0, st>>>(S, t, gv.p), ::pf::g_launches++;
+    std::vector<double> hb(total_vec);
+    PF_CUDA_CHECK(cudaMemcpyAsync(hb.data(), b.p, sizeof(double) * total_vec, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaMemcpyAsync(Z, z.p, sizeof(double) * total_z, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaMemcpyAsync(g, gv.p, sizeof(double) * total_g, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    long long f = 0;
+    for (int p = 0; p < nown(); ++p) {
+      const SubType& T = D.types[OS(p).type];
+      std::copy(hb.begin() + sub_vec[p], hb.begin() + sub_vec[p] + T.n_u, F_u + f);
+      f += T.n_u;
+    }
+  }
+
+  /// FetiOperator::set_precond (feti.hpp:97): switch the preconditioner.
+  /// identity always; generalized and the mortar scaling are built on first
+  /// use; the Dirichlet one needs its data from creation (explicit Sd_s or the
+  /// interior factors).
+  bool gen_built = false, q_built = false;
+  void set_precond(int pk) {
+    if (pk < PF_PREC_IDENTITY || pk > PF_PREC_DIRICHLET_MORTAR) fail(kInvalid, "set_precond: unknown kind");
+    const bool q = pk == PF_PREC_GENERALIZED_MORTAR || pk == PF_PREC_DIRICHLET_MORTAR;
+    const bool dir = pk == PF_PREC_DIRICHLET || pk == PF_PREC_DIRICHLET_MORTAR;
+    const bool gen = pk == PF_PREC_GENERALIZED || pk == PF_PREC_GENERALIZED_MORTAR;
+    if (dir && !dual && !implicit_dir)
+      fail(kInvalid, "set_precond: the Dirichlet preconditioner's data were not built (create the context with a "
+                     "dirichlet preconditioner)");
+    if (gen && !gen_built) {
+      if (h_K.empty()) {
+        h_K.resize(total_kv);
+        PF_CUDA_CHECK(cudaMemcpy(h_K.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
+      }
+      setup_generalized();
+      gen_built = true;
+    }
+    if (q && !q_built) {
+      setup_q();
+      q_built = true;
+    }
+    use_q = q, use_dir = dir, use_gen = gen;
+    D.cfg.precond = pk;
+    ++graph_gen;
+  }
+
+  /// feti_pcg (feti.hpp:263) on device buffers: rhs into kr_rhs, lambda in/out,
+  /// at the given tolerance and iteration cap
+  void krylov_with(double* lambda, double tol, int max_iter, pf_report& rep) {
+    if (!(tol > 0.0)) fail(kNotConverged, "feti_pcg: tolerance must be positive");
+    if (max_iter < 0) fail(kInvalid, "feti_pcg: max_iter must be >= 0");
+    if (tol != D.cfg.tol) D.cfg.tol = tol, ++graph_gen;
+    const int keep = D.cfg.max_iter;
+    D.cfg.max_iter = max_iter;
+    fapplies = papplies = 0;
+    try {
+      krylov_solve(lambda, rep);
+    } catch (...) {
+      D.cfg.max_iter = keep;
+      throw;
+    }
+    D.cfg.max_iter = keep;
+    rep.method = krylov, rep.f_applies = fapplies, rep.precond_applies = papplies;
+  }
+
   /// Join the overlapped K^+ b sweep (hb_st) before anything else touches
   /// Ksys.X on the engine stream: the sweep's result moves to hb_Yb, where
   /// back_substitute finds it when hb_pending is clear.  Host-side only (never
@@ -2877,24 +3001,34 @@ struct Engine {
     PF_CUDA_CHECK(cudaStreamWaitEvent(st, hb_ev1, 0));
     PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
     hb_pending = false;
+    hb_valid = true;
   }
+  bool hb_valid = false;  // hb_Yb holds K^+ b of the current right-hand side
 
-  /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> state
-  void back_substitute(const double* lambda) {
+  /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> dst (default: the state)
+  void back_substitute(const double* lambda, double* dst = nullptr) {
+    if (!dst) dst = state.p;
     if (hb_on) {
       const double* yb = hb_Yb.p;
       if (hb_pending) {  // K^+ b from the overlapped sweep, in place in Ksys.X
         PF_CUDA_CHECK(cudaStreamWaitEvent(st, hb_ev1, 0));
         hb_pending = false;
+        hb_valid = false;  // consumed in place
         yb = Ksys.X.p;
+      } else if (!hb_valid) {  // no K^+ b for this right-hand side yet: one sweep
+        perm_in_K(bvec.p);
+        if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p), ::pf::g_launches++;
+        Ksys.solve(st, 1);
+        PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
+        hb_valid = true;
       }
       launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, lambda, dl_xloc.p);
       launch_pdl(dev::k_h_gemm, hb_nwork, dev::kGThreads, 0, st, hb_work.p, hb_H.p, hb_cin.p, hb_cout.p, dl_xloc.p,
                  yb, Ksys.X.p);
-      perm_out_K(state.p);
+      perm_out_K(dst);
       if (nc && nfloat_local)
         dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
-                                                                d_fxyoff.p, alpha_vec.p, state.p); ::pf::g_launches++;
+                                                                d_fxyoff.p, alpha_vec.p, dst); ::pf::g_launches++;
       return;
     }
     perm_in_K(bvec.p);
@@ -2903,10 +3037,10 @@ struct Engine {
                                                                g_back.idx.p, g_back.val.p, lambda, Ksys.X.p, -1.0, 1); ::pf::g_launches++;
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
     Ksys.solve(st, 1);
-    perm_out_K(state.p);
+    perm_out_K(dst);
     if (nc && nfloat_local)
       dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
-                                                              d_fxyoff.p, alpha_vec.p, state.p); ::pf::g_launches++;
+                                                              d_fxyoff.p, alpha_vec.p, dst); ::pf::g_launches++;
   }
 
   // ------------------------------------------------------------------
@@ -3098,6 +3232,9 @@ struct Engine {
   /// maxit iterations are reached: a graph whose single conditional WHILE node
   /// holds the captured iteration plus k_loop_cond (cudaGraphSetConditional).
   /// One launch and one status read per Krylov solve.
+  // captured graphs hold the tolerance and the preconditioner choice: any
+  // change of either bumps graph_gen and forces a re-capture
+  int graph_gen = 0, lp_gen = -1, kr_gen = -1;
   cudaGraphExec_t lp_exec = nullptr;
   const void* lp_key_ptr = nullptr;
   int lp_key_kind = 0, lp_maxit = 0;
@@ -3110,7 +3247,7 @@ struct Engine {
   int lp_cap_maxit = 0;
   template <class Fn>
   void graphed_loop(const void* key, int kind, int maxit, Fn&& body) {
-    if (!lp_exec || lp_key_ptr != key || lp_key_kind != kind || lp_maxit != maxit) {
+    if (!lp_exec || lp_key_ptr != key || lp_key_kind != kind || lp_maxit != maxit || lp_gen != graph_gen) {
       if (lp_exec) cudaGraphExecDestroy(lp_exec), lp_exec = nullptr;
       cudaGraph_t g;
       PF_CUDA_CHECK(cudaGraphCreate(&g, 0));
@@ -3135,7 +3272,7 @@ struct Engine {
       PF_CUDA_CHECK(cudaGraphDestroy(g));
       lp_nlaunch = ::pf::g_launches - l0, ::pf::g_launches = l0;
       lp_dF = fapplies - f0, lp_dM = papplies - m0, fapplies = f0, papplies = m0;
-      lp_key_ptr = key, lp_key_kind = kind, lp_maxit = maxit;
+      lp_key_ptr = key, lp_key_kind = kind, lp_maxit = maxit, lp_gen = graph_gen;
     }
     const int it0 = h_status[1];
     PF_CUDA_CHECK(cudaGraphLaunch(lp_exec, st));
@@ -3161,7 +3298,7 @@ struct Engine {
       body();
       return;
     }
-    if (!kr_exec || kr_key_ptr != key || kr_key_kind != kind) {
+    if (!kr_exec || kr_key_ptr != key || kr_key_kind != kind || kr_gen != graph_gen) {
       if (kr_exec) cudaGraphExecDestroy(kr_exec), kr_exec = nullptr;
       const long long l0 = ::pf::g_launches;
       const int f0 = fapplies, m0 = papplies;
@@ -3173,7 +3310,7 @@ struct Engine {
       PF_CUDA_CHECK(cudaGraphDestroy(g));
       kr_nlaunch = ::pf::g_launches - l0, ::pf::g_launches = l0;
       kr_dF = fapplies - f0, kr_dM = papplies - m0, fapplies = f0, papplies = m0;
-      kr_key_ptr = key, kr_key_kind = kind;
+      kr_key_ptr = key, kr_key_kind = kind, kr_gen = graph_gen;
     }
     PF_CUDA_CHECK(cudaGraphLaunch(kr_exec, st));
     ::pf::g_launches += kr_nlaunch;
@@ -3271,6 +3408,7 @@ struct Engine {
         lam.zero(st);
       }
       krylov_solve(lam.p, rep);
+      last_hist_n = std::min(rep.iterations, dev::kHistCap) + 1;
       if (!rep.converged) {
         char buf[160];
         std::snprintf(buf, sizeof(buf), "PCG stalled at relative residual %f after %d iterations", rep.rel_residual,
@@ -3278,12 +3416,7 @@ struct Engine {
         fail(kNotConverged, buf);
       }
       cudaEventRecord(e2, st);
-      if (nc > 0) {
-        // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
-        F_(lam.p, kr_tmp.p);
-        dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, kr_rhs.p, 1.0, kr_tmp.p); ::pf::g_launches++;
-        coarse_solve(kr_tmp.p, alpha_vec.p);
-      }
+      recover_rigid(lam.p);  // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
       back_substitute(lam.p);
       cudaEventRecord(e3, st);
       PF_CUDA_CHECK(cudaEventSynchronize(e3));
@@ -3796,8 +3929,187 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
 
 int pf_local_matrices(const double* tri, double mu, double kperm, double mu_f, int order, double* elastic,
                       double* div, double* mass, double* diffusion) {
-  (void)tri, (void)mu, (void)kperm, (void)mu_f, (void)order, (void)elastic, (void)div, (void)mass, (void)diffusion;
-  return PF_INVALID;  // provided through the assembled-matrix parity tests
+  if (!tri || !elastic || !div || !mass || !diffusion || (order != 1 && order != 2)) return PF_INVALID;
+  return guarded(nullptr, [&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) pf::fail(pf::kCuda, "no CUDA device");
+    const double ax = tri[2] - tri[0], ay = tri[3] - tri[1], bx = tri[4] - tri[0], by = tri[5] - tri[1];
+    if (std::abs(ax * by - bx * ay) < 1e-14) pf::fail(pf::kInvalid, "degenerate triangle");  // elements.hpp:139
+    const int nb = order == 2 ? 6 : 3;
+    const std::size_t ne = 4 * nb * nb, nd = 3 * 2 * nb;
+    pf::DevBuf<double> d;
+    d.alloc(6 + ne + nd + 18);
+    PF_CUDA_CHECK(cudaMemcpy(d.p, tri, 6 * sizeof(double), cudaMemcpyHostToDevice));
+    double* de = d.p + 6;
+    double* dd = de + ne;
+    double* dm = dd + nd;
+    pf::dev::k_local_forms<<<1, 64>>>(d.p, order, mu, kperm, mu_f, de, dd, dm, dm + 9);
+    ::pf::g_launches++;
+    PF_CUDA_CHECK(cudaGetLastError());
+    std::vector<double> h(ne + nd + 18);
+    PF_CUDA_CHECK(cudaMemcpy(h.data(), de, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+    std::copy(h.begin(), h.begin() + ne, elastic);
+    std::copy(h.begin() + ne, h.begin() + ne + nd, div);
+    std::copy(h.begin() + ne + nd, h.begin() + ne + nd + 9, mass);
+    std::copy(h.begin() + ne + nd + 9, h.end(), diffusion);
+  });
+}
+
+// ---- FetiOperator / StepSolver pieces the reference exposes ----------------
+
+int pf_krylov(pf_ctx* ctx, const double* rhs, const double* lambda0, double tol, int max_iter, double* lambda_out,
+              pf_report* rep) {
+  if (!ctx || !rhs || !lambda0 || !lambda_out) return PF_INVALID;
+  pf_report local{};
+  const int rc = guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    const int n = E.D.n_lambda;
+    if (!E.kr_user.p) E.kr_user.alloc(std::max(1, n));
+    PF_CUDA_CHECK(cudaMemcpyAsync(E.kr_rhs.p, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, E.st));
+    PF_CUDA_CHECK(cudaMemcpyAsync(E.kr_user.p, lambda0, sizeof(double) * n, cudaMemcpyHostToDevice, E.st));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0), cudaEventCreate(&e1);
+    cudaEventRecord(e0, E.st);
+    bool stalled = false;
+    try {
+      E.krylov_with(E.kr_user.p, tol, max_iter, local);
+      stalled = !local.converged;
+    } catch (...) {
+      cudaEventDestroy(e0), cudaEventDestroy(e1);
+      throw;
+    }
+    cudaEventRecord(e1, E.st);
+    PF_CUDA_CHECK(cudaMemcpyAsync(lambda_out, E.kr_user.p, sizeof(double) * n, cudaMemcpyDeviceToHost, E.st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    local.t_krylov = local.seconds = ms * 1e-3;
+    E.last_hist_n = std::min(local.iterations, pf::dev::kHistCap) + 1;
+    if (stalled) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "feti_pcg stalled at relative residual %g after %d iterations",
+                    local.rel_residual, local.iterations);
+      pf::fail(pf::kNotConverged, buf);
+    }
+  });
+  if (rep) *rep = local;
+  return rc;
+}
+
+int pf_last_history(const pf_ctx* ctx, double* out, int cap) {
+  if (!ctx) return -PF_INVALID;
+  auto& E = const_cast<pf_ctx*>(ctx)->eng;
+  const int n = E.last_hist_n;
+  if (out && cap > 0 && n > 0) {
+    const int k = std::min(n, cap);
+    if (cudaMemcpy(out, E.scal.p + pf::dev::KS_HIST0, sizeof(double) * k, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -PF_CUDA;
+  }
+  return n;
+}
+
+int pf_back_substitute(pf_ctx* ctx, const double* lambda, double* x_out) {
+  if (!ctx || !lambda || !x_out) return PF_INVALID;
+  return guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    const int n = E.D.n_lambda;
+    if (!E.kr_user.p) E.kr_user.alloc(std::max(1, n));
+    if (!E.bs_out.p) E.bs_out.alloc(std::max<long long>(1, E.total_vec));
+    PF_CUDA_CHECK(cudaMemcpyAsync(E.kr_user.p, lambda, sizeof(double) * n, cudaMemcpyHostToDevice, E.st));
+    E.recover_rigid(E.kr_user.p);
+    E.back_substitute(E.kr_user.p, E.bs_out.p);
+    PF_CUDA_CHECK(cudaMemcpyAsync(x_out, E.bs_out.p, sizeof(double) * E.total_vec, cudaMemcpyDeviceToHost, E.st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
+  });
+}
+
+int pf_set_precond(pf_ctx* ctx, int kind) {
+  if (!ctx) return PF_INVALID;
+  return guarded(ctx, [&] { ctx->eng.set_precond(kind); });
+}
+
+int pf_field_size(const pf_ctx* ctx, int field, int s_global) {
+  if (!ctx || field < PF_FIELD_U || field > PF_FIELD_P) return -PF_INVALID;
+  const auto& E = ctx->eng;
+  auto one = [&](int s) -> int {
+    const auto& T = E.D.types[E.D.subs[s].type];
+    if (T.region != pf::kP && (field == PF_FIELD_ETA || field == PF_FIELD_P)) return 0;
+    return field == PF_FIELD_U ? T.n_u : T.n_s;
+  };
+  if (s_global >= 0) {
+    if (s_global >= (int)E.D.subs.size() || E.local_of[s_global] < 0) return -PF_INVALID;
+    return one(s_global);
+  }
+  int n = 0;
+  for (int p = 0; p < E.nown(); ++p) n += one(E.own[p]);
+  return n;
+}
+
+int pf_get_field(pf_ctx* ctx, int field, int s_global, double* out) {
+  if (!ctx || !out) return PF_INVALID;
+  if (pf_field_size(ctx, field, s_global) < 0) return PF_INVALID;
+  return guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    long long o = 0;
+    for (int p = 0; p < E.nown(); ++p) {
+      if (s_global >= 0 && E.own[p] != s_global) continue;
+      const auto& T = E.D.types[E.OS(p).type];
+      if (T.region != pf::kP && (field == PF_FIELD_ETA || field == PF_FIELD_P)) continue;
+      const int off = field == PF_FIELD_U ? 0 : field == PF_FIELD_XI ? T.off_xi : field == PF_FIELD_ETA ? T.off_eta : T.off_p;
+      const int len = field == PF_FIELD_U ? T.n_u : T.n_s;
+      PF_CUDA_CHECK(cudaMemcpyAsync(out + o, E.state.p + E.sub_vec[p] + off, sizeof(double) * len,
+                                    cudaMemcpyDeviceToHost, E.st));
+      o += len;
+    }
+    PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
+  });
+}
+
+int pf_get_constraints(const pf_ctx* ctx, int s_global, int* saddle_index, int* component, double* xy) {
+  if (!ctx || s_global < 0 || s_global >= (int)ctx->eng.D.subs.size()) return -PF_INVALID;
+  const auto& E = ctx->eng;
+  const int p = E.local_of[s_global];
+  if (p < 0) return -PF_INVALID;
+  const auto& T = E.D.types[E.D.subs[s_global].type];
+  const long long g0 = E.h_fsubs[p].gval;
+  for (std::size_t k = 0; k < T.cons.size(); ++k) {
+    if (saddle_index) saddle_index[k] = T.cons[k].sidx;
+    if (component) component[k] = T.cons[k].comp;
+    if (xy) xy[2 * k] = E.h_cxy[2 * (g0 + k)], xy[2 * k + 1] = E.h_cxy[2 * (g0 + k) + 1];
+  }
+  return (int)T.cons.size();
+}
+
+int pf_load_sizes(const pf_ctx* ctx, long long* n_F, long long* n_Z, long long* n_g) {
+  if (!ctx) return PF_INVALID;
+  const auto& E = ctx->eng;
+  long long f = 0, z = 0;
+  for (int p = 0; p < E.nown(); ++p) {
+    const auto& T = E.D.types[E.OS(p).type];
+    f += T.n_u;
+    if (T.region == pf::kP) z += T.n_s;
+  }
+  if (n_F) *n_F = f;
+  if (n_Z) *n_Z = z;
+  if (n_g) *n_g = E.total_g;
+  return PF_OK;
+}
+
+int pf_scenario_loads(pf_ctx* ctx, double t, double* F_u, double* Z, double* g) {
+  if (!ctx || !F_u || !Z || !g) return PF_INVALID;
+  return guarded(ctx, [&] { ctx->eng.scenario_loads(t, F_u, Z, g); });
+}
+
+int pf_set_loads(pf_ctx* ctx, const double* F_u, const double* Z, const double* g, int persistent) {
+  if (!ctx) return PF_INVALID;
+  return guarded(ctx, [&] { ctx->eng.set_loads(F_u, Z, g, persistent != 0); });
+}
+
+int pf_clear_loads(pf_ctx* ctx) {
+  if (!ctx) return PF_INVALID;
+  ctx->eng.loads_set = false;
+  return PF_OK;
 }
 
 }  // extern "C"

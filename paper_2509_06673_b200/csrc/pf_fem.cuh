@@ -137,6 +137,98 @@ __device__ __forceinline__ void add_entry(const FemSet& S, const FemType& T, con
   }
 }
 
+/// Geometry of an arbitrary triangle (AffineMap, elements.hpp:132-144): J =
+/// [v1 - v0, v2 - v0], I = J^{-T}.
+__device__ __forceinline__ void affine_map(const double* tri, Elem& E) {
+  E.ax = tri[0], E.ay = tri[1];
+  E.J00 = tri[2] - tri[0], E.J10 = tri[3] - tri[1], E.J01 = tri[4] - tri[0], E.J11 = tri[5] - tri[1];
+  E.det = E.J00 * E.J11 - E.J01 * E.J10;
+  E.I00 = E.J11 / E.det, E.I01 = -E.J10 / E.det, E.I10 = -E.J01 / E.det, E.I11 = E.J00 / E.det;
+}
+
+/// local_elastic_matrix (elements.hpp:152-175) entry block (i, j): the 2x2
+/// component block 2 mu int eps(phi_i e_a) : eps(phi_j e_b), Dunavant degree 4
+__device__ __forceinline__ void elastic_block(int order, const Elem& E, double mu, int i, int j, double& a00,
+                                              double& a01, double& a10, double& a11) {
+  double v[6], rgx[6], rgy[6];
+  const double adet = fabs(E.det);
+  a00 = a01 = a10 = a11 = 0.0;
+  for (int q = 0; q < 6; ++q) {
+    basis(order, c_qx[q], c_qy[q], v, rgx, rgy);
+    const double gix = E.I00 * rgx[i] + E.I01 * rgy[i], giy = E.I10 * rgx[i] + E.I11 * rgy[i];
+    const double gjx = E.I00 * rgx[j] + E.I01 * rgy[j], gjy = E.I10 * rgx[j] + E.I11 * rgy[j];
+    const double w = 2.0 * mu * (c_qw[q] * adet);
+    a00 += w * (gix * gjx + 0.5 * giy * gjy);
+    a01 += w * 0.5 * giy * gjx;
+    a10 += w * 0.5 * gix * gjy;
+    a11 += w * (giy * gjy + 0.5 * gix * gjx);
+  }
+}
+
+/// local_div_matrix (elements.hpp:178-197) entries (i, 2j), (i, 2j+1):
+/// -int psi_i d_c phi_j
+__device__ __forceinline__ void div_pair(int order, const Elem& E, int i, int j, double& bx, double& by) {
+  double v[6], rgx[6], rgy[6], sv[3], sgx[3], sgy[3];
+  const double adet = fabs(E.det);
+  bx = by = 0.0;
+  for (int q = 0; q < 6; ++q) {
+    basis(order, c_qx[q], c_qy[q], v, rgx, rgy);
+    basis(1, c_qx[q], c_qy[q], sv, sgx, sgy);
+    const double gjx = E.I00 * rgx[j] + E.I01 * rgy[j], gjy = E.I10 * rgx[j] + E.I11 * rgy[j];
+    const double w = c_qw[q] * adet;
+    bx -= w * sv[i] * gjx;
+    by -= w * sv[i] * gjy;
+  }
+}
+
+/// local_mass_matrix (elements.hpp:199-212) and local_diffusion_matrix
+/// (elements.hpp:215-230, isotropic K = kk I) entries (i, j)
+__device__ __forceinline__ void mass_diffusion(const Elem& E, double kk, double mu_f, int i, int j, double& m,
+                                               double& d) {
+  double sv[3], sgx[3], sgy[3];
+  const double adet = fabs(E.det);
+  m = d = 0.0;
+  for (int q = 0; q < 6; ++q) {
+    basis(1, c_qx[q], c_qy[q], sv, sgx, sgy);
+    const double w = c_qw[q] * adet;
+    m += w * sv[i] * sv[j];
+    const double gix = E.I00 * sgx[i] + E.I01 * sgy[i], giy = E.I10 * sgx[i] + E.I11 * sgy[i];
+    const double gjx = E.I00 * sgx[j] + E.I01 * sgy[j], gjy = E.I10 * sgx[j] + E.I11 * sgy[j];
+    d += (c_qw[q] * adet / mu_f) * ((kk * gjx) * gix + (kk * gjy) * giy);
+  }
+}
+
+/// The element-level entry point (pf_local_matrices): the four local forms of
+/// one triangle, thread per entry, by the same device functions the assembly
+/// kernel uses.  Outputs row-major: elastic 2nb x 2nb, div 3 x 2nb, mass and
+/// diffusion 3 x 3.
+__global__ void k_local_forms(const double* tri, int order, double mu, double kk, double mu_f, double* elastic,
+                              double* div, double* mass, double* diffusion) {
+  Elem E;
+  affine_map(tri, E);
+  const int nb = order == 2 ? 6 : 3;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nb * nb) {
+    const int i = t / nb, j = t % nb;
+    double a00, a01, a10, a11;
+    elastic_block(order, E, mu, i, j, a00, a01, a10, a11);
+    const int n2 = 2 * nb;
+    elastic[(2 * i) * n2 + 2 * j] = a00, elastic[(2 * i) * n2 + 2 * j + 1] = a01;
+    elastic[(2 * i + 1) * n2 + 2 * j] = a10, elastic[(2 * i + 1) * n2 + 2 * j + 1] = a11;
+  }
+  if (t < 3 * nb) {
+    const int i = t / nb, j = t % nb;
+    double bx, by;
+    div_pair(order, E, i, j, bx, by);
+    div[i * 2 * nb + 2 * j] = bx, div[i * 2 * nb + 2 * j + 1] = by;
+  }
+  if (t < 9) {
+    double m, d;
+    mass_diffusion(E, kk, mu_f, t / 3, t % 3, m, d);
+    mass[t] = m, diffusion[t] = d;
+  }
+}
+
 /// K1: element assembly of one colour into the constrained saddles + lifting.
 __global__ void k_assemble(FemSet S, int color, double* Kv, double* Lv) {
   int sub;
@@ -147,42 +239,23 @@ __global__ void k_assemble(FemSet S, int color, double* Kv, double* Lv) {
   const int nb = S.order == 2 ? 6 : 3;
   const bool P = T.region == 0;
   const double mu = P ? S.mu_P : S.mu_E;
-  const double adet = fabs(E.det);
   double kk = S.kperm;
   if (S.kelem) kk = S.kelem[E.gl];
-  double v[6], rgx[6], rgy[6], sv[3], sgx[3], sgy[3];
-  // elastic block and div block, accumulated per (i, j) over quadrature points
+  // elastic block and div block (elements.hpp:152-197)
   for (int i = 0; i < nb; ++i) {
     for (int j = 0; j < nb; ++j) {
-      double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
-      for (int q = 0; q < 6; ++q) {
-        basis(S.order, c_qx[q], c_qy[q], v, rgx, rgy);
-        const double gix = E.I00 * rgx[i] + E.I01 * rgy[i], giy = E.I10 * rgx[i] + E.I11 * rgy[i];
-        const double gjx = E.I00 * rgx[j] + E.I01 * rgy[j], gjy = E.I10 * rgx[j] + E.I11 * rgy[j];
-        const double w = 2.0 * mu * (c_qw[q] * adet);
-        a00 += w * (gix * gjx + 0.5 * giy * gjy);
-        a01 += w * 0.5 * giy * gjx;
-        a10 += w * 0.5 * gix * gjy;
-        a11 += w * (giy * gjy + 0.5 * gix * gjx);
-      }
-      double* Kv_ = Kv;
-      add_entry(S, T, F, Kv_, Lv, 2 * E.un[i], 2 * E.un[j], a00);
-      add_entry(S, T, F, Kv_, Lv, 2 * E.un[i], 2 * E.un[j] + 1, a01);
-      add_entry(S, T, F, Kv_, Lv, 2 * E.un[i] + 1, 2 * E.un[j], a10);
-      add_entry(S, T, F, Kv_, Lv, 2 * E.un[i] + 1, 2 * E.un[j] + 1, a11);
+      double a00, a01, a10, a11;
+      elastic_block(S.order, E, mu, i, j, a00, a01, a10, a11);
+      add_entry(S, T, F, Kv, Lv, 2 * E.un[i], 2 * E.un[j], a00);
+      add_entry(S, T, F, Kv, Lv, 2 * E.un[i], 2 * E.un[j] + 1, a01);
+      add_entry(S, T, F, Kv, Lv, 2 * E.un[i] + 1, 2 * E.un[j], a10);
+      add_entry(S, T, F, Kv, Lv, 2 * E.un[i] + 1, 2 * E.un[j] + 1, a11);
     }
   }
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < nb; ++j) {
-      double bx = 0, by = 0;
-      for (int q = 0; q < 6; ++q) {
-        basis(S.order, c_qx[q], c_qy[q], v, rgx, rgy);
-        basis(1, c_qx[q], c_qy[q], sv, sgx, sgy);
-        const double gjx = E.I00 * rgx[j] + E.I01 * rgy[j], gjy = E.I10 * rgx[j] + E.I11 * rgy[j];
-        const double w = c_qw[q] * adet;
-        bx -= w * sv[i] * gjx;
-        by -= w * sv[i] * gjy;
-      }
+      double bx, by;
+      div_pair(S.order, E, i, j, bx, by);
       const int si = T.off_xi + E.v[i];
       add_entry(S, T, F, Kv, Lv, si, 2 * E.un[j], bx);       // B
       add_entry(S, T, F, Kv, Lv, si, 2 * E.un[j] + 1, by);
@@ -191,15 +264,8 @@ __global__ void k_assemble(FemSet S, int color, double* Kv, double* Lv) {
     }
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) {
-      double m = 0, d = 0;
-      for (int q = 0; q < 6; ++q) {
-        basis(1, c_qx[q], c_qy[q], sv, sgx, sgy);
-        const double w = c_qw[q] * adet;
-        m += w * sv[i] * sv[j];
-        const double gix = E.I00 * sgx[i] + E.I01 * sgy[i], giy = E.I10 * sgx[i] + E.I11 * sgy[i];
-        const double gjx = E.I00 * sgx[j] + E.I01 * sgy[j], gjy = E.I10 * sgx[j] + E.I11 * sgy[j];
-        d += (c_qw[q] * adet / S.mu_f) * ((kk * gjx) * gix + (kk * gjy) * giy);
-      }
+      double m, d;
+      mass_diffusion(E, kk, S.mu_f, i, j, m, d);
       const int vi = E.v[i], vj = E.v[j];
       if (P) {
         add_entry(S, T, F, Kv, Lv, T.off_eta + vi, T.off_eta + vj, S.k2 * m);

@@ -287,6 +287,13 @@ enum : int {
   KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR
 };
 enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5 };
+/// residual history (REF PcgReport::residual_history, feti.hpp:65): entry k at
+/// sc[KS_HIST0 + k], k = 0 .. kHistCap (absolute: sqrt(r.z) for PCG, the
+/// quasi-residual tau_k for SQMR), written by the single-thread scalar updates
+constexpr int KS_HIST0 = 64, kHistCap = 8192;
+__device__ __forceinline__ void ks_hist(double* sc, int k, double v) {
+  if (k >= 0 && k <= kHistCap) sc[KS_HIST0 + k] = v;
+}
 
 /// y += sgn * (*coef) * x
 __global__ void k_axpy_s(int n, const double* coef, double sgn, const double* x, double* y) {
@@ -324,6 +331,7 @@ __global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d,
 __device__ __forceinline__ void ks_sqmr_init(double* sc, int* status, double tol) {
   const double t0 = sqrt(sc[KS_RR]);
   sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0, sc[KS_THR] = tol * t0;
+  ks_hist(sc, 0, t0);
   status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
 }
@@ -350,6 +358,7 @@ __device__ __forceinline__ void ks_sqmr_tau(double* sc, int* status, double tol)
   sc[KS_THOLD] = th_old, sc[KS_THETA] = theta, sc[KS_C] = c, sc[KS_TAU] = tau;
   sc[KS_REL] = tau / sc[KS_T0];
   status[1] += 1;
+  ks_hist(sc, status[1], tau);
   // quasi-residual tau_k below the threshold (tol ||r0||, tightened after a
   // failed true-residual check): candidate convergence, confirmed by the host
   if (status[0] == KST_RUN && tau <= sc[KS_THR]) status[0] = KST_CONV;
@@ -362,6 +371,7 @@ __device__ __forceinline__ void ks_sqmr_b(double* sc, int* status) {
 __device__ __forceinline__ void ks_pcg_init(double* sc, int* status) {
   const double d0 = sqrt(fmax(sc[KS_RZ], 0.0));
   sc[KS_D0] = d0, sc[KS_REL] = 1.0;
+  ks_hist(sc, 0, d0);
   status[0] = (d0 == 0.0 || !(d0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
 }
@@ -374,6 +384,7 @@ __device__ __forceinline__ void ks_pcg_beta(double* sc, int* status, double tol)
   const double delta = sqrt(fmax(rzn, 0.0));
   sc[KS_REL] = delta / sc[KS_D0];
   status[1] += 1;
+  ks_hist(sc, status[1], delta);
   if (status[0] != KST_RUN) return;
   if (delta <= tol * sc[KS_D0]) {
     status[0] = KST_CONV;

@@ -1,0 +1,30 @@
+"""compute-sanitizer over the engine's kernels (memcheck, racecheck,
+synccheck) on a c1 step and a 4x4-subdomain c4 step: the hand-written
+mbarrier/TMA ring of the sweeps, programmatic dependent launch (prefetch
+before griddepcontrol.wait) and the two-stream overlap of the
+back-substitution sweep."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("case", ["c1", "c4s"])
+def test_sanitizer_clean(tool, case):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    env = dict(os.environ, PF_NO_GRAPH="1") if tool != "memcheck" else dict(os.environ)
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20",
+           sys.executable, os.path.join(ROOT, "scripts", "sanitize_step.py"), case]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env, cwd=ROOT)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-4000:]
+    assert "sanitize_step ok" in out
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
