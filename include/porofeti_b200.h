@@ -206,6 +206,11 @@ long long pf_launch_count(void);
  * factor-sweep kernels per F-apply and the number of launches per F-apply */
 int pf_kernel_stats(pf_ctx* ctx, double* sweep_ms, int* launches_per_apply);
 
+/* Setup phase wall times of pf_create (each phase ends with a stream sync):
+ * names joined by ';' into names (cap bytes, may be NULL), seconds into secs
+ * (may be NULL; room for the returned count, <= 32). */
+int pf_setup_phases(const pf_ctx* ctx, char* names, int cap, double* secs);
+
 /* Per-kernel timing of the sweeps (see pf_engine.cu): 10 doubles. */
 int pf_phase_stats(pf_ctx* ctx, int iters, double* out);
 

@@ -219,6 +219,7 @@ def lib():
         L.pf_scenario_loads.argtypes = [vp, C.c_double, vp, vp, vp]
         L.pf_set_loads.argtypes = [vp, vp, vp, vp, C.c_int]
         L.pf_clear_loads.argtypes = [vp]
+        L.pf_setup_phases.argtypes = [vp, C.c_char_p, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -316,6 +317,14 @@ class FetiOperator:
         _check(lib().pf_interface_rhs(self.h, _ptr(F)), self.h)
         return F
 
+    def setup_phases(self):
+        """{phase: seconds} of pf_create (setup breakdown)"""
+        buf = C.create_string_buffer(4096)
+        secs = np.zeros(32)
+        n = lib().pf_setup_phases(self.h, buf, 4096, _ptr(secs))
+        names = buf.value.decode().split(";") if n > 0 else []
+        return {k: float(v) for k, v in zip(names, secs[:n])}
+
     def set_precond(self, kind):
         """FetiOperator::set_precond (feti.hpp:97): a PRECONDS name."""
         _check(lib().pf_set_precond(self.h, PRECONDS[kind]), self.h)
@@ -357,7 +366,7 @@ class FetiOperator:
         subdomain concatenated (s = -1)"""
         f = self.FIELDS[name]
         n = lib().pf_field_size(self.h, f, s)
-        if n < 0:
+        if n < 0 or (n == 0 and s >= 0):
             raise ConfigError(f"field {name!r} of subdomain {s}: not available")
         out = np.empty(n)
         _check(lib().pf_get_field(self.h, f, s, _ptr(out)), self.h)

