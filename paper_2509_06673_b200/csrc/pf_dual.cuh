@@ -128,16 +128,36 @@ __global__ void __launch_bounds__(512) k_dual_root(DualSet S) {
     }
     if (tid < PW) Dk[tid] = tid < pw ? at(p0 + tid, p0 + tid) : 0.0;
     __syncthreads();
-    for (int c = r0 + warp; c < m; c += nw) {
-      double w[PW];
+    // trailing update A22 -= L_p D_p L_p^T on the FP64 tensor cores: 8x8
+    // output tiles of the lower triangle (I >= J), warp per tile, K = the
+    // panel width in m8n8k4 steps (A fragment: L_p row lane/4, column lane%4;
+    // B fragment: D_k L_p(c, k) for column lane/4; C: row lane/4, columns
+    // 2 (lane%4) + {0,1}); padded panel columns are zero
+    {
+      const int nt8 = (nr + 7) >> 3;
+      const int ntile = nt8 * (nt8 + 1) / 2;
+      const int fr = lane >> 2, fk = lane & 3;
+      for (int q = warp; q < ntile; q += nw) {
+        int I = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+        while ((I + 1) * (I + 2) / 2 <= q) ++I;
+        while (I * (I + 1) / 2 > q) --I;
+        const int J = q - I * (I + 1) / 2;
+        const int ra = I * 8 + fr, cb = J * 8 + fr;
+        double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int k = 0; k < PW; ++k) w[k] = Dk[k] * Lp[(c - r0) * LD + k];
-      for (int i = c + lane; i < m; i += 32) {
-        const double* li = Lp + (i - r0) * LD;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < PW; k += 2) a0 += li[k] * w[k], a1 += li[k + 1] * w[k + 1];
-        at(i, c) -= a0 + a1;
+        for (int k4 = 0; k4 < PW; k4 += 4) {
+          const int kk = k4 + fk;
+          const double af = ra < nr ? Lp[ra * LD + kk] : 0.0;
+          const double bf = cb < nr ? Dk[kk] * Lp[cb * LD + kk] : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c0), "+d"(c1)
+                       : "d"(af), "d"(bf));
+        }
+        const int r = I * 8 + fr, cc = J * 8 + 2 * fk;
+        if (r < nr) {
+          if (cc < nr && r >= cc) at(r0 + r, r0 + cc) -= c0;
+          if (cc + 1 < nr && r >= cc + 1) at(r0 + r, r0 + cc + 1) -= c1;
+        }
       }
     }
     __syncthreads();

@@ -186,7 +186,12 @@ struct SolveSystem {
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
 
-  void build(const std::vector<const SymFactor*>& types, const std::vector<int>& ptype, int nrhs) {
+  // factor values read from another system's buffer (virtual problems that
+  // share factors): per-problem offsets into it given to build()
+  const double* Lext = nullptr;
+
+  void build(const std::vector<const SymFactor*>& types, const std::vector<int>& ptype, int nrhs,
+             const std::vector<long long>* lval_ext = nullptr) {
     syms = types;
     prob_type = ptype;
     nrhs_alloc = nrhs;
@@ -272,8 +277,8 @@ struct SolveSystem {
       const SymFactor& F = *types[ptype[p]];
       total_L = (total_L + 1) & ~1LL;  // 16-byte aligned value streams
       total_x = (total_x + 1) & ~1LL;  // 16-byte aligned pivot rows for the bulk copies
-      prob_x[p] = total_x, prob_lval[p] = total_L, prob_cb[p] = total_cb;
-      total_x += F.n, total_L += F.nval, total_cb += (long long)F.cb_rows.size();
+      prob_x[p] = total_x, prob_lval[p] = lval_ext ? (*lval_ext)[p] : total_L, prob_cb[p] = total_cb;
+      total_x += F.n, total_L += lval_ext ? 0 : F.nval, total_cb += (long long)F.cb_rows.size();
       nnzL += F.nval;
       for (int t = 0; t < F.ntask; ++t) {
         const int gl = glevel(F, F.task_level[t]);
@@ -357,7 +362,7 @@ struct SolveSystem {
     S.nprob = (int)prob_type.size();
     S.prob_type = d_prob_type.p, S.prob_lval = d_prob_lval.p, S.prob_x = d_prob_x.p, S.prob_cb = d_prob_cb.p;
     S.nwork = level_nwork[level], S.work_prob = d_wp[level].p, S.work_task = d_wt[level].p, S.work = d_work[level].p;
-    S.L = L.p, S.D = D.p, S.X = X.p, S.CB = CB.p;
+    S.L = Lext ? Lext : L.p, S.D = D.p, S.X = X.p, S.CB = CB.p;
     S.nrhs = nrhs;
     S.x_stride = total_x, S.cb_stride = total_cb;
     return S;
@@ -1209,8 +1214,10 @@ struct Engine {
       PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev0, cudaEventDisableTiming));
       PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev1, cudaEventDisableTiming));
     }
+    mark("cuda context");
     nthreads = cfg.threads > 0 ? cfg.threads : (int)std::max(1u, std::thread::hardware_concurrency());
     D = build_disc(cfg, kover);
+    mark("discretization");
     rank = rank_, nranks = std::max(1, nranks_);
     if (rank < 0 || rank >= nranks) fail(kInvalid, "rank out of range");
     local_of.assign(D.subs.size(), -1);
@@ -1248,6 +1255,7 @@ struct Engine {
       parallel_for(nt, nthreads, [&](int t) {
         if (rep[t] >= 0) dtypes[t] = build_dual_type(D.types[t], D.subs[rep[t]]);
       });
+    mark("dual symbolic");
     dual = want_dual;
     for (int t = 0; t < nt; ++t)
       if (rep[t] >= 0 && want_dual && !dtypes[t].ok) {
@@ -1278,7 +1286,7 @@ struct Engine {
       }
     });
     const auto t1 = std::chrono::steady_clock::now();
-    mark("symbolic analysis");
+    mark("factor symbolic");
     setup_fem();
     assemble();
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -2784,6 +2792,7 @@ struct Engine {
   // owned subdomain to read its type's factor (bitwise) and to have its
   // type's G entries; PF_BACKSUB=sweep keeps the sweep.
   bool hb_on = false, hb_pending = false;
+  int hb_rounds = 0, hb_virtual = 0;
   DevBuf<double> hb_H, hb_HT, hb_Yb, hb_Bp;
   DevBuf<dev::HWork> hb_work, hb_twork;
   DevBuf<long long> hb_cin, hb_cout, hb_bpo, hb_tin, hb_tout;
@@ -2828,43 +2837,59 @@ struct Engine {
     }
     hb_HT.alloc(std::max<long long>(1, ttot));
     hb_HT.zero(st);
-    int rounds = 0;
-    for (int t = 0; t < nt; ++t)
-      if (!mem[t].empty()) rounds = std::max(rounds, (hn[t] + (int)mem[t].size() - 1) / (int)mem[t].size());
-    DevBuf<double> T;
-    T.alloc(std::max<long long>(1, total_vec));
-    std::vector<long long> hpx(np);
+    std::vector<long long> hpx(Ksys.prob_x.begin(), Ksys.prob_x.end());
+    // H_t = K_t^+ G_t^T for every type in ONE batched sweep: a solve system of
+    // virtual problems, one per column j of each type (hn[t] of them), all
+    // reading the type's factor from Ksys (no copies of the factor values)
     {
-      std::vector<long long> px(Ksys.prob_x.begin(), Ksys.prob_x.end());
-      for (int p = 0; p < np; ++p) hpx[p] = px[p];
-    }
-    for (int k = 0; k < rounds; ++k) {
+      std::vector<int> vtype, vsrc, vcol;
+      std::vector<long long> vl;
+      for (int t = 0; t < nt; ++t)
+        for (int j = 0; j < hn[t]; ++j) {
+          const int p0 = mem[t][0];
+          vtype.push_back(t), vsrc.push_back(p0), vcol.push_back(j), vl.push_back(Ksys.prob_lval[p0]);
+        }
+      const int nv = (int)vtype.size();
+      std::vector<const SymFactor*> kt;
+      for (auto& f : ksym) kt.push_back(&f);
+      SolveSystem Hs;
+      Hs.build(kt, vtype, 1, &vl);
+      Hs.Lext = Ksys.L.p;
+      Hs.prepare_smem();
+      for (int v = 0; v < nv; ++v)  // pivots of the type's factor (per problem, X layout)
+        PF_CUDA_CHECK(cudaMemcpyAsync(Hs.D.p + Hs.prob_x[v], Ksys.D.p + Ksys.prob_x[vsrc[v]],
+                                      sizeof(double) * ksym[vtype[v]].n, cudaMemcpyDeviceToDevice, st));
+      // right-hand sides G_t^T e_j, permuted, zero at the fixing dofs of floating types
       std::vector<long long> idx;
       std::vector<double> val;
       std::vector<dev::HCol> cols;
-      for (int t = 0; t < nt; ++t)
-        for (std::size_t i = 0; i < mem[t].size(); ++i) {
-          const int j = k * (int)mem[t].size() + (int)i;
-          if (j >= hn[t]) continue;
-          const int p = mem[t][i];
-          for (auto& e : ent[p])
-            if (std::get<0>(e) == j) idx.push_back(sub_vec[p] + std::get<1>(e)), val.push_back(std::get<2>(e));
-          cols.push_back(dev::HCol{hpx[p], hoff[t] + j, htoff[t] + (long long)j * hldt[t], hdim[t], hlda[t], hldt[t], 0});
-        }
-      if (cols.empty()) continue;
-      T.zero(st);
+      std::vector<std::vector<char>> isfix(nt);
+      for (int t = 0; t < nt; ++t) {
+        if (mem[t].empty()) continue;
+        isfix[t].assign(D.types[t].dim, 0);
+        if (D.types[t].floating)
+          for (int f : D.types[t].fix) isfix[t][f] = 1;
+      }
+      for (int v = 0; v < nv; ++v) {
+        const int t = vtype[v], j = vcol[v];
+        for (auto& e : ent[vsrc[v]])
+          if (std::get<0>(e) == j && !isfix[t][std::get<1>(e)])
+            idx.push_back(Hs.prob_x[v] + ksym[t].iperm[std::get<1>(e)]), val.push_back(std::get<2>(e));
+        cols.push_back(dev::HCol{Hs.prob_x[v], hoff[t] + j, htoff[t] + (long long)j * hldt[t], hdim[t], hlda[t],
+                                 hldt[t], 0});
+      }
+      Hs.X.zero(st);
       DevBuf<long long> d_idx;
       DevBuf<double> d_val;
       DevBuf<dev::HCol> d_cols;
       d_idx.upload(idx.empty() ? std::vector<long long>{0} : idx), d_val.upload(val.empty() ? std::vector<double>{0.0} : val);
       d_cols.upload(cols);
-      if (!idx.empty()) dev::k_h_scatter<<<cdiv((long long)idx.size(), 256), 256, 0, st>>>((int)idx.size(), d_idx.p, d_val.p, T.p);
-      perm_in_K(T.p);
-      if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p);
-      Ksys.solve(st, 1);
-      dev::k_h_extract<<<dim3(8, (unsigned)cols.size()), 256, 0, st>>>(d_cols.p, Ksys.X.p, hb_H.p, hb_HT.p);
-      ::pf::g_launches += 3 + (nfix ? 1 : 0);
+      if (!idx.empty()) dev::k_h_scatter<<<cdiv((long long)idx.size(), 256), 256, 0, st>>>((int)idx.size(), d_idx.p, d_val.p, Hs.X.p);
+      Hs.solve(st, 1);
+      dev::k_h_extract<<<dim3(8, (unsigned)cols.size()), 256, 0, st>>>(d_cols.p, Hs.X.p, hb_H.p, hb_HT.p);
+      ::pf::g_launches += 2;
       PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      hb_rounds = 1, hb_virtual = nv;
     }
     // per-step GEMM work: 32x32 tiles over (rows of H_t) x (members)
     std::vector<dev::HWork> work;
@@ -2905,8 +2930,8 @@ struct Engine {
     if ((long long)dl_xloc.n < std::max<long long>(1, dl_nslots)) dl_xloc.alloc(std::max<long long>(1, dl_nslots));
     hb_on = true;
     if (std::getenv("PF_VERBOSE"))
-      std::fprintf(stderr, "[pf] explicit back-substitution: %d rounds of sweeps, H %.1f MB, %.2f GFLOP per step\n",
-                   rounds, 8e-6 * (double)tot, 1e-9 * hb_flops);
+      std::fprintf(stderr, "[pf] explicit back-substitution: one sweep over %d virtual problems, H %.1f MB, %.2f GFLOP per step\n",
+                   hb_virtual, 8e-6 * (double)tot, 1e-9 * hb_flops);
   }
 
   /// eta blocks of the poroelastic subdomains and lambda from host buffers

@@ -46,6 +46,43 @@ struct MfSet {
   int write_factor = 1;
 };
 
+constexpr int kMfPW = 16;  // panel width of the front factorisation
+
+/// F[i][c] -= sum_{k in [p0, pe)} L[i][k] d_k L[c][k] for r0 = pe <= c <= i < m
+/// (front column-major, leading dimension m; L columns scaled, d_k on the
+/// diagonal): 8x8 tiles of the lower triangle, warp per tile, mma.sync
+/// m8n8k4.f64 with the panel read through L1 (A: L rows, B: d_k L(c, k));
+/// columns beyond pe contribute zero.  Fixed order per entry (deterministic).
+__device__ __forceinline__ void mf_trailing_update(double* Fk, int m, int p0, int pe, int warp, int lane, int nw) {
+  const int r0 = pe, nr = m - r0;
+  if (nr <= 0) return;
+  const int nt8 = (nr + 7) >> 3, ntile = nt8 * (nt8 + 1) / 2;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int q = warp; q < ntile; q += nw) {
+    int I = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while ((I + 1) * (I + 2) / 2 <= q) ++I;
+    while (I * (I + 1) / 2 > q) --I;
+    const int J = q - I * (I + 1) / 2;
+    const int ra = r0 + I * 8 + fr, cb = r0 + J * 8 + fr;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kMfPW; k4 += 4) {
+      const int k = p0 + k4 + fk;
+      const bool kin = k < pe;
+      const double af = (kin && ra < m) ? Fk[ra + (long long)k * m] : 0.0;
+      const double bf = (kin && cb < m) ? Fk[k + (long long)k * m] * Fk[cb + (long long)k * m] : 0.0;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c0), "+d"(c1)
+                   : "d"(af), "d"(bf));
+    }
+    const int r = r0 + I * 8 + fr, c = r0 + J * 8 + 2 * fk;
+    if (r < m) {
+      if (c < m && r >= c) Fk[r + (long long)c * m] -= c0;
+      if (c + 1 < m && r >= c + 1) Fk[r + (long long)(c + 1) * m] -= c1;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
   const int it = blockIdx.x;
   if (it >= S.nitem) return;
@@ -81,21 +118,30 @@ __global__ void __launch_bounds__(256) k_mf_factor(MfSet S) {
   }
   if (S.type_stop && k == S.type_stop[t]) return;  // root front: left assembled for the dense phase
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = 0; j < nc; ++j) {
-    const double d = Fk[j + (long long)j * m];
-    if (!(d != 0.0) || !isfinite(d)) {
-      if (threadIdx.x == 0) atomicExch(S.err, 1);
-      return;
+  // partial LDL^T of the nc pivot columns in panels of kMfPW: the panel's own
+  // columns by rank-1 updates, then everything right of the panel -- the
+  // remaining pivot columns and the update matrix for the parent -- by one
+  // trailing update F22 -= L_p D_p L_p^T on the FP64 tensor cores
+  for (int p0 = 0; p0 < nc; p0 += kMfPW) {
+    const int pe = min(nc, p0 + kMfPW);
+    for (int j = p0; j < pe; ++j) {
+      const double d = Fk[j + (long long)j * m];
+      if (!(d != 0.0) || !isfinite(d)) {
+        if (threadIdx.x == 0) atomicExch(S.err, 1);
+        return;
+      }
+      const double inv = 1.0 / d;
+      const double* cj = Fk + (long long)j * m;
+      for (int c = j + 1 + warp; c < pe; c += nw) {
+        const double lc = cj[c] * inv;
+        double* col = Fk + (long long)c * m;
+        for (int i = c + lane; i < m; i += 32) col[i] -= cj[i] * lc;
+      }
+      __syncthreads();
+      for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) Fk[i + (long long)j * m] *= inv;
+      __syncthreads();
     }
-    const double inv = 1.0 / d;
-    const double* cj = Fk + (long long)j * m;
-    for (int c = j + 1 + warp; c < m; c += nw) {
-      const double lc = cj[c] * inv;
-      double* col = Fk + (long long)c * m;
-      for (int i = c + lane; i < m; i += 32) col[i] -= cj[i] * lc;
-    }
-    __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) Fk[i + (long long)j * m] *= inv;
+    mf_trailing_update(Fk, m, p0, pe, warp, lane, nw);
     __syncthreads();
   }
   if (!S.write_factor) return;
