@@ -17,6 +17,7 @@
 #pragma once
 
 #include <map>
+#include <thread>
 #include <memory>
 #include <unordered_map>
 
@@ -328,12 +329,17 @@ inline Disc build_disc(const pf_config& cfg, const double* k_override) {
       if (it == type_of.end()) {
         SubType T;
         T.id = (int)D.types.size(), T.region = reg, T.outer = outer, T.pp = pp, T.topo = topo;
-        build_type(T, cfg);
         it = type_of.emplace(key, T.id).first;
         D.types.push_back(std::move(T));
       }
       S.type = it->second;
     }
+  // the per-type patterns are independent: one thread per type
+  {
+    std::vector<std::thread> th;
+    for (auto& T : D.types) th.emplace_back([&T, &cfg] { build_type(T, cfg); });
+    for (auto& t : th) t.join();
+  }
   // interfaces: per subdomain top then right (same enumeration as the oracle)
   for (int sy = 0; sy < D.SY; ++sy)
     for (int sx = 0; sx < D.SX; ++sx) {
@@ -395,10 +401,19 @@ inline Disc build_disc(const pf_config& cfg, const double* k_override) {
   }
   // G / Gc entries with REF accumulation order (edge by edge)
   std::vector<std::map<std::pair<int, int>, double>> G(D.subs.size()), Gc(D.subs.size());
-  for (int f = 0; f < (int)D.ifs.size(); ++f) {
+  // per subdomain (threads), its interfaces in ascending order: every entry
+  // accumulates its contributions in the same order as an interface-major loop
+  std::vector<std::vector<std::pair<int, int>>> ifs_of(D.subs.size());
+  for (int f = 0; f < (int)D.ifs.size(); ++f)
+    ifs_of[D.ifs[f].a].emplace_back(f, 0), ifs_of[D.ifs[f].b].emplace_back(f, 1);
+  const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  auto build_g = [&](int s_begin, int s_step) {
+  for (int s_ = s_begin; s_ < (int)D.subs.size(); s_ += s_step)
+  for (const auto& fs : ifs_of[s_]) {
+    const int f = fs.first;
     const Interface& I = D.ifs[f];
     const int nseg = I.horiz ? tp.cx : tp.cy;
-    for (int side = 0; side < 2; ++side) {
+    for (int side = fs.second; side == fs.second; ++side) {
       const Subdomain& S = D.subs[side == 0 ? I.a : I.b];
       const SubType& T = D.types[S.type];
       const double sign = side == 0 ? 1.0 : -1.0;
@@ -443,6 +458,12 @@ inline Disc build_disc(const pf_config& cfg, const double* k_override) {
         }
       }
     }
+  }
+  };
+  {
+    std::vector<std::thread> th;
+    for (int k = 0; k < nth; ++k) th.emplace_back(build_g, k, nth);
+    for (auto& t : th) t.join();
   }
   for (auto& S : D.subs) {
     for (auto& kv : G[S.id]) S.g_lam.push_back(kv.first.first), S.g_col.push_back(kv.first.second), S.g_val.push_back(kv.second);
