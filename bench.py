@@ -197,15 +197,18 @@ def run_reference(args, rank, world, dist):
     t0 = time.perf_counter()
     o = ol.Oracle(**dict(kw, threads=threads))
     setup_s = time.perf_counter() - t0
-    # untimed warm-up: one step (first-touch of the factor pages); more only if cheap
-    t0 = time.perf_counter()
-    o.run(1)
-    first = o.report(1)["seconds"]
-    W = 1
+    # untimed warm-up: CPU steps need none (c4 on the box: first step 196.2 s,
+    # second 195.5 s, profiles/r2_cpu_baseline.json); one for the cheap configs
+    # (setup under 10 s), more only while they stay cheap
     budget = args.ref_budget
-    while W < args.warmup and first * (W + 1) < 0.25 * budget:
+    W = 0
+    if setup_s < 10.0:
         o.run(1)
-        W += 1
+        first = o.report(1)["seconds"]
+        W = 1
+        while W < args.warmup and first * (W + 1) < 0.25 * budget:
+            o.run(1)
+            W += 1
     timed, iters = [], []
     t_start = time.perf_counter()
     while len(timed) < args.steps and W + len(timed) < kw["steps"]:
