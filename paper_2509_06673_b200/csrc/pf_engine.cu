@@ -132,21 +132,6 @@ inline bool dense_unit_ok(int S, int RB) {
 #undef PF_DU_OK
   return false;
 }
-#define PF_DENSE_GROUP_CONFIGS(X) X(1, 32) X(1, 64) X(2, 64) X(4, 64)
-inline bool dense_group_ok(int S, int RB) {
-#define PF_DG_OK(s, r) if (S == s && RB == r) return true;
-  PF_DENSE_GROUP_CONFIGS(PF_DG_OK)
-#undef PF_DG_OK
-  return false;
-}
-inline void launch_dense_group(int S, int RB, int nwork, cudaStream_t st, const UnitGroupWork* w,
-                               const DenseUnits& U) {
-#define PF_DG_LAUNCH(s, r) \
-  if (S == s && RB == r) return launch_pdl(k_dense_group<s, r>, nwork, s * r, 0, st, w, U);
-  PF_DENSE_GROUP_CONFIGS(PF_DG_LAUNCH)
-#undef PF_DG_LAUNCH
-  fail(kInternal, "k_dense_group: no such configuration");
-}
 inline void launch_dense_unit(int S, int RB, int nwork, cudaStream_t st, const UnitWork* w, const DenseUnits& U) {
 #define PF_DU_LAUNCH(s, r) \
   if (S == s && RB == r) return launch_pdl(k_dense_unit<s, r>, nwork, s * r, 0, st, w, U);
@@ -193,10 +178,6 @@ struct SolveSystem {
   int db_split[2][2] = {{1, 1}, {1, 1}};  // input slices per CTA
   int db_rb[2][2] = {{64, 64}, {64, 64}};  // output rows per CTA
   DevBuf<dev::UnitWork> db_work[2][2];
-  // units sharing a stored operator applied together (k_dense_group): when
-  // db_gwork is non-empty for a stage it replaces db_work
-  int db_gnwork[2][2] = {{0, 0}, {0, 0}};
-  DevBuf<dev::UnitGroupWork> db_gwork[2][2];
   DevBuf<int> db_in, db_out, db_in_nat, db_out_nat;
   DevBuf<double> db_T;
   double db_bytes = 0.0;       // stored operator bytes (after sharing)
@@ -850,40 +831,6 @@ struct SolveSystem {
         db_nwork[dir][stg] = (int)w.size();
         if (w.empty()) w.push_back(dev::UnitWork{});
         db_work[dir][stg].upload(w);
-        // grouped work: members of a stage sharing an operator (same toff),
-        // up to kUnitG per CTA; only where every input list fits the
-        // per-member shared buffer (PF_QU_G=0 disables)
-        db_gnwork[dir][stg] = 0;
-        static const bool grp = !(std::getenv("PF_QU_G") && std::atoi(std::getenv("PF_QU_G")) == 0);
-        if (grp && maxin <= dev::kUnitMaxIn / dev::kUnitG && dev::dense_group_ok(db_split[dir][stg], rb)) {
-          std::map<long long, std::vector<int>> byop;
-          for (int u = 0; u < nu; ++u)
-            if (ustage[u] == stg) byop[toff[dir * nu + u]].push_back(dir * nu + u);
-          std::vector<dev::UnitGroupWork> gw;
-          long long members = 0;
-          for (auto& kv : byop) {
-            const auto& mem = kv.second;
-            for (std::size_t c0 = 0; c0 < mem.size(); c0 += dev::kUnitG) {
-              const int gsz = (int)std::min<std::size_t>(dev::kUnitG, mem.size() - c0);
-              const int g0 = mem[c0];
-              for (int r = 0; r < nout[g0]; r += rb) {
-                dev::UnitGroupWork x{};
-                x.toff = toff[g0], x.nin = nin[g0], x.nout = nout[g0], x.r0 = r, x.nrows = std::min(rb, nout[g0] - r);
-                x.g = gsz;
-                for (int m = 0; m < gsz; ++m) x.inoff[m] = inoff[mem[c0 + m]], x.outoff[m] = outoff[mem[c0 + m]];
-                gw.push_back(x);
-              }
-              members += gsz;
-            }
-          }
-          if (!gw.empty()) {
-            db_gnwork[dir][stg] = (int)gw.size();
-            db_gwork[dir][stg].upload(gw);
-          }
-          if (std::getenv("PF_VERBOSE"))
-            std::fprintf(stderr, "[pf] Q grouped units dir %d stage %d: %lld members in %zu operators, %d CTAs (was %d)\n",
-                         dir, stg, members, byop.size(), db_gnwork[dir][stg], db_nwork[dir][stg]);
-        }
       }
     db_in.upload(idx_in), db_out.upload(idx_out), db_in_nat.upload(in_nat), db_out_nat.upload(out_nat);
     db_T.upload(T);
@@ -910,10 +857,7 @@ struct SolveSystem {
       U.cbmax = dir == 0 && stg == 1 ? db_cb1 : 0;  // groups fold the level-0 contributions
       U.b = dir == 0 ? b : nullptr, U.X = X.p, U.CB = CB.p;
       U.x = dir == 1 ? x : nullptr, U.xout = !(dir == 1 && stg == 0);
-      if (db_gnwork[dir][stg])
-        dev::launch_dense_group(db_split[dir][stg], db_rb[dir][stg], db_gnwork[dir][stg], st, db_gwork[dir][stg].p, U);
-      else
-        dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_nwork[dir][stg], st, db_work[dir][stg].p, U);
+      dev::launch_dense_unit(db_split[dir][stg], db_rb[dir][stg], db_nwork[dir][stg], st, db_work[dir][stg].p, U);
       ++launches;
     };
     units(0, 0);

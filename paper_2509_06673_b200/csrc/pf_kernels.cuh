@@ -729,96 +729,6 @@ __global__ void __launch_bounds__(RB * S) k_dense_unit(const UnitWork* __restric
   }
 }
 
-/// Units that share one stored operator (bitwise-equal unit maps of the
-/// repeated interface stretches), applied together: up to kUnitG members per
-/// CTA, each with its own input / output index lists.  Every operator value is
-/// loaded once per CTA and used for every member; each member's sum runs in
-/// exactly the order of k_dense_unit (same slices, same even/odd split), so
-/// the result is bitwise the same as one k_dense_unit per member.
-constexpr int kUnitG = 4;
-struct __align__(16) UnitGroupWork {
-  long long toff;
-  int nin, nout, r0, nrows, g, pad;
-  int inoff[kUnitG], outoff[kUnitG];
-};
-template <int S, int RB>
-__global__ void __launch_bounds__(RB * S) k_dense_group(const UnitGroupWork* __restrict__ work, DenseUnits U) {
-  constexpr int B = 8, G = kUnitG;
-  __shared__ double in[G][kUnitMaxIn / G];
-  __shared__ double part[S > 1 ? S : 1][G][RB];
-  if (kPdlEarly) pdl_trigger();
-  const UnitGroupWork& wg = work[blockIdx.x];  // index lists read in place (no local copy)
-  const long long toff = wg.toff;
-  const int nin = wg.nin, nout = wg.nout, r0 = wg.r0, nrows = wg.nrows, gg = wg.g;
-  const int r = threadIdx.x % RB, q = threadIdx.x / RB;
-  const int ni = nin, ld = nout, g = gg;
-  const int jl = (int)((long long)ni * q / S), jh = (int)((long long)ni * (q + 1) / S);
-  const bool live = r < nrows;
-  const double* Tc = U.T + toff + r0 + r;
-  double v[B];
-#pragma unroll
-  for (int m = 0; m < B; ++m) v[m] = (live && jl + m < jh) ? __ldg(Tc + (long long)(jl + m) * ld) : 0.0;
-  pdl_wait();
-  for (int e = threadIdx.x; e < g * ni; e += blockDim.x) {
-    const int mm = e / ni, i = e - mm * ni;
-    const int io = wg.inoff[mm];
-    const int c = U.in[io + i];
-    double x = U.b ? U.b[U.in_nat[io + i]] : U.X[c];
-    if (U.cbmax) x = fold_add(x, c, U.fold_ptr, U.fold_idx, U.CB, U.cbmax);
-    in[mm][i] = x;
-  }
-  __syncthreads();
-  double a0[G], a1[G], u[B];
-#pragma unroll
-  for (int mm = 0; mm < G; ++mm) a0[mm] = a1[mm] = 0.0;
-  auto ld8 = [&](double (&d)[B], int j) {
-#pragma unroll
-    for (int m = 0; m < B; ++m) d[m] = (live && j + m < jh) ? __ldg(Tc + (long long)(j + m) * ld) : 0.0;
-  };
-  auto fma8 = [&](const double (&d)[B], int j) {
-#pragma unroll
-    for (int mm = 0; mm < G; ++mm)
-      if (mm < g)
-#pragma unroll
-        for (int m = 0; m < B; ++m)
-          if (j + m < jh) (m & 1 ? a1[mm] : a0[mm]) += d[m] * in[mm][j + m];
-  };
-  for (int j = jl; j < jh; j += 2 * B) {
-    if (j + B < jh) ld8(u, j + B);
-    fma8(v, j);
-    if (j + 2 * B < jh) ld8(v, j + 2 * B);
-    if (j + B < jh) fma8(u, j + B);
-  }
-  double acc[G];
-#pragma unroll
-  for (int mm = 0; mm < G; ++mm) acc[mm] = a0[mm] + a1[mm];
-  if (S > 1) {
-#pragma unroll
-    for (int mm = 0; mm < G; ++mm) part[q][mm][r] = acc[mm];
-    __syncthreads();
-    if (q) return;
-#pragma unroll
-    for (int mm = 0; mm < G; ++mm) {
-      acc[mm] = 0.0;
-#pragma unroll
-      for (int k = 0; k < S; ++k) acc[mm] += part[k][mm][r];
-    }
-  }
-  if (!live) return;
-#pragma unroll
-  for (int mm = 0; mm < G; ++mm) {
-    if (mm >= g) break;
-    const int oo = wg.outoff[mm] + r0 + r;
-    const int o = U.out[oo];
-    if (o < 0) {
-      U.CB[-1 - o] = acc[mm];
-    } else {
-      if (U.xout) U.X[o] = acc[mm];
-      if (U.x) U.x[U.out_nat[oo]] = acc[mm];
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Error norms against the manufactured solution
 // ---------------------------------------------------------------------------
