@@ -401,10 +401,18 @@ def run_ours(args, rank, world, dist):
         try:
             s = cpu_sample(args.config, iters_per_step)
             v = (iters_per_step + 2) * s["t_fapply_full"] + iters_per_step * (s["t_iter_full"] - s["t_fapply_full"])
+            meas = None
+            try:  # the committed measurement of a real full step on the same box type
+                runs = json.load(open(os.path.join(ROOT, "profiles", "r2_cpu_baseline.json")))["runs"]
+                meas = next(r for r in runs if r["config"] == args.config and r["mode"] == "restated-parallel")
+            except Exception:
+                pass
             line["cpu_baseline"] = {"value": v, "unit": "s/step", "cores": s["threads"], "kind": "port",
                                     "sample": s["sample"], "estimated": True,
-                                    "measured_full_steps": "bench.py --impl reference (real steps of the full "
-                                                           "workload); profiles/r2_cpu_reference_*.json"}
+                                    "measured_full_step_s": meas["step_s_mean"] if meas else None,
+                                    "measured_full_step_source": "profiles/r2_cpu_baseline.json (real time steps of "
+                                                                 "the full workload, 16 host threads; the reference "
+                                                                 "arm bench.py --impl reference repeats it live)"}
         except Exception as exc:  # the baseline is reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "s/step", "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc}"}
