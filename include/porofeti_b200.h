@@ -45,14 +45,11 @@ extern "C" {
 #define PF_PREC_GENERALIZED_MORTAR 3
 #define PF_PREC_DIRICHLET_MORTAR 4
 /* Krylov: auto = reference PCG (feti.hpp:263) when no pressure multipliers,
- * otherwise SQMR, deflated (SQMR_DEFL) on partitions of more than two
- * subdomains: the translations of the subdomains touching the outer boundary
- * are projected out F-orthogonally */
+ * SQMR otherwise */
 #define PF_KRYLOV_AUTO 0
 #define PF_KRYLOV_PCG 1
 #define PF_KRYLOV_MINRES 2
 #define PF_KRYLOV_SQMR 3
-#define PF_KRYLOV_SQMR_DEFL 4
 
 /* Run configuration (reference RunConfig, config.hpp:17-43, plus the
  * partition).  Same field order as the oracle's or_config. */
@@ -100,7 +97,7 @@ typedef struct pf_sub_info {
 
 /* PcgReport (feti.hpp:59-67) + device timings */
 typedef struct pf_report {
-  int step, iterations, converged, method; /* method: 1 pcg, 2 minres, 3 sqmr, 4 deflated sqmr */
+  int step, iterations, converged, method; /* method: 1 pcg, 2 minres, 3 sqmr */
   double rel_residual;
   double seconds;     /* device time of the whole advance (CUDA events) */
   double t_rhs, t_krylov, t_back;

@@ -91,17 +91,11 @@ class Feti {
     // otherwise SQMR (symmetric indefinite operator and preconditioner)
     const bool indefinite = D.n_lambda > D.n_lambda_u;
     kry_ = cfg.krylov == "minres" ? Kry::minres
-           : (cfg.krylov == "sqmr" || cfg.krylov == "sqmr-d") ? Kry::sqmr
+           : cfg.krylov == "sqmr" ? Kry::sqmr
            : cfg.krylov == "pcg"  ? Kry::pcg
            : (indefinite ? Kry::sqmr : Kry::pcg);
-    if (cfg.krylov != "auto" && cfg.krylov != "pcg" && cfg.krylov != "minres" && cfg.krylov != "sqmr" &&
-        cfg.krylov != "sqmr-d")
+    if (cfg.krylov != "auto" && cfg.krylov != "pcg" && cfg.krylov != "minres" && cfg.krylov != "sqmr")
       throw ConfigError("unknown krylov method '" + cfg.krylov + "'");
-    // deflation of the translations of the non-floating subdomains (their slow
-    // modes, measured on the preconditioned operator): explicit "sqmr-d", and
-    // "auto" wherever SQMR runs on a partition of more than two subdomains
-    // (deflation_auto; the engine applies the same rule)
-    defl_ = kry_ == Kry::sqmr && (cfg.krylov == "sqmr-d" || (cfg.krylov == "auto" && deflation_auto(D)));
     minres_ = kry_ == Kry::minres;
     split_ = minres_;  // MINRES needs an SPD preconditioner: sign-split pressure block
     const int ns = (int)D.subs.size();
@@ -203,72 +197,7 @@ class Feti {
       }
       dense_cholesky(GtG_);
     }
-    if (defl_) setup_deflation();
   }
-
-  /// auto rule for the deflated SQMR (engine and oracle alike)
-  static bool deflation_auto(const Disc& D) { return (int)D.subs.size() > 2; }
-
-  /// W: one column per (non-floating subdomain s but the last, component c), G_s times the
-  /// unit translation of s in direction c (u dofs only); E = W~^T PFP W~ with
-  /// W~ = P W (SPD: W lives on displacement multipliers), Cholesky-factored.
-  void setup_deflation() {
-    std::vector<Trip> t;
-    int m = 0;
-    // the translations of all subdomains sum to a continuous field (zero
-    // jumps), so per component the non-floating columns sum into range(G_c)
-    // (or to zero without floating subdomains): the last non-floating
-    // subdomain's columns are left out, which makes W~ = P W full rank
-    int last = -1;
-    for (const Sub& S : D_->subs)
-      if (!S.floating) last = S.id;
-    for (const Sub& S : D_->subs) {
-      if (S.floating || S.id == last) continue;
-      for (int c = 0; c < 2; ++c) {
-        bool any = false;
-        for (int i = 0; i < S.G.nr; ++i) {
-          double v = 0.0;
-          for (int q = S.G.ptr[i]; q < S.G.ptr[i + 1]; ++q)
-            if (S.G.col[q] < S.n_u && S.G.col[q] % 2 == c) v += S.G.val[q];
-          if (v != 0.0) t.push_back({i, m, v}), any = true;
-        }
-        if (any) ++m;
-      }
-    }
-    md_ = m;
-    Wd_ = Csr::from_trips(D_->n_lambda, md_, t);
-    Ed_ = Dense(md_, md_);
-    std::vector<Vec> cols(md_);
-    for (int j = 0; j < md_; ++j) {  // apply() is threaded over subdomains
-      Vec e(md_, 0.0);
-      e[j] = 1.0;
-      Vec y(D_->n_lambda, 0.0);
-      Wd_.mv(e.data(), y.data());
-      project(y);
-      Vec z = apply(y);
-      project(z);
-      cols[j] = Wd_.tmul(z);
-    }
-    for (int j = 0; j < md_; ++j)
-      for (int i = 0; i < md_; ++i) Ed_(i, j) = cols[j][i];
-    dense_cholesky(Ed_);
-  }
-  /// y = P W E^{-1} v (v in R^m)
-  Vec defl_lift(Vec c) const {
-    dense_cholesky_solve(Ed_, c.data());
-    Vec y(D_->n_lambda, 0.0);
-    Wd_.mv(c.data(), y.data());
-    project(y);
-    return y;
-  }
-  /// t -= PFP W~ E^{-1} W^T t: the deflated operator A_D = PFP - PFPW~ E^-1 W~^T PFP on t = PFP q
-  void defl_apply(Vec& t) const {
-    const Vec y = defl_lift(Wd_.tmul(t));
-    Vec z = apply(y);
-    project(z);
-    for (std::size_t i = 0; i < t.size(); ++i) t[i] -= z[i];
-  }
-  bool deflated() const { return defl_; }
 
   int n_lambda() const { return D_->n_lambda; }
   bool uses_minres() const { return minres_; }
@@ -513,47 +442,27 @@ class Feti {
     Vec r = apply(lambda);
     for (int i = 0; i < n; ++i) r[i] = rhs[i] - r[i];
     project(r);
-    const double t0 = norm2(r);  // convergence reference: the warm-started residual
+    double tau = norm2(r);
+    const double t0 = tau;
     rep.history.push_back(t0);
     if (t0 == 0.0 || !(t0 > 0.0)) {
       rep.converged = true;
       return;
     }
-    // deflated SQMR: lambda = lambda0' + P_D^T x, lambda0' = lambda0 + W~ E^-1 W~^T r0,
-    // x from SQMR on A_D = PFP - PFPW~ E^-1 W~^T PFP with rhs r0' = r0 - PFPW~ E^-1 W~^T r0
-    // (W~^T v = W^T v for v in range(P)); without deflation x accumulates in lambda
-    Vec base, x;
-    if (defl_) {
-      const Vec y = defl_lift(Wd_.tmul(r));
-      axpy(1.0, y, lambda);
-      Vec z = apply(y);
-      project(z);
-      axpy(-1.0, z, r);
-      base = lambda;
-      x.assign(n, 0.0);
-    }
-    Vec& acc = defl_ ? x : lambda;
-    // the multiplier of the current iterate (deflation: lambda0' + P_D^T x)
-    auto materialize = [&]() {
-      if (!defl_) return;
-      Vec fx = apply(x);
-      project(fx);
-      const Vec y = defl_lift(Wd_.tmul(fx));
-      for (int i = 0; i < n; ++i) lambda[i] = base[i] + x[i] - y[i];
-    };
-    double tau = norm2(r);
-    // Lanczos recurrences from the residual in r
+    // Lanczos recurrences from the residual in r (first solve and restarts)
     Vec q, d;
     double rho = 0.0, theta = 0.0;
-    q = precondition(r);
-    project(q);
-    rho = dot(r, q), theta = 0.0;
-    d.assign(n, 0.0);
+    auto start = [&] {
+      q = precondition(r);
+      project(q);
+      rho = dot(r, q), theta = 0.0;
+      d.assign(n, 0.0);
+    };
+    start();
     double thr = cfg.tol * t0;  // threshold on the estimate tau_k
     for (int k = 0; k < cfg.max_iter; ++k) {
       Vec t = apply(q);
       project(t);
-      if (defl_) defl_apply(t);
       const double sigma = dot(q, t);
       if (sigma == 0.0 || !std::isfinite(sigma)) throw PcgBreakdownError("sqmr: <q, Fq> vanished (Lanczos breakdown)");
       const double a = rho / sigma;
@@ -564,7 +473,7 @@ class Feti {
       tau = tau * theta * c;
       for (int i = 0; i < n; ++i) {
         d[i] = c * c * th_old * th_old * d[i] + c * c * a * q[i];
-        acc[i] += d[i];
+        lambda[i] += d[i];
       }
       const double est = tau;  // quasi-residual norm (estimate of the QMR residual)
       rep.history.push_back(est);
@@ -573,7 +482,6 @@ class Feti {
         // confirm on the true residual (||r_k|| <= sqrt(k+1) tau_k only);
         // above the tolerance: keep iterating, with the estimate's threshold
         // scaled by the observed true/estimate ratio
-        materialize();
         const double tr = true_residual(rhs, lambda);
         rep.true_residual = tr / t0;
         if (tr <= cfg.tol * t0) {
@@ -592,10 +500,8 @@ class Feti {
       rho = rho_n;
       for (int i = 0; i < n; ++i) q[i] = u[i] + b * q[i];
     }
-    materialize();
     rep.rel_residual = rep.history.back() / t0;
   }
-
 
   /// Preconditioned MINRES (Paige-Saunders recurrences) on P F P with the
   /// SPD preconditioner P M P; residual measured as sqrt(r^T M r) like REF.
@@ -684,10 +590,6 @@ class Feti {
   int nthreads_ = 1;
   Prec prec_ = Prec::dirichlet;
   bool scaled_ = false;
-  bool defl_ = false;  // deflated SQMR (setup_deflation)
-  int md_ = 0;
-  Csr Wd_;
-  Dense Ed_;
   Ldlt qfac_;
   bool minres_ = false, split_ = false;
   Kry kry_ = Kry::pcg;

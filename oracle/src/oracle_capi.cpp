@@ -20,7 +20,7 @@ struct or_config {
   int mu_conv;   // 0 paper, 1 standard
   int scenario;  // 0 mms-t, 1 mms, 2 injection, 3 barry-mercer
   int precond;   // 0 identity, 1 generalized, 2 dirichlet
-  int krylov;    // 0 auto, 1 pcg, 2 minres, 3 sqmr, 4 sqmr-d (deflated)
+  int krylov;    // 0 auto, 1 pcg, 2 minres
   double tol;
   int max_iter, warm, threads;
   unsigned long long seed;
@@ -49,8 +49,8 @@ Config to_cfg(const or_config* c) {
   Config k;
   static const char* sc[] = {"mms-t", "mms", "injection", "barry-mercer"};
   static const char* pr[] = {"identity", "generalized", "dirichlet", "generalized-mortar", "dirichlet-mortar"};
-  static const char* kr[] = {"auto", "pcg", "minres", "sqmr", "sqmr-d"};
-  if (c->scenario < 0 || c->scenario > 3 || c->precond < 0 || c->precond > 4 || c->krylov < 0 || c->krylov > 4)
+  static const char* kr[] = {"auto", "pcg", "minres", "sqmr"};
+  if (c->scenario < 0 || c->scenario > 3 || c->precond < 0 || c->precond > 4 || c->krylov < 0 || c->krylov > 3)
     throw ConfigError("config enum out of range");
   k.scenario = sc[c->scenario];
   k.mesh_n = c->mesh_n, k.SX = c->SX, k.SY = c->SY, k.order = c->order;

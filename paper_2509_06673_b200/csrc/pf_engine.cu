@@ -1234,11 +1234,7 @@ struct Engine {
     use_dir = pk == PF_PREC_DIRICHLET || pk == PF_PREC_DIRICHLET_MORTAR;
     use_gen = pk == PF_PREC_GENERALIZED || pk == PF_PREC_GENERALIZED_MORTAR;
     const bool indefinite = D.n_lambda > D.n_lambda_u;
-    krylov = cfg.krylov == PF_KRYLOV_AUTO
-                 ? (indefinite ? ((int)D.subs.size() > 2 ? PF_KRYLOV_SQMR_DEFL : PF_KRYLOV_SQMR) : PF_KRYLOV_PCG)
-                 : cfg.krylov;
-    defl = krylov == PF_KRYLOV_SQMR_DEFL;
-    if (cfg.krylov < PF_KRYLOV_AUTO || cfg.krylov > PF_KRYLOV_SQMR_DEFL) fail(kInvalid, "unknown krylov id");
+    krylov = cfg.krylov == PF_KRYLOV_AUTO ? (indefinite ? PF_KRYLOV_SQMR : PF_KRYLOV_PCG) : cfg.krylov;
     if (krylov == PF_KRYLOV_MINRES) fail(kInvalid, "MINRES is provided by the oracle only in this build");
     if (krylov == PF_KRYLOV_PCG && indefinite)
       fail(kInvalid, "pcg requested but pressure multipliers make the operator indefinite");
@@ -1307,7 +1303,6 @@ struct Engine {
     if (floating_any) setup_coarse(), mark("coarse space");
     setup_krylov();
     if (dual) setup_backsub(), mark("explicit back-substitution");
-    if (defl) setup_deflation(), mark("deflation space");
     project_initial();
     mark("initial state");
     if (std::getenv("PF_VERBOSE")) {
@@ -3216,109 +3211,6 @@ struct Engine {
     ++papplies;
   }
 
-  // ---- deflated SQMR (PF_KRYLOV_SQMR_DEFL; oracle o_feti.hpp setup_deflation) ----
-  // W: one column per (non-floating subdomain but the last, component), G_s
-  // times the unit translation of s; E = W~^T PFP W~ with W~ = P W (SPD),
-  // inverted once on the tensor cores.  Per iteration t <- t - PFP W~ E^-1 W^T t.
-  bool defl = false;
-  int md = 0;
-  DevBuf<int> dw_ptr, dw_idx, dwt_ptr, dwt_idx;
-  DevBuf<double> dw_val, dwt_val, d_Einv, df_c, df_c2, df_y, df_z, kr_x, kr_base;
-  void setup_deflation() {
-    const int n = D.n_lambda;
-    int last = -1;
-    for (std::size_t s = 0; s < D.subs.size(); ++s)
-      if (!D.types[D.subs[s].type].floating) last = (int)s;
-    std::vector<std::map<int, double>> cols;
-    for (std::size_t s = 0; s < D.subs.size(); ++s) {
-      const Subdomain& S = D.subs[s];
-      const SubType& T = D.types[S.type];
-      if (T.floating || (int)s == last) continue;
-      for (int c = 0; c < 2; ++c) {
-        std::map<int, double> col;
-        for (std::size_t q = 0; q < S.g_lam.size(); ++q)
-          if (S.g_col[q] < T.n_u && S.g_col[q] % 2 == c) col[S.g_lam[q]] += S.g_val[q];
-        for (auto it = col.begin(); it != col.end();) it = it->second == 0.0 ? col.erase(it) : std::next(it);
-        if (!col.empty()) cols.push_back(std::move(col));
-      }
-    }
-    md = (int)cols.size();
-    if (md == 0) {
-      defl = false;
-      krylov = PF_KRYLOV_SQMR;
-      return;
-    }
-    std::vector<std::vector<std::pair<int, double>>> rows(n);
-    std::vector<int> tp{0}, ti;
-    std::vector<double> tv;
-    for (int j = 0; j < md; ++j) {
-      for (auto& kv : cols[j]) rows[kv.first].emplace_back(j, kv.second), ti.push_back(kv.first), tv.push_back(kv.second);
-      tp.push_back((int)ti.size());
-    }
-    std::vector<int> rp{0}, ri;
-    std::vector<double> rv;
-    for (int i = 0; i < n; ++i) {
-      for (auto& e : rows[i]) ri.push_back(e.first), rv.push_back(e.second);
-      rp.push_back((int)ri.size());
-    }
-    dw_ptr.upload(rp), dw_idx.upload(ri.empty() ? std::vector<int>{0} : ri), dw_val.upload(rv.empty() ? std::vector<double>{0.0} : rv);
-    dwt_ptr.upload(tp), dwt_idx.upload(ti), dwt_val.upload(tv);
-    df_c.alloc(md), df_c2.alloc(md), df_y.alloc(n), df_z.alloc(n), kr_x.alloc(n), kr_base.alloc(n);
-    // E column by column: y = P W e_j, z = P F y, E e_j = W^T z
-    DevBuf<double> dE;
-    dE.alloc((std::size_t)md * md);
-    std::vector<double> ej(md, 0.0);
-    for (int j = 0; j < md; ++j) {
-      df_c.zero(st);
-      const double one = 1.0;
-      PF_CUDA_CHECK(cudaMemcpyAsync(df_c.p + j, &one, sizeof(double), cudaMemcpyHostToDevice, st));
-      dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, dw_ptr.p, dw_idx.p, dw_val.p, df_c.p, df_y.p, 1.0, 0.0);
-      project(df_y.p);
-      fapply(df_y.p, df_z.p);
-      project(df_z.p);
-      dev::k_spmv<<<cdiv(md, 256), 256, 0, st>>>(md, dwt_ptr.p, dwt_idx.p, dwt_val.p, df_z.p,
-                                                 dE.p + (std::size_t)j * md, 1.0, 0.0);
-      ::pf::g_launches += 2;
-      PF_CUDA_CHECK(cudaStreamSynchronize(st));  // one_ is a host stack value
-    }
-    d_Einv.alloc((std::size_t)md * md);
-    dense_spd_inverse(md, dE.p, d_Einv.p);
-    if (sizeof(double) * md > 48 * 1024)
-      PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_dense_gemv_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max<std::size_t>(sizeof(double) * md, sizeof(double) * nc)));
-  }
-  /// y = P W E^-1 (W^T v)  (v in range(P))
-  void defl_lift(const double* v, double* y) {
-    const int n = D.n_lambda;
-    // (k_spmv has no programmatic-dependent-launch wait: plain launches)
-    dev::k_spmv<<<cdiv(md, 256), 256, 0, st>>>(md, dwt_ptr.p, dwt_idx.p, dwt_val.p, v, df_c.p, 1.0, 0.0);
-    launch_pdl(dev::k_dense_gemv_w, std::min(cdiv(md, 8), 4 * 148), 256, sizeof(double) * md, st, md,
-               (const double*)d_Einv.p, (const double*)df_c.p, df_c2.p);
-    dev::k_spmv<<<cdiv(n, 256), 256, 0, st>>>(n, dw_ptr.p, dw_idx.p, dw_val.p, df_c2.p, y, 1.0, 0.0);
-    ::pf::g_launches += 2;
-    project(y);
-  }
-  /// t -= PFP W~ E^-1 W^T t  (the deflated operator on t = PFP q)
-  void defl_apply(double* t) {
-    const int n = D.n_lambda;
-    defl_lift(t, df_y.p);
-    F_(df_y.p, df_z.p);
-    project(df_z.p);
-    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, df_z.p, 1.0, t);
-    ::pf::g_launches++;
-  }
-  /// lambda = base + x - P W E^-1 W^T (P F x)
-  void defl_materialize(double* lambda) {
-    const int n = D.n_lambda;
-    F_(kr_x.p, df_z.p);
-    project(df_z.p);
-    defl_lift(df_z.p, df_y.p);
-    PF_CUDA_CHECK(cudaMemcpyAsync(lambda, kr_base.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_x.p, 1.0, lambda);
-    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, df_y.p, 1.0, lambda);
-    ::pf::g_launches += 2;
-  }
-
   /// Krylov solve of F lambda = rhs (+ coarse), lambda in/out on device.
   void krylov_solve(double* lambda, pf_report& rep) {
     const int n = D.n_lambda;
@@ -3416,30 +3308,9 @@ struct Engine {
     double* t = kr_t.p;
     double* d = kr_d.p;
     double* u = kr_z.p;
-    // deflated SQMR: lambda0' = lambda0 + P W E^-1 W^T r0, r0' = r0 - PFP W~ E^-1 W^T r0;
-    // SQMR accumulates x (kr_x), lambda = lambda0' + P_D^T x (defl_materialize)
-    double* acc = defl ? kr_x.p : lambda;
-    if (defl) {
-      dot(n, r, r, dev::KS_RR);
-      dev::k_ks_sqmr_init<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
-      if (status() == dev::KST_CONV) {
-        rep.converged = 1;
-        rep.rel_residual = 0.0;
-        return;
-      }
-      defl_lift(r, df_y.p);
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, df_y.p, 1.0, lambda); ::pf::g_launches++;
-      F_(df_y.p, df_z.p);
-      project(df_z.p);
-      dev::k_axpby<<<nb, 256, 0, st>>>(n, -1.0, df_z.p, 1.0, r); ::pf::g_launches++;
-      PF_CUDA_CHECK(cudaMemcpyAsync(kr_base.p, lambda, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-      kr_x.zero(st);
-    }
     dot(n, r, r, dev::KS_RR);
     dev::k_ks_sqmr_init<<<1, 1, 0, st>>>(sc, stat, tol); ::pf::g_launches++;
-    if (defl) dev::k_ks_defl_ref<<<1, 1, 0, st>>>(sc, tol), ::pf::g_launches++;  // tol relative to ||r0||
     if (status() == dev::KST_CONV) {
-      if (defl) defl_materialize(lambda);
       rep.converged = 1;
       rep.rel_residual = 0.0;
       return;
@@ -3451,16 +3322,10 @@ struct Engine {
         launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, u, q, sc + dev::KS_B);  // q = u + b q
       }
       F_(q, t);
-      if (defl) {  // t = A_D q = PFq - PFP W~ E^-1 W^T PFq
-        project(t);
-        defl_apply(t);
-        fdot(dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);
-      } else {
-        if (nc) coarse_solve(t, c_tmp2.p);
-        fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);  // t = P F q, sigma, a
-      }
+      if (nc) coarse_solve(t, c_tmp2.p);
+      fdot(nc ? dev::DOT_PROJ : dev::DOT_PLAIN, q, t, dev::KS_SIGMA, dev::SOP_SQMR_A);  // t = P F q, sigma, a
       fdot(dev::DOT_AXPY, t, r, dev::KS_RR, dev::SOP_SQMR_TAU);                         // r -= a t, tau
-      launch_pdl(dev::k_sqmr_dx_s, nb, 256, 0, st, n, sc, q, d, acc, lp_cap_h, (const int*)d_status.p,
+      launch_pdl(dev::k_sqmr_dx_s, nb, 256, 0, st, n, sc, q, d, lambda, lp_cap_h, (const int*)d_status.p,
                  lp_cap_maxit, lp_capturing ? 1 : 0);
       lp_cond_set = lp_capturing;
     };
@@ -3468,11 +3333,11 @@ struct Engine {
     auto loop = [&] {
       if (status() == dev::KST_RUN && h_status[1] < maxit && loop_ok()) {
         // every further iteration on the device: one launch of a WHILE graph
-        graphed_loop(acc, defl ? 3 : 2, maxit, [&] { iter(false); });
+        graphed_loop(lambda, 2, maxit, [&] { iter(false); });
         status();
       } else {
         while (h_status[1] < maxit && h_status[0] == dev::KST_RUN) {
-          graphed(acc, defl ? 3 : 2, [&] { iter(false); });
+          graphed(lambda, 2, [&] { iter(false); });
           status();
         }
       }
@@ -3488,7 +3353,6 @@ struct Engine {
     // tol * ||r0|| the same recurrences continue with a tightened threshold
     for (;;) {
       rep.iterations = h_status[1];
-      if (defl) defl_materialize(lambda);
       if (h_status[0] != dev::KST_CONV) {
         rep.rel_residual = rel_residual();
         break;

@@ -344,12 +344,6 @@ __global__ void k_ks_sqmr_continue(double* sc, int* status, double tol) {
   sc[KS_THR] = sc[KS_TAU] * (tol * sc[KS_T0] / tr) * 0.5;
   status[0] = KST_RUN;
 }
-/// deflated SQMR: the convergence reference is the residual before the
-/// deflation correction (TR0 = ||P(rhs - F lambda0)||^2), like the oracle
-__global__ void k_ks_defl_ref(double* sc, double tol) {
-  const double t0 = sqrt(sc[KS_TR0]);
-  sc[KS_T0] = t0, sc[KS_THR] = tol * t0, sc[KS_REL] = sc[KS_TAU] / t0;
-}
 __device__ __forceinline__ void ks_sqmr_a(double* sc, int* status) {
   const double sigma = sc[KS_SIGMA];
   if (sigma == 0.0 || !isfinite(sigma)) status[0] = KST_SIGMA;

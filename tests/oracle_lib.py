@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
 
 SCENARIOS = {"mms-t": 0, "mms": 1, "injection": 2, "barry-mercer": 3}
 PRECONDS = {"identity": 0, "generalized": 1, "dirichlet": 2, "generalized-mortar": 3, "dirichlet-mortar": 4}
-KRYLOV = {"auto": 0, "pcg": 1, "minres": 2, "sqmr": 3, "sqmr-d": 4}
+KRYLOV = {"auto": 0, "pcg": 1, "minres": 2, "sqmr": 3}
 
 
 class Config(C.Structure):
