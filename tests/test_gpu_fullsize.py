@@ -58,6 +58,16 @@ def bar(z, k, j):
     return b
 
 
+def iter_bar(it_o):
+    """+-2, except for the runs of ~1000 SQMR iterations (c3: nu = 0.49999;
+    c5: permeability over six decades) whose count moves with the rounding of
+    the operators -- the same device step through the factor sweeps instead of
+    the explicit local operators (mathematically identical, other summation
+    order) moves c5 by several iterations (test_rounding_sensitivity_c5) --
+    held to 0.5 % of the oracle's count there."""
+    return 2 if it_o <= 500 else max(2, -(-5 * it_o // 1000))
+
+
 def global_fields(op, xs):
     f = op.fields(xs)
     return {k: np.concatenate([fi[k] for fi in f if k in fi]) for k in FIELDS}
@@ -78,7 +88,7 @@ def test_fullsize_matches_oracle_fixture(name):
         xs, lam = op.state()
         assert rel(lam, z[f"lambda{k}"]) <= bar(z, k, 4), (k, rel(lam, z[f"lambda{k}"]))
         it_o = int(z[f"iters{k}"])
-        assert abs(rep["iterations"] - it_o) <= 2, (k, rep["iterations"], it_o)
+        assert abs(rep["iterations"] - it_o) <= iter_bar(it_o), (k, rep["iterations"], it_o)
         f = op.fields(xs)
         norms = z[f"norms{k}"]
         for j, fld in enumerate(FIELDS):
@@ -135,3 +145,25 @@ def test_true_residual_against_interface_rhs(name):
         r = op.project(d - op.apply(lam))
         assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(op.project(d)), (rep, np.linalg.norm(r))
     op.close()
+
+
+def test_rounding_sensitivity_c5():
+    """Evidence for iter_bar: the c5 step (1100+ SQMR iterations) through two
+    mathematically identical device paths -- explicit local dual operators
+    (default) and the factor sweeps (PF_FAPPLY=implicit), different summation
+    orders -- lands a few iterations apart, like engine vs oracle."""
+    z, cfg = load("full_c5")
+    cfg = dict(cfg, steps=1)
+    op = pf.FetiOperator(**cfg)
+    a = op.step()["iterations"]
+    op.close()
+    os.environ["PF_FAPPLY"] = "implicit"
+    try:
+        op = pf.FetiOperator(**cfg)
+        b = op.step()["iterations"]
+        op.close()
+    finally:
+        del os.environ["PF_FAPPLY"]
+    it_o = int(z["iters1"])
+    print(f"c5 step 1: explicit {a}, implicit {b}, oracle {it_o}")
+    assert abs(a - b) <= iter_bar(it_o) and abs(b - it_o) <= iter_bar(it_o)
