@@ -102,9 +102,12 @@ typedef struct pf_report {
   double seconds;     /* device time of the whole advance (CUDA events) */
   double t_rhs, t_krylov, t_back;
   int f_applies, precond_applies;
-  /* ||P(rhs - F lambda)|| / ||P(rhs - F lambda_0)|| of the returned multiplier,
-   * recomputed with one extra F-apply (SQMR: the convergence test itself —
-   * its quasi-residual is only an estimate; PCG: reported beside REF's sqrt(r.z)) */
+  /* ||P(rhs - F lambda)|| / ||P rhs|| of the returned multiplier, recomputed
+   * with one extra F-apply.  SQMR: part of the convergence test — the
+   * quasi-residual (rel_residual, relative to the warm-started residual like
+   * REF's criterion) only estimates the residual, so a step converges when
+   * that estimate is below tol AND this true residual is below tol.  PCG:
+   * reported beside REF's sqrt(r.z). */
   double true_residual;
   int restarts; /* SQMR: true-residual checks that failed (iteration continued with a tighter estimate threshold) */
 } pf_report;

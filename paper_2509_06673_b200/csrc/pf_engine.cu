@@ -3223,6 +3223,12 @@ struct Engine {
     dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, r); ::pf::g_launches++;
     project(r);
     dot(n, r, r, dev::KS_TR0);  // ||r0||^2 of the projected (warm-started) residual
+    // ||P rhs||^2: the reference of the true-residual test (a good warm start
+    // makes ||r0|| << ||P rhs||, and tol ||r0|| can fall below the attainable
+    // accuracy of F lambda after many steps of a smooth solution)
+    PF_CUDA_CHECK(cudaMemcpyAsync(kr_t.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    project(kr_t.p);
+    dot(n, kr_t.p, kr_t.p, dev::KS_RHSN);
     rep.iterations = 0;
     rep.converged = 0;
     rep.true_residual = 0.0;
@@ -3256,7 +3262,7 @@ struct Engine {
       dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, t); ::pf::g_launches++;
       project(t);
       dot(n, t, t, dev::KS_TRUE);
-      const double r0 = read_scal(dev::KS_TR0);
+      const double r0 = read_scal(dev::KS_RHSN);
       return r0 > 0.0 ? std::sqrt(read_scal(dev::KS_TRUE) / r0) : 0.0;
     };
     if (krylov == PF_KRYLOV_PCG) {
@@ -3358,7 +3364,8 @@ struct Engine {
         break;
       }
       const double tr = true_residual(t);
-      rep.true_residual = rep.rel_residual = tr;
+      rep.true_residual = tr;
+      rep.rel_residual = rel_residual();
       if (tr <= tol) {
         rep.converged = 1;
         break;

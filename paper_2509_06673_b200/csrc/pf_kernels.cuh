@@ -284,7 +284,7 @@ __global__ void k_sqmr_dx(int n, const double* sc, const double* q, double* d, d
 // ---------------------------------------------------------------------------
 enum : int {
   KS_RHO = 32, KS_SIGMA, KS_A, KS_RR, KS_THETA, KS_THOLD, KS_C, KS_TAU, KS_T0, KS_RHON, KS_B, KS_REL,
-  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR
+  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR, KS_RHSN
 };
 enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5 };
 /// residual history (REF PcgReport::residual_history, feti.hpp:65): entry k at
@@ -336,12 +336,12 @@ __device__ __forceinline__ void ks_sqmr_init(double* sc, int* status, double tol
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
 }
 /// SQMR convergence check failed on the true residual (TRUE = ||r||^2 of
-/// r = P(rhs - F lambda)): keep iterating with the same recurrences, the
-/// estimate's threshold scaled by the observed true/estimate ratio (the oracle
-/// rule, o_feti.hpp sqmr)
+/// r = P(rhs - F lambda), target tol ||P rhs||, RHSN = ||P rhs||^2): keep
+/// iterating with the same recurrences, the estimate's threshold scaled by
+/// the observed true/target ratio (the oracle rule, o_feti.hpp sqmr)
 __global__ void k_ks_sqmr_continue(double* sc, int* status, double tol) {
   const double tr = sqrt(sc[KS_TRUE]);
-  sc[KS_THR] = sc[KS_TAU] * (tol * sc[KS_T0] / tr) * 0.5;
+  sc[KS_THR] = sc[KS_TAU] * (tol * sqrt(sc[KS_RHSN]) / tr) * 0.5;  // target: tol ||P rhs||
   status[0] = KST_RUN;
 }
 __device__ __forceinline__ void ks_sqmr_a(double* sc, int* status) {
