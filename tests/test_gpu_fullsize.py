@@ -168,3 +168,20 @@ def test_rounding_sensitivity_c5():
         it_o = int(z[f"iters{k}"])
         print(f"c5 step {k}: explicit {a[k - 1]}, implicit {b[k - 1]}, oracle {it_o}")
         assert abs(a[k - 1] - b[k - 1]) <= iter_bar(it_o) and abs(b[k - 1] - it_o) <= iter_bar(it_o)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_every_config_runs_all_its_steps(name):
+    """run_simulation (timeloop.hpp:206-221) over every time step of each
+    BASELINE config: each step converges with the true residual below the
+    tolerance (c5: 100 steps; the warm start makes later steps the hardest
+    for a residual relative to the warm-started one)."""
+    op = pf.FetiOperator(**pf.BASELINE_CONFIGS[name])
+    reps = pf.run_simulation(op)
+    assert len(reps) == op.info.N
+    assert all(r["converged"] and r["true_residual"] <= 1e-10 for r in reps), [
+        (r["step"], r["iterations"], r["true_residual"]) for r in reps if not r["converged"] or r["true_residual"] > 1e-10]
+    its = [r["iterations"] for r in reps]
+    print(f"{name}: {len(reps)} steps, iterations min {min(its)} max {max(its)} mean {sum(its) / len(its):.1f}, "
+          f"device {sum(r['seconds'] for r in reps):.3f} s")
+    op.close()
