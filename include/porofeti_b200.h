@@ -50,6 +50,12 @@ extern "C" {
 #define PF_KRYLOV_PCG 1
 #define PF_KRYLOV_MINRES 2
 #define PF_KRYLOV_SQMR 3
+/* direct interface solve, the GPU analogue of the reference's monolithic
+ * solver (SolverChoice::monolithic, feti.hpp:313-440, timeloop.hpp:139-160):
+ * the coupled system condensed exactly onto the multipliers and solved with a
+ * dense inverse of the interface operator (n_lambda <= 65536) — no Krylov
+ * iterations; the same fields as the reference's direct solve */
+#define PF_KRYLOV_DIRECT 4
 
 /* Run configuration (reference RunConfig, config.hpp:17-43, plus the
  * partition).  Same field order as the oracle's or_config. */
@@ -97,7 +103,7 @@ typedef struct pf_sub_info {
 
 /* PcgReport (feti.hpp:59-67) + device timings */
 typedef struct pf_report {
-  int step, iterations, converged, method; /* method: 1 pcg, 2 minres, 3 sqmr */
+  int step, iterations, converged, method; /* method: 1 pcg, 2 minres, 3 sqmr, 4 direct */
   double rel_residual;
   double seconds;     /* device time of the whole advance (CUDA events) */
   double t_rhs, t_krylov, t_back;
@@ -199,7 +205,8 @@ void pf_host_free(void* p);
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
  * backward over every subdomain), 3 the local dual-operator products alone,
- * 4 one mortar Gram solve Q, 5 one dense coarse GEMV. */
+ * 4 one mortar Gram solve Q, 5 one dense coarse GEMV, 6 the GEMV of the direct
+ * interface solve ([Z | Y_c] applied once; PF_KRYLOV_DIRECT contexts). */
 int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
 /* nsteps device-resident StepSolver::advance calls bracketed by CUDA events. */
 int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total);

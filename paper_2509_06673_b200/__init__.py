@@ -42,8 +42,8 @@ LIB_PATH = os.path.join(PKG, "_lib", "libporofeti_b200" + ("_" + os.environ["PF_
 
 SCENARIOS = {"mms-t": 0, "mms": 1, "injection": 2, "barry-mercer": 3}
 PRECONDS = {"identity": 0, "generalized": 1, "dirichlet": 2, "generalized-mortar": 3, "dirichlet-mortar": 4}
-KRYLOV = {"auto": 0, "pcg": 1, "minres": 2, "sqmr": 3}
-METHODS = {1: "pcg", 2: "minres", 3: "sqmr"}
+KRYLOV = {"auto": 0, "pcg": 1, "minres": 2, "sqmr": 3, "direct": 4, "monolithic": 4}
+METHODS = {1: "pcg", 2: "minres", 3: "sqmr", 4: "direct"}
 
 
 class Error(RuntimeError):

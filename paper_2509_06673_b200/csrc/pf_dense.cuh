@@ -105,9 +105,14 @@ __global__ void __launch_bounds__(kDgThreads) k_dgemm(int M, int N, int K, doubl
 /// Diagonal block of the blocked Cholesky: A[k0:k0+nb, k0:k0+nb] = L L^T in
 /// place (lower), and Linv = L^{-1} (nb x nb, column-major, ld nb; zero above
 /// the diagonal).  One CTA; the block staged in shared memory.
+/// With `sg` (signed Cholesky of a symmetric quasi-definite matrix, A = L S L^T
+/// with S = diag(sg) of +-1, no pivoting): the pivot's sign goes to sg[k0 + j],
+/// l_jj = sqrt(|d_j|), l_ij = r_ij / (s_j l_jj); a pivot below pivmin fails.
 constexpr int kChNb = 64;
-__global__ void __launch_bounds__(256) k_potrf_diag(int n, double* A, int lda, int k0, double* Linv, int* err) {
+__global__ void __launch_bounds__(256) k_potrf_diag(int n, double* A, int lda, int k0, double* Linv, int* err,
+                                                    int* sg = nullptr, double pivmin = 0.0) {
   __shared__ double S[kChNb][kChNb + 1];
+  __shared__ double sj[kChNb];
   const int nb = min(kChNb, n - k0), tid = threadIdx.x;
   for (int q = tid; q < nb * nb; q += blockDim.x) {
     const int i = q % nb, j = q / nb;
@@ -116,19 +121,20 @@ __global__ void __launch_bounds__(256) k_potrf_diag(int n, double* A, int lda, i
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
     const double d = S[j][j];
-    if (!(d > 0.0)) {
-      if (tid == 0) atomicExch(err, 1);
+    const double sgn = sg ? (d < 0.0 ? -1.0 : 1.0) : 1.0;
+    if (sg ? !(fabs(d) > pivmin) : !(d > 0.0)) {
+      if (tid == 0) atomicExch(err, 1 + k0 + j);
       return;
     }
-    const double s = sqrt(d);
+    const double s = sqrt(fabs(d));
     __syncthreads();
-    if (tid == 0) S[j][j] = s;
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) S[i][j] /= s;
+    if (tid == 0) S[j][j] = s, sj[j] = sgn;
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) S[i][j] /= sgn * s;
     __syncthreads();
     // right-looking update of the remaining lower triangle
     for (int q = tid; q < (nb - j - 1) * (nb - j - 1); q += blockDim.x) {
       const int i = j + 1 + q % (nb - j - 1), c = j + 1 + q / (nb - j - 1);
-      if (i >= c) S[i][c] -= S[i][j] * S[c][j];
+      if (i >= c) S[i][c] -= sgn * S[i][j] * S[c][j];
     }
     __syncthreads();
   }
@@ -136,6 +142,8 @@ __global__ void __launch_bounds__(256) k_potrf_diag(int n, double* A, int lda, i
     const int i = q % nb, j = q / nb;
     if (i >= j) A[(k0 + i) + (long long)(k0 + j) * lda] = S[i][j];
   }
+  if (sg)
+    for (int j = tid; j < nb; j += blockDim.x) sg[k0 + j] = sj[j] < 0.0 ? -1 : 1;
   // L^{-1}: thread per column, forward substitution (column j of the inverse)
   for (int j = tid; j < nb; j += blockDim.x) {
     double x[kChNb];
@@ -146,6 +154,28 @@ __global__ void __launch_bounds__(256) k_potrf_diag(int n, double* A, int lda, i
     }
     for (int i = 0; i < nb; ++i) Linv[i + (long long)j * kChNb] = i < j ? 0.0 : x[i];
   }
+}
+
+/// signed Cholesky helpers: T = P (copy, m x kb, ld_t = m) and P[:, j] *= sg[j]
+/// (the panel becomes L21 = A21 L11^{-T} S11; T keeps A21 L11^{-T} = L21 S11
+/// for the trailing update A22 -= L21 T^T)
+__global__ void k_panel_signs(int m, int kb, double* P, int ldp, double* T, const int* __restrict__ sg) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)m * kb) return;
+  const int i = (int)(q % m), j = (int)(q / m);
+  const double v = P[i + (long long)j * ldp];
+  T[i + (long long)j * m] = v;
+  P[i + (long long)j * ldp] = sg[j] < 0 ? -v : v;
+}
+
+/// D[i + j ld] = sg[i] * Y[i + j ld] (rows scaled by the pivot signs: S Y)
+__global__ void k_scale_rows(int n, const double* __restrict__ Y, double* D, int ld, const int* __restrict__ sg) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)n * n) return;
+  const int i = (int)(q % n);
+  const long long j = q / n;
+  const double v = Y[i + j * ld];
+  D[i + j * ld] = sg[i] < 0 ? -v : v;
 }
 
 /// T[:, c0 + i] += e_i for i < nb (rows 0..nb of a block row): the identity
@@ -161,6 +191,102 @@ __global__ void k_copy_rows(int nb, int N, const double* S, int lds, double* Y, 
   if (q >= (long long)nb * N) return;
   const int i = (int)(q % nb), j = (int)(q / nb);
   Y[(r0 + i) + (long long)j * ldy] = S[i + (long long)j * lds];
+}
+
+
+// ---------------------------------------------------------------------------
+// Direct interface solve (the GPU analogue of MonolithicSolver, feti.hpp:313-440)
+// ---------------------------------------------------------------------------
+/// F[g_i, g_j] += F_s[i][j] for every owned subdomain (CTA per subdomain; F_s
+/// row-major n_s x n_s at op[s], local multiplier g = lam[loff[s] + i], < 0:
+/// padding).  An entry of F receives at most two contributions (the multipliers
+/// of one interface lie in its two subdomains; two distinct interfaces share at
+/// most one), and (0 + a) + b == (0 + b) + a in IEEE arithmetic, so the atomic
+/// sums are deterministic.  F column-major n x n (symmetric).
+__global__ void k_dense_assemble(int np, const int* __restrict__ nloc, const long long* __restrict__ op,
+                                 const double* __restrict__ Fs, const long long* __restrict__ loff,
+                                 const int* __restrict__ lam, double* F, int n) {
+  const int s = blockIdx.x, m = nloc[s];
+  const double* A = Fs + op[s];
+  const int* g = lam + loff[s];
+  for (long long q = threadIdx.x; q < (long long)m * m; q += blockDim.x) {
+    const int i = (int)(q / m), j = (int)(q % m);
+    const int gi = g[i], gj = g[j];
+    if (gi >= 0 && gj >= 0) atomicAdd(F + (long long)gi + (long long)gj * n, A[q]);
+  }
+}
+
+/// G dense (n x nc, column-major, zeroed) from the CSR of G^T: column c = row c
+__global__ void k_csr_rows_to_cols(int nc, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                   const double* __restrict__ val, double* G, int n) {
+  const int c = blockIdx.x;
+  for (int q = ptr[c] + threadIdx.x; q < ptr[c + 1]; q += blockDim.x) G[idx[q] + (long long)c * n] = val[q];
+}
+
+/// Z row-major with ld: Z[i * ld + n + c] = Yc[i + c * n] (the coarse columns
+/// of the augmented solution operator [Z | Y_c])
+__global__ void k_aug_coarse(int n, int nc, const double* __restrict__ Yc, double* Z, long long ld) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)n * nc) return;
+  const int i = (int)(q % n), c = (int)(q / n);
+  Z[(long long)i * ld + n + c] = Yc[q];
+}
+
+/// y = A x for a row-major M x N A (ld even: 16-byte rows) too wide for x to
+/// sit in shared memory whole: x staged in chunks of kGvChunk, a warp per two
+/// rows (16-byte loads, eight in flight per lane and row), partial sums in a
+/// fixed lane order and a warp tree: deterministic.  HBM-bound: 8 B per
+/// matrix value, each read once.
+constexpr int kGvChunk = 4096, kGvRows = 2, kGvWarps = 8;
+__global__ void __launch_bounds__(32 * kGvWarps) k_gemv_rows(int M, int N, const double* __restrict__ A,
+                                                            long long ld, const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+  __shared__ __align__(16) double xs[kGvChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (blockIdx.x * kGvWarps + warp) * kGvRows;
+  double acc[kGvRows];
+#pragma unroll
+  for (int r = 0; r < kGvRows; ++r) acc[r] = 0.0;
+  for (int c0 = 0; c0 < N; c0 += kGvChunk) {
+    const int cn = min(kGvChunk, N - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += blockDim.x) xs[i] = x[c0 + i];
+    __syncthreads();
+    const int npair = cn >> 1;
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r) {
+      const int row = r0 + r;
+      if (row >= M) continue;
+      const double2* a2 = reinterpret_cast<const double2*>(A + (long long)row * ld + c0);
+      double s0 = 0.0, s1 = 0.0;
+      int p = lane;
+      for (; p + 7 * 32 < npair; p += 8 * 32) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(a2 + p + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = 2 * (p + 32 * u);
+          s0 += v[u].x * xs[c];
+          s1 += v[u].y * xs[c + 1];
+        }
+      }
+      for (; p < npair; p += 32) {
+        const double2 v = __ldcs(a2 + p);
+        s0 += v.x * xs[2 * p];
+        s1 += v.y * xs[2 * p + 1];
+      }
+      if ((cn & 1) && lane == 0) s0 += A[(long long)row * ld + c0 + cn - 1] * xs[cn - 1];
+      acc[r] += s0 + s1;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kGvRows; ++r) {
+    double v = acc[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && r0 + r < M) y[r0 + r] = v;
+  }
 }
 
 }  // namespace dev

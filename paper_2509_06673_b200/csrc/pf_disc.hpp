@@ -273,7 +273,7 @@ inline Disc build_disc(const pf_config& cfg, const double* k_override) {
   if (cfg.order != 1 && cfg.order != 2) fail(kInvalid, "fe_order must be 1 or 2");
   if (cfg.scenario < 0 || cfg.scenario > 3) fail(kInvalid, "unknown scenario id");
   if (cfg.precond < 0 || cfg.precond > 4) fail(kInvalid, "unknown preconditioner id");
-  if (cfg.krylov < 0 || cfg.krylov > 3) fail(kInvalid, "unknown krylov id");
+  if (cfg.krylov < 0 || cfg.krylov > 4) fail(kInvalid, "unknown krylov id");
   if (cfg.SX < 1 || cfg.SY < 2 || cfg.SY % 2)
     fail(kInvalid, "partition needs SX >= 1 and an even SY >= 2 (P below y=1/2, E above)");
   if (cfg.mesh_n < 1 || cfg.mesh_n % cfg.SX || cfg.mesh_n % cfg.SY)

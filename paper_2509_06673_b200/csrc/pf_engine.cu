@@ -1238,6 +1238,16 @@ struct Engine {
     if (krylov == PF_KRYLOV_MINRES) fail(kInvalid, "MINRES is provided by the oracle only in this build");
     if (krylov == PF_KRYLOV_PCG && indefinite)
       fail(kInvalid, "pcg requested but pressure multipliers make the operator indefinite");
+    if (krylov == PF_KRYLOV_DIRECT) {
+      if (nranks > 1) fail(kInvalid, "direct (monolithic) interface solve: single GPU only");
+      if (D.n_lambda > kDirectMax)
+        fail(kInvalid, "direct (monolithic) interface solve is dense: n_lambda " + std::to_string(D.n_lambda) +
+                           " exceeds " + std::to_string(kDirectMax) + " (use the FETI Krylov solvers)");
+      std::size_t fr = 0, tot = 0;
+      PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+      if (4.2 * 8.0 * D.n_lambda * (double)D.n_lambda > (double)fr)
+        fail(kInvalid, "direct (monolithic) interface solve: not enough device memory for 4 n_lambda^2 doubles");
+    }
     for (auto& S : D.subs) floating_any |= D.types[S.type].floating;
     // symbolic analysis per type (threads)
     const int nt = (int)D.types.size();
@@ -1302,6 +1312,10 @@ struct Engine {
     if (use_q) setup_q(), q_built = true, mark("mortar Gram Q");
     if (floating_any) setup_coarse(), mark("coarse space");
     setup_krylov();
+    if (krylov == PF_KRYLOV_DIRECT) {
+      if (!dn_F.p) fail(kInvalid, "direct (monolithic) interface solve needs the explicit local operators");
+      setup_direct(), mark("direct interface operator");
+    }
     if (dual) setup_backsub(), mark("explicit back-substitution");
     project_initial();
     mark("initial state");
@@ -1965,6 +1979,7 @@ struct Engine {
     // the type's first owned subdomain to 1e-12 (max norm, relative) use one
     // full copy of it through k_type_gemm; the others keep their own
     setup_shared(np, nt, nloc, ploff, pop, d_pop);
+    if (krylov == PF_KRYLOV_DIRECT) assemble_dense_F(nloc, pop, ploff, lamall);
     // symmetric packed storage (lower tile triangle) replaces the full blocks
     std::vector<long long> ppk(np);
     long long pk = 0;
@@ -2439,12 +2454,26 @@ struct Engine {
   /// block, panel P = P L_kk^{-T} and trailing A22 -= P P^T as k_dgemm), then
   /// Y = L^{-1} block row by block row (Y_i = L_ii^{-1} (E_i - L_{i,<i} Y_{<i}))
   /// and X = Y^T Y.  Fixed summation order: deterministic.
-  void dense_spd_inverse(int n, double* dA, double* dX) {
+  /// signed: A symmetric quasi-definite, A = L S L^T with the pivot signs S
+  /// (no pivoting; panel L21 = A21 L11^{-T} S11, trailing A22 -= L21 S11 L21^T)
+  /// and X = Y^T S Y; returns the number of negative pivots.
+  int dense_spd_inverse(int n, double* dA, double* dX, bool sgn = false, const char* what = "coarse problem G^T G") {
     const int nb = dev::kChNb, nblk = cdiv(n, nb);
-    DevBuf<double> Linv, Y, T;
-    DevBuf<int> err;
+    DevBuf<double> Linv, Y, T, T2;
+    DevBuf<int> err, sg;
     Linv.alloc((std::size_t)nblk * nb * nb), Y.alloc((std::size_t)n * n), T.alloc((std::size_t)nb * n);
+    if (sgn) T2.alloc((std::size_t)nb * n), sg.alloc(n);
     err.alloc(1), err.zero(st);
+    // pivots below pivmin (relative to the largest diagonal entry) are treated as zero
+    double pivmin = 0.0;
+    if (sgn) {
+      std::vector<double> dg(n);
+      PF_CUDA_CHECK(cudaMemcpy2DAsync(dg.data(), sizeof(double), dA, sizeof(double) * (n + 1), sizeof(double), n,
+                                      cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (double v : dg) pivmin = std::max(pivmin, std::fabs(v));
+      pivmin *= 1e-14;
+    }
     auto gemm = [&](bool ta, bool tb, int M, int N, int K, double alpha, const double* a, int lda, const double* b,
                     int ldb, double beta, double* c, int ldc, int lower, int ktri) {
       if (M <= 0 || N <= 0) return;
@@ -2460,18 +2489,26 @@ struct Engine {
     for (int b = 0; b < nblk; ++b) {
       const int k0 = b * nb, kb = std::min(nb, n - k0), m = n - k0 - kb;
       double* Lb = Linv.p + (std::size_t)b * nb * nb;
-      dev::k_potrf_diag<<<1, 256, 0, st>>>(n, dA, n, k0, Lb, err.p);
+      dev::k_potrf_diag<<<1, 256, 0, st>>>(n, dA, n, k0, Lb, err.p, sgn ? sg.p : nullptr, pivmin);
       ::pf::g_launches++;
       if (m > 0) {
         double* P = dA + (k0 + kb) + (std::size_t)k0 * n;
         gemm(false, true, m, kb, kb, 1.0, P, n, Lb, nb, 0.0, P, n, 0, 0);  // P L_kk^{-T} (in place: one CTA column)
-        gemm(false, true, m, m, kb, -1.0, P, n, P, n, 1.0, dA + (k0 + kb) + (std::size_t)(k0 + kb) * n, n, 1, 0);
+        if (sgn) {
+          dev::k_panel_signs<<<cdiv((long long)m * kb, 256), 256, 0, st>>>(m, kb, P, n, T2.p, sg.p + k0);
+          ::pf::g_launches++;
+          gemm(false, true, m, m, kb, -1.0, P, n, T2.p, m, 1.0, dA + (k0 + kb) + (std::size_t)(k0 + kb) * n, n, 1, 0);
+        } else {
+          gemm(false, true, m, m, kb, -1.0, P, n, P, n, 1.0, dA + (k0 + kb) + (std::size_t)(k0 + kb) * n, n, 1, 0);
+        }
       }
     }
     int herr = 0;
     PF_CUDA_CHECK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (herr) fail(kSingular, "coarse problem G^T G is not positive definite");
+    if (herr)
+      fail(kSingular, std::string(what) + (sgn ? ": zero pivot (not quasi-definite) at column " : ": not positive definite at column ") +
+                          std::to_string(herr - 1));
     PF_CUDA_CHECK(cudaMemsetAsync(Y.p, 0, sizeof(double) * (std::size_t)n * n, st));
     for (int b = 0; b < nblk; ++b) {
       const int k0 = b * nb, kb = std::min(nb, n - k0);
@@ -2481,9 +2518,139 @@ struct Engine {
       ::pf::g_launches++;
       gemm(false, false, kb, k0 + kb, kb, 1.0, Linv.p + (std::size_t)b * nb * nb, nb, T.p, nb, 0.0, Y.p + k0, n, 0, 0);
     }
-    gemm(true, false, n, n, n, 1.0, Y.p, n, Y.p, n, 0.0, dX, n, 0, 1);  // X = Y^T Y
+    int nneg = 0;
+    if (sgn) {  // X = Y^T (S Y); L (in dA) is no longer needed
+      dev::k_scale_rows<<<cdiv((long long)n * n, 256), 256, 0, st>>>(n, Y.p, dA, n, sg.p);
+      ::pf::g_launches++;
+      gemm(true, false, n, n, n, 1.0, Y.p, n, dA, n, 0.0, dX, n, 0, 1);
+      std::vector<int> hs(n);
+      PF_CUDA_CHECK(cudaMemcpyAsync(hs.data(), sg.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int v : hs) nneg += v < 0;
+    } else {
+      gemm(true, false, n, n, n, 1.0, Y.p, n, Y.p, n, 0.0, dX, n, 0, 1);  // X = Y^T Y
+    }
     PF_CUDA_CHECK(cudaGetLastError());
     PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    return nneg;
+  }
+
+  // ------------------------------------------------------------------
+  // Direct interface solve: the GPU analogue of MonolithicSolver
+  // (feti.hpp:313-440, REF SolverChoice::monolithic).  The full coupled system
+  // [[K, B^T], [B, 0]] is condensed exactly onto the multipliers: with the
+  // rigid-mode constraint of the floating subdomains the interface problem is
+  //   F lambda + G_c mu = rhs,  G_c^T lambda = e,
+  // whose solution is lambda = Z rhs + Y_c e with
+  //   Z = F^{-1} - W S_c^{-1} W^T,  Y_c = W S_c^{-1},  W = F^{-1} G_c,  S_c = G_c^T W.
+  // F (dense, assembled from the explicit local operators F_s) is symmetric
+  // quasi-definite (F_uu > 0, F_pp < 0): its inverse comes
+  // from a signed Cholesky F = L S L^T on the FP64 tensor cores without
+  // pivoting (dense_spd_inverse(signed)); so does S_c^{-1}.  Per step one
+  // HBM-bound GEMV with [Z | Y_c] replaces the Krylov loop; u, xi, eta, p
+  // follow from the same back-substitution.  Dense: for n_lambda up to
+  // kDirectMax (c1, c2, c3, c5; c4's 162k multipliers would need 211 GB).
+  static constexpr int kDirectMax = 65536;
+  DevBuf<double> dn_F, dn_Z, dn_x;
+  long long dn_ld = 0;
+  int dn_nneg = 0;
+  double dn_setup_s = 0.0;
+
+  void assemble_dense_F(const std::vector<int>& nloc, const std::vector<long long>& pop,
+                        const std::vector<long long>& ploff, const std::vector<int>& lamall) {
+    const int n = D.n_lambda, np = nown();
+    dn_F.alloc((std::size_t)n * n);
+    dn_F.zero(st);
+    DevBuf<int> d_nl, d_lam;
+    DevBuf<long long> d_op, d_lo;
+    d_nl.upload(nloc), d_op.upload(pop), d_lo.upload(ploff), d_lam.upload(lamall);
+    dev::k_dense_assemble<<<np, 256, 0, st>>>(np, d_nl.p, d_op.p, dl_F.p, d_lo.p, d_lam.p, dn_F.p, n);
+    ::pf::g_launches++;
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  void setup_direct() {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = D.n_lambda;
+    DevBuf<double> X;
+    X.alloc((std::size_t)n * n);
+    dn_nneg = dense_spd_inverse(n, dn_F.p, X.p, true, "interface operator F");
+    dn_F = DevBuf<double>();
+    dn_ld = n + nc + ((n + nc) & 1);  // even: 16-byte aligned rows
+    auto gemm = [&](bool ta, bool tb, int M, int N, int K, double alpha, const double* a, int lda, const double* b,
+                    int ldb, double beta, double* c, int ldc) {
+      const dim3 grid(cdiv(M, dev::kDgM), cdiv(N, dev::kDgN));
+      if (!ta && tb)
+        dev::k_dgemm<false, true><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, 0, 0);
+      else if (!ta && !tb)
+        dev::k_dgemm<false, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, 0, 0);
+      else
+        dev::k_dgemm<true, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, 0, 0);
+      ::pf::g_launches++;
+    };
+    DevBuf<double> Yc;
+    if (nc > 0) {
+      // G_c dense (n x nc, column-major) from the CSR of G_c^T (row c = column c)
+      DevBuf<double> Gd, W, Sc, Sci;
+      Gd.alloc((std::size_t)n * nc), Gd.zero(st);
+      dev::k_csr_rows_to_cols<<<nc, 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, Gd.p, n);
+      ::pf::g_launches++;
+      W.alloc((std::size_t)n * nc), Sc.alloc((std::size_t)nc * nc), Sci.alloc((std::size_t)nc * nc);
+      Yc.alloc((std::size_t)n * nc);
+      gemm(false, false, n, nc, n, 1.0, X.p, n, Gd.p, n, 0.0, W.p, n);       // W = F^{-1} G_c
+      gemm(true, false, nc, nc, n, 1.0, Gd.p, n, W.p, n, 0.0, Sc.p, nc);     // S_c = G_c^T W
+      dense_spd_inverse(nc, Sc.p, Sci.p, true, "coarse interface problem G_c^T F^{-1} G_c");
+      gemm(false, false, n, nc, nc, 1.0, W.p, n, Sci.p, nc, 0.0, Yc.p, n);   // Y_c = W S_c^{-1}
+      gemm(false, true, n, n, nc, -1.0, Yc.p, n, W.p, n, 1.0, X.p, n);       // Z = F^{-1} - Y_c W^T
+    }
+    // [Z | Y_c] row-major: row i of the (symmetric) Z is column i of X
+    dn_Z.alloc((std::size_t)n * dn_ld);
+    dn_Z.zero(st);
+    PF_CUDA_CHECK(cudaMemcpy2DAsync(dn_Z.p, sizeof(double) * dn_ld, X.p, sizeof(double) * n, sizeof(double) * n, n,
+                                    cudaMemcpyDeviceToDevice, st));
+    if (nc > 0) {
+      dev::k_aug_coarse<<<cdiv((long long)n * nc, 256), 256, 0, st>>>(n, nc, Yc.p, dn_Z.p, dn_ld);
+      ::pf::g_launches++;
+    }
+    dn_x.alloc(dn_ld), dn_x.zero(st);
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    dn_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr, "[pf] direct interface solve: n %d, coarse %d, %d negative pivots, %.3f s\n", n, nc, dn_nneg,
+                   dn_setup_s);
+  }
+
+  /// lambda = Z rhs + Y_c G_c^T lambda_in (kr_rhs = the interface right-hand
+  /// side; the coarse constraint value e = G_c^T lambda_in, the coarse part of
+  /// lambda0), one GEMV; the true residual ||P(rhs - F lambda)|| / ||P rhs|| is
+  /// reported (one F-apply).
+  void direct_solve(double* lambda, pf_report& rep) {
+    const int n = D.n_lambda;
+    PF_CUDA_CHECK(cudaMemcpyAsync(dn_x.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (nc > 0)
+      launch_pdl(dev::k_spmv_warp, cdiv(nc, 8), 256, 0, st, nc, ct_ptr.p, ct_idx.p, ct_val.p, (const double*)lambda,
+                 dn_x.p + n, 1.0, 0.0);
+    direct_gemv(lambda);
+    rep.iterations = 0;
+    rep.converged = 1;
+    rep.rel_residual = 0.0;
+    // evidence: the true residual of the returned multiplier
+    F_(lambda, kr_t.p);
+    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, kr_t.p); ::pf::g_launches++;
+    project(kr_t.p);
+    dot(n, kr_t.p, kr_t.p, dev::KS_TRUE);
+    PF_CUDA_CHECK(cudaMemcpyAsync(kr_q.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    project(kr_q.p);
+    dot(n, kr_q.p, kr_q.p, dev::KS_RHSN);
+    const double r0 = read_scal(dev::KS_RHSN);
+    rep.true_residual = r0 > 0.0 ? std::sqrt(read_scal(dev::KS_TRUE) / r0) : 0.0;
+    rep.rel_residual = rep.true_residual;
+  }
+
+  void direct_gemv(double* y) {
+    const int n = D.n_lambda, rows = dev::kGvWarps * dev::kGvRows;
+    dev::k_gemv_rows<<<cdiv(n, rows), 32 * dev::kGvWarps, 0, st>>>(n, n + nc, dn_Z.p, dn_ld, dn_x.p, y);
+    ::pf::g_launches++;
   }
 
   void setup_krylov() {
@@ -3213,6 +3380,7 @@ struct Engine {
 
   /// Krylov solve of F lambda = rhs (+ coarse), lambda in/out on device.
   void krylov_solve(double* lambda, pf_report& rep) {
+    if (krylov == PF_KRYLOV_DIRECT) return direct_solve(lambda, rep);
     const int n = D.n_lambda;
     const double tol = D.cfg.tol;
     const int maxit = D.cfg.max_iter;
@@ -3910,6 +4078,10 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
       else if (kind == 4) E.qsolve(dx.p, dy.p);
       else if (kind == 5) {
         if (E.nc) E.coarse_gemv(dx.p, dy.p);
+      }
+      else if (kind == 6) {  // the direct solve's GEMV alone ([Z | Y_c] [rhs; e])
+        if (!E.dn_Z.p) pf::fail(pf::kInvalid, "bench op 6: the direct interface solve is not active");
+        E.direct_gemv(dy.p);
       }
       else E.Ksys.solve(E.st, 1);
     };
