@@ -34,6 +34,18 @@ int main() {
       std::printf("step %d iters %d rel %.3e true %.3e err_u %.17g err_p %.17g ms %.3f\n", r.step, r.iterations,
                   r.rel_residual, r.true_residual, eu, ep, r.seconds * 1e3);
     }
+    // SolverChoice::monolithic (timeloop.hpp:139-160): the direct interface
+    // solve, the same discrete solution without Krylov iterations
+    pf_config mcfg = cfg;
+    pb::apply_solver_choice(mcfg, pb::SolverChoice::monolithic);
+    pb::Problem mono(mcfg);
+    for (int n = 0; n < mono.info().N; ++n) {
+      const pb::PcgReport r = mono.step();
+      const auto [eu, ep] = mono.errors();
+      std::printf("%s %d iters %d true %.3e err_u %.17g err_p %.17g ms %.3f\n",
+                  pb::solver_name(pb::SolverChoice::monolithic), r.step, r.iterations, r.true_residual, eu, ep,
+                  r.seconds * 1e3);
+    }
   } catch (const pb::Error& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;

@@ -103,6 +103,35 @@ inline pf_config default_config() {
   return c;
 }
 
+/// Reference SolverChoice (timeloop.hpp:113): feti-generalized and
+/// feti-schur select the FETI preconditioner (the Krylov method follows the
+/// multiplier layout); monolithic selects the direct interface solve, the
+/// device analogue of MonolithicSolver (feti.hpp:313-440): the same discrete
+/// solution without Krylov iterations (dense, n_lambda <= 65536).
+enum class SolverChoice { feti_generalized, feti_schur, monolithic };
+
+inline const char* solver_name(SolverChoice s) {
+  switch (s) {
+    case SolverChoice::feti_generalized: return "feti-generalized";
+    case SolverChoice::feti_schur: return "feti-schur";
+    default: return "monolithic";
+  }
+}
+
+/// cfg.precond / cfg.krylov for a reference SolverChoice (the mortar-scaled
+/// Dirichlet preconditioner on partitions with more than two subdomains)
+inline void apply_solver_choice(pf_config& c, SolverChoice s) {
+  const bool multi = c.SX * c.SY > 2;
+  if (s == SolverChoice::monolithic) {
+    c.krylov = PF_KRYLOV_DIRECT;
+    if (c.precond == PF_PREC_IDENTITY) c.precond = multi ? PF_PREC_DIRICHLET_MORTAR : PF_PREC_DIRICHLET;
+    return;
+  }
+  c.krylov = PF_KRYLOV_AUTO;
+  if (s == SolverChoice::feti_schur) c.precond = multi ? PF_PREC_DIRICHLET_MORTAR : PF_PREC_DIRICHLET;
+  else c.precond = multi ? PF_PREC_GENERALIZED_MORTAR : PF_PREC_GENERALIZED;
+}
+
 /// Discretisation + FETI operator living on the device.
 class Problem {
  public:

@@ -146,7 +146,21 @@ BASELINE_CONFIGS = {
 
 def make_config(mesh_n=32, SX=1, SY=2, order=1, E=1.0, nu=0.3, alpha=1.0, c0=1e-3, kperm=1.0, mu_f=1.0,
                 dt=1e-2, steps=5, mu_conv="paper", scenario="mms-t", precond="dirichlet", krylov="auto",
-                tol=1e-10, max_iter=500, warm=True, threads=0, seed=20240901, logk_mean=-2.0, logk_sd=1.0):
+                tol=1e-10, max_iter=500, warm=True, threads=0, seed=20240901, logk_mean=-2.0, logk_sd=1.0,
+                solver=None):
+    """`solver`: the reference's SolverChoice name (timeloop.hpp:113-121) --
+    "feti-generalized" / "feti-schur" pick the FETI preconditioner (mortar
+    scaled on partitions of more than two subdomains), "monolithic" the direct
+    interface solve (krylov="direct", the device analogue of MonolithicSolver)."""
+    if solver is not None:
+        multi = SX * SY > 2
+        if solver == "monolithic":
+            krylov = "direct"
+        elif solver in ("feti-schur", "feti-generalized"):
+            base = "dirichlet" if solver == "feti-schur" else "generalized"
+            precond, krylov = (base + "-mortar" if multi else base), "auto"
+        else:
+            raise ConfigError(f"unknown solver {solver!r} (feti-generalized, feti-schur, monolithic)")
     return Config(mesh_n, SX, SY, order, E, nu, alpha, c0, kperm, mu_f, dt, steps,
                   0 if mu_conv == "paper" else 1, SCENARIOS[scenario], PRECONDS[precond], KRYLOV[krylov],
                   tol, max_iter, int(warm), threads, seed, logk_mean, logk_sd)

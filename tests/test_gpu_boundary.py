@@ -172,8 +172,17 @@ def test_cpp_shim_example_builds_and_matches_reference(tmp_path):
     pieces = lines[0].split()
     assert pieces[0] == "pieces" and abs(int(pieces[4]) - int(z["iters1"])) <= 2
     assert abs(float(pieces[10]) - np.linalg.norm(z["lambda1"])) <= 1e-8 * np.linalg.norm(z["lambda1"])
-    steps = [ln.split() for ln in lines[1:]]
+    steps = [ln.split() for ln in lines[1:] if ln.startswith("step ")]
     assert len(steps) == 5
+    # SolverChoice::monolithic through the shim: the reference's own monolithic
+    # run's error norms (tests/golden/ref_c1_monolithic.npz), no iterations
+    zm = load("c1_monolithic")
+    mono = [ln.split() for ln in lines[1:] if ln.startswith("monolithic ")]
+    assert len(mono) == 5
+    for k, f in enumerate(mono, start=1):
+        assert int(f[1]) == k and int(f[3]) == 0 and float(f[5]) <= 1e-12
+        assert abs(float(f[7]) - float(zm[f"err_u{k}"])) <= 1e-8 * float(zm[f"err_u{k}"])
+        assert abs(float(f[9]) - float(zm[f"err_p{k}"])) <= 1e-8 * float(zm[f"err_p{k}"])
     for k, f in enumerate(steps, start=1):
         assert int(f[1]) == k and abs(int(f[3]) - int(z[f"iters{k}"])) <= 2
         assert float(f[7]) <= 1e-10  # true residual
