@@ -52,9 +52,14 @@ extern "C" {
 #define PF_KRYLOV_SQMR 3
 /* direct interface solve, the GPU analogue of the reference's monolithic
  * solver (SolverChoice::monolithic, feti.hpp:313-440, timeloop.hpp:139-160):
- * the coupled system condensed exactly onto the multipliers and solved with a
- * dense inverse of the interface operator (n_lambda <= 65536) — no Krylov
- * iterations; the same fields as the reference's direct solve */
+ * the coupled system condensed exactly onto the multipliers — no Krylov
+ * iterations; the same fields as the reference's direct solve.  Up to 4096
+ * multipliers the interface operator is inverted densely (one GEMV per step);
+ * beyond, it is factorised sparsely: a multifrontal block LDL^T over a nested
+ * dissection of the subdomain grid, whose fronts are condensed on the FP64
+ * tensor cores and applied as one HBM-bound GEMV launch per tree depth
+ * (BASELINE c4: 162,378 multipliers, 1023 fronts).  PF_DIRECT=dense|sparse in
+ * the environment overrides the size rule (tests). */
 #define PF_KRYLOV_DIRECT 4
 
 /* Run configuration (reference RunConfig, config.hpp:17-43, plus the
@@ -94,6 +99,11 @@ typedef struct pf_info {
   double bytes_factor_stored; /* factor values stored for the per-step sweeps (after same-type sharing) */
   double flops_backsub;  /* explicit back-substitution GEMM per step (0: the sweep back-substitutes) */
   double bytes_backsub;  /* its operator + vector bytes */
+  double bytes_direct;   /* krylov = direct: operator bytes one interface solve reads (dense [Z | Y_c], or the
+                            front operators M, T of the sparse variant plus Y_c), each once */
+  double t_direct_setup; /* its setup (factorisation / inversion) in seconds */
+  int direct_sparse;     /* 1: multifrontal factorisation over the subdomain grid (pf_iface.hpp) */
+  int direct_fronts;     /* its fronts */
 } pf_info;
 
 typedef struct pf_sub_info {
@@ -205,8 +215,10 @@ void pf_host_free(void* p);
 /* Device-resident micro-benchmarks (CUDA events on the context stream).
  * kind: 0 F-apply, 1 preconditioner, 2 one batched factor sweep (forward +
  * backward over every subdomain), 3 the local dual-operator products alone,
- * 4 one mortar Gram solve Q, 5 one dense coarse GEMV, 6 the GEMV of the direct
- * interface solve ([Z | Y_c] applied once; PF_KRYLOV_DIRECT contexts). */
+ * 4 one mortar Gram solve Q, 5 one dense coarse GEMV, 6 the operator of the
+ * direct interface solve applied once (PF_KRYLOV_DIRECT contexts: the dense
+ * [Z | Y_c] GEMV, or F^{-1} through the fronts of the sparse variant), 7 the
+ * sparse variant's whole interface solve (fronts + rigid-mode border Y_c). */
 int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
 /* nsteps device-resident StepSolver::advance calls bracketed by CUDA events. */
 int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total);

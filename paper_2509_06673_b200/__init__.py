@@ -101,6 +101,8 @@ class Info(C.Structure):
         ("bytes_qsolve_applied", C.c_double), ("bytes_flocal", C.c_double), ("flops_flocal", C.c_double),
         ("bytes_coarse", C.c_double), ("bytes_factor_stored", C.c_double),
         ("flops_backsub", C.c_double), ("bytes_backsub", C.c_double),
+        ("bytes_direct", C.c_double), ("t_direct_setup", C.c_double),
+        ("direct_sparse", C.c_int), ("direct_fronts", C.c_int),
     ]
 
 

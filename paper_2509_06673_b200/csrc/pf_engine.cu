@@ -31,6 +31,8 @@
 #include "pf_dense.cuh"
 #include "pf_symbolic.hpp"
 #include "pf_dual.hpp"
+#include "pf_iface.hpp"
+#include "pf_iface.cuh"
 
 namespace pf {
 
@@ -1209,6 +1211,7 @@ struct Engine {
       int lo = 0, hi = 0;
       PF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       if (std::getenv("PF_NO_PRIO")) hi = lo;  // A/B: both streams at the default priority
+      if (std::getenv("PF_HB_HI")) std::swap(lo, hi);  // A/B: the sweep first
       PF_CUDA_CHECK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
       PF_CUDA_CHECK(cudaStreamCreateWithPriority(&hb_st, cudaStreamNonBlocking, lo));
       PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev0, cudaEventDisableTiming));
@@ -1240,13 +1243,20 @@ struct Engine {
       fail(kInvalid, "pcg requested but pressure multipliers make the operator indefinite");
     if (krylov == PF_KRYLOV_DIRECT) {
       if (nranks > 1) fail(kInvalid, "direct (monolithic) interface solve: single GPU only");
-      if (D.n_lambda > kDirectMax)
-        fail(kInvalid, "direct (monolithic) interface solve is dense: n_lambda " + std::to_string(D.n_lambda) +
-                           " exceeds " + std::to_string(kDirectMax) + " (use the FETI Krylov solvers)");
-      std::size_t fr = 0, tot = 0;
-      PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
-      if (4.2 * 8.0 * D.n_lambda * (double)D.n_lambda > (double)fr)
-        fail(kInvalid, "direct (monolithic) interface solve: not enough device memory for 4 n_lambda^2 doubles");
+      // dense F^{-1} up to kDirectDense multipliers, the multifrontal
+      // factorisation over the subdomain grid beyond (PF_DIRECT=dense|sparse overrides)
+      const char* dv = std::getenv("PF_DIRECT");
+      direct_sparse = dv ? std::string(dv) == "sparse" : D.n_lambda > kDirectDense;
+      if (D.SX * D.SY < 2) direct_sparse = false;
+      if (!direct_sparse) {
+        if (D.n_lambda > kDirectMax)
+          fail(kInvalid, "direct (monolithic) interface solve, dense variant: n_lambda " + std::to_string(D.n_lambda) +
+                             " exceeds " + std::to_string(kDirectMax));
+        std::size_t fr = 0, tot = 0;
+        PF_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+        if (4.2 * 8.0 * D.n_lambda * (double)D.n_lambda > (double)fr)
+          fail(kInvalid, "direct (monolithic) interface solve: not enough device memory for 4 n_lambda^2 doubles");
+      }
     }
     for (auto& S : D.subs) floating_any |= D.types[S.type].floating;
     // symbolic analysis per type (threads)
@@ -1313,8 +1323,10 @@ struct Engine {
     if (floating_any) setup_coarse(), mark("coarse space");
     setup_krylov();
     if (krylov == PF_KRYLOV_DIRECT) {
-      if (!dn_F.p) fail(kInvalid, "direct (monolithic) interface solve needs the explicit local operators");
-      setup_direct(), mark("direct interface operator");
+      if (direct_sparse ? !if_on : !dn_F.p)
+        fail(kInvalid, "direct (monolithic) interface solve needs the explicit local operators");
+      direct_sparse ? setup_direct_sparse() : setup_direct();
+      mark("direct interface operator");
     }
     if (dual) setup_backsub(), mark("explicit back-substitution");
     project_initial();
@@ -1979,7 +1991,10 @@ struct Engine {
     // the type's first owned subdomain to 1e-12 (max norm, relative) use one
     // full copy of it through k_type_gemm; the others keep their own
     setup_shared(np, nt, nloc, ploff, pop, d_pop);
-    if (krylov == PF_KRYLOV_DIRECT) assemble_dense_F(nloc, pop, ploff, lamall);
+    if (krylov == PF_KRYLOV_DIRECT) {
+      if (direct_sparse) factor_iface(nloc, pop, ploff, lamall);
+      else assemble_dense_F(nloc, pop, ploff, lamall);
+    }
     // symmetric packed storage (lower tile triangle) replaces the full blocks
     std::vector<long long> ppk(np);
     long long pk = 0;
@@ -2439,6 +2454,7 @@ struct Engine {
     dA.upload(A);
     c_ainv.alloc((std::size_t)nc * nc);
     dense_spd_inverse(nc, dA.p, c_ainv.p);
+    spd_scratch_free();
 
     if (sizeof(double) * nc > 227 * 1024) fail(kInternal, "coarse space too large for the staged GEMV");
     if (sizeof(double) * nc > 48 * 1024)
@@ -2457,13 +2473,25 @@ struct Engine {
   /// signed: A symmetric quasi-definite, A = L S L^T with the pivot signs S
   /// (no pivoting; panel L21 = A21 L11^{-T} S11, trailing A22 -= L21 S11 L21^T)
   /// and X = Y^T S Y; returns the number of negative pivots.
+  DevBuf<double> sp_Linv, sp_Y, sp_T, sp_T2;
+  DevBuf<int> sp_err, sp_sg;
+  template <class T>
+  static void grow(DevBuf<T>& b, std::size_t count) {
+    if (b.n < count) b.alloc(count);
+  }
+  void spd_scratch_free() {
+    sp_Linv = DevBuf<double>(), sp_Y = DevBuf<double>(), sp_T = DevBuf<double>(), sp_T2 = DevBuf<double>();
+    sp_err = DevBuf<int>(), sp_sg = DevBuf<int>();
+  }
   int dense_spd_inverse(int n, double* dA, double* dX, bool sgn = false, const char* what = "coarse problem G^T G") {
     const int nb = dev::kChNb, nblk = cdiv(n, nb);
-    DevBuf<double> Linv, Y, T, T2;
-    DevBuf<int> err, sg;
-    Linv.alloc((std::size_t)nblk * nb * nb), Y.alloc((std::size_t)n * n), T.alloc((std::size_t)nb * n);
-    if (sgn) T2.alloc((std::size_t)nb * n), sg.alloc(n);
-    err.alloc(1), err.zero(st);
+    // grow-only scratch (the sparse interface factorisation calls this once per front)
+    DevBuf<double>&Linv = sp_Linv, &Y = sp_Y, &T = sp_T, &T2 = sp_T2;
+    DevBuf<int>&err = sp_err, &sg = sp_sg;
+    grow(Linv, (std::size_t)nblk * nb * nb), grow(Y, (std::size_t)n * n), grow(T, (std::size_t)nb * n);
+    if (sgn) grow(T2, (std::size_t)nb * n), grow(sg, (std::size_t)n);
+    grow(err, 1);
+    PF_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int), st));
     // pivots below pivmin (relative to the largest diagonal entry) are treated as zero
     double pivmin = 0.0;
     if (sgn) {
@@ -2549,8 +2577,10 @@ struct Engine {
   // pivoting (dense_spd_inverse(signed)); so does S_c^{-1}.  Per step one
   // HBM-bound GEMV with [Z | Y_c] replaces the Krylov loop; u, xi, eta, p
   // follow from the same back-substitution.  Dense: for n_lambda up to
-  // kDirectMax (c1, c2, c3, c5; c4's 162k multipliers would need 211 GB).
-  static constexpr int kDirectMax = 65536;
+  // kDirectDense (c1, c2; PF_DIRECT=dense: up to kDirectMax); larger interface
+  // problems use the sparse multifrontal variant below (c3, c4, c5).
+  static constexpr int kDirectMax = 65536, kDirectDense = 4096;
+  bool direct_sparse = false;
   DevBuf<double> dn_F, dn_Z, dn_x;
   long long dn_ld = 0;
   int dn_nneg = 0;
@@ -2575,6 +2605,7 @@ struct Engine {
     DevBuf<double> X;
     X.alloc((std::size_t)n * n);
     dn_nneg = dense_spd_inverse(n, dn_F.p, X.p, true, "interface operator F");
+    spd_scratch_free();
     dn_F = DevBuf<double>();
     dn_ld = n + nc + ((n + nc) & 1);  // even: 16-byte aligned rows
     auto gemm = [&](bool ta, bool tb, int M, int N, int K, double alpha, const double* a, int lda, const double* b,
@@ -2600,6 +2631,7 @@ struct Engine {
       gemm(false, false, n, nc, n, 1.0, X.p, n, Gd.p, n, 0.0, W.p, n);       // W = F^{-1} G_c
       gemm(true, false, nc, nc, n, 1.0, Gd.p, n, W.p, n, 0.0, Sc.p, nc);     // S_c = G_c^T W
       dense_spd_inverse(nc, Sc.p, Sci.p, true, "coarse interface problem G_c^T F^{-1} G_c");
+      spd_scratch_free();
       gemm(false, false, n, nc, nc, 1.0, W.p, n, Sci.p, nc, 0.0, Yc.p, n);   // Y_c = W S_c^{-1}
       gemm(false, true, n, n, nc, -1.0, Yc.p, n, W.p, n, 1.0, X.p, n);       // Z = F^{-1} - Y_c W^T
     }
@@ -2626,11 +2658,20 @@ struct Engine {
   /// reported (one F-apply).
   void direct_solve(double* lambda, pf_report& rep) {
     const int n = D.n_lambda;
+    if (if_on) {
+      direct_apply_sparse(lambda);
+      return direct_report(lambda, rep);
+    }
     PF_CUDA_CHECK(cudaMemcpyAsync(dn_x.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     if (nc > 0)
       launch_pdl(dev::k_spmv_warp, cdiv(nc, 8), 256, 0, st, nc, ct_ptr.p, ct_idx.p, ct_val.p, (const double*)lambda,
                  dn_x.p + n, 1.0, 0.0);
     direct_gemv(lambda);
+    direct_report(lambda, rep);
+  }
+
+  void direct_report(double* lambda, pf_report& rep) {
+    const int n = D.n_lambda;
     rep.iterations = 0;
     rep.converged = 1;
     rep.rel_residual = 0.0;
@@ -2651,6 +2692,248 @@ struct Engine {
     const int n = D.n_lambda, rows = dev::kGvWarps * dev::kGvRows;
     dev::k_gemv_rows<<<cdiv(n, rows), 32 * dev::kGvWarps, 0, st>>>(n, n + nc, dn_Z.p, dn_ld, dn_x.p, y);
     ::pf::g_launches++;
+  }
+
+
+  // ------------------------------------------------------------------
+  // Sparse direct interface solve (pf_iface.hpp / pf_iface.cuh): the direct
+  // solve above for partitions whose dense F does not fit (BASELINE c4:
+  // 162,378 multipliers).  F is never formed: the subdomains' explicit local
+  // operators F_s are condensed bottom-up over a nested dissection of the
+  // subdomain grid; each front's separator block is inverted by the signed
+  // Cholesky on the FP64 tensor cores (dense_spd_inverse), T = A21 A11^{-1}
+  // and the Schur complement A22 - T A21^T are DMMA GEMMs.  A solve is one
+  // GEMV launch per tree depth each way, every stored value read once.
+  // The rigid-mode constraint is bordered exactly as in the dense variant:
+  //   lambda = y - Y_c (G_c^T y - e),  y = F^{-1} rhs,  Y_c = W S_c^{-1},
+  //   W = F^{-1} G_c (n_c sparse solves at setup),  S_c = G_c^T W.
+  IfaceTree if_tree;
+  DevBuf<dev::IfaceFrontDev> if_fronts;
+  DevBuf<int2> if_work;
+  DevBuf<int> if_idx;
+  DevBuf<unsigned char> if_side;
+  DevBuf<double> if_M, if_T, if_u, if_y, if_Yc, if_d, if_t;
+  struct IfLaunch {
+    int mode, cls, work0, nwork;
+  };
+  std::vector<IfLaunch> if_launches;
+  bool if_on = false;
+  long long if_ldc = 0, if_values = 0;
+  double if_factor_s = 0.0;
+  int if_nneg = 0;
+
+  void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* a, int lda, const double* b, int ldb,
+             double beta, double* c, int ldc, int lower = 0, int ktri = 0) {
+    if (M <= 0 || N <= 0) return;
+    const dim3 grid(cdiv(M, dev::kDgM), cdiv(N, dev::kDgN));
+    if (!ta && tb)
+      dev::k_dgemm<false, true><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+    else if (!ta && !tb)
+      dev::k_dgemm<false, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+    else
+      dev::k_dgemm<true, false><<<grid, dev::kDgThreads, 0, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, lower, ktri);
+    ::pf::g_launches++;
+  }
+
+  static int if_class(int ncols) { return ncols >= 256 ? 0 : ncols >= 128 ? 1 : 2; }
+  static int if_rows_per_cta(int cls) { return (dev::kIfThreads / (32 >> cls)) * 4; }
+
+  /// Numeric multifrontal factorisation of F over the interface tree, from the
+  /// full (unpacked) local operators dl_F (row-major n_s x n_s at pop[p]).
+  void factor_iface(const std::vector<int>& nloc, const std::vector<long long>& pop,
+                    const std::vector<long long>& ploff, const std::vector<int>& lamall) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = D.n_lambda;
+    if_tree = build_iface_tree(D);
+    auto& FR = if_tree.fronts;
+    const int nf = (int)FR.size();
+    if (!nf) fail(kInvalid, "direct interface solve: the partition has no interface");
+    // storage: M and T per front (rows padded to an even length: 16-byte loads)
+    std::vector<dev::IfaceFrontDev> fd(nf);
+    std::vector<int> idx;
+    std::vector<unsigned char> side;
+    long long oM = 0, oT = 0;
+    for (int f = 0; f < nf; ++f) {
+      const IfaceFront& F = FR[f];
+      const int ldM = F.m() + (F.m() & 1), ldT = F.nsep + (F.nsep & 1);
+      fd[f] = dev::IfaceFrontDev{oM, oT, (long long)idx.size(), F.nsep, F.nbdry, ldM, ldT};
+      oM += (long long)F.nsep * ldM, oT += (long long)F.nbdry * ldT;
+      idx.insert(idx.end(), F.idx.begin(), F.idx.end());
+      side.insert(side.end(), F.nsep, 0);
+      side.insert(side.end(), F.side.begin(), F.side.end());
+    }
+    if_values = oM + oT;
+    if_M.alloc(std::max<long long>(1, oM)), if_T.alloc(std::max<long long>(1, oT));
+    if_M.zero(st), if_T.zero(st);
+    if_fronts.upload(fd), if_idx.upload(idx), if_side.upload(side);
+    // child -> parent position maps, all fronts in one upload
+    std::vector<int> maps, pos(n, -1);
+    std::vector<std::array<long long, 2>> moff(nf, {-1, -1});
+    for (int f = 0; f < nf; ++f) {
+      const IfaceFront& F = FR[f];
+      for (int k = 0; k < F.m(); ++k) pos[F.idx[k]] = k;
+      for (int c = 0; c < 2; ++c) {
+        const int ch = F.child[c];
+        if (ch == IfaceFront::kNone) continue;
+        moff[f][c] = (long long)maps.size();
+        if (ch >= 0) {
+          for (int k = FR[ch].nsep; k < FR[ch].m(); ++k) {
+            if (pos[FR[ch].idx[k]] < 0) fail(kInternal, "interface tree: child boundary outside its parent front");
+            maps.push_back(pos[FR[ch].idx[k]]);
+          }
+        } else {
+          const int p = local_of[-(ch + 1)];
+          for (int i = 0; i < nloc[p]; ++i) {
+            const int g = lamall[ploff[p] + i];
+            if (g >= 0 && pos[g] < 0) fail(kInternal, "interface tree: subdomain multiplier outside its parent front");
+            maps.push_back(g >= 0 ? pos[g] : -1);
+          }
+        }
+      }
+      for (int k = 0; k < F.m(); ++k) pos[F.idx[k]] = -1;
+    }
+    DevBuf<int> d_maps;
+    d_maps.upload(maps.empty() ? std::vector<int>{0} : maps);
+    // numeric: post-order, children first
+    std::vector<DevBuf<double>> front(nf);
+    DevBuf<double> P, X, Tc;
+    if_nneg = 0;
+    for (int f = 0; f < nf; ++f) {
+      const IfaceFront& F = FR[f];
+      const int ns = F.nsep, nb = F.nbdry, m = F.m();
+      if (!m) continue;
+      front[f].alloc((std::size_t)m * m);
+      front[f].zero(st);
+      double* A = front[f].p;
+      for (int c = 0; c < 2; ++c) {
+        const int ch = F.child[c];
+        if (ch == IfaceFront::kNone) continue;
+        if (ch >= 0) {
+          const IfaceFront& C = FR[ch];
+          if (C.nbdry) {
+            dev::k_iface_extend_add<<<cdiv((long long)C.nbdry * C.nbdry, 256), 256, 0, st>>>(
+                C.nbdry, front[ch].p + (long long)C.nsep * (C.m() + 1), C.m(), 0, d_maps.p + moff[f][c], A, m);
+            ::pf::g_launches++;
+          }
+        } else {
+          const int p = local_of[-(ch + 1)];
+          dev::k_iface_extend_add<<<cdiv((long long)nloc[p] * nloc[p], 256), 256, 0, st>>>(
+              nloc[p], dl_F.p + pop[p], nloc[p], 1, d_maps.p + moff[f][c], A, m);
+          ::pf::g_launches++;
+        }
+      }
+      if (ns > 0) {
+        grow(P, (std::size_t)ns * ns), grow(X, (std::size_t)ns * ns);
+        dev::k_iface_copy_sym<<<cdiv((long long)ns * ns, 256), 256, 0, st>>>(ns, A, m, P.p);
+        ::pf::g_launches++;
+        if_nneg += dense_spd_inverse(ns, P.p, X.p, true, "interface separator block");
+        if (nb > 0) {
+          grow(Tc, (std::size_t)nb * ns);
+          dgemm(false, false, nb, ns, ns, 1.0, A + ns, m, X.p, ns, 0.0, Tc.p, nb);                    // T = A21 A11^{-1}
+          dgemm(false, true, nb, nb, ns, -1.0, Tc.p, nb, A + ns, m, 1.0, A + (long long)ns * (m + 1), m, 1);  // A22 -= T A21^T
+        }
+        const long long work = (long long)ns * (ns + nb) + (long long)nb * ns;
+        dev::k_iface_store<<<cdiv(work, 256), 256, 0, st>>>(ns, nb, X.p, Tc.p, if_M.p + fd[f].offM, fd[f].ldM,
+                                                             if_T.p + fd[f].offT, fd[f].ldT);
+        ::pf::g_launches++;
+      }
+      // the children's Schur complements are consumed (cudaFree waits for the stream)
+      for (int c = 0; c < 2; ++c)
+        if (F.child[c] >= 0) front[F.child[c]] = DevBuf<double>();
+    }
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    front.clear();
+    spd_scratch_free();
+    // solve schedule: forward from the deepest fronts up, backward from the root down
+    std::vector<int2> work;
+    if_launches.clear();
+    for (int mode = 0; mode < 2; ++mode)
+      for (int step = 0; step < if_tree.ndepth; ++step) {
+        const int depth = mode ? step : if_tree.ndepth - 1 - step;
+        for (int cls = 0; cls < 3; ++cls) {
+          const int w0 = (int)work.size(), rpc = if_rows_per_cta(cls);
+          for (int f = 0; f < nf; ++f) {
+            const IfaceFront& F = FR[f];
+            if (F.depth != depth || !F.nsep || (!mode && !F.nbdry)) continue;
+            if (if_class(mode ? F.m() : F.nsep) != cls) continue;
+            for (int r = 0; r < (mode ? F.nsep : F.nbdry); r += rpc) work.push_back(make_int2(f, r));
+          }
+          if ((int)work.size() > w0) if_launches.push_back(IfLaunch{mode, cls, w0, (int)work.size() - w0});
+        }
+      }
+    if_work.upload(work);
+    if_u.alloc(2 * (std::size_t)n), if_y.alloc(n), if_t.alloc(n);
+    if_on = true;
+    if_factor_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr,
+                   "[pf] sparse direct interface solve: n %d, %d fronts, depth %d, %.1f M stored values, %d negative "
+                   "pivots, %zu launches per solve, factorisation %.3f s\n",
+                   n, nf, if_tree.ndepth, if_values * 1e-6, if_nneg, if_launches.size(), if_factor_s);
+  }
+
+  /// x = F^{-1} b through the front operators (b is not modified)
+  void iface_solve(const double* b, double* x) {
+    const int n = D.n_lambda;
+    PF_CUDA_CHECK(cudaMemsetAsync(if_u.p, 0, sizeof(double) * 2 * n, st));
+    dev::IfaceSolve S;
+    S.fronts = if_fronts.p, S.work = if_work.p, S.idx = if_idx.p, S.side = if_side.p;
+    S.M = if_M.p, S.T = if_T.p, S.b = b, S.u0 = if_u.p, S.u1 = if_u.p + n, S.x = x;
+    for (const IfLaunch& L : if_launches) {
+#define PF_IF_LAUNCH(MODE, CLS) \
+  if (L.mode == MODE && L.cls == CLS) \
+    launch_pdl(dev::k_iface_gemv<MODE, (32 >> CLS), 4>, L.nwork, dev::kIfThreads, 0, st, S, L.work0);
+      PF_IF_LAUNCH(0, 0) PF_IF_LAUNCH(0, 1) PF_IF_LAUNCH(0, 2) PF_IF_LAUNCH(1, 0) PF_IF_LAUNCH(1, 1) PF_IF_LAUNCH(1, 2)
+#undef PF_IF_LAUNCH
+    }
+  }
+
+  /// the coarse border of the sparse direct solve: Y_c = W S_c^{-1} row-major
+  void setup_direct_sparse() {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = D.n_lambda;
+    if (nc > 0) {
+      DevBuf<double> Gd, W, Sc, Sci, Yc;
+      Gd.alloc((std::size_t)n * nc), Gd.zero(st);
+      dev::k_csr_rows_to_cols<<<nc, 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, Gd.p, n);
+      ::pf::g_launches++;
+      W.alloc((std::size_t)n * nc), Sc.alloc((std::size_t)nc * nc), Sci.alloc((std::size_t)nc * nc);
+      for (int c = 0; c < nc; ++c) iface_solve(Gd.p + (std::size_t)c * n, W.p + (std::size_t)c * n);  // W = F^{-1} G_c
+      dgemm(true, false, nc, nc, n, 1.0, Gd.p, n, W.p, n, 0.0, Sc.p, nc);                                // S_c = G_c^T W
+      Gd = DevBuf<double>();
+      dense_spd_inverse(nc, Sc.p, Sci.p, true, "coarse interface problem G_c^T F^{-1} G_c");
+      spd_scratch_free();
+      Yc.alloc((std::size_t)n * nc);
+      dgemm(false, false, n, nc, nc, 1.0, W.p, n, Sci.p, nc, 0.0, Yc.p, n);                              // Y_c = W S_c^{-1}
+      W = DevBuf<double>();
+      if_ldc = nc + (nc & 1);
+      if_Yc.alloc((std::size_t)n * if_ldc), if_Yc.zero(st);
+      dev::k_iface_to_rows<<<cdiv((long long)n * nc, 256), 256, 0, st>>>(n, nc, Yc.p, if_Yc.p, if_ldc);
+      ::pf::g_launches++;
+      if_d.alloc(if_ldc), if_d.zero(st);
+      PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    dn_nneg = if_nneg;
+    dn_setup_s = if_factor_s + std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr, "[pf] sparse direct interface solve: coarse border %d columns, setup %.3f s in total\n", nc,
+                   dn_setup_s);
+  }
+
+  /// lambda = y - Y_c G_c^T (y - lambda_in), y = F^{-1} rhs (lambda_in carries the
+  /// coarse constraint value e = G_c^T lambda_in)
+  void direct_apply_sparse(double* lambda) {
+    const int n = D.n_lambda;
+    if (nc == 0) return iface_solve(kr_rhs.p, lambda);
+    iface_solve(kr_rhs.p, if_y.p);
+    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, if_y.p, -1.0, lambda); ::pf::g_launches++;  // y - lambda_in
+    launch_pdl(dev::k_spmv_warp, cdiv(nc, 8), 256, 0, st, nc, ct_ptr.p, ct_idx.p, ct_val.p, (const double*)lambda,
+               if_d.p, 1.0, 0.0);
+    const int rows = dev::kGvWarps * dev::kGvRows;
+    dev::k_gemv_rows<<<cdiv(n, rows), 32 * dev::kGvWarps, 0, st>>>(n, nc, if_Yc.p, if_ldc, if_d.p, if_t.p);
+    ::pf::g_launches++;
+    PF_CUDA_CHECK(cudaMemcpyAsync(lambda, if_y.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, -1.0, if_t.p, 1.0, lambda); ::pf::g_launches++;
   }
 
   void setup_krylov() {
@@ -2714,6 +2997,13 @@ struct Engine {
     info.bytes_factor_stored = 8.0 * (double)Ksys.total_L;
     info.flops_backsub = hb_on ? hb_flops : 0.0;
     info.bytes_backsub = hb_on ? hb_bytes : 0.0;
+    info.bytes_direct = 0.0, info.t_direct_setup = dn_setup_s, info.direct_sparse = if_on, info.direct_fronts = 0;
+    if (if_on) {
+      info.bytes_direct = 8.0 * ((double)if_values + (double)D.n_lambda * (double)if_ldc);
+      info.direct_fronts = (int)if_tree.fronts.size();
+    } else if (dn_Z.p) {
+      info.bytes_direct = 8.0 * (double)D.n_lambda * (double)dn_ld;
+    }
   }
 
   // ------------------------------------------------------------------
@@ -4080,8 +4370,14 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
         if (E.nc) E.coarse_gemv(dx.p, dy.p);
       }
       else if (kind == 6) {  // the direct solve's GEMV alone ([Z | Y_c] [rhs; e])
-        if (!E.dn_Z.p) pf::fail(pf::kInvalid, "bench op 6: the direct interface solve is not active");
-        E.direct_gemv(dy.p);
+        if (E.if_on) E.iface_solve(dx.p, dy.p);  // sparse variant: y = F^{-1} x through the front operators
+        else if (!E.dn_Z.p) pf::fail(pf::kInvalid, "bench op 6: the direct interface solve is not active");
+        else E.direct_gemv(dy.p);
+      }
+      else if (kind == 7) {  // sparse direct solve incl. the rigid-mode border (one step's interface solve)
+        if (!E.if_on) pf::fail(pf::kInvalid, "bench op 7: the sparse direct interface solve is not active");
+        PF_CUDA_CHECK(cudaMemcpyAsync(dy.p, dx.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, E.st));
+        E.direct_apply_sparse(dy.p);
       }
       else E.Ksys.solve(E.st, 1);
     };
