@@ -11,6 +11,13 @@ scaled Dirichlet preconditioner, natural coarse projector) and the
 back-substitution.  Inputs (factors, ~16 GB) are far larger than L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+                  [--solver feti|direct]
+
+--solver feti (default) times the FETI Krylov step, the reference's feti-schur
+path with the same tolerance; its line also carries "direct_solver": the same
+K steps through the direct interface solve (krylov="direct", the GPU analogue
+of the reference's SolverChoice::monolithic), measured in the same run.
+--solver direct makes that solver the line's `value`.
 
 --impl reference times the reference's CPU path on the host cores: the C++
 oracle restatement of the reference algorithm (oracle/, all host threads; the
@@ -236,6 +243,64 @@ def run_reference(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
+def direct_arm(args, cfg_name, peak):
+    """K time steps through the direct interface solve (krylov="direct": the
+    multipliers condensed exactly -- dense inverse up to 4096 multipliers, a
+    multifrontal block LDL^T over the subdomain grid above), device time,
+    end to end through pf_advance with pinned host buffers, and the interface
+    solve's GEMV launches against the HBM roofline (every stored front value
+    is read once per solve)."""
+    import numpy as np
+    import paper_2509_06673_b200 as pf
+
+    kw = dict(pf.BASELINE_CONFIGS[cfg_name], krylov="direct")
+    kw["steps"] = max(kw["steps"], args.warmup + 2 * args.steps + 2)
+    t0 = time.perf_counter()
+    op = pf.FetiOperator(**kw)
+    setup_s = time.perf_counter() - t0
+    info = op.info
+    reps = [op.step() for _ in range(args.warmup)]
+    l0 = pf.launch_count()
+    ms, _, _ = op.bench_steps(args.steps)
+    launches = pf.launch_count() - l0
+    xs, lam = op.state()
+    x_cat = np.concatenate(xs)
+    step_idx = pf.lib().pf_current_step(op.h)
+    solver = pf.StepSolver(op)
+    pin = [[pf.pinned_empty(n) for n in (x_cat.size, lam.size)] for _ in range(2)]
+    pin[0][0][:] = x_cat
+    pin[0][1][:] = lam
+    t0 = time.perf_counter()
+    cur_k = step_idx
+    for k in range(args.steps):
+        src, dst = pin[k % 2], pin[(k + 1) % 2]
+        _, _, rep = solver.advance(src[0], src[1], cur_k, out_x=dst[0], out_lambda=dst[1])
+        cur_k = rep["step"]
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    h2d = int(pf.lib().pf_last_h2d_bytes(op.h))
+    rep = op.step()
+    out = {"what": "direct interface solve (krylov=direct): " +
+                   ("multifrontal block LDL^T of F over a nested dissection of the subdomain grid, "
+                    f"{info.direct_fronts} fronts" if info.direct_sparse else "dense inverse of F, one GEMV per step"),
+           "value": ms * 1e-3 / args.steps, "unit": "s/step", "steps": args.steps, "warmup": args.warmup,
+           "iterations_per_step": 0,
+           "true_residual": max([r["true_residual"] for r in reps] + [rep["true_residual"]]),
+           "phase_ms": {"rhs": rep["t_rhs"] * 1e3, "interface_solve": rep["t_krylov"] * 1e3,
+                        "back_substitution": rep["t_back"] * 1e3},
+           "e2e": {"value": e2e_s, "unit": "s/step", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": int(x_cat.nbytes + lam.nbytes)},
+           "setup_s": setup_s, "direct_setup_s": info.t_direct_setup, "gpu_launches": int(launches)}
+    # roofline of the interface solve: stored operator bytes once per solve
+    t7 = op.bench(7, 5, 20)[0]
+    b = float(info.bytes_direct)
+    out["roofline"] = {"bound": "hbm", "kernel": "k_iface_gemv<fwd/bwd> per tree depth + coarse border GEMV"
+                       if info.direct_sparse else "k_gemv_rows: lambda = [Z | Y_c] [rhs; e]",
+                       "ms": t7, "algorithmic_bytes_per_launch": b, "achieved": b / (t7 * 1e-3) / 1e9, "peak": peak,
+                       "unit": "GB/s", "frac": b / (t7 * 1e-3) / 1e9 / peak}
+    op.close()
+    return out
+
+
 def run_ours(args, rank, world, dist):
     import numpy as np
     import paper_2509_06673_b200 as pf
@@ -416,9 +481,42 @@ def run_ours(args, rank, world, dist):
         except Exception as exc:  # the baseline is reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "s/step", "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc}"}
+    op.close()
+    if rank == 0 and world == 1 and args.direct:
+        try:  # the same K steps through the direct interface solve, same run
+            line["direct_solver"] = direct_arm(args, args.config, peak)
+        except Exception as exc:  # reported, never fatal for the FETI line
+            line["direct_solver"] = {"failed": str(exc)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    op.close()
+
+
+def run_direct(args, rank, world, dist):
+    """--solver direct: the direct interface solve as the line's value (one
+    GPU; the sharded engine keeps the FETI Krylov path)."""
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"solver": "direct", "unavailable": "the direct interface solve runs on one GPU"}),
+                  flush=True)
+        return
+    peak, peak_src = _peaks()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        d = direct_arm(args, args.config, peak)
+    import paper_2509_06673_b200 as pf
+    kw = pf.BASELINE_CONFIGS[args.config]
+    line = {"metric": METRIC, "value": d["value"], "unit": "s/step", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": d["value"] * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured solution)",
+            "config": {"workload": (f"BASELINE {args.config}: mesh {kw['mesh_n']}^2 P{kw['order']}, "
+                                    f"{kw['SX']}x{kw['SY']} subdomains, direct interface solve"),
+                       "solver": d["what"],
+                       "l2": "no flush: the interface solve streams its stored fronts once per step (> L2 at c4)",
+                       "parallelism": "single GPU"},
+            "iterations_per_step": 0, "true_residual": d["true_residual"], "phase_ms": d["phase_ms"],
+            "e2e": d["e2e"], "roofline": dict(d["roofline"], traffic=None, peak_source=peak_src),
+            "gpu_launches": d["gpu_launches"], "clocks": clk.summary(), "setup_s": d["setup_s"],
+            "direct_setup_s": d["direct_setup_s"]}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -428,6 +526,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--solver", default="feti", choices=["feti", "direct"],
+                    help="feti: FETI Krylov step (default, + a direct_solver object); direct: the direct "
+                         "interface solve as the line's value")
+    ap.add_argument("--no-direct", dest="direct", action="store_false",
+                    help="--solver feti: skip the direct_solver object")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--ref-budget", type=float, default=240.0,
                     help="--impl reference: wall seconds for the timed CPU steps (at least one step)")
@@ -437,6 +540,8 @@ def main():
     rank, world, dist = dist_init(args.gpus)
     if args.impl == "reference":
         run_reference(args, rank, world, dist)
+    elif args.solver == "direct":
+        run_direct(args, rank, world, dist)
     else:
         run_ours(args, rank, world, dist)
     if dist is not None:

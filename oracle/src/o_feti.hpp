@@ -468,7 +468,12 @@ class Feti {
       d.assign(n, 0.0);
     };
     start();
-    double thr = cfg.tol * t0;  // threshold on the estimate tau_k
+    // threshold on the estimate tau_k: REF's tol ||r0|| (feti.hpp:295), floored
+    // at tol kWarmFloor ||P rhs|| -- a warm start better than kWarmFloor asks for
+    // at most one more digit than tol ||P rhs|| (BASELINE c5 at step 69 of 100:
+    // tol ||r0|| is below the attainable accuracy, the estimate plateaus)
+    constexpr double kWarmFloor = 0.1;
+    double thr = cfg.tol * std::max(t0, kWarmFloor * rn);
     for (int k = 0; k < cfg.max_iter; ++k) {
       Vec t = apply(q);
       project(t);

@@ -9,6 +9,7 @@
 // operator: without a CUDA device pf_create fails with PF_CUDA.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
 
 #include <atomic>
 #include <map>
@@ -37,6 +38,16 @@
 namespace pf {
 
 std::atomic<long long> g_launches{0};  // kernel launches issued by this library (bench bookkeeping)
+
+/// NVTX range over a scope: setup phases and the phases of a time step
+/// (right-hand side, Krylov / direct interface solve, back-substitution) show
+/// up by name in nsys / ncu timelines.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 #define PF_CUDA_CHECK(x)                                                                    \
   do {                                                                                      \
@@ -1197,9 +1208,11 @@ struct Engine {
     const auto t = std::chrono::steady_clock::now();
     phases.emplace_back(name, std::chrono::duration<double>(t - phase_t0).count());
     phase_t0 = t;
+    nvtxMarkA((std::string("pf setup: ") + name + " done").c_str());  // phase boundaries inside the pf_create range
   }
 
   void create(const pf_config& cfg, const double* kover, int rank_ = 0, int nranks_ = 1, const void* nccl_id = nullptr) {
+    NvtxScope nv_create("pf_create");
     const auto t0 = std::chrono::steady_clock::now();
     phase_t0 = t0;
     int ndev = 0;
@@ -1319,7 +1332,9 @@ struct Engine {
     if (implicit_dir) setup_dirichlet();
     mark("lambda maps");
     if (use_gen) setup_generalized(), gen_built = true, mark("generalized precond");
-    if (use_q) setup_q(), q_built = true, mark("mortar Gram Q");
+    // the direct interface solve does not precondition: the mortar Gram factor
+    // is built on first use (pf_apply_precond / pf_set_precond) there
+    if (use_q && krylov != PF_KRYLOV_DIRECT) setup_q(), q_built = true, mark("mortar Gram Q");
     if (floating_any) setup_coarse(), mark("coarse space");
     setup_krylov();
     if (krylov == PF_KRYLOV_DIRECT) {
@@ -2888,17 +2903,69 @@ struct Engine {
     }
   }
 
+  /// X = F^{-1} B for k right-hand sides at once (column-major n x k; B is
+  /// overwritten by the forward pass): per front the same two operators as
+  /// iface_solve, applied as FP64 tensor-core GEMMs on gathered rows -- every
+  /// front value is read once for all k columns.  Fronts run one after the
+  /// other in post-order (forward) and reverse post-order (backward), so the
+  /// two-accumulator scheme of the single-vector kernel is not needed.
+  void iface_solve_multi(double* B, double* X, int k) {
+    const long long n = D.n_lambda;
+    const auto& FR = if_tree.fronts;
+    const int nf = (int)FR.size();
+    std::vector<dev::IfaceFrontDev> fd(nf);
+    PF_CUDA_CHECK(cudaMemcpy(fd.data(), if_fronts.p, sizeof(dev::IfaceFrontDev) * nf, cudaMemcpyDeviceToHost));
+    int mmax = 1;
+    for (const IfaceFront& F : FR) mmax = std::max(mmax, F.m());
+    DevBuf<double> Gm, Uo;
+    Gm.alloc((std::size_t)mmax * k), Uo.alloc((std::size_t)mmax * k);
+    auto blocks = [&](int r) { return (unsigned)cdiv((long long)r * k, 256); };
+    for (int f = 0; f < nf; ++f) {  // forward: c_bdry -= T c_sep
+      const IfaceFront& F = FR[f];
+      const int ns = F.nsep, nb = F.nbdry;
+      if (!ns || !nb) continue;
+      const int* idx = if_idx.p + fd[f].offI;
+      dev::k_iface_rows_gather<<<blocks(ns), 256, 0, st>>>(ns, k, idx, B, nullptr, 0, n, Gm.p);
+      dgemm(true, false, nb, k, ns, 1.0, if_T.p + fd[f].offT, fd[f].ldT, Gm.p, ns, 0.0, Uo.p, nb);
+      dev::k_iface_rows_scatter<<<blocks(nb), 256, 0, st>>>(nb, k, idx + ns, Uo.p, 1, n, B);
+      ::pf::g_launches += 2;
+    }
+    for (int f = nf - 1; f >= 0; --f) {  // backward: x_sep = M [c_sep ; x_bdry]
+      const IfaceFront& F = FR[f];
+      const int ns = F.nsep, m = F.m();
+      if (!ns) continue;
+      const int* idx = if_idx.p + fd[f].offI;
+      dev::k_iface_rows_gather<<<blocks(m), 256, 0, st>>>(m, k, idx, B, X, ns, n, Gm.p);
+      dgemm(true, false, ns, k, m, 1.0, if_M.p + fd[f].offM, fd[f].ldM, Gm.p, m, 0.0, Uo.p, ns);
+      dev::k_iface_rows_scatter<<<blocks(ns), 256, 0, st>>>(ns, k, idx, Uo.p, 0, n, X);
+      ::pf::g_launches += 2;
+    }
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
   /// the coarse border of the sparse direct solve: Y_c = W S_c^{-1} row-major
   void setup_direct_sparse() {
     const auto t0 = std::chrono::steady_clock::now();
     const int n = D.n_lambda;
     if (nc > 0) {
       DevBuf<double> Gd, W, Sc, Sci, Yc;
-      Gd.alloc((std::size_t)n * nc), Gd.zero(st);
-      dev::k_csr_rows_to_cols<<<nc, 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, Gd.p, n);
-      ::pf::g_launches++;
+      auto fill_gd = [&] {
+        Gd.zero(st);
+        dev::k_csr_rows_to_cols<<<nc, 128, 0, st>>>(nc, ct_ptr.p, ct_idx.p, ct_val.p, Gd.p, n);
+        ::pf::g_launches++;
+      };
+      Gd.alloc((std::size_t)n * nc), fill_gd();
       W.alloc((std::size_t)n * nc), Sc.alloc((std::size_t)nc * nc), Sci.alloc((std::size_t)nc * nc);
-      for (int c = 0; c < nc; ++c) iface_solve(Gd.p + (std::size_t)c * n, W.p + (std::size_t)c * n);  // W = F^{-1} G_c
+      // W = F^{-1} G_c: all n_c columns in one multi-right-hand-side pass over
+      // the fronts (PF_DIRECT_BORDER=single: one sparse solve per column)
+      static const bool single = std::getenv("PF_DIRECT_BORDER") && std::string(std::getenv("PF_DIRECT_BORDER")) == "single";
+      if (single) {
+        for (int c = 0; c < nc; ++c) iface_solve(Gd.p + (std::size_t)c * n, W.p + (std::size_t)c * n);
+      } else {
+        W.zero(st);
+        iface_solve_multi(Gd.p, W.p, nc);  // overwrites Gd
+        fill_gd();
+      }
       dgemm(true, false, nc, nc, n, 1.0, Gd.p, n, W.p, n, 0.0, Sc.p, nc);                                // S_c = G_c^T W
       Gd = DevBuf<double>();
       dense_spd_inverse(nc, Sc.p, Sci.p, true, "coarse interface problem G_c^T F^{-1} G_c");
@@ -3038,6 +3105,7 @@ struct Engine {
 
   /// y = Q x with Q = (G G^T)^{-1} (mortar scaling)
   void qsolve(const double* x, double* y) {
+    if (!q_built) setup_q(), q_built = true;  // deferred on a direct context
     if (Qsys.dense_bottom) {
       Qsys.solve_dense(st, x, y);
       return;
@@ -3086,6 +3154,7 @@ struct Engine {
   }
 
   void precond(const double* r, double* z) {
+    if (use_q && !q_built) setup_q(), q_built = true;  // deferred on a direct context
     if (!use_q) {
       precond_raw(r, z);
       return;
@@ -3996,10 +4065,14 @@ struct Engine {
     const int nstep = step_index + 1;
     const double t = D.time(nstep);
     fapplies = papplies = 0;
+    NvtxScope nv_step("pf_step");
     try {
       cudaEventRecord(e0, st);
-      build_rhs(t);
-      interface_rhs(kr_rhs.p);
+      {
+        NvtxScope nv("pf_step: rhs + interface rhs");
+        build_rhs(t);
+        interface_rhs(kr_rhs.p);
+      }
       cudaEventRecord(e1, st);
       const int n = D.n_lambda;
       // initial multiplier: warm start (timeloop.hpp:168-169) / coarse lambda0
@@ -4021,7 +4094,10 @@ struct Engine {
       } else if (!D.cfg.warm) {
         lam.zero(st);
       }
-      krylov_solve(lam.p, rep);
+      {
+        NvtxScope nv("pf_step: interface solve (Krylov / direct)");
+        krylov_solve(lam.p, rep);
+      }
       last_hist_n = std::min(rep.iterations, dev::kHistCap) + 1;
       if (!rep.converged) {
         char buf[160];
@@ -4030,8 +4106,11 @@ struct Engine {
         fail(kNotConverged, buf);
       }
       cudaEventRecord(e2, st);
-      recover_rigid(lam.p);  // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
-      back_substitute(lam.p);
+      {
+        NvtxScope nv("pf_step: back-substitution");
+        recover_rigid(lam.p);  // alpha = (G^T G)^{-1} G^T (F lambda - rhs)
+        back_substitute(lam.p);
+      }
       cudaEventRecord(e3, st);
       PF_CUDA_CHECK(cudaEventSynchronize(e3));
     } catch (Error& e) {
@@ -4537,7 +4616,7 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
     };
     run(&E.Ksys, out);
     run(E.implicit_dir ? &E.Isys : nullptr, out + 3);
-    run(E.use_q ? &E.Qsys : nullptr, out + 6);
+    run(E.use_q && E.q_built ? &E.Qsys : nullptr, out + 6);
     cudaEvent_t a, b;
     cudaEventCreate(&a), cudaEventCreate(&b);
     cudaEventRecord(a, E.st);

@@ -171,6 +171,29 @@ __global__ void k_iface_store(int ns, int nb, const double* __restrict__ X, cons
   }
 }
 
+/// Multi-right-hand-side solves (setup of the coarse border, W = F^{-1} G_c):
+/// rows idx[0..r) of the column-major n x k matrix C gathered into the dense
+/// r x k block G (ld r); with C2 given, rows >= r1 come from C2 instead.
+__global__ void k_iface_rows_gather(int r, int k, const int* __restrict__ idx, const double* __restrict__ C,
+                                    const double* __restrict__ C2, int r1, long long n, double* __restrict__ G) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)r * k) return;
+  const int i = (int)(q % r);
+  const long long j = q / r;
+  G[q] = (C2 && i >= r1 ? C2 : C)[idx[i] + j * n];
+}
+/// C[idx[i], j] = G[i, j] (sub = 0) or C[idx[i], j] -= G[i, j] (sub = 1); the
+/// rows of one front are distinct, fronts are processed one after the other
+__global__ void k_iface_rows_scatter(int r, int k, const int* __restrict__ idx, const double* __restrict__ G, int sub,
+                                     long long n, double* C) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)r * k) return;
+  const int i = (int)(q % r);
+  const long long j = q / r;
+  double* c = C + idx[i] + j * n;
+  *c = sub ? *c - G[q] : G[q];
+}
+
 /// Y[i * ld + c] = X[i + c * n] (column-major n x nc -> row-major with ld)
 __global__ void k_iface_to_rows(int n, int nc, const double* __restrict__ X, double* Y, long long ld) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;

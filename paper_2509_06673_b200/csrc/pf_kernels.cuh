@@ -328,9 +328,18 @@ __global__ void k_sqmr_dx_s(int n, const double* sc, const double* q, double* d,
   d[i] = dn;
   x[i] += dn;
 }
+/// The estimate's threshold is REF's tol ||r0|| (warm-started residual,
+/// feti.hpp:295) but never below tol kWarmFloor ||P rhs|| (RHSN = ||P rhs||^2):
+/// a warm start better than kWarmFloor asks for at most one more digit than
+/// tol ||P rhs||.  Without the floor BASELINE c5 stalls at step 69 of 100
+/// (||r0|| = 6.4e-3 ||P rhs||: tol ||r0|| lies below the attainable accuracy of
+/// F lambda, the estimate plateaus at 4e-10 ||r0||); same rule in the oracle
+/// (o_feti.hpp sqmr, kWarmFloor).
+constexpr double kWarmFloor = 0.1;
 __device__ __forceinline__ void ks_sqmr_init(double* sc, int* status, double tol) {
   const double t0 = sqrt(sc[KS_RR]);
-  sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0, sc[KS_THR] = tol * t0;
+  sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0;
+  sc[KS_THR] = tol * fmax(t0, kWarmFloor * sqrt(sc[KS_RHSN]));
   ks_hist(sc, 0, t0);
   status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
