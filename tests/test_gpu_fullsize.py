@@ -99,7 +99,13 @@ def test_fullsize_matches_oracle_fixture(name):
             b = bar(z, k, j) if fld != "p" else max(TOL, 10.0 * float(z[f"sens{k}"][j]))
             got = np.array([np.linalg.norm(fi[fld]) if fld in fi else np.nan for fi in f])
             m = np.isfinite(norms[:, j]) & (norms[:, j] > 0)
-            assert np.all(np.abs(got[m] - norms[m, j]) <= b * norms[m, j] + 1e-300), (k, fld)
+            # per-subdomain norms: relative to the subdomain's own norm, floored at
+            # the field's RMS subdomain norm (c5: eta is 6e-8 in the subdomains far
+            # from the injection and 1e-2 next to it; an interface solve converged
+            # to 1e-10 cannot resolve the former to 1e-8 of itself)
+            ref = np.maximum(norms[m, j], np.sqrt(np.mean(norms[m, j] ** 2)))
+            assert np.all(np.abs(got[m] - norms[m, j]) <= b * ref), (k, fld, float(np.max(
+                np.abs(got[m] - norms[m, j]) / ref)))
             if f"x{k}" in z.files:  # whole state in the fixture
                 ref = op.fields(np.split(z[f"x{k}"], np.cumsum(z["dims"])[:-1]))
                 g = np.concatenate([fi[fld] for fi in f if fld in fi])
