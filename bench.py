@@ -363,6 +363,7 @@ def run_ours(args, rank, world, dist):
     # F-applies/s from 200 back-to-back applies after 20 warm-up calls
     ms_apply, sweep_ms, launches = op.bench(0, 20, 200)
     ph = pf.phase_stats(op, 3)
+    step_sweep_ms = op.bench(8, 5, 50)[0]  # the K^+ b sweep as a step runs it (wide when set up)
     peak, peak_src = _peaks()
     sweep_bytes = 2.0 * 8.0 * info.nnz_L + 8.0 * info.total_dim  # per sweep (values + D), supernodal storage
     sweep_achieved = sweep_bytes / (sweep_ms * 1e-3) / 1e9
@@ -445,6 +446,10 @@ def run_ours(args, rank, world, dist):
                                      "back-substitution; the implicit F-apply with PF_FAPPLY=implicit)",
                            "work_equivalent_gbs": sweep_achieved, "work_equivalent_frac": sweep_achieved / peak,
                            "unit": "GB/s", "per_subdomain_factor_bytes": sweep_bytes, "ms": sweep_ms,
+                           "per_step_sweep_ms": step_sweep_ms, "per_step_sweep_width": info.sweep_width,
+                           "per_step_sweep": "k_sweep_w: groups of per_step_sweep_width same-type subdomains per warp "
+                                             "task, each factor value streamed once for the group (bitwise the "
+                                             "scalar sweep's results)" if info.sweep_width > 1 else "scalar k_sweep",
                            "stored_factor_bytes": info.bytes_factor_stored,
                            "stored_gbs": info.bytes_factor_stored / (sweep_ms * 1e-3) / 1e9,
                            "note": "same-type subdomains read one shared factor copy (L2); the per-subdomain "

@@ -104,6 +104,9 @@ typedef struct pf_info {
   double t_direct_setup; /* its setup (factorisation / inversion) in seconds */
   int direct_sparse;     /* 1: multifrontal factorisation over the subdomain grid (pf_iface.hpp) */
   int direct_fronts;     /* its fronts */
+  int sweep_width;       /* same-type subdomains per warp task of the per-step factor sweep (1: scalar sweep;
+                            2 / 4: wide sweep, each factor value applied to that many right-hand sides) */
+  int sweep_wide_problems; /* groups of sweep_width subdomains (padded) the wide sweep runs */
 } pf_info;
 
 typedef struct pf_sub_info {
@@ -220,6 +223,9 @@ void pf_host_free(void* p);
  * [Z | Y_c] GEMV, or F^{-1} through the fronts of the sparse variant), 7 the
  * sparse variant's whole interface solve (fronts + rigid-mode border Y_c). */
 int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms_per_op);
+/* tests: wide vs scalar per-step sweep on the current right-hand side; out = (differing entries, max |diff|)
+   per elimination-tree level; returns the level count (negative: status) */
+int pf_debug_wide_check(pf_ctx* ctx, double* out, int cap);
 /* nsteps device-resident StepSolver::advance calls bracketed by CUDA events. */
 int pf_bench_steps(pf_ctx* ctx, int nsteps, double* ms_total, int* iters_total, int* fapplies_total);
 /* number of kernels this library has launched (process-wide counter). */

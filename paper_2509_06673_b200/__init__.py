@@ -103,6 +103,7 @@ class Info(C.Structure):
         ("flops_backsub", C.c_double), ("bytes_backsub", C.c_double),
         ("bytes_direct", C.c_double), ("t_direct_setup", C.c_double),
         ("direct_sparse", C.c_int), ("direct_fronts", C.c_int),
+        ("sweep_width", C.c_int), ("sweep_wide_problems", C.c_int),
     ]
 
 
@@ -212,6 +213,7 @@ def lib():
         L.pf_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
         L.pf_host_free.argtypes = [vp]
         L.pf_bench_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
+        L.pf_debug_wide_check.argtypes = [vp, vp, C.c_int]
         L.pf_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.pf_phase_stats.argtypes = [vp, C.c_int, vp]
         L.pf_bench_steps.argtypes = [vp, C.c_int, vp, vp, vp]
@@ -482,6 +484,15 @@ class FetiOperator:
         it, fa = C.c_int(), C.c_int()
         _check(lib().pf_bench_steps(self.h, nsteps, C.byref(ms), C.byref(it), C.byref(fa)), self.h)
         return ms.value, it.value, fa.value
+
+    def wide_check(self):
+        """tests: wide vs scalar per-step sweep on the current right-hand side,
+        (differing entries, max |diff|) per elimination-tree level"""
+        out = np.zeros(2 * 64)
+        n = lib().pf_debug_wide_check(self.h, _ptr(out), 64)
+        if n < 0:
+            _check(-n, self.h)
+        return out[:2 * n].reshape(n, 2)
 
     def bench(self, kind=0, warmup=5, iters=20):
         ms = C.c_double()

@@ -196,6 +196,7 @@ struct SolveSystem {
   double db_bytes = 0.0;       // stored operator bytes (after sharing)
   double db_unit_bytes = 0.0;  // operator bytes one solve applies (before sharing)
   int nrhs_alloc = 1;
+  int width = 1;  // right-hand sides interleaved per problem (wide sweep, pf_sweep.cuh); set before build()
   long long nnzL = 0;
   int ws_max = 0;  // level-0 warp workspace
 
@@ -344,8 +345,8 @@ struct SolveSystem {
     d_meta.upload(meta), d_slots16.upload(slots16), d_tlbeg.upload(tlbeg), d_tlbytes.upload(tlbytes);
     L.alloc(total_L + 4);
     D.alloc(total_x + 2);  // the pivot unit of the last task may round up past the end
-    X.alloc(total_x * nrhs);
-    CB.alloc(std::max<long long>(1, total_cb * nrhs));
+    X.alloc(total_x * nrhs * width);
+    CB.alloc(std::max<long long>(1, total_cb * nrhs * width));
   }
 
   long long xidx(int p, int pos) const { return prob_x[p] + pos; }
@@ -461,7 +462,10 @@ struct SolveSystem {
   // shared memory of a level's launch (its own workspace and slot-list bounds)
   int lvl_ws(int l) const { return (level_ws[l] + 1) & ~1; }
   int sweep_smem(int l) const {
-    return dev::kSweepWarps * dev::SweepSmem::bytes(lvl_ws(l), level_smax[l]) + dev::kSweepPad;
+    const int b = width == 4   ? dev::SweepSmemW<4>::bytes(lvl_ws(l), level_smax[l])
+                  : width == 2 ? dev::SweepSmemW<2>::bytes(lvl_ws(l), level_smax[l])
+                               : dev::SweepSmem::bytes(lvl_ws(l), level_smax[l]);
+    return dev::kSweepWarps * b + dev::kSweepPad;
   }
   int sweep_smem() const {
     int m = 0;
@@ -475,10 +479,31 @@ struct SolveSystem {
         S, lvl_ws(l), level_smax[l]);
   }
 
+  template <int MODE, int V>
+  void launch_mode_w(cudaStream_t st, const dev::SolveSet& S, int l) {
+    dev::k_sweep_w<MODE, V><<<cdiv(S.nwork, dev::kSweepWarps), 32 * dev::kSweepWarps, sweep_smem(l), st>>>(
+        S, lvl_ws(l), level_smax[l]);
+  }
+  template <int V>
+  void launch_level_w(cudaStream_t st, const dev::SolveSet& S, int l, int mode) {
+    if (mode != 2 && level_folds[l]) {
+      dev::k_fold_level_w<V><<<cdiv(S.nwork, 8), 256, 0, st>>>(S);
+      ::pf::g_launches++;
+      ++launches;
+    }
+    if (mode == 0) launch_mode_w<0, V>(st, S, l);
+    else if (mode == 1) launch_mode_w<1, V>(st, S, l);
+    else launch_mode_w<2, V>(st, S, l);
+    ::pf::g_launches++;
+    ++launches;
+  }
+
   void launch_level(cudaStream_t st, int nrhs, int l, int mode) {
     if (level_nwork[l] == 0) return;
     if (nrhs != 1) fail(kInternal, "the sweep kernels take one right-hand side");
     dev::SolveSet S = set(nrhs, l);
+    if (width == 4) return launch_level_w<4>(st, S, l, mode);
+    if (width == 2) return launch_level_w<2>(st, S, l, mode);
     // fold children into the level's columns (forward) / gather the ancestor
     // values of its tasks (backward) so every task starts with contiguous loads
     if (mode != 2 && level_folds[l]) {
@@ -908,6 +933,12 @@ struct SolveSystem {
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
     PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
+    PF_CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep_w<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax_attr));
 
 
   }
@@ -1529,6 +1560,7 @@ struct Engine {
     }
     Ksys.prepare_smem();
     if (implicit_dir) Isys.prepare_smem();
+    setup_wide();
     mark("factor sharing");
     check_factor_residual();
     mark("seeded residual check");
@@ -3064,6 +3096,7 @@ struct Engine {
     info.bytes_factor_stored = 8.0 * (double)Ksys.total_L;
     info.flops_backsub = hb_on ? hb_flops : 0.0;
     info.bytes_backsub = hb_on ? hb_bytes : 0.0;
+    info.sweep_width = kw_on ? kw_V : 1, info.sweep_wide_problems = kw_on ? kw_nprob : 0;
     info.bytes_direct = 0.0, info.t_direct_setup = dn_setup_s, info.direct_sparse = if_on, info.direct_fronts = 0;
     if (if_on) {
       info.bytes_direct = 8.0 * ((double)if_values + (double)D.n_lambda * (double)if_ldc);
@@ -3506,7 +3539,7 @@ struct Engine {
       dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, hb_st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
                                                                    Ksys.d_prob_perm.p, Ksys.d_perm.p, bvec.p, Ksys.X.p, 1);
       if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, hb_st>>>(nfix, d_fixpos.p, Ksys.X.p);
-      Ksys.solve(hb_st, 1);
+      ksolve(hb_st);
       PF_CUDA_CHECK(cudaEventRecord(hb_ev1, hb_st));
       hb_pending = true;
       hb_valid = false;
@@ -3527,13 +3560,100 @@ struct Engine {
     }
     perm_in_K(bvec.p);
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
-    Ksys.solve(st, 1);
+    ksolve(st);
     if (hb_on) {  // K^+ b for the explicit back-substitution
       PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
       hb_valid = true;
     }
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, out, 1.0, 0, dvec.p);
     reduce(out, D.n_lambda);
+  }
+
+  // ------------------------------------------------------------------
+  // Wide per-step sweep (pf_sweep.cuh k_sweep_w): when every subdomain reads
+  // its type's (bitwise shared) factor copy, groups of V same-type subdomains
+  // become one "wide problem" whose tasks stream each factor value once for V
+  // interleaved right-hand sides.  The last group of a type is padded with
+  // zero members; V is the largest of {4, 2} whose padding stays under 30 %
+  // and that still leaves at least three groups per SM (PF_WIDE overrides).
+  // Results are bitwise those of the scalar sweep (same per-member arithmetic).
+  SolveSystem KW;
+  bool kw_on = false;
+  int kw_V = 0, kw_nprob = 0;
+  DevBuf<long long> kw_wx;  // per scalar problem: offset of its member slot in KW.X
+
+  void setup_wide() {
+    if (std::getenv("PF_NO_WIDE")) return;
+    const int np = nown();
+    if ((int)Ksys.prob_eq.size() != np || np < 2) return;
+    for (int p = 0; p < np; ++p)
+      if (!Ksys.prob_eq[p]) return;  // a subdomain with its own factor values: scalar sweep for all
+    const int nt = (int)ksym.size();
+    std::vector<std::vector<int>> mem(nt);
+    for (int p = 0; p < np; ++p) mem[Ksys.prob_type[p]].push_back(p);
+    auto padded = [&](int V) {
+      long long s = 0;
+      for (auto& m : mem) s += (long long)cdiv((long long)m.size(), V) * V;
+      return s;
+    };
+    int V = 0;
+    if (const char* e = std::getenv("PF_WIDE")) {
+      V = std::atoi(e);
+      if (V != 2 && V != 4) fail(kInvalid, "PF_WIDE: 2 or 4");
+    } else {
+      // measured (scripts/wide_sweep_timing.py): the sweep is bound by the
+      // dependency chain inside a task, so a wider task only pays while the
+      // groups still fill the machine -- c4 (1024 subdomains): scalar 3.42 ms,
+      // V = 2 (516 groups) 2.69 ms, V = 4 (264 groups) 2.86 ms; c3 (64
+      // subdomains, 36 groups): 2.82 -> 3.13 ms, kept scalar
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      for (int c : {4, 2})
+        if (!V && padded(c) * 10 <= 13LL * np && padded(c) / c >= 3LL * sms) V = c;
+    }
+    if (!V) return;
+    std::vector<int> vtype;
+    std::vector<long long> vl;
+    std::vector<std::pair<int, int>> slot(np);  // (wide problem, member)
+    for (int t = 0; t < nt; ++t)
+      for (std::size_t i = 0; i < mem[t].size(); ++i) {
+        if (i % V == 0) vtype.push_back(t), vl.push_back(Ksys.prob_lval[mem[t][0]]);
+        slot[mem[t][i]] = {(int)vtype.size() - 1, (int)(i % V)};
+      }
+    std::vector<const SymFactor*> kt;
+    for (auto& f : ksym) kt.push_back(&f);
+    KW.width = V;
+    KW.build(kt, vtype, 1, &vl);
+    KW.Lext = Ksys.L.p;
+    KW.prepare_smem();
+    for (std::size_t w = 0; w < vtype.size(); ++w)  // pivots of the type's factor copy
+      PF_CUDA_CHECK(cudaMemcpyAsync(KW.D.p + KW.prob_x[w], Ksys.D.p + Ksys.prob_x[mem[vtype[w]][0]],
+                                    sizeof(double) * ksym[vtype[w]].n, cudaMemcpyDeviceToDevice, st));
+    KW.X.zero(st), KW.CB.zero(st);  // padding members stay zero through every solve
+    std::vector<long long> wx(np);
+    for (int p = 0; p < np; ++p) wx[p] = KW.prob_x[slot[p].first] * V + slot[p].second;
+    kw_wx.upload(wx);
+    kw_V = V, kw_on = true;
+    kw_nprob = (int)vtype.size();
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr, "[pf] wide sweep: %d subdomains in %zu groups of %d (%.0f %% padding)\n", np, vtype.size(), V,
+                   100.0 * ((double)padded(V) / np - 1.0));
+  }
+
+  /// Ksys.X <- K^+ Ksys.X (permuted layout, in place) on stream s: the wide
+  /// sweep when it is set up, else the scalar batched sweep.
+  void ksolve(cudaStream_t s) {
+    if (!kw_on) return Ksys.solve(s, 1);
+    const int np = nown();
+    int maxn = 0;
+    for (auto& k : ksym) maxn = std::max(maxn, k.n);
+    const dim3 grid(cdiv(maxn, 256), np);
+    if (kw_V == 4) dev::k_wide_copy<4><<<grid, 256, 0, s>>>(np, Ksys.d_prob_x.p, kw_wx.p, Ksys.d_prob_n.p, Ksys.X.p, KW.X.p, 0);
+    else dev::k_wide_copy<2><<<grid, 256, 0, s>>>(np, Ksys.d_prob_x.p, kw_wx.p, Ksys.d_prob_n.p, Ksys.X.p, KW.X.p, 0);
+    KW.solve(s, 1);
+    if (kw_V == 4) dev::k_wide_copy<4><<<grid, 256, 0, s>>>(np, Ksys.d_prob_x.p, kw_wx.p, Ksys.d_prob_n.p, Ksys.X.p, KW.X.p, 1);
+    else dev::k_wide_copy<2><<<grid, 256, 0, s>>>(np, Ksys.d_prob_x.p, kw_wx.p, Ksys.d_prob_n.p, Ksys.X.p, KW.X.p, 1);
+    ::pf::g_launches += 2;
   }
 
   void perm_in_K(const double* src) {
@@ -3693,7 +3813,7 @@ struct Engine {
       } else if (!hb_valid) {  // no K^+ b for this right-hand side yet: one sweep
         perm_in_K(bvec.p);
         if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p), ::pf::g_launches++;
-        Ksys.solve(st, 1);
+        ksolve(st);
         PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
         hb_valid = true;
       }
@@ -3711,7 +3831,7 @@ struct Engine {
       dev::k_gather_ll<<<cdiv(g_back.nrows, 256), 256, 0, st>>>(g_back.nrows, g_back.rows.p, g_back.ptr.p,
                                                                g_back.idx.p, g_back.val.p, lambda, Ksys.X.p, -1.0, 1); ::pf::g_launches++;
     if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p); ::pf::g_launches++;
-    Ksys.solve(st, 1);
+    ksolve(st);
     perm_out_K(dst);
     if (nc && nfloat_local)
       dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
@@ -4458,6 +4578,7 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
         PF_CUDA_CHECK(cudaMemcpyAsync(dy.p, dx.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, E.st));
         E.direct_apply_sparse(dy.p);
       }
+      else if (kind == 8) E.ksolve(E.st);  // the per-step K^+ b sweep as a step runs it (wide when set up)
       else E.Ksys.solve(E.st, 1);
     };
     for (int i = 0; i < warmup; ++i) op();
@@ -4482,6 +4603,44 @@ int pf_bench_op(pf_ctx* ctx, int kind, int warmup, int iters, double* ms) {
     cudaEventDestroy(c), cudaEventDestroy(d);
     E.last_sweep_ms = t / iters;
   });
+}
+
+/// Debug (tests): the wide sweep against the scalar sweep on the current
+/// right-hand side b: per global level of the elimination tree the number of
+/// differing solution entries and the largest difference (out: 2 doubles per
+/// level, up to cap levels).  Returns the level count or a negative status.
+int pf_debug_wide_check(pf_ctx* ctx, double* out, int cap) {
+  if (!ctx || !out) return -PF_INVALID;
+  int nlev = 0;
+  const int rc = guarded(ctx, [&] {
+    auto& E = ctx->eng;
+    if (!E.kw_on) pf::fail(pf::kInvalid, "wide sweep not set up");
+    E.hb_fence();
+    const long long n = E.Ksys.total_x;
+    std::vector<double> a(n), b(n);
+    for (int pass = 0; pass < 2; ++pass) {
+      E.perm_in_K(E.bvec.p);
+      if (E.nfix) pf::dev::k_zero_idx<<<pf::cdiv(E.nfix, 128), 128, 0, E.st>>>(E.nfix, E.d_fixpos.p, E.Ksys.X.p);
+      if (pass == 0) E.Ksys.solve(E.st, 1);
+      else E.ksolve(E.st);
+      PF_CUDA_CHECK(cudaMemcpyAsync((pass ? b : a).data(), E.Ksys.X.p, sizeof(double) * n, cudaMemcpyDeviceToHost, E.st));
+      PF_CUDA_CHECK(cudaStreamSynchronize(E.st));
+    }
+    nlev = E.Ksys.nlevel;
+    std::vector<double> cnt(nlev, 0.0), mx(nlev, 0.0);
+    for (int p = 0; p < (int)E.Ksys.prob_type.size(); ++p) {
+      const pf::SymFactor& F = *E.Ksys.syms[E.Ksys.prob_type[p]];
+      for (int t = 0; t < F.ntask; ++t) {
+        const int gl = F.task_level[t] == F.nlevel - 1 ? nlev - 1 : F.task_level[t];
+        for (int c = F.task_c0[t]; c < F.task_c1[t]; ++c) {
+          const double d = std::fabs(a[E.Ksys.prob_x[p] + c] - b[E.Ksys.prob_x[p] + c]);
+          if (d > 0.0) cnt[gl] += 1.0, mx[gl] = std::max(mx[gl], d);
+        }
+      }
+    }
+    for (int l = 0; l < nlev && l < cap; ++l) out[2 * l] = cnt[l], out[2 * l + 1] = mx[l];
+  });
+  return rc == PF_OK ? nlev : -rc;
 }
 
 /// K time steps on the device-resident state bracketed by CUDA events on the

@@ -84,8 +84,14 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-constexpr int kCh = 4096;                 // bytes per bulk copy
-constexpr int kNs = 2;                    // chunks in the ring
+#ifndef PF_KCH
+#define PF_KCH 4096
+#endif
+#ifndef PF_KNS
+#define PF_KNS 2
+#endif
+constexpr int kCh = PF_KCH;               // bytes per bulk copy
+constexpr int kNs = PF_KNS;               // chunks in the ring
 constexpr int kRingB = kCh * kNs;         // ring bytes per warp
 constexpr int kHalfCols = 8;              // row blocks are consumed in halves of 8 columns
 constexpr int kMirror = kRB * kHalfCols * 8;  // largest piece consumed at once: mirrored behind the ring
@@ -499,6 +505,369 @@ __global__ void k_scatter_cols(int c0, int n, int cb_top, const int* __restrict_
   for (int q = fold_ptr[c0 + i]; q < fold_ptr[c0 + i + 1]; ++q) {
     const int f = fold_idx[q];
     if (f < cb_top) CB[f] = v;  // entries of the sparse levels only (top tasks never run)
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Wide sweep: V same-type subdomains per warp task (SURVEY §8f rank 2 carried
+// into the sweep).  When every member of a group of V subdomains reads the
+// same (bitwise shared) factor copy, the task streams its factor values ONCE
+// and applies each value to V right-hand sides: the L2 -> shared-memory
+// traffic of the sweep, its bound, drops by V.  Vectors are interleaved,
+// X[(xofs + pos) * V + v], CB[(cbofs + slot) * V + v]; the workspace holds V
+// doubles per slot; pivots D stay one per column.  Every member's arithmetic
+// is the scalar kernel's, operation for operation (same partial sums, same
+// order), so a wide sweep returns bitwise what V scalar sweeps return.
+// ---------------------------------------------------------------------------
+template <int V>
+struct SweepSmemW {
+  static constexpr int kWs = SweepSmem::kWs;
+  __host__ __device__ static int piv(int ws_max) { return kWs + 8 * V * ws_max; }
+  __host__ __device__ static int slots(int ws_max) { return piv(ws_max) + 8 * ws_max; }
+  __host__ __device__ static int bytes(int ws_max, int smax) { return slots(ws_max) + 2 * ((2 * smax + 15) & ~15); }
+};
+
+template <int V>
+__device__ __forceinline__ void ldv(int byte, double (&d)[V]) {
+  static_assert(V % 2 == 0, "wide sweep: even width");
+#pragma unroll
+  for (int k = 0; k < V; k += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(g_sm + byte + 8 * k);
+    d[k] = t.x, d[k + 1] = t.y;
+  }
+}
+template <int V>
+__device__ __forceinline__ void stv(int byte, const double (&d)[V]) {
+#pragma unroll
+  for (int k = 0; k < V; k += 2) *reinterpret_cast<double2*>(g_sm + byte + 8 * k) = make_double2(d[k], d[k + 1]);
+}
+
+template <int PWC, bool EXACT, int V>
+__device__ __forceinline__ void fwd_panel_w(StreamRing& R, int& pos, int slo, int p0, int pw, int m, int wso, int lane) {
+  const bool mine = lane < pw;
+  const int wp = wso + 8 * V * slot_at(slo, p0);
+  if (pw > 1) {
+    const int tb = 8 * tri_pad(pw);
+    const int T = R.need_fwd(pos, tb) + 8 * (lane * (lane - 1) / 2);
+    pos += tb;
+    double lrow[PWC - 1];
+#pragma unroll
+    for (int j = 0; j < PWC - 1; ++j) lrow[j] = (lane > j && mine) ? lds(T + 8 * j) : 0.0;
+    double a[4][V];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[q][v] = 0.0;
+    if (mine) ldv<V>(wp + 8 * V * lane, a[0]);
+#pragma unroll
+    for (int j = 0; j < PWC - 1; ++j) {
+      // operand selected first, then ONE fused multiply-add per member: the
+      // scalar kernel's rounding (a product formed in both branches and added
+      // afterwards would round twice)
+      double xj[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) xj[v] = 0.0;
+      if (EXACT || j < pw) ldv<V>(wp + 8 * V * j, xj);
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[j & 3][v] = fma(lrow[j], xj[v], a[j & 3][v]);
+    }
+    __syncwarp();
+    if (mine) {
+      double t[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) t[v] = (a[0][v] + a[1][v]) + (a[2][v] + a[3][v]);
+      stv<V>(wp + 8 * V * lane, t);
+    }
+    __syncwarp();
+  }
+  double xr[PWC][V];
+#pragma unroll
+  for (int j = 0; j < PWC; ++j) {
+    if (EXACT || j < pw) {
+      ldv<V>(wp + 8 * V * j, xr[j]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) xr[j][v] = 0.0;
+    }
+  }
+  const int nb = m - p0 - pw;
+  for (int b0 = 0; b0 < nb; b0 += kRB) {
+    const int nr = min(kRB, nb - b0);
+    const int ub = 8 * even_up(nr * pw);
+    const int st = 8 * nr;
+    const int ha = pw > kHalfCols ? kHalfCols * st : ub;
+    double a[4][V];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[q][v] = 0.0;
+    {
+      const int U = R.need_fwd(pos, ha) + 8 * lane;
+      if (lane < nr) {
+#pragma unroll
+        for (int j = 0; j < kHalfCols; ++j)
+          if (EXACT || j < pw) {
+            const double l = lds(U + st * j);
+#pragma unroll
+            for (int v = 0; v < V; ++v) a[j & 3][v] = fma(l, xr[j][v], a[j & 3][v]);
+          }
+      }
+    }
+    if (pw > kHalfCols) {
+      const int U = R.need_fwd(pos + ha, ub - ha) + 8 * lane;
+      if (lane < nr) {
+#pragma unroll
+        for (int j = kHalfCols; j < kPW; ++j)
+          if (EXACT || j < pw) {
+            const double l = lds(U + st * (j - kHalfCols));
+#pragma unroll
+            for (int v = 0; v < V; ++v) a[j & 3][v] = fma(l, xr[j][v], a[j & 3][v]);
+          }
+      }
+    }
+    pos += ub;
+    if (lane < nr) {
+      const int wsb = wso + 8 * V * slot_at(slo, p0 + pw + b0 + lane);
+      double t[V];
+      ldv<V>(wsb, t);
+#pragma unroll
+      for (int v = 0; v < V; ++v) t[v] -= (a[0][v] + a[1][v]) + (a[2][v] + a[3][v]);
+      stv<V>(wsb, t);
+    }
+  }
+}
+
+template <int PWC, bool EXACT, int V>
+__device__ __forceinline__ void bwd_panel_w(StreamRing& R, int& pos, int slo, int p0, int pw, int m, int wso, int lane) {
+  double acc[V][PWC];
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int j = 0; j < PWC; ++j) acc[v][j] = 0.0;
+  const int nb = m - p0 - pw;
+  if (nb > 0) {
+    for (int b0 = ((nb - 1) / kRB) * kRB; b0 >= 0; b0 -= kRB) {
+      const int nr = min(kRB, nb - b0);
+      const int ub = 8 * even_up(nr * pw);
+      const int st = 8 * nr;
+      const int ha = pw > kHalfCols ? kHalfCols * st : ub;
+      pos -= ub;
+      double xr[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) xr[v] = 0.0;
+      if (lane < nr) ldv<V>(wso + 8 * V * slot_at(slo, p0 + pw + b0 + lane), xr);
+      if (pw > kHalfCols) {
+        const int U = R.need_bwd(pos + ha, ub - ha) + 8 * lane;
+        if (lane < nr) {
+#pragma unroll
+          for (int j = kHalfCols; j < kPW; ++j)
+            if (EXACT || j < pw) {
+              const double l = lds(U + st * (j - kHalfCols));
+#pragma unroll
+              for (int v = 0; v < V; ++v) acc[v][j] = fma(l, xr[v], acc[v][j]);
+            }
+        }
+      }
+      {
+        const int U = R.need_bwd(pos, ha) + 8 * lane;
+        if (lane < nr) {
+#pragma unroll
+          for (int j = 0; j < kHalfCols; ++j)
+            if (EXACT || j < pw) {
+              const double l = lds(U + st * j);
+#pragma unroll
+              for (int v = 0; v < V; ++v) acc[v][j] = fma(l, xr[v], acc[v][j]);
+            }
+        }
+      }
+    }
+  }
+  double t[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) t[v] = transpose_reduce<PWC>(acc[v], lane);
+  const bool mine = lane < pw;
+  const int wp = wso + 8 * V * slot_at(slo, p0);
+  if (mine) {
+    double c[V];
+    ldv<V>(wp + 8 * V * lane, c);
+#pragma unroll
+    for (int v = 0; v < V; ++v) c[v] -= t[v];
+    stv<V>(wp + 8 * V * lane, c);
+  }
+  if (pw > 1) {
+    const int tb = 8 * tri_pad(pw);
+    pos -= tb;
+    const int T = R.need_bwd(pos, tb) + 8 * lane;
+    double lcol[PWC];
+#pragma unroll
+    for (int k = 1; k < PWC; ++k) lcol[k] = (k > lane && (EXACT || k < pw)) ? lds(T + 8 * (k * (k - 1) / 2)) : 0.0;
+    __syncwarp();
+    double a[4][V];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[q][v] = 0.0;
+    if (mine) ldv<V>(wp + 8 * V * lane, a[0]);
+#pragma unroll
+    for (int k = 1; k < PWC; ++k) {
+      double xk[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) xk[v] = 0.0;
+      if (EXACT || k < pw) ldv<V>(wp + 8 * V * k, xk);
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[k & 3][v] = fma(lcol[k], xk[v], a[k & 3][v]);
+    }
+    __syncwarp();
+    if (mine) {
+      double c[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) c[v] = (a[0][v] + a[1][v]) + (a[2][v] + a[3][v]);
+      stv<V>(wp + 8 * V * lane, c);
+    }
+  }
+  __syncwarp();
+}
+
+template <int V>
+__device__ __forceinline__ void fwd_sn_w(StreamRing& R, int& pos, int slo, int nc, int m, int wso, int lane) {
+  for (int p0 = 0; p0 < nc; p0 += kPW) {
+    const int pw = min(kPW, nc - p0);
+    if (pw == kPW) fwd_panel_w<kPW, true, V>(R, pos, slo, p0, pw, m, wso, lane);
+    else fwd_panel_w<kPW, false, V>(R, pos, slo, p0, pw, m, wso, lane);
+  }
+}
+template <int V>
+__device__ __forceinline__ void bwd_sn_w(StreamRing& R, int& pos, int slo, int nc, int m, int wso, int lane) {
+  for (int p0 = ((nc - 1) / kPW) * kPW; p0 >= 0; p0 -= kPW) {
+    const int pw = min(kPW, nc - p0);
+    if (pw == kPW) bwd_panel_w<kPW, true, V>(R, pos, slo, p0, pw, m, wso, lane);
+    else bwd_panel_w<kPW, false, V>(R, pos, slo, p0, pw, m, wso, lane);
+  }
+}
+
+/// k_sweep for V interleaved right-hand sides per task (MODE 0 / 1 / 2 as above)
+template <int MODE, int V>
+__global__ void __launch_bounds__(32 * kSweepWarps, 1) k_sweep_w(SolveSet S, int ws_max, int smax) {
+  using SM = SweepSmemW<V>;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kSweepWarps + wib;
+  if (w >= S.nwork) return;
+  const int wb = wib * SM::bytes(ws_max, smax);
+  const int wso = wb + SM::kWs;
+  const int pvo = wb + SM::piv(ws_max);
+  const int slb = wb + SM::slots(ws_max);
+  const int sls = (2 * smax + 15) & ~15;
+  const WorkRec wr = S.work[w];
+  const int c0 = wr.c0, nct = wr.nct, cbo = wr.cbo, cbl = wr.cbl, nsn = wr.nsn;
+  StreamRing R;
+  R.k.sbase = smem_u32(g_sm), R.k.wb = wb, R.k.lane = lane, R.r.phase = 0;
+  PF_PROF(R.r.tw = 0);
+  R.k.g = reinterpret_cast<const unsigned char*>(S.L + wr.lofs);
+  const int end = wr.lbytes;
+  R.k.end16 = (end + 15) & ~15, R.k.lastc = (R.k.end16 - 1) / kCh;
+  if (lane == 0) {
+    for (int i = 0; i < kNs; ++i) mbar_init(R.k.bar(i), 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (MODE != 2) R.start_fwd(); else R.start_bwd();
+  for (int i = lane; i < nsn; i += 32)
+    *reinterpret_cast<int2*>(g_sm + wb + SweepSmem::kMeta + 8 * i) = __ldg(S.sn_meta + wr.sn + i);
+  __syncwarp();
+  const uint16_t* table = S.slots + wr.slot_base;
+  double* X = S.X + wr.xofs * V;
+  double* CBp = S.CB + wr.cbofs * V;
+  const int nv = nct * V, cv = cbl * V;
+  if (MODE != 2) {
+    const double* Dp = S.D + wr.xofs + c0;
+    for (int i = lane; i < nv; i += 32) cp_async8(R.k.sbase + wso + 8 * i, X + (long long)c0 * V + i);
+    for (int i = lane; i < nct; i += 32) cp_async8(R.k.sbase + pvo + 8 * i, Dp + i);
+    prefetch_slots(table, meta_at(wb, 0), R.k.sbase + slb, lane);
+    cp_async_commit();
+    for (int i = lane; i < cv; i += 32) ws_at(wso, nv + i) = 0.0;
+    int pos = 0;
+    for (int k = 0; k < nsn; ++k) {
+      if (k + 1 < nsn) prefetch_slots(table, meta_at(wb, k + 1), R.k.sbase + slb + sls * ((k + 1) & 1), lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const int3 mt = meta_at(wb, k);
+      fwd_sn_w<V>(R, pos, slb + sls * (k & 1), mt.x, mt.y, wso, lane);
+      __syncwarp();
+    }
+    for (int i = lane; i < nv; i += 32) ws_at(wso, i) /= lds(pvo + 8 * (i / V));
+    if (MODE == 0)
+      for (int i = lane; i < cv; i += 32) CBp[(long long)cbo * V + i] = ws_at(wso, nv + i);
+    __syncwarp();
+  }
+  if (MODE == 1 || MODE == 2) {
+    if (MODE == 1) R.start_bwd();
+    if (MODE == 2) {
+      for (int i = lane; i < nv; i += 32) cp_async8(R.k.sbase + wso + 8 * i, X + (long long)c0 * V + i);
+      for (int i = lane; i < cv; i += 32) cp_async8(R.k.sbase + wso + 8 * (nv + i), CBp + (long long)cbo * V + i);
+    }
+    prefetch_slots(table, meta_at(wb, nsn - 1), R.k.sbase + slb, lane);
+    cp_async_commit();
+    int pos = end;
+    for (int k = nsn - 1, b = 0; k >= 0; --k, b ^= 1) {
+      if (k > 0) prefetch_slots(table, meta_at(wb, k - 1), R.k.sbase + slb + sls * (b ^ 1), lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const int3 mt = meta_at(wb, k);
+      bwd_sn_w<V>(R, pos, slb + sls * b, mt.x, mt.y, wso, lane);
+      __syncwarp();
+    }
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  for (int i = lane; i < nv; i += 32) X[(long long)c0 * V + i] = ws_at(wso, i);
+  if (MODE == 1 || MODE == 2) {
+    const int* fp = S.fold_ptr + wr.fold_base;
+    const int* fi = S.fold_idx + wr.foldidx_base;
+    for (int i = lane; i < nv; i += 32) {
+      const double v = ws_at(wso, i);
+      const int c = i / V, vv = i % V;
+      for (int q = fp[c0 + c]; q < fp[c0 + c + 1]; ++q) CBp[(long long)fi[q] * V + vv] = v;
+    }
+  }
+}
+
+/// k_fold_level for V interleaved right-hand sides
+template <int V>
+__global__ void k_fold_level_w(SolveSet S) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= S.nwork) return;
+  const WorkRec wr = S.work[w];
+  const int* fp = S.fold_ptr + wr.fold_base;
+  const int* fi = S.fold_idx + wr.foldidx_base;
+  const double* CBp = S.CB + wr.cbofs * V;
+  double* X = S.X + wr.xofs * V;
+  for (int i = lane; i < wr.nct * V; i += 32) {
+    const int c = i / V, vv = i % V;
+    const int q0 = fp[wr.c0 + c], q1 = fp[wr.c0 + c + 1];
+    if (q0 == q1) continue;
+    double v = X[(long long)wr.c0 * V + i];
+    for (int q = q0; q < q1; ++q) v += CBp[(long long)fi[q] * V + vv];
+    X[(long long)wr.c0 * V + i] = v;
+  }
+}
+
+/// scalar layout -> interleaved (dir 0) and back (dir 1): member p of the wide
+/// system holds scalar problem p's vector at Xw[wx[p] + pos * V]
+template <int V>
+__global__ void k_wide_copy(int nprob, const long long* __restrict__ prob_x, const long long* __restrict__ wx,
+                            const int* __restrict__ prob_n, double* Xs, double* Xw, int dir) {
+  const int p = blockIdx.y;
+  if (p >= nprob) return;
+  const int n = prob_n[p];
+  double* xs = Xs + prob_x[p];
+  double* xw = Xw + wx[p];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (dir) xs[i] = xw[(long long)i * V];
+    else xw[(long long)i * V] = xs[i];
   }
 }
 
