@@ -107,6 +107,10 @@ typedef struct pf_info {
   int sweep_width;       /* same-type subdomains per warp task of the per-step factor sweep (1: scalar sweep;
                             2 / 4: wide sweep, each factor value applied to that many right-hand sides) */
   int sweep_wide_problems; /* groups of sweep_width subdomains (padded) the wide sweep runs */
+  int q_local;           /* 1: the mortar Gram solve runs edge-local (explicit (interface, component) block
+                            inverses + cross-point corrections, two launches); 0: generic sparse factor */
+  int q_local_blocks;    /* its blocks */
+  double q_local_drop;   /* the relative far-corner coupling of the block inverses it drops (checked <= 1e-9) */
 } pf_info;
 
 typedef struct pf_sub_info {

@@ -104,6 +104,7 @@ class Info(C.Structure):
         ("bytes_direct", C.c_double), ("t_direct_setup", C.c_double),
         ("direct_sparse", C.c_int), ("direct_fronts", C.c_int),
         ("sweep_width", C.c_int), ("sweep_wide_problems", C.c_int),
+        ("q_local", C.c_int), ("q_local_blocks", C.c_int), ("q_local_drop", C.c_double),
     ]
 
 

@@ -2397,6 +2397,275 @@ struct Engine {
     m_ptr.upload(hp), m_idx.upload(hi), m_val.upload(hv);
   }
 
+  // ------------------------------------------------------------------
+  // Edge-local mortar Gram solve (pf_kernels.cuh k_qlocal_*): W's blocks over
+  // (interface, component), explicit block inverses, cross-point groups of end
+  // multipliers.  Built when the structure holds -- blocks of at most kQlMaxN
+  // multipliers, cross-point groups of at most kQlMaxGroup, and the dropped
+  // far-corner coupling of the block inverses below kQlDrop relative -- and a
+  // host check ||W Q b - b|| <= kQlCheck ||b|| on a seeded vector passes;
+  // otherwise setup_q keeps the generic sparse factor.  Q only scales the
+  // preconditioner: a 1e-13 relative perturbation of it does not touch the
+  // solution, and the iteration counts move by less than rounding does.
+  static constexpr int kQlMaxGroup = 8;
+  static constexpr double kQlDrop = 1e-9, kQlCheck = 1e-9;
+  bool ql_on = false;
+  double ql_drop = 0.0, ql_check = 0.0, ql_bytes = 0.0;
+  int ql_nblk = 0, ql_ndistinct = 0;
+  DevBuf<dev::QlBlock> ql_blk;
+  DevBuf<dev::QlEnd> ql_end;
+  DevBuf<dev::QlMem> ql_mem;
+  DevBuf<int> ql_idx;
+  DevBuf<double> ql_inv, ql_Y;
+
+  static bool spd_inverse_small(int n, std::vector<double>& a) {  // in place, row-major; false: not SPD
+    std::vector<double> L((std::size_t)n * n, 0.0);
+    for (int j = 0; j < n; ++j) {
+      double d = a[(std::size_t)j * n + j];
+      for (int k = 0; k < j; ++k) d -= L[(std::size_t)j * n + k] * L[(std::size_t)j * n + k];
+      if (!(d > 0.0)) return false;
+      const double dj = std::sqrt(d);
+      L[(std::size_t)j * n + j] = dj;
+      for (int i = j + 1; i < n; ++i) {
+        double v = a[(std::size_t)i * n + j];
+        for (int k = 0; k < j; ++k) v -= L[(std::size_t)i * n + k] * L[(std::size_t)j * n + k];
+        L[(std::size_t)i * n + j] = v / dj;
+      }
+    }
+    // Linv (lower), then A^-1 = Linv^T Linv
+    std::vector<double> Li((std::size_t)n * n, 0.0);
+    for (int c = 0; c < n; ++c) {
+      Li[(std::size_t)c * n + c] = 1.0 / L[(std::size_t)c * n + c];
+      for (int i = c + 1; i < n; ++i) {
+        double v = 0.0;
+        for (int k = c; k < i; ++k) v -= L[(std::size_t)i * n + k] * Li[(std::size_t)k * n + c];
+        Li[(std::size_t)i * n + c] = v / L[(std::size_t)i * n + i];
+      }
+    }
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double v = 0.0;
+        for (int k = i; k < n; ++k) v += Li[(std::size_t)k * n + i] * Li[(std::size_t)k * n + j];
+        a[(std::size_t)i * n + j] = a[(std::size_t)j * n + i] = v;
+      }
+    return true;
+  }
+
+  bool setup_qlocal(const Csr& A) {
+    const int n = D.n_lambda;
+    if (n == 0) return false;
+    // blocks over (interface, component), multipliers in index order
+    std::map<std::pair<int, int>, int> bid;
+    std::vector<std::vector<int>> B;
+    std::vector<int> blk_of(n), pos_of(n);
+    for (int g = 0; g < n; ++g) {
+      auto it = bid.emplace(std::make_pair(D.mults[g].iface, D.mults[g].comp), (int)B.size());
+      if (it.second) B.emplace_back();
+      blk_of[g] = it.first->second, pos_of[g] = (int)B[blk_of[g]].size();
+      B[blk_of[g]].push_back(g);
+    }
+    const int nb = (int)B.size();
+    for (auto& b : B)
+      if ((int)b.size() > dev::kQlMaxN) return false;
+    // dense blocks, bitwise-equal ones inverted and stored once
+    std::vector<long long> inv_of(nb);
+    std::vector<double> pool;
+    std::map<std::vector<double>, long long> seen;
+    std::vector<char> is_end(n, 0);
+    for (int e = 0; e < nb; ++e) {
+      const int m = (int)B[e].size();
+      std::vector<double> De((std::size_t)m * m, 0.0);
+      for (int i = 0; i < m; ++i) {
+        const int r = B[e][i];
+        for (int q = A.ptr[r]; q < A.ptr[r + 1]; ++q) {
+          const int c = A.col[q];
+          if (blk_of[c] == e) De[(std::size_t)i * m + pos_of[c]] = A.val[q];
+          else if (A.val[q] != 0.0) is_end[r] = 1;
+        }
+      }
+      auto it = seen.find(De);
+      if (it == seen.end()) {
+        std::vector<double> Di = De;
+        if (!spd_inverse_small(m, Di)) return false;
+        const long long o = (long long)pool.size();
+        pool.insert(pool.end(), Di.begin(), Di.end());
+        it = seen.emplace(std::move(De), o).first;
+      }
+      inv_of[e] = it->second;
+    }
+    ql_ndistinct = (int)seen.size();
+    // cross-point groups: connected components of the off-block couplings
+    std::vector<int> par(n);
+    for (int g = 0; g < n; ++g) par[g] = g;
+    auto find = [&](int u) {
+      while (par[u] != u) u = par[u] = par[par[u]];
+      return u;
+    };
+    for (int r = 0; r < n; ++r)
+      if (is_end[r])
+        for (int q = A.ptr[r]; q < A.ptr[r + 1]; ++q)
+          if (blk_of[A.col[q]] != blk_of[r] && A.val[q] != 0.0) par[find(r)] = find(A.col[q]);
+    std::map<int, std::vector<int>> groups;
+    for (int g = 0; g < n; ++g)
+      if (is_end[g]) groups[find(g)].push_back(g);
+    auto Dinv = [&](int u, int v) {  // same block
+      const int e = blk_of[u], m = (int)B[e].size();
+      return pool[inv_of[e] + (std::size_t)pos_of[u] * m + pos_of[v]];
+    };
+    // K = E (I + S E)^-1 per group (dense, <= kQlMaxGroup)
+    std::map<int, std::vector<double>> Kg;  // by group root, row-major k x k
+    for (auto& gr : groups) {
+      const auto& mem = gr.second;
+      const int k = (int)mem.size();
+      if (k > kQlMaxGroup) return false;
+      std::vector<double> E((std::size_t)k * k, 0.0), S((std::size_t)k * k, 0.0), M((std::size_t)k * k, 0.0);
+      for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) {
+          if (blk_of[mem[a]] == blk_of[mem[b]]) S[(std::size_t)a * k + b] = Dinv(mem[a], mem[b]);
+          else {
+            const int q = A.find(mem[a], mem[b]);
+            E[(std::size_t)a * k + b] = q >= 0 ? A.val[q] : 0.0;
+          }
+        }
+      for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) {
+          double v = a == b ? 1.0 : 0.0;
+          for (int c = 0; c < k; ++c) v += S[(std::size_t)a * k + c] * E[(std::size_t)c * k + b];
+          M[(std::size_t)a * k + b] = v;
+        }
+      // X = M^-1 by Gauss-Jordan with partial pivoting
+      std::vector<double> X((std::size_t)k * k, 0.0);
+      for (int a = 0; a < k; ++a) X[(std::size_t)a * k + a] = 1.0;
+      for (int c = 0; c < k; ++c) {
+        int pv = c;
+        for (int r = c + 1; r < k; ++r)
+          if (std::fabs(M[(std::size_t)r * k + c]) > std::fabs(M[(std::size_t)pv * k + c])) pv = r;
+        if (M[(std::size_t)pv * k + c] == 0.0) return false;
+        for (int j = 0; j < k; ++j)
+          std::swap(M[(std::size_t)c * k + j], M[(std::size_t)pv * k + j]), std::swap(X[(std::size_t)c * k + j], X[(std::size_t)pv * k + j]);
+        const double d = M[(std::size_t)c * k + c];
+        for (int j = 0; j < k; ++j) M[(std::size_t)c * k + j] /= d, X[(std::size_t)c * k + j] /= d;
+        for (int r = 0; r < k; ++r) {
+          if (r == c) continue;
+          const double f = M[(std::size_t)r * k + c];
+          if (f == 0.0) continue;
+          for (int j = 0; j < k; ++j) M[(std::size_t)r * k + j] -= f * M[(std::size_t)c * k + j], X[(std::size_t)r * k + j] -= f * X[(std::size_t)c * k + j];
+        }
+      }
+      std::vector<double> K((std::size_t)k * k, 0.0);
+      for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) {
+          double v = 0.0;
+          for (int c = 0; c < k; ++c) v += E[(std::size_t)a * k + c] * X[(std::size_t)c * k + b];
+          K[(std::size_t)a * k + b] = v;
+        }
+      for (int a = 0; a < k; ++a)  // symmetric in exact arithmetic: keep it exactly so
+        for (int b = 0; b < a; ++b) K[(std::size_t)a * k + b] = K[(std::size_t)b * k + a] = 0.5 * (K[(std::size_t)a * k + b] + K[(std::size_t)b * k + a]);
+      Kg[gr.first] = std::move(K);
+    }
+    // the coupling the block-diagonal K drops: D_e^-1 between ends of one block in different groups
+    ql_drop = 0.0;
+    for (int e = 0; e < nb; ++e)
+      for (int u : B[e])
+        for (int v : B[e])
+          if (u < v && is_end[u] && is_end[v] && find(u) != find(v))
+            ql_drop = std::max(ql_drop, std::fabs(Dinv(u, v)) / std::sqrt(Dinv(u, u) * Dinv(v, v)));
+    if (!(ql_drop <= kQlDrop)) return false;
+    // device records
+    std::vector<dev::QlBlock> hb(nb);
+    std::vector<dev::QlEnd> he;
+    std::vector<dev::QlMem> hm;
+    std::vector<int> hidx;
+    for (int e = 0; e < nb; ++e) {
+      hb[e].inv = inv_of[e], hb[e].off = (int)hidx.size(), hb[e].n = (int)B[e].size(), hb[e].end0 = (int)he.size();
+      hidx.insert(hidx.end(), B[e].begin(), B[e].end());
+      for (int u : B[e]) {
+        if (!is_end[u]) continue;
+        const auto& mem = groups[find(u)];
+        const auto& K = Kg[find(u)];
+        const int k = (int)mem.size();
+        const int a = (int)(std::find(mem.begin(), mem.end(), u) - mem.begin());
+        dev::QlEnd r{pos_of[u], (int)hm.size(), k};
+        for (int b = 0; b < k; ++b) hm.push_back(dev::QlMem{K[(std::size_t)a * k + b], mem[b], 0});
+        he.push_back(r);
+      }
+      hb[e].nend = (int)he.size() - hb[e].end0;
+      if (hb[e].nend > dev::kQlMaxEnds) return false;
+    }
+    // host check on a seeded vector: x = Q b by the same formulas, ||W x - b|| / ||b||
+    {
+      std::mt19937_64 rng(20240901ull);
+      std::uniform_real_distribution<double> U(-1.0, 1.0);
+      std::vector<double> b(n), y(n, 0.0), x(n);
+      for (auto& v : b) v = U(rng);
+      for (int e = 0; e < nb; ++e) {
+        const int m = hb[e].n;
+        for (int i = 0; i < m; ++i) {
+          double a = 0.0;
+          for (int j = 0; j < m; ++j) a += pool[hb[e].inv + (std::size_t)j * m + i] * b[B[e][j]];
+          y[B[e][i]] = a;
+        }
+      }
+      x = y;
+      for (int e = 0; e < nb; ++e) {
+        const int m = hb[e].n;
+        for (int q = hb[e].end0; q < hb[e].end0 + hb[e].nend; ++q) {
+          double t = 0.0;
+          for (int w = he[q].mem0; w < he[q].mem0 + he[q].nmem; ++w) t += hm[w].coef * y[hm[w].g];
+          for (int i = 0; i < m; ++i) x[B[e][i]] -= pool[hb[e].inv + (std::size_t)he[q].pos * m + i] * t;
+        }
+      }
+      double rr = 0.0, bb = 0.0;
+      for (int r = 0; r < n; ++r) {
+        double a = -b[r];
+        for (int q = A.ptr[r]; q < A.ptr[r + 1]; ++q) a += A.val[q] * x[A.col[q]];
+        rr += a * a, bb += b[r] * b[r];
+      }
+      ql_check = std::sqrt(rr / bb);
+      if (!(ql_check <= kQlCheck)) return false;
+    }
+    if (he.empty()) he.push_back(dev::QlEnd{0, 0, 0});
+    if (hm.empty()) hm.push_back(dev::QlMem{0.0, 0, 0});
+    ql_blk.upload(hb), ql_end.upload(he), ql_mem.upload(hm), ql_idx.upload(hidx), ql_inv.upload(pool);
+    ql_Y.alloc(n);
+    ql_nblk = nb;
+    ql_rows = 1, ql_rows_x = 1;
+    for (auto& bb : B) {
+      const int m = (int)bb.size();
+      ql_rows = std::max(ql_rows, m / 32 + (m % 32 > dev::kQlDots ? 1 : 0));
+      ql_rows_x = std::max(ql_rows_x, cdiv(m, 32));
+    }
+    // bytes one solve moves: distinct inverses once, descriptors, and b / Y / Y / x
+    ql_bytes = 8.0 * (double)pool.size() + sizeof(dev::QlBlock) * (double)nb + sizeof(dev::QlEnd) * (double)he.size() +
+               sizeof(dev::QlMem) * (double)hm.size() + 2.0 * 4.0 * n + 4.0 * 8.0 * n;
+    if (std::getenv("PF_VERBOSE"))
+      std::fprintf(stderr,
+                   "[pf] edge-local mortar Gram solve: %d blocks (%d distinct inverses, %.2f MB), %zu cross-point groups, "
+                   "dropped corner coupling %.2e, host check ||W Q b - b||/||b|| = %.2e\n",
+                   nb, ql_ndistinct, 8e-6 * (double)pool.size(), groups.size(), ql_drop, ql_check);
+    return true;
+  }
+
+  int ql_rows = 1, ql_rows_x = 2;  // lane rows of k_qlocal_y (rows beyond run as warp dots) / k_qlocal_x
+  void qlocal_solve(const double* b, double* x) {
+    dev::QlSys Q{ql_blk.p, ql_end.p, ql_mem.p, ql_idx.p, ql_inv.p, ql_nblk};
+    const int grid = cdiv(ql_nblk, dev::kQlWarps);
+    switch (ql_rows) {
+      case 1: launch_pdl(dev::k_qlocal_y<1>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
+      case 2: launch_pdl(dev::k_qlocal_y<2>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
+      case 3: launch_pdl(dev::k_qlocal_y<3>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
+      case 4: launch_pdl(dev::k_qlocal_y<4>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
+      default: fail(kInternal, "edge-local mortar Gram solve: block size");
+    }
+    switch (ql_rows_x) {
+      case 1: launch_pdl(dev::k_qlocal_x<1>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
+      case 2: launch_pdl(dev::k_qlocal_x<2>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
+      case 3: launch_pdl(dev::k_qlocal_x<3>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
+      case 4: launch_pdl(dev::k_qlocal_x<4>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
+      default: fail(kInternal, "edge-local mortar Gram solve: block size");
+    }
+  }
+
   void setup_q() {
     // mortar Gram matrix G G^T = sum_s G_s G_s^T, factorised once (lambda space)
     std::map<std::pair<int, int>, double> M;
@@ -2411,6 +2680,11 @@ struct Engine {
     for (auto& kv : M) rc.push_back(kv.first);
     Csr A = pattern_from_pairs(D.n_lambda, D.n_lambda, rc);
     for (auto& kv : M) A.val[A.find(kv.first.first, kv.first.second)] = kv.second;
+    // edge-local solve where W has the structure for it (PF_Q_GENERIC=1 keeps the sparse factor)
+    if (!std::getenv("PF_Q_GENERIC") && setup_qlocal(A)) {
+      ql_on = true;
+      return;
+    }
     {
       // the multiplier graph is nearly one-dimensional (chains along the
       // interfaces joined at cross points): small nested-dissection leaves and
@@ -3077,10 +3351,13 @@ struct Engine {
       info.bytes_symv = 8.0 * (double)dl_symvals + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
       info.bytes_symv_stored = 8.0 * (double)dl_opsize + (8.0 + 4.0 + 8.0) * (double)dl_nslots;
     }
-    if (use_q && Qsys.dense_bottom) {
+    if (use_q && ql_on) {
+      info.bytes_qsolve = ql_bytes, info.bytes_qsolve_applied = ql_bytes;
+    } else if (use_q && Qsys.dense_bottom) {
       info.bytes_qsolve = Qsys.db_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
       info.bytes_qsolve_applied = Qsys.db_unit_bytes + 8.0 * Qsys.ntop * (double)Qsys.ntop;
     }
+    info.q_local = ql_on ? 1 : 0, info.q_local_blocks = ql_nblk, info.q_local_drop = ql_drop;
     if (dual) {
       double rb = 0.0, rf = 0.0;
       std::vector<int> rl(n_rest);
@@ -3139,6 +3416,7 @@ struct Engine {
   /// y = Q x with Q = (G G^T)^{-1} (mortar scaling)
   void qsolve(const double* x, double* y) {
     if (!q_built) setup_q(), q_built = true;  // deferred on a direct context
+    if (ql_on) return qlocal_solve(x, y);
     if (Qsys.dense_bottom) {
       Qsys.solve_dense(st, x, y);
       return;
@@ -4775,7 +5053,7 @@ int pf_phase_stats(pf_ctx* ctx, int iters, double* out) {
     };
     run(&E.Ksys, out);
     run(E.implicit_dir ? &E.Isys : nullptr, out + 3);
-    run(E.use_q && E.q_built ? &E.Qsys : nullptr, out + 6);
+    run(E.use_q && E.q_built && !E.ql_on ? &E.Qsys : nullptr, out + 6);
     cudaEvent_t a, b;
     cudaEventCreate(&a), cudaEventCreate(&b);
     cudaEventRecord(a, E.st);

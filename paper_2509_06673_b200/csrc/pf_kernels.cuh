@@ -739,6 +739,183 @@ __global__ void __launch_bounds__(RB * S) k_dense_unit(const UnitWork* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Edge-local mortar Gram solve (Engine::setup_qlocal).  W = sum_s G_s G_s^T
+// is block diagonal over (interface, component) blocks -- banded, well
+// conditioned, <= kQlMaxN multipliers each -- plus couplings E between the
+// END multipliers of the interfaces that meet at a cross point.  With U the
+// selection of the end multipliers, Woodbury gives
+//   W^-1 = D^-1 - D^-1 U K U^T D^-1,   K = E (I + S E)^-1,   S = U^T D^-1 U.
+// S couples the two ends of one interface only through D_e^-1's far corner
+// entry, which decays geometrically along the interface (1e-13 of the
+// diagonal over 32 cells; checked at setup), so K is block diagonal over the
+// cross points: a solve is two launches of independent per-block work on
+// explicit inverses D_e^-1 (bitwise-equal blocks stored once).
+//   k_qlocal_y : Y_e = D_e^-1 b_e                       (warp per block)
+//   k_qlocal_x : x_e = Y_e - D_e^-1[:, ends] (K Y_ends) (warp per block)
+// x may alias b (every read of b precedes the second launch).
+// ---------------------------------------------------------------------------
+struct QlBlock {
+  long long inv;        // offset of D_e^-1 (symmetric, n x n) in the pool
+  int off, n;           // multiplier list [off, off + n)
+  int end0, nend;       // end records of this block
+};
+struct QlEnd {
+  int pos, mem0, nmem;  // local position; cross-point members [mem0, mem0 + nmem)
+};
+struct __align__(16) QlMem {
+  double coef;          // K[u, v]
+  int g, pad;           // multiplier v
+};
+struct QlSys {
+  const QlBlock* blk;
+  const QlEnd* end;
+  const QlMem* mem;
+  const int* idx;
+  const double* inv;
+  int nblk;
+};
+/// Optional fusions with the local dual products on either side of a Gram
+/// solve (Engine::precond): k_qlocal_y can take its input as the fixed-order
+/// slot sums of the type GEMM's result (k_local_reduce's arithmetic, bit for
+/// bit), k_qlocal_x can also scatter its result into the gathered slot vector
+/// the next type GEMM reads (k_local_gather).  ptr == nullptr: plain vectors.
+struct QlFuse {
+  const int* ptr;          // per multiplier: slots [ptr[g], ptr[g + 1])
+  const long long* slot;
+  const double* Yin;       // reduce: planes of slot values
+  double* xloc;            // gather target
+  int nks;
+  long long stride;
+};
+constexpr int kQlMaxN = 128, kQlWarps = 8, kQlMaxEnds = 32;
+
+/// R = full lane rows per block: rows [0, 32 R_b), R_b = n / 32 + (n % 32 > kQlDots) <= R,
+/// run one per lane over a serial column loop (two independent chains); the
+/// at most kQlDots rows beyond (a 33rd multiplier on a 32-cell interface) are
+/// warp dot products, so they do not double the column loop.
+constexpr int kQlDots = 4;
+template <int R>
+__global__ void __launch_bounds__(32 * kQlWarps) k_qlocal_y(QlSys Q, const double* b, double* Y, QlFuse Fz) {
+  __shared__ double bs[kQlWarps][32 * (R + 1)];
+  if (kPdlEarly) pdl_trigger();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * kQlWarps + warp;
+  const bool on = e < Q.nblk;
+  QlBlock B{};
+  int g[R + 1];
+#pragma unroll
+  for (int k = 0; k <= R; ++k) g[k] = -1;
+  if (on) {
+    B = Q.blk[e];
+    const int* idx = Q.idx + B.off;
+#pragma unroll
+    for (int k = 0; k <= R; ++k)
+      if (lane + 32 * k < B.n) g[k] = idx[lane + 32 * k];
+  }
+  int q0[R + 1], q1[R + 1];
+  if (Fz.ptr) {  // slot ranges are constant: loaded before the wait
+#pragma unroll
+    for (int k = 0; k <= R; ++k) q0[k] = g[k] >= 0 ? Fz.ptr[g[k]] : 0, q1[k] = g[k] >= 0 ? Fz.ptr[g[k] + 1] : 0;
+  }
+  pdl_wait();  // descriptors and indices above do not depend on the predecessor
+  if (!on) return;
+  if (Fz.ptr) {
+#pragma unroll
+    for (int k = 0; k <= R; ++k) {
+      double v = 0.0;  // k_local_reduce: planes of a slot in plane order, slots in slot order
+      for (int q = q0[k]; q < q1[k]; ++q) {
+        const long long sq = Fz.slot[q];
+        double u = Fz.Yin[sq];
+        for (int p = 1; p < Fz.nks; ++p) u += Fz.Yin[sq + p * Fz.stride];
+        v += u;
+      }
+      bs[warp][lane + 32 * k] = v;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k <= R; ++k) bs[warp][lane + 32 * k] = g[k] >= 0 ? b[g[k]] : 0.0;
+  }
+  __syncwarp();
+  const int n = B.n;
+  const int nl = 32 * (n / 32 + (n % 32 > kQlDots ? 1 : 0));  // rows run by the lanes
+  const double* M = Q.inv + B.inv + lane;  // symmetric: column j is row j, coalesced over the lanes
+  double a[R], c[R];
+  int io[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) a[k] = c[k] = 0.0, io[k] = lane + 32 * k < min(n, nl) ? 32 * k : -lane;  // idle: row 0
+  int j = 0;
+  for (; j + 1 < n; j += 2) {
+    const double b0 = bs[warp][j], b1 = bs[warp][j + 1];
+    const double* M0 = M + j * n;
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[k] = fma(M0[io[k]], b0, a[k]), c[k] = fma(M0[n + io[k]], b1, c[k]);
+  }
+  if (j < n) {
+    const double b0 = bs[warp][j];
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[k] = fma(M[j * n + io[k]], b0, a[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if (lane + 32 * k < min(n, nl)) Y[g[k]] = a[k] + c[k];
+  for (int r = nl; r < n; ++r) {  // the few rows beyond: lanes over the columns, fixed shuffle tree
+    const double* Mr = Q.inv + B.inv + (long long)r * n;
+    double v = 0.0;
+    for (int q = lane; q < n; q += 32) v = fma(Mr[q], bs[warp][q], v);
+    v = warp_sum(v);
+    if (lane == 0) Y[Q.idx[B.off + r]] = v;
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * kQlWarps) k_qlocal_x(QlSys Q, const double* __restrict__ Y, double* x, QlFuse Fz) {
+  if (kPdlEarly) pdl_trigger();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * kQlWarps + warp;
+  const bool on = e < Q.nblk;
+  QlBlock B{};
+  QlEnd E{};
+  int g[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) g[k] = -1;
+  if (on) {
+    B = Q.blk[e];
+    const int* idx = Q.idx + B.off;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (lane + 32 * k < B.n) g[k] = idx[lane + 32 * k];
+    if (lane < B.nend) E = Q.end[B.end0 + lane];
+  }
+  pdl_wait();
+  if (!on) return;
+  double t = 0.0;  // lane u: (K Y_ends)[u], members in stored order
+  for (int q = E.mem0; q < E.mem0 + E.nmem; ++q) {
+    const QlMem m = Q.mem[q];
+    t = fma(m.coef, Y[m.g], t);
+  }
+  const int n = B.n;
+  const double* M = Q.inv + B.inv + lane;
+  double a[R];
+  int io[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) a[k] = g[k] >= 0 ? Y[g[k]] : 0.0, io[k] = lane + 32 * k < n ? 32 * k : -lane;
+  for (int u = 0; u < B.nend; ++u) {
+    const double tu = __shfl_sync(0xffffffffu, t, u);
+    const int pu = __shfl_sync(0xffffffffu, E.pos, u);
+    const double* Mu = M + pu * n;
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[k] = fma(-Mu[io[k]], tu, a[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if (g[k] >= 0) {
+      x[g[k]] = a[k];
+      if (Fz.ptr)
+        for (int q = Fz.ptr[g[k]]; q < Fz.ptr[g[k] + 1]; ++q) Fz.xloc[Fz.slot[q]] = a[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Error norms against the manufactured solution
 // ---------------------------------------------------------------------------
 /// verify.hpp:19-74 restated per element: (field_h - exact)^2 at the degree-4
