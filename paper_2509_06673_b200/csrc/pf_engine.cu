@@ -2647,21 +2647,27 @@ struct Engine {
   }
 
   int ql_rows = 1, ql_rows_x = 2;  // lane rows of k_qlocal_y (rows beyond run as warp dots) / k_qlocal_x
-  void qlocal_solve(const double* b, double* x) {
+  /// x = Q b.  fuse_in: b is not read -- the input is the fixed-order slot sum
+  /// of the type GEMM's result dl_Y (k_local_reduce fused); fuse_out: the
+  /// result also goes to the gathered slot vector dl_xloc (k_local_gather fused).
+  void qlocal_solve(const double* b, double* x, bool fuse_in = false, bool fuse_out = false) {
     dev::QlSys Q{ql_blk.p, ql_end.p, ql_mem.p, ql_idx.p, ql_inv.p, ql_nblk};
+    dev::QlFuse none{nullptr, nullptr, nullptr, nullptr, 0, 0};
+    dev::QlFuse fz{dl_rptr.p, dl_rslot.p, dl_Y.p, dl_xloc.p, dl_nks, (long long)dl_nslots};
+    const dev::QlFuse fi = fuse_in ? fz : none, fo = fuse_out ? fz : none;
     const int grid = cdiv(ql_nblk, dev::kQlWarps);
     switch (ql_rows) {
-      case 1: launch_pdl(dev::k_qlocal_y<1>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
-      case 2: launch_pdl(dev::k_qlocal_y<2>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
-      case 3: launch_pdl(dev::k_qlocal_y<3>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
-      case 4: launch_pdl(dev::k_qlocal_y<4>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p); break;
+      case 1: launch_pdl(dev::k_qlocal_y<1>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p, fi); break;
+      case 2: launch_pdl(dev::k_qlocal_y<2>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p, fi); break;
+      case 3: launch_pdl(dev::k_qlocal_y<3>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p, fi); break;
+      case 4: launch_pdl(dev::k_qlocal_y<4>, grid, 32 * dev::kQlWarps, 0, st, Q, b, ql_Y.p, fi); break;
       default: fail(kInternal, "edge-local mortar Gram solve: block size");
     }
     switch (ql_rows_x) {
-      case 1: launch_pdl(dev::k_qlocal_x<1>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
-      case 2: launch_pdl(dev::k_qlocal_x<2>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
-      case 3: launch_pdl(dev::k_qlocal_x<3>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
-      case 4: launch_pdl(dev::k_qlocal_x<4>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x); break;
+      case 1: launch_pdl(dev::k_qlocal_x<1>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x, fo); break;
+      case 2: launch_pdl(dev::k_qlocal_x<2>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x, fo); break;
+      case 3: launch_pdl(dev::k_qlocal_x<3>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x, fo); break;
+      case 4: launch_pdl(dev::k_qlocal_x<4>, grid, 32 * dev::kQlWarps, 0, st, Q, (const double*)ql_Y.p, x, fo); break;
       default: fail(kInternal, "edge-local mortar Gram solve: block size");
     }
   }
@@ -3468,6 +3474,21 @@ struct Engine {
     if (use_q && !q_built) setup_q(), q_built = true;  // deferred on a direct context
     if (!use_q) {
       precond_raw(r, z);
+      return;
+    }
+    // edge-local Q around the explicit Dirichlet operators on one rank: the
+    // gather into the type GEMM's slot vector rides on the first solve's output
+    // and the slot reduction on the second solve's input (two launches and two
+    // passes over the multipliers less; same arithmetic, bit for bit)
+    static const bool no_fuse = std::getenv("PF_Q_NOFUSE") != nullptr;
+    if (ql_on && q_built && dual && use_dir && !use_gen && sh_nwork && !reducer && nranks == 1 && !no_fuse) {
+      qlocal_solve(r, kr_tmp.p, false, true);
+      launch_pdl(dev::k_type_gemm, sh_nwork, dev::kGThreads, 0, st, sh_work.p, sh_S.p, sh_cols.p, dl_xloc.p, dl_Y.p,
+                 dl_nslots);
+      if (n_rest)
+        launch_pdl(dev::k_local_symv, n_rest, 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p, dl_S.p,
+                   dl_lam.p, kr_tmp.p, dl_Y.p, rest_list.p);
+      qlocal_solve(nullptr, z, true, false);
       return;
     }
     qsolve(r, kr_tmp.p);
