@@ -487,6 +487,8 @@ def run_ours(args, rank, world, dist):
                            "work_equivalent_gbs": sweep_achieved, "work_equivalent_frac": sweep_achieved / peak,
                            "unit": "GB/s", "per_subdomain_factor_bytes": sweep_bytes, "ms": sweep_ms,
                            "per_step_sweep_ms": step_sweep_ms, "per_step_sweep_width": info.sweep_width,
+                           "per_step_work_equivalent_gbs": sweep_bytes / (step_sweep_ms * 1e-3) / 1e9,
+                           "per_step_work_equivalent_frac": sweep_bytes / (step_sweep_ms * 1e-3) / 1e9 / peak,
                            "per_step_sweep": "k_sweep_w: groups of per_step_sweep_width same-type subdomains per warp "
                                              "task, each factor value streamed once for the group (bitwise the "
                                              "scalar sweep's results)" if info.sweep_width > 1 else "scalar k_sweep",

@@ -321,7 +321,10 @@ struct __align__(16) GemmWork {
   short ch0, ch1;   // K-slice: 16-chunks [ch0, ch1); partial written to plane `plane`
   int plane, lda;
 };
-constexpr int kGM = 32, kGN = 32, kGK = 16, kGThreads = 64, kGStages = 4, kGLd = 20;
+#ifndef PF_GSTAGES
+#define PF_GSTAGES 4
+#endif
+constexpr int kGM = 32, kGN = 32, kGK = 16, kGThreads = 64, kGStages = PF_GSTAGES, kGLd = 20;
 
 __device__ __forceinline__ void cp_async16_zfill(unsigned dst, const void* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");

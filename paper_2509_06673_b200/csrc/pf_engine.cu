@@ -3413,10 +3413,10 @@ struct Engine {
     if (g_lam2X.nrows)
       dev::k_gather_ll<<<cdiv(g_lam2X.nrows, 256), 256, 0, st>>>(g_lam2X.nrows, g_lam2X.rows.p, g_lam2X.ptr.p,
                                                                 g_lam2X.idx.p, g_lam2X.val.p, x, Ksys.X.p, 1.0, 0); ::pf::g_launches++;
-    Ksys.solve(st, 1);
+    ksolve(st);  // the wide sweep when it is set up
     spmv2(s_ptr, s_mid, s_idx, s_val, Ksys.X.p, y, 1.0, 0);
     reduce(y, D.n_lambda);
-    launches_per_apply = Ksys.launches + 3;
+    launches_per_apply = (kw_on ? KW.launches + 2 : Ksys.launches) + 3;
   }
 
   /// y = Q x with Q = (G G^T)^{-1} (mortar scaling)
