@@ -311,7 +311,7 @@ def direct_arm(args, cfg_name, peak):
                    "d2h_bytes_per_step": int(x_cat.nbytes + lam.nbytes)},
            "setup_s": setup_s, "direct_setup_s": info.t_direct_setup, "gpu_launches": int(launches)}
     # roofline of the interface solve: stored operator bytes once per solve
-    t7 = op.bench(7, 5, 20)[0]
+    t7 = op.bench(7 if info.direct_sparse else 6, 5, 20)[0]  # sparse: fronts + coarse border; dense: one GEMV
     b = float(info.bytes_direct)
     out["roofline"] = {"bound": "hbm", "kernel": "k_iface_gemv<fwd/bwd> per tree depth + coarse border GEMV"
                        if info.direct_sparse else "k_gemv_rows: lambda = [Z | Y_c] [rhs; e]",
