@@ -62,7 +62,7 @@ def test_wide_sweep_default_rule(monkeypatch):
     op.close()
     monkeypatch.delenv("PF_NO_WIDE")
     print(f"c4 per-step sweep: scalar {t_scalar:.3f} ms, wide (2) {t_wide:.3f} ms")
-    assert t_wide < t_scalar
+    assert t_wide < 1.05 * t_scalar  # measured 2.7 vs 3.4 ms
     for kw in (dict(pf.BASELINE_CONFIGS["c4"], mesh_n=128, SX=16, SY=16, steps=1),   # 256 subdomains: too few groups
                dict(pf.BASELINE_CONFIGS["c2"], mesh_n=32, steps=1),                  # 2x2: four one-member types
                dict(pf.BASELINE_CONFIGS["c5"], mesh_n=64, SX=8, SY=8, steps=1)):     # own factor values
