@@ -42,6 +42,19 @@ def test_wide_sweep_bitwise_equals_scalar(name, krylov, width, monkeypatch):
         assert np.array_equal(xa, xb)
 
 
+@pytest.mark.parametrize("width", [2, 4])
+def test_wide_sweep_per_level_check(width, monkeypatch):
+    """pf_debug_wide_check: the wide and the scalar sweep on the current
+    right-hand side differ in no entry of any elimination-tree level."""
+    monkeypatch.delenv("PF_NO_WIDE", raising=False)
+    monkeypatch.setenv("PF_WIDE", str(width))
+    op = pf.FetiOperator(**dict(pf.BASELINE_CONFIGS["c3"], mesh_n=64, SX=8, SY=8, steps=2))
+    op.step()
+    lv = op.wide_check()
+    assert lv.shape[0] >= 2 and np.all(lv == 0.0), lv
+    op.close()
+
+
 def test_wide_sweep_default_rule(monkeypatch):
     """The width rule: the largest of {4, 2} whose zero padding stays under
     30 % and that leaves at least three groups per SM (the sweep is bound by
