@@ -474,6 +474,16 @@ class Feti {
     // tol ||r0|| is below the attainable accuracy, the estimate plateaus)
     constexpr double kWarmFloor = 0.1;
     double thr = cfg.tol * std::max(t0, kWarmFloor * rn);
+    // stagnation rule: every kStagWindow iterations since the last (re)start the
+    // estimate must have lost the factor kStagRatio against its value one window
+    // earlier, else the Lanczos process has stagnated (BASELINE c5, step 60 of
+    // 100: 1.7e-8 -> 1.3e-8 ||r0|| over 2000 iterations; converging c3 / c5 runs
+    // lose at least 0.48 per window) and restarts from the true residual
+    constexpr int kStagWindow = 128;
+    const char* sr_env = std::getenv("PF_STAG_RATIO");  // tests: force restarts (engine reads the same variable)
+    const double kStagRatio = sr_env ? std::atof(sr_env) : 0.9;
+    double est_ck = t0;
+    int it0 = 0;
     for (int k = 0; k < cfg.max_iter; ++k) {
       Vec t = apply(q);
       project(t);
@@ -505,6 +515,21 @@ class Feti {
         }
         ++rep.restarts;
         thr = est * (cfg.tol * rn / tr) * 0.5;
+      } else if ((k + 1 - it0) % kStagWindow == 0) {
+        if (est > kStagRatio * est_ck) {
+          if (k + 1 >= cfg.max_iter) break;
+          tau = true_residual(rhs, lambda, &r);  // r = P(rhs - F lambda)
+          ++rep.restarts;
+          if (!(tau > 0.0)) {
+            rep.converged = true;
+            rep.rel_residual = 0.0;
+            return;
+          }
+          est_ck = tau, it0 = k + 1;
+          start();
+          continue;
+        }
+        est_ck = est;
       }
       if (rho == 0.0) throw PcgBreakdownError("sqmr: rho vanished");
       Vec u = precondition(r);

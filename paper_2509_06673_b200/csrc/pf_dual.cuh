@@ -206,22 +206,29 @@ __global__ void k_pack_sym(int nsub, const int* __restrict__ nloc, const long lo
 }
 
 /// Y[loff_s + i] = sum_j Op_s[i][j] x[lam[loff_s + j]] with Op_s symmetric,
-/// packed (above).  One CTA per subdomain; x_s gathered straight from the
-/// multiplier vector into shared memory; warp w takes tiles w, w+8, ... and
-/// accumulates row sums (T x_J into y_I) and, off the diagonal, column sums
-/// (T^T x_I into y_J) into its own shared y buffer in tile order; the buffers
-/// are summed in warp order.  Every summation order is fixed (deterministic).
+/// packed (above).  nsplit CTAs per subdomain; x_s gathered straight from the
+/// multiplier vector into shared memory; warp w of CTA h takes tiles
+/// w + 8 (h + nsplit m), m = 0, 1, ... and accumulates row sums (T x_J into y_I)
+/// and, off the diagonal, column sums (T^T x_I into y_J) into its own shared y
+/// buffer in tile order; the buffers are summed in warp order and CTA h writes
+/// its partial result into plane h of Y (the planes are summed in plane order
+/// by the consumer, like the K-slices of the type GEMM).  Every summation
+/// order is fixed (deterministic).  A subdomain's operator is streamed by
+/// nsplit SMs at once: with one CTA per subdomain (BASELINE c5: 130 unshared
+/// subdomains of 0.65 MB each) the launch reached 3.3 TB/s.
 __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restrict__ nloc,
                                                     const long long* __restrict__ loff,
                                                     const long long* __restrict__ opoff,
                                                     const double* __restrict__ Op, const int* __restrict__ lam,
                                                     const double* __restrict__ x, double* __restrict__ Y,
-                                                    const int* __restrict__ list) {
+                                                    const int* __restrict__ list, int nsplit,
+                                                    long long plane_stride) {
   if (kPdlEarly) pdl_trigger();
   pdl_wait();
   extern __shared__ double sm[];
-  if ((int)blockIdx.x >= nsub) return;
-  const int s = list ? list[blockIdx.x] : blockIdx.x;
+  const int sb = blockIdx.x / nsplit, h = blockIdx.x % nsplit;
+  if (sb >= nsub) return;
+  const int s = list ? list[sb] : sb;
   const int n = nloc[s], nt = (n + kSymT - 1) / kSymT, np = nt * kSymT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* xs = sm;            // np
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restr
   double* my = yb + warp * np;
   const int ntile = nt * (nt + 1) / 2;
   int I = 0, J = 0, k = 0;
-  for (int t = warp; t < ntile; t += nw) {
+  for (int t = warp + nw * h; t < ntile; t += nw * nsplit) {
     while (k < t) {  // advance (I, J) to tile t
       if (++J > I) ++I, J = 0;
       ++k;
@@ -258,10 +265,11 @@ __global__ void __launch_bounds__(256) k_local_symv(int nsub, const int* __restr
     __syncwarp();
   }
   __syncthreads();
+  double* Yh = Y + h * plane_stride;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nw; ++w) v += yb[w * np + i];
-    Y[lo + i] = v;
+    Yh[lo + i] = v;
   }
 }
 

@@ -1257,6 +1257,11 @@ struct Engine {
       if (std::getenv("PF_NO_PRIO")) hi = lo;  // A/B: both streams at the default priority
       if (std::getenv("PF_HB_HI")) std::swap(lo, hi);  // A/B: the sweep first
       PF_CUDA_CHECK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+      {  // SQMR stagnation ratio on the selected device (PF_STAG_RATIO: tests force restarts)
+        const char* e = std::getenv("PF_STAG_RATIO");
+        const double v = e ? std::atof(e) : dev::kStagRatio;
+        PF_CUDA_CHECK(cudaMemcpyToSymbol(dev::g_stag_ratio, &v, sizeof(double)));
+      }
       PF_CUDA_CHECK(cudaStreamCreateWithPriority(&hb_st, cudaStreamNonBlocking, lo));
       PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev0, cudaEventDisableTiming));
       PF_CUDA_CHECK(cudaEventCreateWithFlags(&hb_ev1, cudaEventDisableTiming));
@@ -2091,6 +2096,15 @@ struct Engine {
   }
 
   /// local products Y_s = Op_s x_s of every owned subdomain (sd: Dirichlet Sd_s, else F_s)
+  /// CTAs per unshared subdomain of k_local_symv (at most the planes the slot
+  /// reduction sums, dl_nks).  Measured at c5 (130 unshared subdomains,
+  /// scripts/symv_ab.sh): local products 24.2 us with one CTA per subdomain,
+  /// 20.5 us with two, 23.4 us with three; two while they fit one wave.
+  int symv_split() const {
+    static const int forced = std::getenv("PF_SYMV_SPLIT") ? std::atoi(std::getenv("PF_SYMV_SPLIT")) : 0;
+    if (forced > 0) return std::min(forced, dl_nks);
+    return (n_rest > 0 && 2 * n_rest <= 4 * 148) ? std::min(2, dl_nks) : 1;
+  }
   void dual_local(bool sd, const double* x) {
     if (sh_nwork) {
       launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, x, dl_xloc.p);
@@ -2098,8 +2112,8 @@ struct Engine {
                  dl_xloc.p, dl_Y.p, dl_nslots);
     }
     if (n_rest) {
-      launch_pdl(dev::k_local_symv, n_rest, 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p,
-                 sd ? dl_S.p : dl_F.p, dl_lam.p, x, dl_Y.p, rest_list.p);
+      launch_pdl(dev::k_local_symv, n_rest * symv_split(), 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p,
+                 sd ? dl_S.p : dl_F.p, dl_lam.p, x, dl_Y.p, rest_list.p, symv_split(), (long long)dl_nslots);
     }
   }
 
@@ -3486,8 +3500,8 @@ struct Engine {
       launch_pdl(dev::k_type_gemm, sh_nwork, dev::kGThreads, 0, st, sh_work.p, sh_S.p, sh_cols.p, dl_xloc.p, dl_Y.p,
                  dl_nslots);
       if (n_rest)
-        launch_pdl(dev::k_local_symv, n_rest, 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p, dl_opoff.p, dl_S.p,
-                   dl_lam.p, kr_tmp.p, dl_Y.p, rest_list.p);
+        launch_pdl(dev::k_local_symv, n_rest * symv_split(), 256, dl_smem, st, n_rest, dl_nloc.p, dl_loff.p,
+                   dl_opoff.p, dl_S.p, dl_lam.p, kr_tmp.p, dl_Y.p, rest_list.p, symv_split(), (long long)dl_nslots);
       qlocal_solve(nullptr, z, true, false);
       return;
     }
@@ -4293,18 +4307,37 @@ struct Engine {
           status();
         }
       }
-      if (h_status[0] != dev::KST_CONV && h_status[0] != dev::KST_RUN) breakdown(h_status[0]);
+      if (h_status[0] != dev::KST_CONV && h_status[0] != dev::KST_RUN && h_status[0] != dev::KST_STAG)
+        breakdown(h_status[0]);
     };
-    M_(r, q);
-    dot(n, r, q, dev::KS_RHO);
-    kr_d.zero(st);
-    iter(true);
-    loop();
+    // (re)start of the Lanczos recurrences from the residual in r
+    auto start = [&] {
+      M_(r, q);
+      dot(n, r, q, dev::KS_RHO);
+      kr_d.zero(st);
+      iter(true);
+      loop();
+    };
+    start();
     // The quasi-residual tau_k only estimates ||r_k|| (||r_k|| <= sqrt(k+1) tau_k):
     // convergence is confirmed on the true residual P(rhs - F lambda); above
     // tol * ||r0|| the same recurrences continue with a tightened threshold
     for (;;) {
       rep.iterations = h_status[1];
+      if (h_status[0] == dev::KST_STAG && h_status[1] < maxit) {
+        // stagnated Lanczos process (kStagWindow / kStagRatio, the oracle's rule):
+        // restart from the true residual of the current iterate
+        F_(lambda, r);
+        dev::k_axpby<<<nb, 256, 0, st>>>(n, 1.0, kr_rhs.p, -1.0, r); ::pf::g_launches++;
+        project(r);
+        dot(n, r, r, dev::KS_RR);
+        dev::k_ks_sqmr_restart<<<1, 1, 0, st>>>(sc, stat); ::pf::g_launches++;
+        ++rep.restarts;
+        if (status() == dev::KST_RUN) {
+          start();
+          continue;
+        }
+      }
       if (h_status[0] != dev::KST_CONV) {
         rep.rel_residual = rel_residual();
         break;

@@ -284,9 +284,21 @@ __global__ void k_sqmr_dx(int n, const double* sc, const double* q, double* d, d
 // ---------------------------------------------------------------------------
 enum : int {
   KS_RHO = 32, KS_SIGMA, KS_A, KS_RR, KS_THETA, KS_THOLD, KS_C, KS_TAU, KS_T0, KS_RHON, KS_B, KS_REL,
-  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR, KS_RHSN
+  KS_RZ, KS_PKP, KS_PP, KS_RZN, KS_D0, KS_TR0, KS_TRUE, KS_THR, KS_RHSN, KS_CK, KS_IT0
 };
-enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5 };
+enum : int { KST_RUN = 0, KST_CONV = 1, KST_SIGMA = 2, KST_RHO = 3, KST_PKP = 4, KST_RZ = 5, KST_STAG = 6 };
+/// SQMR stagnation rule (same constants in the oracle, o_feti.hpp sqmr): every
+/// kStagWindow iterations since the last (re)start the estimate is compared
+/// with its value one window earlier; a decrease by less than the factor
+/// kStagRatio is a stagnated Lanczos process (BASELINE c5, step 60 of 100:
+/// the estimate creeps from 1.7e-8 to 1.3e-8 ||r0|| over 2000 iterations;
+/// converging runs of c3 / c5 lose at least a factor 0.48 per 128 iterations)
+/// and the recurrences are restarted from the true residual of the iterate.
+constexpr int kStagWindow = 128;
+constexpr double kStagRatio = 0.9;
+/// tests only (PF_STAG_RATIO, read by engine and oracle alike): a smaller ratio
+/// forces restarts so that the restart mechanics are exercised in lockstep
+__device__ double g_stag_ratio = kStagRatio;
 /// residual history (REF PcgReport::residual_history, feti.hpp:65): entry k at
 /// sc[KS_HIST0 + k], k = 0 .. kHistCap (absolute: sqrt(r.z) for PCG, the
 /// quasi-residual tau_k for SQMR), written by the single-thread scalar updates
@@ -340,6 +352,7 @@ __device__ __forceinline__ void ks_sqmr_init(double* sc, int* status, double tol
   const double t0 = sqrt(sc[KS_RR]);
   sc[KS_T0] = t0, sc[KS_TAU] = t0, sc[KS_THETA] = 0.0, sc[KS_REL] = 1.0;
   sc[KS_THR] = tol * fmax(t0, kWarmFloor * sqrt(sc[KS_RHSN]));
+  sc[KS_CK] = t0, sc[KS_IT0] = 0.0;
   ks_hist(sc, 0, t0);
   status[0] = (t0 == 0.0 || !(t0 > 0.0)) ? KST_CONV : KST_RUN, status[1] = 0;
   if (status[0] == KST_CONV) sc[KS_REL] = 0.0;
@@ -370,7 +383,21 @@ __device__ __forceinline__ void ks_sqmr_tau(double* sc, int* status, double tol)
   ks_hist(sc, status[1], tau);
   // quasi-residual tau_k below the threshold (tol ||r0||, tightened after a
   // failed true-residual check): candidate convergence, confirmed by the host
-  if (status[0] == KST_RUN && tau <= sc[KS_THR]) status[0] = KST_CONV;
+  if (status[0] != KST_RUN) return;
+  if (tau <= sc[KS_THR]) {
+    status[0] = KST_CONV;
+  } else if ((status[1] - (int)sc[KS_IT0]) % kStagWindow == 0) {
+    if (tau > g_stag_ratio * sc[KS_CK]) status[0] = KST_STAG;  // the host restarts (k_ks_sqmr_restart)
+    else sc[KS_CK] = tau;
+  }
+}
+/// restart after a stagnation: RR = ||r||^2 of the recomputed true residual
+/// r = P(rhs - F lambda); threshold, reference, history and the iteration
+/// count carry on
+__global__ void k_ks_sqmr_restart(double* sc, int* status) {
+  const double t = sqrt(sc[KS_RR]);
+  sc[KS_TAU] = t, sc[KS_THETA] = 0.0, sc[KS_CK] = t, sc[KS_IT0] = (double)status[1];
+  status[0] = (t == 0.0 || !(t > 0.0)) ? KST_CONV : KST_RUN;
 }
 __device__ __forceinline__ void ks_sqmr_b(double* sc, int* status) {
   if (sc[KS_RHO] == 0.0 && status[0] == KST_RUN) status[0] = KST_RHO;
