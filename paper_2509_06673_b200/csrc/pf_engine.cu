@@ -2105,9 +2105,12 @@ struct Engine {
     if (forced > 0) return std::min(forced, dl_nks);
     return (n_rest > 0 && 2 * n_rest <= 4 * 148) ? std::min(2, dl_nks) : 1;
   }
+  bool dl_xloc_ready = false;  // the caller's producer kernel already gathered x into dl_xloc (one use)
   void dual_local(bool sd, const double* x) {
     if (sh_nwork) {
-      launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, x, dl_xloc.p);
+      if (!dl_xloc_ready)
+        launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, x, dl_xloc.p);
+      dl_xloc_ready = false;
       launch_pdl(dev::k_type_gemm, sh_nwork, dev::kGThreads, 0, st, sh_work.p, sd ? sh_S.p : sh_F.p, sh_cols.p,
                  dl_xloc.p, dl_Y.p, dl_nslots);
     }
@@ -3521,7 +3524,8 @@ struct Engine {
       if (dup == 2) dual_local(true, kr_tmp.p);                       // one more local product (gather+GEMM)
       if (dup == 3) coarse_gemv(r, kr_dup.p);                          // one more dense coarse GEMV
       if (dup == 4) launch_pdl(dev::k_xpay_s, cdiv(D.n_lambda, 256), 256, 0, st, D.n_lambda, (const double*)r,
-                               kr_dup.p, (const double*)(scal.p + dev::KS_B));  // one more tiny vector kernel
+                               kr_dup.p, (const double*)(scal.p + dev::KS_B), (const int*)nullptr,
+                               (const long long*)nullptr, (double*)nullptr);  // one more tiny vector kernel
       if (dup == 5) fdot(dev::DOT_PLAIN, r, kr_tmp.p, 60, dev::SOP_NONE);  // one more fused dot (scratch slot)
     }
   }
@@ -4241,7 +4245,9 @@ struct Engine {
       PF_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       // iteration = [p = z + beta p (not in the first)] F p, alpha, lambda, r, M r, beta
       auto iter = [&](bool first) {
-        if (!first) launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, z, p, sc + dev::KS_B);
+        if (!first)
+          launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, z, p, sc + dev::KS_B, (const int*)nullptr,
+                     (const long long*)nullptr, (double*)nullptr);
         F_(p, q);
         fdot(dev::DOT_PLAIN, p, p, dev::KS_PP, dev::SOP_NONE);
         fdot(dev::DOT_PLAIN, p, q, dev::KS_PKP, dev::SOP_PCG_ALPHA);
@@ -4285,7 +4291,12 @@ struct Engine {
     auto iter = [&](bool first) {
       if (!first) {
         M_dot(r, u, r, dev::KS_RHON, dev::SOP_SQMR_B);                                  // u = P M r, rho
-        launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, u, q, sc + dev::KS_B);  // q = u + b q
+        // q = u + b q; on one rank with type-shared operators the gather of q into
+        // the local products' slot vector rides along (dual_local skips its own)
+        const bool fuse_g = dual && sh_nwork && !reducer && nranks == 1 && !std::getenv("PF_Q_NOFUSE");
+        launch_pdl(dev::k_xpay_s, nb, 256, 0, st, n, (const double*)u, q, (const double*)(sc + dev::KS_B),
+                   fuse_g ? (const int*)dl_rptr.p : (const int*)nullptr, (const long long*)dl_rslot.p, dl_xloc.p);
+        dl_xloc_ready = fuse_g;
       }
       F_(q, t);
       if (nc) coarse_solve(t, c_tmp2.p);

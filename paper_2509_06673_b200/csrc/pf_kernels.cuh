@@ -315,13 +315,20 @@ __global__ void k_axpy_s(int n, const double* coef, double sgn, const double* x,
   const double c = sgn * *coef;
   if (i < n) y[i] += c * x[i];
 }
-/// y = x + (*coef) * y
-__global__ void k_xpay_s(int n, const double* x, double* y, const double* coef) {
+/// y = x + (*coef) * y; with a slot map (ptr, slot) the new y_i is also
+/// scattered into the gathered slot vector xloc of the local dual products
+/// (k_local_gather fused: the F-apply that follows reads xloc directly)
+__global__ void k_xpay_s(int n, const double* x, double* y, const double* coef, const int* __restrict__ ptr,
+                         const long long* __restrict__ slot, double* __restrict__ xloc) {
   if (kPdlEarly) pdl_trigger();
-  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q0 = ptr && i < n ? ptr[i] : 0, q1 = ptr && i < n ? ptr[i + 1] : 0;  // constant map: before the wait
+  pdl_wait();
   const double c = *coef;
-  if (i < n) y[i] = x[i] + c * y[i];
+  if (i >= n) return;
+  const double v = x[i] + c * y[i];
+  y[i] = v;
+  for (int q = q0; q < q1; ++q) xloc[slot[q]] = v;
 }
 /// SQMR: d = c^2 theta_old^2 d + c^2 a q; x += d
 /// With set_cond, block 0 also sets the device-side loop's WHILE condition
