@@ -3000,18 +3000,43 @@ struct Engine {
   /// side; the coarse constraint value e = G_c^T lambda_in, the coarse part of
   /// lambda0), one GEMV; the true residual ||P(rhs - F lambda)|| / ||P rhs|| is
   /// reported (one F-apply).
-  void direct_solve(double* lambda, pf_report& rep) {
+  /// one application of the stored interface factorisation: lambda (in: carrier of
+  /// the coarse constraint value e = G_c^T lambda_in) <- solution for kr_rhs
+  void direct_once(double* lambda) {
     const int n = D.n_lambda;
-    if (if_on) {
-      direct_apply_sparse(lambda);
-      return direct_report(lambda, rep);
-    }
+    if (if_on) return direct_apply_sparse(lambda);
     PF_CUDA_CHECK(cudaMemcpyAsync(dn_x.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     if (nc > 0)
       launch_pdl(dev::k_spmv_warp, cdiv(nc, 8), 256, 0, st, nc, ct_ptr.p, ct_idx.p, ct_val.p, (const double*)lambda,
                  dn_x.p + n, 1.0, 0.0);
     direct_gemv(lambda);
+  }
+
+  /// Direct solve + iterative refinement.  The factorisation's rounding shows in
+  /// the residual where the interface operator is ill-conditioned (BASELINE c3,
+  /// nu = 0.49999: 5.9e-12, a forward error of 1.4e-8 in lambda against SQMR
+  /// converged to 7e-14); while the true residual is above kDirectRefineTol the
+  /// correction delta = F^-1 P(rhs - F lambda) (homogeneous coarse constraint)
+  /// is added, at most kDirectRefineMax times.  c4 and c5 (3e-13) take none.
+  static constexpr double kDirectRefineTol = 1e-12;
+  static constexpr int kDirectRefineMax = 2;
+  void direct_solve(double* lambda, pf_report& rep) {
+    const int n = D.n_lambda;
+    direct_once(lambda);
     direct_report(lambda, rep);
+    for (int it = 0; it < kDirectRefineMax && rep.true_residual > kDirectRefineTol; ++it) {
+      const double before = rep.true_residual;
+      // kr_t holds r = P(rhs - F lambda) (direct_report); solve for it with e = 0
+      PF_CUDA_CHECK(cudaMemcpyAsync(kr_p.p, kr_rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      PF_CUDA_CHECK(cudaMemcpyAsync(kr_rhs.p, kr_t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      kr_d.zero(st);
+      direct_once(kr_d.p);
+      dev::k_axpby<<<cdiv(n, 256), 256, 0, st>>>(n, 1.0, kr_d.p, 1.0, lambda); ::pf::g_launches++;
+      PF_CUDA_CHECK(cudaMemcpyAsync(kr_rhs.p, kr_p.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      direct_report(lambda, rep);
+      ++rep.restarts;  // refinement steps taken
+      if (!(rep.true_residual < 0.5 * before)) break;
+    }
   }
 
   void direct_report(double* lambda, pf_report& rep) {
@@ -3851,16 +3876,18 @@ struct Engine {
       for (auto& k : ksym) maxn = std::max(maxn, k.n);
       // K^+ b for the back-substitution on the low-priority stream, overlapped
       // with the Krylov loop (back_substitute waits for it)
-      PF_CUDA_CHECK(cudaEventRecord(hb_ev0, st));
-      PF_CUDA_CHECK(cudaStreamWaitEvent(hb_st, hb_ev0, 0));
-      dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, hb_st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
-                                                                   Ksys.d_prob_perm.p, Ksys.d_perm.p, bvec.p, Ksys.X.p, 1);
-      if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, hb_st>>>(nfix, d_fixpos.p, Ksys.X.p);
-      ksolve(hb_st);
-      PF_CUDA_CHECK(cudaEventRecord(hb_ev1, hb_st));
-      hb_pending = true;
+      if (!hb_use_sweep) {
+        PF_CUDA_CHECK(cudaEventRecord(hb_ev0, st));
+        PF_CUDA_CHECK(cudaStreamWaitEvent(hb_st, hb_ev0, 0));
+        dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, hb_st>>>(np, Ksys.d_prob_x.p, d_subvec(), Ksys.d_prob_n.p,
+                                                                     Ksys.d_prob_perm.p, Ksys.d_perm.p, bvec.p, Ksys.X.p, 1);
+        if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, hb_st>>>(nfix, d_fixpos.p, Ksys.X.p);
+        ksolve(hb_st);
+        PF_CUDA_CHECK(cudaEventRecord(hb_ev1, hb_st));
+        hb_pending = true;
+        ::pf::g_launches += 1 + (nfix ? 1 : 0);
+      }
       hb_valid = false;
-      ::pf::g_launches += 1 + (nfix ? 1 : 0);
       // F = sum_s H_t^T b_s - d on the engine stream (H_t's rows at fixing dofs are zero)
       const int n = D.n_lambda;
       dev::k_perm_in<<<dim3(cdiv(maxn, 256), np), 256, 0, st>>>(np, hb_bpo.p, d_subvec(), Ksys.d_prob_n.p,
@@ -4118,9 +4145,23 @@ struct Engine {
   bool hb_valid = false;  // hb_Yb holds K^+ b of the current right-hand side
 
   /// x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s -> dst (default: the state)
+  /// The explicit form x = K^+ b - H lambda applies H_t = K_t^+ G_t^T column by
+  /// column: every column carries the rounding of its own solve, and the sum
+  /// over a subdomain's multipliers can cancel heavily (BASELINE c3, nu =
+  /// 0.49999: u came out 7e-9 off the sweep form K^+ (b - G^T lambda), which
+  /// the oracle's local solves agree with to 4e-10; no such loss at c4 / c5).
+  /// Like the reference's seeded factorisation check (feti.hpp:28-36) the first
+  /// back-substitution is therefore done in BOTH forms: if they differ by more
+  /// than kHbDevMax (relative, over the whole state) the engine keeps the sweep
+  /// form for good and the interface right-hand side no longer starts the
+  /// overlapped K^+ b sweep; the first step returns the form that is kept.
+  /// PF_HB_DEV overrides the threshold.
+  static constexpr double kHbDevMax = 1e-9;
+  bool hb_checked = false, hb_use_sweep = false;
+  double hb_dev = 0.0;
   void back_substitute(const double* lambda, double* dst = nullptr) {
     if (!dst) dst = state.p;
-    if (hb_on) {
+    if (hb_on && !hb_use_sweep) {
       const double* yb = hb_Yb.p;
       if (hb_pending) {  // K^+ b from the overlapped sweep, in place in Ksys.X
         PF_CUDA_CHECK(cudaStreamWaitEvent(st, hb_ev1, 0));
@@ -4134,9 +4175,47 @@ struct Engine {
         PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
         hb_valid = true;
       }
+      const bool check = !hb_checked && Ksys.total_x < INT32_MAX;
       launch_pdl(dev::k_local_gather, cdiv(dl_nslots, 256), 256, 0, st, dl_nslots, dl_lam.p, lambda, dl_xloc.p);
       launch_pdl(dev::k_h_gemm, hb_nwork, dev::kGThreads, 0, st, hb_work.p, hb_H.p, hb_cin.p, hb_cout.p, dl_xloc.p,
                  yb, Ksys.X.p);
+      if (!check) {
+        perm_out_K(dst);
+        if (nc && nfloat_local)
+          dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,
+                                                                  d_fxyoff.p, alpha_vec.p, dst); ::pf::g_launches++;
+        return;
+      }
+      // first back-substitution: the same step in the sweep form, the two compared
+      const int nx = (int)Ksys.total_x;
+      PF_CUDA_CHECK(cudaMemcpyAsync(hb_Yb.p, Ksys.X.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
+      perm_in_K(bvec.p);
+      if (g_back.nrows)
+        dev::k_gather_ll<<<cdiv(g_back.nrows, 256), 256, 0, st>>>(g_back.nrows, g_back.rows.p, g_back.ptr.p,
+                                                                 g_back.idx.p, g_back.val.p, lambda, Ksys.X.p, -1.0, 1); ::pf::g_launches++;
+      if (nfix) dev::k_zero_idx<<<cdiv(nfix, 128), 128, 0, st>>>(nfix, d_fixpos.p, Ksys.X.p), ::pf::g_launches++;
+      ksolve(st);
+      {
+        DevBuf<double> diff;  // X_sweep - X_explicit (freed after the check)
+        diff.alloc(Ksys.total_x);
+        PF_CUDA_CHECK(cudaMemcpyAsync(diff.p, hb_Yb.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
+        dev::k_axpby<<<cdiv(nx, 256), 256, 0, st>>>(nx, 1.0, Ksys.X.p, -1.0, diff.p); ::pf::g_launches++;
+        dot(nx, diff.p, diff.p, 60);  // scratch slots 60 / 61
+        dot(nx, Ksys.X.p, Ksys.X.p, 61);
+        PF_CUDA_CHECK(cudaStreamSynchronize(st));
+      }
+      const double nd2 = read_scal(60), nx2 = read_scal(61);
+      hb_checked = true, hb_valid = false;
+      hb_dev = nx2 > 0.0 ? std::sqrt(nd2 / nx2) : 0.0;
+      const char* e = std::getenv("PF_HB_DEV");
+      const double lim = e ? std::atof(e) : kHbDevMax;
+      hb_use_sweep = hb_dev > lim;
+      if (std::getenv("PF_VERBOSE"))
+        std::fprintf(stderr, "[pf] back-substitution check: explicit vs sweep form differ by %.3g (limit %.3g)%s\n", hb_dev,
+                     lim, hb_use_sweep ? " -> sweep form K^+ (b - G^T lambda) from here on" : "");
+      // the form the later steps use is the one this step returns (bitwise the same path)
+      if (!hb_use_sweep)
+        PF_CUDA_CHECK(cudaMemcpyAsync(Ksys.X.p, hb_Yb.p, sizeof(double) * Ksys.total_x, cudaMemcpyDeviceToDevice, st));
       perm_out_K(dst);
       if (nc && nfloat_local)
         dev::k_rigid_add<<<dim3(8, nfloat_local), 256, 0, st>>>(nfloat_local, d_fsub.p, d_fvec.p, d_fnu.p, d_fxy.p,

@@ -9,7 +9,10 @@ saddle values per step), so each fixture holds, per time step:
   * the Krylov iteration count, its residual history, the true residual,
   * the oracle's own sensitivity to the Krylov tolerance (the same run at
     tol/100 -- tol/10 where tol/100 is below the attainable accuracy), per
-    field, so a bar above 1e-8 is backed by evidence rather than widened.
+    field, so a bar above 1e-8 is backed by evidence rather than widened;
+  * the oracle's own forward error of its local solves (refine_estimate: the
+    first step of an iterative refinement of x_s in the oracle's arithmetic),
+    per field -- what u / xi / eta / p are determined to given lambda.
 Small enough to hold whole (``full=True``): c4 at mesh 128 with 4x4
 subdomains of 32x32 cells (c4's true subdomain size).
 
@@ -44,6 +47,29 @@ def global_fields(o, xs):
     return {k: np.concatenate([fi[k] for fi in f if k in fi]) for k in FIELDS}
 
 
+def refine_estimate(o, k, xs, lam):
+    """The oracle's own forward error of its local solves at step k: with the
+    step's right-hand side b_s, r_s = b_s - G_s^T lambda - K_s x_s is the
+    residual of x_s = K_s^+ (b_s - G_s^T lambda) + R_s alpha_s in the oracle's own
+    arithmetic, and delta_s = K_s^+ r_s the first step of an iterative
+    refinement.  ||delta_f|| / ||x_f|| per field f (over all subdomains) is what
+    the fields are determined to given lambda: at nu = 0.49999 (Lame lambda =
+    5e4, 64x64-cell subdomains) cond(K_s) eps reaches 1e-8 in u."""
+    bs, _, _ = o.step_rhs(k - 1)
+    num = {f: 0.0 for f in FIELDS}
+    den = {f: 0.0 for f in FIELDS}
+    for s, (b, x) in enumerate(zip(bs, xs)):
+        K, G = o.matrix(s, "K"), o.matrix(s, "G")
+        r = b - G.T @ lam - K @ x
+        d = o.local_solve(s, r)
+        fd, fx = o.fields([d if i == s else np.zeros_like(xs[i]) for i in range(len(xs))])[s], o.fields(xs)[s]
+        for f in FIELDS:
+            if f in fx:
+                num[f] += float(np.dot(fd[f], fd[f]))
+                den[f] += float(np.dot(fx[f], fx[f]))
+    return np.array([np.sqrt(num[f] / den[f]) if den[f] > 0 else 0.0 for f in FIELDS])
+
+
 def make(name, kw, full):
     t0 = time.time()
     o = ol.Oracle(**kw)
@@ -71,6 +97,9 @@ def make(name, kw, full):
                 if f in fi:
                     norms[s, j] = np.linalg.norm(fi[f])
         out[f"norms{k}"] = norms
+        out[f"refine{k}"] = refine_estimate(o, k, xs, lam)
+        print(name, "step", k, "local-solve forward error (refinement estimate) per field", out[f"refine{k}"].tolist(),
+              flush=True)
         if full:
             out[f"x{k}"] = np.concatenate(xs)
         else:
