@@ -877,17 +877,47 @@ __global__ void __launch_bounds__(32 * kQlWarps) k_qlocal_y(QlSys Q, const doubl
   int io[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) a[k] = c[k] = 0.0, io[k] = lane + 32 * k < min(n, nl) ? 32 * k : -lane;  // idle: row 0
+  // Columns in batches of kB: the batch's operator values are loaded first (kB R
+  // independent loads in flight), then consumed -- a column-by-column loop pays
+  // one L2 round trip per column (every column starts new cache lines), which
+  // made this kernel 8 us on 65-multiplier blocks.  Two chains per row.
+  constexpr int kB = 8;
   int j = 0;
-  for (; j + 1 < n; j += 2) {
-    const double b0 = bs[warp][j], b1 = bs[warp][j + 1];
+  for (; j + kB <= n; j += kB) {
     const double* M0 = M + j * n;
+    double m[kB][R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) a[k] = fma(M0[io[k]], b0, a[k]), c[k] = fma(M0[n + io[k]], b1, c[k]);
+    for (int q = 0; q < kB; ++q)
+#pragma unroll
+      for (int k = 0; k < R; ++k) m[q][k] = M0[q * n + io[k]];
+#pragma unroll
+    for (int q = 0; q < kB; q += 2) {
+      const double b0 = bs[warp][j + q], b1 = bs[warp][j + q + 1];
+#pragma unroll
+      for (int k = 0; k < R; ++k) a[k] = fma(m[q][k], b0, a[k]), c[k] = fma(m[q + 1][k], b1, c[k]);
+    }
   }
-  if (j < n) {
-    const double b0 = bs[warp][j];
+  if (n - j <= 2) {  // one or two columns left (33 = 4 x 8 + 1): no batch
+    for (; j < n; ++j) {
+      const double b0 = bs[warp][j];
 #pragma unroll
-    for (int k = 0; k < R; ++k) a[k] = fma(M[j * n + io[k]], b0, a[k]);
+      for (int k = 0; k < R; ++k) a[k] = fma(M[j * n + io[k]], b0, a[k]);
+    }
+  }
+  if (j < n) {  // tail batch: predicated loads (idle columns read column j), then the same chains
+    const double* M0 = M + j * n;
+    const int nt = n - j;
+    double m[kB][R];
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+#pragma unroll
+      for (int k = 0; k < R; ++k) m[q][k] = M0[(q < nt ? q : 0) * n + io[k]];
+#pragma unroll
+    for (int q = 0; q < kB; q += 2) {
+      const double b0 = q < nt ? bs[warp][j + q] : 0.0, b1 = q + 1 < nt ? bs[warp][j + q + 1] : 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) a[k] = fma(m[q][k], b0, a[k]), c[k] = fma(m[q + 1][k], b1, c[k]);
+    }
   }
 #pragma unroll
   for (int k = 0; k < R; ++k)

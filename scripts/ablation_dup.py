@@ -5,7 +5,7 @@ import os, sys, subprocess
 sys.path.insert(0, '.')
 if len(sys.argv) > 1 and sys.argv[1] == "run":
     import paper_2509_06673_b200 as pf
-    op = pf.FetiOperator(**pf.BASELINE_CONFIGS["c4"])
+    op = pf.FetiOperator(**pf.BASELINE_CONFIGS[os.environ.get("PF_ABL_CFG", "c4")])
     op.step()
     ms, it, _ = op.bench_steps(3)
     r = op.step()
