@@ -132,10 +132,34 @@ inline void apply_solver_choice(pf_config& c, SolverChoice s) {
   else c.precond = multi ? PF_PREC_GENERALIZED_MORTAR : PF_PREC_GENERALIZED;
 }
 
+/// Reference SolveOptions (timeloop.hpp:123-131), same fields and defaults.
+/// `parallel` has no meaning here (every subdomain runs in one launch);
+/// `stride` and `verbose` belong to the caller's output loop.
+struct SolveOptions {
+  SolverChoice solver = SolverChoice::feti_generalized;
+  double tol = 1e-8;
+  int max_iter = 500;
+  bool warm_start = true;
+  bool parallel = true;
+  int stride = 1;
+  bool verbose = false;
+};
+
+/// cfg with the reference's SolveOptions applied (solver choice, tolerance,
+/// iteration cap, warm start): what build_discretization + StepSolver(d, opts)
+/// fix in the reference is fixed at Problem construction here.
+inline pf_config with_options(pf_config c, const SolveOptions& o) {
+  apply_solver_choice(c, o.solver);
+  c.tol = o.tol, c.max_iter = o.max_iter, c.warm = o.warm_start ? 1 : 0;
+  return c;
+}
+
 /// Discretisation + FETI operator living on the device.
 class Problem {
  public:
   explicit Problem(const pf_config& cfg) { check(pf_create(&ctx_, &cfg), nullptr); refresh(); }
+  /// build_discretization(scenario, ...) + StepSolver(d, opts) of the reference in one object
+  Problem(const pf_config& cfg, const SolveOptions& opts) : Problem(with_options(cfg, opts)) {}
   ~Problem() { pf_destroy(ctx_); }
   Problem(const Problem&) = delete;
   Problem& operator=(const Problem&) = delete;
@@ -244,6 +268,9 @@ inline PcgResult feti_pcg(Problem& p, const Vector& rhs, const Vector& lambda_in
 class StepSolver {
  public:
   explicit StepSolver(Problem& p) : p_(&p) {}
+  /// reference signature StepSolver(d, opts): the options were applied when the
+  /// Problem was built (Problem(cfg, opts)); kept for source compatibility
+  StepSolver(Problem& p, const SolveOptions&) : p_(&p) {}
   StateSnapshot advance(const StateSnapshot& prev, PcgReport* report = nullptr) const {
     check_size(prev.x, p_->info().total_dim, "advance: prev.x");
     check_size(prev.lambda, p_->n_lambda(), "advance: prev.lambda");
