@@ -36,9 +36,11 @@ int main() {
     }
     // SolverChoice::monolithic (timeloop.hpp:139-160): the direct interface
     // solve, the same discrete solution without Krylov iterations
-    pf_config mcfg = cfg;
-    pb::apply_solver_choice(mcfg, pb::SolverChoice::monolithic);
-    pb::Problem mono(mcfg);
+    pb::SolveOptions mopts;  // the reference's SolveOptions (timeloop.hpp:123-131)
+    mopts.solver = pb::SolverChoice::monolithic, mopts.tol = cfg.tol, mopts.max_iter = cfg.max_iter;
+    pb::Problem mono(cfg, mopts);
+    pb::StepSolver msolver(mono, mopts);
+    (void)msolver;
     for (int n = 0; n < mono.info().N; ++n) {
       const pb::PcgReport r = mono.step();
       const auto [eu, ep] = mono.errors();
