@@ -137,3 +137,27 @@ def test_singular_subproblem_detected():
     with pytest.raises(ol.OracleError) as e:
         ol.Oracle(mesh_n=8, SX=1, SY=2, order=1, steps=1, nu=0.3, E=-1.0)
     assert e.value.code == 99 or e.value.code == 4
+
+
+def test_sqmr_stagnation_restart_forced(monkeypatch):
+    """The oracle's SQMR stagnation restart (o_feti.hpp sqmr: kStagWindow = 128,
+    kStagRatio = 0.9; the engine carries the same rule) never fires on a
+    converging run; forced with PF_STAG_RATIO = 1e-30 (every window counts as
+    stagnated) the recurrences restart from the true residual every 128
+    iterations and still converge to the same multiplier and fields."""
+    kw = dict(ol.BASELINE_CONFIGS["c3"], mesh_n=32, SX=4, SY=4, steps=1, precond="dirichlet-mortar")
+    monkeypatch.delenv("PF_STAG_RATIO", raising=False)
+    a = ol.Oracle(**kw)
+    a.run(1)
+    ra = a.report(1)
+    monkeypatch.setenv("PF_STAG_RATIO", "1e-30")
+    b = ol.Oracle(**kw)
+    b.run(1)
+    rb = b.report(1)
+    assert ra["iterations"] > 128, ra["iterations"]          # the case has at least one window
+    assert rb["restarts"] > ra["restarts"], (ra["restarts"], rb["restarts"])
+    assert rb["true_residual"] <= 1e-10
+    (xa, la), (xb, lb) = a.state(1), b.state(1)
+    assert np.linalg.norm(la - lb) <= 1e-8 * np.linalg.norm(la)
+    for u, v in zip(xa, xb):
+        assert np.linalg.norm(u - v) <= 1e-7 * max(np.linalg.norm(u), 1e-300)
